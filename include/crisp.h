@@ -1,0 +1,203 @@
+/*
+ * crisp.h -- C ABI of the B200-native CRISP query engine (libcrisp.so).
+ *
+ * CRISP: Correlation-Resilient Indexing via Subspace Partitioning (arXiv
+ * 2603.05180).  Citations "P:Lnnn" are lines of the paper's LaTeX source
+ * (PAPER.md), "S:Lnnn" lines of SPEC.md.  The problem is kNN under L2 over
+ * X in R^{N x D}; results are squared L2 distances.
+ *
+ * Conventions for every call:
+ *  - Ownership: the caller owns every input and output buffer.  Builds copy the
+ *    data into HBM and never keep a caller pointer; an index owns all its device
+ *    memory until crisp_free.
+ *  - Pointers: "host or device" arguments are classified with
+ *    cudaPointerGetAttributes; *_async calls require device pointers and run on
+ *    the given cudaStream_t (passed as void*; NULL = legacy default stream).
+ *  - Layout: row-major, fp32 vectors, int64 ids, Q x k results ascending by
+ *    (distance, id), padded with (-1, +inf) when fewer than k candidates exist.
+ *  - Errors: every call returns a crisp_status; crisp_last_error() returns a
+ *    thread-local message for the last non-OK status of the calling thread.
+ *    CRISP_EINVAL: bad argument (k < 1 or k > N, non-finite data, M < 1, K < 1,
+ *    M > 127, K > 255, NULL pointer).  CRISP_ECUDA / CRISP_ENOMEM pass through
+ *    the CUDA failure (message holds cudaGetErrorString).  There is no CPU
+ *    fallback: without a working CUDA device every compute call fails.
+ *  - Thread safety: an index is read-only during search; concurrent searches
+ *    on different streams are allowed (scratch is per call).  Parameter setters
+ *    must not race with searches.
+ */
+#ifndef CRISP_H
+#define CRISP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CRISP_OK = 0,
+    CRISP_EINVAL = 1,
+    CRISP_EIO = 2,
+    CRISP_ENOMEM = 3,
+    CRISP_ECUDA = 4,
+    CRISP_ENCCL = 5,
+    CRISP_EUNSUPPORTED = 6
+} crisp_status;
+
+/* Execution flag phi (Table 1; Sec. 4.3.2). */
+typedef enum {
+    CRISP_GUARANTEED = 0, /* binary scoring, exhaustive exact-L2 verification */
+    CRISP_OPTIMIZED = 1   /* rank-weighted scoring, Hamming order, patience */
+} crisp_mode;
+
+typedef struct crisp_index crisp_index; /* opaque; owns HBM */
+
+typedef struct {
+    int32_t M;                 /* subspaces (required, no paper default) */
+    int32_t K;                 /* centroids per half-subspace, default 50 */
+    float tau_cev;             /* CEV gate, default 0.85; rotate iff CEV > tau_cev */
+    int32_t rotation;          /* -1 auto (gate), 0 force off, 1 force on */
+    int32_t kmeans_iters;      /* Lloyd iterations, default 20 */
+    int64_t kmeans_sample;     /* k-means training rows, default 100000 */
+    uint64_t seed;             /* drives every random draw of the method (Philox4x32-10) */
+    int32_t device;            /* CUDA device ordinal */
+    double budget_ratio;       /* beta: per-subspace retrieved fraction (range 0.001-0.06 P:L525) */
+    int64_t budget;            /* if > 0 overrides beta: B ids per subspace (exact integer) */
+    double min_collision_ratio;/* alpha: tau = ceil(alpha*M) (range 0.1-0.6 P:L525) */
+    int32_t tau;               /* if > 0 overrides alpha: integer collision threshold */
+    int32_t patience_factor;   /* P = patience_factor * k (default 40); 0 = disabled */
+    int64_t workspace_bytes;   /* per-search scratch cap (query chunking); 0 = default 4 GiB */
+} crisp_params;
+
+typedef struct {
+    int64_t N;          /* points held by this index (shard-local) */
+    int64_t N_global;   /* points of the whole dataset (budget base) */
+    int64_t gid_base;   /* global id of local point 0 */
+    int32_t D;          /* input dimensionality */
+    int32_t padded_D;   /* D zero-padded to a multiple of 2M */
+    int32_t pitch;      /* row pitch of the stored vectors in floats (multiple of 4) */
+    int32_t M, K, dh;   /* dh = padded_D / (2M) */
+    int32_t rotated;    /* 1 if X' = XR was applied */
+    double cev;         /* measured CEV */
+    int64_t budget;     /* B ids per subspace in effect */
+    int32_t tau;        /* collision threshold in effect */
+    int32_t patience_factor;
+    int32_t block_ids;  /* ids per on-chip counter block */
+    int32_t n_blocks;
+    int64_t hbm_bytes;  /* device bytes owned by the index */
+    int64_t logical_bytes; /* 4ND + 4MN + 8M(K^2+1) + codebooks + 8*ceil(D/64)*N + 4D^2 if rotated */
+} crisp_index_info_t;
+
+/* Host buffers filled by crisp_export (any may be NULL to skip). */
+typedef struct {
+    float *R;          /* padded_D x padded_D (only if rotated) */
+    float *X;          /* N x padded_D stored vectors (rotated if applied) */
+    float *codebooks;  /* M x 2 x K x dh */
+    int32_t *cells;    /* M x N cell ids */
+    int64_t *offsets;  /* M x (K^2+1) CSR Offsets */
+    int32_t *ids;      /* M x N CSR ids, local */
+    uint64_t *codes;   /* N x ceil(padded_D/64) binary codes */
+    int64_t *cell_sizes; /* M x K^2 sizes used for budgets (global after crisp_set_global_cell_sizes) */
+} crisp_export_t;
+
+/* Host buffers filled by crisp_search_trace (any may be NULL).  Stage outputs of
+ * Alg. 1 for parity checks. */
+typedef struct {
+    int32_t *act_len;    /* Q x M: activated cells per (q,m) (a2) */
+    int32_t *act_cell;   /* Q x M x K^2: activated cells in pop order (a2) */
+    int32_t *act_w;      /* Q x M x K^2: their weights 1/2 (a2, Alg. 1 l.10-12) */
+    int64_t *retrieved;  /* Q x M: ids retrieved, budget counting (Alg. 1 l.16) */
+    uint8_t *V;          /* Q x N: collision scores (a3, Eq. 1) */
+    int64_t *cand_n;     /* Q: |C_q| (a4) */
+    int32_t *cand;       /* Q x N: C_q local ids ascending (a4, Alg. 1 l.18) */
+    int32_t *order;      /* Q x N: verification order (phi=1: Hamming (h,id); phi=0: C_q) */
+    int64_t *n_verified; /* Q: candidates verified (phi=1: patience stop) */
+    int32_t *fallback;   /* Q: 1 if the underflow fallback fired */
+    float *qrot;         /* Q x padded_D: transformed query q' (a0) */
+} crisp_trace_t;
+
+/* Fill p with the paper's defaults (K=50, tau_cev=0.85, 20 Lloyd iterations,
+ * 1e5 k-means rows, beta=0.01, alpha=0.3, P=40k). */
+crisp_status crisp_default_params(crisp_params *p);
+
+/* Build (P:L249-256 phases 1-2): spectral check on a min(0.1N,1e5) sample
+ * (P:L264-268), adaptive rotation X' = XR in place, 2M k-means
+ * codebooks, cell assignment, per-subspace CSR Offsets/IDs
+ * (P:L363-369), binary codes.  data: N x D fp32 row-major, host or
+ * device.  On success *out owns the index. */
+crisp_status crisp_build(const float *data, int64_t N, int32_t D, const crisp_params *p, crisp_index **out);
+
+/* Same, with the rotation R (padded_D x padded_D fp32 row-major, or NULL for
+ * no rotation) and the codebooks (M x 2 x K x dh fp32) injected instead of
+ * computed; used for parity ("given the same seeded inputs and codebooks"). */
+crisp_status crisp_build_with(const float *data, int64_t N, int32_t D, const crisp_params *p, const float *R_or_null,
+                              const float *codebooks, crisp_index **out);
+
+/* One shard of a point-sharded index: local rows with global ids
+ * gid_base..gid_base+N_local-1, shared R and codebooks (both injected; R may be
+ * NULL).  Budgets use local sizes until crisp_set_global_cell_sizes. */
+crisp_status crisp_build_shard(const float *shard, int64_t N_local, int64_t gid_base, int32_t D, const crisp_params *p,
+                               const float *R_or_null, const float *codebooks, crisp_index **out);
+
+/* Local cell sizes, M x K^2 int64 host buffer (for the allreduce of N3). */
+crisp_status crisp_local_cell_sizes(const crisp_index *idx, int64_t *sizes);
+
+/* Install summed (global) cell sizes, M x K^2 int64 host buffer: the budget
+ * walk of a2 then activates exactly the cells a single global index would. */
+crisp_status crisp_set_global_cell_sizes(crisp_index *idx, const int64_t *sizes);
+
+/* Set search knobs.  beta/alpha are used only when budget/tau <= 0.  B =
+ * ceil(beta*N_global), tau = max(1, ceil(alpha*M)) with a 1e-9 relative snap to
+ * the nearest integer (decimal inputs such as 0.035*20000 give 700). */
+crisp_status crisp_set_search_params(crisp_index *idx, double beta, int64_t budget, double alpha, int32_t tau,
+                                     int32_t patience_factor);
+
+crisp_status crisp_index_info(const crisp_index *idx, crisp_index_info_t *out);
+
+/* Batched search, Alg. 1: a0 query transform, a1 half distances,
+ * a2 Multi-Sequence cell selection under the budget, a3 collision counting
+ * over the CSR lists, a4 threshold + fallback (+ Hamming order if phi=1), a5
+ * exact L2 verification (+ patience if phi=1) and top-k.  queries: Q x D fp32
+ * (host or device); out_ids: Q x k int64 global ids; out_dist2: Q x k fp32
+ * squared L2 (host or device).  Synchronous. */
+crisp_status crisp_search(const crisp_index *idx, const float *queries, int64_t Q, int32_t k, crisp_mode mode,
+                          int64_t *out_ids, float *out_dist2);
+
+/* Stream-ordered search on device pointers; returns after enqueueing. */
+crisp_status crisp_search_async(const crisp_index *idx, const float *queries, int64_t Q, int32_t k, crisp_mode mode,
+                                int64_t *out_ids, float *out_dist2, void *stream);
+
+/* Shard search for multi-GPU merging: like crisp_search_async but returns
+ * fp64 distances (out_dist64, Q x k) so the cross-shard merge orders by the
+ * same dist64 values as a single index (SURVEY App. A.1, A.2 "Merge"). */
+crisp_status crisp_search_shard_async(const crisp_index *idx, const float *queries, int64_t Q, int32_t k,
+                                      crisp_mode mode, int64_t *out_ids, double *out_dist64, void *stream);
+
+/* Global top-k by (d, gid) over G per-shard lists (device pointers, G x Q x k
+ * each, ids < 0 are padding) -> Q x k (a6). */
+crisp_status crisp_merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32_t k, double *out_d64,
+                              float *out_d, int64_t *out_ids, void *stream);
+
+/* Search with stage outputs copied to host buffers (parity / tracing). */
+crisp_status crisp_search_trace(const crisp_index *idx, const float *queries, int64_t Q, int32_t k, crisp_mode mode,
+                                int64_t *out_ids, float *out_dist2, crisp_trace_t *trace);
+
+/* Copy the index contents to host buffers. */
+crisp_status crisp_export(const crisp_index *idx, crisp_export_t *out);
+
+/* Stage timing: when enabled, every crisp_search* records CUDA events around
+ * each stage on its stream and accumulates the device time per stage (ms) into
+ * a per-thread table; crisp_stage_times synchronises on those events, copies up
+ * to n entries (stage order: 0 transform, 1 probe a1+a2, 2 count+select a3+a4,
+ * 3 fallback, 4 hamming+verify a4/a5, 5 merge) and, if reset != 0, clears it. */
+crisp_status crisp_set_stage_timing(int32_t on);
+crisp_status crisp_stage_times(double *ms, int32_t n, int32_t reset);
+
+void crisp_free(crisp_index *idx);
+const char *crisp_last_error(void);
+const char *crisp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CRISP_H */

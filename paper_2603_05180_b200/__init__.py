@@ -1,0 +1,282 @@
+"""paper_2603_05180_b200 -- B200-native CRISP query engine (arXiv 2603.05180).
+
+Thin ctypes binding over the C ABI of ``libcrisp.so`` (include/crisp.h).  This
+module only marshals arguments: every step of build and search runs in the
+CUDA kernels of ``csrc/``.  There is no CPU fallback: if the shared library is
+missing or no CUDA device is present, calls raise ``CrispError``.
+
+Host inputs may be numpy arrays; device inputs may be torch CUDA tensors
+(only their data pointers are used).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcrisp.so")
+
+GUARANTEED, OPTIMIZED = 0, 1
+STAGES = ("transform", "probe", "count_select", "fallback", "verify", "merge")
+
+
+class CrispError(RuntimeError):
+    pass
+
+
+class Params(C.Structure):
+    _fields_ = [
+        ("M", C.c_int32), ("K", C.c_int32), ("tau_cev", C.c_float), ("rotation", C.c_int32),
+        ("kmeans_iters", C.c_int32), ("kmeans_sample", C.c_int64), ("seed", C.c_uint64), ("device", C.c_int32),
+        ("budget_ratio", C.c_double), ("budget", C.c_int64), ("min_collision_ratio", C.c_double), ("tau", C.c_int32),
+        ("patience_factor", C.c_int32), ("workspace_bytes", C.c_int64),
+    ]
+
+
+class Info(C.Structure):
+    _fields_ = [
+        ("N", C.c_int64), ("N_global", C.c_int64), ("gid_base", C.c_int64), ("D", C.c_int32),
+        ("padded_D", C.c_int32), ("pitch", C.c_int32), ("M", C.c_int32), ("K", C.c_int32), ("dh", C.c_int32),
+        ("rotated", C.c_int32), ("cev", C.c_double), ("budget", C.c_int64), ("tau", C.c_int32),
+        ("patience_factor", C.c_int32), ("block_ids", C.c_int32), ("n_blocks", C.c_int32), ("hbm_bytes", C.c_int64),
+        ("logical_bytes", C.c_int64),
+    ]
+
+
+class Export(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("R", "X", "codebooks", "cells", "offsets", "ids", "codes", "cell_sizes")]
+
+
+class Trace(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("act_len", "act_cell", "act_w", "retrieved", "V", "cand_n", "cand", "order",
+                                          "n_verified", "fallback", "qrot")]
+
+
+# Every symbol include/crisp.h declares (checked by tests/test_abi.py).
+ABI_SYMBOLS = (
+    "crisp_default_params", "crisp_build", "crisp_build_with", "crisp_build_shard", "crisp_local_cell_sizes",
+    "crisp_set_global_cell_sizes", "crisp_set_search_params", "crisp_index_info", "crisp_search",
+    "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
+    "crisp_set_stage_timing", "crisp_stage_times", "crisp_free", "crisp_last_error", "crisp_version",
+)
+
+_lib = None
+
+
+def lib():
+    """Load libcrisp.so (fails loudly when the CUDA extension is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CrispError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        P = C.POINTER
+        L.crisp_default_params.argtypes = [P(Params)]
+        L.crisp_build.argtypes = [vp, i64, i32, P(Params), P(vp)]
+        L.crisp_build_with.argtypes = [vp, i64, i32, P(Params), vp, vp, P(vp)]
+        L.crisp_build_shard.argtypes = [vp, i64, i64, i32, P(Params), vp, vp, P(vp)]
+        L.crisp_local_cell_sizes.argtypes = [vp, vp]
+        L.crisp_set_global_cell_sizes.argtypes = [vp, vp]
+        L.crisp_set_search_params.argtypes = [vp, f64, i64, f64, i32, i32]
+        L.crisp_index_info.argtypes = [vp, P(Info)]
+        L.crisp_search.argtypes = [vp, vp, i64, i32, i32, vp, vp]
+        L.crisp_search_async.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp]
+        L.crisp_search_shard_async.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp]
+        L.crisp_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp, vp]
+        L.crisp_search_trace.argtypes = [vp, vp, i64, i32, i32, vp, vp, P(Trace)]
+        L.crisp_export.argtypes = [vp, P(Export)]
+        L.crisp_set_stage_timing.argtypes = [i32]
+        L.crisp_stage_times.argtypes = [vp, i32, i32]
+        L.crisp_free.argtypes = [vp]
+        L.crisp_free.restype = None
+        L.crisp_last_error.restype = C.c_char_p
+        L.crisp_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise CrispError(f"crisp status {st}: {lib().crisp_last_error().decode()}")
+
+
+def _ptr(a):
+    """Data pointer of a numpy array or torch tensor (no copies)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _host(a, dtype):
+    if hasattr(a, "data_ptr"):
+        return a
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def exact_ceil(ratio, n: int) -> int:
+    """ceil(ratio*n) with ratio read as the decimal it was written as (O1)."""
+    return int(math.ceil(Fraction(str(ratio)) * n))
+
+
+def default_params(**kw) -> Params:
+    p = Params()
+    _check(lib().crisp_default_params(C.byref(p)))
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise TypeError(f"unknown parameter {k}")
+        setattr(p, k, v)
+    return p
+
+
+@dataclass
+class SearchKnobs:
+    beta: float | None = None
+    budget: int | None = None
+    alpha: float | None = None
+    tau: int | None = None
+    patience_factor: int = 40
+
+
+class Index:
+    """An index in HBM (crisp_index*)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    # ---------------------------------------------------------------- build
+    @staticmethod
+    def build(data, M: int, R=None, codebooks=None, gid_base: int | None = None, **params) -> "Index":
+        """crisp_build (or crisp_build_with when R/codebooks are given, or
+        crisp_build_shard when gid_base is given)."""
+        p = default_params(M=M, **params)
+        x = _host(data, np.float32)
+        N, D = int(x.shape[0]), int(x.shape[1])
+        out = C.c_void_p()
+        if gid_base is not None:
+            Rh = _host(R, np.float32) if R is not None else None
+            cbh = _host(codebooks, np.float32)
+            _check(lib().crisp_build_shard(_ptr(x), N, gid_base, D, C.byref(p), _ptr(Rh), _ptr(cbh), C.byref(out)))
+        elif R is not None or codebooks is not None:
+            Rh = _host(R, np.float32) if R is not None else None
+            cbh = _host(codebooks, np.float32)
+            _check(lib().crisp_build_with(_ptr(x), N, D, C.byref(p), _ptr(Rh), _ptr(cbh), C.byref(out)))
+        else:
+            _check(lib().crisp_build(_ptr(x), N, D, C.byref(p), C.byref(out)))
+        return Index(out.value)
+
+    def free(self):
+        if self._h and self._h.value:
+            lib().crisp_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- knobs
+    def info(self) -> dict:
+        i = Info()
+        _check(lib().crisp_index_info(self._h, C.byref(i)))
+        return {n: getattr(i, n) for n, _ in Info._fields_}
+
+    def set_search_params(self, beta=None, budget=None, alpha=None, tau=None, patience_factor=40):
+        """B = ceil(beta*N_global) and tau = ceil(alpha*M) are computed exactly
+        here (decimal semantics) and passed as integers."""
+        info = self.info()
+        B = budget if budget else max(1, exact_ceil(beta if beta is not None else 0.01, info["N_global"]))
+        T = tau if tau else max(1, exact_ceil(alpha if alpha is not None else 0.3, info["M"]))
+        _check(lib().crisp_set_search_params(self._h, 0.0, int(B), 0.0, int(T), int(patience_factor)))
+
+    def local_cell_sizes(self) -> np.ndarray:
+        i = self.info()
+        out = np.zeros((i["M"], i["K"] * i["K"]), np.int64)
+        _check(lib().crisp_local_cell_sizes(self._h, _ptr(out)))
+        return out
+
+    def set_global_cell_sizes(self, sizes):
+        s = np.ascontiguousarray(sizes, dtype=np.int64)
+        _check(lib().crisp_set_global_cell_sizes(self._h, _ptr(s)))
+
+    # ---------------------------------------------------------------- search
+    def search(self, queries, k: int, mode: int = GUARANTEED):
+        """crisp_search: host (numpy) or device (torch CUDA) queries.  Returns
+        (ids int64 Qxk, dist2 float32 Qxk) on the same side as the input."""
+        q = _host(queries, np.float32)
+        Q = int(q.shape[0])
+        if hasattr(q, "data_ptr"):
+            import torch
+            ids = torch.empty((Q, k), dtype=torch.int64, device=q.device)
+            d = torch.empty((Q, k), dtype=torch.float32, device=q.device)
+        else:
+            ids = np.zeros((Q, k), np.int64)
+            d = np.zeros((Q, k), np.float32)
+        _check(lib().crisp_search(self._h, _ptr(q), Q, k, mode, _ptr(ids), _ptr(d)))
+        return ids, d
+
+    def search_async(self, q_dev, k: int, mode: int, ids_dev, d_dev, stream_ptr: int = 0):
+        """crisp_search_async on device tensors; stream_ptr = torch stream.cuda_stream."""
+        _check(lib().crisp_search_async(self._h, _ptr(q_dev), int(q_dev.shape[0]), k, mode, _ptr(ids_dev),
+                                        _ptr(d_dev), C.c_void_p(stream_ptr)))
+
+    def search_shard_async(self, q_dev, k: int, mode: int, ids_dev, d64_dev, stream_ptr: int = 0):
+        _check(lib().crisp_search_shard_async(self._h, _ptr(q_dev), int(q_dev.shape[0]), k, mode, _ptr(ids_dev),
+                                              _ptr(d64_dev), C.c_void_p(stream_ptr)))
+
+    def trace(self, queries, k: int, mode: int = GUARANTEED):
+        """crisp_search_trace: stage outputs as numpy arrays."""
+        i = self.info()
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        Q, M, N, KK, Dp = q.shape[0], i["M"], i["N"], i["K"] ** 2, i["padded_D"]
+        t = dict(act_len=np.zeros((Q, M), np.int32), act_cell=np.zeros((Q, M, KK), np.int32),
+                 act_w=np.zeros((Q, M, KK), np.int32), retrieved=np.zeros((Q, M), np.int64),
+                 V=np.zeros((Q, N), np.uint8), cand_n=np.zeros(Q, np.int64), cand=np.zeros((Q, N), np.int32),
+                 order=np.zeros((Q, N), np.int32), n_verified=np.zeros(Q, np.int64), fallback=np.zeros(Q, np.int32),
+                 qrot=np.zeros((Q, Dp), np.float32))
+        tr = Trace(**{n: t[n].ctypes.data for n in t})
+        ids = np.zeros((Q, k), np.int64)
+        d = np.zeros((Q, k), np.float32)
+        _check(lib().crisp_search_trace(self._h, _ptr(q), Q, k, mode, _ptr(ids), _ptr(d), C.byref(tr)))
+        return ids, d, t
+
+    def export(self) -> dict:
+        i = self.info()
+        N, M, K, Dp, dh = i["N"], i["M"], i["K"], i["padded_D"], i["dh"]
+        W = (Dp + 63) // 64
+        e = dict(X=np.zeros((N, Dp), np.float32), codebooks=np.zeros((M, 2, K, dh), np.float32),
+                 cells=np.zeros((M, N), np.int32), offsets=np.zeros((M, K * K + 1), np.int64),
+                 ids=np.zeros((M, N), np.int32), codes=np.zeros((N, W), np.uint64),
+                 cell_sizes=np.zeros((M, K * K), np.int64))
+        if i["rotated"]:
+            e["R"] = np.zeros((Dp, Dp), np.float32)
+        ex = Export(**{n: e[n].ctypes.data for n in e})
+        _check(lib().crisp_export(self._h, C.byref(ex)))
+        if not i["rotated"]:
+            e["R"] = None
+        return e
+
+
+def merge_topk(d64_dev, ids_dev, out_d64, out_d, out_ids, stream_ptr: int = 0):
+    """crisp_merge_topk over (G, Q, k) device tensors."""
+    G, Q, k = d64_dev.shape
+    _check(lib().crisp_merge_topk(_ptr(d64_dev), _ptr(ids_dev), G, Q, k, _ptr(out_d64), _ptr(out_d), _ptr(out_ids),
+                                  C.c_void_p(stream_ptr)))
+
+
+def set_stage_timing(on: bool):
+    _check(lib().crisp_set_stage_timing(1 if on else 0))
+
+
+def stage_times(reset: bool = True) -> dict:
+    a = np.zeros(8, np.float64)
+    _check(lib().crisp_stage_times(_ptr(a), 8, 1 if reset else 0))
+    return {STAGES[i]: float(a[i]) for i in range(len(STAGES))}

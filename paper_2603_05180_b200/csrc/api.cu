@@ -1,0 +1,430 @@
+// api.cu -- extern "C" entry points of libcrisp.so (see include/crisp.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "crisp_internal.cuh"
+
+namespace crisp {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ceil(ratio * n) with a 1e-9 relative snap to the nearest integer, so that
+// decimal inputs give the decimal answer (0.035 * 20000 -> 700).
+int64_t snap_ceil(double ratio, int64_t n) {
+    long double x = (long double)ratio * (long double)n;
+    long double r = nearbyintl(x);
+    long double tol = 1e-9L * std::max<long double>(1.0L, fabsl(x));
+    if (fabsl(x - r) <= tol) return (int64_t)r;
+    return (int64_t)ceill(x);
+}
+
+static void apply_knobs(crisp_index *ix, double beta, int64_t budget, double alpha, int32_t tau, int32_t pf) {
+    if (budget > 0) ix->budget = budget;
+    else {
+        CRISP_CHECK(beta > 0.0 && beta <= 1.0, "budget_ratio must be in (0, 1]");
+        ix->budget = std::max<int64_t>(1, snap_ceil(beta, ix->N_global));
+    }
+    if (tau > 0) ix->tau = tau;
+    else {
+        CRISP_CHECK(alpha > 0.0 && alpha <= 1.0, "min_collision_ratio must be in (0, 1]");
+        ix->tau = (int32_t)std::max<int64_t>(1, snap_ceil(alpha, ix->M));
+    }
+    CRISP_CHECK(pf >= 0, "patience_factor must be >= 0");
+    ix->patience_factor = pf;
+}
+
+static int block_ids_for(int64_t N) {
+    int bs = 32768;
+    if (const char *v = getenv("CRISP_BLOCK_IDS")) bs = std::max(4096, (atoi(v) / 4096) * 4096);
+    int64_t need = ((N + 4095) / 4096) * 4096;
+    return (int)std::min<int64_t>(bs, std::max<int64_t>(4096, need));
+}
+
+template <class T>
+static T *dalloc(crisp_index *ix, size_t n) {
+    void *p = nullptr;
+    CRISP_CUDA(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)));
+    ix->hbm_bytes += (int64_t)(n * sizeof(T));
+    return (T *)p;
+}
+
+static void free_index(crisp_index *ix) {
+    if (!ix) return;
+    cudaSetDevice(ix->device);
+    cudaFree(ix->X);
+    cudaFree(ix->R);
+    cudaFree(ix->cb);
+    cudaFree(ix->cells);
+    cudaFree(ix->ids);
+    cudaFree(ix->off2);
+    cudaFree(ix->gsize);
+    cudaFree(ix->codes);
+    delete ix;
+}
+
+static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
+    CRISP_CHECK(p != nullptr, "params is NULL");
+    CRISP_CHECK(N >= 1, "N must be >= 1");
+    CRISP_CHECK(D >= 1, "D must be >= 1");
+    CRISP_CHECK(p->M >= 1 && p->M <= MAX_M, "M must be in [1, 127]");
+    CRISP_CHECK(p->K >= 1 && p->K <= MAX_K, "K must be in [1, 255]");
+    CRISP_CHECK((int64_t)p->M * N < (1LL << 31), "M*N must be < 2^31");
+    int ndev = 0;
+    CRISP_CUDA(cudaGetDeviceCount(&ndev));
+    CRISP_CHECK(p->device >= 0 && p->device < ndev, "invalid device ordinal");
+    CRISP_CUDA(cudaSetDevice(p->device));
+    {
+        // keep freed search scratch in the pool (no OS round trips per search)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, p->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    crisp_index *ix = new crisp_index();
+    ix->device = p->device;
+    ix->N = N;
+    ix->N_global = N;
+    ix->D = D;
+    ix->M = p->M;
+    ix->K = p->K;
+    ix->Dp = ((D + 2 * p->M - 1) / (2 * p->M)) * (2 * p->M);
+    ix->dh = ix->Dp / (2 * p->M);
+    ix->pitch = ((ix->Dp + 3) / 4) * 4;
+    ix->W = (ix->Dp + 63) / 64;
+    ix->BS = block_ids_for(N);
+    ix->NB = (int32_t)((N + ix->BS - 1) / ix->BS);
+    ix->workspace_bytes = p->workspace_bytes;
+    try {
+        const int64_t KK = (int64_t)ix->K * ix->K;
+        ix->X = dalloc<float>(ix, (size_t)N * ix->pitch);
+        ix->cb = dalloc<float>(ix, (size_t)ix->M * 2 * ix->K * ix->dh);
+        ix->cells = dalloc<int32_t>(ix, (size_t)ix->M * N);
+        ix->ids = dalloc<int32_t>(ix, (size_t)ix->M * N);
+        ix->off2 = dalloc<int32_t>(ix, (size_t)ix->M * KK * (ix->NB + 1));
+        ix->gsize = dalloc<int32_t>(ix, (size_t)ix->M * KK);
+        ix->codes = dalloc<uint64_t>(ix, (size_t)N * ix->W);
+    } catch (...) {
+        free_index(ix);
+        throw;
+    }
+    return ix;
+}
+
+static const float *to_device(const float *src, size_t n, std::vector<void *> &tmp) {
+    if (is_device_ptr(src)) return src;
+    void *p = nullptr;
+    CRISP_CUDA(cudaMalloc(&p, n * sizeof(float)));
+    tmp.push_back(p);
+    CRISP_CUDA(cudaMemcpy(p, src, n * sizeof(float), cudaMemcpyHostToDevice));
+    return (const float *)p;
+}
+
+struct TmpFree {
+    std::vector<void *> v;
+    ~TmpFree() {
+        for (void *p : v) cudaFree(p);
+    }
+};
+
+static crisp_status build_common(const float *data, int64_t N, int64_t gid_base, int32_t D, const crisp_params *p,
+                                 const float *R, const float *cb, bool inject, crisp_index **out) {
+    crisp_index *ix = nullptr;
+    try {
+        CRISP_CHECK(out != nullptr, "out is NULL");
+        CRISP_CHECK(data != nullptr, "data is NULL");
+        if (inject) CRISP_CHECK(cb != nullptr, "codebooks are NULL");
+        ix = new_index(N, D, p);
+        ix->gid_base = gid_base;
+        TmpFree tf;
+        const float *dd = to_device(data, (size_t)N * D, tf.v);
+        const float *Rd = R ? to_device(R, (size_t)ix->Dp * ix->Dp, tf.v) : nullptr;
+        const float *cbd = inject ? to_device(cb, (size_t)ix->M * 2 * ix->K * ix->dh, tf.v) : nullptr;
+        cudaStream_t s;
+        CRISP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct SG {
+            cudaStream_t s;
+            ~SG() { cudaStreamDestroy(s); }
+        } sg{s};
+        build_index(ix, dd, Rd, cbd, p->kmeans_sample > 0 ? p->kmeans_sample : 100000,
+                    p->kmeans_iters > 0 ? p->kmeans_iters : 20, inject ? 0 : p->rotation, p->tau_cev, p->seed, s);
+        apply_knobs(ix, p->budget_ratio, p->budget, p->min_collision_ratio, p->tau, p->patience_factor);
+        *out = ix;
+        return CRISP_OK;
+    } catch (Err &e) {
+        free_index(ix);
+        return e.st;
+    } catch (std::exception &e) {
+        set_error(e.what());
+        free_index(ix);
+        return CRISP_ECUDA;
+    }
+}
+
+}  // namespace crisp
+
+using namespace crisp;
+
+extern "C" {
+
+const char *crisp_last_error(void) { return g_err.c_str(); }
+const char *crisp_version(void) { return "crisp-b200 0.1 (sm_100a)"; }
+
+crisp_status crisp_default_params(crisp_params *p) {
+    if (!p) {
+        set_error("params is NULL");
+        return CRISP_EINVAL;
+    }
+    memset(p, 0, sizeof(*p));
+    p->M = 16;
+    p->K = 50;
+    p->tau_cev = 0.85f;
+    p->rotation = -1;
+    p->kmeans_iters = 20;
+    p->kmeans_sample = 100000;
+    p->seed = 0;
+    p->device = 0;
+    p->budget_ratio = 0.01;
+    p->budget = 0;
+    p->min_collision_ratio = 0.3;
+    p->tau = 0;
+    p->patience_factor = 40;
+    p->workspace_bytes = 0;
+    return CRISP_OK;
+}
+
+crisp_status crisp_build(const float *data, int64_t N, int32_t D, const crisp_params *p, crisp_index **out) {
+    return build_common(data, N, 0, D, p, nullptr, nullptr, false, out);
+}
+
+crisp_status crisp_build_with(const float *data, int64_t N, int32_t D, const crisp_params *p, const float *R,
+                              const float *codebooks, crisp_index **out) {
+    return build_common(data, N, 0, D, p, R, codebooks, true, out);
+}
+
+crisp_status crisp_build_shard(const float *shard, int64_t N_local, int64_t gid_base, int32_t D, const crisp_params *p,
+                               const float *R, const float *codebooks, crisp_index **out) {
+    return build_common(shard, N_local, gid_base, D, p, R, codebooks, true, out);
+}
+
+void crisp_free(crisp_index *idx) { free_index(idx); }
+
+crisp_status crisp_local_cell_sizes(const crisp_index *ix, int64_t *sizes) {
+    try {
+        CRISP_CHECK(ix && sizes, "NULL argument");
+        CRISP_CUDA(cudaSetDevice(ix->device));
+        const int64_t KK = (int64_t)ix->K * ix->K;
+        std::vector<int32_t> off((size_t)ix->M * KK * (ix->NB + 1));
+        CRISP_CUDA(cudaMemcpy(off.data(), ix->off2, off.size() * 4, cudaMemcpyDeviceToHost));
+        for (int m = 0; m < ix->M; m++)
+            for (int64_t c = 0; c < KK; c++) {
+                const int32_t *o = off.data() + ((int64_t)m * KK + c) * (ix->NB + 1);
+                sizes[m * KK + c] = o[ix->NB] - o[0];
+            }
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_set_global_cell_sizes(crisp_index *ix, const int64_t *sizes) {
+    try {
+        CRISP_CHECK(ix && sizes, "NULL argument");
+        CRISP_CUDA(cudaSetDevice(ix->device));
+        const int64_t KK = (int64_t)ix->K * ix->K;
+        std::vector<int32_t> h((size_t)ix->M * KK);
+        int64_t n0 = 0;
+        for (int64_t c = 0; c < KK; c++) n0 += sizes[c];
+        for (int m = 0; m < ix->M; m++) {
+            int64_t nm = 0;
+            for (int64_t c = 0; c < KK; c++) {
+                CRISP_CHECK(sizes[m * KK + c] >= 0 && sizes[m * KK + c] < (1LL << 31), "bad cell size");
+                h[m * KK + c] = (int32_t)sizes[m * KK + c];
+                nm += sizes[m * KK + c];
+            }
+            CRISP_CHECK(nm == n0, "cell sizes must sum to the same N in every subspace");
+        }
+        CRISP_CHECK(n0 >= ix->N, "global sizes smaller than the local shard");
+        CRISP_CUDA(cudaMemcpy(ix->gsize, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+        ix->N_global = n0;
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_set_search_params(crisp_index *ix, double beta, int64_t budget, double alpha, int32_t tau,
+                                     int32_t patience_factor) {
+    try {
+        CRISP_CHECK(ix != nullptr, "index is NULL");
+        apply_knobs(ix, beta, budget, alpha, tau, patience_factor);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_index_info(const crisp_index *ix, crisp_index_info_t *o) {
+    if (!ix || !o) {
+        set_error("NULL argument");
+        return CRISP_EINVAL;
+    }
+    o->N = ix->N;
+    o->N_global = ix->N_global;
+    o->gid_base = ix->gid_base;
+    o->D = ix->D;
+    o->padded_D = ix->Dp;
+    o->pitch = ix->pitch;
+    o->M = ix->M;
+    o->K = ix->K;
+    o->dh = ix->dh;
+    o->rotated = ix->rotated;
+    o->cev = ix->cev;
+    o->budget = ix->budget;
+    o->tau = ix->tau;
+    o->patience_factor = ix->patience_factor;
+    o->block_ids = ix->BS;
+    o->n_blocks = ix->NB;
+    o->hbm_bytes = ix->hbm_bytes;
+    const int64_t KK = (int64_t)ix->K * ix->K;
+    o->logical_bytes = 4 * ix->N * ix->Dp + 4 * (int64_t)ix->M * ix->N + 8 * (int64_t)ix->M * (KK + 1) +
+                       4 * (int64_t)ix->M * 2 * ix->K * ix->dh + 8 * (int64_t)ix->W * ix->N +
+                       (ix->rotated ? 4 * (int64_t)ix->Dp * ix->Dp : 0);
+    return CRISP_OK;
+}
+
+static crisp_status search_impl(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, crisp_mode mode,
+                                int64_t *out_ids, float *out_d, double *out_d64, cudaStream_t s, bool sync_host,
+                                const crisp_trace_t *tr) {
+    try {
+        CRISP_CHECK(ix != nullptr, "index is NULL");
+        CRISP_CHECK(Q >= 0, "Q must be >= 0");
+        CRISP_CHECK(k >= 1 && k <= MAX_TOPK, "k must be in [1, 1024]");
+        CRISP_CHECK(k <= ix->N_global, "k > N");
+        CRISP_CHECK(mode == CRISP_GUARANTEED || mode == CRISP_OPTIMIZED, "bad mode");
+        CRISP_CHECK(out_ids != nullptr, "out_ids is NULL");
+        CRISP_CUDA(cudaSetDevice(ix->device));
+        if (Q == 0) return CRISP_OK;
+        CRISP_CHECK(queries != nullptr, "queries is NULL");
+        if (!sync_host) {
+            CRISP_CHECK(is_device_ptr(queries) && is_device_ptr(out_ids), "async search needs device pointers");
+            SearchOut so{out_ids, out_d, out_d64};
+            search(ix, queries, Q, k, (int)mode, so, s, tr);
+            return CRISP_OK;
+        }
+        TmpFree tf;
+        const float *qd = to_device(queries, (size_t)Q * ix->D, tf.v);
+        bool ids_dev = is_device_ptr(out_ids), d_dev = out_d ? is_device_ptr(out_d) : true;
+        int64_t *oi = out_ids;
+        float *od = out_d;
+        if (!ids_dev) {
+            CRISP_CUDA(cudaMalloc((void **)&oi, (size_t)Q * k * 8));
+            tf.v.push_back(oi);
+        }
+        if (out_d && !d_dev) {
+            CRISP_CUDA(cudaMalloc((void **)&od, (size_t)Q * k * 4));
+            tf.v.push_back(od);
+        }
+        cudaStream_t st;
+        CRISP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        struct SG {
+            cudaStream_t s;
+            ~SG() { cudaStreamDestroy(s); }
+        } sg{st};
+        SearchOut so{oi, od, out_d64};
+        search(ix, qd, Q, k, (int)mode, so, st, tr);
+        if (!ids_dev) CRISP_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)Q * k * 8, cudaMemcpyDeviceToHost, st));
+        if (out_d && !d_dev) CRISP_CUDA(cudaMemcpyAsync(out_d, od, (size_t)Q * k * 4, cudaMemcpyDeviceToHost, st));
+        CRISP_CUDA(cudaStreamSynchronize(st));
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    } catch (std::exception &e) {
+        set_error(e.what());
+        return CRISP_ECUDA;
+    }
+}
+
+crisp_status crisp_search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, crisp_mode mode,
+                          int64_t *out_ids, float *out_dist2) {
+    return search_impl(ix, queries, Q, k, mode, out_ids, out_dist2, nullptr, nullptr, true, nullptr);
+}
+
+crisp_status crisp_search_async(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, crisp_mode mode,
+                                int64_t *out_ids, float *out_dist2, void *stream) {
+    return search_impl(ix, queries, Q, k, mode, out_ids, out_dist2, nullptr, (cudaStream_t)stream, false, nullptr);
+}
+
+crisp_status crisp_search_shard_async(const crisp_index *ix, const float *queries, int64_t Q, int32_t k,
+                                      crisp_mode mode, int64_t *out_ids, double *out_dist64, void *stream) {
+    return search_impl(ix, queries, Q, k, mode, out_ids, nullptr, out_dist64, (cudaStream_t)stream, false, nullptr);
+}
+
+crisp_status crisp_search_trace(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, crisp_mode mode,
+                                int64_t *out_ids, float *out_dist2, crisp_trace_t *trace) {
+    return search_impl(ix, queries, Q, k, mode, out_ids, out_dist2, nullptr, nullptr, true, trace);
+}
+
+crisp_status crisp_merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32_t k, double *out_d64,
+                              float *out_d, int64_t *out_ids, void *stream) {
+    try {
+        CRISP_CHECK(d && ids && out_ids, "NULL argument");
+        CRISP_CHECK(G >= 1 && k >= 1 && Q >= 0, "bad sizes");
+        CRISP_CHECK(is_device_ptr(d) && is_device_ptr(ids) && is_device_ptr(out_ids), "device pointers required");
+        merge_topk(d, ids, G, Q, k, out_d64, out_d, out_ids, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_export(const crisp_index *ix, crisp_export_t *o) {
+    try {
+        CRISP_CHECK(ix && o, "NULL argument");
+        CRISP_CUDA(cudaSetDevice(ix->device));
+        const int64_t N = ix->N, KK = (int64_t)ix->K * ix->K;
+        if (o->R && ix->rotated)
+            CRISP_CUDA(cudaMemcpy(o->R, ix->R, (size_t)ix->Dp * ix->Dp * 4, cudaMemcpyDeviceToHost));
+        if (o->X)
+            CRISP_CUDA(cudaMemcpy2D(o->X, (size_t)ix->Dp * 4, ix->X, (size_t)ix->pitch * 4, (size_t)ix->Dp * 4, N,
+                                    cudaMemcpyDeviceToHost));
+        if (o->codebooks)
+            CRISP_CUDA(cudaMemcpy(o->codebooks, ix->cb, (size_t)ix->M * 2 * ix->K * ix->dh * 4, cudaMemcpyDeviceToHost));
+        if (o->cells) CRISP_CUDA(cudaMemcpy(o->cells, ix->cells, (size_t)ix->M * N * 4, cudaMemcpyDeviceToHost));
+        if (o->ids) CRISP_CUDA(cudaMemcpy(o->ids, ix->ids, (size_t)ix->M * N * 4, cudaMemcpyDeviceToHost));
+        if (o->codes) CRISP_CUDA(cudaMemcpy(o->codes, ix->codes, (size_t)N * ix->W * 8, cudaMemcpyDeviceToHost));
+        if (o->offsets) {
+            std::vector<int32_t> off((size_t)ix->M * KK * (ix->NB + 1));
+            CRISP_CUDA(cudaMemcpy(off.data(), ix->off2, off.size() * 4, cudaMemcpyDeviceToHost));
+            for (int m = 0; m < ix->M; m++) {
+                for (int64_t c = 0; c < KK; c++) o->offsets[m * (KK + 1) + c] = off[((int64_t)m * KK + c) * (ix->NB + 1)];
+                o->offsets[m * (KK + 1) + KK] = N;
+            }
+        }
+        if (o->cell_sizes) {
+            std::vector<int32_t> g((size_t)ix->M * KK);
+            CRISP_CUDA(cudaMemcpy(g.data(), ix->gsize, g.size() * 4, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < g.size(); i++) o->cell_sizes[i] = g[i];
+        }
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+// crisp_internal.cuh -- internal declarations of libcrisp (CUDA path only).
+// Shares nothing with oracle/ (the CPU checker).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/crisp.h"
+
+// ---------------------------------------------------------------------------
+// Error plumbing: every CUDA status is mapped to a crisp_status with a
+// thread-local message (crisp_last_error).
+// ---------------------------------------------------------------------------
+namespace crisp {
+
+void set_error(const std::string &msg);
+
+struct Err {
+    crisp_status st;
+};
+
+#define CRISP_CUDA(call)                                                                                 \
+    do {                                                                                                 \
+        cudaError_t e_ = (call);                                                                         \
+        if (e_ != cudaSuccess) {                                                                         \
+            ::crisp::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));                      \
+            throw ::crisp::Err{e_ == cudaErrorMemoryAllocation ? CRISP_ENOMEM : CRISP_ECUDA};            \
+        }                                                                                                \
+    } while (0)
+
+#define CRISP_CHECK(cond, msg)                                                                           \
+    do {                                                                                                 \
+        if (!(cond)) {                                                                                   \
+            ::crisp::set_error(msg);                                                                     \
+            throw ::crisp::Err{CRISP_EINVAL};                                                            \
+        }                                                                                                \
+    } while (0)
+
+#define CRISP_LAUNCH() CRISP_CUDA(cudaGetLastError())
+
+// Method randomness streams (same numbering as DESIGN.md "Method randomness").
+constexpr uint32_t STREAM_CEV_SAMPLE = 1u;
+constexpr uint32_t STREAM_ROTATION = 2u;
+constexpr uint32_t STREAM_KM_SAMPLE = 3u;
+constexpr uint32_t STREAM_KM_INIT = 4u;
+
+constexpr int MAX_M = 127;   // byte counters hold V <= 2M
+constexpr int MAX_K = 255;
+constexpr int MAX_TOPK = 1024;
+
+}  // namespace crisp
+
+// ---------------------------------------------------------------------------
+// The index: everything lives in HBM (device pointers) except scalars.
+// ---------------------------------------------------------------------------
+struct crisp_index {
+    int device = 0;
+    int64_t N = 0, N_global = 0, gid_base = 0;
+    int32_t D = 0, Dp = 0, pitch = 0, M = 0, K = 0, dh = 0, W = 0;
+    int32_t rotated = 0;
+    double cev = 0.0;
+    float *X = nullptr;        // N x pitch, stored (rotated) vectors, zero padded
+    float *R = nullptr;        // Dp x Dp row-major (rotated only)
+    float *cb = nullptr;       // M x 2 x K x dh
+    int32_t *cells = nullptr;  // M x N
+    int32_t *ids = nullptr;    // M x N CSR ids
+    int32_t *off2 = nullptr;   // M x K^2 x (NB+1): start of ids >= b*BS inside cell c
+    int32_t *gsize = nullptr;  // M x K^2 sizes for the budget walk (local or global)
+    uint64_t *codes = nullptr; // N x W
+    int32_t BS = 0, NB = 0;    // on-chip counter block: ids per block, number of blocks
+    int64_t budget = 0;
+    int32_t tau = 1, patience_factor = 40;
+    int64_t workspace_bytes = 0;
+    int64_t hbm_bytes = 0;
+};
+
+namespace crisp {
+
+// helpers implemented in api.cu
+void *dmalloc(size_t bytes, crisp_index *ix);
+bool is_device_ptr(const void *p);
+int64_t snap_ceil(double ratio, int64_t n);
+
+// build steps (build.cu)
+void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, const float *cb_inj, int64_t kmeans_sample,
+                 int32_t kmeans_iters, int32_t rotation_mode, float tau_cev, uint64_t seed, cudaStream_t s);
+void finish_csr(crisp_index *ix, cudaStream_t s);
+
+// fp64 sequential-order GEMM: Y(rows x Dp, pitch ldy) = fl32(X(rows x Dp, pitch ldx) . R(Dp x Dp))
+void rotate_rows_f64(const float *X, int64_t rows, int32_t Dp, int64_t ldx, const float *R, float *Y, int64_t ldy,
+                     cudaStream_t s);
+
+// search (search.cu)
+struct SearchOut {
+    int64_t *ids;      // Q x k global ids (device)
+    float *d32;        // Q x k fp32 (device) or null
+    double *d64;       // Q x k fp64 (device) or null
+};
+struct TraceDev;  // device-side trace buffers (search.cu)
+void search(const crisp_index *ix, const float *queries_dev, int64_t Q, int32_t k, int mode, SearchOut out,
+            cudaStream_t s, const crisp_trace_t *host_trace);
+void merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32_t k, double *out_d64, float *out_d,
+                int64_t *out_ids, cudaStream_t s);
+
+// stage timing
+bool stage_timing_on();
+void stage_record(int stage, cudaEvent_t a, cudaEvent_t b);
+
+}  // namespace crisp
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+namespace crisp {
+
+// Philox4x32-10 (Salmon et al. SC'11); same generator as the oracle writes on
+// its own.
+__host__ __device__ inline void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                               uint32_t k1, uint32_t out[4]) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+__host__ __device__ inline void draw(uint64_t seed, uint32_t stream, uint64_t idx, uint32_t sub, uint32_t o[4]) {
+    philox4x32_10((uint32_t)idx, (uint32_t)(idx >> 32), stream, sub, (uint32_t)seed, (uint32_t)(seed >> 32), o);
+}
+
+__host__ __device__ inline double u53(uint32_t a, uint32_t b) {
+    uint64_t v = (((uint64_t)a << 32) | (uint64_t)b) >> 11;
+    return (double)v * (1.0 / 9007199254740992.0);
+}
+
+__host__ __device__ inline double uniform(uint64_t seed, uint32_t stream, uint64_t idx, uint32_t sub) {
+    uint32_t o[4];
+    draw(seed, stream, idx, sub, o);
+    return u53(o[0], o[1]);
+}
+
+// dist64 over n floats: d = (double)a - (double)b, s = fma(d, d, s), ascending i.
+__device__ __forceinline__ double dist64(const float *__restrict__ a, const float *__restrict__ b, int n) {
+    double s = 0.0;
+    for (int i = 0; i < n; i++) {
+        double d = __dsub_rn((double)a[i], (double)b[i]);
+        s = __fma_rn(d, d, s);
+    }
+    return s;
+}
+
+}  // namespace crisp

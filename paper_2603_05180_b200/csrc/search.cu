@@ -1,0 +1,1141 @@
+// search.cu -- the batched CRISP query engine (Alg. 1) on sm_100a.
+//
+// Stages:
+//   a0  k_prep_queries / rotate_rows_f64   q' = fl32(q R)
+//   a1+a2  k_probe     half distances (dist64), half sorts, Multi-Sequence
+//                      selection as a staircase argmin (== heap order, App. A.3),
+//                      budget cut, rank weights                (Alg. 1 l.2-17)
+//   a3+a4  k_count_select  collision counting over the CSR slices into
+//                      on-chip byte counters per (query, id block), then the
+//                      threshold compaction in ascending id      (Eq. 1; l.13-18)
+//          k_fallback  |C| < k underflow fallback
+//   a5 (phi=0) k_rerank_exact + k_merge_lists  exact L2 + top-k
+//   a4+a5 (phi=1) k_rerank_patience  Hamming order + exact L2 in that order
+//                      with patience P = factor*k
+//   a6  k_merge_lists  cross-shard merge (multi-GPU)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "crisp_internal.cuh"
+
+namespace crisp {
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+constexpr int WARPS = 8;
+constexpr int THREADS = WARPS * 32;
+constexpr int CS_CAP = 1024;          // slice-table entries per round (count kernel)
+constexpr int CS_U = 16;              // ids per thread per round
+constexpr int CS_TCAP = THREADS * CS_U;  // positions per round
+constexpr int PATIENCE_CH = 64;       // rows verified per patience chunk
+
+__device__ __forceinline__ bool less_di(double a, int64_t ia, double b, int64_t ib) {
+    return a < b || (a == b && ia < ib);
+}
+
+// ---------------------------------------------------------------------------
+// a0: zero-padded copy of the queries (pitch floats per row)
+// ---------------------------------------------------------------------------
+__global__ void k_prep_queries(const float *__restrict__ q, int64_t Qc, int D, int pitch, float *__restrict__ out) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= Qc * pitch) return;
+    int64_t r = e / pitch;
+    int c = (int)(e % pitch);
+    out[e] = c < D ? q[r * D + c] : 0.0f;
+}
+
+// ---------------------------------------------------------------------------
+// a1 + a2: one warp per (query, subspace)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qrot, int pitch, int64_t Qc,
+                                                    const float *__restrict__ cb, int M, int K, int dh,
+                                                    const int32_t *__restrict__ gsize, int smem_gsize, int64_t budget,
+                                                    int wk, uint32_t *__restrict__ act, int32_t *__restrict__ act_len,
+                                                    int64_t *__restrict__ retrieved) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int KK = K * K;
+    const int m = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t *gs = (int32_t *)sm;
+    unsigned char *wbase = sm + (smem_gsize ? ((KK * 4 + 15) & ~15) : 0);
+    const int per_warp = ((4 * K * 8) + 3 * K + 15) & ~15;
+    double *tmp = (double *)(wbase + warp * per_warp);  // 2K
+    double *a = tmp + 2 * K, *b = a + K;
+    unsigned char *pa = (unsigned char *)(b + K), *pb = pa + K, *col = pb + K;
+    const int32_t *gsm = gsize + (int64_t)m * KK;
+    if (smem_gsize) {
+        for (int i = threadIdx.x; i < KK; i += THREADS) gs[i] = gsm[i];
+        __syncthreads();
+        gsm = gs;
+    }
+    const int64_t q = (int64_t)blockIdx.x * WARPS + warp;
+    if (q >= Qc) return;
+    const float *qm = qrot + q * pitch + (int64_t)m * 2 * dh;
+    // half distances (Alg. 1 l.4): dist64, exactly the oracle's order
+    for (int side = 0; side < 2; side++) {
+        const float *C = cb + (int64_t)(m * 2 + side) * K * dh;
+        for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64(qm + side * dh, C + (int64_t)c * dh, dh);
+    }
+    __syncwarp();
+    // sort each half by (delta, c) via ranks
+    for (int side = 0; side < 2; side++) {
+        const double *t = tmp + side * K;
+        double *dst = side ? b : a;
+        unsigned char *pdst = side ? pb : pa;
+        for (int c = lane; c < K; c += 32) {
+            double v = t[c];
+            int r = 0;
+            for (int c2 = 0; c2 < K; c2++) {
+                double u = t[c2];
+                r += (u < v) || (u == v && c2 < c);
+            }
+            dst[r] = v;
+            pdst[r] = (unsigned char)c;
+        }
+    }
+    for (int i = lane; i < K; i += 32) col[i] = 0;
+    __syncwarp();
+    // Multi-Sequence as a staircase argmin over (a_i + b_col[i], i)
+    uint32_t *out = act + (q * M + m) * (int64_t)KK;
+    int rank = 0;
+    int64_t ret = 0;
+    while (ret < budget && rank < KK) {
+        double bc = INFINITY;
+        int bi = 0x7fffffff;
+        for (int i = lane; i < K; i += 32) {
+            int ci = col[i];
+            if (ci < K && (i == 0 || col[i - 1] > ci)) {
+                double cost = __dadd_rn(a[i], b[ci]);
+                if (cost < bc) {  // rows visited in ascending i: first wins ties
+                    bc = cost;
+                    bi = i;
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            double oc = __shfl_xor_sync(0xffffffffu, bc, off);
+            int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (oc < bc || (oc == bc && oi < bi)) {
+                bc = oc;
+                bi = oi;
+            }
+        }
+        const int j = col[bi];
+        const int cell = pa[bi] * K + pb[j];
+        rank++;
+        const int w = (wk > 0 && rank <= wk) ? 2 : 1;  // Alg. 1 l.10-12
+        __syncwarp();
+        if (lane == 0) {
+            out[rank - 1] = (uint32_t)cell | ((uint32_t)w << 16);
+            col[bi] = (unsigned char)(j + 1);
+        }
+        ret += gsm[cell];
+        __syncwarp();
+    }
+    if (lane == 0) {
+        act_len[q * M + m] = rank;
+        retrieved[q * M + m] = ret;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a3: collision counting of one (query, id block) into smem byte counters.
+// Slices of all activated cells of all subspaces restricted to the block are
+// flattened (table + scan + position->slice fill) and streamed with coalesced,
+// independent loads; updates are packed-byte shared atomics (ATOMIC) or, with
+// per-subspace rounds and barriers, plain read-modify-writes (partition
+// property: an id occurs once per subspace).
+// ---------------------------------------------------------------------------
+struct CountSmem {
+    int32_t gst[CS_CAP];       // global start of the slice in ids[]
+    int32_t pre[CS_CAP + 1];   // exclusive prefix of slice lengths
+    unsigned char w[CS_CAP];
+    uint16_t sid[CS_TCAP];     // position -> slice
+    int32_t lpre[MAX_M + 2];   // prefix of act_len over m
+    int32_t round_e, round_n, round_T, round_skip;
+    typename cub::BlockScan<int, THREADS>::TempStorage scan;
+};
+
+template <bool ATOMIC>
+__device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, int b, const uint32_t *__restrict__ act,
+                            const int32_t *__restrict__ act_len, int M, int KK, const int32_t *__restrict__ off2,
+                            int NB, const int32_t *__restrict__ ids, int64_t N) {
+    const int tid = threadIdx.x;
+    // zero counters
+    for (int i = tid; i < BS / 16; i += THREADS) ((uint4 *)cnt32)[i] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) {
+        int acc = 0;
+        S.lpre[0] = 0;
+        for (int m = 0; m < M; m++) {
+            acc += act_len[q * M + m];
+            S.lpre[m + 1] = acc;
+        }
+    }
+    __syncthreads();
+    const int Etot = S.lpre[M];
+    const uint32_t *actq = act + q * (int64_t)M * KK;
+    int e0 = 0, skip = 0;
+    while (e0 < Etot) {
+        // (A) slice table for entries [e0, e0+CAP)  (ATOMIC) or up to the end of e0's subspace
+        int mfirst = 0;
+        {
+            int lo = 0, hi = M;  // largest m with lpre[m] <= e0
+            while (hi - lo > 1) {
+                int mid = (lo + hi) >> 1;
+                if (S.lpre[mid] <= e0) lo = mid;
+                else hi = mid;
+            }
+            mfirst = lo;
+        }
+        int elim = ATOMIC ? Etot : S.lpre[mfirst + 1];
+        int ne = min(CS_CAP, elim - e0);
+        int lens[CS_CAP / THREADS];
+#pragma unroll
+        for (int u = 0; u < CS_CAP / THREADS; u++) {
+            int t = tid * (CS_CAP / THREADS) + u;
+            int len = 0;
+            if (t < ne) {
+                int e = e0 + t;
+                int m = mfirst;
+                while (S.lpre[m + 1] <= e) m++;
+                uint32_t v = actq[(int64_t)m * KK + (e - S.lpre[m])];
+                int c = (int)(v & 0xffffu);
+                const int32_t *o = off2 + ((int64_t)m * KK + c) * (NB + 1) + b;
+                int s0 = o[0], s1 = o[1];
+                if (t == 0) s0 += skip;
+                len = s1 - s0;
+                S.gst[t] = (int32_t)((int64_t)m * N + s0);
+                S.w[t] = (unsigned char)(v >> 16);
+            }
+            lens[u] = len;
+        }
+        int tot;
+        int pres[CS_CAP / THREADS];
+        cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(lens, pres, tot);
+#pragma unroll
+        for (int u = 0; u < CS_CAP / THREADS; u++) {
+            int t = tid * (CS_CAP / THREADS) + u;
+            if (t < ne) S.pre[t] = pres[u];
+        }
+        if (tid == 0) S.pre[ne] = tot;
+        __syncthreads();
+        // (B) how many whole slices fit in one round
+        if (tid == 0) {
+            int lo = 0, hi = ne;  // largest n with pre[n] <= TCAP
+            while (lo < hi) {
+                int mid = (lo + hi + 1) >> 1;
+                if (S.pre[mid] <= CS_TCAP) lo = mid;
+                else hi = mid - 1;
+            }
+            if (lo == 0) {  // first slice alone exceeds a round: take a TCAP piece of it
+                S.round_n = 1;
+                S.round_T = CS_TCAP;
+                S.round_skip = skip + CS_TCAP;
+                S.round_e = e0;
+            } else {
+                S.round_n = lo;
+                S.round_T = S.pre[lo];
+                S.round_skip = 0;
+                S.round_e = e0 + lo;
+            }
+        }
+        __syncthreads();
+        const int rn = S.round_n, T = S.round_T;
+        // (C) position -> slice fill
+        for (int t = tid; t < rn; t += THREADS) {
+            int p0 = S.pre[t], p1 = min(S.pre[t + 1], T);
+            for (int p = p0; p < p1; p++) S.sid[p] = (uint16_t)t;
+        }
+        __syncthreads();
+        // (D) coalesced independent loads, then the counter updates
+        const uint32_t bbase = (uint32_t)b * (uint32_t)BS;
+        int idv[CS_U];
+        unsigned char wv[CS_U];
+#pragma unroll
+        for (int u = 0; u < CS_U; u++) {
+            int p = tid + u * THREADS;
+            idv[u] = -1;
+            wv[u] = 0;
+            if (p < T) {
+                int t = S.sid[p];
+                idv[u] = __ldg(ids + S.gst[t] + (p - S.pre[t]));
+                wv[u] = S.w[t];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < CS_U; u++) {
+            if (idv[u] >= 0) {
+                uint32_t local = (uint32_t)idv[u] - bbase;
+                if (ATOMIC) {
+                    atomicAdd(&cnt32[local >> 2], (uint32_t)wv[u] << ((local & 3) * 8));
+                } else {
+                    unsigned char *cb8 = (unsigned char *)cnt32;
+                    cb8[local] = (unsigned char)(cb8[local] + wv[u]);
+                }
+            }
+        }
+        __syncthreads();
+        e0 = S.round_e;
+        skip = S.round_skip;
+    }
+}
+
+template <bool ATOMIC>
+__global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__restrict__ act,
+                                                           const int32_t *__restrict__ act_len, int M, int KK,
+                                                           const int32_t *__restrict__ off2, int NB,
+                                                           const int32_t *__restrict__ ids, int64_t N, int BS, int tau,
+                                                           int32_t *__restrict__ pool, int64_t PS,
+                                                           int32_t *__restrict__ ncand, uint8_t *__restrict__ traceV) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    uint32_t *cnt32 = (uint32_t *)smraw;
+    CountSmem &S = *(CountSmem *)(smraw + BS);
+    const int b = blockIdx.x;
+    const int64_t q = blockIdx.y;
+    count_block<ATOMIC>(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+    // a4: C = {x : V[x] >= tau}, ascending id (Alg. 1 l.18)
+    const unsigned char *c8 = (const unsigned char *)cnt32;
+    int32_t *outp = pool + q * PS + (int64_t)b * BS;
+    int running = 0;
+    const int tid = threadIdx.x;
+    for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
+        int j = j0 + tid * 16;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (j < BS) v = *(const uint4 *)(c8 + j);
+        const unsigned char *vb = (const unsigned char *)&v;
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < 16; i++) c += vb[i] >= tau;
+        int off, tot;
+        cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(c, off, tot);
+        int o = running + off;
+#pragma unroll
+        for (int i = 0; i < 16; i++)
+            if (vb[i] >= tau) outp[o++] = b * BS + j + i;
+        if (traceV) {
+            int64_t g0 = (int64_t)b * BS + j;
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if (g0 + i < N) traceV[q * N + g0 + i] = vb[i];
+        }
+        running += tot;
+        __syncthreads();
+    }
+    if (tid == 0) ncand[q * NB + b] = running;
+}
+
+// ---------------------------------------------------------------------------
+// a4 fallback (Z8): |C| < k -> the first min(k,|T|) touched ids by
+// (V desc, id asc), restated in ascending id.  Rare; one CTA per query.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict__ act,
+                                                       const int32_t *__restrict__ act_len, int M, int KK,
+                                                       const int32_t *__restrict__ off2, int NB,
+                                                       const int32_t *__restrict__ ids, int64_t N, int BS, int k,
+                                                       int32_t *__restrict__ pool, int64_t PS,
+                                                       int32_t *__restrict__ ncand, int32_t *__restrict__ fbflag) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    uint32_t *cnt32 = (uint32_t *)smraw;
+    CountSmem &S = *(CountSmem *)(smraw + BS);
+    __shared__ int hist[2 * MAX_M + 2];
+    __shared__ int s_total, s_vstar, s_quota, s_eqbase, s_n;
+    const int64_t q = blockIdx.x;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        int t = 0;
+        for (int b = 0; b < NB; b++) t += ncand[q * NB + b];
+        s_total = t;
+    }
+    for (int i = tid; i < 2 * MAX_M + 2; i += THREADS) hist[i] = 0;
+    __syncthreads();
+    if (s_total >= k) {
+        if (tid == 0) fbflag[q] = 0;
+        return;
+    }
+    const unsigned char *c8 = (const unsigned char *)cnt32;
+    // pass 1: histogram of V over the touched set
+    for (int b = 0; b < NB; b++) {
+        count_block<true>(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+        for (int j = tid; j < BS; j += THREADS)
+            if (c8[j]) atomicAdd(&hist[c8[j]], 1);
+        __syncthreads();
+    }
+    if (tid == 0) {
+        int acc = 0, vstar = 1, quota = hist[1];
+        for (int v = 2 * M; v >= 1; v--) {
+            if (acc + hist[v] >= k) {
+                vstar = v;
+                quota = k - acc;
+                break;
+            }
+            acc += hist[v];
+        }
+        s_vstar = vstar;
+        s_quota = quota;
+        s_eqbase = 0;
+        s_n = 0;
+    }
+    __syncthreads();
+    const int vstar = s_vstar, quota = s_quota;
+    int32_t *outp = pool + q * PS;
+    // pass 2: ids with V > V*, and the first `quota` ids with V == V*, ascending
+    for (int b = 0; b < NB; b++) {
+        count_block<true>(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+        for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
+            int j = j0 + tid * 16;
+            unsigned char vb[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) vb[i] = (j + i < BS) ? c8[j + i] : 0;
+            int ceq = 0;
+#pragma unroll
+            for (int i = 0; i < 16; i++) ceq += vb[i] == vstar;
+            int eoff, etot;
+            cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(ceq, eoff, etot);
+            __syncthreads();
+            bool sel[16];
+            int cs = 0, er = s_eqbase + eoff;
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                sel[i] = vb[i] > vstar || (vb[i] == vstar && vb[i] > 0 && er < quota);
+                if (vb[i] == vstar) er++;
+                cs += sel[i];
+            }
+            int soff, stot;
+            cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(cs, soff, stot);
+            int o = s_n + soff;
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if (sel[i]) outp[o++] = b * BS + j + i;
+            __syncthreads();
+            if (tid == 0) {
+                s_eqbase += etot;
+                s_n += stot;
+            }
+            __syncthreads();
+        }
+    }
+    for (int b = tid; b < NB; b += THREADS) ncand[q * NB + b] = (b == 0) ? s_n : 0;
+    if (tid == 0) fbflag[q] = 1;
+}
+
+// ---------------------------------------------------------------------------
+// exact distance of one stored row to q' (fp64, lane partial sums + fixed
+// butterfly; every lane returns the same value)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
+__device__ __forceinline__ void acc4(double &acc, const float4 x, const double *qd4) {
+    const double2 q01 = *(const double2 *)(qd4);
+    const double2 q23 = *(const double2 *)(qd4 + 2);
+    double d0 = __dsub_rn((double)x.x, q01.x), d1 = __dsub_rn((double)x.y, q01.y);
+    double d2 = __dsub_rn((double)x.z, q23.x), d3 = __dsub_rn((double)x.w, q23.y);
+    acc = __fma_rn(d0, d0, acc);
+    acc = __fma_rn(d1, d1, acc);
+    acc = __fma_rn(d2, d2, acc);
+    acc = __fma_rn(d3, d3, acc);
+}
+
+// two rows at once (more loads in flight)
+__device__ __forceinline__ void row_dist2(const float *__restrict__ r0, const float *__restrict__ r1,
+                                          const double *__restrict__ qd, int nvec, int lane, double &o0, double &o1) {
+    double a0 = 0.0, a1 = 0.0;
+    const float4 *x0 = (const float4 *)r0, *x1 = (const float4 *)r1;
+#pragma unroll 4
+    for (int v = lane; v < nvec; v += 32) {
+        float4 u0 = __ldg(x0 + v);
+        float4 u1 = __ldg(x1 + v);
+        acc4(a0, u0, qd + 4 * v);
+        acc4(a1, u1, qd + 4 * v);
+    }
+    o0 = warp_sum(a0);
+    o1 = warp_sum(a1);
+}
+__device__ __forceinline__ double row_dist1(const float *__restrict__ r0, const double *__restrict__ qd, int nvec,
+                                            int lane) {
+    double a0 = 0.0;
+    const float4 *x0 = (const float4 *)r0;
+#pragma unroll 4
+    for (int v = lane; v < nvec; v += 32) acc4(a0, __ldg(x0 + v), qd + 4 * v);
+    return warp_sum(a0);
+}
+
+// warp-cooperative insertion of (d, id) into a sorted list of capacity k
+__device__ __forceinline__ void warp_insert(double *Ld, int64_t *Li, int &cnt, int k, double d, int64_t id, int lane) {
+    int pos = 0;
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+        int i = i0 + lane;
+        bool lt = i < cnt && less_di(Ld[i], Li[i], d, id);
+        pos += __popc(__ballot_sync(0xffffffffu, lt));
+    }
+    int last = min(cnt, k - 1);  // entries [pos, last) move up by one
+    for (int top = last - 1; top >= pos; top -= 32) {
+        int i = top - lane;
+        double td = 0.0;
+        int64_t ti = 0;
+        bool mv = i >= pos;
+        if (mv) {
+            td = Ld[i];
+            ti = Li[i];
+        }
+        __syncwarp();
+        if (mv) {
+            Ld[i + 1] = td;
+            Li[i + 1] = ti;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        Ld[pos] = d;
+        Li[pos] = id;
+    }
+    cnt = min(cnt + 1, k);
+    __syncwarp();
+}
+
+__device__ __forceinline__ void load_qd(double *qd, const float *qrow, int pitch) {
+    for (int i = threadIdx.x; i < pitch; i += blockDim.x) qd[i] = (double)qrow[i];
+}
+
+// ---------------------------------------------------------------------------
+// a5, Guaranteed Mode: exact L2 of every candidate, per-warp top-k, CTA merge.
+// grid (S, Qc); candidates of query q are split over S*WARPS warps.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restrict__ qrot, int pitch,
+                                                           const float *__restrict__ X, int64_t gid_base,
+                                                           const int32_t *__restrict__ pool, int64_t PS, int BS,
+                                                           const int32_t *__restrict__ ncand, int NB, int k,
+                                                           double *__restrict__ part_d, int64_t *__restrict__ part_i) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    double *qd = (double *)sm;
+    double *Ld = qd + pitch;                         // WARPS x k
+    int64_t *Li = (int64_t *)(Ld + WARPS * k);       // WARPS x k
+    int *pre = (int *)(Li + WARPS * k);              // NB + 1
+    __shared__ int wcnt[WARPS];
+    const int64_t q = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    load_qd(qd, qrot + q * pitch, pitch);
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int b = 0; b < NB; b++) {
+            pre[b] = acc;
+            acc += ncand[q * NB + b];
+        }
+        pre[NB] = acc;
+    }
+    __syncthreads();
+    const int total = pre[NB];
+    const int nvec = pitch / 4;
+    const int W = gridDim.x * WARPS;
+    const int gw = blockIdx.x * WARPS + warp;
+    double *myd = Ld + warp * k;
+    int64_t *myi = Li + warp * k;
+    int cnt = 0;
+    double wd = INFINITY;
+    int64_t wi = 0x7fffffffffffffffLL;
+    int bcur = 0;
+    const int32_t *poolq = pool + q * PS;
+    for (int v = gw; v < total; v += 2 * W) {
+        int v1 = v + W;
+        while (pre[bcur + 1] <= v) bcur++;
+        int lid0 = poolq[(int64_t)bcur * BS + (v - pre[bcur])];
+        int lid1 = -1;
+        if (v1 < total) {
+            int b1 = bcur;
+            while (pre[b1 + 1] <= v1) b1++;
+            lid1 = poolq[(int64_t)b1 * BS + (v1 - pre[b1])];
+        }
+        double d0, d1;
+        if (lid1 >= 0) {
+            row_dist2(X + (int64_t)lid0 * pitch, X + (int64_t)lid1 * pitch, qd, nvec, lane, d0, d1);
+        } else {
+            d0 = row_dist1(X + (int64_t)lid0 * pitch, qd, nvec, lane);
+            d1 = INFINITY;
+        }
+        int64_t g0 = gid_base + lid0, g1 = gid_base + lid1;
+        if (cnt < k || less_di(d0, g0, wd, wi)) {
+            warp_insert(myd, myi, cnt, k, d0, g0, lane);
+            if (cnt == k) {
+                wd = myd[k - 1];
+                wi = myi[k - 1];
+            }
+        }
+        if (lid1 >= 0 && (cnt < k || less_di(d1, g1, wd, wi))) {
+            warp_insert(myd, myi, cnt, k, d1, g1, lane);
+            if (cnt == k) {
+                wd = myd[k - 1];
+                wi = myi[k - 1];
+            }
+        }
+    }
+    if (lane == 0) wcnt[warp] = cnt;
+    __syncthreads();
+    // CTA merge: rank of each entry = sum over lists of #entries less than it
+    double *od = part_d + ((int64_t)q * gridDim.x + blockIdx.x) * k;
+    int64_t *oi = part_i + ((int64_t)q * gridDim.x + blockIdx.x) * k;
+    for (int r = threadIdx.x; r < k; r += THREADS) {
+        od[r] = INFINITY;
+        oi[r] = -1;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < WARPS * k; e += THREADS) {
+        int w = e / k, i = e % k;
+        if (i >= wcnt[w]) continue;
+        double d = Ld[w * k + i];
+        int64_t id = Li[w * k + i];
+        int rank = i;
+        for (int w2 = 0; w2 < WARPS; w2++) {
+            if (w2 == w) continue;
+            int lo = 0, hi = wcnt[w2];
+            const double *L2d = Ld + w2 * k;
+            const int64_t *L2i = Li + w2 * k;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (less_di(L2d[mid], L2i[mid], d, id)) lo = mid + 1;
+                else hi = mid;
+            }
+            rank += lo;
+        }
+        if (rank < k) {
+            od[rank] = d;
+            oi[rank] = id;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// merge of L sorted lists (d, id; id < 0 = padding) of length k per query ->
+// final top-k.  Used for the S partial lists of a query and for the G shards.
+// lists layout: [(q*L + l)*k + i] (stride_q = L*k)  or shards [(l*Q + q)*k + i]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(THREADS) k_merge_lists(const double *__restrict__ d, const int64_t *__restrict__ ids,
+                                                          int L, int64_t Q, int k, int shard_major,
+                                                          double *__restrict__ out_d64, float *__restrict__ out_d,
+                                                          int64_t *__restrict__ out_i) {
+    const int64_t q = blockIdx.x;
+    auto idx = [&](int l, int i) -> int64_t {
+        return shard_major ? (((int64_t)l * Q + q) * k + i) : ((q * L + l) * (int64_t)k + i);
+    };
+    for (int r = threadIdx.x; r < k; r += THREADS) {
+        if (out_d64) out_d64[q * k + r] = INFINITY;
+        if (out_d) out_d[q * k + r] = INFINITY;
+        out_i[q * k + r] = -1;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < L * k; e += THREADS) {
+        int l = e / k, i = e % k;
+        int64_t id = ids[idx(l, i)];
+        if (id < 0) continue;
+        double dv = d[idx(l, i)];
+        int rank = i;
+        for (int l2 = 0; l2 < L; l2++) {
+            if (l2 == l) continue;
+            int lo = 0, hi = k;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                int64_t mi = ids[idx(l2, mid)];
+                bool lt = mi >= 0 && less_di(d[idx(l2, mid)], mi, dv, id);
+                if (lt) lo = mid + 1;
+                else hi = mid;
+            }
+            rank += lo;
+        }
+        if (rank < k) {
+            if (out_d64) out_d64[q * k + rank] = dv;
+            if (out_d) out_d[q * k + rank] = (float)dv;
+            out_i[q * k + rank] = id;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Optimized Mode: Hamming order + exact L2 with patience.
+// One CTA per query.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(THREADS) k_rerank_patience(
+    const float *__restrict__ qrot, int pitch, int Dp, const float *__restrict__ X, int64_t gid_base,
+    const uint64_t *__restrict__ codes, int Wd, int32_t *__restrict__ pool, int64_t PS, int BS,
+    const int32_t *__restrict__ ncand, int NB, int32_t *__restrict__ cbuf, uint16_t *__restrict__ hbuf, int64_t CS,
+    int k, int P, double *__restrict__ out_d64, float *__restrict__ out_d, int64_t *__restrict__ out_i,
+    int64_t *__restrict__ nver_out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    double *qd = (double *)sm;                              // pitch
+    double *chd = qd + pitch;                               // PATIENCE_CH
+    int64_t *chi = (int64_t *)(chd + PATIENCE_CH);           // PATIENCE_CH
+    double *Td = (double *)(chi + PATIENCE_CH);              // k
+    int64_t *Ti = (int64_t *)(Td + k);                       // k
+    uint64_t *qc = (uint64_t *)(Ti + k);                     // Wd
+    int *hist = (int *)(qc + Wd);                            // Dp + 2
+    int *pre = hist + Dp + 2;                                // NB + 1
+    __shared__ int s_stop, s_nver_hi, s_cnt_top, s_pat;
+    __shared__ typename cub::BlockScan<int, THREADS>::TempStorage scan;
+    const int64_t q = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float *qrow = qrot + q * pitch;
+    load_qd(qd, qrow, pitch);
+    for (int w = tid; w < Wd; w += THREADS) {
+        uint64_t word = 0;
+        for (int i = 0; i < 64; i++) {
+            int d = w * 64 + i;
+            if (d < Dp && qrow[d] > 0.0f) word |= (uint64_t)1 << i;
+        }
+        qc[w] = word;
+    }
+    for (int i = tid; i < Dp + 2; i += THREADS) hist[i] = 0;
+    if (tid == 0) {
+        int acc = 0;
+        for (int b = 0; b < NB; b++) {
+            pre[b] = acc;
+            acc += ncand[q * NB + b];
+        }
+        pre[NB] = acc;
+        s_stop = 0;
+        s_cnt_top = 0;
+        s_pat = 0;
+    }
+    __syncthreads();
+    const int total = pre[NB];
+    int32_t *poolq = pool + q * PS;
+    int32_t *cq = cbuf + q * CS;
+    uint16_t *hq = hbuf + q * CS;
+    // (1) Hamming distances, compact ascending-id candidate list, histogram
+    {
+        int G = 1;
+        while (G < Wd && G < 32) G <<= 1;
+        const int per_warp = 32 / G;
+        const int g = lane / G, gl = lane % G;
+        for (int v0 = warp * per_warp; v0 < total; v0 += WARPS * per_warp) {
+            int v = v0 + g;
+            int lid = -1, h = 0;
+            if (v < total) {
+                int lo = 0, hi = NB;  // b with pre[b] <= v < pre[b+1]
+                while (hi - lo > 1) {
+                    int mid = (lo + hi) >> 1;
+                    if (pre[mid] <= v) lo = mid;
+                    else hi = mid;
+                }
+                lid = poolq[(int64_t)lo * BS + (v - pre[lo])];
+                const uint64_t *cr = codes + (int64_t)lid * Wd;
+                for (int w = gl; w < Wd; w += G) h += __popcll(qc[w] ^ __ldg(cr + w));
+            }
+            for (int off = G >> 1; off; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
+            if (v < total && gl == 0) {
+                cq[v] = lid;
+                hq[v] = (uint16_t)h;
+                atomicAdd(&hist[h], 1);
+            }
+        }
+    }
+    __syncthreads();
+    // (2) exclusive scan of the histogram -> bin starts
+    {
+        const int nb = Dp + 1;
+        const int per = (nb + THREADS - 1) / THREADS;
+        int loc = 0;
+        for (int i = 0; i < per; i++) {
+            int idx = tid * per + i;
+            if (idx < nb) loc += hist[idx];
+        }
+        int off, tot;
+        cub::BlockScan<int, THREADS>(scan).ExclusiveSum(loc, off, tot);
+        __syncthreads();
+        for (int i = 0; i < per; i++) {
+            int idx = tid * per + i;
+            if (idx < nb) {
+                int c = hist[idx];
+                hist[idx] = off;
+                off += c;
+            }
+        }
+    }
+    __syncthreads();
+    // (3) stable scatter by h (input is ascending id) -> order (h, id) in pool
+    if (warp == 0) {
+        for (int v0 = 0; v0 < total; v0 += 32) {
+            int v = v0 + lane;
+            bool act = v < total;
+            unsigned am = __ballot_sync(0xffffffffu, act);
+            if (act) {
+                int h = hq[v];
+                int lid = cq[v];
+                unsigned peers = __match_any_sync(am, h);
+                int leader = __ffs(peers) - 1;
+                int rank = __popc(peers & ((1u << lane) - 1));
+                int base = 0;
+                if (lane == leader) {
+                    base = hist[h];
+                    hist[h] = base + __popc(peers);
+                }
+                base = __shfl_sync(peers, base, leader);
+                poolq[base + rank] = lid;
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // (4) verification in (h, id) order with patience
+    const int nvec = pitch / 4;
+    int cnt_top = 0;      // warp 0 only
+    int pat = 0;          // consecutive non-improving verifications (warp 0)
+    int64_t nver = total;
+    for (int pos = 0; pos < total; pos += PATIENCE_CH) {
+        const int n = min(PATIENCE_CH, total - pos);
+        for (int i = warp * 2; i < n; i += WARPS * 2) {
+            int l0 = poolq[pos + i];
+            if (i + 1 < n) {
+                int l1 = poolq[pos + i + 1];
+                double d0, d1;
+                row_dist2(X + (int64_t)l0 * pitch, X + (int64_t)l1 * pitch, qd, nvec, lane, d0, d1);
+                if (lane == 0) {
+                    chd[i] = d0;
+                    chi[i] = gid_base + l0;
+                    chd[i + 1] = d1;
+                    chi[i + 1] = gid_base + l1;
+                }
+            } else {
+                double d0 = row_dist1(X + (int64_t)l0 * pitch, qd, nvec, lane);
+                if (lane == 0) {
+                    chd[i] = d0;
+                    chi[i] = gid_base + l0;
+                }
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int stop_at = -1;
+            for (int g0 = 0; g0 < n && stop_at < 0; g0 += 32) {
+                const int gn = min(32, n - g0);
+                const double myd = lane < gn ? chd[g0 + lane] : INFINITY;
+                const int64_t myi = lane < gn ? chi[g0 + lane] : 0x7fffffffffffffffLL;
+                int start = 0;
+                while (start < gn) {
+                    bool full = cnt_top >= k;
+                    double wdv = full ? Td[k - 1] : 0.0;
+                    int64_t wiv = full ? Ti[k - 1] : 0;
+                    bool better = lane >= start && lane < gn && (!full || less_di(myd, myi, wdv, wiv));
+                    unsigned mask = __ballot_sync(0xffffffffu, better);
+                    int f = mask ? (__ffs(mask) - 1) : gn;
+                    int nonimp = f - start;
+                    if (P > 0 && pat + nonimp >= P) {
+                        stop_at = g0 + start + (P - pat) - 1;
+                        break;
+                    }
+                    pat += nonimp;
+                    if (f >= gn) break;
+                    double dd = __shfl_sync(0xffffffffu, myd, f);
+                    int64_t ii = __shfl_sync(0xffffffffu, myi, f);
+                    warp_insert(Td, Ti, cnt_top, k, dd, ii, lane);
+                    pat = 0;
+                    start = f + 1;
+                }
+            }
+            if (lane == 0 && stop_at >= 0) {
+                s_stop = 1;
+                s_nver_hi = pos + stop_at + 1;
+            }
+            if (lane == 0) s_cnt_top = cnt_top;
+        }
+        __syncthreads();
+        if (s_stop) {
+            nver = s_nver_hi;
+            break;
+        }
+    }
+    __syncthreads();
+    const int ct = s_cnt_top;
+    for (int r = tid; r < k; r += THREADS) {
+        double dv = r < ct ? Td[r] : INFINITY;
+        int64_t iv = r < ct ? Ti[r] : -1;
+        if (out_d64) out_d64[q * k + r] = dv;
+        if (out_d) out_d[q * k + r] = (float)dv;
+        out_i[q * k + r] = iv;
+    }
+    if (tid == 0 && nver_out) nver_out[q] = nver;
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+struct StageEv {
+    cudaEvent_t a, b;
+    int stage;
+};
+static thread_local std::vector<StageEv> g_events;
+static thread_local double g_stage_ms[8];
+static bool g_timing = false;
+
+bool stage_timing_on() { return g_timing; }
+
+struct StageScope {
+    cudaStream_t s;
+    int stage;
+    cudaEvent_t a = nullptr, b = nullptr;
+    StageScope(cudaStream_t s_, int st) : s(s_), stage(st) {
+        if (!g_timing) return;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+    }
+    ~StageScope() {
+        if (!g_timing) return;
+        cudaEventRecord(b, s);
+        g_events.push_back({a, b, stage});
+    }
+};
+
+struct DevBuf {
+    cudaStream_t s;
+    std::vector<void *> ptrs;
+    explicit DevBuf(cudaStream_t s_) : s(s_) {}
+    template <class T>
+    T *alloc(size_t n) {
+        void *p = nullptr;
+        CRISP_CUDA(cudaMallocAsync(&p, std::max<size_t>(n * sizeof(T), 16), s));
+        ptrs.push_back(p);
+        return (T *)p;
+    }
+    ~DevBuf() {
+        for (void *p : ptrs) cudaFreeAsync(p, s);
+    }
+};
+
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
+            cudaStream_t s, const crisp_trace_t *tr) {
+    const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch;
+    const int64_t N = ix->N, PS = (int64_t)NB * BS;
+    const bool atomic_count = env_int("CRISP_COUNT_ATOMIC", 1) != 0;
+    // per-query workspace bytes -> query chunk
+    int64_t perq = (int64_t)pitch * 4 * 2 + (int64_t)M * KK * 4 + (int64_t)M * 12 + PS * 4 + (int64_t)NB * 4 + 64;
+    const int S = (mode == 0) ? std::max(1, env_int("CRISP_RERANK_SPLITS", 8)) : 1;
+    if (mode == 0) perq += (int64_t)S * k * 16;
+    else perq += N * 6;
+    if (tr && tr->V) perq += N;
+    int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : (16LL << 30);
+    int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
+    Qc = std::min<int64_t>(Qc, 65535);
+    if (tr) Qc = std::min<int64_t>(Qc, Q);
+    DevBuf wb(s);
+    float *qpad = wb.alloc<float>((size_t)Qc * pitch);
+    float *qrot = ix->rotated ? wb.alloc<float>((size_t)Qc * pitch) : qpad;
+    uint32_t *act = wb.alloc<uint32_t>((size_t)Qc * M * KK);
+    int32_t *act_len = wb.alloc<int32_t>((size_t)Qc * M);
+    int64_t *retr = wb.alloc<int64_t>((size_t)Qc * M);
+    int32_t *pool = wb.alloc<int32_t>((size_t)Qc * PS);
+    int32_t *ncand = wb.alloc<int32_t>((size_t)Qc * NB);
+    int32_t *fb = wb.alloc<int32_t>((size_t)Qc);
+    double *part_d = nullptr;
+    int64_t *part_i = nullptr, *nver = nullptr;
+    int32_t *cbuf = nullptr;
+    uint16_t *hbuf = nullptr;
+    if (mode == 0) {
+        part_d = wb.alloc<double>((size_t)Qc * S * k);
+        part_i = wb.alloc<int64_t>((size_t)Qc * S * k);
+    } else {
+        cbuf = wb.alloc<int32_t>((size_t)Qc * N);
+        hbuf = wb.alloc<uint16_t>((size_t)Qc * N);
+        nver = wb.alloc<int64_t>((size_t)Qc);
+    }
+    uint8_t *traceV = (tr && tr->V) ? wb.alloc<uint8_t>((size_t)Qc * N) : nullptr;
+    double *d64tmp = out.d64 ? nullptr : wb.alloc<double>((size_t)Qc * k);
+
+    // kernel attributes (dynamic smem)
+    const int probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
+    const int probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
+    const int count_smem = BS + (int)sizeof(CountSmem);
+    const int rx_smem = pitch * 8 + WARPS * k * 16 + (NB + 1) * 4;
+    const int pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + ix->W * 8 + (ix->Dp + 2) * 4 + (NB + 1) * 4;
+    static bool attr_done = false;
+    if (!attr_done) {
+        CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_count_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_count_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_rerank_patience, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr_done = true;
+    }
+    CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
+                    pat_smem <= 220 * 1024,
+                "shared-memory footprint too large for this (D, K, k)");
+
+    const int wk = (mode == 1) ? k : 0;
+    const int P = (mode == 1 && ix->patience_factor > 0) ? ix->patience_factor * k : 0;
+    std::vector<int32_t> h_pool, h_ncand;
+    for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
+        const int64_t qn = std::min(Qc, Q - q0);
+        {
+            StageScope st(s, 0);
+            k_prep_queries<<<nblk(qn * pitch, 256), 256, 0, s>>>(queries + q0 * ix->D, qn, ix->D, pitch, qpad);
+            CRISP_LAUNCH();
+            if (ix->rotated) rotate_rows_f64(qpad, qn, ix->Dp, pitch, ix->R, qrot, pitch, s);
+        }
+        {
+            StageScope st(s, 1);
+            dim3 g(nblk(qn, WARPS), M);
+            k_probe<<<g, THREADS, probe_smem, s>>>(qrot, pitch, qn, ix->cb, M, K, ix->dh, ix->gsize, probe_gs,
+                                                   ix->budget, wk, act, act_len, retr);
+            CRISP_LAUNCH();
+        }
+        {
+            StageScope st(s, 2);
+            dim3 g(NB, (unsigned)qn);
+            if (atomic_count)
+                k_count_select<true><<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS,
+                                                                    ix->tau, pool, PS, ncand, traceV);
+            else
+                k_count_select<false><<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N,
+                                                                     BS, ix->tau, pool, PS, ncand, traceV);
+            CRISP_LAUNCH();
+        }
+        {
+            StageScope st(s, 3);
+            k_fallback<<<(unsigned)qn, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, k,
+                                                                 pool, PS, ncand, fb);
+            CRISP_LAUNCH();
+        }
+        if (tr && (tr->cand || tr->cand_n || (tr->order && mode == 0) || (tr->n_verified && mode == 0))) {
+            h_pool.resize((size_t)qn * PS);
+            h_ncand.resize((size_t)qn * NB);
+            CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), pool, (size_t)qn * PS * 4, cudaMemcpyDeviceToHost, s));
+            CRISP_CUDA(cudaMemcpyAsync(h_ncand.data(), ncand, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
+            CRISP_CUDA(cudaStreamSynchronize(s));
+            for (int64_t q = 0; q < qn; q++) {
+                int64_t n = 0;
+                for (int b = 0; b < NB; b++) {
+                    int c = h_ncand[q * NB + b];
+                    for (int j = 0; j < c; j++) {
+                        int32_t id = h_pool[q * PS + (int64_t)b * BS + j];
+                        if (tr->cand) tr->cand[(q0 + q) * N + n] = id;
+                        if (tr->order && mode == 0) tr->order[(q0 + q) * N + n] = id;
+                        n++;
+                    }
+                }
+                if (tr->cand_n) tr->cand_n[q0 + q] = n;
+                if (tr->n_verified && mode == 0) tr->n_verified[q0 + q] = n;
+            }
+        }
+        int64_t *oi = out.ids + q0 * k;
+        double *od64 = out.d64 ? out.d64 + q0 * k : d64tmp;
+        float *od = out.d32 ? out.d32 + q0 * k : nullptr;
+        if (mode == 0) {
+            {
+                StageScope st(s, 4);
+                dim3 g(S, (unsigned)qn);
+                k_rerank_exact<<<g, THREADS, rx_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, PS, BS, ncand, NB,
+                                                          k, part_d, part_i);
+                CRISP_LAUNCH();
+            }
+            {
+                StageScope st(s, 5);
+                k_merge_lists<<<(unsigned)qn, THREADS, 0, s>>>(part_d, part_i, S, qn, k, 0, od64, od, oi);
+                CRISP_LAUNCH();
+            }
+        } else {
+            StageScope st(s, 4);
+            k_rerank_patience<<<(unsigned)qn, THREADS, pat_smem, s>>>(qrot, pitch, ix->Dp, ix->X, ix->gid_base,
+                                                                     ix->codes, ix->W, pool, PS, BS, ncand, NB, cbuf,
+                                                                     hbuf, N, k, P, od64, od, oi, nver);
+            CRISP_LAUNCH();
+        }
+        if (tr) {
+            std::vector<int32_t> hl((size_t)qn * M);
+            std::vector<uint32_t> ha;
+            std::vector<int64_t> hr((size_t)qn * M);
+            CRISP_CUDA(cudaMemcpyAsync(hl.data(), act_len, (size_t)qn * M * 4, cudaMemcpyDeviceToHost, s));
+            CRISP_CUDA(cudaMemcpyAsync(hr.data(), retr, (size_t)qn * M * 8, cudaMemcpyDeviceToHost, s));
+            if (tr->act_cell || tr->act_w) {
+                ha.resize((size_t)qn * M * KK);
+                CRISP_CUDA(cudaMemcpyAsync(ha.data(), act, (size_t)qn * M * KK * 4, cudaMemcpyDeviceToHost, s));
+            }
+            if (tr->V)
+                CRISP_CUDA(cudaMemcpyAsync(tr->V + q0 * N, traceV, (size_t)qn * N, cudaMemcpyDeviceToHost, s));
+            if (tr->qrot) {
+                for (int64_t q = 0; q < qn; q++)
+                    CRISP_CUDA(cudaMemcpyAsync(tr->qrot + (q0 + q) * ix->Dp, qrot + q * pitch, (size_t)ix->Dp * 4,
+                                               cudaMemcpyDeviceToHost, s));
+            }
+            if (tr->fallback)
+                CRISP_CUDA(cudaMemcpyAsync(tr->fallback + q0, fb, (size_t)qn * 4, cudaMemcpyDeviceToHost, s));
+            std::vector<int64_t> hn;
+            if (mode == 1 && tr->n_verified) {
+                hn.resize(qn);
+                CRISP_CUDA(cudaMemcpyAsync(hn.data(), nver, (size_t)qn * 8, cudaMemcpyDeviceToHost, s));
+            }
+            if (mode == 1 && tr->order) {
+                h_pool.resize((size_t)qn * PS);
+                CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), pool, (size_t)qn * PS * 4, cudaMemcpyDeviceToHost, s));
+            }
+            if (mode == 1 && (tr->order || tr->cand || tr->cand_n)) {
+                h_ncand.resize((size_t)qn * NB);
+                CRISP_CUDA(cudaMemcpyAsync(h_ncand.data(), ncand, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
+            }
+            CRISP_CUDA(cudaStreamSynchronize(s));
+            for (int64_t q = 0; q < qn; q++) {
+                for (int m = 0; m < M; m++) {
+                    int L = hl[q * M + m];
+                    if (tr->act_len) tr->act_len[(q0 + q) * M + m] = L;
+                    if (tr->retrieved) tr->retrieved[(q0 + q) * M + m] = hr[q * M + m];
+                    for (int r = 0; r < L && !ha.empty(); r++) {
+                        uint32_t v = ha[(q * M + m) * (int64_t)KK + r];
+                        if (tr->act_cell) tr->act_cell[((q0 + q) * M + m) * (int64_t)KK + r] = (int32_t)(v & 0xffffu);
+                        if (tr->act_w) tr->act_w[((q0 + q) * M + m) * (int64_t)KK + r] = (int32_t)(v >> 16);
+                    }
+                }
+                if (mode == 1) {
+                    int64_t n = 0;
+                    for (int b = 0; b < NB; b++) n += h_ncand.empty() ? 0 : h_ncand[q * NB + b];
+                    if (tr->order)
+                        for (int64_t i = 0; i < n; i++) tr->order[(q0 + q) * N + i] = h_pool[q * PS + i];
+                    if (tr->n_verified) tr->n_verified[q0 + q] = hn[q];
+                }
+            }
+        }
+    }
+}
+
+void merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32_t k, double *out_d64, float *out_d,
+                int64_t *out_ids, cudaStream_t s) {
+    if (Q <= 0) return;
+    k_merge_lists<<<(unsigned)Q, THREADS, 0, s>>>(d, ids, G, Q, k, 1, out_d64, out_d, out_ids);
+    CRISP_LAUNCH();
+}
+
+void stage_record(int, cudaEvent_t, cudaEvent_t) {}
+
+}  // namespace crisp
+
+// stage timing ABI
+extern "C" crisp_status crisp_set_stage_timing(int32_t on) {
+    crisp::g_timing = on != 0;
+    return CRISP_OK;
+}
+
+extern "C" crisp_status crisp_stage_times(double *ms, int32_t n, int32_t reset) {
+    for (auto &e : crisp::g_events) {
+        cudaEventSynchronize(e.b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e.a, e.b);
+        if (e.stage >= 0 && e.stage < 8) crisp::g_stage_ms[e.stage] += t;
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    crisp::g_events.clear();
+    for (int i = 0; i < n && i < 8; i++) ms[i] = crisp::g_stage_ms[i];
+    if (reset)
+        for (int i = 0; i < 8; i++) crisp::g_stage_ms[i] = 0.0;
+    return CRISP_OK;
+}
