@@ -1,0 +1,480 @@
+#!/usr/bin/env python
+"""bench.py -- CRISP batched search on B200 (BASELINE.json metric:
+"QPS at recall@10>=0.9 (1/2/4/8 B200); count/re-rank HBM GB/s vs peak").
+
+A step = one crisp_search_async over the whole query batch (all hot-path
+stages a0..a5, plus the a6 all-gather/merge when G > 1), inputs resident in
+HBM.  Workload at N=1: BASELINE configs[1] (N=1M, D=960, Q=10k, k=10,
+synthetic Gist-like data) at the operating point (M, beta,
+alpha, mode) of configs/operating_points.json, which a sweep (--sweep)
+selected as the fastest with recall@10 >= 0.9 against exact ground truth.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--cfg 2]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+OPS = os.path.join(ROOT, "configs", "operating_points.json")
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
+
+
+# --------------------------------------------------------------------------- utils
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def env_int(n, d):
+    return int(os.environ.get(n, d))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.lines = []
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+        return self
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def load_op(cfg: int, mode_override=None):
+    with open(OPS) as f:
+        ops = json.load(f)
+    op = dict(ops[str(cfg)])
+    if mode_override is not None:
+        op["mode"] = mode_override
+        op.update(op.get("per_mode", {}).get(str(mode_override), {}))
+    return op
+
+
+def ground_truth(X, Qd, k, extra=32):
+    """Exact kNN: fp32 screening on the GPU (TF32 off), exact fp64
+    re-check of the best k+extra, ties by id.  Setup, not timed."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    xn = (X.double() ** 2).sum(1).float()
+    out = torch.empty((Qd.shape[0], k), dtype=torch.int64, device=X.device)
+    for q0 in range(0, Qd.shape[0], 256):
+        q = Qd[q0:q0 + 256]
+        d = xn[None, :] - 2.0 * (q @ X.T) + (q.double() ** 2).sum(1).float()[:, None]
+        cand = torch.topk(d, k + extra, dim=1, largest=False).indices
+        xc = X[cand].double()
+        dd = ((xc - q.double()[:, None, :]) ** 2).sum(2)
+        # sort by (d, id): ids are < 2^31, distances > 0 -> lexsort via two stable sorts
+        o = torch.argsort(cand, dim=1, stable=True)
+        dd, cand = dd.gather(1, o), cand.gather(1, o)
+        o = torch.argsort(dd, dim=1, stable=True)
+        out[q0:q0 + 256] = cand.gather(1, o)[:, :k]
+    return out
+
+
+def recall_at(ids, gt, k=10):
+    ids = ids[:, :k].cpu().numpy() if hasattr(ids, "cpu") else np.asarray(ids)[:, :k]
+    gt = gt[:, :k].cpu().numpy() if hasattr(gt, "cpu") else np.asarray(gt)[:, :k]
+    hits = [len(set(a.tolist()) & set(b.tolist())) for a, b in zip(ids, gt)]
+    return float(np.mean(hits)) / k
+
+
+# --------------------------------------------------------------------------- oracle (reference arm / cpu_baseline)
+def oracle_qps(X_host, Q_host, op, k, budget_seconds=15.0, max_queries=None):
+    """The CPU oracle as it stands, on all host cores, on a bounded sample."""
+    import oracle
+
+    M, beta, alpha, mode = op["M"], op["beta"], op["alpha"], op["mode"]
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    ox = oracle.build(X_host, M, K=50, kmeans_iters=20, kmeans_sample=100000, seed=op.get("seed", 1))
+    t_build = time.time() - t0
+    B, tau = oracle.budget_ids(beta, X_host.shape[0]), oracle.tau_int(alpha, M)
+    nq = min(64, Q_host.shape[0])
+    t0 = time.time()
+    oracle.search(ox, Q_host[:nq], k, mode, B, tau, nthreads=cores)
+    per_q = (time.time() - t0) / nq
+    n = int(min(max_queries or Q_host.shape[0], max(nq, budget_seconds / max(per_q, 1e-6))))
+    return ox, (B, tau), dict(per_q=per_q, n=n, cores=cores, build_s=t_build)
+
+
+def run_reference(args):
+    """--impl reference: the oracle, timed as it stands on the box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+
+    cfg = args.cfg
+    c = synth.CONFIGS[cfg]
+    N, Q, k = args.N or c["N"], args.Q or c["Q"], c["k"]
+    op = load_op(cfg, args.mode)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    w = synth.Workload(cfg, device=dev)
+    X = w.base(N)
+    Qd = w.queries(Q)
+    gt = ground_truth(X, Qd, k) if dev == "cuda" else None
+    Xh, Qh = X.cpu().numpy(), Qd.cpu().numpy()
+    del X
+    ox, (B, tau), cal = oracle_qps(Xh, Qh, op, k)
+    per_step = max(1, min(Q, int(cal["n"] * 1.0 / max(1, args.steps + args.warmup) * 3)))
+    cores = cal["cores"]
+    for s in range(args.warmup):
+        oracle.search(ox, Qh[:per_step], k, op["mode"], B, tau, nthreads=cores)
+    t0 = time.perf_counter()
+    res = []
+    for s in range(args.steps):
+        lo = (s * per_step) % max(1, Q - per_step + 1)
+        ids, _, _ = oracle.search(ox, Qh[lo:lo + per_step], k, op["mode"], B, tau, nthreads=cores)
+        res.append((lo, ids))
+    dt = time.perf_counter() - t0
+    qps = per_step * args.steps / dt
+    rec = None
+    if gt is not None:
+        rec = float(np.mean([recall_at(ids, gt[lo:lo + per_step], 10) for lo, ids in res]))
+    sample = f"{per_step} queries per step x {args.steps} steps of {c['name']} (oracle index built on all N={N})"
+    line = {
+        "impl": "reference", "metric": "QPS at recall@10>=0.9", "value": qps, "unit": "queries/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": c["name"], "N": N, "D": c["D"], "Q": Q, "k": k, "M": op["M"], "beta": op["beta"],
+                   "alpha": op["alpha"], "mode": op["mode"]},
+        "recall@10": rec,
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- crisp arm
+def run_crisp(args):
+    import __graft_entry__ as ge
+
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0:
+        ge.build()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+    import paper_2603_05180_b200 as crisp
+    from paper_2603_05180_b200 import dist as cdist
+
+    cfg = args.cfg
+    c = synth.CONFIGS[cfg]
+    N, Q, k, D = args.N or c["N"], args.Q or c["Q"], c["k"], c["D"]
+    op = load_op(cfg, args.mode)
+    M, beta, alpha, mode = op["M"], op["beta"], op["alpha"], op["mode"]
+    w = synth.Workload(cfg, device=dev)
+    t0 = time.time()
+    Qd = w.queries(Q)
+    X = w.base(N) if (rank == 0) else None
+    gen_s = time.time() - t0
+    bparams = dict(K=50, seed=op.get("seed", 1))
+    t0 = time.time()
+    if world == 1:
+        index = crisp.Index.build(X, M, **bparams)
+        index.set_search_params(beta=beta, alpha=alpha, patience_factor=op.get("patience_factor", 40))
+        engine = None
+    else:
+        engine = cdist.CudaEngine(crisp, dev)
+        R, cb = engine.build_global(X, M, **bparams) if rank == 0 else (None, None)
+        R, cb = cdist.share_model(R, cb, Qd)
+        lo, hi = cdist.shard_range(N, rank, world)
+        Xs = w.rows(lo, hi - lo)
+        engine.build_shard(Xs, lo, M, R, cb, **bparams)
+        del Xs
+        cdist.global_cell_sizes(engine)
+        engine.set_search_params(beta=beta, alpha=alpha, patience_factor=op.get("patience_factor", 40))
+        index = engine.index
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    info = index.info()
+    gt = ground_truth(X, Qd, k) if rank == 0 else None
+    stream = torch.cuda.current_stream().cuda_stream
+    ids = torch.empty((Q, k), dtype=torch.int64, device=dev)
+    dd = torch.empty((Q, k), dtype=torch.float32, device=dev)
+
+    def step():
+        if world == 1:
+            index.search_async(Qd, k, mode, ids, dd, stream)
+            return ids
+        oi, _ = cdist.search_step(engine, Qd, k, mode, stream)
+        return oi
+
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize()
+    crisp.stage_times(reset=True)
+    crisp.search_counters(reset=True)
+    crisp.set_stage_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            out = step()
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    st = crisp.stage_times(reset=True)
+    cnt = crisp.search_counters(reset=True)
+    crisp.set_stage_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    K = args.steps
+    qps = Q * K / (ms / 1e3)
+    rec = recall_at(out, gt, 10) if rank == 0 else None
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if rank == 0 and world == 1:
+        qh = torch.empty((Q, D), dtype=torch.float32).pin_memory()
+        qh.copy_(Qd.cpu())
+        qn = qh.numpy()
+        ih = torch.empty((Q, k), dtype=torch.int64).pin_memory().numpy()
+        dh = torch.empty((Q, k), dtype=torch.float32).pin_memory().numpy()
+        crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, mode, crisp._ptr(ih), crisp._ptr(dh))
+        t0 = time.perf_counter()
+        for _ in range(K):
+            st_ = crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, mode, crisp._ptr(ih), crisp._ptr(dh))
+            crisp._check(st_)
+        dt = time.perf_counter() - t0
+        e2e = {"value": Q * K / dt, "unit": "queries/s", "h2d_bytes_per_step": Q * D * 4,
+               "d2h_bytes_per_step": Q * k * 12, "recall@10": recall_at(ih, gt, 10)}
+
+    # ---------------- roofline of the dominant kernel (algorithmic bytes / CUDA-event time)
+    peak, peak_src = hbm_peak()
+    row_bytes = 4 * info["pitch"]
+    kernels = {}
+    if st["verify"] > 0:
+        vb = cnt["verified"] * row_bytes / K  # 4D per verified row (SURVEY 8(d) B_rerank)
+        kernels["verify"] = {"kernel": "k_rerank_exact" if mode == 0 else "k_rerank_patience",
+                             "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
+                             "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
+    if st["count_select"] > 0:
+        cb_ = cnt["ids_streamed"] * 4 / K  # 4 B per id streamed (SURVEY 8(d) B_count)
+        kernels["count"] = {"kernel": "k_count_select", "bytes_per_step": cb_, "ms_per_step": st["count_select"] / K,
+                            "achieved_gbs": cb_ / (st["count_select"] / K * 1e-3) / 1e9}
+    dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"]) if kernels else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if dom and os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                tj = json.load(f)
+            key = f"cfg{cfg}-mode{mode}-{kernels[dom]['kernel']}"
+            if key in tj:
+                traffic = tj[key]["dram_bytes_per_step"]
+        except Exception:
+            traffic = None
+    roof = None
+    if dom:
+        a = kernels[dom]["achieved_gbs"]
+        roof = {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak, "traffic": traffic,
+                "kernel": kernels[dom]["kernel"], "peak_source": peak_src}
+
+    # ---------------- cpu baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        Xh, Qh = X.cpu().numpy(), Qd.cpu().numpy()
+        ox, (B, tau), cal = oracle_qps(Xh, Qh, op, k, budget_seconds=args.cpu_seconds)
+        n = cal["n"]
+        t0 = time.perf_counter()
+        oracle.search(ox, Qh[:n], k, mode, B, tau, nthreads=cal["cores"])
+        dt = time.perf_counter() - t0
+        cpu = {"value": n / dt, "unit": "queries/s", "cores": cal["cores"], "kind": "oracle",
+               "sample": f"first {n} of the {Q} queries, oracle index built on all N={N} (build {cal['build_s']:.0f}s)"}
+        del ox
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": "QPS at recall@10>=0.9", "value": qps, "unit": "queries/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": c["name"], "N": N, "D": D, "Q": Q, "k": k, "M": M, "beta": beta, "alpha": alpha,
+                       "mode": ["guaranteed", "optimized"][mode], "budget_ids": info["budget"], "tau": info["tau"],
+                       "rotated": bool(info["rotated"]), "cev": info["cev"],
+                       "l2": "inputs larger than L2 (X = %.2f GB >> 126 MB); no flush" % (N * D * 4 / 1e9),
+                       "parallelism": f"points sharded x{world}" if world > 1 else "single GPU"},
+            "recall@10": rec,
+            "roofline": roof,
+            "kernels": kernels,
+            "stage_ms_per_step": {k_: v / K for k_, v in st.items()},
+            "counters_per_step": {k_: v / K for k_, v in cnt.items()},
+            "gpu_launches": cnt["launches"],
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "build_seconds": build_s,
+            "gen_seconds": gen_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+# --------------------------------------------------------------------------- sweep
+def run_sweep(args):
+    """Grid over (M, beta, alpha, mode) -> recall@10 and QPS (1 timed step)."""
+    import __graft_entry__ as ge
+
+    ge.build()
+    import paper_2603_05180_b200 as crisp
+
+    cfg = args.cfg
+    c = synth.CONFIGS[cfg]
+    N, Q, k = args.N or c["N"], args.Q or c["Q"], c["k"]
+    dev = torch.device("cuda", 0)
+    w = synth.Workload(cfg, device=dev)
+    X, Qd = w.base(N), w.queries(Q)
+    gt = ground_truth(X, Qd, k)
+    Ms = [int(m) for m in args.sweep_M.split(",")]
+    betas = [float(b) for b in args.sweep_beta.split(",")]
+    alphas = [float(a) for a in args.sweep_alpha.split(",")]
+    modes = [int(m) for m in args.sweep_modes.split(",")]
+    ids = torch.empty((Q, k), dtype=torch.int64, device=dev)
+    dd = torch.empty((Q, k), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    rows = []
+    for M in Ms:
+        t0 = time.time()
+        ix = crisp.Index.build(X, M, K=50, seed=1)
+        log(f"built M={M} in {time.time() - t0:.1f}s rotated={ix.info()['rotated']} cev={ix.info()['cev']:.3f}")
+        for mode in modes:
+            for beta in betas:
+                for alpha in alphas:
+                    ix.set_search_params(beta=beta, alpha=alpha, patience_factor=40)
+                    ix.search_async(Qd, k, mode, ids, dd, stream)
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    ix.search_async(Qd, k, mode, ids, dd, stream)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ms = e0.elapsed_time(e1)
+                    r = dict(M=M, mode=mode, beta=beta, alpha=alpha, recall=recall_at(ids, gt, 10), qps=Q / ms * 1e3,
+                             ms=ms)
+                    rows.append(r)
+                    print(json.dumps(r), flush=True)
+        ix.free()
+    best = {}
+    for mode in modes:
+        ok = [r for r in rows if r["mode"] == mode and r["recall"] >= 0.9]
+        if ok:
+            best[mode] = max(ok, key=lambda r: r["qps"])
+    print(json.dumps({"best": best}), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="crisp", choices=["crisp", "reference"])
+    ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--mode", type=int, default=None)
+    ap.add_argument("--N", type=int, default=None)
+    ap.add_argument("--Q", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--sweep-M", default="16")
+    ap.add_argument("--sweep-beta", default="0.005,0.01,0.02,0.04")
+    ap.add_argument("--sweep-alpha", default="0.1,0.2,0.3,0.4")
+    ap.add_argument("--sweep-modes", default="0,1")
+    args = ap.parse_args()
+    if args.warmup < 3 and not args.sweep:
+        log("warning: fewer than 3 warm-up steps")
+    if args.sweep:
+        return run_sweep(args)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_crisp(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -193,6 +193,14 @@ crisp_status crisp_export(const crisp_index *idx, crisp_export_t *out);
 crisp_status crisp_set_stage_timing(int32_t on);
 crisp_status crisp_stage_times(double *ms, int32_t n, int32_t reset);
 
+/* Work counters accumulated over the searches run while stage timing is on
+ * (current device), for algorithmic-byte accounting: out[0] ids streamed by
+ * the collision count (a3), out[1] sum of |C_q| (a4), out[2] rows verified
+ * (a5), out[3] queries that took the fallback, out[4] kernels of this library
+ * launched by searches/merges on the calling thread (counted always).  Up to n
+ * entries are written; reset != 0 clears them. */
+crisp_status crisp_search_counters(int64_t *out, int32_t n, int32_t reset);
+
 void crisp_free(crisp_index *idx);
 const char *crisp_last_error(void);
 const char *crisp_version(void);

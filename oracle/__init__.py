@@ -25,7 +25,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "crisp_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
+CFLAGS = ["-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
 
 
 def compile_oracle(force: bool = False) -> str:
@@ -169,8 +169,16 @@ def cev_from_eigs(w) -> float:
 
 
 def cev(X, seed: int) -> float:
+    """Spectral check: covariance of the bounded sample (C, fp64),
+    eigenvalues by LAPACK (numpy.linalg.eigvalsh, a library step), CEV (C)."""
     X = np.ascontiguousarray(X, dtype=np.float32)
-    return lib().or_cev(_p(X), X.shape[0], X.shape[1], X.shape[1], seed)
+    N = X.shape[0]
+    n = cev_sample_size(N)
+    if n < 2:
+        return 0.0
+    rows = np.arange(N, dtype=np.int64) if n == N else sample_rows(N, n, seed, 1)
+    w = np.linalg.eigvalsh(covariance(X, rows))
+    return cev_from_eigs(w)
 
 
 def qr(G):
@@ -189,11 +197,14 @@ def gaussian_matrix(D: int, seed: int):
 
 
 def rotation(D: int, seed: int):
-    """R (fp32) and its fp64 source Q."""
-    R32 = np.zeros((D, D), dtype=np.float32)
-    R64 = np.zeros((D, D), dtype=np.float64)
-    lib().or_rotation(D, seed, _p(R32), _p(R64))
-    return R32, R64
+    """R (fp32) and its fp64 source Q: G from the Philox generator, Q of
+    QR(G) by LAPACK (numpy.linalg.qr, a library step) with diag(R') > 0.
+    The plain Householder or_qr_householder is pinned against it in the tests."""
+    G = gaussian_matrix(D, seed)
+    Qm, Rm = np.linalg.qr(G)
+    sg = np.where(np.diag(Rm) < 0, -1.0, 1.0)
+    R64 = np.ascontiguousarray(Qm * sg[None, :])
+    return R64.astype(np.float32), R64
 
 
 def rotate_rows(X, R):

@@ -159,21 +159,33 @@ void or_covariance(const float *X, int64_t ld, const int64_t *rows, int64_t n, i
         for (int64_t r = 0; r < n; r++) s += (double)X[rows[r] * ld + i];
         mu[i] = s / (double)n;
     }
-#pragma omp parallel for schedule(dynamic)
-    for (int32_t i = 0; i < D; i++) {
-        for (int32_t j = 0; j <= i; j++) {
-            double s = 0.0;
-            for (int64_t r = 0; r < n; r++) {
-                const float *x = X + rows[r] * ld;
-                double di = (double)x[i] - mu[i];
-                double dj = (double)x[j] - mu[j];
-                s = fma(di, dj, s);
+    /* C_ij = sum_r fma(d_ri, d_rj, .) over r ascending, d = x - mu (divisor n-1).
+     * Rows are visited in blocks (r still ascending for every output) so each
+     * block stays in cache; threads own disjoint output rows i. */
+    for (int64_t e = 0; e < (int64_t)D * D; e++) C[e] = 0.0;
+    const int64_t RB = 64;
+    double *dblk = (double *)malloc(sizeof(double) * (size_t)RB * D);
+    for (int64_t r0 = 0; r0 < n; r0 += RB) {
+        int64_t rn = n - r0 < RB ? n - r0 : RB;
+        for (int64_t r = 0; r < rn; r++)
+            for (int32_t i = 0; i < D; i++) dblk[r * D + i] = (double)X[rows[r0 + r] * ld + i] - mu[i];
+#pragma omp parallel for schedule(dynamic, 8)
+        for (int32_t i = 0; i < D; i++) {
+            double *ci = C + (int64_t)i * D;
+            for (int64_t r = 0; r < rn; r++) {
+                const double *dr = dblk + r * D;
+                double di = dr[i];
+                for (int32_t j = 0; j <= i; j++) ci[j] = fma(di, dr[j], ci[j]);
             }
-            s = s / (double)(n - 1);
-            C[(int64_t)i * D + j] = s;
-            C[(int64_t)j * D + i] = s;
         }
     }
+    for (int32_t i = 0; i < D; i++)
+        for (int32_t j = 0; j <= i; j++) {
+            double v = C[(int64_t)i * D + j] / (double)(n - 1);
+            C[(int64_t)i * D + j] = v;
+            C[(int64_t)j * D + i] = v;
+        }
+    free(dblk);
     free(mu);
 }
 
@@ -340,18 +352,20 @@ void or_rotate_rows(const float *X, int64_t n, int32_t D, int64_t ld, const floa
 {
 #pragma omp parallel
     {
-        float *buf = (float *)malloc(sizeof(float) * (size_t)D); /* the D-float buffer of P:L283 */
+        double *acc = (double *)malloc(sizeof(double) * (size_t)D); /* the D-entry buffer of P:L283 */
 #pragma omp for schedule(static)
         for (int64_t r = 0; r < n; r++) {
             const float *x = X + r * ld;
-            for (int32_t j = 0; j < D; j++) {
-                double s = 0.0;
-                for (int32_t i = 0; i < D; i++) s = fma((double)x[i], (double)R[(int64_t)i * D + j], s);
-                buf[j] = (float)s;
+            for (int32_t j = 0; j < D; j++) acc[j] = 0.0;
+            /* every output j accumulates fma(x_i, R_ij, .) with i ascending */
+            for (int32_t i = 0; i < D; i++) {
+                double xi = (double)x[i];
+                const float *Ri = R + (int64_t)i * D;
+                for (int32_t j = 0; j < D; j++) acc[j] = fma(xi, (double)Ri[j], acc[j]);
             }
-            memcpy(Y + r * ldy, buf, sizeof(float) * (size_t)D);
+            for (int32_t j = 0; j < D; j++) Y[r * ldy + j] = (float)acc[j];
         }
-        free(buf);
+        free(acc);
     }
 }
 

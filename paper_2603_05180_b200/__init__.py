@@ -62,7 +62,7 @@ ABI_SYMBOLS = (
     "crisp_default_params", "crisp_build", "crisp_build_with", "crisp_build_shard", "crisp_local_cell_sizes",
     "crisp_set_global_cell_sizes", "crisp_set_search_params", "crisp_index_info", "crisp_search",
     "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
-    "crisp_set_stage_timing", "crisp_stage_times", "crisp_free", "crisp_last_error", "crisp_version",
+    "crisp_set_stage_timing", "crisp_stage_times", "crisp_search_counters", "crisp_free", "crisp_last_error", "crisp_version",
 )
 
 _lib = None
@@ -93,6 +93,7 @@ def lib():
         L.crisp_export.argtypes = [vp, P(Export)]
         L.crisp_set_stage_timing.argtypes = [i32]
         L.crisp_stage_times.argtypes = [vp, i32, i32]
+        L.crisp_search_counters.argtypes = [vp, i32, i32]
         L.crisp_free.argtypes = [vp]
         L.crisp_free.restype = None
         L.crisp_last_error.restype = C.c_char_p
@@ -280,3 +281,11 @@ def stage_times(reset: bool = True) -> dict:
     a = np.zeros(8, np.float64)
     _check(lib().crisp_stage_times(_ptr(a), 8, 1 if reset else 0))
     return {STAGES[i]: float(a[i]) for i in range(len(STAGES))}
+
+
+def search_counters(reset: bool = True) -> dict:
+    """Work counters of the searches run with stage timing on (crisp_search_counters)."""
+    a = np.zeros(5, np.int64)
+    _check(lib().crisp_search_counters(_ptr(a), 5, 1 if reset else 0))
+    return dict(ids_streamed=int(a[0]), candidates=int(a[1]), verified=int(a[2]), fallback=int(a[3]),
+                launches=int(a[4]))

@@ -327,25 +327,33 @@ static crisp_status search_impl(const crisp_index *ix, const float *queries, int
             search(ix, queries, Q, k, (int)mode, so, s, tr);
             return CRISP_OK;
         }
-        TmpFree tf;
-        const float *qd = to_device(queries, (size_t)Q * ix->D, tf.v);
-        bool ids_dev = is_device_ptr(out_ids), d_dev = out_d ? is_device_ptr(out_d) : true;
-        int64_t *oi = out_ids;
-        float *od = out_d;
-        if (!ids_dev) {
-            CRISP_CUDA(cudaMalloc((void **)&oi, (size_t)Q * k * 8));
-            tf.v.push_back(oi);
-        }
-        if (out_d && !d_dev) {
-            CRISP_CUDA(cudaMalloc((void **)&od, (size_t)Q * k * 4));
-            tf.v.push_back(od);
-        }
+        // host buffers: stream-ordered device staging (H2D in, D2H out)
         cudaStream_t st;
         CRISP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         struct SG {
             cudaStream_t s;
-            ~SG() { cudaStreamDestroy(s); }
-        } sg{st};
+            std::vector<void *> v;
+            ~SG() {
+                for (void *p : v) cudaFreeAsync(p, s);
+                cudaStreamSynchronize(s);
+                cudaStreamDestroy(s);
+            }
+        } sg{st, {}};
+        auto stage = [&](size_t bytes) {
+            void *p = nullptr;
+            CRISP_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), st));
+            sg.v.push_back(p);
+            return p;
+        };
+        const float *qd = queries;
+        if (!is_device_ptr(queries)) {
+            float *t = (float *)stage((size_t)Q * ix->D * 4);
+            CRISP_CUDA(cudaMemcpyAsync(t, queries, (size_t)Q * ix->D * 4, cudaMemcpyHostToDevice, st));
+            qd = t;
+        }
+        bool ids_dev = is_device_ptr(out_ids), d_dev = out_d ? is_device_ptr(out_d) : true;
+        int64_t *oi = ids_dev ? out_ids : (int64_t *)stage((size_t)Q * k * 8);
+        float *od = (out_d && !d_dev) ? (float *)stage((size_t)Q * k * 4) : out_d;
         SearchOut so{oi, od, out_d64};
         search(ix, qd, Q, k, (int)mode, so, st, tr);
         if (!ids_dev) CRISP_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)Q * k * 8, cudaMemcpyDeviceToHost, st));

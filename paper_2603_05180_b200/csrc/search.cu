@@ -863,6 +863,37 @@ __global__ void __launch_bounds__(THREADS) k_rerank_patience(
 }
 
 // ---------------------------------------------------------------------------
+// per-query work counters for the roofline (only when stage timing is on):
+// [0] ids streamed by the count (local slice lengths summed over activated
+// cells), [1] sum |C_q|, [2] rows verified, [3] fallback queries
+// ---------------------------------------------------------------------------
+__device__ unsigned long long d_stats[4];
+
+__global__ void k_stats(const uint32_t *__restrict__ act, const int32_t *__restrict__ act_len, int M, int KK,
+                        const int32_t *__restrict__ off2, int NB, const int32_t *__restrict__ ncand,
+                        const int64_t *__restrict__ nver, const int32_t *__restrict__ fb, int64_t Qc) {
+    const int64_t q = blockIdx.x;
+    unsigned long long ids = 0;
+    for (int m = 0; m < M; m++) {
+        const int L = act_len[q * M + m];
+        for (int r = threadIdx.x; r < L; r += blockDim.x) {
+            int c = (int)(act[(q * M + m) * (int64_t)KK + r] & 0xffffu);
+            const int32_t *o = off2 + ((int64_t)m * KK + c) * (NB + 1);
+            ids += (unsigned long long)(o[NB] - o[0]);
+        }
+    }
+    for (int off = 16; off; off >>= 1) ids += __shfl_xor_sync(0xffffffffu, ids, off);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&d_stats[0], ids);
+    if (threadIdx.x == 0) {
+        unsigned long long c = 0;
+        for (int b = 0; b < NB; b++) c += (unsigned long long)ncand[q * NB + b];
+        atomicAdd(&d_stats[1], c);
+        atomicAdd(&d_stats[2], nver ? (unsigned long long)nver[q] : c);
+        atomicAdd(&d_stats[3], (unsigned long long)fb[q]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------
 struct StageEv {
@@ -872,6 +903,7 @@ struct StageEv {
 static thread_local std::vector<StageEv> g_events;
 static thread_local double g_stage_ms[8];
 static bool g_timing = false;
+static thread_local int64_t g_launches = 0;  // kernels of this library launched by searches on this thread
 
 bool stage_timing_on() { return g_timing; }
 
@@ -981,7 +1013,11 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
             StageScope st(s, 0);
             k_prep_queries<<<nblk(qn * pitch, 256), 256, 0, s>>>(queries + q0 * ix->D, qn, ix->D, pitch, qpad);
             CRISP_LAUNCH();
-            if (ix->rotated) rotate_rows_f64(qpad, qn, ix->Dp, pitch, ix->R, qrot, pitch, s);
+            g_launches++;
+            if (ix->rotated) {
+                rotate_rows_f64(qpad, qn, ix->Dp, pitch, ix->R, qrot, pitch, s);
+                g_launches++;
+            }
         }
         {
             StageScope st(s, 1);
@@ -989,6 +1025,7 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
             k_probe<<<g, THREADS, probe_smem, s>>>(qrot, pitch, qn, ix->cb, M, K, ix->dh, ix->gsize, probe_gs,
                                                    ix->budget, wk, act, act_len, retr);
             CRISP_LAUNCH();
+            g_launches++;
         }
         {
             StageScope st(s, 2);
@@ -1000,12 +1037,14 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
                 k_count_select<false><<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N,
                                                                      BS, ix->tau, pool, PS, ncand, traceV);
             CRISP_LAUNCH();
+            g_launches++;
         }
         {
             StageScope st(s, 3);
             k_fallback<<<(unsigned)qn, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, k,
                                                                  pool, PS, ncand, fb);
             CRISP_LAUNCH();
+            g_launches++;
         }
         if (tr && (tr->cand || tr->cand_n || (tr->order && mode == 0) || (tr->n_verified && mode == 0))) {
             h_pool.resize((size_t)qn * PS);
@@ -1038,11 +1077,13 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
                 k_rerank_exact<<<g, THREADS, rx_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, PS, BS, ncand, NB,
                                                           k, part_d, part_i);
                 CRISP_LAUNCH();
+            g_launches++;
             }
             {
                 StageScope st(s, 5);
                 k_merge_lists<<<(unsigned)qn, THREADS, 0, s>>>(part_d, part_i, S, qn, k, 0, od64, od, oi);
                 CRISP_LAUNCH();
+            g_launches++;
             }
         } else {
             StageScope st(s, 4);
@@ -1050,6 +1091,13 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
                                                                      ix->codes, ix->W, pool, PS, BS, ncand, NB, cbuf,
                                                                      hbuf, N, k, P, od64, od, oi, nver);
             CRISP_LAUNCH();
+            g_launches++;
+        }
+        if (g_timing) {
+            k_stats<<<(unsigned)qn, 128, 0, s>>>(act, act_len, M, KK, ix->off2, NB, ncand, mode == 1 ? nver : nullptr,
+                                                 fb, qn);
+            CRISP_LAUNCH();
+            g_launches++;
         }
         if (tr) {
             std::vector<int32_t> hl((size_t)qn * M);
@@ -1112,6 +1160,7 @@ void merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32
     if (Q <= 0) return;
     k_merge_lists<<<(unsigned)Q, THREADS, 0, s>>>(d, ids, G, Q, k, 1, out_d64, out_d, out_ids);
     CRISP_LAUNCH();
+    g_launches++;
 }
 
 void stage_record(int, cudaEvent_t, cudaEvent_t) {}
@@ -1121,6 +1170,22 @@ void stage_record(int, cudaEvent_t, cudaEvent_t) {}
 // stage timing ABI
 extern "C" crisp_status crisp_set_stage_timing(int32_t on) {
     crisp::g_timing = on != 0;
+    return CRISP_OK;
+}
+
+extern "C" crisp_status crisp_search_counters(int64_t *out, int32_t n, int32_t reset) {
+    unsigned long long h[4];
+    if (cudaMemcpyFromSymbol(h, crisp::d_stats, sizeof(h)) != cudaSuccess) {
+        crisp::set_error("cudaMemcpyFromSymbol failed");
+        return CRISP_ECUDA;
+    }
+    for (int i = 0; i < 4 && i < n; i++) out[i] = (int64_t)h[i];
+    if (n > 4) out[4] = crisp::g_launches;
+    if (reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(crisp::d_stats, z, sizeof(z));
+        crisp::g_launches = 0;
+    }
     return CRISP_OK;
 }
 

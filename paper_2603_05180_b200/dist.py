@@ -1,0 +1,115 @@
+"""Point-sharded multi-GPU search: one process per GPU.
+
+Collective call sites:
+  N1/N2  broadcast of R and the codebooks from rank 0 (shared by every shard)
+  N3     all-reduce (sum) of the local cell sizes -> global sizes, so every
+         shard's budget walk activates exactly the cells a single index would
+  N7     all-gather of the per-shard top-k (dist64, gid), then the a6 merge
+         kernel (crisp_merge_topk) by (d, gid)
+
+The orchestration is written against a small engine interface so the same
+code runs with the CUDA engine (NCCL over NVLink) and, in the CPU tests, with
+a test-supplied engine over gloo.  torch.distributed is plumbing only.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+class CudaEngine:
+    """Engine over libcrisp.so for one rank (device tensors)."""
+
+    def __init__(self, crisp, device):
+        self.crisp = crisp
+        self.device = device
+        self.index = None
+
+    def build_global(self, X, M, **params):
+        """Full build on this rank (rank 0): the shared (R or None, codebooks)
+        come from the global CEV sample and the global k-means sample."""
+        ix = self.crisp.Index.build(X, M, **params)
+        e = ix.export()
+        ix.free()
+        R = torch.from_numpy(e["R"]) if e["R"] is not None else None
+        return R, torch.from_numpy(e["codebooks"])
+
+    def build_shard(self, X_shard, gid_base, M, R, codebooks, **params):
+        R = R.cpu().numpy() if R is not None else None
+        self.index = self.crisp.Index.build(X_shard, M, R=R, codebooks=codebooks.cpu().numpy(), gid_base=gid_base,
+                                            **params)
+
+    def local_cell_sizes(self):
+        return torch.from_numpy(self.index.local_cell_sizes())
+
+    def set_global_cell_sizes(self, sizes):
+        self.index.set_global_cell_sizes(sizes.cpu().numpy())
+
+    def set_search_params(self, **kw):
+        self.index.set_search_params(**kw)
+
+    def search_shard(self, q_dev, k, mode, stream=0):
+        Q = q_dev.shape[0]
+        ids = torch.empty((Q, k), dtype=torch.int64, device=q_dev.device)
+        d64 = torch.empty((Q, k), dtype=torch.float64, device=q_dev.device)
+        self.index.search_shard_async(q_dev, k, mode, ids, d64, stream)
+        return ids, d64
+
+    def merge(self, d64_all, ids_all, stream=0):
+        G, Q, k = d64_all.shape
+        od64 = torch.empty((Q, k), dtype=torch.float64, device=d64_all.device)
+        od = torch.empty((Q, k), dtype=torch.float32, device=d64_all.device)
+        oi = torch.empty((Q, k), dtype=torch.int64, device=d64_all.device)
+        self.crisp.merge_topk(d64_all, ids_all, od64, od, oi, stream)
+        return oi, od
+
+
+def shard_range(N: int, rank: int, world: int):
+    """Contiguous global id ranges [g*N/G, (g+1)*N/G)."""
+    lo = (N * rank) // world
+    hi = (N * (rank + 1)) // world
+    return lo, hi
+
+
+def share_model(R, codebooks, like, src=0):
+    """N1/N2: broadcast R (or 'no rotation') and the codebooks from rank src."""
+    flag = torch.tensor([1 if R is not None else 0], dtype=torch.int64, device=like.device)
+    dist.broadcast(flag, src)
+    cb = codebooks.to(like.device) if codebooks is not None else None
+    shape = torch.tensor(list(cb.shape) if cb is not None else [0, 0, 0, 0], dtype=torch.int64, device=like.device)
+    dist.broadcast(shape, src)
+    if cb is None:
+        cb = torch.empty(tuple(shape.tolist()), dtype=torch.float32, device=like.device)
+    dist.broadcast(cb, src)
+    Rt = None
+    if int(flag.item()):
+        Dp = int(shape[0] * 2 * shape[3])  # padded_D = M * 2 * dh
+        Rt = R.to(like.device) if R is not None else torch.empty((Dp, Dp), dtype=torch.float32, device=like.device)
+        dist.broadcast(Rt, src)
+    return Rt, cb
+
+
+def global_cell_sizes(engine):
+    """N3: sum of the local cell-size tables."""
+    s = engine.local_cell_sizes()
+    dev = _coll_device()
+    t = s.to(dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    engine.set_global_cell_sizes(t)
+    return t
+
+
+def search_step(engine, q_dev, k, mode, stream=0):
+    """One sharded search of the batch: local a0..a5, then N7 + a6."""
+    ids, d64 = engine.search_shard(q_dev, k, mode, stream)
+    world = dist.get_world_size()
+    gd = [torch.empty_like(d64) for _ in range(world)]
+    gi = [torch.empty_like(ids) for _ in range(world)]
+    dist.all_gather(gd, d64)
+    dist.all_gather(gi, ids)
+    return engine.merge(torch.stack(gd), torch.stack(gi), stream)
+
+
+def _coll_device():
+    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")

@@ -484,3 +484,19 @@ def test_guaranteed_mode_recall_bound_invariant():
     p_lo = float(np.quantile(pst, 0.25))
     if M * p_lo > tau:
         assert np.mean(hit) >= oracle.hoeffding_bound(M, p_lo, tau) - 0.02
+
+
+def test_rotation_library_qr_matches_plain_householder():
+    """oracle.rotation uses LAPACK's QR as a library step; the plain C
+    Householder (pinned above) gives the same sign-fixed Q."""
+    G = oracle.gaussian_matrix(48, 5)
+    Qh, _ = oracle.qr(G)
+    _, R64 = oracle.rotation(48, 5)
+    assert np.abs(Qh - R64).max() < 1e-12
+
+
+def test_jacobi_matches_lapack_eigvalsh():
+    r = rng(30)
+    A = r.standard_normal((40, 40))
+    A = A @ A.T
+    assert np.allclose(np.sort(oracle.eig_sym(A)), np.linalg.eigvalsh(A), rtol=1e-10, atol=1e-9)
