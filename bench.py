@@ -107,12 +107,14 @@ def hbm_peak():
 
 
 def load_op(cfg: int, mode_override=None):
+    """{M, seed, modes: {mode: {beta, alpha}}} restricted to --mode if given."""
     with open(OPS) as f:
         ops = json.load(f)
     op = dict(ops[str(cfg)])
+    modes = {int(m): v for m, v in op["modes"].items()}
     if mode_override is not None:
-        op["mode"] = mode_override
-        op.update(op.get("per_mode", {}).get(str(mode_override), {}))
+        modes = {mode_override: modes.get(mode_override, next(iter(modes.values())))}
+    op["modes"] = modes
     return op
 
 
@@ -173,6 +175,8 @@ def run_reference(args):
     c = synth.CONFIGS[cfg]
     N, Q, k = args.N or c["N"], args.Q or c["Q"], c["k"]
     op = load_op(cfg, args.mode)
+    mode0 = sorted(op["modes"])[-1] if args.mode is None else args.mode
+    op.update(op["modes"][mode0], mode=mode0)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     w = synth.Workload(cfg, device=dev)
     X = w.base(N)
@@ -233,7 +237,7 @@ def run_crisp(args):
     c = synth.CONFIGS[cfg]
     N, Q, k, D = args.N or c["N"], args.Q or c["Q"], c["k"], c["D"]
     op = load_op(cfg, args.mode)
-    M, beta, alpha, mode = op["M"], op["beta"], op["alpha"], op["mode"]
+    M = op["M"]
     w = synth.Workload(cfg, device=dev)
     t0 = time.time()
     Qd = w.queries(Q)
@@ -243,7 +247,6 @@ def run_crisp(args):
     t0 = time.time()
     if world == 1:
         index = crisp.Index.build(X, M, **bparams)
-        index.set_search_params(beta=beta, alpha=alpha, patience_factor=op.get("patience_factor", 40))
         engine = None
     else:
         engine = cdist.CudaEngine(crisp, dev)
@@ -254,138 +257,160 @@ def run_crisp(args):
         engine.build_shard(Xs, lo, M, R, cb, **bparams)
         del Xs
         cdist.global_cell_sizes(engine)
-        engine.set_search_params(beta=beta, alpha=alpha, patience_factor=op.get("patience_factor", 40))
         index = engine.index
     torch.cuda.synchronize()
     build_s = time.time() - t0
-    info = index.info()
     gt = ground_truth(X, Qd, k) if rank == 0 else None
     stream = torch.cuda.current_stream().cuda_stream
     ids = torch.empty((Q, k), dtype=torch.int64, device=dev)
     dd = torch.empty((Q, k), dtype=torch.float32, device=dev)
-
-    def step():
-        if world == 1:
-            index.search_async(Qd, k, mode, ids, dd, stream)
-            return ids
-        oi, _ = cdist.search_step(engine, Qd, k, mode, stream)
-        return oi
-
-    for _ in range(args.warmup):
-        out = step()
-    torch.cuda.synchronize()
-    crisp.stage_times(reset=True)
-    crisp.search_counters(reset=True)
-    crisp.set_stage_timing(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(args.steps):
-            out = step()
-        e1.record()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-    ms = e0.elapsed_time(e1)
-    st = crisp.stage_times(reset=True)
-    cnt = crisp.search_counters(reset=True)
-    crisp.set_stage_timing(False)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    peak, peak_src = hbm_peak()
     K = args.steps
-    qps = Q * K / (ms / 1e3)
-    rec = recall_at(out, gt, 10) if rank == 0 else None
+    results = {}
+    for mode, mp in sorted(op["modes"].items()):
+        index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
+        info = index.info()
 
-    # ---------------- e2e through the public API with host buffers
+        def step():
+            if world == 1:
+                index.search_async(Qd, k, mode, ids, dd, stream)
+                return ids
+            oi, _ = cdist.search_step(engine, Qd, k, mode, stream)
+            return oi
+
+        for _ in range(args.warmup):
+            out = step()
+        torch.cuda.synchronize()
+        crisp.stage_times(reset=True)
+        crisp.search_counters(reset=True)
+        crisp.set_stage_timing(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with Clocks(local) as clk:
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(K):
+                out = step()
+            e1.record()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+        ms = e0.elapsed_time(e1)
+        st = crisp.stage_times(reset=True)
+        cnt = crisp.search_counters(reset=True)
+        crisp.set_stage_timing(False)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        rec = recall_at(out, gt, 10) if rank == 0 else None
+
+        # roofline of the hot kernels: algorithmic bytes / CUDA-event time per step
+        row_bytes = 4 * info["pitch"]
+        kernels = {}
+        if st["verify"] > 0:
+            vb = cnt["verified"] * row_bytes / K  # 4D per verified row (SURVEY 8(d) B_rerank)
+            kernels["verify"] = {"kernel": "k_rerank_exact" if mode == 0 else "k_rerank_patience",
+                                 "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
+                                 "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
+        if st["count_select"] > 0:
+            cb_ = cnt["ids_streamed"] * 4 / K  # 4 B per id streamed (SURVEY 8(d) B_count)
+            kernels["count"] = {"kernel": "k_count_select", "bytes_per_step": cb_,
+                                "ms_per_step": st["count_select"] / K,
+                                "achieved_gbs": cb_ / (st["count_select"] / K * 1e-3) / 1e9}
+        for kk in kernels.values():
+            kk["frac_of_peak"] = kk["achieved_gbs"] / peak
+        dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"]) if kernels else None
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if dom and os.path.exists(tf):
+            try:
+                with open(tf) as f:
+                    tj = json.load(f)
+                key = f"cfg{cfg}-mode{mode}-{kernels[dom]['kernel']}"
+                if key in tj:
+                    traffic = tj[key]["dram_bytes_per_step"]
+            except Exception:
+                traffic = None
+        roof = None
+        if dom:
+            a = kernels[dom]["achieved_gbs"]
+            roof = {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak, "traffic": traffic,
+                    "kernel": kernels[dom]["kernel"], "peak_source": peak_src}
+        results[mode] = dict(qps=Q * K / (ms / 1e3), ms=ms / K, recall=rec, beta=mp["beta"], alpha=mp["alpha"],
+                             budget_ids=info["budget"], tau=info["tau"], roofline=roof, kernels=kernels,
+                             stage_ms_per_step={k_: v / K for k_, v in st.items()},
+                             counters_per_step={k_: v / K for k_, v in cnt.items()}, launches=cnt["launches"],
+                             clocks=clk.summary())
+        if rank == 0:
+            log(f"mode {mode}: {results[mode]['qps']:.0f} QPS recall@10 {rec:.4f} stages {results[mode]['stage_ms_per_step']}")
+
+    # headline: the fastest mode whose recall@10 >= 0.9
+    ok = [m for m, r in results.items() if r["recall"] is None or r["recall"] >= 0.9]
+    head = max(ok or list(results), key=lambda m: results[m]["qps"])
+    hr = results[head]
+
+    # e2e through the public API with host buffers (H2D queries + D2H results per step)
     e2e = None
     if rank == 0 and world == 1:
+        mp = op["modes"][head]
+        index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
         qh = torch.empty((Q, D), dtype=torch.float32).pin_memory()
         qh.copy_(Qd.cpu())
         qn = qh.numpy()
         ih = torch.empty((Q, k), dtype=torch.int64).pin_memory().numpy()
         dh = torch.empty((Q, k), dtype=torch.float32).pin_memory().numpy()
-        crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, mode, crisp._ptr(ih), crisp._ptr(dh))
+        for _ in range(2):
+            crisp._check(crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, head, crisp._ptr(ih),
+                                                  crisp._ptr(dh)))
         t0 = time.perf_counter()
         for _ in range(K):
-            st_ = crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, mode, crisp._ptr(ih), crisp._ptr(dh))
-            crisp._check(st_)
+            crisp._check(crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, head, crisp._ptr(ih),
+                                                  crisp._ptr(dh)))
         dt = time.perf_counter() - t0
         e2e = {"value": Q * K / dt, "unit": "queries/s", "h2d_bytes_per_step": Q * D * 4,
-               "d2h_bytes_per_step": Q * k * 12, "recall@10": recall_at(ih, gt, 10)}
+               "d2h_bytes_per_step": Q * k * 12, "recall@10": recall_at(ih, gt, 10), "api": "crisp_search (host buffers)"}
 
-    # ---------------- roofline of the dominant kernel (algorithmic bytes / CUDA-event time)
-    peak, peak_src = hbm_peak()
-    row_bytes = 4 * info["pitch"]
-    kernels = {}
-    if st["verify"] > 0:
-        vb = cnt["verified"] * row_bytes / K  # 4D per verified row (SURVEY 8(d) B_rerank)
-        kernels["verify"] = {"kernel": "k_rerank_exact" if mode == 0 else "k_rerank_patience",
-                             "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
-                             "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
-    if st["count_select"] > 0:
-        cb_ = cnt["ids_streamed"] * 4 / K  # 4 B per id streamed (SURVEY 8(d) B_count)
-        kernels["count"] = {"kernel": "k_count_select", "bytes_per_step": cb_, "ms_per_step": st["count_select"] / K,
-                            "achieved_gbs": cb_ / (st["count_select"] / K * 1e-3) / 1e9}
-    dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"]) if kernels else None
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if dom and os.path.exists(tf):
-        try:
-            with open(tf) as f:
-                tj = json.load(f)
-            key = f"cfg{cfg}-mode{mode}-{kernels[dom]['kernel']}"
-            if key in tj:
-                traffic = tj[key]["dram_bytes_per_step"]
-        except Exception:
-            traffic = None
-    roof = None
-    if dom:
-        a = kernels[dom]["achieved_gbs"]
-        roof = {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak, "traffic": traffic,
-                "kernel": kernels[dom]["kernel"], "peak_source": peak_src}
-
-    # ---------------- cpu baseline (rank 0, N=1 only)
+    # cpu baseline (rank 0, N=1 only): the oracle as it stands on the host cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
 
+        opx = dict(op, mode=head, **op["modes"][head])
         Xh, Qh = X.cpu().numpy(), Qd.cpu().numpy()
-        ox, (B, tau), cal = oracle_qps(Xh, Qh, op, k, budget_seconds=args.cpu_seconds)
+        ox, (B, tau), cal = oracle_qps(Xh, Qh, opx, k, budget_seconds=args.cpu_seconds)
         n = cal["n"]
         t0 = time.perf_counter()
-        oracle.search(ox, Qh[:n], k, mode, B, tau, nthreads=cal["cores"])
+        oracle.search(ox, Qh[:n], k, head, B, tau, nthreads=cal["cores"])
         dt = time.perf_counter() - t0
         cpu = {"value": n / dt, "unit": "queries/s", "cores": cal["cores"], "kind": "oracle",
-               "sample": f"first {n} of the {Q} queries, oracle index built on all N={N} (build {cal['build_s']:.0f}s)"}
+               "sample": f"first {n} of the {Q} queries ({['guaranteed', 'optimized'][head]} mode), oracle index "
+                         f"built on all N={N} (build {cal['build_s']:.0f}s, not timed)"}
         del ox
 
-    clocks = clk.summary()
     if rank == 0:
+        info = index.info()
         line = {
-            "metric": "QPS at recall@10>=0.9", "value": qps, "unit": "queries/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
+            "metric": "QPS at recall@10>=0.9", "value": hr["qps"], "unit": "queries/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": hr["ms"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": c["name"], "N": N, "D": D, "Q": Q, "k": k, "M": M, "beta": beta, "alpha": alpha,
-                       "mode": ["guaranteed", "optimized"][mode], "budget_ids": info["budget"], "tau": info["tau"],
-                       "rotated": bool(info["rotated"]), "cev": info["cev"],
+            "config": {"workload": c["name"], "N": N, "D": D, "Q": Q, "k": k, "M": M, "beta": hr["beta"],
+                       "alpha": hr["alpha"], "mode": ["guaranteed", "optimized"][head], "budget_ids": hr["budget_ids"],
+                       "tau": hr["tau"], "rotated": bool(info["rotated"]), "cev": info["cev"],
                        "l2": "inputs larger than L2 (X = %.2f GB >> 126 MB); no flush" % (N * D * 4 / 1e9),
                        "parallelism": f"points sharded x{world}" if world > 1 else "single GPU"},
-            "recall@10": rec,
-            "roofline": roof,
-            "kernels": kernels,
-            "stage_ms_per_step": {k_: v / K for k_, v in st.items()},
-            "counters_per_step": {k_: v / K for k_, v in cnt.items()},
-            "gpu_launches": cnt["launches"],
+            "recall@10": hr["recall"],
+            "roofline": hr["roofline"],
+            "kernels": hr["kernels"],
+            "stage_ms_per_step": hr["stage_ms_per_step"],
+            "counters_per_step": hr["counters_per_step"],
+            "gpu_launches": hr["launches"],
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "clocks": clocks,
+            "clocks": hr["clocks"],
+            "per_mode": {["guaranteed", "optimized"][m]: {k_: v for k_, v in r.items() if k_ != "clocks"}
+                         for m, r in results.items()},
             "build_seconds": build_s,
             "gen_seconds": gen_s,
         }

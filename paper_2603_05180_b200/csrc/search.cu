@@ -30,7 +30,7 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 constexpr int WARPS = 8;
 constexpr int THREADS = WARPS * 32;
 constexpr int CS_CAP = 1024;          // slice-table entries per round (count kernel)
-constexpr int CS_U = 16;              // ids per thread per round
+constexpr int CS_U = 16;              // ids staged per thread per round
 constexpr int CS_TCAP = THREADS * CS_U;  // positions per round
 constexpr int PATIENCE_CH = 64;       // rows verified per patience chunk
 
@@ -146,28 +146,27 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
 
 // ---------------------------------------------------------------------------
 // a3: collision counting of one (query, id block) into smem byte counters.
-// Slices of all activated cells of all subspaces restricted to the block are
-// flattened (table + scan + position->slice fill) and streamed with coalesced,
-// independent loads; updates are packed-byte shared atomics (ATOMIC) or, with
-// per-subspace rounds and barriers, plain read-modify-writes (partition
-// property: an id occurs once per subspace).
+// The slices of all activated cells of all subspaces, restricted to the block,
+// are flattened (table + scan + warp-cooperative position fill), their ids are
+// staged into shared memory with coalesced independent loads (one memory
+// latency per round), then applied subspace by subspace as plain byte
+// read-modify-writes with a barrier between subspaces: inside one subspace an
+// id occurs at most once (the CSR partition property), so no atomics.
 // ---------------------------------------------------------------------------
 struct CountSmem {
-    int32_t gst[CS_CAP];       // global start of the slice in ids[]
+    int32_t gst[CS_CAP];       // global start of the slice in ids[] | (w==2) << 31
     int32_t pre[CS_CAP + 1];   // exclusive prefix of slice lengths
-    unsigned char w[CS_CAP];
-    uint16_t sid[CS_TCAP];     // position -> slice
+    int32_t pos[CS_TCAP];      // per position: ids[] index | w flag, then local id | w flag
     int32_t lpre[MAX_M + 2];   // prefix of act_len over m
     int32_t round_e, round_n, round_T, round_skip;
     typename cub::BlockScan<int, THREADS>::TempStorage scan;
 };
 
-template <bool ATOMIC>
 __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, int b, const uint32_t *__restrict__ act,
                             const int32_t *__restrict__ act_len, int M, int KK, const int32_t *__restrict__ off2,
                             int NB, const int32_t *__restrict__ ids, int64_t N) {
-    const int tid = threadIdx.x;
-    // zero counters
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    unsigned char *cnt8 = (unsigned char *)cnt32;
     for (int i = tid; i < BS / 16; i += THREADS) ((uint4 *)cnt32)[i] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
         int acc = 0;
@@ -180,9 +179,9 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
     __syncthreads();
     const int Etot = S.lpre[M];
     const uint32_t *actq = act + q * (int64_t)M * KK;
+    const uint32_t bbase = (uint32_t)b * (uint32_t)BS;
     int e0 = 0, skip = 0;
     while (e0 < Etot) {
-        // (A) slice table for entries [e0, e0+CAP)  (ATOMIC) or up to the end of e0's subspace
         int mfirst = 0;
         {
             int lo = 0, hi = M;  // largest m with lpre[m] <= e0
@@ -193,25 +192,24 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
             }
             mfirst = lo;
         }
-        int elim = ATOMIC ? Etot : S.lpre[mfirst + 1];
-        int ne = min(CS_CAP, elim - e0);
+        // (A) slice table for entries [e0, e0 + CAP)
+        const int ne = min(CS_CAP, Etot - e0);
         int lens[CS_CAP / THREADS];
 #pragma unroll
         for (int u = 0; u < CS_CAP / THREADS; u++) {
-            int t = tid * (CS_CAP / THREADS) + u;
+            const int t = tid * (CS_CAP / THREADS) + u;
             int len = 0;
             if (t < ne) {
-                int e = e0 + t;
+                const int e = e0 + t;
                 int m = mfirst;
                 while (S.lpre[m + 1] <= e) m++;
-                uint32_t v = actq[(int64_t)m * KK + (e - S.lpre[m])];
-                int c = (int)(v & 0xffffu);
+                const uint32_t v = __ldg(actq + (int64_t)m * KK + (e - S.lpre[m]));
+                const int c = (int)(v & 0xffffu);
                 const int32_t *o = off2 + ((int64_t)m * KK + c) * (NB + 1) + b;
-                int s0 = o[0], s1 = o[1];
+                int s0 = __ldg(o), s1 = __ldg(o + 1);
                 if (t == 0) s0 += skip;
                 len = s1 - s0;
-                S.gst[t] = (int32_t)((int64_t)m * N + s0);
-                S.w[t] = (unsigned char)(v >> 16);
+                S.gst[t] = (int32_t)((int64_t)m * N + s0) | (((v >> 16) == 2u) ? (int32_t)0x80000000 : 0);
             }
             lens[u] = len;
         }
@@ -220,7 +218,7 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
         cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(lens, pres, tot);
 #pragma unroll
         for (int u = 0; u < CS_CAP / THREADS; u++) {
-            int t = tid * (CS_CAP / THREADS) + u;
+            const int t = tid * (CS_CAP / THREADS) + u;
             if (t < ne) S.pre[t] = pres[u];
         }
         if (tid == 0) S.pre[ne] = tot;
@@ -233,7 +231,7 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
                 if (S.pre[mid] <= CS_TCAP) lo = mid;
                 else hi = mid - 1;
             }
-            if (lo == 0) {  // first slice alone exceeds a round: take a TCAP piece of it
+            if (lo == 0) {  // the first slice alone exceeds a round: take a TCAP piece of it
                 S.round_n = 1;
                 S.round_T = CS_TCAP;
                 S.round_skip = skip + CS_TCAP;
@@ -247,46 +245,52 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
         }
         __syncthreads();
         const int rn = S.round_n, T = S.round_T;
-        // (C) position -> slice fill
-        for (int t = tid; t < rn; t += THREADS) {
-            int p0 = S.pre[t], p1 = min(S.pre[t + 1], T);
-            for (int p = p0; p < p1; p++) S.sid[p] = (uint16_t)t;
+        // (C) warp-cooperative fill: position -> ids[] index (| w flag)
+        for (int t = warp; t < rn; t += WARPS) {
+            const int p0 = S.pre[t], p1 = min(S.pre[t + 1], T);
+            const int g = S.gst[t];
+            for (int p = p0 + lane; p < p1; p += 32) S.pos[p] = g + (p - p0);
         }
         __syncthreads();
-        // (D) coalesced independent loads, then the counter updates
-        const uint32_t bbase = (uint32_t)b * (uint32_t)BS;
-        int idv[CS_U];
-        unsigned char wv[CS_U];
+        // (D) stage the ids: independent coalesced loads, one latency per round
+        {
+            int v[CS_U], idv[CS_U];
 #pragma unroll
-        for (int u = 0; u < CS_U; u++) {
-            int p = tid + u * THREADS;
-            idv[u] = -1;
-            wv[u] = 0;
-            if (p < T) {
-                int t = S.sid[p];
-                idv[u] = __ldg(ids + S.gst[t] + (p - S.pre[t]));
-                wv[u] = S.w[t];
+            for (int u = 0; u < CS_U; u++) {
+                const int p = tid + u * THREADS;
+                v[u] = p < T ? S.pos[p] : 0;
             }
-        }
 #pragma unroll
-        for (int u = 0; u < CS_U; u++) {
-            if (idv[u] >= 0) {
-                uint32_t local = (uint32_t)idv[u] - bbase;
-                if (ATOMIC) {
-                    atomicAdd(&cnt32[local >> 2], (uint32_t)wv[u] << ((local & 3) * 8));
-                } else {
-                    unsigned char *cb8 = (unsigned char *)cnt32;
-                    cb8[local] = (unsigned char)(cb8[local] + wv[u]);
-                }
+            for (int u = 0; u < CS_U; u++) {
+                const int p = tid + u * THREADS;
+                idv[u] = p < T ? __ldg(ids + (v[u] & 0x7fffffff)) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < CS_U; u++) {
+                const int p = tid + u * THREADS;
+                if (p < T) S.pos[p] = (int32_t)(((uint32_t)idv[u] - bbase) | ((uint32_t)v[u] & 0x80000000u));
             }
         }
         __syncthreads();
+        // (E) subspace by subspace, plain byte RMW, barrier between subspaces
+        const int elast = e0 + rn - 1;
+        int mlast = mfirst;
+        while (S.lpre[mlast + 1] <= elast) mlast++;
+        for (int m = mfirst; m <= mlast; m++) {
+            const int ps = (m == mfirst) ? 0 : S.pre[S.lpre[m] - e0];
+            const int pe = (m == mlast) ? T : S.pre[S.lpre[m + 1] - e0];
+            for (int p = ps + tid; p < pe; p += THREADS) {
+                const uint32_t x = (uint32_t)S.pos[p];
+                const uint32_t local = x & 0x7fffffffu;
+                cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
+            }
+            __syncthreads();
+        }
         e0 = S.round_e;
         skip = S.round_skip;
     }
 }
 
-template <bool ATOMIC>
 __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__restrict__ act,
                                                            const int32_t *__restrict__ act_len, int M, int KK,
                                                            const int32_t *__restrict__ off2, int NB,
@@ -298,7 +302,7 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
     CountSmem &S = *(CountSmem *)(smraw + BS);
     const int b = blockIdx.x;
     const int64_t q = blockIdx.y;
-    count_block<ATOMIC>(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+    count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
     // a4: C = {x : V[x] >= tau}, ascending id (Alg. 1 l.18)
     const unsigned char *c8 = (const unsigned char *)cnt32;
     int32_t *outp = pool + q * PS + (int64_t)b * BS;
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
     const unsigned char *c8 = (const unsigned char *)cnt32;
     // pass 1: histogram of V over the touched set
     for (int b = 0; b < NB; b++) {
-        count_block<true>(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+        count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
         for (int j = tid; j < BS; j += THREADS)
             if (c8[j]) atomicAdd(&hist[c8[j]], 1);
         __syncthreads();
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
     int32_t *outp = pool + q * PS;
     // pass 2: ids with V > V*, and the first `quota` ids with V == V*, ascending
     for (int b = 0; b < NB; b++) {
-        count_block<true>(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+        count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
         for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
             int j = j0 + tid * 16;
             unsigned char vb[16];
@@ -949,7 +953,6 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
             cudaStream_t s, const crisp_trace_t *tr) {
     const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch;
     const int64_t N = ix->N, PS = (int64_t)NB * BS;
-    const bool atomic_count = env_int("CRISP_COUNT_ATOMIC", 1) != 0;
     // per-query workspace bytes -> query chunk
     int64_t perq = (int64_t)pitch * 4 * 2 + (int64_t)M * KK * 4 + (int64_t)M * 12 + PS * 4 + (int64_t)NB * 4 + 64;
     const int S = (mode == 0) ? std::max(1, env_int("CRISP_RERANK_SPLITS", 8)) : 1;
@@ -993,8 +996,7 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
     static bool attr_done = false;
     if (!attr_done) {
         CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_count_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_count_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CRISP_CUDA(cudaFuncSetAttribute(k_rerank_patience, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1030,12 +1032,8 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
         {
             StageScope st(s, 2);
             dim3 g(NB, (unsigned)qn);
-            if (atomic_count)
-                k_count_select<true><<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS,
-                                                                    ix->tau, pool, PS, ncand, traceV);
-            else
-                k_count_select<false><<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N,
-                                                                     BS, ix->tau, pool, PS, ncand, traceV);
+            k_count_select<<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, ix->tau,
+                                                          pool, PS, ncand, traceV);
             CRISP_LAUNCH();
             g_launches++;
         }
