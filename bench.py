@@ -311,9 +311,13 @@ def run_crisp(args):
         kernels = {}
         if st["verify"] > 0:
             vb = cnt["verified"] * row_bytes / K  # 4D per verified row (SURVEY 8(d) B_rerank)
-            kernels["verify"] = {"kernel": "k_rerank_exact" if mode == 0 else "k_rerank_patience",
+            kernels["verify"] = {"kernel": "k_rerank_exact" if mode == 0 else "k_verify_rows+k_patience_scan",
                                  "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
                                  "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
+        if st.get("hamming", 0) > 0:
+            hb = cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K  # SURVEY 8(d) B_ham
+            kernels["hamming"] = {"kernel": "k_hamming+k_hsort", "bytes_per_step": hb,
+                                  "ms_per_step": st["hamming"] / K, "achieved_gbs": hb / (st["hamming"] / K * 1e-3) / 1e9}
         if st["count_select"] > 0:
             cb_ = cnt["ids_streamed"] * 4 / K  # 4 B per id streamed (SURVEY 8(d) B_count)
             kernels["count"] = {"kernel": "k_count_select", "bytes_per_step": cb_,

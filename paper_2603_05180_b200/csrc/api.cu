@@ -48,11 +48,15 @@ static void apply_knobs(crisp_index *ix, double beta, int64_t budget, double alp
     ix->patience_factor = pf;
 }
 
+// ids per on-chip counter block: a power of two in [4096, 32768] (the count
+// kernel gives each of its 8 warps BS/8 counters)
 static int block_ids_for(int64_t N) {
-    int bs = 32768;
-    if (const char *v = getenv("CRISP_BLOCK_IDS")) bs = std::max(4096, (atoi(v) / 4096) * 4096);
-    int64_t need = ((N + 4095) / 4096) * 4096;
-    return (int)std::min<int64_t>(bs, std::max<int64_t>(4096, need));
+    int cap = 32768;
+    if (const char *v = getenv("CRISP_BLOCK_IDS")) cap = std::max(4096, std::min(65536, atoi(v)));
+    int bs = 4096;
+    while (bs < cap && bs < N) bs <<= 1;
+    while (bs > cap) bs >>= 1;
+    return std::max(4096, bs);
 }
 
 template <class T>

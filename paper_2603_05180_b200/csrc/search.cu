@@ -167,14 +167,27 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
                             int NB, const int32_t *__restrict__ ids, int64_t N) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     unsigned char *cnt8 = (unsigned char *)cnt32;
-    for (int i = tid; i < BS / 16; i += THREADS) ((uint4 *)cnt32)[i] = make_uint4(0, 0, 0, 0);
-    if (tid == 0) {
+    // every warp owns counters [warp*BS/8, (warp+1)*BS/8): it zeroes, updates
+    // and scans only those, so no inter-warp hazards exist on the counters
+    const int wshift = 31 - __clz(BS) - 3;
+    {
+        uint4 *mine = (uint4 *)(cnt8 + (warp << wshift));
+        for (int i = lane; i < (BS >> 3) / 16; i += 32) mine[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (warp == 0) {
         int acc = 0;
-        S.lpre[0] = 0;
-        for (int m = 0; m < M; m++) {
-            acc += act_len[q * M + m];
-            S.lpre[m + 1] = acc;
+        for (int m0 = 0; m0 < M; m0 += 32) {
+            const int m = m0 + lane;
+            int v = m < M ? __ldg(act_len + q * M + m) : 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += t;
+            }
+            if (m < M) S.lpre[m + 1] = acc + v;
+            acc += __shfl_sync(0xffffffffu, v, 31);
         }
+        if (lane == 0) S.lpre[0] = 0;
     }
     __syncthreads();
     const int Etot = S.lpre[M];
@@ -272,20 +285,22 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
             }
         }
         __syncthreads();
-        // (E) subspace by subspace, plain byte RMW, barrier between subspaces
+        // (E) subspace by subspace, plain byte RMW by the owning warp only: an id
+        // occurs once per subspace, and one warp walks the subspaces in order
         const int elast = e0 + rn - 1;
         int mlast = mfirst;
         while (S.lpre[mlast + 1] <= elast) mlast++;
         for (int m = mfirst; m <= mlast; m++) {
             const int ps = (m == mfirst) ? 0 : S.pre[S.lpre[m] - e0];
             const int pe = (m == mlast) ? T : S.pre[S.lpre[m + 1] - e0];
-            for (int p = ps + tid; p < pe; p += THREADS) {
+            for (int p = ps + lane; p < pe; p += 32) {
                 const uint32_t x = (uint32_t)S.pos[p];
                 const uint32_t local = x & 0x7fffffffu;
-                cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
+                if ((int)(local >> wshift) == warp) cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
             }
-            __syncthreads();
+            __syncwarp();
         }
+        __syncthreads();
         e0 = S.round_e;
         skip = S.round_skip;
     }
@@ -303,35 +318,59 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
     const int b = blockIdx.x;
     const int64_t q = blockIdx.y;
     count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
-    // a4: C = {x : V[x] >= tau}, ascending id (Alg. 1 l.18)
+    // a4: C = {x : V[x] >= tau}, ascending id (Alg. 1 l.18); each warp
+    // compacts its own counter range (count pass, one barrier, write pass)
     const unsigned char *c8 = (const unsigned char *)cnt32;
-    int32_t *outp = pool + q * PS + (int64_t)b * BS;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int span = BS >> 3;
+    const unsigned char *mine = c8 + warp * span;
+    __shared__ int wtot[WARPS];
+    int cw = 0;
+    for (int j = lane * 16; j < span; j += 512) {
+        const uint4 v = *(const uint4 *)(mine + j);
+        const unsigned char *vb = (const unsigned char *)&v;
+#pragma unroll
+        for (int i = 0; i < 16; i++) cw += vb[i] >= tau;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) cw += __shfl_xor_sync(0xffffffffu, cw, off);
+    if (lane == 0) wtot[warp] = cw;
+    __syncthreads();
     int running = 0;
-    const int tid = threadIdx.x;
-    for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
-        int j = j0 + tid * 16;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (j < BS) v = *(const uint4 *)(c8 + j);
+    for (int w2 = 0; w2 < warp; w2++) running += wtot[w2];
+    int32_t *outp = pool + q * PS + (int64_t)b * BS;
+    const int gbase = b * BS + warp * span;
+    for (int j = lane * 16; j < span; j += 512) {
+        const uint4 v = *(const uint4 *)(mine + j);
         const unsigned char *vb = (const unsigned char *)&v;
         int c = 0;
 #pragma unroll
         for (int i = 0; i < 16; i++) c += vb[i] >= tau;
-        int off, tot;
-        cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(c, off, tot);
-        int o = running + off;
+        int inc = c;
 #pragma unroll
-        for (int i = 0; i < 16; i++)
-            if (vb[i] >= tau) outp[o++] = b * BS + j + i;
+        for (int off = 1; off < 32; off <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += t;
+        }
+        int o = running + inc - c;
+        if (c) {
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if (vb[i] >= tau) outp[o++] = gbase + j + i;
+        }
         if (traceV) {
-            int64_t g0 = (int64_t)b * BS + j;
+            const int64_t g0 = (int64_t)gbase + j;
 #pragma unroll
             for (int i = 0; i < 16; i++)
                 if (g0 + i < N) traceV[q * N + g0 + i] = vb[i];
         }
-        running += tot;
-        __syncthreads();
+        running += __shfl_sync(0xffffffffu, inc, 31);
     }
-    if (tid == 0) ncand[q * NB + b] = running;
+    if (tid == 0) {
+        int t = 0;
+        for (int w2 = 0; w2 < WARPS; w2++) t += wtot[w2];
+        ncand[q * NB + b] = t;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -662,141 +701,333 @@ __global__ void __launch_bounds__(THREADS) k_merge_lists(const double *__restric
 }
 
 // ---------------------------------------------------------------------------
-// Optimized Mode: Hamming order + exact L2 with patience.
-// One CTA per query.
+// Optimized Mode (phi=1), stage a4: Hamming order (Z9 ties by id).
+// k_hamming: grid (HS, Qc); CTA s of query q takes a contiguous slice of the
+// ascending-id candidate list, G lanes per candidate read its code words
+// (coalesced), h = popcount(b(q') xor b(x)); per-CTA histogram of h, flushed
+// to a per-query histogram with one atomic per non-empty bin.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(THREADS) k_rerank_patience(
-    const float *__restrict__ qrot, int pitch, int Dp, const float *__restrict__ X, int64_t gid_base,
-    const uint64_t *__restrict__ codes, int Wd, int32_t *__restrict__ pool, int64_t PS, int BS,
-    const int32_t *__restrict__ ncand, int NB, int32_t *__restrict__ cbuf, uint16_t *__restrict__ hbuf, int64_t CS,
-    int k, int P, double *__restrict__ out_d64, float *__restrict__ out_d, int64_t *__restrict__ out_i,
-    int64_t *__restrict__ nver_out) {
+__global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ qrot, int pitch, int Dp,
+                                                      const uint64_t *__restrict__ codes, int Wd,
+                                                      const int32_t *__restrict__ pool, int64_t PS, int BS,
+                                                      const int32_t *__restrict__ ncand, int NB,
+                                                      int32_t *__restrict__ cbuf, uint16_t *__restrict__ hbuf,
+                                                      int64_t CS, int32_t *__restrict__ ghist) {
     extern __shared__ __align__(16) unsigned char sm[];
-    double *qd = (double *)sm;                              // pitch
-    double *chd = qd + pitch;                               // PATIENCE_CH
-    int64_t *chi = (int64_t *)(chd + PATIENCE_CH);           // PATIENCE_CH
-    double *Td = (double *)(chi + PATIENCE_CH);              // k
-    int64_t *Ti = (int64_t *)(Td + k);                       // k
-    uint64_t *qc = (uint64_t *)(Ti + k);                     // Wd
-    int *hist = (int *)(qc + Wd);                            // Dp + 2
-    int *pre = hist + Dp + 2;                                // NB + 1
-    __shared__ int s_stop, s_nver_hi, s_cnt_top, s_pat;
-    __shared__ typename cub::BlockScan<int, THREADS>::TempStorage scan;
-    const int64_t q = blockIdx.x;
+    uint64_t *qc = (uint64_t *)sm;          // Wd
+    int *hist = (int *)(qc + Wd);           // Dp + 1
+    int *pre = hist + Dp + 1;               // NB + 1
+    const int64_t q = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float *qrow = qrot + q * pitch;
-    load_qd(qd, qrow, pitch);
     for (int w = tid; w < Wd; w += THREADS) {
         uint64_t word = 0;
         for (int i = 0; i < 64; i++) {
-            int d = w * 64 + i;
-            if (d < Dp && qrow[d] > 0.0f) word |= (uint64_t)1 << i;
+            const int d = w * 64 + i;
+            if (d < Dp && qrow[d] > 0.0f) word |= (uint64_t)1 << i;  // b(q') with the [x > 0] convention (Z10)
         }
         qc[w] = word;
     }
-    for (int i = tid; i < Dp + 2; i += THREADS) hist[i] = 0;
-    if (tid == 0) {
+    for (int i = tid; i < Dp + 1; i += THREADS) hist[i] = 0;
+    if (warp == 0) {
         int acc = 0;
-        for (int b = 0; b < NB; b++) {
-            pre[b] = acc;
-            acc += ncand[q * NB + b];
+        for (int b0 = 0; b0 < NB; b0 += 32) {
+            const int b = b0 + lane;
+            int v = b < NB ? ncand[q * NB + b] : 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += t;
+            }
+            if (b < NB) pre[b + 1] = acc + v;
+            acc += __shfl_sync(0xffffffffu, v, 31);
         }
-        pre[NB] = acc;
-        s_stop = 0;
-        s_cnt_top = 0;
-        s_pat = 0;
+        if (lane == 0) pre[0] = 0;
     }
     __syncthreads();
     const int total = pre[NB];
-    int32_t *poolq = pool + q * PS;
-    int32_t *cq = cbuf + q * CS;
-    uint16_t *hq = hbuf + q * CS;
-    // (1) Hamming distances, compact ascending-id candidate list, histogram
-    {
-        int G = 1;
-        while (G < Wd && G < 32) G <<= 1;
-        const int per_warp = 32 / G;
-        const int g = lane / G, gl = lane % G;
-        for (int v0 = warp * per_warp; v0 < total; v0 += WARPS * per_warp) {
-            int v = v0 + g;
-            int lid = -1, h = 0;
-            if (v < total) {
-                int lo = 0, hi = NB;  // b with pre[b] <= v < pre[b+1]
+    const int per = (total + gridDim.x - 1) / gridDim.x;
+    const int v_lo = blockIdx.x * per, v_hi = min(total, v_lo + per);
+    int G = 1;
+    while (G < Wd && G < 32) G <<= 1;
+    const int gpw = 32 / G, g = lane / G, gl = lane % G;
+    const int32_t *poolq = pool + q * PS;
+    for (int v0 = v_lo + warp * gpw * 4; v0 < v_hi; v0 += WARPS * gpw * 4) {
+        int lid[4], h[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int v = v0 + u * gpw + g;
+            lid[u] = -1;
+            if (v < v_hi) {
+                int lo = 0, hi = NB;  // block b with pre[b] <= v < pre[b+1]
                 while (hi - lo > 1) {
-                    int mid = (lo + hi) >> 1;
+                    const int mid = (lo + hi) >> 1;
                     if (pre[mid] <= v) lo = mid;
                     else hi = mid;
                 }
-                lid = poolq[(int64_t)lo * BS + (v - pre[lo])];
-                const uint64_t *cr = codes + (int64_t)lid * Wd;
-                for (int w = gl; w < Wd; w += G) h += __popcll(qc[w] ^ __ldg(cr + w));
-            }
-            for (int off = G >> 1; off; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
-            if (v < total && gl == 0) {
-                cq[v] = lid;
-                hq[v] = (uint16_t)h;
-                atomicAdd(&hist[h], 1);
+                lid[u] = __ldg(poolq + (int64_t)lo * BS + (v - pre[lo]));
             }
         }
-    }
-    __syncthreads();
-    // (2) exclusive scan of the histogram -> bin starts
-    {
-        const int nb = Dp + 1;
-        const int per = (nb + THREADS - 1) / THREADS;
-        int loc = 0;
-        for (int i = 0; i < per; i++) {
-            int idx = tid * per + i;
-            if (idx < nb) loc += hist[idx];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            h[u] = 0;
+            if (lid[u] >= 0) {
+                const uint64_t *cr = codes + (int64_t)lid[u] * Wd;
+                for (int w = gl; w < Wd; w += G) h[u] += __popcll(qc[w] ^ __ldg(cr + w));
+            }
         }
-        int off, tot;
-        cub::BlockScan<int, THREADS>(scan).ExclusiveSum(loc, off, tot);
-        __syncthreads();
-        for (int i = 0; i < per; i++) {
-            int idx = tid * per + i;
-            if (idx < nb) {
-                int c = hist[idx];
-                hist[idx] = off;
-                off += c;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            for (int off = G >> 1; off; off >>= 1) h[u] += __shfl_xor_sync(0xffffffffu, h[u], off);
+            const int v = v0 + u * gpw + g;
+            if (lid[u] >= 0 && gl == 0) {
+                cbuf[q * CS + v] = lid[u];
+                hbuf[q * CS + v] = (uint16_t)h[u];
+                atomicAdd(&hist[h[u]], 1);
             }
         }
     }
     __syncthreads();
-    // (3) stable scatter by h (input is ascending id) -> order (h, id) in pool
-    if (warp == 0) {
-        for (int v0 = 0; v0 < total; v0 += 32) {
-            int v = v0 + lane;
-            bool act = v < total;
-            unsigned am = __ballot_sync(0xffffffffu, act);
-            if (act) {
-                int h = hq[v];
-                int lid = cq[v];
-                unsigned peers = __match_any_sync(am, h);
-                int leader = __ffs(peers) - 1;
-                int rank = __popc(peers & ((1u << lane) - 1));
-                int base = 0;
-                if (lane == leader) {
-                    base = hist[h];
-                    hist[h] = base + __popc(peers);
-                }
-                base = __shfl_sync(peers, base, leader);
-                poolq[base + rank] = lid;
-            }
-            __syncwarp();
+    int32_t *gh = ghist + q * (int64_t)(Dp + 1);
+    for (int i = tid; i < Dp + 1; i += THREADS)
+        if (hist[i]) atomicAdd(&gh[i], hist[i]);
+}
+
+// k_hsort: one warp per query; stable counting sort of the ascending-id list by
+// h -> order (h, id), written over the query's pool region.
+__global__ void __launch_bounds__(32) k_hsort(const int32_t *__restrict__ ncand, int NB, int Dp,
+                                              const int32_t *__restrict__ ghist, const int32_t *__restrict__ cbuf,
+                                              const uint16_t *__restrict__ hbuf, int64_t CS,
+                                              int32_t *__restrict__ pool, int64_t PS, int32_t *__restrict__ total_out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    int *start = (int *)sm;  // Dp + 1
+    const int64_t q = blockIdx.x;
+    const int lane = threadIdx.x;
+    const int32_t *gh = ghist + q * (int64_t)(Dp + 1);
+    int acc = 0;
+    for (int b0 = 0; b0 < Dp + 1; b0 += 32) {
+        const int i = b0 + lane;
+        int v = i < Dp + 1 ? gh[i] : 0;
+        int inc = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += t;
         }
+        if (i < Dp + 1) start[i] = acc + inc - v;
+        acc += __shfl_sync(0xffffffffu, inc, 31);
     }
+    const int total = acc;
+    if (lane == 0) total_out[q] = total;
+    __syncwarp();
+    const int32_t *cq = cbuf + q * CS;
+    const uint16_t *hq = hbuf + q * CS;
+    int32_t *out = pool + q * PS;
+    int nh = lane < total ? hq[lane] : 0;
+    int nl = lane < total ? cq[lane] : 0;
+    for (int v0 = 0; v0 < total; v0 += 32) {
+        const int v = v0 + lane;
+        const bool act = v < total;
+        const int h = nh, lid = nl;
+        if (v + 32 < total) {  // prefetch the next chunk
+            nh = hq[v + 32];
+            nl = cq[v + 32];
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        if (act) {
+            const unsigned peers = __match_any_sync(am, h);
+            const int leader = __ffs(peers) - 1;
+            const int rank = __popc(peers & ((1u << lane) - 1));
+            int base = 0;
+            if (lane == leader) {
+                base = start[h];
+                start[h] = base + __popc(peers);
+            }
+            base = __shfl_sync(peers, base, leader);
+            out[base + rank] = lid;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Optimized Mode, stage a5: exact L2 in (h, id) order with patience.
+// Speculative rounds: k_verify_rows computes dist64 of candidates
+// [r*S0, (r+1)*S0) of every unfinished query in parallel (HBM streaming like
+// the Guaranteed-Mode kernel); k_patience_scan then replays them in order per
+// query (warp per query) and stops exactly where the sequential rule stops.
+// Queries still running after the speculative rounds finish in k_patience_tail.
+// ---------------------------------------------------------------------------
+struct PatState {
+    double *Td;       // Qc x k, sorted top-k distances
+    int64_t *Ti;      // Qc x k, their global ids
+    int32_t *cnt;     // Qc, entries in the top-k list
+    int32_t *pat;     // Qc, consecutive non-improving verifications
+    int32_t *done;    // Qc
+    int64_t *nver;    // Qc, rows verified when done
+};
+
+__global__ void __launch_bounds__(THREADS) k_verify_rows(const float *__restrict__ qrot, int pitch,
+                                                          const float *__restrict__ X, const int32_t *__restrict__ pool,
+                                                          int64_t PS, const int32_t *__restrict__ totals,
+                                                          const int32_t *__restrict__ done, int r, int S0,
+                                                          double *__restrict__ dbuf) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    double *qd = (double *)sm;
+    const int64_t q = blockIdx.y;
+    if (done[q]) return;
+    const int total = totals[q];
+    const int j0 = r * S0;
+    const int n = min(S0, total - j0);
+    if (n <= 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    load_qd(qd, qrot + q * pitch, pitch);
     __syncthreads();
-    // (4) verification in (h, id) order with patience
     const int nvec = pitch / 4;
-    int cnt_top = 0;      // warp 0 only
-    int pat = 0;          // consecutive non-improving verifications (warp 0)
+    const int W = gridDim.x * WARPS;
+    const int32_t *ord = pool + q * PS + j0;
+    double *dq = dbuf + q * (int64_t)S0;
+    for (int j = blockIdx.x * WARPS + warp; j < n; j += 2 * W) {
+        const int j1 = j + W;
+        const int l0 = ord[j];
+        if (j1 < n) {
+            double d0, d1;
+            row_dist2(X + (int64_t)l0 * pitch, X + (int64_t)ord[j1] * pitch, qd, nvec, lane, d0, d1);
+            if (lane == 0) {
+                dq[j] = d0;
+                dq[j1] = d1;
+            }
+        } else {
+            const double d0 = row_dist1(X + (int64_t)l0 * pitch, qd, nvec, lane);
+            if (lane == 0) dq[j] = d0;
+        }
+    }
+}
+
+// one warp scans up to 32 (d, id) entries (lanes >= gn invalid) against the
+// top-k list with the patience counter; returns the stop index or -1
+__device__ __forceinline__ int patience_group(double myd, int64_t myi, int gn, double *Td, int64_t *Ti, int &cnt_top,
+                                              int &pat, int k, int P, int lane) {
+    int start = 0;
+    while (start < gn) {
+        const bool full = cnt_top >= k;
+        const double wdv = full ? Td[k - 1] : 0.0;
+        const int64_t wiv = full ? Ti[k - 1] : 0;
+        const bool better = lane >= start && lane < gn && (!full || less_di(myd, myi, wdv, wiv));
+        const unsigned mask = __ballot_sync(0xffffffffu, better);
+        const int f = mask ? (__ffs(mask) - 1) : gn;
+        const int nonimp = f - start;
+        if (P > 0 && pat + nonimp >= P) return start + (P - pat) - 1;  // the P-th consecutive miss
+        pat += nonimp;
+        if (f >= gn) break;
+        const double dd = __shfl_sync(0xffffffffu, myd, f);
+        const int64_t ii = __shfl_sync(0xffffffffu, myi, f);
+        warp_insert(Td, Ti, cnt_top, k, dd, ii, lane);
+        pat = 0;
+        start = f + 1;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ void write_topk(int64_t q, int k, int cnt_top, const double *Td, const int64_t *Ti,
+                                           double *out_d64, float *out_d, int64_t *out_i, int lane, int stride) {
+    for (int r = lane; r < k; r += stride) {
+        const double dv = r < cnt_top ? Td[r] : INFINITY;
+        const int64_t iv = r < cnt_top ? Ti[r] : -1;
+        if (out_d64) out_d64[q * k + r] = dv;
+        if (out_d) out_d[q * k + r] = (float)dv;
+        out_i[q * k + r] = iv;
+    }
+}
+
+// warp per query; dynamic smem WARPS x k (d, id)
+__global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int32_t *__restrict__ totals,
+                                                            const int32_t *__restrict__ pool, int64_t PS,
+                                                            int64_t gid_base, const double *__restrict__ dbuf, int r,
+                                                            int S0, int k, int P, PatState st,
+                                                            double *__restrict__ out_d64, float *__restrict__ out_d,
+                                                            int64_t *__restrict__ out_i) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * WARPS + warp;
+    if (q >= Qc || st.done[q]) return;
+    double *Td = (double *)sm + warp * k;
+    int64_t *Ti = (int64_t *)((double *)sm + WARPS * k) + warp * k;
+    int cnt_top = st.cnt[q], pat = st.pat[q];
+    for (int i = lane; i < cnt_top; i += 32) {
+        Td[i] = st.Td[q * k + i];
+        Ti[i] = st.Ti[q * k + i];
+    }
+    __syncwarp();
+    const int total = totals[q];
+    const int j0 = r * S0;
+    const int n = max(0, min(S0, total - j0));
+    const int32_t *ord = pool + q * PS + j0;
+    const double *dq = dbuf + q * (int64_t)S0;
+    int64_t stop = -1;
+    for (int g0 = 0; g0 < n && stop < 0; g0 += 32) {
+        const int gn = min(32, n - g0);
+        const double myd = lane < gn ? dq[g0 + lane] : INFINITY;
+        const int64_t myi = lane < gn ? gid_base + ord[g0 + lane] : 0x7fffffffffffffffLL;
+        const int s = patience_group(myd, myi, gn, Td, Ti, cnt_top, pat, k, P, lane);
+        if (s >= 0) stop = (int64_t)j0 + g0 + s + 1;
+    }
+    const bool fin = stop >= 0 || j0 + n >= total;
+    for (int i = lane; i < cnt_top; i += 32) {
+        st.Td[q * k + i] = Td[i];
+        st.Ti[q * k + i] = Ti[i];
+    }
+    if (lane == 0) {
+        st.cnt[q] = cnt_top;
+        st.pat[q] = pat;
+        if (fin) {
+            st.done[q] = 1;
+            st.nver[q] = stop >= 0 ? stop : total;
+        }
+    }
+    if (fin) write_topk(q, k, cnt_top, Td, Ti, out_d64, out_d, out_i, lane, 32);
+}
+
+// CTA per query still running after the speculative rounds: chunked
+// sequential verification from position `from`.
+__global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restrict__ qrot, int pitch,
+                                                            const float *__restrict__ X, int64_t gid_base,
+                                                            const int32_t *__restrict__ pool, int64_t PS,
+                                                            const int32_t *__restrict__ totals, int from, int k, int P,
+                                                            PatState st, double *__restrict__ out_d64,
+                                                            float *__restrict__ out_d, int64_t *__restrict__ out_i) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int64_t q = blockIdx.x;
+    if (st.done[q]) return;
+    double *qd = (double *)sm;                       // pitch
+    double *chd = qd + pitch;                        // PATIENCE_CH
+    int64_t *chi = (int64_t *)(chd + PATIENCE_CH);   // PATIENCE_CH
+    double *Td = (double *)(chi + PATIENCE_CH);      // k
+    int64_t *Ti = (int64_t *)(Td + k);               // k
+    __shared__ int s_stop, s_cnt;
+    __shared__ int64_t s_nver;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    load_qd(qd, qrot + q * pitch, pitch);
+    int cnt_top = st.cnt[q], pat = st.pat[q];
+    for (int i = tid; i < cnt_top; i += THREADS) {
+        Td[i] = st.Td[q * k + i];
+        Ti[i] = st.Ti[q * k + i];
+    }
+    if (tid == 0) {
+        s_stop = 0;
+        s_cnt = cnt_top;
+    }
+    __syncthreads();
+    const int total = totals[q];
+    const int32_t *ord = pool + q * PS;
+    const int nvec = pitch / 4;
     int64_t nver = total;
-    for (int pos = 0; pos < total; pos += PATIENCE_CH) {
+    for (int pos = from; pos < total; pos += PATIENCE_CH) {
         const int n = min(PATIENCE_CH, total - pos);
         for (int i = warp * 2; i < n; i += WARPS * 2) {
-            int l0 = poolq[pos + i];
+            const int l0 = ord[pos + i];
             if (i + 1 < n) {
-                int l1 = poolq[pos + i + 1];
+                const int l1 = ord[pos + i + 1];
                 double d0, d1;
                 row_dist2(X + (int64_t)l0 * pitch, X + (int64_t)l1 * pitch, qd, nvec, lane, d0, d1);
                 if (lane == 0) {
@@ -806,7 +1037,7 @@ __global__ void __launch_bounds__(THREADS) k_rerank_patience(
                     chi[i + 1] = gid_base + l1;
                 }
             } else {
-                double d0 = row_dist1(X + (int64_t)l0 * pitch, qd, nvec, lane);
+                const double d0 = row_dist1(X + (int64_t)l0 * pitch, qd, nvec, lane);
                 if (lane == 0) {
                     chd[i] = d0;
                     chi[i] = gid_base + l0;
@@ -815,55 +1046,36 @@ __global__ void __launch_bounds__(THREADS) k_rerank_patience(
         }
         __syncthreads();
         if (warp == 0) {
-            int stop_at = -1;
-            for (int g0 = 0; g0 < n && stop_at < 0; g0 += 32) {
+            int64_t stop = -1;
+            for (int g0 = 0; g0 < n && stop < 0; g0 += 32) {
                 const int gn = min(32, n - g0);
                 const double myd = lane < gn ? chd[g0 + lane] : INFINITY;
                 const int64_t myi = lane < gn ? chi[g0 + lane] : 0x7fffffffffffffffLL;
-                int start = 0;
-                while (start < gn) {
-                    bool full = cnt_top >= k;
-                    double wdv = full ? Td[k - 1] : 0.0;
-                    int64_t wiv = full ? Ti[k - 1] : 0;
-                    bool better = lane >= start && lane < gn && (!full || less_di(myd, myi, wdv, wiv));
-                    unsigned mask = __ballot_sync(0xffffffffu, better);
-                    int f = mask ? (__ffs(mask) - 1) : gn;
-                    int nonimp = f - start;
-                    if (P > 0 && pat + nonimp >= P) {
-                        stop_at = g0 + start + (P - pat) - 1;
-                        break;
-                    }
-                    pat += nonimp;
-                    if (f >= gn) break;
-                    double dd = __shfl_sync(0xffffffffu, myd, f);
-                    int64_t ii = __shfl_sync(0xffffffffu, myi, f);
-                    warp_insert(Td, Ti, cnt_top, k, dd, ii, lane);
-                    pat = 0;
-                    start = f + 1;
+                const int s = patience_group(myd, myi, gn, Td, Ti, cnt_top, pat, k, P, lane);
+                if (s >= 0) stop = (int64_t)pos + g0 + s + 1;
+            }
+            if (lane == 0) {
+                s_cnt = cnt_top;
+                if (stop >= 0) {
+                    s_stop = 1;
+                    s_nver = stop;
                 }
             }
-            if (lane == 0 && stop_at >= 0) {
-                s_stop = 1;
-                s_nver_hi = pos + stop_at + 1;
-            }
-            if (lane == 0) s_cnt_top = cnt_top;
         }
         __syncthreads();
         if (s_stop) {
-            nver = s_nver_hi;
+            nver = s_nver;
             break;
         }
     }
     __syncthreads();
-    const int ct = s_cnt_top;
-    for (int r = tid; r < k; r += THREADS) {
-        double dv = r < ct ? Td[r] : INFINITY;
-        int64_t iv = r < ct ? Ti[r] : -1;
-        if (out_d64) out_d64[q * k + r] = dv;
-        if (out_d) out_d[q * k + r] = (float)dv;
-        out_i[q * k + r] = iv;
+    const int ct = s_cnt;
+    write_topk(q, k, ct, Td, Ti, out_d64, out_d, out_i, tid, THREADS);
+    if (tid == 0) {
+        st.done[q] = 1;
+        st.nver[q] = nver;
+        st.cnt[q] = ct;
     }
-    if (tid == 0 && nver_out) nver_out[q] = nver;
 }
 
 // ---------------------------------------------------------------------------
@@ -905,7 +1117,7 @@ struct StageEv {
     int stage;
 };
 static thread_local std::vector<StageEv> g_events;
-static thread_local double g_stage_ms[8];
+static thread_local double g_stage_ms[8];  // 0 transform 1 probe 2 count 3 fallback 4 verify 5 merge 6 hamming
 static bool g_timing = false;
 static thread_local int64_t g_launches = 0;  // kernels of this library launched by searches on this thread
 
@@ -955,9 +1167,12 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
     const int64_t N = ix->N, PS = (int64_t)NB * BS;
     // per-query workspace bytes -> query chunk
     int64_t perq = (int64_t)pitch * 4 * 2 + (int64_t)M * KK * 4 + (int64_t)M * 12 + PS * 4 + (int64_t)NB * 4 + 64;
-    const int S = (mode == 0) ? std::max(1, env_int("CRISP_RERANK_SPLITS", 8)) : 1;
+    const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));     // CTAs per query in the row kernels
+    const int HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 4));   // CTAs per query in k_hamming
+    const int S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
+    const int R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
     if (mode == 0) perq += (int64_t)S * k * 16;
-    else perq += N * 6;
+    else perq += N * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
     if (tr && tr->V) perq += N;
     int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : (16LL << 30);
     int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
@@ -972,17 +1187,27 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
     int32_t *pool = wb.alloc<int32_t>((size_t)Qc * PS);
     int32_t *ncand = wb.alloc<int32_t>((size_t)Qc * NB);
     int32_t *fb = wb.alloc<int32_t>((size_t)Qc);
-    double *part_d = nullptr;
+    double *part_d = nullptr, *dbuf = nullptr;
     int64_t *part_i = nullptr, *nver = nullptr;
-    int32_t *cbuf = nullptr;
+    int32_t *cbuf = nullptr, *ghist = nullptr, *totals = nullptr;
     uint16_t *hbuf = nullptr;
+    PatState pst{};
     if (mode == 0) {
         part_d = wb.alloc<double>((size_t)Qc * S * k);
         part_i = wb.alloc<int64_t>((size_t)Qc * S * k);
     } else {
         cbuf = wb.alloc<int32_t>((size_t)Qc * N);
         hbuf = wb.alloc<uint16_t>((size_t)Qc * N);
-        nver = wb.alloc<int64_t>((size_t)Qc);
+        ghist = wb.alloc<int32_t>((size_t)Qc * (ix->Dp + 1));
+        totals = wb.alloc<int32_t>((size_t)Qc);
+        dbuf = wb.alloc<double>((size_t)Qc * S0);
+        pst.Td = wb.alloc<double>((size_t)Qc * k);
+        pst.Ti = wb.alloc<int64_t>((size_t)Qc * k);
+        pst.cnt = wb.alloc<int32_t>((size_t)Qc * 3);
+        pst.pat = pst.cnt + Qc;
+        pst.done = pst.pat + Qc;
+        pst.nver = wb.alloc<int64_t>((size_t)Qc);
+        nver = pst.nver;
     }
     uint8_t *traceV = (tr && tr->V) ? wb.alloc<uint8_t>((size_t)Qc * N) : nullptr;
     double *d64tmp = out.d64 ? nullptr : wb.alloc<double>((size_t)Qc * k);
@@ -992,18 +1217,26 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
     const int probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
     const int count_smem = BS + (int)sizeof(CountSmem);
     const int rx_smem = pitch * 8 + WARPS * k * 16 + (NB + 1) * 4;
-    const int pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + ix->W * 8 + (ix->Dp + 2) * 4 + (NB + 1) * 4;
+    const int ham_smem = ix->W * 8 + (ix->Dp + 1) * 4 + (NB + 1) * 4;
+    const int hsort_smem = (ix->Dp + 1) * 4;
+    const int vr_smem = pitch * 8;
+    const int scan_smem = WARPS * k * 16;
+    const int pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16;
     static bool attr_done = false;
     if (!attr_done) {
         CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_rerank_patience, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CRISP_CUDA(cudaFuncSetAttribute(k_patience_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr_done = true;
     }
     CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
-                    pat_smem <= 220 * 1024,
+                    pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
                 "shared-memory footprint too large for this (D, K, k)");
 
     const int wk = (mode == 1) ? k : 0;
@@ -1084,12 +1317,37 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
             g_launches++;
             }
         } else {
-            StageScope st(s, 4);
-            k_rerank_patience<<<(unsigned)qn, THREADS, pat_smem, s>>>(qrot, pitch, ix->Dp, ix->X, ix->gid_base,
-                                                                     ix->codes, ix->W, pool, PS, BS, ncand, NB, cbuf,
-                                                                     hbuf, N, k, P, od64, od, oi, nver);
-            CRISP_LAUNCH();
-            g_launches++;
+            CRISP_CUDA(cudaMemsetAsync(ghist, 0, (size_t)qn * (ix->Dp + 1) * 4, s));
+            CRISP_CUDA(cudaMemsetAsync(pst.cnt, 0, (size_t)Qc * 3 * 4, s));
+            {
+                StageScope st(s, 6);
+                dim3 g(HS, (unsigned)qn);
+                k_hamming<<<g, THREADS, ham_smem, s>>>(qrot, pitch, ix->Dp, ix->codes, ix->W, pool, PS, BS, ncand, NB,
+                                                       cbuf, hbuf, N, ghist);
+                CRISP_LAUNCH();
+                g_launches++;
+                k_hsort<<<(unsigned)qn, 32, hsort_smem, s>>>(ncand, NB, ix->Dp, ghist, cbuf, hbuf, N, pool, PS, totals);
+                CRISP_LAUNCH();
+                g_launches++;
+            }
+            {
+                StageScope st(s, 4);
+                for (int r = 0; r < R0; r++) {
+                    dim3 g(S, (unsigned)qn);
+                    k_verify_rows<<<g, THREADS, vr_smem, s>>>(qrot, pitch, ix->X, pool, PS, totals, pst.done, r, S0,
+                                                              dbuf);
+                    CRISP_LAUNCH();
+                    g_launches++;
+                    k_patience_scan<<<nblk(qn, WARPS), THREADS, scan_smem, s>>>(qn, totals, pool, PS, ix->gid_base, dbuf,
+                                                                                r, S0, k, P, pst, od64, od, oi);
+                    CRISP_LAUNCH();
+                    g_launches++;
+                }
+                k_patience_tail<<<(unsigned)qn, THREADS, pat_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, PS,
+                                                                        totals, R0 * S0, k, P, pst, od64, od, oi);
+                CRISP_LAUNCH();
+                g_launches++;
+            }
         }
         if (g_timing) {
             k_stats<<<(unsigned)qn, 128, 0, s>>>(act, act_len, M, KK, ix->off2, NB, ncand, mode == 1 ? nver : nullptr,
