@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcrisp.so")
 
 GUARANTEED, OPTIMIZED = 0, 1
-STAGES = ("transform", "probe", "count_select", "fallback", "verify", "merge", "hamming")
+STAGES = ("transform", "probe", "count_select", "fallback", "verify", "merge", "hamming", "hsort")
 
 
 class CrispError(RuntimeError):

@@ -164,7 +164,7 @@ struct CountSmem {
 
 __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, int b, const uint32_t *__restrict__ act,
                             const int32_t *__restrict__ act_len, int M, int KK, const int32_t *__restrict__ off2,
-                            int NB, const int32_t *__restrict__ ids, int64_t N) {
+                            int NB, const int32_t *__restrict__ ids, int64_t N, int emode) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     unsigned char *cnt8 = (unsigned char *)cnt32;
     // every warp owns counters [warp*BS/8, (warp+1)*BS/8): it zeroes, updates
@@ -285,20 +285,30 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
             }
         }
         __syncthreads();
-        // (E) subspace by subspace, plain byte RMW by the owning warp only: an id
-        // occurs once per subspace, and one warp walks the subspaces in order
+        // (E) subspace by subspace, plain byte RMW (an id occurs once per
+        // subspace).  emode 0: all threads, barrier between subspaces;
+        // emode 1: only the warp owning the counter, no barriers.
         const int elast = e0 + rn - 1;
         int mlast = mfirst;
         while (S.lpre[mlast + 1] <= elast) mlast++;
         for (int m = mfirst; m <= mlast; m++) {
             const int ps = (m == mfirst) ? 0 : S.pre[S.lpre[m] - e0];
             const int pe = (m == mlast) ? T : S.pre[S.lpre[m + 1] - e0];
-            for (int p = ps + lane; p < pe; p += 32) {
-                const uint32_t x = (uint32_t)S.pos[p];
-                const uint32_t local = x & 0x7fffffffu;
-                if ((int)(local >> wshift) == warp) cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
+            if (emode == 0) {
+                for (int p = ps + tid; p < pe; p += THREADS) {
+                    const uint32_t x = (uint32_t)S.pos[p];
+                    const uint32_t local = x & 0x7fffffffu;
+                    cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
+                }
+                __syncthreads();
+            } else {
+                for (int p = ps + lane; p < pe; p += 32) {
+                    const uint32_t x = (uint32_t)S.pos[p];
+                    const uint32_t local = x & 0x7fffffffu;
+                    if ((int)(local >> wshift) == warp) cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
         __syncthreads();
         e0 = S.round_e;
@@ -311,13 +321,14 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
                                                            const int32_t *__restrict__ off2, int NB,
                                                            const int32_t *__restrict__ ids, int64_t N, int BS, int tau,
                                                            int32_t *__restrict__ pool, int64_t PS,
-                                                           int32_t *__restrict__ ncand, uint8_t *__restrict__ traceV) {
+                                                           int32_t *__restrict__ ncand, uint8_t *__restrict__ traceV,
+                                                           int emode) {
     extern __shared__ __align__(16) unsigned char smraw[];
     uint32_t *cnt32 = (uint32_t *)smraw;
     CountSmem &S = *(CountSmem *)(smraw + BS);
     const int b = blockIdx.x;
     const int64_t q = blockIdx.y;
-    count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+    count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N, emode);
     // a4: C = {x : V[x] >= tau}, ascending id (Alg. 1 l.18); each warp
     // compacts its own counter range (count pass, one barrier, write pass)
     const unsigned char *c8 = (const unsigned char *)cnt32;
@@ -404,7 +415,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
     const unsigned char *c8 = (const unsigned char *)cnt32;
     // pass 1: histogram of V over the touched set
     for (int b = 0; b < NB; b++) {
-        count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+        count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N, 0);
         for (int j = tid; j < BS; j += THREADS)
             if (c8[j]) atomicAdd(&hist[c8[j]], 1);
         __syncthreads();
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
     int32_t *outp = pool + q * PS;
     // pass 2: ids with V > V*, and the first `quota` ids with V == V*, ascending
     for (int b = 0; b < NB; b++) {
-        count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N);
+        count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N, 0);
         for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
             int j = j0 + tid * 16;
             unsigned char vb[16];
@@ -1171,6 +1182,7 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
     const int HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 4));   // CTAs per query in k_hamming
     const int S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
     const int R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
+    const int emode = env_int("CRISP_COUNT_EMODE", 0);
     if (mode == 0) perq += (int64_t)S * k * 16;
     else perq += N * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
     if (tr && tr->V) perq += N;
@@ -1266,7 +1278,7 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
             StageScope st(s, 2);
             dim3 g(NB, (unsigned)qn);
             k_count_select<<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, ix->tau,
-                                                          pool, PS, ncand, traceV);
+                                                          pool, PS, ncand, traceV, emode);
             CRISP_LAUNCH();
             g_launches++;
         }
@@ -1326,6 +1338,9 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
                                                        cbuf, hbuf, N, ghist);
                 CRISP_LAUNCH();
                 g_launches++;
+            }
+            {
+                StageScope st(s, 7);
                 k_hsort<<<(unsigned)qn, 32, hsort_smem, s>>>(ncand, NB, ix->Dp, ghist, cbuf, hbuf, N, pool, PS, totals);
                 CRISP_LAUNCH();
                 g_launches++;

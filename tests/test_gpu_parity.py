@@ -203,3 +203,20 @@ def test_gpu_rotation_properties(crisp):
     assert np.abs(R - ox["R"]).max() < 1e-5
     auto = crisp.Index.build(X, 4, K=8, kmeans_iters=2, seed=4)
     assert auto.info()["rotated"] == (ox["cev"] > 0.85) == 1
+
+
+@pytest.mark.parametrize("batch,rounds", [(64, 1), (64, 0), (128, 3)])
+def test_patience_rounds_and_tail(crisp, monkeypatch, batch, rounds):
+    """Optimized mode through every verification path: speculative rounds of
+    `batch` rows, then the sequential tail kernel; results and the patience stop
+    index must equal the oracle's sequential rule."""
+    monkeypatch.setenv("CRISP_PATIENCE_BATCH", str(batch))
+    monkeypatch.setenv("CRISP_PATIENCE_ROUNDS", str(rounds))
+    X, Qv, ox = make_case(cfg=1, N=12000, D=128, Q=24, M=4, K=9, seed=7)
+    ix = build_gpu(crisp, X, ox, block_ids=4096)
+    for pf, B in ((1, 900), (3, 2500), (0, 700)):
+        ix.set_search_params(budget=B, tau=1, patience_factor=pf)
+        ids, d, t = ix.trace(Qv, 5, 1)
+        r_ids, r_d, ot = oracle.search(ox, Qv, 5, 1, B, 1, patience_factor=pf, trace=True)
+        compare_trace(t, ot, 1, X.shape[0])
+        assert_topk_parity(ids, d, r_ids, r_d, f"patience batch={batch} rounds={rounds} pf={pf}")
