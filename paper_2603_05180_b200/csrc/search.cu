@@ -145,35 +145,44 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
 }
 
 // ---------------------------------------------------------------------------
-// a3: collision counting of one (query, id block) into smem byte counters.
-// The slices of all activated cells of all subspaces, restricted to the block,
-// are flattened (table + scan + warp-cooperative position fill), their ids are
-// staged into shared memory with coalesced independent loads (one memory
-// latency per round), then applied subspace by subspace as plain byte
-// read-modify-writes with a barrier between subspaces: inside one subspace an
-// id occurs at most once (the CSR partition property), so no atomics.
+// a3: collision counting into on-chip byte counters.  A CTA owns one query and a
+// run of BPC consecutive id blocks of BS ids.  The query's activated cells
+// (all subspaces) are cached once in shared memory; for each block their CSR
+// slices restricted to the block are flattened (off2 offsets, prefetched one
+// block ahead), the ids of a window of positions are staged into shared memory
+// with coalesced independent loads (one memory latency per window), and then
+// applied subspace by subspace as plain byte read-modify-writes with a barrier
+// between subspaces: inside one subspace an id occurs at most once (the CSR
+// partition property), so no atomics are needed.
 // ---------------------------------------------------------------------------
+constexpr int CS_EPT = CS_CAP / THREADS;  // table entries per thread
+constexpr uint32_t WFLAG = 0x80000000u;   // weight-2 flag (Alg. 1 l.10-12)
+
 struct CountSmem {
-    int32_t gst[CS_CAP];       // global start of the slice in ids[] | (w==2) << 31
+    uint32_t erow[CS_CAP];     // cached entries: (m*KK + cell) | WFLAG
+    int32_t gst[CS_CAP];       // per block: ids[] index of the slice start | WFLAG
     int32_t pre[CS_CAP + 1];   // exclusive prefix of slice lengths
-    int32_t pos[CS_TCAP];      // per position: ids[] index | w flag, then local id | w flag
+    int32_t pos[CS_TCAP];      // window: ids[] index | WFLAG, then local id | WFLAG
     int32_t lpre[MAX_M + 2];   // prefix of act_len over m
-    int32_t round_e, round_n, round_T, round_skip;
+    int32_t wtot[WARPS];
+    int32_t base;
     typename cub::BlockScan<int, THREADS>::TempStorage scan;
 };
 
-__device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, int b, const uint32_t *__restrict__ act,
-                            const int32_t *__restrict__ act_len, int M, int KK, const int32_t *__restrict__ off2,
-                            int NB, const int32_t *__restrict__ ids, int64_t N, int emode) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    unsigned char *cnt8 = (unsigned char *)cnt32;
-    // every warp owns counters [warp*BS/8, (warp+1)*BS/8): it zeroes, updates
-    // and scans only those, so no inter-warp hazards exist on the counters
-    const int wshift = 31 - __clz(BS) - 3;
-    {
-        uint4 *mine = (uint4 *)(cnt8 + (warp << wshift));
-        for (int i = lane; i < (BS >> 3) / 16; i += 32) mine[i] = make_uint4(0, 0, 0, 0);
+__device__ __forceinline__ int m_of_entry(const int32_t *lpre, int M, int e) {
+    int lo = 0, hi = M;  // largest m with lpre[m] <= e
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (lpre[mid] <= e) lo = mid;
+        else hi = mid;
     }
+    return lo;
+}
+
+// lpre and (if they fit) the cached entries of query q; returns Etot
+__device__ int count_setup(CountSmem &S, int64_t q, const uint32_t *__restrict__ act,
+                           const int32_t *__restrict__ act_len, int M, int KK) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == 0) {
         int acc = 0;
         for (int m0 = 0; m0 < M; m0 += 32) {
@@ -191,211 +200,237 @@ __device__ void count_block(CountSmem &S, uint32_t *cnt32, int BS, int64_t q, in
     }
     __syncthreads();
     const int Etot = S.lpre[M];
-    const uint32_t *actq = act + q * (int64_t)M * KK;
+    if (Etot <= CS_CAP) {
+        const uint32_t *actq = act + q * (int64_t)M * KK;
+        for (int t = tid; t < Etot; t += THREADS) {
+            const int m = m_of_entry(S.lpre, M, t);
+            const uint32_t v = __ldg(actq + (int64_t)m * KK + (t - S.lpre[m]));
+            S.erow[t] = (uint32_t)(m * KK + (int)(v & 0xffffu)) | ((v >> 16) == 2u ? WFLAG : 0u);
+        }
+    }
+    __syncthreads();
+    return Etot;
+}
+
+__device__ __forceinline__ uint32_t entry_of(const CountSmem &S, int e, bool cached, const uint32_t *__restrict__ act,
+                                             int64_t q, int M, int KK) {
+    if (cached) return S.erow[e];
+    const int m = m_of_entry(S.lpre, M, e);
+    const uint32_t v = __ldg(act + q * (int64_t)M * KK + (int64_t)m * KK + (e - S.lpre[m]));
+    return (uint32_t)(m * KK + (int)(v & 0xffffu)) | ((v >> 16) == 2u ? WFLAG : 0u);
+}
+
+// Count block b of query q into the zeroed counters.  s0r/s1r: off2 values of
+// this block for the thread's cached entries (cached case), refilled for nb.
+__device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64_t q, int b, int nb, int Etot,
+                                const uint32_t *__restrict__ act, int M, int KK, const int32_t *__restrict__ off2,
+                                int NB, const int32_t *__restrict__ ids, int64_t N, int (&s0r)[CS_EPT],
+                                int (&s1r)[CS_EPT]) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool cached = Etot <= CS_CAP;
     const uint32_t bbase = (uint32_t)b * (uint32_t)BS;
-    int e0 = 0, skip = 0;
-    while (e0 < Etot) {
-        int mfirst = 0;
-        {
-            int lo = 0, hi = M;  // largest m with lpre[m] <= e0
-            while (hi - lo > 1) {
-                int mid = (lo + hi) >> 1;
-                if (S.lpre[mid] <= e0) lo = mid;
-                else hi = mid;
-            }
-            mfirst = lo;
-        }
-        // (A) slice table for entries [e0, e0 + CAP)
+    for (int e0 = 0; e0 < Etot; e0 += CS_CAP) {
         const int ne = min(CS_CAP, Etot - e0);
-        int lens[CS_CAP / THREADS];
+        int lens[CS_EPT];
 #pragma unroll
-        for (int u = 0; u < CS_CAP / THREADS; u++) {
-            const int t = tid * (CS_CAP / THREADS) + u;
-            int len = 0;
+        for (int u = 0; u < CS_EPT; u++) {
+            const int t = tid * CS_EPT + u;
+            lens[u] = 0;
             if (t < ne) {
-                const int e = e0 + t;
-                int m = mfirst;
-                while (S.lpre[m + 1] <= e) m++;
-                const uint32_t v = __ldg(actq + (int64_t)m * KK + (e - S.lpre[m]));
-                const int c = (int)(v & 0xffffu);
-                const int32_t *o = off2 + ((int64_t)m * KK + c) * (NB + 1) + b;
-                int s0 = __ldg(o), s1 = __ldg(o + 1);
-                if (t == 0) s0 += skip;
-                len = s1 - s0;
-                S.gst[t] = (int32_t)((int64_t)m * N + s0) | (((v >> 16) == 2u) ? (int32_t)0x80000000 : 0);
+                const uint32_t erw = entry_of(S, e0 + t, cached, act, q, M, KK);
+                const int row = (int)(erw & ~WFLAG);
+                int s0, s1;
+                if (cached) {
+                    s0 = s0r[u];
+                    s1 = s1r[u];
+                    if (nb >= 0) {  // prefetch the next block's offsets
+                        const int32_t *o = off2 + (int64_t)row * (NB + 1) + nb;
+                        s0r[u] = __ldg(o);
+                        s1r[u] = __ldg(o + 1);
+                    }
+                } else {
+                    const int32_t *o = off2 + (int64_t)row * (NB + 1) + b;
+                    s0 = __ldg(o);
+                    s1 = __ldg(o + 1);
+                }
+                S.gst[t] = (int32_t)((uint32_t)((int64_t)(row / KK) * N + s0) | (erw & WFLAG));
+                lens[u] = s1 - s0;
             }
-            lens[u] = len;
         }
-        int tot;
-        int pres[CS_CAP / THREADS];
-        cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(lens, pres, tot);
+        int pres[CS_EPT], T;
+        cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(lens, pres, T);
 #pragma unroll
-        for (int u = 0; u < CS_CAP / THREADS; u++) {
-            const int t = tid * (CS_CAP / THREADS) + u;
+        for (int u = 0; u < CS_EPT; u++) {
+            const int t = tid * CS_EPT + u;
             if (t < ne) S.pre[t] = pres[u];
         }
-        if (tid == 0) S.pre[ne] = tot;
+        if (tid == 0) S.pre[ne] = T;
         __syncthreads();
-        // (B) how many whole slices fit in one round
-        if (tid == 0) {
-            int lo = 0, hi = ne;  // largest n with pre[n] <= TCAP
-            while (lo < hi) {
-                int mid = (lo + hi + 1) >> 1;
-                if (S.pre[mid] <= CS_TCAP) lo = mid;
-                else hi = mid - 1;
+        const int ma = m_of_entry(S.lpre, M, e0), mb = m_of_entry(S.lpre, M, e0 + ne - 1);
+        for (int P0 = 0; P0 < T; P0 += CS_TCAP) {
+            const int Wn = min(CS_TCAP, T - P0);
+            // fill the window: position -> ids[] index (| weight flag)
+            for (int t = warp; t < ne; t += WARPS) {
+                const int p0 = S.pre[t];
+                const int a = max(p0, P0), z = min(S.pre[t + 1], P0 + Wn);
+                const int g = S.gst[t];
+                for (int p = a + lane; p < z; p += 32) S.pos[p - P0] = g + (p - p0);
             }
-            if (lo == 0) {  // the first slice alone exceeds a round: take a TCAP piece of it
-                S.round_n = 1;
-                S.round_T = CS_TCAP;
-                S.round_skip = skip + CS_TCAP;
-                S.round_e = e0;
-            } else {
-                S.round_n = lo;
-                S.round_T = S.pre[lo];
-                S.round_skip = 0;
-                S.round_e = e0 + lo;
-            }
-        }
-        __syncthreads();
-        const int rn = S.round_n, T = S.round_T;
-        // (C) warp-cooperative fill: position -> ids[] index (| w flag)
-        for (int t = warp; t < rn; t += WARPS) {
-            const int p0 = S.pre[t], p1 = min(S.pre[t + 1], T);
-            const int g = S.gst[t];
-            for (int p = p0 + lane; p < p1; p += 32) S.pos[p] = g + (p - p0);
-        }
-        __syncthreads();
-        // (D) stage the ids: independent coalesced loads, one latency per round
-        {
-            int v[CS_U], idv[CS_U];
+            __syncthreads();
+            // stage the window's ids: independent coalesced loads
+            {
+                int v[CS_U], idv[CS_U];
 #pragma unroll
-            for (int u = 0; u < CS_U; u++) {
-                const int p = tid + u * THREADS;
-                v[u] = p < T ? S.pos[p] : 0;
-            }
+                for (int u = 0; u < CS_U; u++) {
+                    const int p = tid + u * THREADS;
+                    v[u] = p < Wn ? S.pos[p] : 0;
+                }
 #pragma unroll
-            for (int u = 0; u < CS_U; u++) {
-                const int p = tid + u * THREADS;
-                idv[u] = p < T ? __ldg(ids + (v[u] & 0x7fffffff)) : 0;
-            }
+                for (int u = 0; u < CS_U; u++) {
+                    const int p = tid + u * THREADS;
+                    idv[u] = p < Wn ? __ldg(ids + ((uint32_t)v[u] & ~WFLAG)) : 0;
+                }
 #pragma unroll
-            for (int u = 0; u < CS_U; u++) {
-                const int p = tid + u * THREADS;
-                if (p < T) S.pos[p] = (int32_t)(((uint32_t)idv[u] - bbase) | ((uint32_t)v[u] & 0x80000000u));
+                for (int u = 0; u < CS_U; u++) {
+                    const int p = tid + u * THREADS;
+                    if (p < Wn) S.pos[p] = (int32_t)(((uint32_t)idv[u] - bbase) | ((uint32_t)v[u] & WFLAG));
+                }
             }
-        }
-        __syncthreads();
-        // (E) subspace by subspace, plain byte RMW (an id occurs once per
-        // subspace).  emode 0: all threads, barrier between subspaces;
-        // emode 1: only the warp owning the counter, no barriers.
-        const int elast = e0 + rn - 1;
-        int mlast = mfirst;
-        while (S.lpre[mlast + 1] <= elast) mlast++;
-        for (int m = mfirst; m <= mlast; m++) {
-            const int ps = (m == mfirst) ? 0 : S.pre[S.lpre[m] - e0];
-            const int pe = (m == mlast) ? T : S.pre[S.lpre[m + 1] - e0];
-            if (emode == 0) {
+            __syncthreads();
+            // subspace by subspace: plain byte RMW, barrier between subspaces
+            for (int m = ma; m <= mb; m++) {
+                const int ea = max(S.lpre[m], e0) - e0, eb = min(S.lpre[m + 1], e0 + ne) - e0;
+                const int ps = max(S.pre[ea], P0), pe = min(S.pre[eb], P0 + Wn);
                 for (int p = ps + tid; p < pe; p += THREADS) {
-                    const uint32_t x = (uint32_t)S.pos[p];
-                    const uint32_t local = x & 0x7fffffffu;
+                    const uint32_t x = (uint32_t)S.pos[p - P0];
+                    const uint32_t local = x & ~WFLAG;
                     cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
                 }
                 __syncthreads();
-            } else {
-                for (int p = ps + lane; p < pe; p += 32) {
-                    const uint32_t x = (uint32_t)S.pos[p];
-                    const uint32_t local = x & 0x7fffffffu;
-                    if ((int)(local >> wshift) == warp) cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
-                }
-                __syncwarp();
             }
         }
-        __syncthreads();
-        e0 = S.round_e;
-        skip = S.round_skip;
+        if (T == 0) __syncthreads();
     }
 }
 
+__device__ __forceinline__ void zero_counters(unsigned char *cnt8, int BS) {
+    for (int i = threadIdx.x; i < BS / 16; i += THREADS) ((uint4 *)cnt8)[i] = make_uint4(0, 0, 0, 0);
+}
+
+__device__ __forceinline__ void prefetch_first(const CountSmem &S, int Etot, const int32_t *__restrict__ off2, int NB,
+                                               int b, int (&s0r)[CS_EPT], int (&s1r)[CS_EPT]) {
+    if (Etot > CS_CAP) return;
+#pragma unroll
+    for (int u = 0; u < CS_EPT; u++) {
+        const int t = threadIdx.x * CS_EPT + u;
+        if (t < Etot) {
+            const int32_t *o = off2 + (int64_t)(S.erow[t] & ~WFLAG) * (NB + 1) + b;
+            s0r[u] = __ldg(o);
+            s1r[u] = __ldg(o + 1);
+        }
+    }
+}
+
+// a3 + a4 for BPC blocks of one query; candidates go to the query's pool
+// region at a per-block base taken from an atomic cursor (blocks keep their
+// ascending-id order inside; consumers enumerate blocks in ascending order).
 __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__restrict__ act,
                                                            const int32_t *__restrict__ act_len, int M, int KK,
                                                            const int32_t *__restrict__ off2, int NB,
-                                                           const int32_t *__restrict__ ids, int64_t N, int BS, int tau,
-                                                           int32_t *__restrict__ pool, int64_t PS,
-                                                           int32_t *__restrict__ ncand, uint8_t *__restrict__ traceV,
-                                                           int emode) {
+                                                           const int32_t *__restrict__ ids, int64_t N, int BS, int BPC,
+                                                           int tau, int32_t *__restrict__ pool, int64_t CAPQ,
+                                                           int32_t *__restrict__ cursor, int32_t *__restrict__ cbase,
+                                                           int32_t *__restrict__ ncand, int32_t *__restrict__ need,
+                                                           uint8_t *__restrict__ traceV) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    uint32_t *cnt32 = (uint32_t *)smraw;
+    unsigned char *cnt8 = smraw;
     CountSmem &S = *(CountSmem *)(smraw + BS);
-    const int b = blockIdx.x;
     const int64_t q = blockIdx.y;
-    count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N, emode);
-    // a4: C = {x : V[x] >= tau}, ascending id (Alg. 1 l.18); each warp
-    // compacts its own counter range (count pass, one barrier, write pass)
-    const unsigned char *c8 = (const unsigned char *)cnt32;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int b_lo = blockIdx.x * BPC, b_hi = min(NB, b_lo + BPC);
+    const int Etot = count_setup(S, q, act, act_len, M, KK);
+    int s0r[CS_EPT], s1r[CS_EPT];
+    prefetch_first(S, Etot, off2, NB, b_lo, s0r, s1r);
     const int span = BS >> 3;
-    const unsigned char *mine = c8 + warp * span;
-    __shared__ int wtot[WARPS];
-    int cw = 0;
-    for (int j = lane * 16; j < span; j += 512) {
-        const uint4 v = *(const uint4 *)(mine + j);
-        const unsigned char *vb = (const unsigned char *)&v;
+    for (int b = b_lo; b < b_hi; b++) {
+        zero_counters(cnt8, BS);
+        __syncthreads();
+        count_one_block(S, cnt8, BS, q, b, b + 1 < b_hi ? b + 1 : -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r);
+        // a4: C = {x : V[x] >= tau}, ascending id (Alg. 1 l.18); each warp
+        // compacts its own counter range (count pass, one barrier, write pass)
+        const unsigned char *mine = cnt8 + warp * span;
+        int cw = 0;
+        for (int j = lane * 16; j < span; j += 512) {
+            const uint4 v = *(const uint4 *)(mine + j);
+            const unsigned char *vb = (const unsigned char *)&v;
 #pragma unroll
-        for (int i = 0; i < 16; i++) cw += vb[i] >= tau;
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) cw += __shfl_xor_sync(0xffffffffu, cw, off);
-    if (lane == 0) wtot[warp] = cw;
-    __syncthreads();
-    int running = 0;
-    for (int w2 = 0; w2 < warp; w2++) running += wtot[w2];
-    int32_t *outp = pool + q * PS + (int64_t)b * BS;
-    const int gbase = b * BS + warp * span;
-    for (int j = lane * 16; j < span; j += 512) {
-        const uint4 v = *(const uint4 *)(mine + j);
-        const unsigned char *vb = (const unsigned char *)&v;
-        int c = 0;
-#pragma unroll
-        for (int i = 0; i < 16; i++) c += vb[i] >= tau;
-        int inc = c;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, inc, off);
-            if (lane >= off) inc += t;
+            for (int i = 0; i < 16; i++) cw += vb[i] >= tau;
         }
-        int o = running + inc - c;
-        if (c) {
 #pragma unroll
-            for (int i = 0; i < 16; i++)
-                if (vb[i] >= tau) outp[o++] = gbase + j + i;
+        for (int off = 16; off; off >>= 1) cw += __shfl_xor_sync(0xffffffffu, cw, off);
+        if (lane == 0) S.wtot[warp] = cw;
+        __syncthreads();
+        if (tid == 0) {
+            int n = 0;
+            for (int w2 = 0; w2 < WARPS; w2++) n += S.wtot[w2];
+            const int base = atomicAdd(cursor + q, n);
+            S.base = base;
+            cbase[q * NB + b] = base;
+            ncand[q * NB + b] = n;
+            if ((int64_t)base + n > CAPQ) atomicMax(need, base + n);
         }
-        if (traceV) {
-            const int64_t g0 = (int64_t)gbase + j;
+        __syncthreads();
+        int running = S.base;
+        for (int w2 = 0; w2 < warp; w2++) running += S.wtot[w2];
+        int32_t *outp = pool + q * CAPQ;
+        const int gbase = b * BS + warp * span;
+        for (int j = lane * 16; j < span; j += 512) {
+            const uint4 v = *(const uint4 *)(mine + j);
+            const unsigned char *vb = (const unsigned char *)&v;
+            int c = 0;
 #pragma unroll
-            for (int i = 0; i < 16; i++)
-                if (g0 + i < N) traceV[q * N + g0 + i] = vb[i];
+            for (int i = 0; i < 16; i++) c += vb[i] >= tau;
+            int inc = c;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, inc, off);
+                if (lane >= off) inc += t;
+            }
+            int o = running + inc - c;
+            if (c) {
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    if (vb[i] >= tau) {
+                        if (o < CAPQ) outp[o] = gbase + j + i;
+                        o++;
+                    }
+            }
+            if (traceV) {
+                const int64_t g0 = (int64_t)gbase + j;
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    if (g0 + i < N) traceV[q * N + g0 + i] = vb[i];
+            }
+            running += __shfl_sync(0xffffffffu, inc, 31);
         }
-        running += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    if (tid == 0) {
-        int t = 0;
-        for (int w2 = 0; w2 < WARPS; w2++) t += wtot[w2];
-        ncand[q * NB + b] = t;
+        __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
 // a4 fallback (Z8): |C| < k -> the first min(k,|T|) touched ids by
-// (V desc, id asc), restated in ascending id.  Rare; one CTA per query.
+// (V desc, id asc), restated in ascending id.  Rare; one CTA per query,
+// counting every block twice (histogram of V, then selection).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict__ act,
                                                        const int32_t *__restrict__ act_len, int M, int KK,
                                                        const int32_t *__restrict__ off2, int NB,
                                                        const int32_t *__restrict__ ids, int64_t N, int BS, int k,
-                                                       int32_t *__restrict__ pool, int64_t PS,
-                                                       int32_t *__restrict__ ncand, int32_t *__restrict__ fbflag) {
+                                                       int32_t *__restrict__ pool, int64_t CAPQ,
+                                                       int32_t *__restrict__ cbase, int32_t *__restrict__ ncand,
+                                                       int32_t *__restrict__ fbflag) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    uint32_t *cnt32 = (uint32_t *)smraw;
+    unsigned char *cnt8 = smraw;
     CountSmem &S = *(CountSmem *)(smraw + BS);
     __shared__ int hist[2 * MAX_M + 2];
     __shared__ int s_total, s_vstar, s_quota, s_eqbase, s_n;
@@ -412,12 +447,16 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
         if (tid == 0) fbflag[q] = 0;
         return;
     }
-    const unsigned char *c8 = (const unsigned char *)cnt32;
+    const int Etot = count_setup(S, q, act, act_len, M, KK);
+    int s0r[CS_EPT], s1r[CS_EPT];
     // pass 1: histogram of V over the touched set
     for (int b = 0; b < NB; b++) {
-        count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N, 0);
+        prefetch_first(S, Etot, off2, NB, b, s0r, s1r);
+        zero_counters(cnt8, BS);
+        __syncthreads();
+        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r);
         for (int j = tid; j < BS; j += THREADS)
-            if (c8[j]) atomicAdd(&hist[c8[j]], 1);
+            if (cnt8[j]) atomicAdd(&hist[cnt8[j]], 1);
         __syncthreads();
     }
     if (tid == 0) {
@@ -437,15 +476,18 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
     }
     __syncthreads();
     const int vstar = s_vstar, quota = s_quota;
-    int32_t *outp = pool + q * PS;
+    int32_t *outp = pool + q * CAPQ;
     // pass 2: ids with V > V*, and the first `quota` ids with V == V*, ascending
     for (int b = 0; b < NB; b++) {
-        count_block(S, cnt32, BS, q, b, act, act_len, M, KK, off2, NB, ids, N, 0);
+        prefetch_first(S, Etot, off2, NB, b, s0r, s1r);
+        zero_counters(cnt8, BS);
+        __syncthreads();
+        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r);
         for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
-            int j = j0 + tid * 16;
+            const int j = j0 + tid * 16;
             unsigned char vb[16];
 #pragma unroll
-            for (int i = 0; i < 16; i++) vb[i] = (j + i < BS) ? c8[j + i] : 0;
+            for (int i = 0; i < 16; i++) vb[i] = (j + i < BS) ? cnt8[j + i] : 0;
             int ceq = 0;
 #pragma unroll
             for (int i = 0; i < 16; i++) ceq += vb[i] == vstar;
@@ -474,7 +516,10 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
             __syncthreads();
         }
     }
-    for (int b = tid; b < NB; b += THREADS) ncand[q * NB + b] = (b == 0) ? s_n : 0;
+    for (int b = tid; b < NB; b += THREADS) {
+        ncand[q * NB + b] = (b == 0) ? s_n : 0;
+        cbase[q * NB + b] = 0;
+    }
     if (tid == 0) fbflag[q] = 1;
 }
 
@@ -564,9 +609,32 @@ __device__ __forceinline__ void load_qd(double *qd, const float *qrow, int pitch
 // a5, Guaranteed Mode: exact L2 of every candidate, per-warp top-k, CTA merge.
 // grid (S, Qc); candidates of query q are split over S*WARPS warps.
 // ---------------------------------------------------------------------------
+// prefix over the blocks' candidate counts (pre, NB+1) and their pool bases
+__device__ __forceinline__ void block_prefix(const int32_t *__restrict__ ncand, const int32_t *__restrict__ cbase,
+                                             int64_t q, int NB, int *pre, int *cbs) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        int acc = 0;
+        for (int b0 = 0; b0 < NB; b0 += 32) {
+            const int b = b0 + lane;
+            int v = b < NB ? ncand[q * NB + b] : 0;
+            if (b < NB) cbs[b] = cbase[q * NB + b];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += t;
+            }
+            if (b < NB) pre[b + 1] = acc + v;
+            acc += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (lane == 0) pre[0] = 0;
+    }
+}
+
 __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restrict__ qrot, int pitch,
                                                            const float *__restrict__ X, int64_t gid_base,
-                                                           const int32_t *__restrict__ pool, int64_t PS, int BS,
+                                                           const int32_t *__restrict__ pool, int64_t CAPQ,
+                                                           const int32_t *__restrict__ cbase,
                                                            const int32_t *__restrict__ ncand, int NB, int k,
                                                            double *__restrict__ part_d, int64_t *__restrict__ part_i) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -574,18 +642,12 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
     double *Ld = qd + pitch;                         // WARPS x k
     int64_t *Li = (int64_t *)(Ld + WARPS * k);       // WARPS x k
     int *pre = (int *)(Li + WARPS * k);              // NB + 1
+    int *cbs = pre + NB + 1;                         // NB
     __shared__ int wcnt[WARPS];
     const int64_t q = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     load_qd(qd, qrot + q * pitch, pitch);
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int b = 0; b < NB; b++) {
-            pre[b] = acc;
-            acc += ncand[q * NB + b];
-        }
-        pre[NB] = acc;
-    }
+    block_prefix(ncand, cbase, q, NB, pre, cbs);
     __syncthreads();
     const int total = pre[NB];
     const int nvec = pitch / 4;
@@ -597,16 +659,16 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
     double wd = INFINITY;
     int64_t wi = 0x7fffffffffffffffLL;
     int bcur = 0;
-    const int32_t *poolq = pool + q * PS;
+    const int32_t *poolq = pool + q * CAPQ;
     for (int v = gw; v < total; v += 2 * W) {
         int v1 = v + W;
         while (pre[bcur + 1] <= v) bcur++;
-        int lid0 = poolq[(int64_t)bcur * BS + (v - pre[bcur])];
+        int lid0 = poolq[cbs[bcur] + (v - pre[bcur])];
         int lid1 = -1;
         if (v1 < total) {
             int b1 = bcur;
             while (pre[b1 + 1] <= v1) b1++;
-            lid1 = poolq[(int64_t)b1 * BS + (v1 - pre[b1])];
+            lid1 = poolq[cbs[b1] + (v1 - pre[b1])];
         }
         double d0, d1;
         if (lid1 >= 0) {
@@ -720,14 +782,17 @@ __global__ void __launch_bounds__(THREADS) k_merge_lists(const double *__restric
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ qrot, int pitch, int Dp,
                                                       const uint64_t *__restrict__ codes, int Wd,
-                                                      const int32_t *__restrict__ pool, int64_t PS, int BS,
+                                                      const int32_t *__restrict__ pool, int64_t CAPQ,
+                                                      const int32_t *__restrict__ cbase,
                                                       const int32_t *__restrict__ ncand, int NB,
                                                       int32_t *__restrict__ cbuf, uint16_t *__restrict__ hbuf,
-                                                      int64_t CS, int32_t *__restrict__ ghist) {
+                                                      int32_t *__restrict__ ghist) {
     extern __shared__ __align__(16) unsigned char sm[];
     uint64_t *qc = (uint64_t *)sm;          // Wd
     int *hist = (int *)(qc + Wd);           // Dp + 1
     int *pre = hist + Dp + 1;               // NB + 1
+    int *cbs = pre + NB + 1;                // NB
+    const int64_t CS = CAPQ;
     const int64_t q = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float *qrow = qrot + q * pitch;
@@ -740,21 +805,7 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
         qc[w] = word;
     }
     for (int i = tid; i < Dp + 1; i += THREADS) hist[i] = 0;
-    if (warp == 0) {
-        int acc = 0;
-        for (int b0 = 0; b0 < NB; b0 += 32) {
-            const int b = b0 + lane;
-            int v = b < NB ? ncand[q * NB + b] : 0;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                int t = __shfl_up_sync(0xffffffffu, v, off);
-                if (lane >= off) v += t;
-            }
-            if (b < NB) pre[b + 1] = acc + v;
-            acc += __shfl_sync(0xffffffffu, v, 31);
-        }
-        if (lane == 0) pre[0] = 0;
-    }
+    block_prefix(ncand, cbase, q, NB, pre, cbs);
     __syncthreads();
     const int total = pre[NB];
     const int per = (total + gridDim.x - 1) / gridDim.x;
@@ -762,7 +813,7 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
     int G = 1;
     while (G < Wd && G < 32) G <<= 1;
     const int gpw = 32 / G, g = lane / G, gl = lane % G;
-    const int32_t *poolq = pool + q * PS;
+    const int32_t *poolq = pool + q * CAPQ;
     for (int v0 = v_lo + warp * gpw * 4; v0 < v_hi; v0 += WARPS * gpw * 4) {
         int lid[4], h[4];
 #pragma unroll
@@ -776,7 +827,7 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
                     if (pre[mid] <= v) lo = mid;
                     else hi = mid;
                 }
-                lid[u] = __ldg(poolq + (int64_t)lo * BS + (v - pre[lo]));
+                lid[u] = __ldg(poolq + cbs[lo] + (v - pre[lo]));
             }
         }
 #pragma unroll
@@ -1172,32 +1223,51 @@ static int env_int(const char *name, int dflt) {
     return v ? atoi(v) : dflt;
 }
 
-void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
-            cudaStream_t s, const crisp_trace_t *tr) {
-    const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch;
-    const int64_t N = ix->N, PS = (int64_t)NB * BS;
-    // per-query workspace bytes -> query chunk
-    int64_t perq = (int64_t)pitch * 4 * 2 + (int64_t)M * KK * 4 + (int64_t)M * 12 + PS * 4 + (int64_t)NB * 4 + 64;
-    const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));     // CTAs per query in the row kernels
-    const int HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 4));   // CTAs per query in k_hamming
+static void set_attrs() {
+    static bool done = false;
+    if (done) return;
+    CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_patience_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    done = true;
+}
+
+// One attempt over all queries with candidate capacity CAPQ per query; returns
+// false (and the capacity needed) if some query's candidate set overflowed.
+static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
+                        cudaStream_t s, const crisp_trace_t *tr, int64_t CAPQ, int64_t *need_out) {
+    const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch, Dp = ix->Dp;
+    const int64_t N = ix->N;
+    const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));       // CTAs per query in the row kernels
+    const int HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 4));     // CTAs per query in k_hamming
     const int S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
     const int R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
-    const int emode = env_int("CRISP_COUNT_EMODE", 0);
+    const int BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 8)));  // id blocks per count CTA
+    // per-query workspace bytes -> query chunk
+    int64_t perq = (int64_t)pitch * 4 * 2 + (int64_t)M * KK * 4 + (int64_t)M * 12 + CAPQ * 4 + (int64_t)NB * 8 + 64;
     if (mode == 0) perq += (int64_t)S * k * 16;
-    else perq += N * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
+    else perq += CAPQ * 6 + (int64_t)(Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
     if (tr && tr->V) perq += N;
-    int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : (16LL << 30);
+    const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : (16LL << 30);
     int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
     Qc = std::min<int64_t>(Qc, 65535);
-    if (tr) Qc = std::min<int64_t>(Qc, Q);
     DevBuf wb(s);
     float *qpad = wb.alloc<float>((size_t)Qc * pitch);
     float *qrot = ix->rotated ? wb.alloc<float>((size_t)Qc * pitch) : qpad;
     uint32_t *act = wb.alloc<uint32_t>((size_t)Qc * M * KK);
     int32_t *act_len = wb.alloc<int32_t>((size_t)Qc * M);
     int64_t *retr = wb.alloc<int64_t>((size_t)Qc * M);
-    int32_t *pool = wb.alloc<int32_t>((size_t)Qc * PS);
+    int32_t *pool = wb.alloc<int32_t>((size_t)Qc * CAPQ);
     int32_t *ncand = wb.alloc<int32_t>((size_t)Qc * NB);
+    int32_t *cbase = wb.alloc<int32_t>((size_t)Qc * NB);
+    int32_t *cursor = wb.alloc<int32_t>((size_t)Qc + 1);  // [Qc] = overflow need
+    int32_t *need = cursor + Qc;
     int32_t *fb = wb.alloc<int32_t>((size_t)Qc);
     double *part_d = nullptr, *dbuf = nullptr;
     int64_t *part_i = nullptr, *nver = nullptr;
@@ -1208,9 +1278,9 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
         part_d = wb.alloc<double>((size_t)Qc * S * k);
         part_i = wb.alloc<int64_t>((size_t)Qc * S * k);
     } else {
-        cbuf = wb.alloc<int32_t>((size_t)Qc * N);
-        hbuf = wb.alloc<uint16_t>((size_t)Qc * N);
-        ghist = wb.alloc<int32_t>((size_t)Qc * (ix->Dp + 1));
+        cbuf = wb.alloc<int32_t>((size_t)Qc * CAPQ);
+        hbuf = wb.alloc<uint16_t>((size_t)Qc * CAPQ);
+        ghist = wb.alloc<int32_t>((size_t)Qc * (Dp + 1));
         totals = wb.alloc<int32_t>((size_t)Qc);
         dbuf = wb.alloc<double>((size_t)Qc * S0);
         pst.Td = wb.alloc<double>((size_t)Qc * k);
@@ -1224,36 +1294,23 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
     uint8_t *traceV = (tr && tr->V) ? wb.alloc<uint8_t>((size_t)Qc * N) : nullptr;
     double *d64tmp = out.d64 ? nullptr : wb.alloc<double>((size_t)Qc * k);
 
-    // kernel attributes (dynamic smem)
     const int probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
     const int probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
     const int count_smem = BS + (int)sizeof(CountSmem);
-    const int rx_smem = pitch * 8 + WARPS * k * 16 + (NB + 1) * 4;
-    const int ham_smem = ix->W * 8 + (ix->Dp + 1) * 4 + (NB + 1) * 4;
-    const int hsort_smem = (ix->Dp + 1) * 4;
+    const int rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NB + 1) * 4;
+    const int ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NB + 1) * 4;
+    const int hsort_smem = (Dp + 1) * 4;
     const int vr_smem = pitch * 8;
     const int scan_smem = WARPS * k * 16;
     const int pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16;
-    static bool attr_done = false;
-    if (!attr_done) {
-        CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CRISP_CUDA(cudaFuncSetAttribute(k_patience_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr_done = true;
-    }
+    set_attrs();
     CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
                     pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
                 "shared-memory footprint too large for this (D, K, k)");
 
     const int wk = (mode == 1) ? k : 0;
     const int P = (mode == 1 && ix->patience_factor > 0) ? ix->patience_factor * k : 0;
-    std::vector<int32_t> h_pool, h_ncand;
+    std::vector<int32_t> h_pool, h_ncand, h_cbase;
     for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
         const int64_t qn = std::min(Qc, Q - q0);
         {
@@ -1262,7 +1319,7 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
             CRISP_LAUNCH();
             g_launches++;
             if (ix->rotated) {
-                rotate_rows_f64(qpad, qn, ix->Dp, pitch, ix->R, qrot, pitch, s);
+                rotate_rows_f64(qpad, qn, Dp, pitch, ix->R, qrot, pitch, s);
                 g_launches++;
             }
         }
@@ -1276,31 +1333,44 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
         }
         {
             StageScope st(s, 2);
-            dim3 g(NB, (unsigned)qn);
-            k_count_select<<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, ix->tau,
-                                                          pool, PS, ncand, traceV, emode);
+            CRISP_CUDA(cudaMemsetAsync(cursor, 0, (size_t)(Qc + 1) * 4, s));
+            dim3 g(nblk(NB, BPC), (unsigned)qn);
+            k_count_select<<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, BPC,
+                                                          ix->tau, pool, CAPQ, cursor, cbase, ncand, need, traceV);
             CRISP_LAUNCH();
             g_launches++;
         }
         {
             StageScope st(s, 3);
             k_fallback<<<(unsigned)qn, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, k,
-                                                                 pool, PS, ncand, fb);
+                                                                 pool, CAPQ, cbase, ncand, fb);
             CRISP_LAUNCH();
             g_launches++;
         }
-        if (tr && (tr->cand || tr->cand_n || (tr->order && mode == 0) || (tr->n_verified && mode == 0))) {
-            h_pool.resize((size_t)qn * PS);
+        {
+            // exactness guard: a candidate set larger than the capacity -> redo
+            int32_t hneed = 0;
+            CRISP_CUDA(cudaMemcpyAsync(&hneed, need, 4, cudaMemcpyDeviceToHost, s));
+            CRISP_CUDA(cudaStreamSynchronize(s));
+            if (hneed > CAPQ) {
+                *need_out = hneed;
+                return false;
+            }
+        }
+        if (tr) {
+            h_pool.resize((size_t)qn * CAPQ);
             h_ncand.resize((size_t)qn * NB);
-            CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), pool, (size_t)qn * PS * 4, cudaMemcpyDeviceToHost, s));
+            h_cbase.resize((size_t)qn * NB);
+            CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), pool, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
             CRISP_CUDA(cudaMemcpyAsync(h_ncand.data(), ncand, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
+            CRISP_CUDA(cudaMemcpyAsync(h_cbase.data(), cbase, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
             CRISP_CUDA(cudaStreamSynchronize(s));
             for (int64_t q = 0; q < qn; q++) {
                 int64_t n = 0;
                 for (int b = 0; b < NB; b++) {
-                    int c = h_ncand[q * NB + b];
+                    const int c = h_ncand[q * NB + b], base = h_cbase[q * NB + b];
                     for (int j = 0; j < c; j++) {
-                        int32_t id = h_pool[q * PS + (int64_t)b * BS + j];
+                        const int32_t id = h_pool[q * CAPQ + base + j];
                         if (tr->cand) tr->cand[(q0 + q) * N + n] = id;
                         if (tr->order && mode == 0) tr->order[(q0 + q) * N + n] = id;
                         n++;
@@ -1317,31 +1387,32 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
             {
                 StageScope st(s, 4);
                 dim3 g(S, (unsigned)qn);
-                k_rerank_exact<<<g, THREADS, rx_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, PS, BS, ncand, NB,
-                                                          k, part_d, part_i);
+                k_rerank_exact<<<g, THREADS, rx_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, CAPQ, cbase, ncand,
+                                                          NB, k, part_d, part_i);
                 CRISP_LAUNCH();
-            g_launches++;
+                g_launches++;
             }
             {
                 StageScope st(s, 5);
                 k_merge_lists<<<(unsigned)qn, THREADS, 0, s>>>(part_d, part_i, S, qn, k, 0, od64, od, oi);
                 CRISP_LAUNCH();
-            g_launches++;
+                g_launches++;
             }
         } else {
-            CRISP_CUDA(cudaMemsetAsync(ghist, 0, (size_t)qn * (ix->Dp + 1) * 4, s));
+            CRISP_CUDA(cudaMemsetAsync(ghist, 0, (size_t)qn * (Dp + 1) * 4, s));
             CRISP_CUDA(cudaMemsetAsync(pst.cnt, 0, (size_t)Qc * 3 * 4, s));
             {
                 StageScope st(s, 6);
                 dim3 g(HS, (unsigned)qn);
-                k_hamming<<<g, THREADS, ham_smem, s>>>(qrot, pitch, ix->Dp, ix->codes, ix->W, pool, PS, BS, ncand, NB,
-                                                       cbuf, hbuf, N, ghist);
+                k_hamming<<<g, THREADS, ham_smem, s>>>(qrot, pitch, Dp, ix->codes, ix->W, pool, CAPQ, cbase, ncand, NB,
+                                                       cbuf, hbuf, ghist);
                 CRISP_LAUNCH();
                 g_launches++;
             }
             {
                 StageScope st(s, 7);
-                k_hsort<<<(unsigned)qn, 32, hsort_smem, s>>>(ncand, NB, ix->Dp, ghist, cbuf, hbuf, N, pool, PS, totals);
+                k_hsort<<<(unsigned)qn, 32, hsort_smem, s>>>(ncand, NB, Dp, ghist, cbuf, hbuf, CAPQ, pool, CAPQ,
+                                                             totals);
                 CRISP_LAUNCH();
                 g_launches++;
             }
@@ -1349,16 +1420,16 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
                 StageScope st(s, 4);
                 for (int r = 0; r < R0; r++) {
                     dim3 g(S, (unsigned)qn);
-                    k_verify_rows<<<g, THREADS, vr_smem, s>>>(qrot, pitch, ix->X, pool, PS, totals, pst.done, r, S0,
+                    k_verify_rows<<<g, THREADS, vr_smem, s>>>(qrot, pitch, ix->X, pool, CAPQ, totals, pst.done, r, S0,
                                                               dbuf);
                     CRISP_LAUNCH();
                     g_launches++;
-                    k_patience_scan<<<nblk(qn, WARPS), THREADS, scan_smem, s>>>(qn, totals, pool, PS, ix->gid_base, dbuf,
-                                                                                r, S0, k, P, pst, od64, od, oi);
+                    k_patience_scan<<<nblk(qn, WARPS), THREADS, scan_smem, s>>>(qn, totals, pool, CAPQ, ix->gid_base,
+                                                                                dbuf, r, S0, k, P, pst, od64, od, oi);
                     CRISP_LAUNCH();
                     g_launches++;
                 }
-                k_patience_tail<<<(unsigned)qn, THREADS, pat_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, PS,
+                k_patience_tail<<<(unsigned)qn, THREADS, pat_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, CAPQ,
                                                                         totals, R0 * S0, k, P, pst, od64, od, oi);
                 CRISP_LAUNCH();
                 g_launches++;
@@ -1373,56 +1444,61 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
         if (tr) {
             std::vector<int32_t> hl((size_t)qn * M);
             std::vector<uint32_t> ha;
-            std::vector<int64_t> hr((size_t)qn * M);
+            std::vector<int64_t> hr((size_t)qn * M), hn;
             CRISP_CUDA(cudaMemcpyAsync(hl.data(), act_len, (size_t)qn * M * 4, cudaMemcpyDeviceToHost, s));
             CRISP_CUDA(cudaMemcpyAsync(hr.data(), retr, (size_t)qn * M * 8, cudaMemcpyDeviceToHost, s));
             if (tr->act_cell || tr->act_w) {
                 ha.resize((size_t)qn * M * KK);
                 CRISP_CUDA(cudaMemcpyAsync(ha.data(), act, (size_t)qn * M * KK * 4, cudaMemcpyDeviceToHost, s));
             }
-            if (tr->V)
-                CRISP_CUDA(cudaMemcpyAsync(tr->V + q0 * N, traceV, (size_t)qn * N, cudaMemcpyDeviceToHost, s));
-            if (tr->qrot) {
+            if (tr->V) CRISP_CUDA(cudaMemcpyAsync(tr->V + q0 * N, traceV, (size_t)qn * N, cudaMemcpyDeviceToHost, s));
+            if (tr->qrot)
                 for (int64_t q = 0; q < qn; q++)
-                    CRISP_CUDA(cudaMemcpyAsync(tr->qrot + (q0 + q) * ix->Dp, qrot + q * pitch, (size_t)ix->Dp * 4,
+                    CRISP_CUDA(cudaMemcpyAsync(tr->qrot + (q0 + q) * Dp, qrot + q * pitch, (size_t)Dp * 4,
                                                cudaMemcpyDeviceToHost, s));
-            }
             if (tr->fallback)
                 CRISP_CUDA(cudaMemcpyAsync(tr->fallback + q0, fb, (size_t)qn * 4, cudaMemcpyDeviceToHost, s));
-            std::vector<int64_t> hn;
-            if (mode == 1 && tr->n_verified) {
+            if (mode == 1) {
                 hn.resize(qn);
                 CRISP_CUDA(cudaMemcpyAsync(hn.data(), nver, (size_t)qn * 8, cudaMemcpyDeviceToHost, s));
-            }
-            if (mode == 1 && tr->order) {
-                h_pool.resize((size_t)qn * PS);
-                CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), pool, (size_t)qn * PS * 4, cudaMemcpyDeviceToHost, s));
-            }
-            if (mode == 1 && (tr->order || tr->cand || tr->cand_n)) {
-                h_ncand.resize((size_t)qn * NB);
-                CRISP_CUDA(cudaMemcpyAsync(h_ncand.data(), ncand, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
+                CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), pool, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
             }
             CRISP_CUDA(cudaStreamSynchronize(s));
             for (int64_t q = 0; q < qn; q++) {
                 for (int m = 0; m < M; m++) {
-                    int L = hl[q * M + m];
+                    const int L = hl[q * M + m];
                     if (tr->act_len) tr->act_len[(q0 + q) * M + m] = L;
                     if (tr->retrieved) tr->retrieved[(q0 + q) * M + m] = hr[q * M + m];
                     for (int r = 0; r < L && !ha.empty(); r++) {
-                        uint32_t v = ha[(q * M + m) * (int64_t)KK + r];
+                        const uint32_t v = ha[(q * M + m) * (int64_t)KK + r];
                         if (tr->act_cell) tr->act_cell[((q0 + q) * M + m) * (int64_t)KK + r] = (int32_t)(v & 0xffffu);
                         if (tr->act_w) tr->act_w[((q0 + q) * M + m) * (int64_t)KK + r] = (int32_t)(v >> 16);
                     }
                 }
                 if (mode == 1) {
                     int64_t n = 0;
-                    for (int b = 0; b < NB; b++) n += h_ncand.empty() ? 0 : h_ncand[q * NB + b];
+                    for (int b = 0; b < NB; b++) n += h_ncand[q * NB + b];
                     if (tr->order)
-                        for (int64_t i = 0; i < n; i++) tr->order[(q0 + q) * N + i] = h_pool[q * PS + i];
+                        for (int64_t i = 0; i < n; i++) tr->order[(q0 + q) * N + i] = h_pool[q * CAPQ + i];
                     if (tr->n_verified) tr->n_verified[q0 + q] = hn[q];
                 }
             }
         }
+    }
+    return true;
+}
+
+void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
+            cudaStream_t s, const crisp_trace_t *tr) {
+    // candidate capacity per query: optimistic, grown (and the batch redone)
+    // if any query's |C_q| exceeds it, so results never depend on it
+    const int64_t NBS = (int64_t)ix->NB * ix->BS;
+    int64_t cap = std::min<int64_t>(NBS, std::max<int64_t>(4096, env_int("CRISP_CAND_CAP", 1 << 17)));
+    if (tr) cap = NBS;
+    for (;;) {
+        int64_t need = 0;
+        if (search_pass(ix, queries, Q, k, mode, out, s, tr, cap, &need)) return;
+        cap = std::min<int64_t>(NBS, std::max<int64_t>(cap * 2, need + need / 4));
     }
 }
 

@@ -220,3 +220,18 @@ def test_patience_rounds_and_tail(crisp, monkeypatch, batch, rounds):
         r_ids, r_d, ot = oracle.search(ox, Qv, 5, 1, B, 1, patience_factor=pf, trace=True)
         compare_trace(t, ot, 1, X.shape[0])
         assert_topk_parity(ids, d, r_ids, r_d, f"patience batch={batch} rounds={rounds} pf={pf}")
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_candidate_capacity_regrow(crisp, monkeypatch, mode):
+    """|C_q| larger than the optimistic per-query candidate capacity: the batch
+    is redone with a larger capacity, results unchanged (exactness guard)."""
+    monkeypatch.setenv("CRISP_CAND_CAP", "4096")
+    monkeypatch.setenv("CRISP_COUNT_BPC", "2")
+    X, Qv, ox = make_case(cfg=1, N=14000, D=64, Q=20, M=4, K=6, seed=11)
+    ix = build_gpu(crisp, X, ox, block_ids=4096)
+    ix.set_search_params(budget=9000, tau=1, patience_factor=0)
+    ids, d = ix.search(Qv, 10, mode)
+    r_ids, r_d, ot = oracle.search(ox, Qv, 10, mode, 9000, 1, patience_factor=0, trace=True)
+    assert ot["cand_n"].max() > 4096
+    assert_topk_parity(ids, d, r_ids, r_d, "capacity regrow")
