@@ -164,6 +164,7 @@ struct CountSmem {
     int32_t pre[CS_CAP + 1];   // exclusive prefix of slice lengths
     int32_t pos[CS_TCAP];      // window: ids[] index | WFLAG, then local id | WFLAG
     int32_t lpre[MAX_M + 2];   // prefix of act_len over m
+    int32_t mps[MAX_M + 1], mpe[MAX_M + 1];  // per-window position range of each subspace
     int32_t wtot[WARPS];
     int32_t base;
     typename cub::BlockScan<int, THREADS>::TempStorage scan;
@@ -222,10 +223,12 @@ __device__ __forceinline__ uint32_t entry_of(const CountSmem &S, int e, bool cac
 
 // Count block b of query q into the zeroed counters.  s0r/s1r: off2 values of
 // this block for the thread's cached entries (cached case), refilled for nb.
+// If cross != nullptr, the ids whose count crosses tau (old < tau <= new; a
+// count only grows, so each id crosses at most once) are flagged in the bitmap.
 __device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64_t q, int b, int nb, int Etot,
                                 const uint32_t *__restrict__ act, int M, int KK, const int32_t *__restrict__ off2,
                                 int NB, const int32_t *__restrict__ ids, int64_t N, int (&s0r)[CS_EPT],
-                                int (&s1r)[CS_EPT]) {
+                                int (&s1r)[CS_EPT], int tau, uint32_t *cross) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool cached = Etot <= CS_CAP;
     const uint32_t bbase = (uint32_t)b * (uint32_t)BS;
@@ -296,15 +299,23 @@ __device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64
                     if (p < Wn) S.pos[p] = (int32_t)(((uint32_t)idv[u] - bbase) | ((uint32_t)v[u] & WFLAG));
                 }
             }
+            if (tid <= mb - ma) {  // window position range of each subspace
+                const int m = ma + tid;
+                const int ea = max(S.lpre[m], e0) - e0, eb = min(S.lpre[m + 1], e0 + ne) - e0;
+                S.mps[tid] = max(S.pre[ea], P0) - P0;
+                S.mpe[tid] = min(S.pre[eb], P0 + Wn) - P0;
+            }
             __syncthreads();
             // subspace by subspace: plain byte RMW, barrier between subspaces
-            for (int m = ma; m <= mb; m++) {
-                const int ea = max(S.lpre[m], e0) - e0, eb = min(S.lpre[m + 1], e0 + ne) - e0;
-                const int ps = max(S.pre[ea], P0), pe = min(S.pre[eb], P0 + Wn);
-                for (int p = ps + tid; p < pe; p += THREADS) {
-                    const uint32_t x = (uint32_t)S.pos[p - P0];
+            for (int mi = 0; mi <= mb - ma; mi++) {
+                const int pe = S.mpe[mi];
+                for (int p = S.mps[mi] + tid; p < pe; p += THREADS) {
+                    const uint32_t x = (uint32_t)S.pos[p];
                     const uint32_t local = x & ~WFLAG;
-                    cnt8[local] = (unsigned char)(cnt8[local] + 1 + (x >> 31));
+                    const int old = cnt8[local];
+                    const int nw = old + 1 + (int)(x >> 31);
+                    cnt8[local] = (unsigned char)nw;
+                    if (cross && old < tau && nw >= tau) atomicOr(cross + (local >> 5), 1u << (local & 31));
                 }
                 __syncthreads();
             }
@@ -344,28 +355,24 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
                                                            uint8_t *__restrict__ traceV) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;
-    CountSmem &S = *(CountSmem *)(smraw + BS);
+    uint32_t *cross = (uint32_t *)(smraw + BS);            // BS bits
+    CountSmem &S = *(CountSmem *)(smraw + BS + BS / 8);
     const int64_t q = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b_lo = blockIdx.x * BPC, b_hi = min(NB, b_lo + BPC);
     const int Etot = count_setup(S, q, act, act_len, M, KK);
     int s0r[CS_EPT], s1r[CS_EPT];
     prefetch_first(S, Etot, off2, NB, b_lo, s0r, s1r);
-    const int span = BS >> 3;
+    const int wwords = BS / 256;  // bitmap words per warp
     for (int b = b_lo; b < b_hi; b++) {
-        zero_counters(cnt8, BS);
+        zero_counters(cnt8, BS + BS / 8);
         __syncthreads();
-        count_one_block(S, cnt8, BS, q, b, b + 1 < b_hi ? b + 1 : -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r);
-        // a4: C = {x : V[x] >= tau}, ascending id (Alg. 1 l.18); each warp
-        // compacts its own counter range (count pass, one barrier, write pass)
-        const unsigned char *mine = cnt8 + warp * span;
+        count_one_block(S, cnt8, BS, q, b, b + 1 < b_hi ? b + 1 : -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r,
+                        tau, cross);
+        // a4: C = {x : V[x] >= tau} (Alg. 1 l.18), ascending id: the crossing
+        // bitmap holds exactly those ids; each warp compacts its word range
         int cw = 0;
-        for (int j = lane * 16; j < span; j += 512) {
-            const uint4 v = *(const uint4 *)(mine + j);
-            const unsigned char *vb = (const unsigned char *)&v;
-#pragma unroll
-            for (int i = 0; i < 16; i++) cw += vb[i] >= tau;
-        }
+        for (int i = lane; i < wwords; i += 32) cw += __popc(cross[warp * wwords + i]);
 #pragma unroll
         for (int off = 16; off; off >>= 1) cw += __shfl_xor_sync(0xffffffffu, cw, off);
         if (lane == 0) S.wtot[warp] = cw;
@@ -383,13 +390,10 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
         int running = S.base;
         for (int w2 = 0; w2 < warp; w2++) running += S.wtot[w2];
         int32_t *outp = pool + q * CAPQ;
-        const int gbase = b * BS + warp * span;
-        for (int j = lane * 16; j < span; j += 512) {
-            const uint4 v = *(const uint4 *)(mine + j);
-            const unsigned char *vb = (const unsigned char *)&v;
-            int c = 0;
-#pragma unroll
-            for (int i = 0; i < 16; i++) c += vb[i] >= tau;
+        for (int i0 = 0; i0 < wwords; i0 += 32) {
+            const int i = i0 + lane;
+            uint32_t word = i < wwords ? cross[warp * wwords + i] : 0u;
+            const int c = __popc(word);
             int inc = c;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
@@ -397,21 +401,18 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
                 if (lane >= off) inc += t;
             }
             int o = running + inc - c;
-            if (c) {
-#pragma unroll
-                for (int i = 0; i < 16; i++)
-                    if (vb[i] >= tau) {
-                        if (o < CAPQ) outp[o] = gbase + j + i;
-                        o++;
-                    }
-            }
-            if (traceV) {
-                const int64_t g0 = (int64_t)gbase + j;
-#pragma unroll
-                for (int i = 0; i < 16; i++)
-                    if (g0 + i < N) traceV[q * N + g0 + i] = vb[i];
+            const int g0 = b * BS + (warp * wwords + i) * 32;
+            while (word) {
+                const int bit = __ffs(word) - 1;
+                if (o < CAPQ) outp[o] = g0 + bit;
+                o++;
+                word &= word - 1;
             }
             running += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (traceV) {
+            for (int j = tid; j < BS; j += THREADS)
+                if ((int64_t)b * BS + j < N) traceV[q * N + (int64_t)b * BS + j] = cnt8[j];
         }
         __syncthreads();
     }
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
                                                        int32_t *__restrict__ fbflag) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;
-    CountSmem &S = *(CountSmem *)(smraw + BS);
+    CountSmem &S = *(CountSmem *)(smraw + BS + BS / 8);
     __shared__ int hist[2 * MAX_M + 2];
     __shared__ int s_total, s_vstar, s_quota, s_eqbase, s_n;
     const int64_t q = blockIdx.x;
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
         prefetch_first(S, Etot, off2, NB, b, s0r, s1r);
         zero_counters(cnt8, BS);
         __syncthreads();
-        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r);
+        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r, 0, nullptr);
         for (int j = tid; j < BS; j += THREADS)
             if (cnt8[j]) atomicAdd(&hist[cnt8[j]], 1);
         __syncthreads();
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
         prefetch_first(S, Etot, off2, NB, b, s0r, s1r);
         zero_counters(cnt8, BS);
         __syncthreads();
-        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r);
+        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r, 0, nullptr);
         for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
             const int j = j0 + tid * 16;
             unsigned char vb[16];
@@ -1296,7 +1297,7 @@ static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, 
 
     const int probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
     const int probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
-    const int count_smem = BS + (int)sizeof(CountSmem);
+    const int count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
     const int rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NB + 1) * 4;
     const int ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NB + 1) * 4;
     const int hsort_smem = (Dp + 1) * 4;
