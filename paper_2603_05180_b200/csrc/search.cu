@@ -811,42 +811,35 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
     const int total = pre[NB];
     const int per = (total + gridDim.x - 1) / gridDim.x;
     const int v_lo = blockIdx.x * per, v_hi = min(total, v_lo + per);
+    // G lanes per candidate, each loading at most two code words
     int G = 1;
-    while (G < Wd && G < 32) G <<= 1;
+    while (G < 32 && G * 2 < Wd) G <<= 1;
     const int gpw = 32 / G, g = lane / G, gl = lane % G;
     const int32_t *poolq = pool + q * CAPQ;
-    for (int v0 = v_lo + warp * gpw * 4; v0 < v_hi; v0 += WARPS * gpw * 4) {
-        int lid[4], h[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int v = v0 + u * gpw + g;
-            lid[u] = -1;
-            if (v < v_hi) {
-                int lo = 0, hi = NB;  // block b with pre[b] <= v < pre[b+1]
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (pre[mid] <= v) lo = mid;
-                    else hi = mid;
-                }
-                lid[u] = __ldg(poolq + cbs[lo] + (v - pre[lo]));
-            }
+    int bl = 0;  // block of this lane's candidate (monotone in v)
+    for (int v0 = v_lo + warp * 32; v0 < v_hi; v0 += WARPS * 32) {
+        const int v = v0 + lane;
+        int lid = -1;
+        if (v < v_hi) {
+            while (pre[bl + 1] <= v) bl++;
+            lid = __ldg(poolq + cbs[bl] + (v - pre[bl]));
         }
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            h[u] = 0;
-            if (lid[u] >= 0) {
-                const uint64_t *cr = codes + (int64_t)lid[u] * Wd;
-                for (int w = gl; w < Wd; w += G) h[u] += __popcll(qc[w] ^ __ldg(cr + w));
+#pragma unroll 4
+        for (int r = 0; r < 32 / gpw; r++) {
+            const int src = r * gpw + g;
+            const int lr = __shfl_sync(0xffffffffu, lid, src);
+            int hv = 0;
+            if (lr >= 0) {
+                const uint64_t *cr = codes + (int64_t)lr * Wd;
+                if (gl < Wd) hv = __popcll(qc[gl] ^ __ldg(cr + gl));
+                if (gl + G < Wd) hv += __popcll(qc[gl + G] ^ __ldg(cr + gl + G));
             }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            for (int off = G >> 1; off; off >>= 1) h[u] += __shfl_xor_sync(0xffffffffu, h[u], off);
-            const int v = v0 + u * gpw + g;
-            if (lid[u] >= 0 && gl == 0) {
-                cbuf[q * CS + v] = lid[u];
-                hbuf[q * CS + v] = (uint16_t)h[u];
-                atomicAdd(&hist[h[u]], 1);
+            for (int off = G >> 1; off; off >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, off);
+            if (lr >= 0 && gl == 0) {
+                const int vs = v0 + src;
+                cbuf[q * CS + vs] = lr;
+                hbuf[q * CS + vs] = (uint16_t)hv;
+                atomicAdd(&hist[hv], 1);
             }
         }
     }
@@ -886,30 +879,35 @@ __global__ void __launch_bounds__(32) k_hsort(const int32_t *__restrict__ ncand,
     const int32_t *cq = cbuf + q * CS;
     const uint16_t *hq = hbuf + q * CS;
     int32_t *out = pool + q * PS;
-    int nh = lane < total ? hq[lane] : 0;
-    int nl = lane < total ? cq[lane] : 0;
-    for (int v0 = 0; v0 < total; v0 += 32) {
-        const int v = v0 + lane;
-        const bool act = v < total;
-        const int h = nh, lid = nl;
-        if (v + 32 < total) {  // prefetch the next chunk
-            nh = hq[v + 32];
-            nl = cq[v + 32];
+    constexpr int U = 8;  // chunks of 32 loaded ahead (independent loads)
+    for (int v00 = 0; v00 < total; v00 += 32 * U) {
+        int hh[U], ll[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int v = v00 + u * 32 + lane;
+            hh[u] = v < total ? hq[v] : 0;
+            ll[u] = v < total ? cq[v] : 0;
         }
-        const unsigned am = __ballot_sync(0xffffffffu, act);
-        if (act) {
-            const unsigned peers = __match_any_sync(am, h);
-            const int leader = __ffs(peers) - 1;
-            const int rank = __popc(peers & ((1u << lane) - 1));
-            int base = 0;
-            if (lane == leader) {
-                base = start[h];
-                start[h] = base + __popc(peers);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int v = v00 + u * 32 + lane;
+            const bool act = v < total;
+            const unsigned am = __ballot_sync(0xffffffffu, act);
+            if (act) {
+                const int h = hh[u];
+                const unsigned peers = __match_any_sync(am, h);
+                const int leader = __ffs(peers) - 1;
+                const int rank = __popc(peers & ((1u << lane) - 1));
+                int base = 0;
+                if (lane == leader) {
+                    base = start[h];
+                    start[h] = base + __popc(peers);
+                }
+                base = __shfl_sync(peers, base, leader);
+                out[base + rank] = ll[u];
             }
-            base = __shfl_sync(peers, base, leader);
-            out[base + rank] = lid;
+            __syncwarp();
         }
-        __syncwarp();
     }
 }
 
