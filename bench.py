@@ -450,7 +450,7 @@ def run_sweep(args):
     rows = []
     for M in Ms:
         t0 = time.time()
-        ix = crisp.Index.build(X, M, K=50, seed=1)
+        ix = crisp.Index.build(X, M, K=50, seed=c["seed"])
         log(f"built M={M} in {time.time() - t0:.1f}s rotated={ix.info()['rotated']} cev={ix.info()['cev']:.3f}")
         for mode in modes:
             for beta in betas:
@@ -464,8 +464,8 @@ def run_sweep(args):
                     e1.record()
                     torch.cuda.synchronize()
                     ms = e0.elapsed_time(e1)
-                    r = dict(M=M, mode=mode, beta=beta, alpha=alpha, recall=recall_at(ids, gt, 10), qps=Q / ms * 1e3,
-                             ms=ms)
+                    r = dict(cfg=cfg, M=M, mode=mode, beta=beta, alpha=alpha, recall=recall_at(ids, gt, 10),
+                             qps=Q / ms * 1e3, ms=ms)
                     rows.append(r)
                     print(json.dumps(r), flush=True)
         ix.free()
