@@ -122,7 +122,9 @@ def ground_truth(X, Qd, k, extra=32):
     """Exact kNN: fp32 screening on the GPU (TF32 off), exact fp64
     re-check of the best k+extra, ties by id.  Setup, not timed."""
     torch.backends.cuda.matmul.allow_tf32 = False
-    xn = (X.double() ** 2).sum(1).float()
+    xn = torch.empty(X.shape[0], dtype=torch.float32, device=X.device)
+    for r0 in range(0, X.shape[0], 65536):  # row norms without an N x D fp64 temporary
+        xn[r0:r0 + 65536] = (X[r0:r0 + 65536].double() ** 2).sum(1).float()
     out = torch.empty((Qd.shape[0], k), dtype=torch.int64, device=X.device)
     for q0 in range(0, Qd.shape[0], 256):
         q = Qd[q0:q0 + 256]
@@ -135,6 +137,7 @@ def ground_truth(X, Qd, k, extra=32):
         dd, cand = dd.gather(1, o), cand.gather(1, o)
         o = torch.argsort(dd, dim=1, stable=True)
         out[q0:q0 + 256] = cand.gather(1, o)[:, :k]
+    torch.cuda.empty_cache()
     return out
 
 
