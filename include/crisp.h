@@ -50,7 +50,8 @@ typedef enum {
     CRISP_OPTIMIZED = 1   /* rank-weighted scoring, Hamming order, patience */
 } crisp_mode;
 
-typedef struct crisp_index crisp_index; /* opaque; owns HBM */
+typedef struct crisp_index crisp_index;     /* opaque; owns HBM */
+typedef struct crisp_session crisp_session; /* opaque; one phased shard search (owns its scratch) */
 
 typedef struct {
     int32_t M;                 /* subspaces (required, no paper default) */
@@ -177,6 +178,27 @@ crisp_status crisp_search_shard_async(const crisp_index *idx, const float *queri
  * each, ids < 0 are padding) -> Q x k (a6). */
 crisp_status crisp_merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32_t k, double *out_d64,
                               float *out_d, int64_t *out_ids, void *stream);
+
+/* Phased shard search with the EXACT global underflow fallback (P:L449 applied
+ * to the whole point-sharded dataset).  All pointers are device
+ * pointers on `stream`; the caller runs the collectives in between:
+ *   1. begin: a0..a4 without the fallback; local_counts[q] = local |C_q|.
+ *   2. caller: all-reduce(SUM) local_counts -> global_counts.
+ *   3. hist: for queries with global |C_q| < k, local_hist[q][v] = number of
+ *      touched local ids with score v (v = 0..2M; Q x (2M+2) int32).
+ *   4. caller: all-gather local_hist over the G ranks -> all_hist (G x Q x (2M+2)).
+ *   5. finish: fallback queries take the global top-k touched ids by
+ *      (V desc, gid asc) -- this rank keeps ids with V > V* and its share of the
+ *      V == V* quota in rank (= global id) order -- then a5 verification;
+ *      out_ids / out_dist64 are this shard's Q x k top-k by (d, gid).
+ * The batch is processed as one chunk.  free releases the session. */
+crisp_status crisp_shard_search_begin(const crisp_index *idx, const float *queries, int64_t Q, int32_t k,
+                                      crisp_mode mode, int32_t *local_counts, crisp_session **out, void *stream);
+crisp_status crisp_shard_search_hist(crisp_session *s, const int32_t *global_counts, int32_t *local_hist,
+                                     void *stream);
+crisp_status crisp_shard_search_finish(crisp_session *s, const int32_t *global_counts, const int32_t *all_hist,
+                                       int32_t G, int32_t rank, int64_t *out_ids, double *out_dist64, void *stream);
+void crisp_shard_search_free(crisp_session *s);
 
 /* Search with stage outputs copied to host buffers (parity / tracing). */
 crisp_status crisp_search_trace(const crisp_index *idx, const float *queries, int64_t Q, int32_t k, crisp_mode mode,

@@ -84,7 +84,7 @@ def _declare(L):
     L.or_half_sorted.argtypes = [vp, vp, i32, i32, vp, vp]
     L.or_multisequence.argtypes = [vp, vp, vp, vp, i32, vp, i64, i32, vp, vp, vp]
     L.or_multisequence.restype = i32
-    L.or_search.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i32, i32,
+    L.or_search.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, vp,
                             vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.or_max_threads.restype = i32
     L.or_bruteforce_knn.argtypes = [vp, i64, i32, vp, i64, i32, vp, vp]
@@ -368,8 +368,11 @@ def build(X, M: int, K: int = 50, tau_cev: float = 0.85, rotation_mode: int = -1
 
 
 def search(index, queries, k: int, mode: int, budget: int, tau: int, patience_factor: int = 40,
-           trace: bool = False, nthreads: int = 0):
+           trace: bool = False, nthreads: int = 0, fallback: bool = True, ext_cand=None, ext_n=None):
     """Alg. 1 for a batch of queries.  budget/tau are the exact integers (O1).
+    fallback=False skips the underflow fallback (first phase of the sharded
+    protocol); ext_cand/ext_n (Q x N, Q; n < 0 = not given) replace C_q by a
+    given ascending candidate list (its final phase).
     Returns (ids int64 QxK global, d64 QxK, trace dict or None)."""
     ix = index
     q = np.ascontiguousarray(queries, dtype=np.float32)
@@ -390,9 +393,11 @@ def search(index, queries, k: int, mode: int, budget: int, tau: int, patience_fa
     T = (lambda key: _p(t[key])) if t is not None else (lambda key: None)
     patience = patience_factor * k if patience_factor > 0 else 0
     gsize = np.ascontiguousarray(ix["gsize"], dtype=np.int64)
+    ec = np.ascontiguousarray(ext_cand, dtype=np.int32) if ext_cand is not None else None
+    en = np.ascontiguousarray(ext_n, dtype=np.int64) if ext_n is not None else None
     lib().or_search(N, ix["gid_base"], ix["Dp"], M, K, ix["dh"], _p(ix["X"]),
                     _p(ix["R"]) if ix["R"] is not None else None, _p(ix["cb"]), _p(ix["off"]), _p(ix["ids"]),
-                    _p(ix["codes"]), _p(gsize), budget, tau, patience,
+                    _p(ix["codes"]), _p(gsize), budget, tau, patience, 0 if fallback else 1, _p(ec), _p(en),
                     _p(qp), Q, k, mode, nthreads, _p(out_ids), _p(out_d),
                     T("act_len"), T("act_cell"), T("act_w"), T("retrieved"), T("V"), T("cand_n"), T("cand"),
                     T("order"), T("n_verified"), T("fallback"), T("qrot"))

@@ -670,6 +670,9 @@ typedef struct {
     int64_t budget;       /* B ids per subspace (exact integer, O1) */
     int32_t tau;          /* integer threshold (exact, O1) */
     int32_t patience;     /* P = factor*k, 0 = disabled */
+    int32_t fb_mode;      /* 0: underflow fallback; 1: none (sharded protocol, first phase) */
+    const int32_t *ext_cand; /* Q x N external candidate lists (ascending local ids) or NULL */
+    const int64_t *ext_n;    /* Q: length of the external list, < 0 = compute C normally */
 } or_index;
 
 typedef struct {
@@ -734,9 +737,15 @@ static void search_one(const or_index *ix, const float *q_in, int32_t k, int32_t
     /* a4: C = {x : V[x] >= tau} in ascending id (Alg. 1 l.18) */
     int32_t *C = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1));
     int64_t nc = 0;
-    for (int64_t x = 0; x < N; x++) if (V[x] >= ix->tau) C[nc++] = (int32_t)x;
     int32_t fb = 0;
-    if (nc < k) {
+    const int ext = ix->ext_n && ix->ext_n[qi] >= 0;
+    if (ext) {  /* candidate set decided outside (sharded global fallback) */
+        nc = ix->ext_n[qi];
+        memcpy(C, ix->ext_cand + qi * N, sizeof(int32_t) * (size_t)nc);
+    } else {
+        for (int64_t x = 0; x < N; x++) if (V[x] >= ix->tau) C[nc++] = (int32_t)x;
+    }
+    if (!ext && ix->fb_mode == 0 && nc < k) {
         /* fallback (Z8): first min(k,|T|) touched ids by (V desc, id asc),
          * then restated in ascending id */
         fb = 1;
@@ -820,13 +829,15 @@ static void search_one(const or_index *ix, const float *q_in, int32_t k, int32_t
 void or_search(int64_t N, int64_t gid_base, int32_t D, int32_t M, int32_t K, int32_t dh,
                const float *X, const float *R, const float *cb, const int64_t *off, const int32_t *ids,
                const uint64_t *codes, const int64_t *gsize, int64_t budget, int32_t tau, int32_t patience,
+               int32_t fb_mode, const int32_t *ext_cand, const int64_t *ext_n,
                const float *queries, int64_t Q, int32_t k, int32_t mode, int32_t nthreads,
                int64_t *out_ids, double *out_d,
                int32_t *t_act_len, int32_t *t_act_cell, int32_t *t_act_w, int64_t *t_retrieved,
                uint16_t *t_V, int64_t *t_cand_n, int32_t *t_cand, int32_t *t_order, int64_t *t_nver,
                int32_t *t_fallback, float *t_qrot)
 {
-    or_index ix = {N, gid_base, D, M, K, dh, X, R, cb, off, ids, codes, gsize, budget, tau, patience};
+    or_index ix = {N, gid_base, D, M, K, dh, X, R, cb, off, ids, codes, gsize, budget, tau, patience,
+                   fb_mode, ext_cand, ext_n};
     or_trace tr = {t_act_len, t_act_cell, t_act_w, t_retrieved, t_V, t_cand_n, t_cand, t_order, t_nver,
                    t_fallback, t_qrot};
 #ifdef _OPENMP

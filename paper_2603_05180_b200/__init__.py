@@ -63,6 +63,7 @@ ABI_SYMBOLS = (
     "crisp_set_global_cell_sizes", "crisp_set_search_params", "crisp_index_info", "crisp_search",
     "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
     "crisp_set_stage_timing", "crisp_stage_times", "crisp_search_counters", "crisp_free", "crisp_last_error", "crisp_version",
+    "crisp_shard_search_begin", "crisp_shard_search_hist", "crisp_shard_search_finish", "crisp_shard_search_free",
 )
 
 _lib = None
@@ -94,6 +95,11 @@ def lib():
         L.crisp_set_stage_timing.argtypes = [i32]
         L.crisp_stage_times.argtypes = [vp, i32, i32]
         L.crisp_search_counters.argtypes = [vp, i32, i32]
+        L.crisp_shard_search_begin.argtypes = [vp, vp, i64, i32, i32, vp, P(vp), vp]
+        L.crisp_shard_search_hist.argtypes = [vp, vp, vp, vp]
+        L.crisp_shard_search_finish.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp]
+        L.crisp_shard_search_free.argtypes = [vp]
+        L.crisp_shard_search_free.restype = None
         L.crisp_free.argtypes = [vp]
         L.crisp_free.restype = None
         L.crisp_last_error.restype = C.c_char_p
@@ -232,6 +238,28 @@ class Index:
     def search_shard_async(self, q_dev, k: int, mode: int, ids_dev, d64_dev, stream_ptr: int = 0):
         _check(lib().crisp_search_shard_async(self._h, _ptr(q_dev), int(q_dev.shape[0]), k, mode, _ptr(ids_dev),
                                               _ptr(d64_dev), C.c_void_p(stream_ptr)))
+
+    # ------------------------------------------------- phased shard search
+    def shard_begin(self, q_dev, k: int, mode: int, local_counts_dev, stream_ptr: int = 0):
+        """crisp_shard_search_begin -> session handle (see include/crisp.h)."""
+        ss = C.c_void_p()
+        _check(lib().crisp_shard_search_begin(self._h, _ptr(q_dev), int(q_dev.shape[0]), k, mode,
+                                              _ptr(local_counts_dev), C.byref(ss), C.c_void_p(stream_ptr)))
+        return ss
+
+    @staticmethod
+    def shard_hist(ss, global_counts_dev, local_hist_dev, stream_ptr: int = 0):
+        _check(lib().crisp_shard_search_hist(ss, _ptr(global_counts_dev), _ptr(local_hist_dev),
+                                             C.c_void_p(stream_ptr)))
+
+    @staticmethod
+    def shard_finish(ss, global_counts_dev, all_hist_dev, G: int, rank: int, ids_dev, d64_dev, stream_ptr: int = 0):
+        _check(lib().crisp_shard_search_finish(ss, _ptr(global_counts_dev), _ptr(all_hist_dev), G, rank,
+                                               _ptr(ids_dev), _ptr(d64_dev), C.c_void_p(stream_ptr)))
+
+    @staticmethod
+    def shard_free(ss):
+        lib().crisp_shard_search_free(ss)
 
     def trace(self, queries, k: int, mode: int = GUARANTEED):
         """crisp_search_trace: stage outputs as numpy arrays."""

@@ -405,6 +405,47 @@ crisp_status crisp_merge_topk(const double *d, const int64_t *ids, int32_t G, in
     }
 }
 
+crisp_status crisp_shard_search_begin(const crisp_index *ix, const float *queries, int64_t Q, int32_t k,
+                                      crisp_mode mode, int32_t *local_counts, crisp_session **out, void *stream) {
+    try {
+        CRISP_CHECK(ix && queries && local_counts && out, "NULL argument");
+        CRISP_CHECK(Q >= 1, "Q must be >= 1");
+        CRISP_CHECK(k >= 1 && k <= MAX_TOPK && k <= ix->N_global, "bad k");
+        CRISP_CHECK(mode == CRISP_GUARANTEED || mode == CRISP_OPTIMIZED, "bad mode");
+        CRISP_CHECK(is_device_ptr(queries) && is_device_ptr(local_counts), "device pointers required");
+        CRISP_CUDA(cudaSetDevice(ix->device));
+        *out = session_begin(ix, queries, Q, k, (int)mode, local_counts, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_shard_search_hist(crisp_session *s, const int32_t *global_counts, int32_t *local_hist,
+                                     void *stream) {
+    try {
+        CRISP_CHECK(s && global_counts && local_hist, "NULL argument");
+        session_hist(s, global_counts, local_hist, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_shard_search_finish(crisp_session *s, const int32_t *global_counts, const int32_t *all_hist,
+                                       int32_t G, int32_t rank, int64_t *out_ids, double *out_dist64, void *stream) {
+    try {
+        CRISP_CHECK(s && global_counts && all_hist && out_ids && out_dist64, "NULL argument");
+        CRISP_CHECK(G >= 1 && rank >= 0 && rank < G, "bad G / rank");
+        session_finish(s, global_counts, all_hist, G, rank, out_ids, out_dist64, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+void crisp_shard_search_free(crisp_session *s) { session_free(s); }
+
 crisp_status crisp_export(const crisp_index *ix, crisp_export_t *o) {
     try {
         CRISP_CHECK(ix && o, "NULL argument");

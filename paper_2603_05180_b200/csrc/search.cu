@@ -421,8 +421,95 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
 // ---------------------------------------------------------------------------
 // a4 fallback (Z8): |C| < k -> the first min(k,|T|) touched ids by
 // (V desc, id asc), restated in ascending id.  Rare; one CTA per query,
-// counting every block twice (histogram of V, then selection).
+// counting every block twice (histogram of V, then selection).  For a sharded
+// index the decision (global |C|), the histogram (summed over shards) and the
+// quota of ids with V == V* (given to shards in global-id order) are global.
 // ---------------------------------------------------------------------------
+__device__ void fb_hist_pass(CountSmem &S, unsigned char *cnt8, int BS, int64_t q, int Etot,
+                             const uint32_t *__restrict__ act, int M, int KK, const int32_t *__restrict__ off2, int NB,
+                             const int32_t *__restrict__ ids, int64_t N, int *hist) {
+    const int tid = threadIdx.x;
+    int s0r[CS_EPT], s1r[CS_EPT];
+    for (int b = 0; b < NB; b++) {
+        prefetch_first(S, Etot, off2, NB, b, s0r, s1r);
+        zero_counters(cnt8, BS);
+        __syncthreads();
+        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r, 0, nullptr);
+        for (int j = tid; j < BS; j += THREADS)
+            if (cnt8[j]) atomicAdd(&hist[cnt8[j]], 1);
+        __syncthreads();
+    }
+}
+
+// selects ids with V > vstar and the first `quota` ids with V == vstar, in
+// ascending id, into outp; returns the count (all threads)
+__device__ int fb_select_pass(CountSmem &S, unsigned char *cnt8, int BS, int64_t q, int Etot,
+                              const uint32_t *__restrict__ act, int M, int KK, const int32_t *__restrict__ off2,
+                              int NB, const int32_t *__restrict__ ids, int64_t N, int vstar, int quota, int32_t *outp,
+                              int *s_eqbase, int *s_n) {
+    const int tid = threadIdx.x;
+    int s0r[CS_EPT], s1r[CS_EPT];
+    if (tid == 0) {
+        *s_eqbase = 0;
+        *s_n = 0;
+    }
+    __syncthreads();
+    for (int b = 0; b < NB; b++) {
+        prefetch_first(S, Etot, off2, NB, b, s0r, s1r);
+        zero_counters(cnt8, BS);
+        __syncthreads();
+        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r, 0, nullptr);
+        for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
+            const int j = j0 + tid * 16;
+            unsigned char vb[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) vb[i] = (j + i < BS) ? cnt8[j + i] : 0;
+            int ceq = 0;
+#pragma unroll
+            for (int i = 0; i < 16; i++) ceq += vb[i] == vstar;
+            int eoff, etot;
+            cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(ceq, eoff, etot);
+            __syncthreads();
+            bool sel[16];
+            int cs = 0, er = *s_eqbase + eoff;
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                sel[i] = vb[i] > vstar || (vb[i] == vstar && vb[i] > 0 && er < quota);
+                if (vb[i] == vstar) er++;
+                cs += sel[i];
+            }
+            int soff, stot;
+            cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(cs, soff, stot);
+            int o = *s_n + soff;
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if (sel[i]) outp[o++] = b * BS + j + i;
+            __syncthreads();
+            if (tid == 0) {
+                *s_eqbase += etot;
+                *s_n += stot;
+            }
+            __syncthreads();
+        }
+    }
+    return *s_n;
+}
+
+// V* and the quota of ids with V == V* from a histogram of V over the touched set
+__device__ __forceinline__ void fb_threshold(const int *hist, int M, int k, int *vstar, int *quota) {
+    int acc = 0;
+    *vstar = 1;
+    *quota = hist[1];
+    for (int v = 2 * M; v >= 1; v--) {
+        if (acc + hist[v] >= k) {
+            *vstar = v;
+            *quota = k - acc;
+            return;
+        }
+        acc += hist[v];
+    }
+}
+
 __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict__ act,
                                                        const int32_t *__restrict__ act_len, int M, int KK,
                                                        const int32_t *__restrict__ off2, int NB,
@@ -449,79 +536,93 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
         return;
     }
     const int Etot = count_setup(S, q, act, act_len, M, KK);
-    int s0r[CS_EPT], s1r[CS_EPT];
-    // pass 1: histogram of V over the touched set
-    for (int b = 0; b < NB; b++) {
-        prefetch_first(S, Etot, off2, NB, b, s0r, s1r);
-        zero_counters(cnt8, BS);
-        __syncthreads();
-        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r, 0, nullptr);
-        for (int j = tid; j < BS; j += THREADS)
-            if (cnt8[j]) atomicAdd(&hist[cnt8[j]], 1);
-        __syncthreads();
-    }
-    if (tid == 0) {
-        int acc = 0, vstar = 1, quota = hist[1];
-        for (int v = 2 * M; v >= 1; v--) {
-            if (acc + hist[v] >= k) {
-                vstar = v;
-                quota = k - acc;
-                break;
-            }
-            acc += hist[v];
-        }
-        s_vstar = vstar;
-        s_quota = quota;
-        s_eqbase = 0;
-        s_n = 0;
-    }
+    fb_hist_pass(S, cnt8, BS, q, Etot, act, M, KK, off2, NB, ids, N, hist);
+    if (tid == 0) fb_threshold(hist, M, k, &s_vstar, &s_quota);
     __syncthreads();
-    const int vstar = s_vstar, quota = s_quota;
-    int32_t *outp = pool + q * CAPQ;
-    // pass 2: ids with V > V*, and the first `quota` ids with V == V*, ascending
-    for (int b = 0; b < NB; b++) {
-        prefetch_first(S, Etot, off2, NB, b, s0r, s1r);
-        zero_counters(cnt8, BS);
-        __syncthreads();
-        count_one_block(S, cnt8, BS, q, b, -1, Etot, act, M, KK, off2, NB, ids, N, s0r, s1r, 0, nullptr);
-        for (int j0 = 0; j0 < BS; j0 += THREADS * 16) {
-            const int j = j0 + tid * 16;
-            unsigned char vb[16];
-#pragma unroll
-            for (int i = 0; i < 16; i++) vb[i] = (j + i < BS) ? cnt8[j + i] : 0;
-            int ceq = 0;
-#pragma unroll
-            for (int i = 0; i < 16; i++) ceq += vb[i] == vstar;
-            int eoff, etot;
-            cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(ceq, eoff, etot);
-            __syncthreads();
-            bool sel[16];
-            int cs = 0, er = s_eqbase + eoff;
-#pragma unroll
-            for (int i = 0; i < 16; i++) {
-                sel[i] = vb[i] > vstar || (vb[i] == vstar && vb[i] > 0 && er < quota);
-                if (vb[i] == vstar) er++;
-                cs += sel[i];
-            }
-            int soff, stot;
-            cub::BlockScan<int, THREADS>(S.scan).ExclusiveSum(cs, soff, stot);
-            int o = s_n + soff;
-#pragma unroll
-            for (int i = 0; i < 16; i++)
-                if (sel[i]) outp[o++] = b * BS + j + i;
-            __syncthreads();
-            if (tid == 0) {
-                s_eqbase += etot;
-                s_n += stot;
-            }
-            __syncthreads();
-        }
-    }
+    const int n = fb_select_pass(S, cnt8, BS, q, Etot, act, M, KK, off2, NB, ids, N, s_vstar, s_quota, pool + q * CAPQ,
+                                 &s_eqbase, &s_n);
     for (int b = tid; b < NB; b += THREADS) {
-        ncand[q * NB + b] = (b == 0) ? s_n : 0;
+        ncand[q * NB + b] = (b == 0) ? n : 0;
         cbase[q * NB + b] = 0;
     }
     if (tid == 0) fbflag[q] = 1;
+}
+
+// sharded: local histogram of V for queries whose GLOBAL |C| < k (zeros otherwise)
+__global__ void __launch_bounds__(THREADS) k_fb_hist(const uint32_t *__restrict__ act,
+                                                      const int32_t *__restrict__ act_len, int M, int KK,
+                                                      const int32_t *__restrict__ off2, int NB,
+                                                      const int32_t *__restrict__ ids, int64_t N, int BS, int k,
+                                                      const int32_t *__restrict__ gcount, int32_t *__restrict__ lhist) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    unsigned char *cnt8 = smraw;
+    CountSmem &S = *(CountSmem *)(smraw + BS + BS / 8);
+    __shared__ int hist[2 * MAX_M + 2];
+    const int64_t q = blockIdx.x;
+    const int HB = 2 * M + 2;
+    for (int i = threadIdx.x; i < 2 * MAX_M + 2; i += THREADS) hist[i] = 0;
+    __syncthreads();
+    if (gcount[q] < k) {
+        const int Etot = count_setup(S, q, act, act_len, M, KK);
+        fb_hist_pass(S, cnt8, BS, q, Etot, act, M, KK, off2, NB, ids, N, hist);
+    }
+    for (int i = threadIdx.x; i < HB; i += THREADS) lhist[q * HB + i] = hist[i];
+}
+
+// sharded: selection with the global V*/quota; this shard's share of the
+// V == V* quota follows the global id order (shard g owns [g*N/G, (g+1)*N/G))
+__global__ void __launch_bounds__(THREADS) k_fb_select(const uint32_t *__restrict__ act,
+                                                        const int32_t *__restrict__ act_len, int M, int KK,
+                                                        const int32_t *__restrict__ off2, int NB,
+                                                        const int32_t *__restrict__ ids, int64_t N, int BS, int k,
+                                                        const int32_t *__restrict__ gcount,
+                                                        const int32_t *__restrict__ allhist, int G, int rank, int64_t Q,
+                                                        int32_t *__restrict__ pool, int64_t CAPQ,
+                                                        int32_t *__restrict__ cbase, int32_t *__restrict__ ncand,
+                                                        int32_t *__restrict__ fbflag) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    unsigned char *cnt8 = smraw;
+    CountSmem &S = *(CountSmem *)(smraw + BS + BS / 8);
+    __shared__ int hist[2 * MAX_M + 2];
+    __shared__ int s_vstar, s_quota, s_eqbase, s_n;
+    const int64_t q = blockIdx.x;
+    const int tid = threadIdx.x, HB = 2 * M + 2;
+    if (gcount[q] >= k) {
+        if (tid == 0) fbflag[q] = 0;
+        return;
+    }
+    for (int i = tid; i < HB; i += THREADS) {
+        int t = 0;
+        for (int g = 0; g < G; g++) t += allhist[((int64_t)g * Q + q) * HB + i];
+        hist[i] = t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int vstar, quota;
+        fb_threshold(hist, M, k, &vstar, &quota);
+        int before = 0;
+        for (int g = 0; g < rank; g++) before += allhist[((int64_t)g * Q + q) * HB + vstar];
+        const int mine = allhist[((int64_t)rank * Q + q) * HB + vstar];
+        s_vstar = vstar;
+        s_quota = max(0, min(mine, quota - before));
+    }
+    __syncthreads();
+    const int Etot = count_setup(S, q, act, act_len, M, KK);
+    const int n = fb_select_pass(S, cnt8, BS, q, Etot, act, M, KK, off2, NB, ids, N, s_vstar, s_quota, pool + q * CAPQ,
+                                 &s_eqbase, &s_n);
+    for (int b = tid; b < NB; b += THREADS) {
+        ncand[q * NB + b] = (b == 0) ? n : 0;
+        cbase[q * NB + b] = 0;
+    }
+    if (tid == 0) fbflag[q] = 1;
+}
+
+__global__ void k_local_counts(const int32_t *__restrict__ ncand, int NB, int64_t Qc, int32_t *__restrict__ out) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Qc) return;
+    int t = 0;
+    for (int b = 0; b < NB; b++) t += ncand[q * NB + b];
+    out[q] = t;
 }
 
 // ---------------------------------------------------------------------------
@@ -1228,6 +1329,8 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_fb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1237,252 +1340,320 @@ static void set_attrs() {
     done = true;
 }
 
-// One attempt over all queries with candidate capacity CAPQ per query; returns
-// false (and the capacity needed) if some query's candidate set overflowed.
-static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
-                        cudaStream_t s, const crisp_trace_t *tr, int64_t CAPQ, int64_t *need_out) {
-    const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch, Dp = ix->Dp;
-    const int64_t N = ix->N;
-    const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));       // CTAs per query in the row kernels
-    const int HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 4));     // CTAs per query in k_hamming
-    const int S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
-    const int R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
-    const int BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 8)));  // id blocks per count CTA
-    // per-query workspace bytes -> query chunk
-    int64_t perq = (int64_t)pitch * 4 * 2 + (int64_t)M * KK * 4 + (int64_t)M * 12 + CAPQ * 4 + (int64_t)NB * 8 + 64;
-    if (mode == 0) perq += (int64_t)S * k * 16;
-    else perq += CAPQ * 6 + (int64_t)(Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
-    if (tr && tr->V) perq += N;
-    const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : (16LL << 30);
-    int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
-    Qc = std::min<int64_t>(Qc, 65535);
-    DevBuf wb(s);
-    float *qpad = wb.alloc<float>((size_t)Qc * pitch);
-    float *qrot = ix->rotated ? wb.alloc<float>((size_t)Qc * pitch) : qpad;
-    uint32_t *act = wb.alloc<uint32_t>((size_t)Qc * M * KK);
-    int32_t *act_len = wb.alloc<int32_t>((size_t)Qc * M);
-    int64_t *retr = wb.alloc<int64_t>((size_t)Qc * M);
-    int32_t *pool = wb.alloc<int32_t>((size_t)Qc * CAPQ);
-    int32_t *ncand = wb.alloc<int32_t>((size_t)Qc * NB);
-    int32_t *cbase = wb.alloc<int32_t>((size_t)Qc * NB);
-    int32_t *cursor = wb.alloc<int32_t>((size_t)Qc + 1);  // [Qc] = overflow need
-    int32_t *need = cursor + Qc;
-    int32_t *fb = wb.alloc<int32_t>((size_t)Qc);
-    double *part_d = nullptr, *dbuf = nullptr;
+// ---------------------------------------------------------------------------
+// Work buffers of one query chunk and the stages that run on them.
+// ---------------------------------------------------------------------------
+struct Work {
+    const crisp_index *ix;
+    int k, mode;
+    int64_t Qc, CAPQ;
+    int S, HS, S0, R0, BPC;
+    DevBuf buf;
+    float *qpad = nullptr, *qrot = nullptr;
+    uint32_t *act = nullptr;
+    int32_t *act_len = nullptr;
+    int64_t *retr = nullptr;
+    int32_t *pool = nullptr, *ncand = nullptr, *cbase = nullptr, *cursor = nullptr, *need = nullptr, *fb = nullptr;
+    double *part_d = nullptr, *dbuf = nullptr, *d64tmp = nullptr;
     int64_t *part_i = nullptr, *nver = nullptr;
     int32_t *cbuf = nullptr, *ghist = nullptr, *totals = nullptr;
     uint16_t *hbuf = nullptr;
     PatState pst{};
-    if (mode == 0) {
-        part_d = wb.alloc<double>((size_t)Qc * S * k);
-        part_i = wb.alloc<int64_t>((size_t)Qc * S * k);
-    } else {
-        cbuf = wb.alloc<int32_t>((size_t)Qc * CAPQ);
-        hbuf = wb.alloc<uint16_t>((size_t)Qc * CAPQ);
-        ghist = wb.alloc<int32_t>((size_t)Qc * (Dp + 1));
-        totals = wb.alloc<int32_t>((size_t)Qc);
-        dbuf = wb.alloc<double>((size_t)Qc * S0);
-        pst.Td = wb.alloc<double>((size_t)Qc * k);
-        pst.Ti = wb.alloc<int64_t>((size_t)Qc * k);
-        pst.cnt = wb.alloc<int32_t>((size_t)Qc * 3);
-        pst.pat = pst.cnt + Qc;
-        pst.done = pst.pat + Qc;
-        pst.nver = wb.alloc<int64_t>((size_t)Qc);
-        nver = pst.nver;
+    uint8_t *traceV = nullptr;
+    int probe_gs, probe_smem, count_smem, rx_smem, ham_smem, hsort_smem, vr_smem, scan_smem, pat_smem;
+
+    static int64_t per_query_bytes(const crisp_index *ix, int k, int mode, int64_t CAPQ, bool traceV) {
+        const int KK = ix->K * ix->K;
+        const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));
+        const int S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));
+        int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 4 + (int64_t)ix->M * 12 + CAPQ * 4 +
+                       (int64_t)ix->NB * 8 + 64;
+        if (mode == 0) perq += (int64_t)S * k * 16;
+        else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
+        if (traceV) perq += ix->N;
+        return perq;
     }
-    uint8_t *traceV = (tr && tr->V) ? wb.alloc<uint8_t>((size_t)Qc * N) : nullptr;
-    double *d64tmp = out.d64 ? nullptr : wb.alloc<double>((size_t)Qc * k);
 
-    const int probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
-    const int probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
-    const int count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
-    const int rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NB + 1) * 4;
-    const int ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NB + 1) * 4;
-    const int hsort_smem = (Dp + 1) * 4;
-    const int vr_smem = pitch * 8;
-    const int scan_smem = WARPS * k * 16;
-    const int pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16;
-    set_attrs();
-    CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
-                    pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
-                "shared-memory footprint too large for this (D, K, k)");
+    Work(const crisp_index *ix_, int k_, int mode_, int64_t Qc_, int64_t CAPQ_, bool want_traceV, bool want_d64tmp,
+         cudaStream_t s)
+        : ix(ix_), k(k_), mode(mode_), Qc(Qc_), CAPQ(CAPQ_), buf(s) {
+        const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch, Dp = ix->Dp;
+        S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));       // CTAs per query in the row kernels
+        HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 4));     // CTAs per query in k_hamming
+        S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
+        R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
+        BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 8)));  // id blocks per count CTA
+        qpad = buf.alloc<float>((size_t)Qc * pitch);
+        qrot = ix->rotated ? buf.alloc<float>((size_t)Qc * pitch) : qpad;
+        act = buf.alloc<uint32_t>((size_t)Qc * M * KK);
+        act_len = buf.alloc<int32_t>((size_t)Qc * M);
+        retr = buf.alloc<int64_t>((size_t)Qc * M);
+        pool = buf.alloc<int32_t>((size_t)Qc * CAPQ);
+        ncand = buf.alloc<int32_t>((size_t)Qc * NB);
+        cbase = buf.alloc<int32_t>((size_t)Qc * NB);
+        cursor = buf.alloc<int32_t>((size_t)Qc + 1);  // [Qc] = overflow need
+        need = cursor + Qc;
+        fb = buf.alloc<int32_t>((size_t)Qc);
+        if (mode == 0) {
+            part_d = buf.alloc<double>((size_t)Qc * S * k);
+            part_i = buf.alloc<int64_t>((size_t)Qc * S * k);
+        } else {
+            cbuf = buf.alloc<int32_t>((size_t)Qc * CAPQ);
+            hbuf = buf.alloc<uint16_t>((size_t)Qc * CAPQ);
+            ghist = buf.alloc<int32_t>((size_t)Qc * (Dp + 1));
+            totals = buf.alloc<int32_t>((size_t)Qc);
+            dbuf = buf.alloc<double>((size_t)Qc * S0);
+            pst.Td = buf.alloc<double>((size_t)Qc * k);
+            pst.Ti = buf.alloc<int64_t>((size_t)Qc * k);
+            pst.cnt = buf.alloc<int32_t>((size_t)Qc * 3);
+            pst.pat = pst.cnt + Qc;
+            pst.done = pst.pat + Qc;
+            pst.nver = buf.alloc<int64_t>((size_t)Qc);
+            nver = pst.nver;
+        }
+        if (want_traceV) traceV = buf.alloc<uint8_t>((size_t)Qc * ix->N);
+        if (want_d64tmp) d64tmp = buf.alloc<double>((size_t)Qc * k);
+        probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
+        probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
+        count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
+        rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NB + 1) * 4;
+        ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NB + 1) * 4;
+        hsort_smem = (Dp + 1) * 4;
+        vr_smem = pitch * 8;
+        scan_smem = WARPS * k * 16;
+        pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16;
+        set_attrs();
+        CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
+                        pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
+                    "shared-memory footprint too large for this (D, K, k)");
+    }
+};
 
-    const int wk = (mode == 1) ? k : 0;
-    const int P = (mode == 1 && ix->patience_factor > 0) ? ix->patience_factor * k : 0;
-    std::vector<int32_t> h_pool, h_ncand, h_cbase;
+// a0, a1+a2, a3+a4 (count/select) for queries [0, qn) of the chunk
+static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s) {
+    const crisp_index *ix = w.ix;
+    const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, pitch = ix->pitch;
+    {
+        StageScope st(s, 0);
+        k_prep_queries<<<nblk(qn * pitch, 256), 256, 0, s>>>(queries, qn, ix->D, pitch, w.qpad);
+        CRISP_LAUNCH();
+        g_launches++;
+        if (ix->rotated) {
+            rotate_rows_f64(w.qpad, qn, ix->Dp, pitch, ix->R, w.qrot, pitch, s);
+            g_launches++;
+        }
+    }
+    {
+        StageScope st(s, 1);
+        dim3 g(nblk(qn, WARPS), M);
+        k_probe<<<g, THREADS, w.probe_smem, s>>>(w.qrot, pitch, qn, ix->cb, M, K, ix->dh, ix->gsize, w.probe_gs,
+                                                 ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr);
+        CRISP_LAUNCH();
+        g_launches++;
+    }
+    {
+        StageScope st(s, 2);
+        CRISP_CUDA(cudaMemsetAsync(w.cursor, 0, (size_t)(w.Qc + 1) * 4, s));
+        dim3 g(nblk(NB, w.BPC), (unsigned)qn);
+        k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N, ix->BS,
+                                                        w.BPC, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase, w.ncand,
+                                                        w.need, w.traceV);
+        CRISP_LAUNCH();
+        g_launches++;
+    }
+}
+
+static int32_t read_need(Work &w, cudaStream_t s) {
+    int32_t h = 0;
+    CRISP_CUDA(cudaMemcpyAsync(&h, w.need, 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+static void run_fallback_local(Work &w, int64_t qn, cudaStream_t s) {
+    const crisp_index *ix = w.ix;
+    StageScope st(s, 3);
+    k_fallback<<<(unsigned)qn, THREADS, w.count_smem, s>>>(w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB,
+                                                           ix->ids, ix->N, ix->BS, w.k, w.pool, w.CAPQ, w.cbase,
+                                                           w.ncand, w.fb);
+    CRISP_LAUNCH();
+    g_launches++;
+}
+
+// a4 (phi=1 Hamming order) + a5 for queries [0, qn) of the chunk -> outputs
+static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64, cudaStream_t s) {
+    const crisp_index *ix = w.ix;
+    const int NB = ix->NB, pitch = ix->pitch, Dp = ix->Dp, k = w.k;
+    if (!od64) od64 = w.d64tmp;
+    if (w.mode == 0) {
+        {
+            StageScope st(s, 4);
+            dim3 g(w.S, (unsigned)qn);
+            k_rerank_exact<<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ, w.cbase,
+                                                         w.ncand, NB, k, w.part_d, w.part_i);
+            CRISP_LAUNCH();
+            g_launches++;
+        }
+        {
+            StageScope st(s, 5);
+            k_merge_lists<<<(unsigned)qn, THREADS, 0, s>>>(w.part_d, w.part_i, w.S, qn, k, 0, od64, od, oi);
+            CRISP_LAUNCH();
+            g_launches++;
+        }
+        return;
+    }
+    const int P = ix->patience_factor > 0 ? ix->patience_factor * k : 0;
+    CRISP_CUDA(cudaMemsetAsync(w.ghist, 0, (size_t)qn * (Dp + 1) * 4, s));
+    CRISP_CUDA(cudaMemsetAsync(w.pst.cnt, 0, (size_t)w.Qc * 3 * 4, s));
+    {
+        StageScope st(s, 6);
+        dim3 g(w.HS, (unsigned)qn);
+        k_hamming<<<g, THREADS, w.ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->W, w.pool, w.CAPQ, w.cbase, w.ncand,
+                                                 NB, w.cbuf, w.hbuf, w.ghist);
+        CRISP_LAUNCH();
+        g_launches++;
+    }
+    {
+        StageScope st(s, 7);
+        k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, NB, Dp, w.ghist, w.cbuf, w.hbuf, w.CAPQ, w.pool, w.CAPQ,
+                                                       w.totals);
+        CRISP_LAUNCH();
+        g_launches++;
+    }
+    StageScope st(s, 4);
+    for (int r = 0; r < w.R0; r++) {
+        dim3 g(w.S, (unsigned)qn);
+        k_verify_rows<<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.pool, w.CAPQ, w.totals, w.pst.done, r,
+                                                    w.S0, w.dbuf);
+        CRISP_LAUNCH();
+        g_launches++;
+        k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.pool, w.CAPQ, ix->gid_base,
+                                                                      w.dbuf, r, w.S0, k, P, w.pst, od64, od, oi);
+        CRISP_LAUNCH();
+        g_launches++;
+    }
+    k_patience_tail<<<(unsigned)qn, THREADS, w.pat_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ,
+                                                              w.totals, w.R0 * w.S0, k, P, w.pst, od64, od, oi);
+    CRISP_LAUNCH();
+    g_launches++;
+}
+
+static void run_stats(Work &w, int64_t qn, cudaStream_t s) {
+    if (!g_timing) return;
+    const crisp_index *ix = w.ix;
+    k_stats<<<(unsigned)qn, 128, 0, s>>>(w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB, w.ncand,
+                                         w.mode == 1 ? w.nver : nullptr, w.fb, qn);
+    CRISP_LAUNCH();
+    g_launches++;
+}
+
+static void trace_candidates(Work &w, int64_t q0, int64_t qn, const crisp_trace_t *tr, cudaStream_t s) {
+    const int NB = w.ix->NB;
+    const int64_t N = w.ix->N, CAPQ = w.CAPQ;
+    std::vector<int32_t> h_pool((size_t)qn * CAPQ), h_ncand((size_t)qn * NB), h_cbase((size_t)qn * NB);
+    CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), w.pool, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaMemcpyAsync(h_ncand.data(), w.ncand, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaMemcpyAsync(h_cbase.data(), w.cbase, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaStreamSynchronize(s));
+    for (int64_t q = 0; q < qn; q++) {
+        int64_t n = 0;
+        for (int b = 0; b < NB; b++) {
+            const int c = h_ncand[q * NB + b], base = h_cbase[q * NB + b];
+            for (int j = 0; j < c; j++) {
+                const int32_t id = h_pool[q * CAPQ + base + j];
+                if (tr->cand) tr->cand[(q0 + q) * N + n] = id;
+                if (tr->order && w.mode == 0) tr->order[(q0 + q) * N + n] = id;
+                n++;
+            }
+        }
+        if (tr->cand_n) tr->cand_n[q0 + q] = n;
+        if (tr->n_verified && w.mode == 0) tr->n_verified[q0 + q] = n;
+    }
+}
+
+static void trace_rest(Work &w, int64_t q0, int64_t qn, const crisp_trace_t *tr, cudaStream_t s) {
+    const crisp_index *ix = w.ix;
+    const int M = ix->M, KK = ix->K * ix->K, NB = ix->NB, Dp = ix->Dp, pitch = ix->pitch;
+    const int64_t N = ix->N, CAPQ = w.CAPQ;
+    std::vector<int32_t> hl((size_t)qn * M), h_pool, h_ncand;
+    std::vector<uint32_t> ha;
+    std::vector<int64_t> hr((size_t)qn * M), hn;
+    CRISP_CUDA(cudaMemcpyAsync(hl.data(), w.act_len, (size_t)qn * M * 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaMemcpyAsync(hr.data(), w.retr, (size_t)qn * M * 8, cudaMemcpyDeviceToHost, s));
+    if (tr->act_cell || tr->act_w) {
+        ha.resize((size_t)qn * M * KK);
+        CRISP_CUDA(cudaMemcpyAsync(ha.data(), w.act, (size_t)qn * M * KK * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (tr->V && w.traceV)
+        CRISP_CUDA(cudaMemcpyAsync(tr->V + q0 * N, w.traceV, (size_t)qn * N, cudaMemcpyDeviceToHost, s));
+    if (tr->qrot)
+        for (int64_t q = 0; q < qn; q++)
+            CRISP_CUDA(cudaMemcpyAsync(tr->qrot + (q0 + q) * Dp, w.qrot + q * pitch, (size_t)Dp * 4,
+                                       cudaMemcpyDeviceToHost, s));
+    if (tr->fallback) CRISP_CUDA(cudaMemcpyAsync(tr->fallback + q0, w.fb, (size_t)qn * 4, cudaMemcpyDeviceToHost, s));
+    if (w.mode == 1) {
+        hn.resize(qn);
+        h_pool.resize((size_t)qn * CAPQ);
+        h_ncand.resize((size_t)qn * NB);
+        CRISP_CUDA(cudaMemcpyAsync(hn.data(), w.nver, (size_t)qn * 8, cudaMemcpyDeviceToHost, s));
+        CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), w.pool, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
+        CRISP_CUDA(cudaMemcpyAsync(h_ncand.data(), w.ncand, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
+    }
+    CRISP_CUDA(cudaStreamSynchronize(s));
+    for (int64_t q = 0; q < qn; q++) {
+        for (int m = 0; m < M; m++) {
+            const int L = hl[q * M + m];
+            if (tr->act_len) tr->act_len[(q0 + q) * M + m] = L;
+            if (tr->retrieved) tr->retrieved[(q0 + q) * M + m] = hr[q * M + m];
+            for (int r = 0; r < L && !ha.empty(); r++) {
+                const uint32_t v = ha[(q * M + m) * (int64_t)KK + r];
+                if (tr->act_cell) tr->act_cell[((q0 + q) * M + m) * (int64_t)KK + r] = (int32_t)(v & 0xffffu);
+                if (tr->act_w) tr->act_w[((q0 + q) * M + m) * (int64_t)KK + r] = (int32_t)(v >> 16);
+            }
+        }
+        if (w.mode == 1) {
+            int64_t n = 0;
+            for (int b = 0; b < NB; b++) n += h_ncand[q * NB + b];
+            if (tr->order)
+                for (int64_t i = 0; i < n; i++) tr->order[(q0 + q) * N + i] = h_pool[q * CAPQ + i];
+            if (tr->n_verified) tr->n_verified[q0 + q] = hn[q];
+        }
+    }
+}
+
+static int64_t initial_capacity(const crisp_index *ix, bool trace) {
+    const int64_t NBS = (int64_t)ix->NB * ix->BS;
+    if (trace) return NBS;
+    return std::min<int64_t>(NBS, std::max<int64_t>(4096, env_int("CRISP_CAND_CAP", 1 << 17)));
+}
+
+static int64_t grow_capacity(const crisp_index *ix, int64_t cap, int64_t need) {
+    return std::min<int64_t>((int64_t)ix->NB * ix->BS, std::max<int64_t>(cap * 2, need + need / 4));
+}
+
+// One attempt over all queries with candidate capacity CAPQ per query; returns
+// false (and the capacity needed) if some query's candidate set overflowed.
+static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
+                        cudaStream_t s, const crisp_trace_t *tr, int64_t CAPQ, int64_t *need_out) {
+    const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : (16LL << 30);
+    const int64_t perq = Work::per_query_bytes(ix, k, mode, CAPQ, tr && tr->V);
+    int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
+    Qc = std::min<int64_t>(Qc, 65535);
+    Work w(ix, k, mode, Qc, CAPQ, tr && tr->V, out.d64 == nullptr, s);
     for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
         const int64_t qn = std::min(Qc, Q - q0);
-        {
-            StageScope st(s, 0);
-            k_prep_queries<<<nblk(qn * pitch, 256), 256, 0, s>>>(queries + q0 * ix->D, qn, ix->D, pitch, qpad);
-            CRISP_LAUNCH();
-            g_launches++;
-            if (ix->rotated) {
-                rotate_rows_f64(qpad, qn, Dp, pitch, ix->R, qrot, pitch, s);
-                g_launches++;
-            }
+        run_front(w, queries + q0 * ix->D, qn, s);
+        run_fallback_local(w, qn, s);
+        const int32_t need = read_need(w, s);  // exactness guard
+        if (need > CAPQ) {
+            *need_out = need;
+            return false;
         }
-        {
-            StageScope st(s, 1);
-            dim3 g(nblk(qn, WARPS), M);
-            k_probe<<<g, THREADS, probe_smem, s>>>(qrot, pitch, qn, ix->cb, M, K, ix->dh, ix->gsize, probe_gs,
-                                                   ix->budget, wk, act, act_len, retr);
-            CRISP_LAUNCH();
-            g_launches++;
-        }
-        {
-            StageScope st(s, 2);
-            CRISP_CUDA(cudaMemsetAsync(cursor, 0, (size_t)(Qc + 1) * 4, s));
-            dim3 g(nblk(NB, BPC), (unsigned)qn);
-            k_count_select<<<g, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, BPC,
-                                                          ix->tau, pool, CAPQ, cursor, cbase, ncand, need, traceV);
-            CRISP_LAUNCH();
-            g_launches++;
-        }
-        {
-            StageScope st(s, 3);
-            k_fallback<<<(unsigned)qn, THREADS, count_smem, s>>>(act, act_len, M, KK, ix->off2, NB, ix->ids, N, BS, k,
-                                                                 pool, CAPQ, cbase, ncand, fb);
-            CRISP_LAUNCH();
-            g_launches++;
-        }
-        {
-            // exactness guard: a candidate set larger than the capacity -> redo
-            int32_t hneed = 0;
-            CRISP_CUDA(cudaMemcpyAsync(&hneed, need, 4, cudaMemcpyDeviceToHost, s));
-            CRISP_CUDA(cudaStreamSynchronize(s));
-            if (hneed > CAPQ) {
-                *need_out = hneed;
-                return false;
-            }
-        }
-        if (tr) {
-            h_pool.resize((size_t)qn * CAPQ);
-            h_ncand.resize((size_t)qn * NB);
-            h_cbase.resize((size_t)qn * NB);
-            CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), pool, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
-            CRISP_CUDA(cudaMemcpyAsync(h_ncand.data(), ncand, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
-            CRISP_CUDA(cudaMemcpyAsync(h_cbase.data(), cbase, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
-            CRISP_CUDA(cudaStreamSynchronize(s));
-            for (int64_t q = 0; q < qn; q++) {
-                int64_t n = 0;
-                for (int b = 0; b < NB; b++) {
-                    const int c = h_ncand[q * NB + b], base = h_cbase[q * NB + b];
-                    for (int j = 0; j < c; j++) {
-                        const int32_t id = h_pool[q * CAPQ + base + j];
-                        if (tr->cand) tr->cand[(q0 + q) * N + n] = id;
-                        if (tr->order && mode == 0) tr->order[(q0 + q) * N + n] = id;
-                        n++;
-                    }
-                }
-                if (tr->cand_n) tr->cand_n[q0 + q] = n;
-                if (tr->n_verified && mode == 0) tr->n_verified[q0 + q] = n;
-            }
-        }
-        int64_t *oi = out.ids + q0 * k;
-        double *od64 = out.d64 ? out.d64 + q0 * k : d64tmp;
-        float *od = out.d32 ? out.d32 + q0 * k : nullptr;
-        if (mode == 0) {
-            {
-                StageScope st(s, 4);
-                dim3 g(S, (unsigned)qn);
-                k_rerank_exact<<<g, THREADS, rx_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, CAPQ, cbase, ncand,
-                                                          NB, k, part_d, part_i);
-                CRISP_LAUNCH();
-                g_launches++;
-            }
-            {
-                StageScope st(s, 5);
-                k_merge_lists<<<(unsigned)qn, THREADS, 0, s>>>(part_d, part_i, S, qn, k, 0, od64, od, oi);
-                CRISP_LAUNCH();
-                g_launches++;
-            }
-        } else {
-            CRISP_CUDA(cudaMemsetAsync(ghist, 0, (size_t)qn * (Dp + 1) * 4, s));
-            CRISP_CUDA(cudaMemsetAsync(pst.cnt, 0, (size_t)Qc * 3 * 4, s));
-            {
-                StageScope st(s, 6);
-                dim3 g(HS, (unsigned)qn);
-                k_hamming<<<g, THREADS, ham_smem, s>>>(qrot, pitch, Dp, ix->codes, ix->W, pool, CAPQ, cbase, ncand, NB,
-                                                       cbuf, hbuf, ghist);
-                CRISP_LAUNCH();
-                g_launches++;
-            }
-            {
-                StageScope st(s, 7);
-                k_hsort<<<(unsigned)qn, 32, hsort_smem, s>>>(ncand, NB, Dp, ghist, cbuf, hbuf, CAPQ, pool, CAPQ,
-                                                             totals);
-                CRISP_LAUNCH();
-                g_launches++;
-            }
-            {
-                StageScope st(s, 4);
-                for (int r = 0; r < R0; r++) {
-                    dim3 g(S, (unsigned)qn);
-                    k_verify_rows<<<g, THREADS, vr_smem, s>>>(qrot, pitch, ix->X, pool, CAPQ, totals, pst.done, r, S0,
-                                                              dbuf);
-                    CRISP_LAUNCH();
-                    g_launches++;
-                    k_patience_scan<<<nblk(qn, WARPS), THREADS, scan_smem, s>>>(qn, totals, pool, CAPQ, ix->gid_base,
-                                                                                dbuf, r, S0, k, P, pst, od64, od, oi);
-                    CRISP_LAUNCH();
-                    g_launches++;
-                }
-                k_patience_tail<<<(unsigned)qn, THREADS, pat_smem, s>>>(qrot, pitch, ix->X, ix->gid_base, pool, CAPQ,
-                                                                        totals, R0 * S0, k, P, pst, od64, od, oi);
-                CRISP_LAUNCH();
-                g_launches++;
-            }
-        }
-        if (g_timing) {
-            k_stats<<<(unsigned)qn, 128, 0, s>>>(act, act_len, M, KK, ix->off2, NB, ncand, mode == 1 ? nver : nullptr,
-                                                 fb, qn);
-            CRISP_LAUNCH();
-            g_launches++;
-        }
-        if (tr) {
-            std::vector<int32_t> hl((size_t)qn * M);
-            std::vector<uint32_t> ha;
-            std::vector<int64_t> hr((size_t)qn * M), hn;
-            CRISP_CUDA(cudaMemcpyAsync(hl.data(), act_len, (size_t)qn * M * 4, cudaMemcpyDeviceToHost, s));
-            CRISP_CUDA(cudaMemcpyAsync(hr.data(), retr, (size_t)qn * M * 8, cudaMemcpyDeviceToHost, s));
-            if (tr->act_cell || tr->act_w) {
-                ha.resize((size_t)qn * M * KK);
-                CRISP_CUDA(cudaMemcpyAsync(ha.data(), act, (size_t)qn * M * KK * 4, cudaMemcpyDeviceToHost, s));
-            }
-            if (tr->V) CRISP_CUDA(cudaMemcpyAsync(tr->V + q0 * N, traceV, (size_t)qn * N, cudaMemcpyDeviceToHost, s));
-            if (tr->qrot)
-                for (int64_t q = 0; q < qn; q++)
-                    CRISP_CUDA(cudaMemcpyAsync(tr->qrot + (q0 + q) * Dp, qrot + q * pitch, (size_t)Dp * 4,
-                                               cudaMemcpyDeviceToHost, s));
-            if (tr->fallback)
-                CRISP_CUDA(cudaMemcpyAsync(tr->fallback + q0, fb, (size_t)qn * 4, cudaMemcpyDeviceToHost, s));
-            if (mode == 1) {
-                hn.resize(qn);
-                CRISP_CUDA(cudaMemcpyAsync(hn.data(), nver, (size_t)qn * 8, cudaMemcpyDeviceToHost, s));
-                CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), pool, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
-            }
-            CRISP_CUDA(cudaStreamSynchronize(s));
-            for (int64_t q = 0; q < qn; q++) {
-                for (int m = 0; m < M; m++) {
-                    const int L = hl[q * M + m];
-                    if (tr->act_len) tr->act_len[(q0 + q) * M + m] = L;
-                    if (tr->retrieved) tr->retrieved[(q0 + q) * M + m] = hr[q * M + m];
-                    for (int r = 0; r < L && !ha.empty(); r++) {
-                        const uint32_t v = ha[(q * M + m) * (int64_t)KK + r];
-                        if (tr->act_cell) tr->act_cell[((q0 + q) * M + m) * (int64_t)KK + r] = (int32_t)(v & 0xffffu);
-                        if (tr->act_w) tr->act_w[((q0 + q) * M + m) * (int64_t)KK + r] = (int32_t)(v >> 16);
-                    }
-                }
-                if (mode == 1) {
-                    int64_t n = 0;
-                    for (int b = 0; b < NB; b++) n += h_ncand[q * NB + b];
-                    if (tr->order)
-                        for (int64_t i = 0; i < n; i++) tr->order[(q0 + q) * N + i] = h_pool[q * CAPQ + i];
-                    if (tr->n_verified) tr->n_verified[q0 + q] = hn[q];
-                }
-            }
-        }
+        if (tr) trace_candidates(w, q0, qn, tr, s);
+        run_verify(w, qn, out.ids + q0 * k, out.d32 ? out.d32 + q0 * k : nullptr, out.d64 ? out.d64 + q0 * k : nullptr,
+                   s);
+        run_stats(w, qn, s);
+        if (tr) trace_rest(w, q0, qn, tr, s);
     }
     return true;
 }
@@ -1491,14 +1662,82 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
             cudaStream_t s, const crisp_trace_t *tr) {
     // candidate capacity per query: optimistic, grown (and the batch redone)
     // if any query's |C_q| exceeds it, so results never depend on it
-    const int64_t NBS = (int64_t)ix->NB * ix->BS;
-    int64_t cap = std::min<int64_t>(NBS, std::max<int64_t>(4096, env_int("CRISP_CAND_CAP", 1 << 17)));
-    if (tr) cap = NBS;
+    int64_t cap = initial_capacity(ix, tr != nullptr);
     for (;;) {
         int64_t need = 0;
         if (search_pass(ix, queries, Q, k, mode, out, s, tr, cap, &need)) return;
-        cap = std::min<int64_t>(NBS, std::max<int64_t>(cap * 2, need + need / 4));
+        cap = grow_capacity(ix, cap, need);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Shard session: the search split at the two exchange points of the exact
+// global fallback.  The whole batch is one chunk.
+// ---------------------------------------------------------------------------
+}  // namespace crisp
+
+struct crisp_session {
+    const crisp_index *ix;
+    crisp::Work *w;
+    int64_t Q;
+    int k, mode;
+};
+
+namespace crisp {
+
+crisp_session *session_begin(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode,
+                             int32_t *local_counts, cudaStream_t s) {
+    int64_t cap = initial_capacity(ix, false);
+    for (;;) {
+        Work *w = new Work(ix, k, mode, std::max<int64_t>(Q, 1), cap, false, false, s);
+        try {
+            run_front(*w, queries, Q, s);
+            const int32_t need = read_need(*w, s);
+            if (need <= cap) {
+                k_local_counts<<<nblk(Q, 256), 256, 0, s>>>(w->ncand, ix->NB, Q, local_counts);
+                CRISP_LAUNCH();
+                g_launches++;
+                return new crisp_session{ix, w, Q, k, mode};
+            }
+            delete w;
+            cap = grow_capacity(ix, cap, need);
+        } catch (...) {
+            delete w;
+            throw;
+        }
+    }
+}
+
+void session_hist(crisp_session *ss, const int32_t *gcount, int32_t *lhist, cudaStream_t s) {
+    Work &w = *ss->w;
+    const crisp_index *ix = ss->ix;
+    StageScope st(s, 3);
+    k_fb_hist<<<(unsigned)ss->Q, THREADS, w.count_smem, s>>>(w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB,
+                                                             ix->ids, ix->N, ix->BS, ss->k, gcount, lhist);
+    CRISP_LAUNCH();
+    g_launches++;
+}
+
+void session_finish(crisp_session *ss, const int32_t *gcount, const int32_t *allhist, int32_t G, int32_t rank,
+                    int64_t *out_ids, double *out_d64, cudaStream_t s) {
+    Work &w = *ss->w;
+    const crisp_index *ix = ss->ix;
+    {
+        StageScope st(s, 3);
+        k_fb_select<<<(unsigned)ss->Q, THREADS, w.count_smem, s>>>(
+            w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB, ix->ids, ix->N, ix->BS, ss->k, gcount, allhist,
+            G, rank, ss->Q, w.pool, w.CAPQ, w.cbase, w.ncand, w.fb);
+        CRISP_LAUNCH();
+        g_launches++;
+    }
+    run_verify(w, ss->Q, out_ids, nullptr, out_d64, s);
+    run_stats(w, ss->Q, s);
+}
+
+void session_free(crisp_session *ss) {
+    if (!ss) return;
+    delete ss->w;
+    delete ss;
 }
 
 void merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32_t k, double *out_d64, float *out_d,

@@ -56,6 +56,27 @@ class CudaEngine:
         self.index.search_shard_async(q_dev, k, mode, ids, d64, stream)
         return ids, d64
 
+    # phased shard search (exact global fallback), see include/crisp.h
+    def begin(self, q_dev, k, mode, stream=0):
+        counts = torch.empty(q_dev.shape[0], dtype=torch.int32, device=q_dev.device)
+        self._ss = self.index.shard_begin(q_dev, k, mode, counts, stream)
+        self._Q, self._k = q_dev.shape[0], k
+        return counts
+
+    def hist(self, global_counts, stream=0):
+        M = self.index.info()["M"]
+        h = torch.zeros((self._Q, 2 * M + 2), dtype=torch.int32, device=global_counts.device)
+        self.index.shard_hist(self._ss, global_counts, h, stream)
+        return h
+
+    def finish(self, global_counts, all_hist, G, rank, stream=0):
+        ids = torch.empty((self._Q, self._k), dtype=torch.int64, device=global_counts.device)
+        d64 = torch.empty((self._Q, self._k), dtype=torch.float64, device=global_counts.device)
+        self.index.shard_finish(self._ss, global_counts, all_hist, G, rank, ids, d64, stream)
+        self.index.shard_free(self._ss)
+        self._ss = None
+        return ids, d64
+
     def merge(self, d64_all, ids_all, stream=0):
         G, Q, k = d64_all.shape
         od64 = torch.empty((Q, k), dtype=torch.float64, device=d64_all.device)
@@ -104,6 +125,25 @@ def search_step(engine, q_dev, k, mode, stream=0):
     """One sharded search of the batch: local a0..a5, then N7 + a6."""
     ids, d64 = engine.search_shard(q_dev, k, mode, stream)
     world = dist.get_world_size()
+    gd = [torch.empty_like(d64) for _ in range(world)]
+    gi = [torch.empty_like(ids) for _ in range(world)]
+    dist.all_gather(gd, d64)
+    dist.all_gather(gi, ids)
+    return engine.merge(torch.stack(gd), torch.stack(gi), stream)
+
+
+def search_step_exact(engine, q_dev, k, mode, stream=0):
+    """One sharded search with the EXACT global underflow fallback: N5
+    all-reduce of |C_q|, all-gather of the V histograms of underflowing
+    queries, then a5 on each shard and N7 + a6.  For phi=0 the result equals
+    the single index for every G."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    counts = engine.begin(q_dev, k, mode, stream)
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    hist = engine.hist(counts, stream)
+    all_h = [torch.empty_like(hist) for _ in range(world)]
+    dist.all_gather(all_h, hist)
+    ids, d64 = engine.finish(counts, torch.stack(all_h), world, rank, stream)
     gd = [torch.empty_like(d64) for _ in range(world)]
     gi = [torch.empty_like(ids) for _ in range(world)]
     dist.all_gather(gd, d64)

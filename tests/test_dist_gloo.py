@@ -47,6 +47,54 @@ class OracleEngine:
         ids, d, _ = oracle.search(self.ix, q.numpy(), k, mode, self.B, self.tau, patience_factor=0)
         return torch.from_numpy(ids), torch.from_numpy(d)
 
+    # phased protocol (exact global fallback), emulated on the oracle
+    def begin(self, q, k, mode, stream=0):
+        import oracle
+
+        _, _, t = oracle.search(self.ix, q.numpy(), k, mode, self.B, self.tau, patience_factor=0, trace=True,
+                                fallback=False)
+        self._t, self._q, self._k, self._mode = t, q.numpy(), k, mode
+        return torch.from_numpy(t["cand_n"].astype(np.int32))
+
+    def hist(self, gcounts, stream=0):
+        M, k = self.ix["M"], self._k
+        h = np.zeros((len(gcounts), 2 * M + 2), np.int32)
+        for q in range(len(gcounts)):
+            if int(gcounts[q]) < k:
+                h[q] = np.bincount(self._t["V"][q], minlength=2 * M + 2)[: 2 * M + 2]
+                h[q, 0] = 0
+        return torch.from_numpy(h)
+
+    def finish(self, gcounts, all_hist, G, rank, stream=0):
+        import oracle
+
+        M, k, t = self.ix["M"], self._k, self._t
+        N = self.ix["N"]
+        Q = len(gcounts)
+        cand = np.zeros((Q, N), np.int32)
+        n = np.zeros(Q, np.int64)
+        ah = all_hist.numpy()
+        for q in range(Q):
+            if int(gcounts[q]) >= k:
+                c = t["cand"][q, : t["cand_n"][q]]
+            else:  # global top-k touched by (V desc, gid asc); V* / quota from the summed histogram
+                tot = ah[:, q].sum(0)
+                acc, vstar, quota = 0, 1, int(tot[1])
+                for v in range(2 * M, 0, -1):
+                    if acc + tot[v] >= k:
+                        vstar, quota = v, k - acc
+                        break
+                    acc += tot[v]
+                share = max(0, min(int(ah[rank, q, vstar]), quota - int(ah[:rank, q, vstar].sum())))
+                V = t["V"][q].astype(int)
+                eq = np.nonzero(V == vstar)[0][:share]
+                c = np.sort(np.concatenate([np.nonzero(V > vstar)[0], eq])).astype(np.int32)
+            cand[q, : len(c)] = c
+            n[q] = len(c)
+        ids, d, _ = oracle.search(self.ix, self._q, k, self._mode, self.B, self.tau, patience_factor=0, ext_cand=cand,
+                                  ext_n=n)
+        return torch.from_numpy(ids), torch.from_numpy(d)
+
     def merge(self, d_all, ids_all, stream=0):
         import oracle
 
@@ -61,14 +109,14 @@ def _data():
     return X, Q
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, exact=False, tau=2):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2603_05180_b200 import dist as cdist
 
         X, Q = _data()
-        M, k, B, tau = 4, 5, 300, 2
+        M, k, B = 4, 5, 300
         eng = OracleEngine()
         R, cb = eng.build_global(X, M) if rank == 0 else (None, None)
         R, cb = cdist.share_model(R, cb, torch.zeros(1))
@@ -76,7 +124,8 @@ def _worker(rank, world, port, out):
         eng.build_shard(X[lo:hi], lo, M, R, cb)
         sizes = cdist.global_cell_sizes(eng)
         eng.set_search_params(B, tau)
-        ids, d = cdist.search_step(eng, torch.from_numpy(Q), k, 0)
+        step = cdist.search_step_exact if exact else cdist.search_step
+        ids, d = step(eng, torch.from_numpy(Q), k, 0)
         if rank == 0:
             np.savez(out, ids=ids.numpy(), d=d.numpy(), sizes=sizes.numpy(), R=R.numpy(), cb=cb.numpy())
     finally:
@@ -91,13 +140,34 @@ def _free_port():
     return p
 
 
+def _run(exact, tau):
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "r0.npz")
+        mp.start_processes(_worker, args=(2, _free_port(), out, exact, tau), nprocs=2, join=True,
+                           start_method="spawn")
+        return dict(np.load(out))
+
+
+def test_exact_global_fallback_matches_single_index():
+    """search_step_exact: every query, fallback ones included, equals the
+    single index (P:L449 applied to the whole dataset)."""
+    import oracle
+
+    tau = 4
+    res = _run(True, tau)
+    X, Q = _data()
+    full = oracle.build(X, 4, K=6, R=res["R"], codebooks=res["cb"])
+    ids, d, t = oracle.search(full, Q, 5, 0, 300, tau, trace=True)
+    assert t["fallback"].sum() >= 2  # the case under test occurs
+    assert np.array_equal(res["ids"], ids)
+    fin = np.isfinite(d)
+    assert np.allclose(res["d"][fin], d[fin].astype(np.float32))
+
+
 def test_sharded_orchestration_matches_single_index():
     import oracle
 
-    with tempfile.TemporaryDirectory() as td:
-        out = os.path.join(td, "r0.npz")
-        mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
-        res = np.load(out)
+    res = _run(False, 2)
     X, Q = _data()
     M, k, B, tau = 4, 5, 300, 2
     full = oracle.build(X, M, K=6, R=res["R"], codebooks=res["cb"])

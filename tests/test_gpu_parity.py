@@ -235,3 +235,57 @@ def test_candidate_capacity_regrow(crisp, monkeypatch, mode):
     r_ids, r_d, ot = oracle.search(ox, Qv, 10, mode, 9000, 1, patience_factor=0, trace=True)
     assert ot["cand_n"].max() > 4096
     assert_topk_parity(ids, d, r_ids, r_d, "capacity regrow")
+
+
+@pytest.mark.parametrize("tau", [2, 5])
+def test_shard_emulation_exact_fallback(crisp, tau):
+    """G=3 point shards on one GPU through the phased shard session (exact
+    global fallback), 'collectives' as device sums/stacks, then the a6 merge
+    kernel: Guaranteed-Mode results equal the single index for every query,
+    fallback queries included."""
+    import torch
+
+    X, Qv, ox = make_case(cfg=1, N=9001, D=64, Q=40, M=4, K=8, seed=13)
+    k, B, G = 6, 400, 3
+    single = build_gpu(crisp, X, ox, block_ids=4096)
+    single.set_search_params(budget=B, tau=tau)
+    ids1, d1 = single.search(Qv, k, 0)
+    _, _, ot = oracle.search(ox, Qv, k, 0, B, tau, trace=True)
+    shards = []
+    for g in range(G):
+        lo, hi = (9001 * g) // G, (9001 * (g + 1)) // G
+        os.environ["CRISP_BLOCK_IDS"] = "4096"
+        try:
+            shards.append(crisp.Index.build(X[lo:hi], ox["M"], codebooks=ox["cb"], K=ox["K"], gid_base=lo))
+        finally:
+            os.environ.pop("CRISP_BLOCK_IDS", None)
+    sizes = sum(s.local_cell_sizes() for s in shards)
+    assert np.array_equal(sizes, ox["gsize"])
+    for s in shards:
+        s.set_global_cell_sizes(sizes)
+        s.set_search_params(budget=B, tau=tau)
+    q = torch.from_numpy(Qv).cuda()
+    counts = [torch.empty(len(Qv), dtype=torch.int32, device="cuda") for _ in shards]
+    sess = [s.shard_begin(q, k, 0, c) for s, c in zip(shards, counts)]
+    gc = sum(counts)
+    hists = [torch.zeros((len(Qv), 2 * ox["M"] + 2), dtype=torch.int32, device="cuda") for _ in shards]
+    for ss, h in zip(sess, hists):
+        crisp.Index.shard_hist(ss, gc, h)
+    allh = torch.stack(hists).contiguous()
+    outs = []
+    for g, ss in enumerate(sess):
+        gi = torch.empty((len(Qv), k), dtype=torch.int64, device="cuda")
+        gd = torch.empty((len(Qv), k), dtype=torch.float64, device="cuda")
+        crisp.Index.shard_finish(ss, gc, allh, G, g, gi, gd)
+        crisp.Index.shard_free(ss)
+        outs.append((gi, gd))
+    od64 = torch.empty((len(Qv), k), dtype=torch.float64, device="cuda")
+    od = torch.empty((len(Qv), k), dtype=torch.float32, device="cuda")
+    oi = torch.empty((len(Qv), k), dtype=torch.int64, device="cuda")
+    crisp.merge_topk(torch.stack([o[1] for o in outs]).contiguous(), torch.stack([o[0] for o in outs]).contiguous(),
+                     od64, od, oi)
+    torch.cuda.synchronize()
+    if tau == 5:
+        assert ot["fallback"].sum() >= 2
+    assert np.array_equal(oi.cpu().numpy(), ids1)
+    assert np.array_equal(od.cpu().numpy(), d1)
