@@ -278,7 +278,7 @@ def run_crisp(args):
             if world == 1:
                 index.search_async(Qd, k, mode, ids, dd, stream)
                 return ids
-            oi, _ = cdist.search_step(engine, Qd, k, mode, stream)
+            oi, _ = cdist.search_step_exact(engine, Qd, k, mode, stream)
             return oi
 
         for _ in range(args.warmup):
