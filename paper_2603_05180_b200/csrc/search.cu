@@ -952,64 +952,92 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
 
 // k_hsort: one warp per query; stable counting sort of the ascending-id list by
 // h -> order (h, id), written over the query's pool region.
-__global__ void __launch_bounds__(32) k_hsort(const int32_t *__restrict__ ncand, int NB, int Dp,
-                                              const int32_t *__restrict__ ghist, const int32_t *__restrict__ cbuf,
-                                              const uint16_t *__restrict__ hbuf, int64_t CS,
-                                              int32_t *__restrict__ pool, int64_t PS, int32_t *__restrict__ total_out) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    int *start = (int *)sm;  // Dp + 1
-    const int64_t q = blockIdx.x;
-    const int lane = threadIdx.x;
-    const int32_t *gh = ghist + q * (int64_t)(Dp + 1);
-    int acc = 0;
+// One warp: bin starts of the per-query histogram (start[], Dp+1) and the
+// stable scatter of the ascending-id candidate list by h into `out`.  Only the
+// bins whose start is below `limit` are scattered (the positions the
+// speculative rounds read); limit = INT_MAX scatters everything.
+__device__ int hsort_warp(const int32_t *__restrict__ gh, int Dp, const int32_t *__restrict__ cq,
+                          const uint16_t *__restrict__ hq, int32_t *__restrict__ out, int *start, int limit) {
+    const int lane = threadIdx.x & 31;
+    int acc = 0, cut = -1;
     for (int b0 = 0; b0 < Dp + 1; b0 += 32) {
         const int i = b0 + lane;
-        int v = i < Dp + 1 ? gh[i] : 0;
+        const int v = i < Dp + 1 ? gh[i] : 0;
         int inc = v;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, inc, off);
+            const int t = __shfl_up_sync(0xffffffffu, inc, off);
             if (lane >= off) inc += t;
         }
-        if (i < Dp + 1) start[i] = acc + inc - v;
+        const int st = acc + inc - v;
+        if (i < Dp + 1) start[i] = st;
+        const unsigned below = __ballot_sync(0xffffffffu, i < Dp + 1 && st < limit);
+        if (below) cut = b0 + 31 - __clz(below);  // starts are monotone
         acc += __shfl_sync(0xffffffffu, inc, 31);
     }
     const int total = acc;
-    if (lane == 0) total_out[q] = total;
     __syncwarp();
-    const int32_t *cq = cbuf + q * CS;
-    const uint16_t *hq = hbuf + q * CS;
-    int32_t *out = pool + q * PS;
+    const bool full = cut >= Dp;
     constexpr int U = 8;  // chunks of 32 loaded ahead (independent loads)
     for (int v00 = 0; v00 < total; v00 += 32 * U) {
         int hh[U], ll[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int v = v00 + u * 32 + lane;
-            hh[u] = v < total ? hq[v] : 0;
+            hh[u] = v < total ? hq[v] : 0x7fffffff;
             ll[u] = v < total ? cq[v] : 0;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const int v = v00 + u * 32 + lane;
-            const bool act = v < total;
-            const unsigned am = __ballot_sync(0xffffffffu, act);
-            if (act) {
-                const int h = hh[u];
-                const unsigned peers = __match_any_sync(am, h);
-                const int leader = __ffs(peers) - 1;
-                const int rank = __popc(peers & ((1u << lane) - 1));
-                int base = 0;
-                if (lane == leader) {
-                    base = start[h];
-                    start[h] = base + __popc(peers);
+            const int h = hh[u];
+            const bool qual = h <= cut;
+            const unsigned qm = __ballot_sync(0xffffffffu, qual);
+            if (!qm) continue;
+            int rank = 0, cnt = 0, leader = 32;
+            if (full) {
+                if (qual) {
+                    const unsigned peers = __match_any_sync(qm, h);
+                    leader = __ffs(peers) - 1;
+                    rank = __popc(peers & ((1u << lane) - 1));
+                    cnt = __popc(peers);
                 }
-                base = __shfl_sync(peers, base, leader);
-                out[base + rank] = ll[u];
+            } else {
+                for (unsigned m = qm; m; m &= m - 1) {  // few qualifying lanes: O(qualifying)
+                    const int j = __ffs(m) - 1;
+                    const int hj = __shfl_sync(0xffffffffu, h, j);
+                    if (qual && hj == h) {
+                        if (leader == 32) leader = j;
+                        rank += j < lane;
+                        cnt++;
+                    }
+                }
             }
+            int base = 0;
+            if (qual && lane == leader) {
+                base = start[h];
+                start[h] = base + cnt;
+            }
+            base = __shfl_sync(0xffffffffu, base, qual ? leader : lane);
+            if (qual) out[base + rank] = ll[u];
             __syncwarp();
         }
     }
+    return total;
+}
+
+// k_hsort: one warp per query; order (h, id) of the positions the speculative
+// rounds read, written over the query's pool region.
+__global__ void __launch_bounds__(32) k_hsort(const int32_t *__restrict__ ncand, int NB, int Dp,
+                                              const int32_t *__restrict__ ghist, const int32_t *__restrict__ cbuf,
+                                              const uint16_t *__restrict__ hbuf, int64_t CS,
+                                              int32_t *__restrict__ pool, int64_t PS, int32_t *__restrict__ total_out,
+                                              int limit) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    int *start = (int *)sm;  // Dp + 1
+    const int64_t q = blockIdx.x;
+    const int total = hsort_warp(ghist + q * (int64_t)(Dp + 1), Dp, cbuf + q * CS, hbuf + q * CS, pool + q * PS, start,
+                                 limit);
+    if (threadIdx.x == 0) total_out[q] = total;
 }
 
 // ---------------------------------------------------------------------------
@@ -1154,10 +1182,13 @@ __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int
 // sequential verification from position `from`.
 __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restrict__ qrot, int pitch,
                                                             const float *__restrict__ X, int64_t gid_base,
-                                                            const int32_t *__restrict__ pool, int64_t PS,
+                                                            int32_t *__restrict__ pool, int64_t PS,
                                                             const int32_t *__restrict__ totals, int from, int k, int P,
                                                             PatState st, double *__restrict__ out_d64,
-                                                            float *__restrict__ out_d, int64_t *__restrict__ out_i) {
+                                                            float *__restrict__ out_d, int64_t *__restrict__ out_i,
+                                                            int Dp, const int32_t *__restrict__ ghist,
+                                                            const int32_t *__restrict__ cbuf,
+                                                            const uint16_t *__restrict__ hbuf) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int64_t q = blockIdx.x;
     if (st.done[q]) return;
@@ -1166,9 +1197,15 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
     int64_t *chi = (int64_t *)(chd + PATIENCE_CH);   // PATIENCE_CH
     double *Td = (double *)(chi + PATIENCE_CH);      // k
     int64_t *Ti = (int64_t *)(Td + k);               // k
+    int *hstart = (int *)(Ti + k);                   // Dp + 1
     __shared__ int s_stop, s_cnt;
     __shared__ int64_t s_nver;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // k_hsort ordered only the positions the rounds read: complete the order
+    if (warp == 0)
+        hsort_warp(ghist + q * (int64_t)(Dp + 1), Dp, cbuf + q * PS, hbuf + q * PS, pool + q * PS, hstart,
+                   0x7fffffff);
+    __syncthreads();
     load_qd(qd, qrot + q * pitch, pitch);
     int cnt_top = st.cnt[q], pat = st.pat[q];
     for (int i = tid; i < cnt_top; i += THREADS) {
@@ -1360,6 +1397,7 @@ struct Work {
     uint16_t *hbuf = nullptr;
     PatState pst{};
     uint8_t *traceV = nullptr;
+    bool full_order = false;  // trace: order every candidate (not only what the rounds read)
     int probe_gs, probe_smem, count_smem, rx_smem, ham_smem, hsort_smem, vr_smem, scan_smem, pat_smem;
 
     static int64_t per_query_bytes(const crisp_index *ix, int k, int mode, int64_t CAPQ, bool traceV) {
@@ -1421,7 +1459,7 @@ struct Work {
         hsort_smem = (Dp + 1) * 4;
         vr_smem = pitch * 8;
         scan_smem = WARPS * k * 16;
-        pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16;
+        pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + (Dp + 1) * 4;
         set_attrs();
         CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
                         pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
@@ -1516,7 +1554,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     {
         StageScope st(s, 7);
         k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, NB, Dp, w.ghist, w.cbuf, w.hbuf, w.CAPQ, w.pool, w.CAPQ,
-                                                       w.totals);
+                                                       w.totals, w.full_order ? 0x7fffffff : w.R0 * w.S0);
         CRISP_LAUNCH();
         g_launches++;
     }
@@ -1533,7 +1571,8 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         g_launches++;
     }
     k_patience_tail<<<(unsigned)qn, THREADS, w.pat_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ,
-                                                              w.totals, w.R0 * w.S0, k, P, w.pst, od64, od, oi);
+                                                              w.totals, w.R0 * w.S0, k, P, w.pst, od64, od, oi, Dp,
+                                                              w.ghist, w.cbuf, w.hbuf);
     CRISP_LAUNCH();
     g_launches++;
 }
@@ -1640,6 +1679,7 @@ static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, 
     int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
     Qc = std::min<int64_t>(Qc, 65535);
     Work w(ix, k, mode, Qc, CAPQ, tr && tr->V, out.d64 == nullptr, s);
+    w.full_order = tr != nullptr;
     for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
         const int64_t qn = std::min(Qc, Q - q0);
         run_front(w, queries + q0 * ix->D, qn, s);
