@@ -76,6 +76,7 @@ static void free_index(crisp_index *ix) {
     cudaFree(ix->cells);
     cudaFree(ix->ids);
     cudaFree(ix->off2);
+    cudaFree(ix->off2w);
     cudaFree(ix->gsize);
     cudaFree(ix->codes);
     delete ix;
@@ -113,6 +114,8 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
     ix->W = (ix->Dp + 63) / 64;
     ix->BS = block_ids_for(N);
     ix->NB = (int32_t)((N + ix->BS - 1) / ix->BS);
+    ix->SBW = ix->BS / 8;
+    ix->NBW = ix->NB * 8;
     ix->workspace_bytes = p->workspace_bytes;
     try {
         const int64_t KK = (int64_t)ix->K * ix->K;
@@ -121,6 +124,7 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
         ix->cells = dalloc<int32_t>(ix, (size_t)ix->M * N);
         ix->ids = dalloc<int32_t>(ix, (size_t)ix->M * N);
         ix->off2 = dalloc<int32_t>(ix, (size_t)ix->M * KK * (ix->NB + 1));
+        ix->off2w = dalloc<int32_t>(ix, (size_t)ix->M * KK * (ix->NBW + 1));
         ix->gsize = dalloc<int32_t>(ix, (size_t)ix->M * KK);
         ix->codes = dalloc<uint64_t>(ix, (size_t)N * ix->W);
     } catch (...) {

@@ -581,18 +581,24 @@ void finish_csr(crisp_index *ix, cudaStream_t s) {
         CRISP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, ix->cells + (int64_t)m * N, kout, iota,
                                                    ix->ids + (int64_t)m * N, (int)N, 0, bits, s));
     }
-    int64_t ne = (int64_t)KK * NB;
-    int32_t *cnt = sc.alloc<int32_t>((size_t)M * ne), *scan = sc.alloc<int32_t>((size_t)M * ne);
-    CRISP_CUDA(cudaMemsetAsync(cnt, 0, (size_t)M * ne * 4, s));
-    k_hist2<<<nblk(N * M, 256), 256, 0, s>>>(ix->cells, N, M, KK, BS, NB, cnt);
-    CRISP_LAUNCH();
-    size_t tb2 = 0;
-    CRISP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, scan, (int)ne, s));
-    void *tmp2 = sc.get(tb2);
-    for (int m = 0; m < M; m++)
-        CRISP_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, cnt + (int64_t)m * ne, scan + (int64_t)m * ne, (int)ne, s));
-    k_off2<<<nblk((int64_t)M * KK * (NB + 1), 256), 256, 0, s>>>(scan, N, M, KK, NB, ix->off2, ix->gsize);
-    CRISP_LAUNCH();
+    // block offsets (off2, BS ids) and warp sub-block offsets (off2w, SBW ids)
+    for (int level = 0; level < 2; level++) {
+        const int nb = level == 0 ? NB : ix->NBW, bs = level == 0 ? BS : ix->SBW;
+        int32_t *dst = level == 0 ? ix->off2 : ix->off2w;
+        const int64_t ne = (int64_t)KK * nb;
+        int32_t *cnt = sc.alloc<int32_t>((size_t)M * ne), *scan = sc.alloc<int32_t>((size_t)M * ne);
+        CRISP_CUDA(cudaMemsetAsync(cnt, 0, (size_t)M * ne * 4, s));
+        k_hist2<<<nblk(N * M, 256), 256, 0, s>>>(ix->cells, N, M, KK, bs, nb, cnt);
+        CRISP_LAUNCH();
+        size_t tb2 = 0;
+        CRISP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, scan, (int)ne, s));
+        void *tmp2 = sc.get(tb2);
+        for (int m = 0; m < M; m++)
+            CRISP_CUDA(
+                cub::DeviceScan::ExclusiveSum(tmp2, tb2, cnt + (int64_t)m * ne, scan + (int64_t)m * ne, (int)ne, s));
+        k_off2<<<nblk((int64_t)M * KK * (nb + 1), 256), 256, 0, s>>>(scan, N, M, KK, nb, dst, ix->gsize);
+        CRISP_LAUNCH();
+    }
     CRISP_CUDA(cudaStreamSynchronize(s));
 }
 

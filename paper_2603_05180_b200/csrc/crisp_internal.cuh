@@ -67,9 +67,11 @@ struct crisp_index {
     int32_t *cells = nullptr;  // M x N
     int32_t *ids = nullptr;    // M x N CSR ids
     int32_t *off2 = nullptr;   // M x K^2 x (NB+1): start of ids >= b*BS inside cell c
+    int32_t *off2w = nullptr;  // M x K^2 x (NBW+1): the same at warp sub-block granularity SBW = BS/8
     int32_t *gsize = nullptr;  // M x K^2 sizes for the budget walk (local or global)
     uint64_t *codes = nullptr; // N x W
     int32_t BS = 0, NB = 0;    // on-chip counter block: ids per block, number of blocks
+    int32_t SBW = 0, NBW = 0;  // warp sub-block: ids per sub-block (BS/8), number of sub-blocks (8*NB)
     int64_t budget = 0;
     int32_t tau = 1, patience_factor = 40;
     int64_t workspace_bytes = 0;

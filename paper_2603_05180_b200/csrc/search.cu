@@ -419,6 +419,235 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
 }
 
 // ---------------------------------------------------------------------------
+// a3 + a4, warp-owned counters (default).  Each warp owns the SBW = BS/8 byte
+// counters of one sub-block of ids and streams that sub-block's part of every
+// activated slice (off2w offsets) on its own: no CTA barrier after setup, no
+// staging through shared memory.  A warp walks the slices in activation order
+// (subspace-major) in batches of 32 consecutive positions of ONE slice, so
+// the lanes of a batch hit distinct counters and plain byte read-modify-
+// writes suffice; __syncwarp orders consecutive batches (an id recurs only
+// across subspaces, CSR partition property).  The (slice, offset)
+// walk is a warp-uniform state machine; the id loads of CW_U batches are in
+// flight before their read-modify-writes.  a4 is a SWAR scan of the warp's
+// counters in ascending id that also re-zeroes them; each sub-block is its
+// own candidate segment (base from an atomic cursor, ascending ids inside).
+// ---------------------------------------------------------------------------
+constexpr int CW_U = 8;  // 32-position batches with loads in flight per warp (k_count_warp)
+struct CountWSmem {
+    uint32_t erow[CS_CAP];  // cached entries: (m*KK + cell) | WFLAG
+    uint32_t emw[CS_CAP];   // cached entries: m | WFLAG
+    int32_t lpre[MAX_M + 2];
+};
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// 4-bit mask of the bytes of w that are >= t (t4 = t in every byte)
+template <bool SWAR>
+__device__ __forceinline__ uint32_t bytes_ge(uint32_t w, uint32_t t4) {
+    uint32_t h;
+    if (SWAR) h = ((w | 0x80808080u) - t4) & 0x80808080u;  // bytes and t < 128: no borrow between bytes
+    else h = __vcmpgeu4(w, t4) & 0x80808080u;
+    return (h * 0x00204081u) >> 28;  // bits 7,15,23,31 -> 28..31
+}
+
+template <bool SWAR>
+__global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__restrict__ act,
+                                                           const int32_t *__restrict__ act_len, int M, int KK,
+                                                           const int32_t *__restrict__ off2w, int NBW,
+                                                           const int32_t *__restrict__ ids, int64_t N, int BS, int BPC,
+                                                           int NB, int tau, int32_t *__restrict__ pool, int64_t CAPQ,
+                                                           int32_t *__restrict__ cursor, int32_t *__restrict__ cbase,
+                                                           int32_t *__restrict__ ncand, int32_t *__restrict__ need,
+                                                           uint8_t *__restrict__ traceV) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    unsigned char *cnt8 = smraw;  // BS byte counters (+16 dummy bytes); warp w owns [w*SBW, (w+1)*SBW)
+    CountWSmem &S = *(CountWSmem *)(smraw + BS + 16);
+    const int64_t q = blockIdx.y;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int SBW = BS >> 3;
+    const int b_lo = blockIdx.x * BPC, b_hi = min(NB, b_lo + BPC);
+    unsigned char *wc = cnt8 + warp * SBW;
+    const uint32_t sm_cnt = (uint32_t)__cvta_generic_to_shared(cnt8);
+    const uint32_t sm_dummy = sm_cnt + (uint32_t)BS;
+    // lpre (exclusive prefix of act_len over m) and the cached entries
+    if (warp == 0) {
+        int acc = 0;
+        for (int m0 = 0; m0 < M; m0 += 32) {
+            const int m = m0 + lane;
+            int v = m < M ? __ldg(act_len + q * M + m) : 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += t;
+            }
+            if (m < M) S.lpre[m + 1] = acc + v;
+            acc += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (lane == 0) S.lpre[0] = 0;
+    }
+    for (int i = tid; i < SBW * WARPS / 16; i += THREADS) ((uint4 *)cnt8)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int Etot = S.lpre[M];
+    const bool cached = Etot <= CS_CAP;
+    const uint32_t *actq = act + q * (int64_t)M * KK;
+    if (cached)
+        for (int t = tid; t < Etot; t += THREADS) {
+            const int m = m_of_entry(S.lpre, M, t);
+            const uint32_t v = __ldg(actq + (int64_t)m * KK + (t - S.lpre[m]));
+            const uint32_t f = (v >> 16) == 2u ? WFLAG : 0u;
+            S.erow[t] = (uint32_t)(m * KK + (int)(v & 0xffffu)) | f;
+            S.emw[t] = (uint32_t)m | f;
+        }
+    __syncthreads();
+    const int nchunk = SBW / 512;  // 16-byte lane chunks of the warp's counters
+    const uint32_t tau4 = (uint32_t)tau * 0x01010101u;
+    int32_t *outp = pool + q * CAPQ;
+    for (int b = b_lo; b < b_hi; b++) {
+        const int sb = b * 8 + warp;
+        const uint32_t lbase = (uint32_t)b * (uint32_t)BS;  // local id of counter 0 of the CTA
+        if ((int64_t)sb * SBW < N) {
+            for (int e0 = 0; e0 < Etot; e0 += 32) {
+                // this lane's entry: slice of the sub-block (ids[] start g, length len), weight flag
+                const int e = e0 + lane;
+                uint32_t wf = 0;
+                int len = 0, g = 0;
+                if (e < Etot) {
+                    uint32_t erw, mw;
+                    if (cached) {
+                        erw = S.erow[e];
+                        mw = S.emw[e];
+                    } else {
+                        const int m = m_of_entry(S.lpre, M, e);
+                        const uint32_t v = __ldg(actq + (int64_t)m * KK + (e - S.lpre[m]));
+                        const uint32_t f = (v >> 16) == 2u ? WFLAG : 0u;
+                        erw = (uint32_t)(m * KK + (int)(v & 0xffffu)) | f;
+                        mw = (uint32_t)m | f;
+                    }
+                    const int32_t *o = off2w + (int64_t)(erw & ~WFLAG) * (NBW + 1) + sb;
+                    const int s0 = __ldg(o), s1 = __ldg(o + 1);
+                    len = s1 - s0;
+                    g = (int)(mw & ~WFLAG) * (int)N + s0;
+                    wf = mw >> 31;
+                }
+                uint32_t rest = __ballot_sync(0xffffffffu, len > 0);  // slices still to walk
+                // warp-uniform walk state: current slice (start G, length L, flag F), offset p
+                int G = 0, L = 0, p = 0;
+                uint32_t F = 0;
+                if (rest) {
+                    const int j = __ffs(rest) - 1;
+                    rest &= rest - 1;
+                    G = __shfl_sync(0xffffffffu, g, j);
+                    L = __shfl_sync(0xffffffffu, len, j);
+                    F = __shfl_sync(0xffffffffu, wf, j);
+                }
+                while (L > 0) {
+                    uint32_t xa[CW_U], xf[CW_U];
+#pragma unroll
+                    for (int u = 0; u < CW_U; u++) {
+                        const bool ok = p + lane < L;
+                        // unconditional load (past the slice end: its first id) so that no
+                        // branch joins on the result and all CW_U loads are in flight
+                        xa[u] = (uint32_t)__ldg(ids + (uint32_t)(G + (ok ? p + lane : 0)));
+                        xf[u] = ok ? F : 2u;  // 2: not a position
+                        p += 32;
+                        if (p >= L) {  // next slice (uniform)
+                            p = 0;
+                            L = 0;
+                            if (rest) {
+                                const int j = __ffs(rest) - 1;
+                                rest &= rest - 1;
+                                G = __shfl_sync(0xffffffffu, g, j);
+                                L = __shfl_sync(0xffffffffu, len, j);
+                                F = __shfl_sync(0xffffffffu, wf, j);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < CW_U; u++) {
+                        const uint32_t a = xf[u] == 2u ? sm_dummy : sm_cnt + (xa[u] - lbase);
+                        sts_u8(a, lds_u8(a) + 1u + xf[u]);
+                        __syncwarp();
+                    }
+                }
+            }
+        }
+        // a4: C = {x : V[x] >= tau} (Alg. 1 l.18) in ascending id; re-zero.
+        // Lane chunk i of the warp covers counters [i*512 + lane*16, +16).
+        uint32_t mk[8];
+        uint32_t s16[4] = {0, 0, 0, 0};  // per-chunk counts, 16-bit fields: chunks (0,1) (2,3) (4,5) (6,7)
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            mk[i] = 0;
+            if (i < nchunk) {
+                uint4 *pv = (uint4 *)(wc + i * 512 + lane * 16);
+                const uint4 v = *pv;
+                if (traceV) {
+                    const int64_t x0 = (int64_t)lbase + warp * SBW + i * 512 + lane * 16;
+                    const unsigned char *vb = (const unsigned char *)&v;
+                    for (int j = 0; j < 16; j++)
+                        if (x0 + j < N) traceV[q * N + x0 + j] = vb[j];
+                }
+                const uint32_t m16 = bytes_ge<SWAR>(v.x, tau4) | (bytes_ge<SWAR>(v.y, tau4) << 4) |
+                                     (bytes_ge<SWAR>(v.z, tau4) << 8) | (bytes_ge<SWAR>(v.w, tau4) << 12);
+                mk[i] = m16;
+                s16[i >> 1] |= (uint32_t)__popc(m16) << ((i & 1) * 16);
+                *pv = make_uint4(0, 0, 0, 0);
+            }
+        }
+        uint32_t inc16[4];
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+            uint32_t v = s16[h];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += t;
+            }
+            inc16[h] = v;
+        }
+        int ctot[8];
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+            const uint32_t t = __shfl_sync(0xffffffffu, inc16[h], 31);
+            ctot[2 * h] = (int)(t & 0xffffu);
+            ctot[2 * h + 1] = (int)(t >> 16);
+        }
+        int n = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) n += ctot[i];
+        int base = 0;
+        if (lane == 0) {
+            base = atomicAdd(cursor + q, n);
+            cbase[q * NBW + sb] = base;
+            ncand[q * NBW + sb] = n;
+            if ((int64_t)base + n > CAPQ) atomicMax(need, base + n);
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        int run = base;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            uint32_t word = mk[i];
+            const uint32_t inc = (inc16[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+            int o = run + (int)inc - __popc(word);
+            const int g0 = (int)lbase + warp * SBW + i * 512 + lane * 16;
+            while (word) {
+                const int bit = __ffs(word) - 1;
+                if (o < CAPQ) outp[o] = g0 + bit;
+                o++;
+                word &= word - 1;
+            }
+            run += ctot[i];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // a4 fallback (Z8): |C| < k -> the first min(k,|T|) touched ids by
 // (V desc, id asc), restated in ascending id.  Rare; one CTA per query,
 // counting every block twice (histogram of V, then selection).  For a sharded
@@ -515,7 +744,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
                                                        const int32_t *__restrict__ off2, int NB,
                                                        const int32_t *__restrict__ ids, int64_t N, int BS, int k,
                                                        int32_t *__restrict__ pool, int64_t CAPQ,
-                                                       int32_t *__restrict__ cbase, int32_t *__restrict__ ncand,
+                                                       int32_t *__restrict__ cbase, int32_t *__restrict__ ncand, int NS,
                                                        int32_t *__restrict__ fbflag) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;
@@ -526,7 +755,7 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
     const int tid = threadIdx.x;
     if (tid == 0) {
         int t = 0;
-        for (int b = 0; b < NB; b++) t += ncand[q * NB + b];
+        for (int b = 0; b < NS; b++) t += ncand[q * NS + b];
         s_total = t;
     }
     for (int i = tid; i < 2 * MAX_M + 2; i += THREADS) hist[i] = 0;
@@ -541,9 +770,9 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
     __syncthreads();
     const int n = fb_select_pass(S, cnt8, BS, q, Etot, act, M, KK, off2, NB, ids, N, s_vstar, s_quota, pool + q * CAPQ,
                                  &s_eqbase, &s_n);
-    for (int b = tid; b < NB; b += THREADS) {
-        ncand[q * NB + b] = (b == 0) ? n : 0;
-        cbase[q * NB + b] = 0;
+    for (int b = tid; b < NS; b += THREADS) {
+        ncand[q * NS + b] = (b == 0) ? n : 0;
+        cbase[q * NS + b] = 0;
     }
     if (tid == 0) fbflag[q] = 1;
 }
@@ -579,7 +808,7 @@ __global__ void __launch_bounds__(THREADS) k_fb_select(const uint32_t *__restric
                                                         const int32_t *__restrict__ allhist, int G, int rank, int64_t Q,
                                                         int32_t *__restrict__ pool, int64_t CAPQ,
                                                         int32_t *__restrict__ cbase, int32_t *__restrict__ ncand,
-                                                        int32_t *__restrict__ fbflag) {
+                                                        int NS, int32_t *__restrict__ fbflag) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;
     CountSmem &S = *(CountSmem *)(smraw + BS + BS / 8);
@@ -610,9 +839,9 @@ __global__ void __launch_bounds__(THREADS) k_fb_select(const uint32_t *__restric
     const int Etot = count_setup(S, q, act, act_len, M, KK);
     const int n = fb_select_pass(S, cnt8, BS, q, Etot, act, M, KK, off2, NB, ids, N, s_vstar, s_quota, pool + q * CAPQ,
                                  &s_eqbase, &s_n);
-    for (int b = tid; b < NB; b += THREADS) {
-        ncand[q * NB + b] = (b == 0) ? n : 0;
-        cbase[q * NB + b] = 0;
+    for (int b = tid; b < NS; b += THREADS) {
+        ncand[q * NS + b] = (b == 0) ? n : 0;
+        cbase[q * NS + b] = 0;
     }
     if (tid == 0) fbflag[q] = 1;
 }
@@ -1285,7 +1514,7 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
 __device__ unsigned long long d_stats[4];
 
 __global__ void k_stats(const uint32_t *__restrict__ act, const int32_t *__restrict__ act_len, int M, int KK,
-                        const int32_t *__restrict__ off2, int NB, const int32_t *__restrict__ ncand,
+                        const int32_t *__restrict__ off2, int NB, const int32_t *__restrict__ ncand, int NS,
                         const int64_t *__restrict__ nver, const int32_t *__restrict__ fb, int64_t Qc) {
     const int64_t q = blockIdx.x;
     unsigned long long ids = 0;
@@ -1301,7 +1530,7 @@ __global__ void k_stats(const uint32_t *__restrict__ act, const int32_t *__restr
     if ((threadIdx.x & 31) == 0) atomicAdd(&d_stats[0], ids);
     if (threadIdx.x == 0) {
         unsigned long long c = 0;
-        for (int b = 0; b < NB; b++) c += (unsigned long long)ncand[q * NB + b];
+        for (int b = 0; b < NS; b++) c += (unsigned long long)ncand[q * NS + b];
         atomicAdd(&d_stats[1], c);
         atomicAdd(&d_stats[2], nver ? (unsigned long long)nver[q] : c);
         atomicAdd(&d_stats[3], (unsigned long long)fb[q]);
@@ -1365,6 +1594,8 @@ static void set_attrs() {
     if (done) return;
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1384,7 +1615,7 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
-    int S, HS, S0, R0, BPC;
+    int S, HS, S0, R0, BPC, count_kernel, NS;
     DevBuf buf;
     float *qpad = nullptr, *qrot = nullptr;
     uint32_t *act = nullptr;
@@ -1398,14 +1629,14 @@ struct Work {
     PatState pst{};
     uint8_t *traceV = nullptr;
     bool full_order = false;  // trace: order every candidate (not only what the rounds read)
-    int probe_gs, probe_smem, count_smem, rx_smem, ham_smem, hsort_smem, vr_smem, scan_smem, pat_smem;
+    int probe_gs, probe_smem, count_smem, countw_smem, rx_smem, ham_smem, hsort_smem, vr_smem, scan_smem, pat_smem;
 
     static int64_t per_query_bytes(const crisp_index *ix, int k, int mode, int64_t CAPQ, bool traceV) {
         const int KK = ix->K * ix->K;
         const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));
         const int S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));
         int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 4 + (int64_t)ix->M * 12 + CAPQ * 4 +
-                       (int64_t)ix->NB * 8 + 64;
+                       (int64_t)ix->NBW * 8 + 64;
         if (mode == 0) perq += (int64_t)S * k * 16;
         else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
         if (traceV) perq += ix->N;
@@ -1421,14 +1652,16 @@ struct Work {
         S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
         R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
         BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 8)));  // id blocks per count CTA
+        count_kernel = env_int("CRISP_COUNT_KERNEL", 1);  // 0: k_count_select, 1: k_count_warp
+        NS = count_kernel == 0 ? NB : ix->NBW;  // candidate segments per query (id blocks or sub-blocks)
         qpad = buf.alloc<float>((size_t)Qc * pitch);
         qrot = ix->rotated ? buf.alloc<float>((size_t)Qc * pitch) : qpad;
         act = buf.alloc<uint32_t>((size_t)Qc * M * KK);
         act_len = buf.alloc<int32_t>((size_t)Qc * M);
         retr = buf.alloc<int64_t>((size_t)Qc * M);
         pool = buf.alloc<int32_t>((size_t)Qc * CAPQ);
-        ncand = buf.alloc<int32_t>((size_t)Qc * NB);
-        cbase = buf.alloc<int32_t>((size_t)Qc * NB);
+        ncand = buf.alloc<int32_t>((size_t)Qc * NS);
+        cbase = buf.alloc<int32_t>((size_t)Qc * NS);
         cursor = buf.alloc<int32_t>((size_t)Qc + 1);  // [Qc] = overflow need
         need = cursor + Qc;
         fb = buf.alloc<int32_t>((size_t)Qc);
@@ -1454,8 +1687,9 @@ struct Work {
         probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
         probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
-        rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NB + 1) * 4;
-        ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NB + 1) * 4;
+        countw_smem = BS + 16 + (int)sizeof(CountWSmem);
+        rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NS + 1) * 4;
+        ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NS + 1) * 4;
         hsort_smem = (Dp + 1) * 4;
         vr_smem = pitch * 8;
         scan_smem = WARPS * k * 16;
@@ -1493,9 +1727,18 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
         StageScope st(s, 2);
         CRISP_CUDA(cudaMemsetAsync(w.cursor, 0, (size_t)(w.Qc + 1) * 4, s));
         dim3 g(nblk(NB, w.BPC), (unsigned)qn);
-        k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N, ix->BS,
-                                                        w.BPC, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase, w.ncand,
-                                                        w.need, w.traceV);
+        if (w.count_kernel == 0)
+            k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N,
+                                                            ix->BS, w.BPC, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase,
+                                                            w.ncand, w.need, w.traceV);
+        else if (2 * M < 128)
+            k_count_warp<true><<<g, THREADS, w.countw_smem, s>>>(
+                w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
+                w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV);
+        else
+            k_count_warp<false><<<g, THREADS, w.countw_smem, s>>>(
+                w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
+                w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV);
         CRISP_LAUNCH();
         g_launches++;
     }
@@ -1513,7 +1756,7 @@ static void run_fallback_local(Work &w, int64_t qn, cudaStream_t s) {
     StageScope st(s, 3);
     k_fallback<<<(unsigned)qn, THREADS, w.count_smem, s>>>(w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB,
                                                            ix->ids, ix->N, ix->BS, w.k, w.pool, w.CAPQ, w.cbase,
-                                                           w.ncand, w.fb);
+                                                           w.ncand, w.NS, w.fb);
     CRISP_LAUNCH();
     g_launches++;
 }
@@ -1521,7 +1764,7 @@ static void run_fallback_local(Work &w, int64_t qn, cudaStream_t s) {
 // a4 (phi=1 Hamming order) + a5 for queries [0, qn) of the chunk -> outputs
 static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64, cudaStream_t s) {
     const crisp_index *ix = w.ix;
-    const int NB = ix->NB, pitch = ix->pitch, Dp = ix->Dp, k = w.k;
+    const int NB = w.NS, pitch = ix->pitch, Dp = ix->Dp, k = w.k;  // NB: candidate segments
     if (!od64) od64 = w.d64tmp;
     if (w.mode == 0) {
         {
@@ -1580,14 +1823,14 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
 static void run_stats(Work &w, int64_t qn, cudaStream_t s) {
     if (!g_timing) return;
     const crisp_index *ix = w.ix;
-    k_stats<<<(unsigned)qn, 128, 0, s>>>(w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB, w.ncand,
+    k_stats<<<(unsigned)qn, 128, 0, s>>>(w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB, w.ncand, w.NS,
                                          w.mode == 1 ? w.nver : nullptr, w.fb, qn);
     CRISP_LAUNCH();
     g_launches++;
 }
 
 static void trace_candidates(Work &w, int64_t q0, int64_t qn, const crisp_trace_t *tr, cudaStream_t s) {
-    const int NB = w.ix->NB;
+    const int NB = w.NS;  // candidate segments
     const int64_t N = w.ix->N, CAPQ = w.CAPQ;
     std::vector<int32_t> h_pool((size_t)qn * CAPQ), h_ncand((size_t)qn * NB), h_cbase((size_t)qn * NB);
     CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), w.pool, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
@@ -1612,7 +1855,7 @@ static void trace_candidates(Work &w, int64_t q0, int64_t qn, const crisp_trace_
 
 static void trace_rest(Work &w, int64_t q0, int64_t qn, const crisp_trace_t *tr, cudaStream_t s) {
     const crisp_index *ix = w.ix;
-    const int M = ix->M, KK = ix->K * ix->K, NB = ix->NB, Dp = ix->Dp, pitch = ix->pitch;
+    const int M = ix->M, KK = ix->K * ix->K, NB = w.NS, Dp = ix->Dp, pitch = ix->pitch;  // NB: segments
     const int64_t N = ix->N, CAPQ = w.CAPQ;
     std::vector<int32_t> hl((size_t)qn * M), h_pool, h_ncand;
     std::vector<uint32_t> ha;
@@ -1734,7 +1977,7 @@ crisp_session *session_begin(const crisp_index *ix, const float *queries, int64_
             run_front(*w, queries, Q, s);
             const int32_t need = read_need(*w, s);
             if (need <= cap) {
-                k_local_counts<<<nblk(Q, 256), 256, 0, s>>>(w->ncand, ix->NB, Q, local_counts);
+                k_local_counts<<<nblk(Q, 256), 256, 0, s>>>(w->ncand, w->NS, Q, local_counts);
                 CRISP_LAUNCH();
                 g_launches++;
                 return new crisp_session{ix, w, Q, k, mode};
@@ -1766,7 +2009,7 @@ void session_finish(crisp_session *ss, const int32_t *gcount, const int32_t *all
         StageScope st(s, 3);
         k_fb_select<<<(unsigned)ss->Q, THREADS, w.count_smem, s>>>(
             w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB, ix->ids, ix->N, ix->BS, ss->k, gcount, allhist,
-            G, rank, ss->Q, w.pool, w.CAPQ, w.cbase, w.ncand, w.fb);
+            G, rank, ss->Q, w.pool, w.CAPQ, w.cbase, w.ncand, w.NS, w.fb);
         CRISP_LAUNCH();
         g_launches++;
     }

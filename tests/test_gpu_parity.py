@@ -96,9 +96,12 @@ def compare_trace(t, ot, mode, N):
         assert np.array_equal(t["n_verified"], ot["n_verified"]), "a5 patience stop"
 
 
+@pytest.mark.parametrize("count_kernel", [0, 1])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_cfg1_stagewise(crisp, mode):
-    """BASELINE configs[0] (PR1: N=20k, D=256, Q=100, k=10) in full, M=8."""
+def test_cfg1_stagewise(crisp, monkeypatch, mode, count_kernel):
+    """BASELINE configs[0] (PR1: N=20k, D=256, Q=100, k=10) in full, M=8;
+    both collision-count kernels (block-staged and warp-owned counters)."""
+    monkeypatch.setenv("CRISP_COUNT_KERNEL", str(count_kernel))
     X, Qv, ox = make_case()
     ix = build_gpu(crisp, X, ox)
     compare_index(ix, ox)
@@ -113,10 +116,12 @@ def test_cfg1_stagewise(crisp, mode):
     assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
 
 
+@pytest.mark.parametrize("count_kernel", [0, 1])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_rotated_multiblock_ragged(crisp, mode):
+def test_rotated_multiblock_ragged(crisp, monkeypatch, mode, count_kernel):
     """Rotation injected (R from the oracle), 5 id blocks with a ragged tail,
     D not a multiple of 2M (zero padding), K=31."""
+    monkeypatch.setenv("CRISP_COUNT_KERNEL", str(count_kernel))
     X, Qv, ox = make_case(cfg=2, N=18001, D=90, Q=40, M=4, K=31, rotation=1, seed=3)
     assert ox["rotated"] and ox["Dp"] == 96
     ix = build_gpu(crisp, X, ox, block_ids=4096)
