@@ -464,10 +464,16 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
                                                            int NB, int tau, int32_t *__restrict__ pool, int64_t CAPQ,
                                                            int32_t *__restrict__ cursor, int32_t *__restrict__ cbase,
                                                            int32_t *__restrict__ ncand, int32_t *__restrict__ need,
-                                                           uint8_t *__restrict__ traceV) {
+                                                           uint8_t *__restrict__ traceV, const float *__restrict__ qrot,
+                                                           int pitch, int Dp, const uint64_t *__restrict__ codes,
+                                                           int Wd, uint16_t *__restrict__ hbuf,
+                                                           int32_t *__restrict__ ghist) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;  // BS byte counters (+16 dummy bytes); warp w owns [w*SBW, (w+1)*SBW)
     CountWSmem &S = *(CountWSmem *)(smraw + BS + 16);
+    // phi=1 (hbuf != null): b(q') and the query's Hamming histogram of this CTA
+    uint64_t *qc = (uint64_t *)(smraw + BS + 16 + ((sizeof(CountWSmem) + 15) & ~(size_t)15));  // Wd
+    int *hist = (int *)(qc + Wd);                                                              // Dp + 1
     const int64_t q = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int SBW = BS >> 3;
@@ -492,6 +498,15 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
         if (lane == 0) S.lpre[0] = 0;
     }
     for (int i = tid; i < SBW * WARPS / 16; i += THREADS) ((uint4 *)cnt8)[i] = make_uint4(0, 0, 0, 0);
+    if (hbuf) {
+        const float *qrow = qrot + q * pitch;
+        for (int d0 = warp * 32; d0 < Wd * 64; d0 += THREADS) {  // bit (i mod 64) of word i/64 = [q'_i > 0] (Z10)
+            const int d = d0 + lane;
+            const unsigned bits = __ballot_sync(0xffffffffu, d < Dp && qrow[d] > 0.0f);
+            if (lane == 0) ((uint32_t *)qc)[d0 >> 5] = bits;
+        }
+        for (int i = tid; i < Dp + 1; i += THREADS) hist[i] = 0;
+    }
     __syncthreads();
     const int Etot = S.lpre[M];
     const bool cached = Etot <= CS_CAP;
@@ -644,6 +659,56 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
             }
             run += ctot[i];
         }
+        if (hbuf && n > 0) {
+            // a4, phi=1: h(x) = popcount(b(q') xor b(x)) (Alg. 1 l.19) of this segment's
+            // candidates; 4 lanes per candidate, 16 candidates per pass, h at the pool position
+            __syncwarp();
+            const int g4 = lane >> 2, gl = lane & 3, wpl = (Wd + 3) >> 2;
+            for (int v0 = 0; v0 < n; v0 += 16) {
+                int pos[2], id[2];
+                bool okv[2];
+#pragma unroll
+                for (int r = 0; r < 2; r++) {
+                    const int vi = v0 + r * 8 + g4;
+                    pos[r] = base + vi;
+                    okv[r] = vi < n && pos[r] < CAPQ;
+                    id[r] = okv[r] ? outp[pos[r]] : 0;
+                }
+                int h0 = 0, h1 = 0;
+#pragma unroll 4
+                for (int t = 0; t < wpl; t++) {
+                    const int wd = gl + 4 * t;
+                    const int wc2 = min(wd, Wd - 1);
+                    const uint64_t qw = qc[wc2];
+                    const int c0 = __popcll(qw ^ __ldg(codes + (int64_t)id[0] * Wd + wc2));
+                    const int c1 = __popcll(qw ^ __ldg(codes + (int64_t)id[1] * Wd + wc2));
+                    if (wd < Wd) {
+                        h0 += c0;
+                        h1 += c1;
+                    }
+                }
+                h0 += __shfl_xor_sync(0xffffffffu, h0, 1);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+                h0 += __shfl_xor_sync(0xffffffffu, h0, 2);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                if (gl == 0) {
+                    if (okv[0]) {
+                        hbuf[q * CAPQ + pos[0]] = (uint16_t)h0;
+                        atomicAdd(&hist[h0], 1);
+                    }
+                    if (okv[1]) {
+                        hbuf[q * CAPQ + pos[1]] = (uint16_t)h1;
+                        atomicAdd(&hist[h1], 1);
+                    }
+                }
+            }
+        }
+    }
+    if (hbuf) {
+        __syncthreads();
+        int32_t *gh = ghist + q * (int64_t)(Dp + 1);
+        for (int i = tid; i < Dp + 1; i += THREADS)
+            if (hist[i]) atomicAdd(&gh[i], hist[i]);
     }
 }
 
@@ -745,7 +810,8 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
                                                        const int32_t *__restrict__ ids, int64_t N, int BS, int k,
                                                        int32_t *__restrict__ pool, int64_t CAPQ,
                                                        int32_t *__restrict__ cbase, int32_t *__restrict__ ncand, int NS,
-                                                       int32_t *__restrict__ fbflag) {
+                                                       int32_t *__restrict__ fbflag, int32_t *__restrict__ ghist,
+                                                       int GHB) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;
     CountSmem &S = *(CountSmem *)(smraw + BS + BS / 8);
@@ -753,12 +819,15 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
     __shared__ int s_total, s_vstar, s_quota, s_eqbase, s_n;
     const int64_t q = blockIdx.x;
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        int t = 0;
-        for (int b = 0; b < NS; b++) t += ncand[q * NS + b];
-        s_total = t;
-    }
+    if (tid == 0) s_total = 0;
     for (int i = tid; i < 2 * MAX_M + 2; i += THREADS) hist[i] = 0;
+    __syncthreads();
+    {
+        int t = 0;
+        for (int b = tid; b < NS; b += THREADS) t += ncand[q * NS + b];
+        for (int off = 16; off; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if ((tid & 31) == 0 && t) atomicAdd(&s_total, t);
+    }
     __syncthreads();
     if (s_total >= k) {
         if (tid == 0) fbflag[q] = 0;
@@ -774,6 +843,9 @@ __global__ void __launch_bounds__(THREADS) k_fallback(const uint32_t *__restrict
         ncand[q * NS + b] = (b == 0) ? n : 0;
         cbase[q * NS + b] = 0;
     }
+    // phi=1: the Hamming histogram of the replaced candidate set restarts (k_hamming refills it)
+    if (ghist)
+        for (int i = tid; i < GHB; i += THREADS) ghist[q * GHB + i] = 0;
     if (tid == 0) fbflag[q] = 1;
 }
 
@@ -808,7 +880,8 @@ __global__ void __launch_bounds__(THREADS) k_fb_select(const uint32_t *__restric
                                                         const int32_t *__restrict__ allhist, int G, int rank, int64_t Q,
                                                         int32_t *__restrict__ pool, int64_t CAPQ,
                                                         int32_t *__restrict__ cbase, int32_t *__restrict__ ncand,
-                                                        int NS, int32_t *__restrict__ fbflag) {
+                                                        int NS, int32_t *__restrict__ fbflag,
+                                                        int32_t *__restrict__ ghist, int GHB) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;
     CountSmem &S = *(CountSmem *)(smraw + BS + BS / 8);
@@ -843,6 +916,9 @@ __global__ void __launch_bounds__(THREADS) k_fb_select(const uint32_t *__restric
         ncand[q * NS + b] = (b == 0) ? n : 0;
         cbase[q * NS + b] = 0;
     }
+    // phi=1: the Hamming histogram of the replaced candidate set restarts (k_hamming refills it)
+    if (ghist)
+        for (int i = tid; i < GHB; i += THREADS) ghist[q * GHB + i] = 0;
     if (tid == 0) fbflag[q] = 1;
 }
 
@@ -1116,15 +1192,15 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
                                                       const int32_t *__restrict__ pool, int64_t CAPQ,
                                                       const int32_t *__restrict__ cbase,
                                                       const int32_t *__restrict__ ncand, int NB,
-                                                      int32_t *__restrict__ cbuf, uint16_t *__restrict__ hbuf,
-                                                      int32_t *__restrict__ ghist) {
+                                                      uint16_t *__restrict__ hbuf, int32_t *__restrict__ ghist,
+                                                      const int32_t *__restrict__ only_fb) {
     extern __shared__ __align__(16) unsigned char sm[];
     uint64_t *qc = (uint64_t *)sm;          // Wd
     int *hist = (int *)(qc + Wd);           // Dp + 1
     int *pre = hist + Dp + 1;               // NB + 1
     int *cbs = pre + NB + 1;                // NB
-    const int64_t CS = CAPQ;
     const int64_t q = blockIdx.y;
+    if (only_fb && !only_fb[q]) return;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float *qrow = qrot + q * pitch;
     for (int w = tid; w < Wd; w += THREADS) {
@@ -1149,15 +1225,17 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
     int bl = 0;  // block of this lane's candidate (monotone in v)
     for (int v0 = v_lo + warp * 32; v0 < v_hi; v0 += WARPS * 32) {
         const int v = v0 + lane;
-        int lid = -1;
+        int lid = -1, pos = 0;
         if (v < v_hi) {
             while (pre[bl + 1] <= v) bl++;
-            lid = __ldg(poolq + cbs[bl] + (v - pre[bl]));
+            pos = cbs[bl] + (v - pre[bl]);
+            lid = __ldg(poolq + pos);
         }
 #pragma unroll 4
         for (int r = 0; r < 32 / gpw; r++) {
             const int src = r * gpw + g;
             const int lr = __shfl_sync(0xffffffffu, lid, src);
+            const int ps = __shfl_sync(0xffffffffu, pos, src);
             int hv = 0;
             if (lr >= 0) {
                 const uint64_t *cr = codes + (int64_t)lr * Wd;
@@ -1166,9 +1244,7 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
             }
             for (int off = G >> 1; off; off >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, off);
             if (lr >= 0 && gl == 0) {
-                const int vs = v0 + src;
-                cbuf[q * CS + vs] = lr;
-                hbuf[q * CS + vs] = (uint16_t)hv;
+                hbuf[q * CAPQ + ps] = (uint16_t)hv;  // h at the candidate's pool position
                 atomicAdd(&hist[hv], 1);
             }
         }
@@ -1186,7 +1262,10 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
 // bins whose start is below `limit` are scattered (the positions the
 // speculative rounds read); limit = INT_MAX scatters everything.
 __device__ int hsort_warp(const int32_t *__restrict__ gh, int Dp, const int32_t *__restrict__ cq,
-                          const uint16_t *__restrict__ hq, int32_t *__restrict__ out, int *start, int limit) {
+                          const uint16_t *__restrict__ hq, const int *pre, const int *cbs, int32_t *__restrict__ out,
+                          int *start, int limit) {
+    // cq/hq: the query's pool (ids, h) at candidate positions; pre/cbs: the
+    // segment prefix and bases (ascending id order = ascending segments)
     const int lane = threadIdx.x & 31;
     int acc = 0, cut = -1;
     for (int b0 = 0; b0 < Dp + 1; b0 += 32) {
@@ -1208,13 +1287,20 @@ __device__ int hsort_warp(const int32_t *__restrict__ gh, int Dp, const int32_t 
     __syncwarp();
     const bool full = cut >= Dp;
     constexpr int U = 8;  // chunks of 32 loaded ahead (independent loads)
+    int bl = 0;           // segment of this lane's position (monotone)
     for (int v00 = 0; v00 < total; v00 += 32 * U) {
         int hh[U], ll[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int v = v00 + u * 32 + lane;
-            hh[u] = v < total ? hq[v] : 0x7fffffff;
-            ll[u] = v < total ? cq[v] : 0;
+            hh[u] = 0x7fffffff;
+            ll[u] = 0;
+            if (v < total) {
+                while (pre[bl + 1] <= v) bl++;
+                const int pos = cbs[bl] + (v - pre[bl]);
+                hh[u] = hq[pos];
+                ll[u] = cq[pos];
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -1256,16 +1342,39 @@ __device__ int hsort_warp(const int32_t *__restrict__ gh, int Dp, const int32_t 
 
 // k_hsort: one warp per query; order (h, id) of the positions the speculative
 // rounds read, written over the query's pool region.
-__global__ void __launch_bounds__(32) k_hsort(const int32_t *__restrict__ ncand, int NB, int Dp,
-                                              const int32_t *__restrict__ ghist, const int32_t *__restrict__ cbuf,
-                                              const uint16_t *__restrict__ hbuf, int64_t CS,
-                                              int32_t *__restrict__ pool, int64_t PS, int32_t *__restrict__ total_out,
+__device__ void warp_segments(const int32_t *__restrict__ ncand, const int32_t *__restrict__ cbase, int64_t q, int NS,
+                              int *pre, int *cbs) {
+    const int lane = threadIdx.x & 31;
+    int acc = 0;
+    for (int b0 = 0; b0 < NS; b0 += 32) {
+        const int b = b0 + lane;
+        int v = b < NS ? ncand[q * NS + b] : 0;
+        if (b < NS) cbs[b] = cbase[q * NS + b];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off) v += t;
+        }
+        if (b < NS) pre[b + 1] = acc + v;
+        acc += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) pre[0] = 0;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) k_hsort(const int32_t *__restrict__ ncand, const int32_t *__restrict__ cbase,
+                                              int NS, int Dp, const int32_t *__restrict__ ghist,
+                                              const int32_t *__restrict__ pool, const uint16_t *__restrict__ hbuf,
+                                              int64_t CS, int32_t *__restrict__ order, int32_t *__restrict__ total_out,
                                               int limit) {
     extern __shared__ __align__(16) unsigned char sm[];
-    int *start = (int *)sm;  // Dp + 1
+    int *start = (int *)sm;       // Dp + 1
+    int *pre = start + Dp + 1;    // NS + 1
+    int *cbs = pre + NS + 1;      // NS
     const int64_t q = blockIdx.x;
-    const int total = hsort_warp(ghist + q * (int64_t)(Dp + 1), Dp, cbuf + q * CS, hbuf + q * CS, pool + q * PS, start,
-                                 limit);
+    warp_segments(ncand, cbase, q, NS, pre, cbs);
+    const int total = hsort_warp(ghist + q * (int64_t)(Dp + 1), Dp, pool + q * CS, hbuf + q * CS, pre, cbs,
+                                 order + q * CS, start, limit);
     if (threadIdx.x == 0) total_out[q] = total;
 }
 
@@ -1411,13 +1520,15 @@ __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int
 // sequential verification from position `from`.
 __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restrict__ qrot, int pitch,
                                                             const float *__restrict__ X, int64_t gid_base,
-                                                            int32_t *__restrict__ pool, int64_t PS,
+                                                            int32_t *__restrict__ order, int64_t PS,
                                                             const int32_t *__restrict__ totals, int from, int k, int P,
                                                             PatState st, double *__restrict__ out_d64,
                                                             float *__restrict__ out_d, int64_t *__restrict__ out_i,
                                                             int Dp, const int32_t *__restrict__ ghist,
-                                                            const int32_t *__restrict__ cbuf,
-                                                            const uint16_t *__restrict__ hbuf) {
+                                                            const int32_t *__restrict__ pool,
+                                                            const uint16_t *__restrict__ hbuf,
+                                                            const int32_t *__restrict__ ncand,
+                                                            const int32_t *__restrict__ cbase, int NS) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int64_t q = blockIdx.x;
     if (st.done[q]) return;
@@ -1427,13 +1538,17 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
     double *Td = (double *)(chi + PATIENCE_CH);      // k
     int64_t *Ti = (int64_t *)(Td + k);               // k
     int *hstart = (int *)(Ti + k);                   // Dp + 1
+    int *spre = hstart + Dp + 1;                     // NS + 1
+    int *scbs = spre + NS + 1;                       // NS
     __shared__ int s_stop, s_cnt;
     __shared__ int64_t s_nver;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // k_hsort ordered only the positions the rounds read: complete the order
-    if (warp == 0)
-        hsort_warp(ghist + q * (int64_t)(Dp + 1), Dp, cbuf + q * PS, hbuf + q * PS, pool + q * PS, hstart,
-                   0x7fffffff);
+    if (warp == 0) {
+        warp_segments(ncand, cbase, q, NS, spre, scbs);
+        hsort_warp(ghist + q * (int64_t)(Dp + 1), Dp, pool + q * PS, hbuf + q * PS, spre, scbs, order + q * PS,
+                   hstart, 0x7fffffff);
+    }
     __syncthreads();
     load_qd(qd, qrot + q * pitch, pitch);
     int cnt_top = st.cnt[q], pat = st.pat[q];
@@ -1447,7 +1562,7 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
     }
     __syncthreads();
     const int total = totals[q];
-    const int32_t *ord = pool + q * PS;
+    const int32_t *ord = order + q * PS;
     const int nvec = pitch / 4;
     int64_t nver = total;
     for (int pos = from; pos < total; pos += PATIENCE_CH) {
@@ -1629,7 +1744,7 @@ struct Work {
     PatState pst{};
     uint8_t *traceV = nullptr;
     bool full_order = false;  // trace: order every candidate (not only what the rounds read)
-    int probe_gs, probe_smem, count_smem, countw_smem, rx_smem, ham_smem, hsort_smem, vr_smem, scan_smem, pat_smem;
+    int probe_gs, probe_smem, count_smem, countw_smem, countw_ham_smem, rx_smem, ham_smem, hsort_smem, vr_smem, scan_smem, pat_smem;
 
     static int64_t per_query_bytes(const crisp_index *ix, int k, int mode, int64_t CAPQ, bool traceV) {
         const int KK = ix->K * ix->K;
@@ -1687,13 +1802,14 @@ struct Work {
         probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
         probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
-        countw_smem = BS + 16 + (int)sizeof(CountWSmem);
+        countw_smem = BS + 16 + (int)((sizeof(CountWSmem) + 15) & ~(size_t)15);
+        countw_ham_smem = ix->W * 8 + (Dp + 1) * 4;
         rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NS + 1) * 4;
         ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NS + 1) * 4;
-        hsort_smem = (Dp + 1) * 4;
+        hsort_smem = (Dp + 1 + 2 * NS + 1) * 4;
         vr_smem = pitch * 8;
         scan_smem = WARPS * k * 16;
-        pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + (Dp + 1) * 4;
+        pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + (Dp + 1 + 2 * NS + 1) * 4;
         set_attrs();
         CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
                         pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
@@ -1726,19 +1842,26 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
     {
         StageScope st(s, 2);
         CRISP_CUDA(cudaMemsetAsync(w.cursor, 0, (size_t)(w.Qc + 1) * 4, s));
+        if (w.mode == 1) CRISP_CUDA(cudaMemsetAsync(w.ghist, 0, (size_t)qn * (ix->Dp + 1) * 4, s));
         dim3 g(nblk(NB, w.BPC), (unsigned)qn);
         if (w.count_kernel == 0)
             k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N,
                                                             ix->BS, w.BPC, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase,
                                                             w.ncand, w.need, w.traceV);
-        else if (2 * M < 128)
-            k_count_warp<true><<<g, THREADS, w.countw_smem, s>>>(
-                w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
-                w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV);
-        else
-            k_count_warp<false><<<g, THREADS, w.countw_smem, s>>>(
-                w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
-                w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV);
+        else {
+            uint16_t *hb = w.mode == 1 ? w.hbuf : nullptr;  // phi=1: Hamming fused into the count
+            const int smem = w.countw_smem + (w.mode == 1 ? w.countw_ham_smem : 0);
+            if (2 * M < 128)
+                k_count_warp<true><<<g, THREADS, smem, s>>>(
+                    w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
+                    w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->W, hb,
+                    w.ghist);
+            else
+                k_count_warp<false><<<g, THREADS, smem, s>>>(
+                    w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
+                    w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->W, hb,
+                    w.ghist);
+        }
         CRISP_LAUNCH();
         g_launches++;
     }
@@ -1756,7 +1879,7 @@ static void run_fallback_local(Work &w, int64_t qn, cudaStream_t s) {
     StageScope st(s, 3);
     k_fallback<<<(unsigned)qn, THREADS, w.count_smem, s>>>(w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB,
                                                            ix->ids, ix->N, ix->BS, w.k, w.pool, w.CAPQ, w.cbase,
-                                                           w.ncand, w.NS, w.fb);
+                                                           w.ncand, w.NS, w.fb, w.ghist, ix->Dp + 1);
     CRISP_LAUNCH();
     g_launches++;
 }
@@ -1784,38 +1907,40 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         return;
     }
     const int P = ix->patience_factor > 0 ? ix->patience_factor * k : 0;
-    CRISP_CUDA(cudaMemsetAsync(w.ghist, 0, (size_t)qn * (Dp + 1) * 4, s));
     CRISP_CUDA(cudaMemsetAsync(w.pst.cnt, 0, (size_t)w.Qc * 3 * 4, s));
     {
+        // k_count_warp computed h and the histogram with the count; only
+        // queries whose candidate set the fallback replaced are done here
         StageScope st(s, 6);
         dim3 g(w.HS, (unsigned)qn);
         k_hamming<<<g, THREADS, w.ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->W, w.pool, w.CAPQ, w.cbase, w.ncand,
-                                                 NB, w.cbuf, w.hbuf, w.ghist);
+                                                 NB, w.hbuf, w.ghist, w.count_kernel == 0 ? nullptr : w.fb);
         CRISP_LAUNCH();
         g_launches++;
     }
     {
+        // (h, id) order into cbuf
         StageScope st(s, 7);
-        k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, NB, Dp, w.ghist, w.cbuf, w.hbuf, w.CAPQ, w.pool, w.CAPQ,
-                                                       w.totals, w.full_order ? 0x7fffffff : w.R0 * w.S0);
+        k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ,
+                                                       w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.R0 * w.S0);
         CRISP_LAUNCH();
         g_launches++;
     }
     StageScope st(s, 4);
     for (int r = 0; r < w.R0; r++) {
         dim3 g(w.S, (unsigned)qn);
-        k_verify_rows<<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.pool, w.CAPQ, w.totals, w.pst.done, r,
+        k_verify_rows<<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst.done, r,
                                                     w.S0, w.dbuf);
         CRISP_LAUNCH();
         g_launches++;
-        k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.pool, w.CAPQ, ix->gid_base,
+        k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.cbuf, w.CAPQ, ix->gid_base,
                                                                       w.dbuf, r, w.S0, k, P, w.pst, od64, od, oi);
         CRISP_LAUNCH();
         g_launches++;
     }
-    k_patience_tail<<<(unsigned)qn, THREADS, w.pat_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ,
+    k_patience_tail<<<(unsigned)qn, THREADS, w.pat_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.cbuf, w.CAPQ,
                                                               w.totals, w.R0 * w.S0, k, P, w.pst, od64, od, oi, Dp,
-                                                              w.ghist, w.cbuf, w.hbuf);
+                                                              w.ghist, w.pool, w.hbuf, w.ncand, w.cbase, NB);
     CRISP_LAUNCH();
     g_launches++;
 }
@@ -1878,7 +2003,7 @@ static void trace_rest(Work &w, int64_t q0, int64_t qn, const crisp_trace_t *tr,
         h_pool.resize((size_t)qn * CAPQ);
         h_ncand.resize((size_t)qn * NB);
         CRISP_CUDA(cudaMemcpyAsync(hn.data(), w.nver, (size_t)qn * 8, cudaMemcpyDeviceToHost, s));
-        CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), w.pool, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
+        CRISP_CUDA(cudaMemcpyAsync(h_pool.data(), w.cbuf, (size_t)qn * CAPQ * 4, cudaMemcpyDeviceToHost, s));
         CRISP_CUDA(cudaMemcpyAsync(h_ncand.data(), w.ncand, (size_t)qn * NB * 4, cudaMemcpyDeviceToHost, s));
     }
     CRISP_CUDA(cudaStreamSynchronize(s));
@@ -2009,7 +2134,7 @@ void session_finish(crisp_session *ss, const int32_t *gcount, const int32_t *all
         StageScope st(s, 3);
         k_fb_select<<<(unsigned)ss->Q, THREADS, w.count_smem, s>>>(
             w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB, ix->ids, ix->N, ix->BS, ss->k, gcount, allhist,
-            G, rank, ss->Q, w.pool, w.CAPQ, w.cbase, w.ncand, w.NS, w.fb);
+            G, rank, ss->Q, w.pool, w.CAPQ, w.cbase, w.ncand, w.NS, w.fb, w.ghist, ix->Dp + 1);
         CRISP_LAUNCH();
         g_launches++;
     }
