@@ -467,14 +467,15 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
                                                            uint8_t *__restrict__ traceV, const float *__restrict__ qrot,
                                                            int pitch, int Dp, const uint64_t *__restrict__ codes,
                                                            int Wd, uint16_t *__restrict__ hbuf,
-                                                           int32_t *__restrict__ ghist) {
+                                                           int32_t *__restrict__ ghist,
+                                                           const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;  // BS byte counters (+16 dummy bytes); warp w owns [w*SBW, (w+1)*SBW)
     CountWSmem &S = *(CountWSmem *)(smraw + BS + 16);
     // phi=1 (hbuf != null): b(q') and the query's Hamming histogram of this CTA
     uint64_t *qc = (uint64_t *)(smraw + BS + 16 + ((sizeof(CountWSmem) + 15) & ~(size_t)15));  // Wd
     int *hist = (int *)(qc + Wd);                                                              // Dp + 1
-    const int64_t q = blockIdx.y;
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int SBW = BS >> 3;
     const int b_lo = blockIdx.x * BPC, b_hi = min(NB, b_lo + BPC);
@@ -922,6 +923,20 @@ __global__ void __launch_bounds__(THREADS) k_fb_select(const uint32_t *__restric
     if (tid == 0) fbflag[q] = 1;
 }
 
+// Query locality order: queries whose first-ranked cells in subspaces 0 and 1
+// agree share most of their candidates (and so their CSR slices, codes and
+// rows in L2); the count and verification grids visit queries in the order of
+// this key.  A pure scheduling permutation: every per-query result is the same.
+__global__ void k_query_key(const uint32_t *__restrict__ act, int M, int KK, int64_t Qc, uint32_t *__restrict__ key,
+                            int32_t *__restrict__ iota) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Qc) return;
+    const uint32_t *a = act + q * (int64_t)M * KK;
+    const uint32_t c0 = a[0] & 0xffffu, c1 = M > 1 ? (a[KK] & 0xffffu) : 0u;
+    key[q] = c0 * (uint32_t)KK + c1;
+    iota[q] = (int32_t)q;
+}
+
 __global__ void k_local_counts(const int32_t *__restrict__ ncand, int NB, int64_t Qc, int32_t *__restrict__ out) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= Qc) return;
@@ -1043,7 +1058,8 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
                                                            const int32_t *__restrict__ pool, int64_t CAPQ,
                                                            const int32_t *__restrict__ cbase,
                                                            const int32_t *__restrict__ ncand, int NB, int k,
-                                                           double *__restrict__ part_d, int64_t *__restrict__ part_i) {
+                                                           double *__restrict__ part_d, int64_t *__restrict__ part_i,
+                                                           const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
     double *Ld = qd + pitch;                         // WARPS x k
@@ -1051,7 +1067,7 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
     int *pre = (int *)(Li + WARPS * k);              // NB + 1
     int *cbs = pre + NB + 1;                         // NB
     __shared__ int wcnt[WARPS];
-    const int64_t q = blockIdx.y;
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     load_qd(qd, qrot + q * pitch, pitch);
     block_prefix(ncand, cbase, q, NB, pre, cbs);
@@ -1399,10 +1415,11 @@ __global__ void __launch_bounds__(THREADS) k_verify_rows(const float *__restrict
                                                           const float *__restrict__ X, const int32_t *__restrict__ pool,
                                                           int64_t PS, const int32_t *__restrict__ totals,
                                                           const int32_t *__restrict__ done, int r, int S0,
-                                                          double *__restrict__ dbuf) {
+                                                          double *__restrict__ dbuf,
+                                                          const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
-    const int64_t q = blockIdx.y;
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
     if (done[q]) return;
     const int total = totals[q];
     const int j0 = r * S0;
@@ -1528,9 +1545,10 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
                                                             const int32_t *__restrict__ pool,
                                                             const uint16_t *__restrict__ hbuf,
                                                             const int32_t *__restrict__ ncand,
-                                                            const int32_t *__restrict__ cbase, int NS) {
+                                                            const int32_t *__restrict__ cbase, int NS,
+                                                            const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char sm[];
-    const int64_t q = blockIdx.x;
+    const int64_t q = qperm ? qperm[blockIdx.x] : blockIdx.x;  // locality order (query_order)
     if (st.done[q]) return;
     double *qd = (double *)sm;                       // pitch
     double *chd = qd + pitch;                        // PATIENCE_CH
@@ -1740,6 +1758,10 @@ struct Work {
     double *part_d = nullptr, *dbuf = nullptr, *d64tmp = nullptr;
     int64_t *part_i = nullptr, *nver = nullptr;
     int32_t *cbuf = nullptr, *ghist = nullptr, *totals = nullptr;
+    uint32_t *qkey = nullptr, *qkey2 = nullptr;
+    int32_t *qiota = nullptr, *qperm = nullptr;  // qperm: query locality order (null: identity)
+    void *qsort_tmp = nullptr;
+    size_t qsort_bytes = 0;
     uint16_t *hbuf = nullptr;
     PatState pst{};
     uint8_t *traceV = nullptr;
@@ -1780,6 +1802,15 @@ struct Work {
         cursor = buf.alloc<int32_t>((size_t)Qc + 1);  // [Qc] = overflow need
         need = cursor + Qc;
         fb = buf.alloc<int32_t>((size_t)Qc);
+        if (env_int("CRISP_QUERY_ORDER", 1)) {
+            qkey = buf.alloc<uint32_t>((size_t)Qc);
+            qkey2 = buf.alloc<uint32_t>((size_t)Qc);
+            qiota = buf.alloc<int32_t>((size_t)Qc);
+            qperm = buf.alloc<int32_t>((size_t)Qc);
+            CRISP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, qsort_bytes, qkey, qkey2, qiota, qperm, (int)Qc, 0, 32,
+                                                       s));
+            qsort_tmp = buf.alloc<unsigned char>(qsort_bytes);
+        }
         if (mode == 0) {
             part_d = buf.alloc<double>((size_t)Qc * S * k);
             part_i = buf.alloc<int64_t>((size_t)Qc * S * k);
@@ -1838,6 +1869,16 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
                                                  ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr);
         CRISP_LAUNCH();
         g_launches++;
+        if (w.qperm) {
+            k_query_key<<<nblk(qn, 256), 256, 0, s>>>(w.act, M, KK, qn, w.qkey, w.qiota);
+            CRISP_LAUNCH();
+            g_launches++;
+            int bits = 1;
+            while ((1ull << bits) < (unsigned long long)KK * KK) bits++;
+            size_t tb = w.qsort_bytes;
+            CRISP_CUDA(cub::DeviceRadixSort::SortPairs(w.qsort_tmp, tb, w.qkey, w.qkey2, w.qiota, w.qperm, (int)qn, 0,
+                                                       bits, s));
+        }
     }
     {
         StageScope st(s, 2);
@@ -1855,12 +1896,12 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
                 k_count_warp<true><<<g, THREADS, smem, s>>>(
                     w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
                     w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->W, hb,
-                    w.ghist);
+                    w.ghist, w.qperm);
             else
                 k_count_warp<false><<<g, THREADS, smem, s>>>(
                     w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
                     w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->W, hb,
-                    w.ghist);
+                    w.ghist, w.qperm);
         }
         CRISP_LAUNCH();
         g_launches++;
@@ -1894,7 +1935,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
             StageScope st(s, 4);
             dim3 g(w.S, (unsigned)qn);
             k_rerank_exact<<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ, w.cbase,
-                                                         w.ncand, NB, k, w.part_d, w.part_i);
+                                                         w.ncand, NB, k, w.part_d, w.part_i, w.qperm);
             CRISP_LAUNCH();
             g_launches++;
         }
@@ -1930,7 +1971,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     for (int r = 0; r < w.R0; r++) {
         dim3 g(w.S, (unsigned)qn);
         k_verify_rows<<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst.done, r,
-                                                    w.S0, w.dbuf);
+                                                    w.S0, w.dbuf, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
         k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.cbuf, w.CAPQ, ix->gid_base,
@@ -1940,7 +1981,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     }
     k_patience_tail<<<(unsigned)qn, THREADS, w.pat_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.cbuf, w.CAPQ,
                                                               w.totals, w.R0 * w.S0, k, P, w.pst, od64, od, oi, Dp,
-                                                              w.ghist, w.pool, w.hbuf, w.ncand, w.cbase, NB);
+                                                              w.ghist, w.pool, w.hbuf, w.ncand, w.cbase, NB, w.qperm);
     CRISP_LAUNCH();
     g_launches++;
 }
