@@ -317,14 +317,15 @@ def run_crisp(args):
             kernels["verify"] = {"kernel": "k_rerank_exact" if mode == 0 else "k_verify_rows+k_patience_scan",
                                  "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
                                  "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
-        if st.get("hamming", 0) > 0:
-            hb = cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K  # SURVEY 8(d) B_ham
-            kernels["hamming"] = {"kernel": "k_hamming+k_hsort", "bytes_per_step": hb,
-                                  "ms_per_step": st["hamming"] / K, "achieved_gbs": hb / (st["hamming"] / K * 1e-3) / 1e9}
         if st["count_select"] > 0:
-            cb_ = cnt["ids_streamed"] * 4 / K  # 4 B per id streamed (SURVEY 8(d) B_count)
-            kernels["count"] = {"kernel": "k_count_select", "bytes_per_step": cb_,
-                                "ms_per_step": st["count_select"] / K,
+            # a3 streams 4 B per id (SURVEY 8(d) B_count); at phi=1 the same kernel
+            # (k_count_warp) also gathers 8*ceil(D'/64) B of code per candidate (B_ham)
+            cb_ = cnt["ids_streamed"] * 4 / K
+            name = "k_count_warp"
+            if mode == 1:
+                cb_ += cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K
+                name = "k_count_warp (collision count + fused Hamming)"
+            kernels["count"] = {"kernel": name, "bytes_per_step": cb_, "ms_per_step": st["count_select"] / K,
                                 "achieved_gbs": cb_ / (st["count_select"] / K * 1e-3) / 1e9}
         for kk in kernels.values():
             kk["frac_of_peak"] = kk["achieved_gbs"] / peak

@@ -49,10 +49,10 @@ static void apply_knobs(crisp_index *ix, double beta, int64_t budget, double alp
 }
 
 // ids per on-chip counter block: a power of two in [4096, 32768] (the count
-// kernel gives each of its 8 warps BS/8 counters)
+// kernel gives each of its 8 warps BS/8 <= 4096 counters)
 static int block_ids_for(int64_t N) {
     int cap = 32768;
-    if (const char *v = getenv("CRISP_BLOCK_IDS")) cap = std::max(4096, std::min(65536, atoi(v)));
+    if (const char *v = getenv("CRISP_BLOCK_IDS")) cap = std::max(4096, std::min(32768, atoi(v)));
     int bs = 4096;
     while (bs < cap && bs < N) bs <<= 1;
     while (bs > cap) bs >>= 1;

@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
             S.emw[t] = (uint32_t)m | f;
         }
     __syncthreads();
-    const int nchunk = SBW / 512;  // 16-byte lane chunks of the warp's counters
+    const int nchunk = SBW / 512;  // 16-byte lane chunks of the warp's counters (SBW <= 4096: <= 8)
     const uint32_t tau4 = (uint32_t)tau * 0x01010101u;
     int32_t *outp = pool + q * CAPQ;
     for (int b = b_lo; b < b_hi; b++) {
@@ -955,28 +955,39 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-__device__ __forceinline__ void acc4(double &acc, const float4 x, const double *qd4) {
-    const double2 q01 = *(const double2 *)(qd4);
-    const double2 q23 = *(const double2 *)(qd4 + 2);
-    double d0 = __dsub_rn((double)x.x, q01.x), d1 = __dsub_rn((double)x.y, q01.y);
-    double d2 = __dsub_rn((double)x.z, q23.x), d3 = __dsub_rn((double)x.w, q23.y);
+// The query is staged in shared memory as doubles in component-major order
+// (qd[c*nvec + v] = q'[4v + c], see load_qd) so that the lanes of a warp,
+// which take consecutive float4s v, read consecutive doubles (no bank
+// conflicts); one read serves both rows of row_dist2.
+struct Q4 {
+    double a, b, c, d;
+};
+__device__ __forceinline__ Q4 q4_at(const double *__restrict__ qd, int v, int nvec) {
+    return {qd[v], qd[nvec + v], qd[2 * nvec + v], qd[3 * nvec + v]};
+}
+__device__ __forceinline__ void acc4(double &acc, const float4 x, const Q4 &q) {
+    const double d0 = __dsub_rn((double)x.x, q.a), d1 = __dsub_rn((double)x.y, q.b);
+    const double d2 = __dsub_rn((double)x.z, q.c), d3 = __dsub_rn((double)x.w, q.d);
     acc = __fma_rn(d0, d0, acc);
     acc = __fma_rn(d1, d1, acc);
     acc = __fma_rn(d2, d2, acc);
     acc = __fma_rn(d3, d3, acc);
 }
 
-// two rows at once (more loads in flight)
+// Row distances, a warp per row: lane l takes the float4s l, l+32, ... of the
+// row in ascending order (its partial sum), then a butterfly.  Two rows at
+// once share the query reads and double the loads in flight.
 __device__ __forceinline__ void row_dist2(const float *__restrict__ r0, const float *__restrict__ r1,
                                           const double *__restrict__ qd, int nvec, int lane, double &o0, double &o1) {
     double a0 = 0.0, a1 = 0.0;
     const float4 *x0 = (const float4 *)r0, *x1 = (const float4 *)r1;
 #pragma unroll 4
     for (int v = lane; v < nvec; v += 32) {
-        float4 u0 = __ldg(x0 + v);
-        float4 u1 = __ldg(x1 + v);
-        acc4(a0, u0, qd + 4 * v);
-        acc4(a1, u1, qd + 4 * v);
+        const float4 u0 = __ldg(x0 + v);
+        const float4 u1 = __ldg(x1 + v);
+        const Q4 qv = q4_at(qd, v, nvec);
+        acc4(a0, u0, qv);
+        acc4(a1, u1, qv);
     }
     o0 = warp_sum(a0);
     o1 = warp_sum(a1);
@@ -986,7 +997,7 @@ __device__ __forceinline__ double row_dist1(const float *__restrict__ r0, const 
     double a0 = 0.0;
     const float4 *x0 = (const float4 *)r0;
 #pragma unroll 4
-    for (int v = lane; v < nvec; v += 32) acc4(a0, __ldg(x0 + v), qd + 4 * v);
+    for (int v = lane; v < nvec; v += 32) acc4(a0, __ldg(x0 + v), q4_at(qd, v, nvec));
     return warp_sum(a0);
 }
 
@@ -1023,8 +1034,10 @@ __device__ __forceinline__ void warp_insert(double *Ld, int64_t *Li, int &cnt, i
     __syncwarp();
 }
 
+// q' as doubles, component-major: qd[c*nvec + v] = q'[4v + c], nvec = pitch/4
 __device__ __forceinline__ void load_qd(double *qd, const float *qrow, int pitch) {
-    for (int i = threadIdx.x; i < pitch; i += blockDim.x) qd[i] = (double)qrow[i];
+    const int nvec = pitch >> 2;
+    for (int i = threadIdx.x; i < pitch; i += blockDim.x) qd[(i & 3) * nvec + (i >> 2)] = (double)qrow[i];
 }
 
 // ---------------------------------------------------------------------------

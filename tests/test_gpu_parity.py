@@ -135,6 +135,25 @@ def test_rotated_multiblock_ragged(crisp, monkeypatch, mode, count_kernel):
     assert_topk_parity(ids, d, r_ids, r_d, "rotated")
 
 
+@pytest.mark.parametrize("count_kernel", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_full_blocks_ragged_tail(crisp, monkeypatch, mode, count_kernel):
+    """Full 32768-id counter blocks (4096 counters per warp) with a ragged
+    third block, stage by stage."""
+    monkeypatch.setenv("CRISP_COUNT_KERNEL", str(count_kernel))
+    X, Qv, ox = make_case(cfg=1, N=70001, D=64, Q=24, M=4, K=16, seed=5)
+    ix = build_gpu(crisp, X, ox, block_ids=32768)
+    assert ix.info()["n_blocks"] == 3
+    B, tau, k = 9000, 2, 10
+    ix.set_search_params(budget=B, tau=tau, patience_factor=3)
+    ids, d, t = ix.trace(Qv, k, mode)
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, mode, B, tau, patience_factor=3, trace=True)
+    compare_trace(t, ot, mode, X.shape[0])
+    assert_topk_parity(ids, d, r_ids, r_d, "full blocks")
+    ids2, d2 = ix.search(Qv, k, mode)
+    assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
+
+
 @pytest.mark.parametrize("mode", [0, 1])
 def test_fallback_and_small_k(crisp, mode):
     """tau above every reachable score -> the underflow fallback."""

@@ -12,7 +12,9 @@ stalls = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
 data = []
 tot = 0
 for r in rows[2:]:
-    if len(r) != len(h):
+    if len(r) != len(h) or r[0] == "Address":
+        if r and r[0] == "Kernel Name" and data:
+            break  # several kernels in one export: the first only
         continue
     s = float(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
     tot += s
