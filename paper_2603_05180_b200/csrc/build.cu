@@ -135,11 +135,90 @@ struct StoreCov {
     __device__ void operator()(int64_t i, int j, double v) const { C[i * D + j] = v / nm1; }
 };
 
+// ---------------------------------------------------------------------------
+// Rotation Y = fl32(X . R), the same sequential fp64 order per
+// output as k_gemm_seq (k ascending from +0; padded k contribute fma(0, 0, s) =
+// s exactly), with a larger register tile: 128x64 outputs per CTA, 8x4 per
+// thread, k-tiles of 32 staged as doubles in shared memory (A via float4).
+// ---------------------------------------------------------------------------
+constexpr int RT_BM = 128, RT_BN = 64, RT_BK = 32;
+__global__ void __launch_bounds__(256) k_rotate_f64(int64_t Mr, int Dp, const float *__restrict__ X, int64_t ldx,
+                                                     const float *__restrict__ R, float *__restrict__ Y, int64_t ldy) {
+    extern __shared__ __align__(16) double rsm[];
+    double *As = rsm;                  // [RT_BK][RT_BM]
+    double *Bs = rsm + RT_BK * RT_BM;  // [RT_BK][RT_BN]
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t m0 = (int64_t)blockIdx.y * RT_BM;
+    const int n0 = blockIdx.x * RT_BN;
+    double acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j] = 0.0;
+    const bool vecA = (ldx & 3) == 0;
+    for (int k0 = 0; k0 < Dp; k0 += RT_BK) {
+        // A: 128 rows x 32 k, one float4 of 4 consecutive k per (row, quad)
+        for (int e = tid; e < RT_BM * (RT_BK / 4); e += 256) {
+            const int r = e >> 3, kq = (e & 7) * 4;
+            const int64_t m = m0 + r;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (m < Mr) {
+                const float *src = X + m * ldx + k0 + kq;
+                if (vecA && k0 + kq + 3 < Dp) v = *(const float4 *)src;
+                else {
+                    v.x = k0 + kq < Dp ? src[0] : 0.f;
+                    v.y = k0 + kq + 1 < Dp ? src[1] : 0.f;
+                    v.z = k0 + kq + 2 < Dp ? src[2] : 0.f;
+                    v.w = k0 + kq + 3 < Dp ? src[3] : 0.f;
+                }
+            }
+            As[(kq + 0) * RT_BM + r] = (double)v.x;
+            As[(kq + 1) * RT_BM + r] = (double)v.y;
+            As[(kq + 2) * RT_BM + r] = (double)v.z;
+            As[(kq + 3) * RT_BM + r] = (double)v.w;
+        }
+        // B: 32 k x 64 n
+        for (int e = tid; e < RT_BK * RT_BN; e += 256) {
+            const int kk = e >> 6, nn = e & 63;
+            const int k = k0 + kk, n = n0 + nn;
+            Bs[kk * RT_BN + nn] = (k < Dp && n < Dp) ? (double)R[(int64_t)k * Dp + n] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < RT_BK; kk++) {
+            double a[8], b[4];
+#pragma unroll
+            for (int i = 0; i < 8; i++) a[i] = As[kk * RT_BM + ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; j++) b[j] = Bs[kk * RT_BN + tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int64_t m = m0 + ty + 16 * i;
+            const int n = n0 + tx + 16 * j;
+            if (m < Mr && n < Dp) Y[m * ldy + n] = (float)acc[i][j];
+        }
+}
+
 void rotate_rows_f64(const float *X, int64_t rows, int32_t Dp, int64_t ldx, const float *R, float *Y, int64_t ldy,
                      cudaStream_t s) {
     if (rows <= 0) return;
-    dim3 grid(nblk(Dp, 64), (unsigned)((rows + 63) / 64));
-    k_gemm_seq<<<grid, 256, 0, s>>>(rows, Dp, Dp, LoadRowF32{X, ldx}, LoadMatF32{R, Dp}, StoreF32{Y, ldy});
+    static bool attr = false;
+    const int smem = (RT_BK * RT_BM + RT_BK * RT_BN) * 8;
+    if (!attr) {
+        CRISP_CUDA(cudaFuncSetAttribute(k_rotate_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    dim3 grid(nblk(Dp, RT_BN), (unsigned)((rows + RT_BM - 1) / RT_BM));
+    k_rotate_f64<<<grid, 256, smem, s>>>(rows, Dp, X, ldx, R, Y, ldy);
     CRISP_LAUNCH();
 }
 

@@ -1391,6 +1391,142 @@ __device__ void warp_segments(const int32_t *__restrict__ ncand, const int32_t *
     __syncwarp();
 }
 
+// k_hsort_cta: the same (h, id) order of the bins below the cut with a CTA per
+// query: each warp takes a contiguous range of the ascending candidate list,
+// counts its qualifying elements per bin, the per-(warp, bin) offsets follow
+// from the bin starts (stable: earlier warps first), and each warp scatters
+// its range in order.  smem: start (Dp+1), segments (2NS+1), counts WARPS x (Dp+1).
+__global__ void __launch_bounds__(THREADS) k_hsort_cta(const int32_t *__restrict__ ncand,
+                                                        const int32_t *__restrict__ cbase, int NS, int Dp,
+                                                        const int32_t *__restrict__ ghist,
+                                                        const int32_t *__restrict__ pool,
+                                                        const uint16_t *__restrict__ hbuf, int64_t CS,
+                                                        int32_t *__restrict__ order, int32_t *__restrict__ total_out,
+                                                        int limit) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    int *start = (int *)sm;         // Dp + 1
+    int *pre = start + Dp + 1;      // NS + 1
+    int *cbs = pre + NS + 1;        // NS
+    int *wcnt = cbs + NS;           // WARPS x (Dp + 1)
+    __shared__ int s_total, s_cut;
+    const int64_t q = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int HB = Dp + 1;
+    if (warp == 0) {
+        warp_segments(ncand, cbase, q, NS, pre, cbs);
+        const int32_t *gh = ghist + q * (int64_t)HB;
+        int acc = 0, cut = -1;
+        for (int b0 = 0; b0 < HB; b0 += 32) {
+            const int i = b0 + lane;
+            const int v = i < HB ? gh[i] : 0;
+            int inc = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, off);
+                if (lane >= off) inc += t;
+            }
+            const int st = acc + inc - v;
+            if (i < HB) start[i] = st;
+            const unsigned below = __ballot_sync(0xffffffffu, i < HB && st < limit);
+            if (below) cut = b0 + 31 - __clz(below);  // starts are monotone
+            acc += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) {
+            s_total = acc;
+            s_cut = cut;
+        }
+    }
+    __syncthreads();
+    const int total = s_total, cut = s_cut;
+    for (int i = tid; i < WARPS * (cut + 1); i += THREADS) wcnt[(i / (cut + 1)) * HB + i % (cut + 1)] = 0;
+    __syncthreads();
+    const int per = (total + WARPS - 1) / WARPS;
+    const int lo = min(total, warp * per), hi = min(total, lo + per);
+    const int32_t *cq = pool + q * CS;
+    const uint16_t *hq = hbuf + q * CS;
+    int *mycnt = wcnt + warp * HB;
+    int bl0 = 0;  // segment holding position lo
+    {
+        int a = 0, b = NS;  // largest a with pre[a] <= lo
+        while (b - a > 1) {
+            const int mid = (a + b) >> 1;
+            if (pre[mid] <= lo) a = mid;
+            else b = mid;
+        }
+        bl0 = a;
+    }
+    constexpr int U = 8;
+    // phase A: per-bin counts of this warp's qualifying elements
+    int bl = bl0;
+    for (int v00 = lo; v00 < hi; v00 += 32 * U) {
+        int hh[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int v = v00 + u * 32 + lane;
+            hh[u] = 0x7fffffff;
+            if (v < hi) {
+                while (pre[bl + 1] <= v) bl++;
+                hh[u] = hq[cbs[bl] + (v - pre[bl])];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (hh[u] <= cut) atomicAdd(&mycnt[hh[u]], 1);
+    }
+    __syncthreads();
+    // per-(warp, bin) output offsets: bin start + the bin's elements of earlier warps
+    for (int h = tid; h <= cut; h += THREADS) {
+        int run = start[h];
+        for (int w2 = 0; w2 < WARPS; w2++) {
+            const int c = wcnt[w2 * HB + h];
+            wcnt[w2 * HB + h] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    // phase B: stable scatter of this warp's range
+    int32_t *out = order + q * CS;
+    bl = bl0;
+    for (int v00 = lo; v00 < hi; v00 += 32 * U) {
+        int hh[U], ll[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int v = v00 + u * 32 + lane;
+            hh[u] = 0x7fffffff;
+            ll[u] = 0;
+            if (v < hi) {
+                while (pre[bl + 1] <= v) bl++;
+                const int pos = cbs[bl] + (v - pre[bl]);
+                hh[u] = hq[pos];
+                ll[u] = cq[pos];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int h = hh[u];
+            const bool qual = h <= cut;
+            const unsigned qm = __ballot_sync(0xffffffffu, qual);
+            if (!qm) continue;
+            int rank = 0, cnt = 0, leader = 32;
+            if (qual) {
+                const unsigned peers = __match_any_sync(qm, h);
+                leader = __ffs(peers) - 1;
+                rank = __popc(peers & ((1u << lane) - 1));
+                cnt = __popc(peers);
+            }
+            int base = 0;
+            if (qual && lane == leader) {
+                base = mycnt[h];
+                mycnt[h] = base + cnt;
+            }
+            base = __shfl_sync(0xffffffffu, base, qual ? leader : lane);
+            if (qual) out[base + rank] = ll[u];
+            __syncwarp();
+        }
+    }
+    if (tid == 0) total_out[q] = total;
+}
+
 __global__ void __launch_bounds__(32) k_hsort(const int32_t *__restrict__ ncand, const int32_t *__restrict__ cbase,
                                               int NS, int Dp, const int32_t *__restrict__ ghist,
                                               const int32_t *__restrict__ pool, const uint16_t *__restrict__ hbuf,
@@ -1748,6 +1884,7 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1779,7 +1916,7 @@ struct Work {
     PatState pst{};
     uint8_t *traceV = nullptr;
     bool full_order = false;  // trace: order every candidate (not only what the rounds read)
-    int probe_gs, probe_smem, count_smem, countw_smem, countw_ham_smem, rx_smem, ham_smem, hsort_smem, vr_smem, scan_smem, pat_smem;
+    int probe_gs, probe_smem, count_smem, countw_smem, countw_ham_smem, rx_smem, ham_smem, hsort_smem, hsort_cta_smem, vr_smem, scan_smem, pat_smem;
 
     static int64_t per_query_bytes(const crisp_index *ix, int k, int mode, int64_t CAPQ, bool traceV) {
         const int KK = ix->K * ix->K;
@@ -1851,6 +1988,7 @@ struct Work {
         rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NS + 1) * 4;
         ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NS + 1) * 4;
         hsort_smem = (Dp + 1 + 2 * NS + 1) * 4;
+        hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
         vr_smem = pitch * 8;
         scan_smem = WARPS * k * 16;
         pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + (Dp + 1 + 2 * NS + 1) * 4;
@@ -1975,8 +2113,13 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     {
         // (h, id) order into cbuf
         StageScope st(s, 7);
-        k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ,
-                                                       w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.R0 * w.S0);
+        if (w.hsort_cta_smem <= 200 * 1024)
+            k_hsort_cta<<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
+                w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals,
+                w.full_order ? 0x7fffffff : w.R0 * w.S0);
+        else
+            k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ,
+                                                           w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.R0 * w.S0);
         CRISP_LAUNCH();
         g_launches++;
     }
