@@ -437,6 +437,7 @@ struct CountWSmem {
     uint32_t erow[CS_CAP];  // cached entries: (m*KK + cell) | WFLAG
     uint32_t emw[CS_CAP];   // cached entries: m | WFLAG
     int32_t lpre[MAX_M + 2];
+    int next;               // next sub-block task of the CTA (dynamic: warps stay balanced)
 };
 
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
@@ -496,7 +497,10 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
             if (m < M) S.lpre[m + 1] = acc + v;
             acc += __shfl_sync(0xffffffffu, v, 31);
         }
-        if (lane == 0) S.lpre[0] = 0;
+        if (lane == 0) {
+            S.lpre[0] = 0;
+            S.next = 0;
+        }
     }
     for (int i = tid; i < SBW * WARPS / 16; i += THREADS) ((uint4 *)cnt8)[i] = make_uint4(0, 0, 0, 0);
     if (hbuf) {
@@ -524,10 +528,17 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
     const int nchunk = SBW / 512;  // 16-byte lane chunks of the warp's counters (SBW <= 4096: <= 8)
     const uint32_t tau4 = (uint32_t)tau * 0x01010101u;
     int32_t *outp = pool + q * CAPQ;
-    for (int b = b_lo; b < b_hi; b++) {
-        const int sb = b * 8 + warp;
-        const uint32_t lbase = (uint32_t)b * (uint32_t)BS;  // local id of counter 0 of the CTA
-        if ((int64_t)sb * SBW < N) {
+    const int ntask = (b_hi - b_lo) * 8;
+    for (;;) {
+        // next sub-block of the CTA's run (any warp may take any: its own counters)
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&S.next, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntask) break;
+        const int sb = b_lo * 8 + t;
+        const int sbase = sb * SBW;                                      // first id of the sub-block
+        const uint32_t lbase = (uint32_t)sbase - (uint32_t)(warp * SBW);  // id - lbase: this warp's counter
+        if ((int64_t)sbase < N) {
             for (int e0 = 0; e0 < Etot; e0 += 32) {
                 // this lane's entry: slice of the sub-block (ids[] start g, length len), weight flag
                 const int e = e0 + lane;
@@ -604,7 +615,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
                 uint4 *pv = (uint4 *)(wc + i * 512 + lane * 16);
                 const uint4 v = *pv;
                 if (traceV) {
-                    const int64_t x0 = (int64_t)lbase + warp * SBW + i * 512 + lane * 16;
+                    const int64_t x0 = (int64_t)sbase + i * 512 + lane * 16;
                     const unsigned char *vb = (const unsigned char *)&v;
                     for (int j = 0; j < 16; j++)
                         if (x0 + j < N) traceV[q * N + x0 + j] = vb[j];
@@ -651,7 +662,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
             uint32_t word = mk[i];
             const uint32_t inc = (inc16[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
             int o = run + (int)inc - __popc(word);
-            const int g0 = (int)lbase + warp * SBW + i * 512 + lane * 16;
+            const int g0 = sbase + i * 512 + lane * 16;
             while (word) {
                 const int bit = __ffs(word) - 1;
                 if (o < CAPQ) outp[o] = g0 + bit;
@@ -1938,7 +1949,7 @@ struct Work {
         HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 4));     // CTAs per query in k_hamming
         S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
         R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
-        BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 8)));  // id blocks per count CTA
+        BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 16)));  // id blocks per count CTA
         count_kernel = env_int("CRISP_COUNT_KERNEL", 1);  // 0: k_count_select, 1: k_count_warp
         NS = count_kernel == 0 ? NB : ix->NBW;  // candidate segments per query (id blocks or sub-blocks)
         qpad = buf.alloc<float>((size_t)Qc * pitch);
