@@ -155,6 +155,22 @@ def test_full_blocks_ragged_tail(crisp, monkeypatch, mode, count_kernel):
 
 
 @pytest.mark.parametrize("mode", [0, 1])
+def test_many_subspaces_wide_counters(crisp, mode):
+    """M=64 (scores up to 2M=128 do not fit the 7-bit SWAR compare: the
+    __vcmpgeu4 path of the threshold scan), stage by stage."""
+    X, Qv, ox = make_case(cfg=1, N=9001, D=256, Q=16, M=64, K=6, seed=7)
+    ix = build_gpu(crisp, X, ox, block_ids=4096)
+    B, tau, k = 1500, 30, 10
+    ix.set_search_params(budget=B, tau=tau, patience_factor=2)
+    ids, d, t = ix.trace(Qv, k, mode)
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, mode, B, tau, patience_factor=2, trace=True)
+    compare_trace(t, ot, mode, X.shape[0])
+    if mode == 1:
+        assert int(ot["V"].max()) >= 64, "scores above 63 exercise the wide compare"
+    assert_topk_parity(ids, d, r_ids, r_d, "M=64")
+
+
+@pytest.mark.parametrize("mode", [0, 1])
 def test_fallback_and_small_k(crisp, mode):
     """tau above every reachable score -> the underflow fallback."""
     X, Qv, ox = make_case(cfg=3, N=9000, D=64, Q=30, M=4, K=12, seed=5)
