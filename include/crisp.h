@@ -125,7 +125,8 @@ crisp_status crisp_default_params(crisp_params *p);
  * (P:L264-268), adaptive rotation X' = XR in place, 2M k-means
  * codebooks, cell assignment, per-subspace CSR Offsets/IDs
  * (P:L363-369), binary codes.  data: N x D fp32 row-major, host or
- * device.  On success *out owns the index. */
+ * device; a device buffer may still be being written on any stream: the call
+ * synchronizes the device first.  On success *out owns the index. */
 crisp_status crisp_build(const float *data, int64_t N, int32_t D, const crisp_params *p, crisp_index **out);
 
 /* Same, with the rotation R (padded_D x padded_D fp32 row-major, or NULL for

@@ -159,6 +159,9 @@ static crisp_status build_common(const float *data, int64_t N, int64_t gid_base,
         if (inject) CRISP_CHECK(cb != nullptr, "codebooks are NULL");
         ix = new_index(N, D, p);
         ix->gid_base = gid_base;
+        // device inputs may still be in flight on the caller's streams (the build
+        // runs on its own non-blocking stream): order the build after all of it
+        CRISP_CUDA(cudaDeviceSynchronize());
         TmpFree tf;
         const float *dd = to_device(data, (size_t)N * D, tf.v);
         const float *Rd = R ? to_device(R, (size_t)ix->Dp * ix->Dp, tf.v) : nullptr;

@@ -329,3 +329,23 @@ def test_shard_emulation_exact_fallback(crisp, tau):
         assert ot["fallback"].sum() >= 2
     assert np.array_equal(oi.cpu().numpy(), ids1)
     assert np.array_equal(od.cpu().numpy(), d1)
+
+
+def test_build_waits_for_pending_device_writes(crisp):
+    """crisp_build on a device buffer that is still being written on the
+    caller's stream: the stored vectors must be the final ones."""
+    import torch
+
+    N, D = 200000, 64
+    X = torch.zeros((N, D), dtype=torch.float32, device="cuda")
+    a = torch.randn((4096, 4096), device="cuda")
+    for _ in range(20):  # keep the stream busy
+        a = a @ a * 1e-3
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    X.normal_(generator=g)
+    X.add_(a[0, 0] * 0)
+    ix = crisp.Index.build(X, 4, K=8, seed=1, rotation=0)
+    e = ix.export()
+    assert np.array_equal(e["X"][:, :D], X.cpu().numpy())
+    ix.free()
