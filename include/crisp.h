@@ -87,6 +87,8 @@ typedef struct {
     int32_t n_blocks;
     int64_t hbm_bytes;  /* device bytes owned by the index */
     int64_t logical_bytes; /* 4ND + 4MN + 8M(K^2+1) + codebooks + 8*ceil(D/64)*N + 4D^2 if rotated */
+    double slice_hint;  /* expected ids per activated slice and 4096-id warp sub-block: >= 8 selects the
+                           warp-owned collision-count kernel, else the CTA-flattened one (env CRISP_COUNT_KERNEL) */
 } crisp_index_info_t;
 
 /* Host buffers filled by crisp_export (any may be NULL to skip). */

@@ -273,6 +273,7 @@ crisp_status crisp_set_global_cell_sizes(crisp_index *ix, const int64_t *sizes) 
         CRISP_CHECK(n0 >= ix->N, "global sizes smaller than the local shard");
         CRISP_CUDA(cudaMemcpy(ix->gsize, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
         ix->N_global = n0;
+        ix->slice_hint = slice_hint_of(h.data(), ix->M, KK, n0, ix->SBW);
         return CRISP_OK;
     } catch (Err &e) {
         return e.st;
@@ -301,6 +302,7 @@ crisp_status crisp_index_info(const crisp_index *ix, crisp_index_info_t *o) {
     o->D = ix->D;
     o->padded_D = ix->Dp;
     o->pitch = ix->pitch;
+    o->slice_hint = ix->slice_hint;
     o->M = ix->M;
     o->K = ix->K;
     o->dh = ix->dh;

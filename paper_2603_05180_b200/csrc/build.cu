@@ -678,7 +678,21 @@ void finish_csr(crisp_index *ix, cudaStream_t s) {
         k_off2<<<nblk((int64_t)M * KK * (nb + 1), 256), 256, 0, s>>>(scan, N, M, KK, nb, dst, ix->gsize);
         CRISP_LAUNCH();
     }
+    {
+        std::vector<int32_t> h((size_t)M * KK);
+        CRISP_CUDA(cudaMemcpyAsync(h.data(), ix->gsize, h.size() * 4, cudaMemcpyDeviceToHost, s));
+        CRISP_CUDA(cudaStreamSynchronize(s));
+        ix->slice_hint = slice_hint_of(h.data(), M, KK, ix->N_global, ix->SBW);
+    }
     CRISP_CUDA(cudaStreamSynchronize(s));
+}
+
+double slice_hint_of(const int32_t *sizes, int M, int64_t KK, int64_t N_global, int SBW) {
+    double acc = 0.0;
+    for (int m = 0; m < M; m++)
+        for (int64_t c = 0; c < KK; c++) acc += (double)sizes[m * KK + c] * (double)sizes[m * KK + c];
+    const double es = acc / ((double)M * (double)std::max<int64_t>(1, N_global));
+    return es * (double)SBW / (double)std::max<int64_t>(1, N_global);
 }
 
 __global__ void k_check_finite(const float *X, int64_t N, int64_t pitch, int D, int *bad) {

@@ -72,6 +72,7 @@ struct crisp_index {
     uint64_t *codes = nullptr; // N x W
     int32_t BS = 0, NB = 0;    // on-chip counter block: ids per block, number of blocks
     int32_t SBW = 0, NBW = 0;  // warp sub-block: ids per sub-block (BS/8), number of sub-blocks (8*NB)
+    double slice_hint = 0.0;   // expected ids of a query's activated slice per warp sub-block (count kernel choice)
     int64_t budget = 0;
     int32_t tau = 1, patience_factor = 40;
     int64_t workspace_bytes = 0;
@@ -79,6 +80,10 @@ struct crisp_index {
 };
 
 namespace crisp {
+
+// expected slice length per warp sub-block from cell sizes (M x K^2, host):
+// the size of the cell holding a random point, E[s] = sum s^2 / N, scaled to SBW
+double slice_hint_of(const int32_t *sizes_host, int M, int64_t KK, int64_t N_global, int SBW);
 
 // helpers implemented in api.cu
 void *dmalloc(size_t bytes, crisp_index *ix);

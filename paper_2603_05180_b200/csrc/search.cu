@@ -352,12 +352,13 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
                                                            int tau, int32_t *__restrict__ pool, int64_t CAPQ,
                                                            int32_t *__restrict__ cursor, int32_t *__restrict__ cbase,
                                                            int32_t *__restrict__ ncand, int32_t *__restrict__ need,
-                                                           uint8_t *__restrict__ traceV) {
+                                                           uint8_t *__restrict__ traceV,
+                                                           const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;
     uint32_t *cross = (uint32_t *)(smraw + BS);            // BS bits
     CountSmem &S = *(CountSmem *)(smraw + BS + BS / 8);
-    const int64_t q = blockIdx.y;
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b_lo = blockIdx.x * BPC, b_hi = min(NB, b_lo + BPC);
     const int Etot = count_setup(S, q, act, act_len, M, KK);
@@ -1233,13 +1234,14 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
                                                       const int32_t *__restrict__ cbase,
                                                       const int32_t *__restrict__ ncand, int NB,
                                                       uint16_t *__restrict__ hbuf, int32_t *__restrict__ ghist,
-                                                      const int32_t *__restrict__ only_fb) {
+                                                      const int32_t *__restrict__ only_fb,
+                                                      const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char sm[];
     uint64_t *qc = (uint64_t *)sm;          // Wd
     int *hist = (int *)(qc + Wd);           // Dp + 1
     int *pre = hist + Dp + 1;               // NB + 1
     int *cbs = pre + NB + 1;                // NB
-    const int64_t q = blockIdx.y;
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
     if (only_fb && !only_fb[q]) return;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float *qrow = qrot + q * pitch;
@@ -1950,7 +1952,9 @@ struct Work {
         S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
         R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
         BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 16)));  // id blocks per count CTA
-        count_kernel = env_int("CRISP_COUNT_KERNEL", 1);  // 0: k_count_select, 1: k_count_warp
+        // 0: k_count_select (CTA-flattened slices, for many small cells), 1: k_count_warp
+        // (warp-owned sub-blocks, for slices of >= 8 ids per sub-block); env overrides
+        count_kernel = env_int("CRISP_COUNT_KERNEL", ix->slice_hint >= 8.0 ? 1 : 0);
         NS = count_kernel == 0 ? NB : ix->NBW;  // candidate segments per query (id blocks or sub-blocks)
         qpad = buf.alloc<float>((size_t)Qc * pitch);
         qrot = ix->rotated ? buf.alloc<float>((size_t)Qc * pitch) : qpad;
@@ -2050,7 +2054,7 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
         if (w.count_kernel == 0)
             k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N,
                                                             ix->BS, w.BPC, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase,
-                                                            w.ncand, w.need, w.traceV);
+                                                            w.ncand, w.need, w.traceV, w.qperm);
         else {
             uint16_t *hb = w.mode == 1 ? w.hbuf : nullptr;  // phi=1: Hamming fused into the count
             const int smem = w.countw_smem + (w.mode == 1 ? w.countw_ham_smem : 0);
@@ -2117,7 +2121,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         StageScope st(s, 6);
         dim3 g(w.HS, (unsigned)qn);
         k_hamming<<<g, THREADS, w.ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->W, w.pool, w.CAPQ, w.cbase, w.ncand,
-                                                 NB, w.hbuf, w.ghist, w.count_kernel == 0 ? nullptr : w.fb);
+                                                 NB, w.hbuf, w.ghist, w.count_kernel == 0 ? nullptr : w.fb, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
     }
