@@ -2,7 +2,7 @@
 times (Q=10k queries at the operating point of configs/operating_points.json,
 both modes), on sampled outputs the oracle computes one by one.
 
-cfg2 (N=1M, D=960, rotated) and cfg3 (N=1M, D=1024) run by default.  The
+cfg2 (N=1M, D=960, rotated) and cfg3 (N=1M, D=1024), about a minute: the
 oracle builds the index itself (its R, its codebooks, its X' = XR); the GPU
 index is built with crisp_build_with from the oracle's R and codebooks, so X',
 cells, CSR and codes must come out bit-identical, and the sampled queries'
