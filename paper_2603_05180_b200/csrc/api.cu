@@ -112,6 +112,7 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
     ix->dh = ix->Dp / (2 * p->M);
     ix->pitch = ((ix->Dp + 3) / 4) * 4;
     ix->W = (ix->Dp + 63) / 64;
+    ix->Wp = (ix->W + 7) / 8 * 8;
     ix->BS = block_ids_for(N);
     ix->NB = (int32_t)((N + ix->BS - 1) / ix->BS);
     ix->SBW = ix->BS / 8;
@@ -126,7 +127,7 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
         ix->off2 = dalloc<int32_t>(ix, (size_t)ix->M * KK * (ix->NB + 1));
         ix->off2w = dalloc<int32_t>(ix, (size_t)ix->M * KK * (ix->NBW + 1));
         ix->gsize = dalloc<int32_t>(ix, (size_t)ix->M * KK);
-        ix->codes = dalloc<uint64_t>(ix, (size_t)N * ix->W);
+        ix->codes = dalloc<uint64_t>(ix, (size_t)N * ix->Wp);
     } catch (...) {
         free_index(ix);
         throw;
@@ -469,7 +470,9 @@ crisp_status crisp_export(const crisp_index *ix, crisp_export_t *o) {
             CRISP_CUDA(cudaMemcpy(o->codebooks, ix->cb, (size_t)ix->M * 2 * ix->K * ix->dh * 4, cudaMemcpyDeviceToHost));
         if (o->cells) CRISP_CUDA(cudaMemcpy(o->cells, ix->cells, (size_t)ix->M * N * 4, cudaMemcpyDeviceToHost));
         if (o->ids) CRISP_CUDA(cudaMemcpy(o->ids, ix->ids, (size_t)ix->M * N * 4, cudaMemcpyDeviceToHost));
-        if (o->codes) CRISP_CUDA(cudaMemcpy(o->codes, ix->codes, (size_t)N * ix->W * 8, cudaMemcpyDeviceToHost));
+        if (o->codes)
+            CRISP_CUDA(cudaMemcpy2D(o->codes, (size_t)ix->W * 8, ix->codes, (size_t)ix->Wp * 8, (size_t)ix->W * 8, N,
+                                    cudaMemcpyDeviceToHost));
         if (o->offsets) {
             std::vector<int32_t> off((size_t)ix->M * KK * (ix->NB + 1));
             CRISP_CUDA(cudaMemcpy(off.data(), ix->off2, off.size() * 4, cudaMemcpyDeviceToHost));

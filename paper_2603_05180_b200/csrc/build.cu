@@ -746,7 +746,7 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
     k_assign<<<nblk(N * ix->M, 128), 128, 0, s>>>(ix->X, N, ix->pitch, ix->M, ix->K, ix->dh, ix->cb, ix->cells);
     CRISP_LAUNCH();
     finish_csr(ix, s);
-    k_codes<<<nblk(N * (int64_t)ix->W * 64, 256), 256, 0, s>>>(ix->X, N, ix->pitch, ix->Dp, ix->W,
+    k_codes<<<nblk(N * (int64_t)ix->Wp * 64, 256), 256, 0, s>>>(ix->X, N, ix->pitch, ix->Dp, ix->Wp,
                                                                   (uint32_t *)ix->codes);
     CRISP_LAUNCH();
     CRISP_CUDA(cudaStreamSynchronize(s));

@@ -59,6 +59,7 @@ struct crisp_index {
     int device = 0;
     int64_t N = 0, N_global = 0, gid_base = 0;
     int32_t D = 0, Dp = 0, pitch = 0, M = 0, K = 0, dh = 0, W = 0;
+    int32_t Wp = 0;            // code row stride in words: W rounded up to 8 (64-B rows, 16-B loads)
     int32_t rotated = 0;
     double cev = 0.0;
     float *X = nullptr;        // N x pitch, stored (rotated) vectors, zero padded

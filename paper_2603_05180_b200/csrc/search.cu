@@ -674,45 +674,47 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
         }
         if (hbuf && n > 0) {
             // a4, phi=1: h(x) = popcount(b(q') xor b(x)) (Alg. 1 l.19) of this segment's
-            // candidates; 4 lanes per candidate, 16 candidates per pass, h at the pool position
+            // candidates.  4 lanes per candidate, each lane 16-byte loads of its words
+            // (code rows are Wd = 8j words); 32 candidates per pass, all loads in flight;
+            // h is written at the candidate's pool position.
             __syncwarp();
-            const int g4 = lane >> 2, gl = lane & 3, wpl = (Wd + 3) >> 2;
-            for (int v0 = 0; v0 < n; v0 += 16) {
-                int pos[2], id[2];
-                bool okv[2];
+            const int g4 = lane >> 2, gl = lane & 3, nt = Wd >> 3;
+            for (int v0 = 0; v0 < n; v0 += 32) {
+                int pos[4], id[4];
+                bool okv[4];
 #pragma unroll
-                for (int r = 0; r < 2; r++) {
+                for (int r = 0; r < 4; r++) {
                     const int vi = v0 + r * 8 + g4;
                     pos[r] = base + vi;
                     okv[r] = vi < n && pos[r] < CAPQ;
                     id[r] = okv[r] ? outp[pos[r]] : 0;
                 }
-                int h0 = 0, h1 = 0;
-#pragma unroll 4
-                for (int t = 0; t < wpl; t++) {
-                    const int wd = gl + 4 * t;
-                    const int wc2 = min(wd, Wd - 1);
-                    const uint64_t qw = qc[wc2];
-                    const int c0 = __popcll(qw ^ __ldg(codes + (int64_t)id[0] * Wd + wc2));
-                    const int c1 = __popcll(qw ^ __ldg(codes + (int64_t)id[1] * Wd + wc2));
-                    if (wd < Wd) {
-                        h0 += c0;
-                        h1 += c1;
-                    }
+                int hr[4] = {0, 0, 0, 0};
+#pragma unroll 2
+                for (int t = 0; t < nt; t++) {
+                    const int wd = 2 * gl + 8 * t;
+                    const uint64_t q0 = qc[wd], q1 = qc[wd + 1];
+                    ulonglong2 cw[4];
+#pragma unroll
+                    for (int r = 0; r < 4; r++)
+                        cw[r] = __ldg((const ulonglong2 *)(codes + (int64_t)id[r] * Wd + wd));
+#pragma unroll
+                    for (int r = 0; r < 4; r++) hr[r] += __popcll(q0 ^ cw[r].x) + __popcll(q1 ^ cw[r].y);
                 }
-                h0 += __shfl_xor_sync(0xffffffffu, h0, 1);
-                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
-                h0 += __shfl_xor_sync(0xffffffffu, h0, 2);
-                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                // sum over the 4 lanes of a candidate; two candidates per word (h <= 65535)
+                uint32_t p01 = (uint32_t)hr[0] | ((uint32_t)hr[1] << 16), p23 = (uint32_t)hr[2] | ((uint32_t)hr[3] << 16);
+                p01 += __shfl_xor_sync(0xffffffffu, p01, 1);
+                p23 += __shfl_xor_sync(0xffffffffu, p23, 1);
+                p01 += __shfl_xor_sync(0xffffffffu, p01, 2);
+                p23 += __shfl_xor_sync(0xffffffffu, p23, 2);
                 if (gl == 0) {
-                    if (okv[0]) {
-                        hbuf[q * CAPQ + pos[0]] = (uint16_t)h0;
-                        atomicAdd(&hist[h0], 1);
-                    }
-                    if (okv[1]) {
-                        hbuf[q * CAPQ + pos[1]] = (uint16_t)h1;
-                        atomicAdd(&hist[h1], 1);
-                    }
+                    const int hh[4] = {(int)(p01 & 0xffffu), (int)(p01 >> 16), (int)(p23 & 0xffffu), (int)(p23 >> 16)};
+#pragma unroll
+                    for (int r = 0; r < 4; r++)
+                        if (okv[r]) {
+                            hbuf[q * CAPQ + pos[r]] = (uint16_t)hh[r];
+                            atomicAdd(&hist[hh[r]], 1);
+                        }
                 }
             }
         }
@@ -1999,9 +2001,9 @@ struct Work {
         probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
         countw_smem = BS + 16 + (int)((sizeof(CountWSmem) + 15) & ~(size_t)15);
-        countw_ham_smem = ix->W * 8 + (Dp + 1) * 4;
+        countw_ham_smem = ix->Wp * 8 + (Dp + 1) * 4;
         rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NS + 1) * 4;
-        ham_smem = ix->W * 8 + (Dp + 1) * 4 + (2 * NS + 1) * 4;
+        ham_smem = ix->Wp * 8 + (Dp + 1) * 4 + (2 * NS + 1) * 4;
         hsort_smem = (Dp + 1 + 2 * NS + 1) * 4;
         hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
         vr_smem = pitch * 8;
@@ -2061,12 +2063,12 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
             if (2 * M < 128)
                 k_count_warp<true><<<g, THREADS, smem, s>>>(
                     w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
-                    w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->W, hb,
+                    w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp, hb,
                     w.ghist, w.qperm);
             else
                 k_count_warp<false><<<g, THREADS, smem, s>>>(
                     w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
-                    w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->W, hb,
+                    w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp, hb,
                     w.ghist, w.qperm);
         }
         CRISP_LAUNCH();
@@ -2120,7 +2122,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         // queries whose candidate set the fallback replaced are done here
         StageScope st(s, 6);
         dim3 g(w.HS, (unsigned)qn);
-        k_hamming<<<g, THREADS, w.ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->W, w.pool, w.CAPQ, w.cbase, w.ncand,
+        k_hamming<<<g, THREADS, w.ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool, w.CAPQ, w.cbase, w.ncand,
                                                  NB, w.hbuf, w.ghist, w.count_kernel == 0 ? nullptr : w.fb, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
