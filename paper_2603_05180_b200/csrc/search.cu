@@ -458,8 +458,8 @@ __device__ __forceinline__ uint32_t bytes_ge(uint32_t w, uint32_t t4) {
     return (h * 0x00204081u) >> 28;  // bits 7,15,23,31 -> 28..31
 }
 
-template <bool SWAR>
-__global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__restrict__ act,
+template <bool SWAR, bool HAM>
+__global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint32_t *__restrict__ act,
                                                            const int32_t *__restrict__ act_len, int M, int KK,
                                                            const int32_t *__restrict__ off2w, int NBW,
                                                            const int32_t *__restrict__ ids, int64_t N, int BS, int BPC,
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
         }
     }
     for (int i = tid; i < SBW * WARPS / 16; i += THREADS) ((uint4 *)cnt8)[i] = make_uint4(0, 0, 0, 0);
-    if (hbuf) {
+    if (HAM && hbuf) {
         const float *qrow = qrot + q * pitch;
         for (int d0 = warp * 32; d0 < Wd * 64; d0 += THREADS) {  // bit (i mod 64) of word i/64 = [q'_i > 0] (Z10)
             const int d = d0 + lane;
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
             }
             run += ctot[i];
         }
-        if (hbuf && n > 0) {
+        if (HAM && hbuf && n > 0) {
             // a4, phi=1: h(x) = popcount(b(q') xor b(x)) (Alg. 1 l.19) of this segment's
             // candidates.  4 lanes per candidate, each lane 16-byte loads of its words
             // (code rows are Wd = 8j words); 32 candidates per pass, all loads in flight;
@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_warp(const uint32_t *__res
             }
         }
     }
-    if (hbuf) {
+    if (HAM && hbuf) {
         __syncthreads();
         int32_t *gh = ghist + q * (int64_t)(Dp + 1);
         for (int i = tid; i < Dp + 1; i += THREADS)
@@ -1291,6 +1291,78 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
                 hbuf[q * CAPQ + ps] = (uint16_t)hv;  // h at the candidate's pool position
                 atomicAdd(&hist[hv], 1);
             }
+        }
+    }
+    __syncthreads();
+    int32_t *gh = ghist + q * (int64_t)(Dp + 1);
+    for (int i = tid; i < Dp + 1; i += THREADS)
+        if (hist[i]) atomicAdd(&gh[i], hist[i]);
+}
+
+// k_hamming_dense (a4, phi=1, after k_count_warp without the fused popcount):
+// the query's candidates occupy pool positions [0, |C_q|) exactly (segment
+// bases come from a cursor starting at 0), so a CTA takes a contiguous range
+// of positions: 4 lanes per candidate with 16-byte code loads, h written at
+// the position, a CTA histogram flushed to the query's histogram.
+__global__ void __launch_bounds__(THREADS) k_hamming_dense(const float *__restrict__ qrot, int pitch, int Dp,
+                                                            const uint64_t *__restrict__ codes, int Wd,
+                                                            const int32_t *__restrict__ pool, int64_t CAPQ,
+                                                            const int32_t *__restrict__ cursor,
+                                                            uint16_t *__restrict__ hbuf, int32_t *__restrict__ ghist,
+                                                            const int32_t *__restrict__ fb,
+                                                            const int32_t *__restrict__ qperm) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    uint64_t *qc = (uint64_t *)sm;     // Wd
+    int *hist = (int *)(qc + Wd);      // Dp + 1
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;
+    if (fb[q]) return;  // the fallback replaced C_q: k_hamming handles it
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float *qrow = qrot + q * pitch;
+    for (int d0 = warp * 32; d0 < Wd * 64; d0 += THREADS) {
+        const int d = d0 + lane;
+        const unsigned bits = __ballot_sync(0xffffffffu, d < Dp && qrow[d] > 0.0f);
+        if (lane == 0) ((uint32_t *)qc)[d0 >> 5] = bits;
+    }
+    for (int i = tid; i < Dp + 1; i += THREADS) hist[i] = 0;
+    __syncthreads();
+    const int total = (int)min((int64_t)cursor[q], CAPQ);
+    const int per = (total + gridDim.x - 1) / gridDim.x;
+    const int lo = blockIdx.x * per, hi = min(total, lo + per);
+    const int32_t *poolq = pool + q * CAPQ;
+    const int g4 = lane >> 2, gl = lane & 3, nt = Wd >> 3;
+    for (int v0 = lo + warp * 32; v0 < hi; v0 += WARPS * 32) {
+        int id[4];
+        bool okv[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const int v = v0 + r * 8 + g4;
+            okv[r] = v < hi;
+            id[r] = okv[r] ? __ldg(poolq + v) : 0;
+        }
+        int hr[4] = {0, 0, 0, 0};
+#pragma unroll 2
+        for (int t = 0; t < nt; t++) {
+            const int wd = 2 * gl + 8 * t;
+            const uint64_t q0 = qc[wd], q1 = qc[wd + 1];
+            ulonglong2 cw[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) cw[r] = __ldg((const ulonglong2 *)(codes + (int64_t)id[r] * Wd + wd));
+#pragma unroll
+            for (int r = 0; r < 4; r++) hr[r] += __popcll(q0 ^ cw[r].x) + __popcll(q1 ^ cw[r].y);
+        }
+        uint32_t p01 = (uint32_t)hr[0] | ((uint32_t)hr[1] << 16), p23 = (uint32_t)hr[2] | ((uint32_t)hr[3] << 16);
+        p01 += __shfl_xor_sync(0xffffffffu, p01, 1);
+        p23 += __shfl_xor_sync(0xffffffffu, p23, 1);
+        p01 += __shfl_xor_sync(0xffffffffu, p01, 2);
+        p23 += __shfl_xor_sync(0xffffffffu, p23, 2);
+        if (gl == 0) {
+            const int hh[4] = {(int)(p01 & 0xffffu), (int)(p01 >> 16), (int)(p23 & 0xffffu), (int)(p23 >> 16)};
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (okv[r]) {
+                    hbuf[q * CAPQ + v0 + r * 8 + g4] = (uint16_t)hh[r];
+                    atomicAdd(&hist[hh[r]], 1);
+                }
         }
     }
     __syncthreads();
@@ -1891,13 +1963,17 @@ static void set_attrs() {
     if (done) return;
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1913,7 +1989,7 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
-    int S, HS, S0, R0, BPC, count_kernel, NS;
+    int S, HS, S0, R0, BPC, count_kernel, NS, ham_fused;
     DevBuf buf;
     float *qpad = nullptr, *qrot = nullptr;
     uint32_t *act = nullptr;
@@ -1950,7 +2026,7 @@ struct Work {
         : ix(ix_), k(k_), mode(mode_), Qc(Qc_), CAPQ(CAPQ_), buf(s) {
         const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch, Dp = ix->Dp;
         S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));       // CTAs per query in the row kernels
-        HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 4));     // CTAs per query in k_hamming
+        HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 2));     // CTAs per query in k_hamming(_dense)
         S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
         R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
         BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 16)));  // id blocks per count CTA
@@ -1958,6 +2034,7 @@ struct Work {
         // (warp-owned sub-blocks, for slices of >= 8 ids per sub-block); env overrides
         count_kernel = env_int("CRISP_COUNT_KERNEL", ix->slice_hint >= 8.0 ? 1 : 0);
         NS = count_kernel == 0 ? NB : ix->NBW;  // candidate segments per query (id blocks or sub-blocks)
+        ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
         qpad = buf.alloc<float>((size_t)Qc * pitch);
         qrot = ix->rotated ? buf.alloc<float>((size_t)Qc * pitch) : qpad;
         act = buf.alloc<uint32_t>((size_t)Qc * M * KK);
@@ -2058,18 +2135,19 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
                                                             ix->BS, w.BPC, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase,
                                                             w.ncand, w.need, w.traceV, w.qperm);
         else {
-            uint16_t *hb = w.mode == 1 ? w.hbuf : nullptr;  // phi=1: Hamming fused into the count
-            const int smem = w.countw_smem + (w.mode == 1 ? w.countw_ham_smem : 0);
-            if (2 * M < 128)
-                k_count_warp<true><<<g, THREADS, smem, s>>>(
-                    w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
-                    w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp, hb,
-                    w.ghist, w.qperm);
-            else
-                k_count_warp<false><<<g, THREADS, smem, s>>>(
-                    w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, w.BPC, NB, ix->tau, w.pool,
-                    w.CAPQ, w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp, hb,
-                    w.ghist, w.qperm);
+            uint16_t *hb = (w.mode == 1 && w.ham_fused) ? w.hbuf : nullptr;  // phi=1: Hamming fused into the count
+            const int smem = w.countw_smem + (hb ? w.countw_ham_smem : 0);
+#define CRISP_COUNT_WARP(SW, HM)                                                                               \
+    k_count_warp<SW, HM><<<g, THREADS, smem, s>>>(w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, \
+                                                  w.BPC, NB, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase, w.ncand,      \
+                                                  w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp, hb,      \
+                                                  w.ghist, w.qperm)
+            const bool sw = 2 * M < 128;
+            if (sw && hb) CRISP_COUNT_WARP(true, true);
+            else if (sw) CRISP_COUNT_WARP(true, false);
+            else if (hb) CRISP_COUNT_WARP(false, true);
+            else CRISP_COUNT_WARP(false, false);
+#undef CRISP_COUNT_WARP
         }
         CRISP_LAUNCH();
         g_launches++;
@@ -2126,6 +2204,13 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
                                                  NB, w.hbuf, w.ghist, w.count_kernel == 0 ? nullptr : w.fb, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
+        if (w.count_kernel == 1 && !w.ham_fused) {
+            dim3 g2(w.HS, (unsigned)qn);
+            k_hamming_dense<<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
+                                                                   w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb, w.qperm);
+            CRISP_LAUNCH();
+            g_launches++;
+        }
     }
     {
         // (h, id) order into cbuf

@@ -96,12 +96,20 @@ def compare_trace(t, ot, mode, N):
         assert np.array_equal(t["n_verified"], ot["n_verified"]), "a5 patience stop"
 
 
-@pytest.mark.parametrize("count_kernel", [0, 1])
+# collision-count variants: CTA-flattened, warp-owned (+ standalone dense
+# Hamming at phi=1), warp-owned with the Hamming popcounts fused
+COUNT_VARIANTS = {"select": {"CRISP_COUNT_KERNEL": "0"},
+                  "warp": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "0"},
+                  "warp_fused": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "1"}}
+
+
+@pytest.mark.parametrize("variant", list(COUNT_VARIANTS))
 @pytest.mark.parametrize("mode", [0, 1])
-def test_cfg1_stagewise(crisp, monkeypatch, mode, count_kernel):
+def test_cfg1_stagewise(crisp, monkeypatch, mode, variant):
     """BASELINE configs[0] (PR1: N=20k, D=256, Q=100, k=10) in full, M=8;
-    both collision-count kernels (block-staged and warp-owned counters)."""
-    monkeypatch.setenv("CRISP_COUNT_KERNEL", str(count_kernel))
+    every collision-count variant."""
+    for k_, v_ in COUNT_VARIANTS[variant].items():
+        monkeypatch.setenv(k_, v_)
     X, Qv, ox = make_case()
     ix = build_gpu(crisp, X, ox)
     compare_index(ix, ox)
@@ -116,12 +124,13 @@ def test_cfg1_stagewise(crisp, monkeypatch, mode, count_kernel):
     assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
 
 
-@pytest.mark.parametrize("count_kernel", [0, 1])
+@pytest.mark.parametrize("variant", list(COUNT_VARIANTS))
 @pytest.mark.parametrize("mode", [0, 1])
-def test_rotated_multiblock_ragged(crisp, monkeypatch, mode, count_kernel):
+def test_rotated_multiblock_ragged(crisp, monkeypatch, mode, variant):
     """Rotation injected (R from the oracle), 5 id blocks with a ragged tail,
     D not a multiple of 2M (zero padding), K=31."""
-    monkeypatch.setenv("CRISP_COUNT_KERNEL", str(count_kernel))
+    for k_, v_ in COUNT_VARIANTS[variant].items():
+        monkeypatch.setenv(k_, v_)
     X, Qv, ox = make_case(cfg=2, N=18001, D=90, Q=40, M=4, K=31, rotation=1, seed=3)
     assert ox["rotated"] and ox["Dp"] == 96
     ix = build_gpu(crisp, X, ox, block_ids=4096)
@@ -135,12 +144,13 @@ def test_rotated_multiblock_ragged(crisp, monkeypatch, mode, count_kernel):
     assert_topk_parity(ids, d, r_ids, r_d, "rotated")
 
 
-@pytest.mark.parametrize("count_kernel", [0, 1])
+@pytest.mark.parametrize("variant", list(COUNT_VARIANTS))
 @pytest.mark.parametrize("mode", [0, 1])
-def test_full_blocks_ragged_tail(crisp, monkeypatch, mode, count_kernel):
+def test_full_blocks_ragged_tail(crisp, monkeypatch, mode, variant):
     """Full 32768-id counter blocks (4096 counters per warp) with a ragged
     third block, stage by stage."""
-    monkeypatch.setenv("CRISP_COUNT_KERNEL", str(count_kernel))
+    for k_, v_ in COUNT_VARIANTS[variant].items():
+        monkeypatch.setenv(k_, v_)
     X, Qv, ox = make_case(cfg=1, N=70001, D=64, Q=24, M=4, K=16, seed=5)
     ix = build_gpu(crisp, X, ox, block_ids=32768)
     assert ix.info()["n_blocks"] == 3
