@@ -1006,6 +1006,28 @@ __device__ __forceinline__ void row_dist2(const float *__restrict__ r0, const fl
     o0 = warp_sum(a0);
     o1 = warp_sum(a1);
 }
+// four rows at once: the query reads (shared-memory wavefronts) are amortised
+// over four rows and four loads per lane are in flight per step
+__device__ __forceinline__ void row_dist4(const float *__restrict__ r0, const float *__restrict__ r1,
+                                          const float *__restrict__ r2, const float *__restrict__ r3,
+                                          const double *__restrict__ qd, int nvec, int lane, double (&o)[4]) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const float4 *x0 = (const float4 *)r0, *x1 = (const float4 *)r1, *x2 = (const float4 *)r2,
+                 *x3 = (const float4 *)r3;
+#pragma unroll 2
+    for (int v = lane; v < nvec; v += 32) {
+        const float4 u0 = __ldg(x0 + v), u1 = __ldg(x1 + v), u2 = __ldg(x2 + v), u3 = __ldg(x3 + v);
+        const Q4 qv = q4_at(qd, v, nvec);
+        acc4(a0, u0, qv);
+        acc4(a1, u1, qv);
+        acc4(a2, u2, qv);
+        acc4(a3, u3, qv);
+    }
+    o[0] = warp_sum(a0);
+    o[1] = warp_sum(a1);
+    o[2] = warp_sum(a2);
+    o[3] = warp_sum(a3);
+}
 __device__ __forceinline__ double row_dist1(const float *__restrict__ r0, const double *__restrict__ qd, int nvec,
                                             int lane) {
     double a0 = 0.0;
@@ -1110,37 +1132,49 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
     int64_t wi = 0x7fffffffffffffffLL;
     int bcur = 0;
     const int32_t *poolq = pool + q * CAPQ;
-    for (int v = gw; v < total; v += 2 * W) {
-        int v1 = v + W;
-        while (pre[bcur + 1] <= v) bcur++;
-        int lid0 = poolq[cbs[bcur] + (v - pre[bcur])];
-        int lid1 = -1;
-        if (v1 < total) {
+    // up to four rows per warp step (v, v+W, v+2W, v+3W); the candidate ids come
+    // from the segments through a monotone segment pointer
+    auto lid_at = [&](int vv, int &bc) -> int {
+        while (pre[bc + 1] <= vv) bc++;
+        return poolq[cbs[bc] + (vv - pre[bc])];
+    };
+    auto offer = [&](double dd, int64_t gg) {
+        if (cnt < k || less_di(dd, gg, wd, wi)) {
+            warp_insert(myd, myi, cnt, k, dd, gg, lane);
+            if (cnt == k) {
+                wd = myd[k - 1];
+                wi = myi[k - 1];
+            }
+        }
+    };
+    for (int v = gw; v < total; v += 4 * W) {
+        if (v + 3 * W < total) {
             int b1 = bcur;
-            while (pre[b1 + 1] <= v1) b1++;
-            lid1 = poolq[cbs[b1] + (v1 - pre[b1])];
+            const int l0 = lid_at(v, bcur), l1 = lid_at(v + W, b1), l2 = lid_at(v + 2 * W, b1),
+                      l3 = lid_at(v + 3 * W, b1);
+            double d4[4];
+            row_dist4(X + (int64_t)l0 * pitch, X + (int64_t)l1 * pitch, X + (int64_t)l2 * pitch,
+                      X + (int64_t)l3 * pitch, qd, nvec, lane, d4);
+            offer(d4[0], gid_base + l0);
+            offer(d4[1], gid_base + l1);
+            offer(d4[2], gid_base + l2);
+            offer(d4[3], gid_base + l3);
+            continue;
         }
-        double d0, d1;
-        if (lid1 >= 0) {
-            row_dist2(X + (int64_t)lid0 * pitch, X + (int64_t)lid1 * pitch, qd, nvec, lane, d0, d1);
-        } else {
-            d0 = row_dist1(X + (int64_t)lid0 * pitch, qd, nvec, lane);
-            d1 = INFINITY;
-        }
-        int64_t g0 = gid_base + lid0, g1 = gid_base + lid1;
-        if (cnt < k || less_di(d0, g0, wd, wi)) {
-            warp_insert(myd, myi, cnt, k, d0, g0, lane);
-            if (cnt == k) {
-                wd = myd[k - 1];
-                wi = myi[k - 1];
+        for (int vv = v; vv < total; vv += 2 * W) {
+            const int v1 = vv + W;
+            int b1 = bcur;
+            const int lid0 = lid_at(vv, bcur);
+            const int lid1 = v1 < total ? lid_at(v1, b1) : -1;
+            double d0, d1;
+            if (lid1 >= 0) {
+                row_dist2(X + (int64_t)lid0 * pitch, X + (int64_t)lid1 * pitch, qd, nvec, lane, d0, d1);
+            } else {
+                d0 = row_dist1(X + (int64_t)lid0 * pitch, qd, nvec, lane);
+                d1 = INFINITY;
             }
-        }
-        if (lid1 >= 0 && (cnt < k || less_di(d1, g1, wd, wi))) {
-            warp_insert(myd, myi, cnt, k, d1, g1, lane);
-            if (cnt == k) {
-                wd = myd[k - 1];
-                wi = myi[k - 1];
-            }
+            offer(d0, gid_base + lid0);
+            if (lid1 >= 0) offer(d1, gid_base + lid1);
         }
     }
     if (lane == 0) wcnt[warp] = cnt;
@@ -1668,19 +1702,33 @@ __global__ void __launch_bounds__(THREADS) k_verify_rows(const float *__restrict
     const int W = gridDim.x * WARPS;
     const int32_t *ord = pool + q * PS + j0;
     double *dq = dbuf + q * (int64_t)S0;
-    for (int j = blockIdx.x * WARPS + warp; j < n; j += 2 * W) {
-        const int j1 = j + W;
-        const int l0 = ord[j];
-        if (j1 < n) {
-            double d0, d1;
-            row_dist2(X + (int64_t)l0 * pitch, X + (int64_t)ord[j1] * pitch, qd, nvec, lane, d0, d1);
+    for (int j = blockIdx.x * WARPS + warp; j < n; j += 4 * W) {
+        if (j + 3 * W < n) {
+            double d4[4];
+            row_dist4(X + (int64_t)ord[j] * pitch, X + (int64_t)ord[j + W] * pitch, X + (int64_t)ord[j + 2 * W] * pitch,
+                      X + (int64_t)ord[j + 3 * W] * pitch, qd, nvec, lane, d4);
             if (lane == 0) {
-                dq[j] = d0;
-                dq[j1] = d1;
+                dq[j] = d4[0];
+                dq[j + W] = d4[1];
+                dq[j + 2 * W] = d4[2];
+                dq[j + 3 * W] = d4[3];
             }
-        } else {
-            const double d0 = row_dist1(X + (int64_t)l0 * pitch, qd, nvec, lane);
-            if (lane == 0) dq[j] = d0;
+            continue;
+        }
+        for (int jj = j; jj < n; jj += 2 * W) {
+            const int j1 = jj + W;
+            const int l0 = ord[jj];
+            if (j1 < n) {
+                double d0, d1;
+                row_dist2(X + (int64_t)l0 * pitch, X + (int64_t)ord[j1] * pitch, qd, nvec, lane, d0, d1);
+                if (lane == 0) {
+                    dq[jj] = d0;
+                    dq[j1] = d1;
+                }
+            } else {
+                const double d0 = row_dist1(X + (int64_t)l0 * pitch, qd, nvec, lane);
+                if (lane == 0) dq[jj] = d0;
+            }
         }
     }
 }
@@ -2011,7 +2059,7 @@ struct Work {
 
     static int64_t per_query_bytes(const crisp_index *ix, int k, int mode, int64_t CAPQ, bool traceV) {
         const int KK = ix->K * ix->K;
-        const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));
+        const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 4));
         const int S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));
         int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 4 + (int64_t)ix->M * 12 + CAPQ * 4 +
                        (int64_t)ix->NBW * 8 + 64;
@@ -2025,7 +2073,7 @@ struct Work {
          cudaStream_t s)
         : ix(ix_), k(k_), mode(mode_), Qc(Qc_), CAPQ(CAPQ_), buf(s) {
         const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch, Dp = ix->Dp;
-        S = std::max(1, env_int("CRISP_RERANK_SPLITS", 8));       // CTAs per query in the row kernels
+        S = std::max(1, env_int("CRISP_RERANK_SPLITS", 4));       // CTAs per query in the row kernels
         HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 2));     // CTAs per query in k_hamming(_dense)
         S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
         R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
