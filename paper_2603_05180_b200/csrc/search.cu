@@ -1108,7 +1108,7 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
                                                            const int32_t *__restrict__ cbase,
                                                            const int32_t *__restrict__ ncand, int NB, int k,
                                                            double *__restrict__ part_d, int64_t *__restrict__ part_i,
-                                                           const int32_t *__restrict__ qperm) {
+                                                           const int32_t *__restrict__ qperm, int rows4) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
     double *Ld = qd + pitch;                         // WARPS x k
@@ -1148,7 +1148,7 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
         }
     };
     for (int v = gw; v < total; v += 4 * W) {
-        if (v + 3 * W < total) {
+        if (rows4 && v + 3 * W < total) {
             int b1 = bcur;
             const int l0 = lid_at(v, bcur), l1 = lid_at(v + W, b1), l2 = lid_at(v + 2 * W, b1),
                       l3 = lid_at(v + 3 * W, b1);
@@ -1176,6 +1176,7 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
             offer(d0, gid_base + lid0);
             if (lid1 >= 0) offer(d1, gid_base + lid1);
         }
+        break;  // the two-row loop took every remaining row of this warp
     }
     if (lane == 0) wcnt[warp] = cnt;
     __syncthreads();
@@ -1686,7 +1687,7 @@ __global__ void __launch_bounds__(THREADS) k_verify_rows(const float *__restrict
                                                           int64_t PS, const int32_t *__restrict__ totals,
                                                           const int32_t *__restrict__ done, int r, int S0,
                                                           double *__restrict__ dbuf,
-                                                          const int32_t *__restrict__ qperm) {
+                                                          const int32_t *__restrict__ qperm, int rows4) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
@@ -1703,7 +1704,7 @@ __global__ void __launch_bounds__(THREADS) k_verify_rows(const float *__restrict
     const int32_t *ord = pool + q * PS + j0;
     double *dq = dbuf + q * (int64_t)S0;
     for (int j = blockIdx.x * WARPS + warp; j < n; j += 4 * W) {
-        if (j + 3 * W < n) {
+        if (rows4 && j + 3 * W < n) {
             double d4[4];
             row_dist4(X + (int64_t)ord[j] * pitch, X + (int64_t)ord[j + W] * pitch, X + (int64_t)ord[j + 2 * W] * pitch,
                       X + (int64_t)ord[j + 3 * W] * pitch, qd, nvec, lane, d4);
@@ -1730,6 +1731,7 @@ __global__ void __launch_bounds__(THREADS) k_verify_rows(const float *__restrict
                 if (lane == 0) dq[jj] = d0;
             }
         }
+        break;  // the two-row loop took every remaining row of this warp
     }
 }
 
@@ -2037,7 +2039,7 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
-    int S, HS, S0, R0, BPC, count_kernel, NS, ham_fused;
+    int S, HS, S0, R0, BPC, count_kernel, NS, ham_fused, rows4;
     DevBuf buf;
     float *qpad = nullptr, *qrot = nullptr;
     uint32_t *act = nullptr;
@@ -2083,6 +2085,8 @@ struct Work {
         count_kernel = env_int("CRISP_COUNT_KERNEL", ix->slice_hint >= 8.0 ? 1 : 0);
         NS = count_kernel == 0 ? NB : ix->NBW;  // candidate segments per query (id blocks or sub-blocks)
         ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
+        // row kernels: four rows per warp step for rows up to 4 KB (measured: faster at D=960, slower at 4096)
+        rows4 = env_int("CRISP_ROWS4", pitch <= 1024 ? 1 : 0);
         qpad = buf.alloc<float>((size_t)Qc * pitch);
         qrot = ix->rotated ? buf.alloc<float>((size_t)Qc * pitch) : qpad;
         act = buf.alloc<uint32_t>((size_t)Qc * M * KK);
@@ -2229,7 +2233,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
             StageScope st(s, 4);
             dim3 g(w.S, (unsigned)qn);
             k_rerank_exact<<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ, w.cbase,
-                                                         w.ncand, NB, k, w.part_d, w.part_i, w.qperm);
+                                                         w.ncand, NB, k, w.part_d, w.part_i, w.qperm, w.rows4);
             CRISP_LAUNCH();
             g_launches++;
         }
@@ -2277,7 +2281,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     for (int r = 0; r < w.R0; r++) {
         dim3 g(w.S, (unsigned)qn);
         k_verify_rows<<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst.done, r,
-                                                    w.S0, w.dbuf, w.qperm);
+                                                    w.S0, w.dbuf, w.qperm, w.rows4);
         CRISP_LAUNCH();
         g_launches++;
         k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.cbuf, w.CAPQ, ix->gid_base,

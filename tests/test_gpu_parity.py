@@ -97,10 +97,11 @@ def compare_trace(t, ot, mode, N):
 
 
 # collision-count variants: CTA-flattened, warp-owned (+ standalone dense
-# Hamming at phi=1), warp-owned with the Hamming popcounts fused
-COUNT_VARIANTS = {"select": {"CRISP_COUNT_KERNEL": "0"},
+# Hamming at phi=1), warp-owned with the Hamming popcounts fused; the row
+# kernels run two-row steps in the first and one CTA per query in the last
+COUNT_VARIANTS = {"select": {"CRISP_COUNT_KERNEL": "0", "CRISP_ROWS4": "0"},
                   "warp": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "0"},
-                  "warp_fused": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "1"}}
+                  "warp_fused": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "1", "CRISP_RERANK_SPLITS": "1"}}
 
 
 @pytest.mark.parametrize("variant", list(COUNT_VARIANTS))
