@@ -322,15 +322,17 @@ def run_crisp(args):
             # (k_count_warp) also gathers 8*ceil(D'/64) B of code per candidate (B_ham)
             cb_ = cnt["ids_streamed"] * 4 / K
             warp_kernel = os.environ.get("CRISP_COUNT_KERNEL", "1" if info["slice_hint"] >= 8.0 else "0") != "0"
+            fused = warp_kernel and os.environ.get("CRISP_HAMMING_FUSED", "0") != "0"
             name = "k_count_warp" if warp_kernel else "k_count_select"
-            if mode == 1 and warp_kernel:
+            if mode == 1 and fused:
                 cb_ += cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K
                 name = "k_count_warp (collision count + fused Hamming)"
             kernels["count"] = {"kernel": name, "bytes_per_step": cb_, "ms_per_step": st["count_select"] / K,
                                 "achieved_gbs": cb_ / (st["count_select"] / K * 1e-3) / 1e9}
-            if mode == 1 and not warp_kernel and st.get("hamming", 0) > 0:
+            if mode == 1 and not fused and st.get("hamming", 0) > 0:
                 hb = cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K  # SURVEY 8(d) B_ham
-                kernels["hamming"] = {"kernel": "k_hamming", "bytes_per_step": hb, "ms_per_step": st["hamming"] / K,
+                kernels["hamming"] = {"kernel": "k_hamming_dense" if warp_kernel else "k_hamming",
+                                      "bytes_per_step": hb, "ms_per_step": st["hamming"] / K,
                                       "achieved_gbs": hb / (st["hamming"] / K * 1e-3) / 1e9}
         for kk in kernels.values():
             kk["frac_of_peak"] = kk["achieved_gbs"] / peak
