@@ -1102,13 +1102,14 @@ __device__ __forceinline__ void block_prefix(const int32_t *__restrict__ ncand, 
     }
 }
 
+template <bool ROWS4>
 __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restrict__ qrot, int pitch,
                                                            const float *__restrict__ X, int64_t gid_base,
                                                            const int32_t *__restrict__ pool, int64_t CAPQ,
                                                            const int32_t *__restrict__ cbase,
                                                            const int32_t *__restrict__ ncand, int NB, int k,
                                                            double *__restrict__ part_d, int64_t *__restrict__ part_i,
-                                                           const int32_t *__restrict__ qperm, int rows4) {
+                                                           const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
     double *Ld = qd + pitch;                         // WARPS x k
@@ -1148,7 +1149,7 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
         }
     };
     for (int v = gw; v < total; v += 4 * W) {
-        if (rows4 && v + 3 * W < total) {
+        if (ROWS4 && v + 3 * W < total) {
             int b1 = bcur;
             const int l0 = lid_at(v, bcur), l1 = lid_at(v + W, b1), l2 = lid_at(v + 2 * W, b1),
                       l3 = lid_at(v + 3 * W, b1);
@@ -1682,12 +1683,13 @@ struct PatState {
     int64_t *nver;    // Qc, rows verified when done
 };
 
-__global__ void __launch_bounds__(THREADS) k_verify_rows(const float *__restrict__ qrot, int pitch,
+template <bool ROWS4>
+__global__ void __launch_bounds__(THREADS, 5) k_verify_rows(const float *__restrict__ qrot, int pitch,
                                                           const float *__restrict__ X, const int32_t *__restrict__ pool,
                                                           int64_t PS, const int32_t *__restrict__ totals,
                                                           const int32_t *__restrict__ done, int r, int S0,
                                                           double *__restrict__ dbuf,
-                                                          const int32_t *__restrict__ qperm, int rows4) {
+                                                          const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
@@ -1704,7 +1706,7 @@ __global__ void __launch_bounds__(THREADS) k_verify_rows(const float *__restrict
     const int32_t *ord = pool + q * PS + j0;
     double *dq = dbuf + q * (int64_t)S0;
     for (int j = blockIdx.x * WARPS + warp; j < n; j += 4 * W) {
-        if (rows4 && j + 3 * W < n) {
+        if (ROWS4 && j + 3 * W < n) {
             double d4[4];
             row_dist4(X + (int64_t)ord[j] * pitch, X + (int64_t)ord[j + W] * pitch, X + (int64_t)ord[j + 2 * W] * pitch,
                       X + (int64_t)ord[j + 3 * W] * pitch, qd, nvec, lane, d4);
@@ -2021,12 +2023,14 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     done = true;
@@ -2232,8 +2236,12 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         {
             StageScope st(s, 4);
             dim3 g(w.S, (unsigned)qn);
-            k_rerank_exact<<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ, w.cbase,
-                                                         w.ncand, NB, k, w.part_d, w.part_i, w.qperm, w.rows4);
+            if (w.rows4)
+                k_rerank_exact<true><<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ,
+                                                                   w.cbase, w.ncand, NB, k, w.part_d, w.part_i, w.qperm);
+            else
+                k_rerank_exact<false><<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ,
+                                                                    w.cbase, w.ncand, NB, k, w.part_d, w.part_i, w.qperm);
             CRISP_LAUNCH();
             g_launches++;
         }
@@ -2280,8 +2288,12 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     StageScope st(s, 4);
     for (int r = 0; r < w.R0; r++) {
         dim3 g(w.S, (unsigned)qn);
-        k_verify_rows<<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst.done, r,
-                                                    w.S0, w.dbuf, w.qperm, w.rows4);
+        if (w.rows4)
+            k_verify_rows<true><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst.done,
+                                                              r, w.S0, w.dbuf, w.qperm);
+        else
+            k_verify_rows<false><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals,
+                                                               w.pst.done, r, w.S0, w.dbuf, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
         k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.cbuf, w.CAPQ, ix->gid_base,
