@@ -272,8 +272,18 @@ __device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64
         const int ma = m_of_entry(S.lpre, M, e0), mb = m_of_entry(S.lpre, M, e0 + ne - 1);
         for (int P0 = 0; P0 < T; P0 += CS_TCAP) {
             const int Wn = min(CS_TCAP, T - P0);
-            // fill the window: position -> ids[] index (| weight flag)
-            for (int t = warp; t < ne; t += WARPS) {
+            // fill the window: position -> ids[] index (| weight flag), visiting only
+            // the entries that overlap [P0, P0 + Wn): the first by binary search
+            int ta = 0;
+            {
+                int hi2 = ne;  // largest ta with pre[ta] <= P0
+                while (hi2 - ta > 1) {
+                    const int mid = (ta + hi2) >> 1;
+                    if (S.pre[mid] <= P0) ta = mid;
+                    else hi2 = mid;
+                }
+            }
+            for (int t = ta + warp; t < ne && S.pre[t] < P0 + Wn; t += WARPS) {
                 const int p0 = S.pre[t];
                 const int a = max(p0, P0), z = min(S.pre[t + 1], P0 + Wn);
                 const int g = S.gst[t];
