@@ -170,6 +170,9 @@ struct CountSmem {
     typename cub::BlockScan<int, THREADS>::TempStorage scan;
 };
 
+// bank swizzle of the staged window positions (k_count_select)
+__device__ __forceinline__ int pos_swz(int p) { return p ^ ((p >> 4) & 15); }
+
 __device__ __forceinline__ int m_of_entry(const int32_t *lpre, int M, int e) {
     int lo = 0, hi = M;  // largest m with lpre[m] <= e
     while (hi - lo > 1) {
@@ -272,22 +275,34 @@ __device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64
         const int ma = m_of_entry(S.lpre, M, e0), mb = m_of_entry(S.lpre, M, e0 + ne - 1);
         for (int P0 = 0; P0 < T; P0 += CS_TCAP) {
             const int Wn = min(CS_TCAP, T - P0);
-            // fill the window: position -> ids[] index (| weight flag), visiting only
-            // the entries that overlap [P0, P0 + Wn): the first by binary search
-            int ta = 0;
+            // fill the window: position -> ids[] index (| weight flag).  Thread tid
+            // takes the CS_U consecutive positions from tid*CS_U: a binary search
+            // finds the entry of the first, then it walks forward (S.pos is
+            // swizzled, pos_swz, so these writes and the strided reads below are
+            // nearly conflict-free)
             {
-                int hi2 = ne;  // largest ta with pre[ta] <= P0
-                while (hi2 - ta > 1) {
-                    const int mid = (ta + hi2) >> 1;
-                    if (S.pre[mid] <= P0) ta = mid;
-                    else hi2 = mid;
+                const int pa = tid * CS_U;
+                if (pa < Wn) {
+                    int t = 0, hi2 = ne;  // largest t with pre[t] <= P0 + pa
+                    while (hi2 - t > 1) {
+                        const int mid = (t + hi2) >> 1;
+                        if (S.pre[mid] <= P0 + pa) t = mid;
+                        else hi2 = mid;
+                    }
+                    int nxt = S.pre[t + 1], cur = S.pre[t], g = S.gst[t];
+#pragma unroll 4
+                    for (int i = 0; i < CS_U; i++) {
+                        const int P = P0 + pa + i;
+                        if (pa + i >= Wn) break;
+                        while (nxt <= P) {
+                            t++;
+                            cur = nxt;
+                            nxt = S.pre[t + 1];
+                            g = S.gst[t];
+                        }
+                        S.pos[pos_swz(pa + i)] = g + (P - cur);
+                    }
                 }
-            }
-            for (int t = ta + warp; t < ne && S.pre[t] < P0 + Wn; t += WARPS) {
-                const int p0 = S.pre[t];
-                const int a = max(p0, P0), z = min(S.pre[t + 1], P0 + Wn);
-                const int g = S.gst[t];
-                for (int p = a + lane; p < z; p += 32) S.pos[p - P0] = g + (p - p0);
             }
             __syncthreads();
             // stage the window's ids: independent coalesced loads
@@ -296,7 +311,7 @@ __device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64
 #pragma unroll
                 for (int u = 0; u < CS_U; u++) {
                     const int p = tid + u * THREADS;
-                    v[u] = p < Wn ? S.pos[p] : 0;
+                    v[u] = p < Wn ? S.pos[pos_swz(p)] : 0;
                 }
 #pragma unroll
                 for (int u = 0; u < CS_U; u++) {
@@ -306,7 +321,7 @@ __device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64
 #pragma unroll
                 for (int u = 0; u < CS_U; u++) {
                     const int p = tid + u * THREADS;
-                    if (p < Wn) S.pos[p] = (int32_t)(((uint32_t)idv[u] - bbase) | ((uint32_t)v[u] & WFLAG));
+                    if (p < Wn) S.pos[pos_swz(p)] = (int32_t)(((uint32_t)idv[u] - bbase) | ((uint32_t)v[u] & WFLAG));
                 }
             }
             if (tid <= mb - ma) {  // window position range of each subspace
@@ -320,7 +335,7 @@ __device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64
             for (int mi = 0; mi <= mb - ma; mi++) {
                 const int pe = S.mpe[mi];
                 for (int p = S.mps[mi] + tid; p < pe; p += THREADS) {
-                    const uint32_t x = (uint32_t)S.pos[p];
+                    const uint32_t x = (uint32_t)S.pos[pos_swz(p)];
                     const uint32_t local = x & ~WFLAG;
                     const int old = cnt8[local];
                     const int nw = old + 1 + (int)(x >> 31);
