@@ -195,6 +195,26 @@ def test_fallback_and_small_k(crisp, mode):
     assert ot["fallback"].any()
 
 
+@pytest.mark.parametrize("variant", list(COUNT_VARIANTS))
+@pytest.mark.parametrize("mode", [0, 1])
+def test_k100_text_like(crisp, monkeypatch, mode, variant):
+    """k = 100 (cfg4's k) on a cfg4-like rotated, normalised low-rank case:
+    the per-warp top-k lists, their merge and the patience scan at k = 100,
+    against the oracle end to end and stage by stage."""
+    for k_, v_ in COUNT_VARIANTS[variant].items():
+        monkeypatch.setenv(k_, v_)
+    X, Qv, ox = make_case(cfg=4, N=30000, D=192, Q=20, M=8, K=24, rotation=1, seed=9)
+    ix = build_gpu(crisp, X, ox, block_ids=8192)
+    B, tau, k = 1500, 3, 100
+    ix.set_search_params(budget=B, tau=tau, patience_factor=4)
+    ids, d, t = ix.trace(Qv, k, mode)
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, mode, B, tau, patience_factor=4, trace=True)
+    compare_trace(t, ot, mode, X.shape[0])
+    assert_topk_parity(ids, d, r_ids, r_d, "k=100")
+    ids2, d2 = ix.search(Qv, k, mode)
+    assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
+
+
 def test_full_coverage_is_exact_knn(crisp):
     X, Qv, ox = make_case(cfg=1, N=6000, D=128, Q=25, M=4, K=10)
     ix = build_gpu(crisp, X, ox)
