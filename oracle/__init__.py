@@ -84,8 +84,12 @@ def _declare(L):
     L.or_half_sorted.argtypes = [vp, vp, i32, i32, vp, vp]
     L.or_multisequence.argtypes = [vp, vp, vp, vp, i32, vp, i64, i32, vp, vp, vp]
     L.or_multisequence.restype = i32
-    L.or_search.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, vp,
-                            vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.or_search.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, f64, i32,
+                            i32, vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.or_adsampling_threshold.argtypes = [f64, i32, i32, f64]
+    L.or_adsampling_threshold.restype = f64
+    L.or_adsampling_verify.argtypes = [vp, vp, i32, f64, f64, i32, vp]
+    L.or_adsampling_verify.restype = i32
     L.or_max_threads.restype = i32
     L.or_bruteforce_knn.argtypes = [vp, i64, i32, vp, i64, i32, vp, vp]
     L.or_bruteforce_scores.argtypes = [vp, i64, i32, i32, i32, i32, vp, vp, i64, i64, i32, vp]
@@ -367,12 +371,28 @@ def build(X, M: int, K: int = 50, tau_cev: float = 0.85, rotation_mode: int = -1
                 cb=cb, cells=cells, off=off, ids=ids, codes=cds, gsize=gsize, gid_base=gid_base, N_budget=N)
 
 
+def adsampling_threshold(rk2: float, t: int, D: int, eps0: float = 2.1) -> float:
+    """Eq. 2 (P:L240-244): r_k^2 * (t/D) * (1 + eps0/sqrt(t))^2."""
+    return lib().or_adsampling_threshold(rk2, t, D, eps0)
+
+
+def adsampling_verify(q, x, rk2: float, eps0: float = 2.1, stride: int = 32):
+    """SPEC adsampling_verify: (pruned, partial-or-exact squared distance)."""
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.zeros(1, dtype=np.float64)
+    pr = lib().or_adsampling_verify(_p(q), _p(x), q.size, rk2, eps0, stride, _p(out))
+    return bool(pr), float(out[0])
+
+
 def search(index, queries, k: int, mode: int, budget: int, tau: int, patience_factor: int = 40,
-           trace: bool = False, nthreads: int = 0, fallback: bool = True, ext_cand=None, ext_n=None):
+           trace: bool = False, nthreads: int = 0, fallback: bool = True, ext_cand=None, ext_n=None,
+           adsampling: bool = False, eps0: float = 2.1, ad_stride: int = 32):
     """Alg. 1 for a batch of queries.  budget/tau are the exact integers (O1).
     fallback=False skips the underflow fallback (first phase of the sharded
     protocol); ext_cand/ext_n (Q x N, Q; n < 0 = not given) replace C_q by a
     given ascending candidate list (its final phase).
+    adsampling=True verifies Optimized Mode candidates by ADSampling (Eq. 2).
     Returns (ids int64 QxK global, d64 QxK, trace dict or None)."""
     ix = index
     q = np.ascontiguousarray(queries, dtype=np.float32)
@@ -397,7 +417,8 @@ def search(index, queries, k: int, mode: int, budget: int, tau: int, patience_fa
     en = np.ascontiguousarray(ext_n, dtype=np.int64) if ext_n is not None else None
     lib().or_search(N, ix["gid_base"], ix["Dp"], M, K, ix["dh"], _p(ix["X"]),
                     _p(ix["R"]) if ix["R"] is not None else None, _p(ix["cb"]), _p(ix["off"]), _p(ix["ids"]),
-                    _p(ix["codes"]), _p(gsize), budget, tau, patience, 0 if fallback else 1, _p(ec), _p(en),
+                    _p(ix["codes"]), _p(gsize), budget, tau, patience, 1 if adsampling else 0, eps0, ad_stride,
+                    0 if fallback else 1, _p(ec), _p(en),
                     _p(qp), Q, k, mode, nthreads, _p(out_ids), _p(out_d),
                     T("act_len"), T("act_cell"), T("act_w"), T("retrieved"), T("V"), T("cand_n"), T("cand"),
                     T("order"), T("n_verified"), T("fallback"), T("qrot"))

@@ -670,6 +670,9 @@ typedef struct {
     int64_t budget;       /* B ids per subspace (exact integer, O1) */
     int32_t tau;          /* integer threshold (exact, O1) */
     int32_t patience;     /* P = factor*k, 0 = disabled */
+    int32_t ad_on;        /* phi=1 verification by ADSampling (Eq. 2) */
+    double ad_eps0;       /* its safety margin epsilon_0 (2.1) */
+    int32_t ad_stride;    /* checks every ad_stride dimensions (32) */
     int32_t fb_mode;      /* 0: underflow fallback; 1: none (sharded protocol, first phase) */
     const int32_t *ext_cand; /* Q x N external candidate lists (ascending local ids) or NULL */
     const int64_t *ext_n;    /* Q: length of the external list, < 0 = compute C normally */
@@ -688,6 +691,37 @@ typedef struct {
     int32_t *fallback;    /* Q flag                (or NULL) */
     float *qrot;          /* Q x D rotated query   (or NULL) */
 } or_trace;
+
+/* ADSampling (Eq. 2; SPEC adsampling_verify): the pruning
+ * threshold r_k^2 * (t/D) * (1 + eps0/sqrt(t))^2, evaluated in this order. */
+double or_adsampling_threshold(double rk2, int32_t t, int32_t D, double eps0)
+{
+    const double f = 1.0 + eps0 / sqrt((double)t);
+    return ((rk2 * (double)t) / (double)D) * (f * f);
+}
+
+/* Accumulate (q_i - x_i)^2 in dimension order (the dist64 chain); at every
+ * multiple t of stride with t < D, prune if the partial sum exceeds the
+ * threshold.  Returns 1 (pruned, *out = the partial sum at the pruning t) or
+ * 0 (*out = the exact dist64).  rk2 = +inf never prunes.  A check at t = D is
+ * not made: it could only prune a candidate whose exact distance exceeds r_k,
+ * which is non-improving either way. */
+int32_t or_adsampling_verify(const float *q, const float *x, int32_t D, double rk2, double eps0, int32_t stride,
+                             double *out)
+{
+    double s = 0.0;
+    for (int32_t i = 0; i < D; i++) {
+        double d = (double)q[i] - (double)x[i];
+        s = fma(d, d, s);
+        const int32_t t = i + 1;
+        if (stride > 0 && t % stride == 0 && t < D && s > or_adsampling_threshold(rk2, t, D, eps0)) {
+            *out = s;
+            return 1;
+        }
+    }
+    *out = s;
+    return 0;
+}
 
 static void search_one(const or_index *ix, const float *q_in, int32_t k, int32_t mode,
                        int64_t qi, int64_t *out_id, double *out_d, const or_trace *tr)
@@ -796,13 +830,25 @@ static void search_one(const or_index *ix, const float *q_in, int32_t k, int32_t
         }
         qsort(hs, (size_t)nc, sizeof(ham_id), cmp_ham_id);
         if (tr && tr->order) for (int64_t i = 0; i < nc; i++) tr->order[qi * N + i] = hs[i].id;
-        /* a5 (phi=1): exact L2 in that order with patience (Z11, Z12) */
+        /* a5 (phi=1): exact L2 in that order with patience (Z11, Z12),
+         * or ADSampling (Eq. 2) when ad_on: r_k^2 = +inf until k results exist, and a
+         * pruned candidate counts as a non-improving verification */
         int64_t cnt = 0;
         for (int64_t i = 0; i < nc; i++) {
             dist_id e;
-            e.d = or_dist64(q, ix->X + (int64_t)hs[i].id * D, D);
             e.id = ix->gid_base + hs[i].id;
             nver++;
+            if (ix->ad_on) {
+                const double rk2 = nb < k ? INFINITY : best[nb - 1].d;
+                if (or_adsampling_verify(q, ix->X + (int64_t)hs[i].id * D, D, rk2, ix->ad_eps0, ix->ad_stride,
+                                         &e.d)) {
+                    cnt++;
+                    if (ix->patience > 0 && cnt == ix->patience) break;
+                    continue;
+                }
+            } else {
+                e.d = or_dist64(q, ix->X + (int64_t)hs[i].id * D, D);
+            }
             if (nb < k || less_dist_id(e, best[nb - 1])) {
                 /* insert into the sorted top-k, evicting the worst when full */
                 int32_t pos = nb < k ? nb : k - 1;
@@ -829,6 +875,7 @@ static void search_one(const or_index *ix, const float *q_in, int32_t k, int32_t
 void or_search(int64_t N, int64_t gid_base, int32_t D, int32_t M, int32_t K, int32_t dh,
                const float *X, const float *R, const float *cb, const int64_t *off, const int32_t *ids,
                const uint64_t *codes, const int64_t *gsize, int64_t budget, int32_t tau, int32_t patience,
+               int32_t ad_on, double ad_eps0, int32_t ad_stride,
                int32_t fb_mode, const int32_t *ext_cand, const int64_t *ext_n,
                const float *queries, int64_t Q, int32_t k, int32_t mode, int32_t nthreads,
                int64_t *out_ids, double *out_d,
@@ -837,7 +884,7 @@ void or_search(int64_t N, int64_t gid_base, int32_t D, int32_t M, int32_t K, int
                int32_t *t_fallback, float *t_qrot)
 {
     or_index ix = {N, gid_base, D, M, K, dh, X, R, cb, off, ids, codes, gsize, budget, tau, patience,
-                   fb_mode, ext_cand, ext_n};
+                   ad_on, ad_eps0, ad_stride, fb_mode, ext_cand, ext_n};
     or_trace tr = {t_act_len, t_act_cell, t_act_w, t_retrieved, t_V, t_cand_n, t_cand, t_order, t_nver,
                    t_fallback, t_qrot};
 #ifdef _OPENMP

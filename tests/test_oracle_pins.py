@@ -500,3 +500,83 @@ def test_jacobi_matches_lapack_eigvalsh():
     A = r.standard_normal((40, 40))
     A = A @ A.T
     assert np.allclose(np.sort(oracle.eig_sym(A)), np.linalg.eigvalsh(A), rtol=1e-10, atol=1e-9)
+
+
+# ---------------------------------------------------------------- f1: ADSampling (Eq. 2)
+def test_adsampling_spec_example_S386():
+    """SPEC adsampling_verify: D=64, stride 32, a candidate whose first 32 dims
+    contribute 100 with r_k^2 = 10 is pruned at t = 32 (100 > ~9.4); r_k^2 = inf
+    never prunes and gives the exact squared distance."""
+    q = np.zeros(64, np.float32)
+    x = np.zeros(64, np.float32)
+    x[:32] = np.float32(math.sqrt(100 / 32))
+    x[32:] = 1000.0  # a candidate pruned at t = 32 never reads these
+    pruned, part = oracle.adsampling_verify(q, x, 10.0)
+    assert pruned and abs(part - 100.0) < 1e-4
+    pruned, full = oracle.adsampling_verify(q, x, math.inf)
+    assert not pruned and full == oracle.dist64(q, x)
+
+
+def test_adsampling_threshold_brackets_spec_value():
+    """The t = 32 threshold of the SPEC example (r_k^2 = 10, D = 64) lies
+    between 9.0 and 9.6 (SPEC prints ~9.37): partial 9.0 survives, 9.6 is pruned."""
+    q = np.zeros(64, np.float32)
+    for part, expect in ((9.0, False), (9.6, True)):
+        x = np.zeros(64, np.float32)
+        x[:32] = np.float32(math.sqrt(part / 32))
+        assert oracle.adsampling_verify(q, x, 10.0)[0] is expect
+
+
+def test_adsampling_checks_only_at_stride_multiples():
+    """A large early contribution is caught at the first checkpoint, t = 32: the
+    returned partial covers exactly the first 32 dimensions."""
+    q = np.zeros(96, np.float32)
+    x = np.full(96, 0.5, np.float32)
+    x[:4] = 50.0
+    pruned, part = oracle.adsampling_verify(q, x, 1.0)
+    assert pruned and part == oracle.dist64(q[:32], x[:32])
+    # stride 0 disables the checks entirely
+    assert oracle.adsampling_verify(q, x, 1.0, stride=0) == (False, oracle.dist64(q, x))
+
+
+def test_adsampling_prune_monotone_in_rk_and_margin():
+    """A smaller r_k or a smaller margin can only prune more (Eq. 2 is monotone)."""
+    r = rng(3)
+    D = 128
+    for _ in range(300):
+        q = r.standard_normal(D).astype(np.float32)
+        x = (q + 0.5 * r.standard_normal(D)).astype(np.float32)
+        full = oracle.dist64(q, x)
+        for rk2 in (0.3 * full, 0.6 * full, 0.9 * full, 1.2 * full):
+            if oracle.adsampling_verify(q, x, rk2, eps0=2.1)[0]:
+                assert oracle.adsampling_verify(q, x, 0.7 * rk2, eps0=2.1)[0]
+                assert oracle.adsampling_verify(q, x, rk2, eps0=1.0)[0]
+
+
+def test_adsampling_degenerate_margin_is_exact_verification():
+    """eps0 -> 1e9: no candidate is ever pruned, so Optimized Mode with
+    ADSampling equals Optimized Mode with exact L2 (SPEC mode-consistency),
+    including the patience stop."""
+    ix, _, Qv = small_index(N=3000)
+    kw = dict(k=5, mode=1, budget=400, tau=1, patience_factor=2, trace=True)
+    a = oracle.search(ix, Qv, **kw)
+    b = oracle.search(ix, Qv, adsampling=True, eps0=1e9, **kw)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2]["n_verified"], b[2]["n_verified"])
+
+
+def test_adsampling_search_exact_distances_and_recall():
+    """With ADSampling on a rotated index: every returned distance is the exact
+    dist64 of its id (a pruned candidate is never returned), prunes count as
+    non-improving verifications, and the result stays close to exact
+    verification (P:L732: "negligible cost to recall")."""
+    ix, X, Qv = small_index(N=4000, D=64, M=4, K=8, rot=1)
+    kw = dict(k=10, mode=1, budget=800, tau=1, patience_factor=5, trace=True)
+    ids_e, d_e, _ = oracle.search(ix, Qv, **kw)
+    ids_a, d_a, t = oracle.search(ix, Qv, adsampling=True, **kw)
+    hits = 0
+    for q in range(Qv.shape[0]):
+        for i, x in enumerate(ids_a[q]):
+            assert x >= 0 and d_a[q, i] == oracle.dist64(t["qrot"][q], ix["X"][x])
+        hits += len(set(ids_a[q].tolist()) & set(ids_e[q].tolist()))
+    assert hits / ids_e.size >= 0.9
