@@ -156,6 +156,17 @@ crisp_status crisp_set_global_cell_sizes(crisp_index *idx, const int64_t *sizes)
 crisp_status crisp_set_search_params(crisp_index *idx, double beta, int64_t budget, double alpha, int32_t tau,
                                      int32_t patience_factor);
 
+/* Optimized Mode verification by ADSampling (Eq. 2; SURVEY 8(f)
+ * row f1): a candidate is pruned at the first t = stride, 2*stride, ... < D at
+ * which its partial squared distance over the first t stored dimensions
+ * exceeds r_k^2 * (t/D) * (1 + eps0/sqrt(t))^2, r_k^2 being the current k-th
+ * best squared distance (+inf until k results exist); a pruned candidate counts
+ * as a non-improving verification for the patience rule.  enable = 0
+ * restores exact verification.  The paper's values are eps0 = 2.1 and
+ * stride = 32.  stride must divide 128 and be a multiple of 4; eps0
+ * must be >= 0.  Applies to searches with mode CRISP_OPTIMIZED only. */
+crisp_status crisp_set_adsampling(crisp_index *idx, int32_t enable, double eps0, int32_t stride);
+
 crisp_status crisp_index_info(const crisp_index *idx, crisp_index_info_t *out);
 
 /* Batched search, Alg. 1: a0 query transform, a1 half distances,

@@ -64,6 +64,7 @@ ABI_SYMBOLS = (
     "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
     "crisp_set_stage_timing", "crisp_stage_times", "crisp_search_counters", "crisp_free", "crisp_last_error", "crisp_version",
     "crisp_shard_search_begin", "crisp_shard_search_hist", "crisp_shard_search_finish", "crisp_shard_search_free",
+    "crisp_set_adsampling",
 )
 
 _lib = None
@@ -83,6 +84,7 @@ def lib():
         L.crisp_build_with.argtypes = [vp, i64, i32, P(Params), vp, vp, P(vp)]
         L.crisp_build_shard.argtypes = [vp, i64, i64, i32, P(Params), vp, vp, P(vp)]
         L.crisp_local_cell_sizes.argtypes = [vp, vp]
+        L.crisp_set_adsampling.argtypes = [vp, i32, f64, i32]
         L.crisp_set_global_cell_sizes.argtypes = [vp, vp]
         L.crisp_set_search_params.argtypes = [vp, f64, i64, f64, i32, i32]
         L.crisp_index_info.argtypes = [vp, P(Info)]
@@ -203,6 +205,10 @@ class Index:
         B = budget if budget else max(1, exact_ceil(beta if beta is not None else 0.01, info["N_global"]))
         T = tau if tau else max(1, exact_ceil(alpha if alpha is not None else 0.3, info["M"]))
         _check(lib().crisp_set_search_params(self._h, 0.0, int(B), 0.0, int(T), int(patience_factor)))
+
+    def set_adsampling(self, enable: bool = True, eps0: float = 2.1, stride: int = 32):
+        """crisp_set_adsampling: Optimized Mode verification by ADSampling (Eq. 2)."""
+        _check(lib().crisp_set_adsampling(self._h, 1 if enable else 0, float(eps0), int(stride)))
 
     def local_cell_sizes(self) -> np.ndarray:
         i = self.info()

@@ -281,6 +281,23 @@ crisp_status crisp_set_global_cell_sizes(crisp_index *ix, const int64_t *sizes) 
     }
 }
 
+crisp_status crisp_set_adsampling(crisp_index *ix, int32_t enable, double eps0, int32_t stride) {
+    try {
+        CRISP_CHECK(ix != nullptr, "index is NULL");
+        CRISP_CHECK(!enable || (stride >= 4 && stride % 4 == 0 && 128 % stride == 0),
+                    "ADSampling stride must be a multiple of 4 that divides 128");
+        CRISP_CHECK(!enable || (eps0 >= 0.0 && std::isfinite(eps0)), "ADSampling eps0 must be finite and >= 0");
+        ix->ad_on = enable ? 1 : 0;
+        if (enable) {
+            ix->ad_eps0 = eps0;
+            ix->ad_stride = stride;
+        }
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
 crisp_status crisp_set_search_params(crisp_index *ix, double beta, int64_t budget, double alpha, int32_t tau,
                                      int32_t patience_factor) {
     try {

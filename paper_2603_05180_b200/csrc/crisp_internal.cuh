@@ -76,6 +76,8 @@ struct crisp_index {
     double slice_hint = 0.0;   // expected ids of a query's activated slice per warp sub-block (count kernel choice)
     int64_t budget = 0;
     int32_t tau = 1, patience_factor = 40;
+    int32_t ad_on = 0, ad_stride = 32;  // Optimized Mode ADSampling (crisp_set_adsampling)
+    double ad_eps0 = 2.1;
     int64_t workspace_bytes = 0;
     int64_t hbm_bytes = 0;
 };

@@ -1712,16 +1712,16 @@ template <bool ROWS4>
 __global__ void __launch_bounds__(THREADS, 5) k_verify_rows(const float *__restrict__ qrot, int pitch,
                                                           const float *__restrict__ X, const int32_t *__restrict__ pool,
                                                           int64_t PS, const int32_t *__restrict__ totals,
-                                                          const int32_t *__restrict__ done, int r, int S0,
-                                                          double *__restrict__ dbuf,
+                                                          const int32_t *__restrict__ done, int j0r, int len,
+                                                          int dstride, double *__restrict__ dbuf,
                                                           const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
     if (done[q]) return;
     const int total = totals[q];
-    const int j0 = r * S0;
-    const int n = min(S0, total - j0);
+    const int j0 = j0r;
+    const int n = min(len, total - j0);
     if (n <= 0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     load_qd(qd, qrot + q * pitch, pitch);
@@ -1729,7 +1729,7 @@ __global__ void __launch_bounds__(THREADS, 5) k_verify_rows(const float *__restr
     const int nvec = pitch / 4;
     const int W = gridDim.x * WARPS;
     const int32_t *ord = pool + q * PS + j0;
-    double *dq = dbuf + q * (int64_t)S0;
+    double *dq = dbuf + q * (int64_t)dstride;
     for (int j = blockIdx.x * WARPS + warp; j < n; j += 4 * W) {
         if (ROWS4 && j + 3 * W < n) {
             double d4[4];
@@ -1762,16 +1762,135 @@ __global__ void __launch_bounds__(THREADS, 5) k_verify_rows(const float *__restr
     }
 }
 
+// ADSampling context of Optimized Mode verification (Eq. 2; crisp_set_adsampling)
+struct AdCtx {
+    int on;
+    double eps0;
+    int stride;
+    int Dp;
+    const float *X;   // stored rows (pitch floats)
+    int pitch;
+    int64_t gid_base;
+    const float *q;   // this query's q' (fp32, pitch floats)
+};
+
+// Eq. 2 threshold r_k^2 * (t/D) * (1 + eps0/sqrt(t))^2, in the oracle's order
+__device__ __forceinline__ double ad_thr(double rk2, int t, int D, double eps0) {
+    const double f = __dadd_rn(1.0, __ddiv_rn(eps0, __dsqrt_rn((double)t)));
+    return __dmul_rn(__ddiv_rn(__dmul_rn(rk2, (double)t), (double)D), __dmul_rn(f, f));
+}
+
+// Eq. 2 decided exactly as the oracle does: the partial sums in dimension
+// order (the dist64 chain), checked at t = stride, 2*stride, ... < D.  Lane 0
+// computes; the answer is broadcast.  Used only for candidates that would
+// enter the top-k (for every other candidate pruned and non-improving are the
+// same outcome).
+__device__ bool ad_pruned_seq(const AdCtx &ad, int64_t gid, double rk2, int lane) {
+    int pr = 0;
+    if (lane == 0) {
+        const float4 *x4 = (const float4 *)(ad.X + (gid - ad.gid_base) * (int64_t)ad.pitch);
+        const float4 *q4 = (const float4 *)ad.q;
+        double s = 0.0;
+        for (int v = 0; v < ad.Dp / 4 && !pr; v++) {
+            const float4 xv = __ldg(x4 + v), qv = __ldg(q4 + v);
+            const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, qa[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const double d = __dsub_rn((double)qa[c], (double)xa[c]);
+                s = __fma_rn(d, d, s);
+                const int t = 4 * v + c + 1;
+                if (!pr && t % ad.stride == 0 && t < ad.Dp && s > ad_thr(rk2, t, ad.Dp, ad.eps0)) pr = 1;
+            }
+        }
+    }
+    return __shfl_sync(0xffffffffu, pr, 0) != 0;
+}
+
+// One row under ADSampling with a certified early stop (warp per row): the
+// partial sums are formed 128 dimensions at a time (lane partials of 4 dims and
+// a warp prefix scan), and the row stops at the first checkpoint whose partial
+// exceeds thr(t) * (1 + 1e-12).  That margin exceeds the difference between
+// this summation order and the oracle's sequential chain (< t * 2^-52
+// relative for sums of non-negative terms), so a stopped row is pruned in the
+// sequential rule under this r_k, and so under any smaller r_k met later in
+// the same round (Eq. 2 is monotone in r_k).  Returns NaN for a stopped row,
+// else the full squared distance.  thr: thresholds per checkpoint c (t =
+// (c+1)*stride), already times (1 + 1e-12).
+__device__ __forceinline__ double ad_row(const float *__restrict__ row, const double *__restrict__ qd, int nvec, int Dp,
+                                         int stride, const double *__restrict__ thr, bool prune, int lane) {
+    const float4 *x4 = (const float4 *)row;
+    double run = 0.0;
+    const int per = stride >> 2;  // float4s per checkpoint interval
+    for (int v0 = 0; v0 < nvec; v0 += 32) {
+        const int v = v0 + lane;
+        double p = 0.0;
+        if (v < nvec) acc4(p, __ldg(x4 + v), q4_at(qd, v, nvec));
+        double sc = p;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, sc, off);
+            if (lane >= off) sc = __dadd_rn(sc, t);
+        }
+        if (prune) {
+            const int t = 4 * (v + 1);  // dimensions up to and including this lane's float4
+            bool over = false;
+            if (v < nvec && (v + 1) % per == 0 && t < Dp) over = __dadd_rn(run, sc) > thr[(v + 1) / per - 1];
+            if (__ballot_sync(0xffffffffu, over)) return __longlong_as_double(0x7ff8000000000000LL);  // NaN
+        }
+        run = __dadd_rn(run, __shfl_sync(0xffffffffu, sc, 31));
+    }
+    return run;
+}
+
+// k_verify_rows_ad: a speculative round under ADSampling.  r_k^2 is the query's
+// k-th best at the start of the round (+inf while fewer than k: no pruning).
+__global__ void __launch_bounds__(THREADS) k_verify_rows_ad(const float *__restrict__ qrot, int pitch, int Dp,
+                                                             const float *__restrict__ X,
+                                                             const int32_t *__restrict__ pool, int64_t PS,
+                                                             const int32_t *__restrict__ totals, PatState st, int k,
+                                                             int j0r, int len, int dstride, double *__restrict__ dbuf,
+                                                             const int32_t *__restrict__ qperm, double eps0,
+                                                             int stride) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    double *qd = (double *)sm;      // pitch
+    double *thr = qd + pitch;       // Dp / stride
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;
+    if (st.done[q]) return;
+    const int total = totals[q];
+    const int j0 = j0r;
+    const int n = min(len, total - j0);
+    if (n <= 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool prune = st.cnt[q] >= k;
+    const double rk2 = prune ? st.Td[q * k + k - 1] : 0.0;
+    load_qd(qd, qrot + q * pitch, pitch);
+    for (int c = threadIdx.x; c < Dp / stride; c += THREADS)
+        thr[c] = __dmul_rn(ad_thr(rk2, (c + 1) * stride, Dp, eps0), 1.0 + 1e-12);
+    __syncthreads();
+    const int nvec = pitch / 4;
+    const int W = gridDim.x * WARPS;
+    const int32_t *ord = pool + q * PS + j0;
+    double *dq = dbuf + q * (int64_t)dstride;
+    for (int j = blockIdx.x * WARPS + warp; j < n; j += W) {
+        const double d = ad_row(X + (int64_t)ord[j] * pitch, qd, nvec, Dp, stride, thr, prune, lane);
+        if (lane == 0) dq[j] = d;
+    }
+}
+
 // one warp scans up to 32 (d, id) entries (lanes >= gn invalid) against the
 // top-k list with the patience counter; returns the stop index or -1
+// The patience rule over one group of <= 32 verified candidates in order
+// (myd: exact d, or NaN = pruned by a round's certified early stop).  With
+// ADSampling a candidate that would enter a full top-k is first checked
+// against Eq. 2 under the current r_k; pruned candidates count as misses.
 __device__ __forceinline__ int patience_group(double myd, int64_t myi, int gn, double *Td, int64_t *Ti, int &cnt_top,
-                                              int &pat, int k, int P, int lane) {
+                                              int &pat, int k, int P, int lane, const AdCtx *ad = nullptr) {
     int start = 0;
     while (start < gn) {
         const bool full = cnt_top >= k;
         const double wdv = full ? Td[k - 1] : 0.0;
         const int64_t wiv = full ? Ti[k - 1] : 0;
-        const bool better = lane >= start && lane < gn && (!full || less_di(myd, myi, wdv, wiv));
+        const bool better = lane >= start && lane < gn && !isnan(myd) && (!full || less_di(myd, myi, wdv, wiv));
         const unsigned mask = __ballot_sync(0xffffffffu, better);
         const int f = mask ? (__ffs(mask) - 1) : gn;
         const int nonimp = f - start;
@@ -1780,6 +1899,12 @@ __device__ __forceinline__ int patience_group(double myd, int64_t myi, int gn, d
         if (f >= gn) break;
         const double dd = __shfl_sync(0xffffffffu, myd, f);
         const int64_t ii = __shfl_sync(0xffffffffu, myi, f);
+        if (ad && ad->on && full && ad_pruned_seq(*ad, ii, wdv, lane)) {
+            if (P > 0 && pat + 1 >= P) return f;
+            pat += 1;
+            start = f + 1;
+            continue;
+        }
         warp_insert(Td, Ti, cnt_top, k, dd, ii, lane);
         pat = 0;
         start = f + 1;
@@ -1801,10 +1926,11 @@ __device__ __forceinline__ void write_topk(int64_t q, int k, int cnt_top, const 
 // warp per query; dynamic smem WARPS x k (d, id)
 __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int32_t *__restrict__ totals,
                                                             const int32_t *__restrict__ pool, int64_t PS,
-                                                            int64_t gid_base, const double *__restrict__ dbuf, int r,
-                                                            int S0, int k, int P, PatState st,
+                                                            int64_t gid_base, const double *__restrict__ dbuf, int j0r,
+                                                            int len, int dstride, int k, int P, PatState st,
                                                             double *__restrict__ out_d64, float *__restrict__ out_d,
-                                                            int64_t *__restrict__ out_i) {
+                                                            int64_t *__restrict__ out_i, AdCtx ad,
+                                                            const float *__restrict__ qrot) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t q = (int64_t)blockIdx.x * WARPS + warp;
@@ -1818,16 +1944,17 @@ __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int
     }
     __syncwarp();
     const int total = totals[q];
-    const int j0 = r * S0;
-    const int n = max(0, min(S0, total - j0));
+    const int j0 = j0r;
+    const int n = max(0, min(len, total - j0));
     const int32_t *ord = pool + q * PS + j0;
-    const double *dq = dbuf + q * (int64_t)S0;
+    const double *dq = dbuf + q * (int64_t)dstride;
+    ad.q = qrot + q * (int64_t)ad.pitch;
     int64_t stop = -1;
     for (int g0 = 0; g0 < n && stop < 0; g0 += 32) {
         const int gn = min(32, n - g0);
         const double myd = lane < gn ? dq[g0 + lane] : INFINITY;
         const int64_t myi = lane < gn ? gid_base + ord[g0 + lane] : 0x7fffffffffffffffLL;
-        const int s = patience_group(myd, myi, gn, Td, Ti, cnt_top, pat, k, P, lane);
+        const int s = patience_group(myd, myi, gn, Td, Ti, cnt_top, pat, k, P, lane, &ad);
         if (s >= 0) stop = (int64_t)j0 + g0 + s + 1;
     }
     const bool fin = stop >= 0 || j0 + n >= total;
@@ -1859,7 +1986,7 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
                                                             const uint16_t *__restrict__ hbuf,
                                                             const int32_t *__restrict__ ncand,
                                                             const int32_t *__restrict__ cbase, int NS,
-                                                            const int32_t *__restrict__ qperm) {
+                                                            const int32_t *__restrict__ qperm, AdCtx ad) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int64_t q = qperm ? qperm[blockIdx.x] : blockIdx.x;  // locality order (query_order)
     if (st.done[q]) return;
@@ -1868,7 +1995,8 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
     int64_t *chi = (int64_t *)(chd + PATIENCE_CH);   // PATIENCE_CH
     double *Td = (double *)(chi + PATIENCE_CH);      // k
     int64_t *Ti = (int64_t *)(Td + k);               // k
-    int *hstart = (int *)(Ti + k);                   // Dp + 1
+    double *thr = (double *)(Ti + k);                // Dp / 4 + 1 (ADSampling thresholds of a chunk)
+    int *hstart = (int *)(thr + Dp / 4 + 1);         // Dp + 1
     int *spre = hstart + Dp + 1;                     // NS + 1
     int *scbs = spre + NS + 1;                       // NS
     __shared__ int s_stop, s_cnt;
@@ -1896,8 +2024,26 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
     const int32_t *ord = order + q * PS;
     const int nvec = pitch / 4;
     int64_t nver = total;
+    ad.q = qrot + q * (int64_t)pitch;
     for (int pos = from; pos < total; pos += PATIENCE_CH) {
         const int n = min(PATIENCE_CH, total - pos);
+        if (ad.on) {
+            // ADSampling: rows of the chunk with the certified early stop under the
+            // r_k at the chunk's start (see ad_row), then the in-order scan
+            const bool prune = s_cnt >= k;
+            const double rk2 = prune ? Td[k - 1] : 0.0;
+            for (int c = tid; c < Dp / ad.stride; c += THREADS)
+                thr[c] = __dmul_rn(ad_thr(rk2, (c + 1) * ad.stride, Dp, ad.eps0), 1.0 + 1e-12);
+            __syncthreads();
+            for (int i = warp; i < n; i += WARPS) {
+                const int l0 = ord[pos + i];
+                const double d0 = ad_row(X + (int64_t)l0 * pitch, qd, nvec, Dp, ad.stride, thr, prune, lane);
+                if (lane == 0) {
+                    chd[i] = d0;
+                    chi[i] = gid_base + l0;
+                }
+            }
+        } else
         for (int i = warp * 2; i < n; i += WARPS * 2) {
             const int l0 = ord[pos + i];
             if (i + 1 < n) {
@@ -1925,7 +2071,7 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
                 const int gn = min(32, n - g0);
                 const double myd = lane < gn ? chd[g0 + lane] : INFINITY;
                 const int64_t myi = lane < gn ? chi[g0 + lane] : 0x7fffffffffffffffLL;
-                const int s = patience_group(myd, myi, gn, Td, Ti, cnt_top, pat, k, P, lane);
+                const int s = patience_group(myd, myi, gn, Td, Ti, cnt_top, pat, k, P, lane, &ad);
                 if (s >= 0) stop = (int64_t)pos + g0 + s + 1;
             }
             if (lane == 0) {
@@ -2057,6 +2203,7 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows_ad, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     done = true;
 }
@@ -2068,7 +2215,9 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
-    int S, HS, S0, R0, BPC, count_kernel, NS, ham_fused, rows4;
+    int S, HS, S0, R0, BPC, count_kernel, NS, ham_fused, rows4, ad, F, vra_smem;
+    // end of the speculative rounds (positions the Hamming order must cover)
+    int rounds_end() const { return R0 == 0 ? 0 : F + (R0 - 1) * S0; }
     DevBuf buf;
     float *qpad = nullptr, *qrot = nullptr;
     uint32_t *act = nullptr;
@@ -2116,6 +2265,11 @@ struct Work {
         ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
         // row kernels: four rows per warp step for rows up to 4 KB (measured: faster at D=960, slower at 4096)
         rows4 = env_int("CRISP_ROWS4", pitch <= 1024 ? 1 : 0);
+        // ADSampling (Optimized Mode): a short first round establishes r_k, later
+        // rounds prune under it
+        ad = (mode == 1 && ix->ad_on) ? 1 : 0;
+        F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", 256))) : S0;
+        vra_smem = pitch * 8 + (Dp / 4 + 1) * 8;
         qpad = buf.alloc<float>((size_t)Qc * pitch);
         qrot = ix->rotated ? buf.alloc<float>((size_t)Qc * pitch) : qpad;
         act = buf.alloc<uint32_t>((size_t)Qc * M * KK);
@@ -2166,7 +2320,7 @@ struct Work {
         hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
         vr_smem = pitch * 8;
         scan_smem = WARPS * k * 16;
-        pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + (Dp + 1 + 2 * NS + 1) * 4;
+        pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + (Dp / 4 + 1) * 8 + (Dp + 1 + 2 * NS + 1) * 4;
         set_attrs();
         CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
                         pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
@@ -2303,32 +2457,41 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         if (w.hsort_cta_smem <= 200 * 1024)
             k_hsort_cta<<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
                 w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals,
-                w.full_order ? 0x7fffffff : w.R0 * w.S0);
+                w.full_order ? 0x7fffffff : w.rounds_end());
         else
             k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ,
-                                                           w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.R0 * w.S0);
+                                                           w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.rounds_end());
         CRISP_LAUNCH();
         g_launches++;
     }
     StageScope st(s, 4);
+    // speculative rounds: round 0 = positions [0, F), round r >= 1 = [F + (r-1) S0, F + r S0)
+    AdCtx ad{w.ad, ix->ad_eps0, ix->ad_stride, Dp, ix->X, pitch, ix->gid_base, nullptr};
     for (int r = 0; r < w.R0; r++) {
+        const int j0 = r == 0 ? 0 : w.F + (r - 1) * w.S0, len = r == 0 ? w.F : w.S0;
         dim3 g(w.S, (unsigned)qn);
-        if (w.rows4)
+        if (w.ad)
+            k_verify_rows_ad<<<g, THREADS, w.vra_smem, s>>>(w.qrot, pitch, Dp, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst,
+                                                            k, j0, len, w.S0, w.dbuf, w.qperm, ix->ad_eps0,
+                                                            ix->ad_stride);
+        else if (w.rows4)
             k_verify_rows<true><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst.done,
-                                                              r, w.S0, w.dbuf, w.qperm);
+                                                              j0, len, w.S0, w.dbuf, w.qperm);
         else
             k_verify_rows<false><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals,
-                                                               w.pst.done, r, w.S0, w.dbuf, w.qperm);
+                                                               w.pst.done, j0, len, w.S0, w.dbuf, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
         k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.cbuf, w.CAPQ, ix->gid_base,
-                                                                      w.dbuf, r, w.S0, k, P, w.pst, od64, od, oi);
+                                                                      w.dbuf, j0, len, w.S0, k, P, w.pst, od64, od, oi,
+                                                                      ad, w.qrot);
         CRISP_LAUNCH();
         g_launches++;
     }
     k_patience_tail<<<(unsigned)qn, THREADS, w.pat_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.cbuf, w.CAPQ,
-                                                              w.totals, w.R0 * w.S0, k, P, w.pst, od64, od, oi, Dp,
-                                                              w.ghist, w.pool, w.hbuf, w.ncand, w.cbase, NB, w.qperm);
+                                                              w.totals, w.rounds_end(), k, P, w.pst, od64, od, oi, Dp,
+                                                              w.ghist, w.pool, w.hbuf, w.ncand, w.cbase, NB, w.qperm,
+                                                              ad);
     CRISP_LAUNCH();
     g_launches++;
 }

@@ -380,3 +380,68 @@ def test_build_waits_for_pending_device_writes(crisp):
     e = ix.export()
     assert np.array_equal(e["X"][:, :D], X.cpu().numpy())
     ix.free()
+
+
+# ---------------------------------------------------------------- f1: ADSampling (Eq. 2)
+@pytest.mark.parametrize("rounds", [(256, 1024, 2), (32, 64, 2), (32, 64, 0)])
+def test_adsampling_stagewise(crisp, monkeypatch, rounds):
+    """Optimized Mode with ADSampling against the oracle, stage by stage
+    (Hamming order, patience stop, ids, distances): the default rounds, short
+    rounds (several pruning rounds and the sequential tail) and the tail alone."""
+    first, batch, nr = rounds
+    monkeypatch.setenv("CRISP_AD_FIRST", str(first))
+    monkeypatch.setenv("CRISP_PATIENCE_BATCH", str(max(batch, 64)))
+    monkeypatch.setenv("CRISP_PATIENCE_ROUNDS", str(nr))
+    X, Qv, ox = make_case(cfg=2, N=18001, D=90, Q=40, M=4, K=31, rotation=1, seed=3)
+    ix = build_gpu(crisp, X, ox, block_ids=4096)
+    B, tau, k = 700, 2, 7
+    for pf in (3, 40):
+        ix.set_search_params(budget=B, tau=tau, patience_factor=pf)
+        ix.set_adsampling(True, 2.1, 32)
+        ids, d, t = ix.trace(Qv, k, 1)
+        r_ids, r_d, ot = oracle.search(ox, Qv, k, 1, B, tau, patience_factor=pf, trace=True, adsampling=True)
+        compare_trace(t, ot, 1, X.shape[0])
+        assert_topk_parity(ids, d, r_ids, r_d, f"adsampling pf={pf}")
+        ids2, d2 = ix.search(Qv, k, 1)
+        assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
+
+
+@pytest.mark.parametrize("eps0,stride", [(2.1, 32), (0.5, 16), (2.1, 128)])
+def test_adsampling_margins_and_strides(crisp, eps0, stride):
+    """Other margins and checkpoint strides, cfg1 (N=20k, D=256, M=8)."""
+    X, Qv, ox = make_case()
+    ix = build_gpu(crisp, X, ox)
+    B, tau, k = oracle.budget_ids(0.01, 20000), 3, 10
+    ix.set_search_params(budget=B, tau=tau, patience_factor=40)
+    ix.set_adsampling(True, eps0, stride)
+    ids, d, t = ix.trace(Qv, k, 1)
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, 1, B, tau, patience_factor=40, trace=True, adsampling=True,
+                                   eps0=eps0, ad_stride=stride)
+    compare_trace(t, ot, 1, X.shape[0])
+    assert_topk_parity(ids, d, r_ids, r_d, f"adsampling eps0={eps0} stride={stride}")
+    # switching it off restores exact verification
+    ix.set_adsampling(False)
+    ids3, _ = ix.search(Qv, k, 1)
+    r3, _, _ = oracle.search(ox, Qv, k, 1, B, tau, patience_factor=40)
+    assert np.array_equal(ids3, r3)
+
+
+def test_adsampling_k100(crisp):
+    X, Qv, ox = make_case(cfg=4, N=30000, D=192, Q=20, M=8, K=24, rotation=1, seed=9)
+    ix = build_gpu(crisp, X, ox, block_ids=8192)
+    B, tau, k = 1500, 3, 100
+    ix.set_search_params(budget=B, tau=tau, patience_factor=4)
+    ix.set_adsampling(True)
+    ids, d, t = ix.trace(Qv, k, 1)
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, 1, B, tau, patience_factor=4, trace=True, adsampling=True)
+    compare_trace(t, ot, 1, X.shape[0])
+    assert_topk_parity(ids, d, r_ids, r_d, "adsampling k=100")
+
+
+def test_adsampling_rejects_bad_stride(crisp):
+    X, Qv, ox = make_case(cfg=1, N=2000, D=64, Q=4, M=4, K=6)
+    ix = build_gpu(crisp, X, ox)
+    with pytest.raises(crisp.CrispError):
+        ix.set_adsampling(True, 2.1, 24)
+    with pytest.raises(crisp.CrispError):
+        ix.set_adsampling(True, -1.0, 32)
