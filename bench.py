@@ -106,6 +106,15 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+MODE_NAMES = ["guaranteed", "optimized", "optimized_adsampling"]
+
+
+def phi(mode: int) -> int:
+    """Execution flag of a bench mode: 0 Guaranteed, 1 Optimized; bench mode 2 is
+    Optimized Mode verified by ADSampling (Eq. 2, crisp_set_adsampling)."""
+    return 0 if mode == 0 else 1
+
+
 def load_op(cfg: int, mode_override=None):
     """{M, seed, modes: {mode: {beta, alpha}}} restricted to --mode if given."""
     with open(OPS) as f:
@@ -161,7 +170,7 @@ def oracle_qps(X_host, Q_host, op, k, budget_seconds=15.0, max_queries=None):
     B, tau = oracle.budget_ids(beta, X_host.shape[0]), oracle.tau_int(alpha, M)
     nq = min(64, Q_host.shape[0])
     t0 = time.time()
-    oracle.search(ox, Q_host[:nq], k, mode, B, tau, nthreads=cores)
+    oracle.search(ox, Q_host[:nq], k, phi(mode), B, tau, nthreads=cores, adsampling=mode == 2)
     per_q = (time.time() - t0) / nq
     n = int(min(max_queries or Q_host.shape[0], max(nq, budget_seconds / max(per_q, 1e-6))))
     return ox, (B, tau), dict(per_q=per_q, n=n, cores=cores, build_s=t_build)
@@ -191,12 +200,13 @@ def run_reference(args):
     per_step = max(1, min(Q, int(cal["n"] * 1.0 / max(1, args.steps + args.warmup) * 3)))
     cores = cal["cores"]
     for s in range(args.warmup):
-        oracle.search(ox, Qh[:per_step], k, op["mode"], B, tau, nthreads=cores)
+        oracle.search(ox, Qh[:per_step], k, phi(op["mode"]), B, tau, nthreads=cores, adsampling=op["mode"] == 2)
     t0 = time.perf_counter()
     res = []
     for s in range(args.steps):
         lo = (s * per_step) % max(1, Q - per_step + 1)
-        ids, _, _ = oracle.search(ox, Qh[lo:lo + per_step], k, op["mode"], B, tau, nthreads=cores)
+        ids, _, _ = oracle.search(ox, Qh[lo:lo + per_step], k, phi(op["mode"]), B, tau, nthreads=cores,
+                                  adsampling=op["mode"] == 2)
         res.append((lo, ids))
     dt = time.perf_counter() - t0
     qps = per_step * args.steps / dt
@@ -272,13 +282,14 @@ def run_crisp(args):
     results = {}
     for mode, mp in sorted(op["modes"].items()):
         index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
+        index.set_adsampling(mode == 2)
         info = index.info()
 
         def step():
             if world == 1:
-                index.search_async(Qd, k, mode, ids, dd, stream)
+                index.search_async(Qd, k, phi(mode), ids, dd, stream)
                 return ids
-            oi, _ = cdist.search_step_exact(engine, Qd, k, mode, stream)
+            oi, _ = cdist.search_step_exact(engine, Qd, k, phi(mode), stream)
             return oi
 
         for _ in range(args.warmup):
@@ -314,7 +325,8 @@ def run_crisp(args):
         kernels = {}
         if st["verify"] > 0:
             vb = cnt["verified"] * row_bytes / K  # 4D per verified row (SURVEY 8(d) B_rerank)
-            kernels["verify"] = {"kernel": "k_rerank_exact" if mode == 0 else "k_verify_rows+k_patience_scan",
+            kernels["verify"] = {"kernel": ["k_rerank_exact", "k_verify_rows+k_patience_scan",
+                                            "k_verify_rows_ad+k_patience_scan"][mode],
                                  "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
                                  "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
         if st["count_select"] > 0:
@@ -324,12 +336,12 @@ def run_crisp(args):
             warp_kernel = os.environ.get("CRISP_COUNT_KERNEL", "1" if info["slice_hint"] >= 8.0 else "0") != "0"
             fused = warp_kernel and os.environ.get("CRISP_HAMMING_FUSED", "0") != "0"
             name = "k_count_warp" if warp_kernel else "k_count_select"
-            if mode == 1 and fused:
+            if phi(mode) == 1 and fused:
                 cb_ += cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K
                 name = "k_count_warp (collision count + fused Hamming)"
             kernels["count"] = {"kernel": name, "bytes_per_step": cb_, "ms_per_step": st["count_select"] / K,
                                 "achieved_gbs": cb_ / (st["count_select"] / K * 1e-3) / 1e9}
-            if mode == 1 and not fused and st.get("hamming", 0) > 0:
+            if phi(mode) == 1 and not fused and st.get("hamming", 0) > 0:
                 hb = cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K  # SURVEY 8(d) B_ham
                 kernels["hamming"] = {"kernel": "k_hamming_dense" if warp_kernel else "k_hamming",
                                       "bytes_per_step": hb, "ms_per_step": st["hamming"] / K,
@@ -371,17 +383,18 @@ def run_crisp(args):
     if rank == 0 and world == 1:
         mp = op["modes"][head]
         index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
+        index.set_adsampling(head == 2)
         qh = torch.empty((Q, D), dtype=torch.float32).pin_memory()
         qh.copy_(Qd.cpu())
         qn = qh.numpy()
         ih = torch.empty((Q, k), dtype=torch.int64).pin_memory().numpy()
         dh = torch.empty((Q, k), dtype=torch.float32).pin_memory().numpy()
         for _ in range(2):
-            crisp._check(crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, head, crisp._ptr(ih),
+            crisp._check(crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, phi(head), crisp._ptr(ih),
                                                   crisp._ptr(dh)))
         t0 = time.perf_counter()
         for _ in range(K):
-            crisp._check(crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, head, crisp._ptr(ih),
+            crisp._check(crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, phi(head), crisp._ptr(ih),
                                                   crisp._ptr(dh)))
         dt = time.perf_counter() - t0
         e2e = {"value": Q * K / dt, "unit": "queries/s", "h2d_bytes_per_step": Q * D * 4,
@@ -397,10 +410,10 @@ def run_crisp(args):
         ox, (B, tau), cal = oracle_qps(Xh, Qh, opx, k, budget_seconds=args.cpu_seconds)
         n = cal["n"]
         t0 = time.perf_counter()
-        oracle.search(ox, Qh[:n], k, head, B, tau, nthreads=cal["cores"])
+        oracle.search(ox, Qh[:n], k, phi(head), B, tau, nthreads=cal["cores"], adsampling=head == 2)
         dt = time.perf_counter() - t0
         cpu = {"value": n / dt, "unit": "queries/s", "cores": cal["cores"], "kind": "oracle",
-               "sample": f"first {n} of the {Q} queries ({['guaranteed', 'optimized'][head]} mode), oracle index "
+               "sample": f"first {n} of the {Q} queries ({MODE_NAMES[head]} mode), oracle index "
                          f"built on all N={N} (build {cal['build_s']:.0f}s, not timed)"}
         del ox
 
@@ -411,7 +424,7 @@ def run_crisp(args):
             "warmup": args.warmup, "ms_per_step": hr["ms"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": c["name"], "N": N, "D": D, "Q": Q, "k": k, "M": M, "beta": hr["beta"],
-                       "alpha": hr["alpha"], "mode": ["guaranteed", "optimized"][head], "budget_ids": hr["budget_ids"],
+                       "alpha": hr["alpha"], "mode": MODE_NAMES[head], "budget_ids": hr["budget_ids"],
                        "tau": hr["tau"], "rotated": bool(info["rotated"]), "cev": info["cev"],
                        "l2": "inputs larger than L2 (X = %.2f GB >> 126 MB); no flush" % (N * D * 4 / 1e9),
                        "parallelism": f"points sharded x{world}" if world > 1 else "single GPU"},
@@ -424,7 +437,7 @@ def run_crisp(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": hr["clocks"],
-            "per_mode": {["guaranteed", "optimized"][m]: {k_: v for k_, v in r.items() if k_ != "clocks"}
+            "per_mode": {MODE_NAMES[m]: {k_: v for k_, v in r.items() if k_ != "clocks"}
                          for m, r in results.items()},
             "build_seconds": build_s,
             "gen_seconds": gen_s,
@@ -467,11 +480,12 @@ def run_sweep(args):
             for beta in betas:
                 for alpha in alphas:
                     ix.set_search_params(beta=beta, alpha=alpha, patience_factor=40)
-                    ix.search_async(Qd, k, mode, ids, dd, stream)
+                    ix.set_adsampling(mode == 2)
+                    ix.search_async(Qd, k, phi(mode), ids, dd, stream)
                     torch.cuda.synchronize()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
-                    ix.search_async(Qd, k, mode, ids, dd, stream)
+                    ix.search_async(Qd, k, phi(mode), ids, dd, stream)
                     e1.record()
                     torch.cuda.synchronize()
                     ms = e0.elapsed_time(e1)

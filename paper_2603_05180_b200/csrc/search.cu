@@ -1781,17 +1781,57 @@ __device__ __forceinline__ double ad_thr(double rk2, int t, int D, double eps0) 
 }
 
 // Eq. 2 decided exactly as the oracle does: the partial sums in dimension
-// order (the dist64 chain), checked at t = stride, 2*stride, ... < D.  Lane 0
-// computes; the answer is broadcast.  Used only for candidates that would
-// enter the top-k (for every other candidate pruned and non-improving are the
-// same outcome).
+// order (the dist64 chain), checked at t = stride, 2*stride, ... < D.  Used
+// only for candidates that would enter the top-k (for every other candidate
+// pruned and non-improving are the same outcome).  The warp first forms the
+// partial sums in parallel (prefix scans, 128 dims per step) and the
+// thresholds (one checkpoint per lane); a decision whose partial sum is
+// farther than 1e-12 relative from its threshold is the sequential chain's
+// decision too (the two sums of non-negative terms differ by < t * 2^-52
+// relative).  Only if a checkpoint is that close does lane 0 run the
+// sequential chain itself.
 __device__ bool ad_pruned_seq(const AdCtx &ad, int64_t gid, double rk2, int lane) {
-    int pr = 0;
+    const float4 *x4 = (const float4 *)(ad.X + (gid - ad.gid_base) * (int64_t)ad.pitch);
+    const float4 *q4 = (const float4 *)ad.q;
+    const int nv = ad.Dp / 4, per = ad.stride >> 2, ncp = (ad.Dp - 1) / ad.stride;  // checkpoints t < D
+    double run = 0.0;
+    int verdict = 0;  // 0 undecided, 1 pruned, 2 not pruned, 3 ambiguous
+    for (int v0 = 0; v0 < nv && verdict == 0; v0 += 32) {
+        const int v = v0 + lane;
+        double p = 0.0;
+        if (v < nv) {
+            const float4 xv = __ldg(x4 + v), qv = __ldg(q4 + v);
+            const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, qa[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const double d = __dsub_rn((double)qa[c], (double)xa[c]);
+                p = __fma_rn(d, d, p);
+            }
+        }
+        double sc = p;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, sc, off);
+            if (lane >= off) sc = __dadd_rn(sc, t);
+        }
+        const double s = __dadd_rn(run, sc);
+        const int cp = (v + 1) / per;  // checkpoint index + 1 when (v + 1) % per == 0
+        bool above = false, close = false;
+        if (v < nv && (v + 1) % per == 0 && cp <= ncp) {
+            const double th = ad_thr(rk2, cp * ad.stride, ad.Dp, ad.eps0);
+            above = s > __dmul_rn(th, 1.0 + 1e-12);
+            close = !above && s >= __dmul_rn(th, 1.0 - 1e-12);
+        }
+        const unsigned ma = __ballot_sync(0xffffffffu, above), mc = __ballot_sync(0xffffffffu, close);
+        if (ma | mc) verdict = (mc && (!ma || __ffs(mc) < __ffs(ma))) ? 3 : 1;  // the first decisive checkpoint
+        run = __dadd_rn(run, __shfl_sync(0xffffffffu, sc, 31));
+    }
+    if (verdict == 0) verdict = 2;
+    if (verdict != 3) return verdict == 1;
+    int pr = 0;  // ambiguous: the sequential chain, as the oracle
     if (lane == 0) {
-        const float4 *x4 = (const float4 *)(ad.X + (gid - ad.gid_base) * (int64_t)ad.pitch);
-        const float4 *q4 = (const float4 *)ad.q;
         double s = 0.0;
-        for (int v = 0; v < ad.Dp / 4 && !pr; v++) {
+        for (int v = 0; v < nv && !pr; v++) {
             const float4 xv = __ldg(x4 + v), qv = __ldg(q4 + v);
             const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, qa[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
@@ -2268,7 +2308,7 @@ struct Work {
         // ADSampling (Optimized Mode): a short first round establishes r_k, later
         // rounds prune under it
         ad = (mode == 1 && ix->ad_on) ? 1 : 0;
-        F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", 256))) : S0;
+        F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : S0;
         vra_smem = pitch * 8 + (Dp / 4 + 1) * 8;
         qpad = buf.alloc<float>((size_t)Qc * pitch);
         qrot = ix->rotated ? buf.alloc<float>((size_t)Qc * pitch) : qpad;
@@ -2470,7 +2510,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     for (int r = 0; r < w.R0; r++) {
         const int j0 = r == 0 ? 0 : w.F + (r - 1) * w.S0, len = r == 0 ? w.F : w.S0;
         dim3 g(w.S, (unsigned)qn);
-        if (w.ad)
+        if (w.ad && r > 0)  // round 0 starts with an empty top-k: nothing to prune
             k_verify_rows_ad<<<g, THREADS, w.vra_smem, s>>>(w.qrot, pitch, Dp, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst,
                                                             k, j0, len, w.S0, w.dbuf, w.qperm, ix->ad_eps0,
                                                             ix->ad_stride);

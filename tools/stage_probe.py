@@ -48,7 +48,9 @@ for var in args.variants.split(";"):
         if mode not in op["modes"]:
             continue
         mp = op["modes"][mode]
-        index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=40)
+        index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=int(os.environ.get("PROBE_PF", "40")))
+        if mode == 1:
+            index.set_adsampling(os.environ.get("PROBE_AD", "0") == "1")
         index.search_async(Qd, k, mode, ids, dd, stream)
         torch.cuda.synchronize()
         crisp.stage_times(reset=True)
