@@ -683,17 +683,22 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
         }
         base = __shfl_sync(0xffffffffu, base, 0);
         int run = base;
+        const bool fits = (int64_t)base + n <= CAPQ;  // else only the positions below CAPQ are written
 #pragma unroll
         for (int i = 0; i < 8; i++) {
             uint32_t word = mk[i];
             const uint32_t inc = (inc16[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
-            int o = run + (int)inc - __popc(word);
+            const int o = run + (int)inc - __popc(word);
             const int g0 = sbase + i * 512 + lane * 16;
-            while (word) {
-                const int bit = __ffs(word) - 1;
-                if (o < CAPQ) outp[o] = g0 + bit;
-                o++;
-                word &= word - 1;
+            if (fits) {
+                int32_t *dst = outp + o;
+                while (word) {
+                    *dst++ = g0 + __ffs(word) - 1;
+                    word &= word - 1;
+                }
+            } else {
+                for (int oo = o; word; oo++, word &= word - 1)
+                    if (oo < CAPQ) outp[oo] = g0 + __ffs(word) - 1;
             }
             run += ctot[i];
         }
