@@ -56,30 +56,39 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
                                                     const float *__restrict__ cb, int M, int K, int dh,
                                                     const int32_t *__restrict__ gsize, int smem_gsize, int64_t budget,
                                                     int wk, uint32_t *__restrict__ act, int32_t *__restrict__ act_len,
-                                                    int64_t *__restrict__ retrieved) {
+                                                    int64_t *__restrict__ retrieved, int qpw, int smem_cb) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int KK = K * K;
     const int m = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int32_t *gs = (int32_t *)sm;
-    unsigned char *wbase = sm + (smem_gsize ? ((KK * 4 + 15) & ~15) : 0);
-    const int per_warp = ((4 * K * 8) + 3 * K + 15) & ~15;
+    float *cbs = (float *)(sm + (smem_gsize ? ((KK * 4 + 15) & ~15) : 0));  // this subspace's 2 x K x dh (smem_cb)
+    unsigned char *wbase = (unsigned char *)cbs + (smem_cb ? ((2 * K * dh * 4 + 15) & ~15) : 0);
+    const int per_warp = ((4 * K * 8) + 3 * K + 2 * dh * 4 + 15) & ~15;
     double *tmp = (double *)(wbase + warp * per_warp);  // 2K
     double *a = tmp + 2 * K, *b = a + K;
-    unsigned char *pa = (unsigned char *)(b + K), *pb = pa + K, *col = pb + K;
+    float *qs = (float *)(b + K);                       // 2 dh: this query's two halves
+    unsigned char *pa = (unsigned char *)(qs + 2 * dh), *pb = pa + K, *col = pb + K;
     const int32_t *gsm = gsize + (int64_t)m * KK;
-    if (smem_gsize) {
+    const float *cbm = cb + (int64_t)m * 2 * K * dh;
+    if (smem_gsize)
         for (int i = threadIdx.x; i < KK; i += THREADS) gs[i] = gsm[i];
-        __syncthreads();
-        gsm = gs;
-    }
-    const int64_t q = (int64_t)blockIdx.x * WARPS + warp;
+    if (smem_cb)
+        for (int i = threadIdx.x; i < 2 * K * dh; i += THREADS) cbs[i] = cbm[i];
+    __syncthreads();
+    if (smem_gsize) gsm = gs;
+    if (smem_cb) cbm = cbs;
+    // each warp takes qpw queries in turn (the codebooks and sizes staged once per CTA)
+    for (int qi = 0; qi < qpw; qi++) {
+    const int64_t q = ((int64_t)blockIdx.x * WARPS + warp) * qpw + qi;
     if (q >= Qc) return;
     const float *qm = qrot + q * pitch + (int64_t)m * 2 * dh;
+    for (int i = lane; i < 2 * dh; i += 32) qs[i] = qm[i];
+    __syncwarp();
     // half distances (Alg. 1 l.4): dist64, exactly the oracle's order
     for (int side = 0; side < 2; side++) {
-        const float *C = cb + (int64_t)(m * 2 + side) * K * dh;
-        for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64(qm + side * dh, C + (int64_t)c * dh, dh);
+        const float *C = cbm + (int64_t)side * K * dh;
+        for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64(qs + side * dh, C + (int64_t)c * dh, dh);
     }
     __syncwarp();
     // sort each half by (delta, c) via ranks
@@ -141,6 +150,8 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     if (lane == 0) {
         act_len[q * M + m] = rank;
         retrieved[q * M + m] = ret;
+    }
+    __syncwarp();
     }
 }
 
@@ -2280,7 +2291,7 @@ struct Work {
     PatState pst{};
     uint8_t *traceV = nullptr;
     bool full_order = false;  // trace: order every candidate (not only what the rounds read)
-    int probe_gs, probe_smem, count_smem, countw_smem, countw_ham_smem, rx_smem, ham_smem, hsort_smem, hsort_cta_smem, vr_smem, scan_smem, pat_smem;
+    int probe_gs, probe_cb, probe_qpw, probe_smem, count_smem, countw_smem, countw_ham_smem, rx_smem, ham_smem, hsort_smem, hsort_cta_smem, vr_smem, scan_smem, pat_smem;
 
     static int64_t per_query_bytes(const crisp_index *ix, int k, int mode, int64_t CAPQ, bool traceV) {
         const int KK = ix->K * ix->K;
@@ -2355,7 +2366,10 @@ struct Work {
         if (want_traceV) traceV = buf.alloc<uint8_t>((size_t)Qc * ix->N);
         if (want_d64tmp) d64tmp = buf.alloc<double>((size_t)Qc * k);
         probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
-        probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + WARPS * (((4 * K * 8) + 3 * K + 15) & ~15);
+        probe_cb = (2 * K * ix->dh * 4 <= 96 * 1024) ? 1 : 0;
+        probe_qpw = std::max(1, env_int("CRISP_PROBE_QPW", 4));  // queries per warp in k_probe
+        probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + (probe_cb ? ((2 * K * ix->dh * 4 + 15) & ~15) : 0) +
+                     WARPS * (((4 * K * 8) + 3 * K + 2 * ix->dh * 4 + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
         countw_smem = BS + 16 + (int)((sizeof(CountWSmem) + 15) & ~(size_t)15);
         countw_ham_smem = ix->Wp * 8 + (Dp + 1) * 4;
@@ -2389,9 +2403,10 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
     }
     {
         StageScope st(s, 1);
-        dim3 g(nblk(qn, WARPS), M);
+        dim3 g(nblk(qn, WARPS * w.probe_qpw), M);
         k_probe<<<g, THREADS, w.probe_smem, s>>>(w.qrot, pitch, qn, ix->cb, M, K, ix->dh, ix->gsize, w.probe_gs,
-                                                 ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr);
+                                                 ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr,
+                                                 w.probe_qpw, w.probe_cb);
         CRISP_LAUNCH();
         g_launches++;
         if (w.qperm) {
