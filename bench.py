@@ -234,6 +234,11 @@ def run_crisp(args):
 
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: CRISP_BENCH_DEVICE pins every rank to one GPU, with the gloo
+    # backend (no GPU kernel waits on another rank), to exercise the N>1 path
+    # on a single-GPU box; the driver's N>1 runs use one GPU per rank and NCCL
+    if os.environ.get("CRISP_BENCH_DEVICE") is not None:
+        local = int(os.environ["CRISP_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if rank == 0:
@@ -241,7 +246,10 @@ def run_crisp(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("CRISP_BENCH_DEVICE") is not None:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         dist.barrier()
     import paper_2603_05180_b200 as crisp
     from paper_2603_05180_b200 import dist as cdist
