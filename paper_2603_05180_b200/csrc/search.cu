@@ -2312,7 +2312,7 @@ struct Work {
         S = std::max(1, env_int("CRISP_RERANK_SPLITS", 4));       // CTAs per query in the row kernels
         HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 2));     // CTAs per query in k_hamming(_dense)
         S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
-        R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));
+        R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));  // speculative rounds (then the sequential tail)
         BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 16)));  // id blocks per count CTA
         // 0: k_count_select (CTA-flattened slices, for many small cells), 1: k_count_warp
         // (warp-owned sub-blocks, for slices of >= 8 ids per sub-block); env overrides
@@ -2495,15 +2495,16 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     const int P = ix->patience_factor > 0 ? ix->patience_factor * k : 0;
     CRISP_CUDA(cudaMemsetAsync(w.pst.cnt, 0, (size_t)w.Qc * 3 * 4, s));
     {
-        // k_count_warp computed h and the histogram with the count; only
-        // queries whose candidate set the fallback replaced are done here
+        // h of the queries whose candidate set the fallback replaced (k_hamming),
+        // then of all others over their dense pool positions (k_hamming_dense),
+        // unless k_count_warp computed it with the count
         StageScope st(s, 6);
         dim3 g(w.HS, (unsigned)qn);
         k_hamming<<<g, THREADS, w.ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool, w.CAPQ, w.cbase, w.ncand,
-                                                 NB, w.hbuf, w.ghist, w.count_kernel == 0 ? nullptr : w.fb, w.qperm);
+                                                 NB, w.hbuf, w.ghist, w.fb, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
-        if (w.count_kernel == 1 && !w.ham_fused) {
+        if (!(w.count_kernel == 1 && w.ham_fused)) {
             dim3 g2(w.HS, (unsigned)qn);
             k_hamming_dense<<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
                                                                    w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb, w.qperm);
