@@ -465,17 +465,24 @@ __global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__rest
 // writes suffice; __syncwarp orders consecutive batches (an id recurs only
 // across subspaces, CSR partition property).  The (slice, offset)
 // walk is a warp-uniform state machine; the id loads of CW_U batches are in
-// flight before their read-modify-writes.  a4 is a SWAR scan of the warp's
-// counters in ascending id that also re-zeroes them; each sub-block is its
-// own candidate segment (base from an atomic cursor, ascending ids inside).
+// flight before their read-modify-writes.
+// a4 (C = {x : V[x] >= tau}, Alg. 1 l.18) is taken at the read-modify-write:
+// V only grows, by 1 or 2, so x enters C exactly once, at the increment that
+// lifts V[x] from below tau to tau or more; that increment sets x's bit in the
+// warp's candidate bitmap (SBW bits).  After the sub-block the warp reads the
+// bitmap in ascending id (its own candidate segment, base from an atomic
+// cursor) and re-zeroes counters and bitmap; the counters are not scanned.
 // ---------------------------------------------------------------------------
 constexpr int CW_U = 8;  // 32-position batches with loads in flight per warp (k_count_warp)
+constexpr uint32_t CW_EMASK = 0xffffffu;  // cached entry: (m*KK + cell) | m << 24 | WFLAG
 struct CountWSmem {
-    uint32_t erow[CS_CAP];  // cached entries: (m*KK + cell) | WFLAG
-    uint32_t emw[CS_CAP];   // cached entries: m | WFLAG
+    uint32_t erow[CS_CAP];
     int32_t lpre[MAX_M + 2];
     int next;               // next sub-block task of the CTA (dynamic: warps stay balanced)
 };
+__host__ __device__ constexpr size_t countw_fixed_smem(int BS) {  // counters + dummy, bitmaps, CountWSmem
+    return (size_t)BS + 16 + (size_t)BS / 8 + ((sizeof(CountWSmem) + 15) & ~(size_t)15);
+}
 
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     uint32_t v;
@@ -485,16 +492,14 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-// 4-bit mask of the bytes of w that are >= t (t4 = t in every byte)
-template <bool SWAR>
-__device__ __forceinline__ uint32_t bytes_ge(uint32_t w, uint32_t t4) {
-    uint32_t h;
-    if (SWAR) h = ((w | 0x80808080u) - t4) & 0x80808080u;  // bytes and t < 128: no borrow between bytes
-    else h = __vcmpgeu4(w, t4) & 0x80808080u;
-    return (h * 0x00204081u) >> 28;  // bits 7,15,23,31 -> 28..31
+__device__ __forceinline__ uint32_t cw_entry(const uint32_t *__restrict__ actq, const int32_t *lpre, int M, int KK,
+                                             int e) {
+    const int m = m_of_entry(lpre, M, e);
+    const uint32_t v = __ldg(actq + (int64_t)m * KK + (e - lpre[m]));
+    return (uint32_t)(m * KK + (int)(v & 0xffffu)) | ((uint32_t)m << 24) | ((v >> 16) == 2u ? WFLAG : 0u);
 }
 
-template <bool SWAR, bool HAM>
+template <bool HAM>
 __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint32_t *__restrict__ act,
                                                            const int32_t *__restrict__ act_len, int M, int KK,
                                                            const int32_t *__restrict__ off2w, int NBW,
@@ -509,15 +514,17 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
                                                            const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned char *cnt8 = smraw;  // BS byte counters (+16 dummy bytes); warp w owns [w*SBW, (w+1)*SBW)
-    CountWSmem &S = *(CountWSmem *)(smraw + BS + 16);
+    uint32_t *bm = (uint32_t *)(smraw + BS + 16);  // candidate bitmaps: warp w owns words [w*SBW/32, +SBW/32)
+    CountWSmem &S = *(CountWSmem *)(smraw + BS + 16 + BS / 8);
     // phi=1 (hbuf != null): b(q') and the query's Hamming histogram of this CTA
-    uint64_t *qc = (uint64_t *)(smraw + BS + 16 + ((sizeof(CountWSmem) + 15) & ~(size_t)15));  // Wd
-    int *hist = (int *)(qc + Wd);                                                              // Dp + 1
+    uint64_t *qc = (uint64_t *)(smraw + countw_fixed_smem(BS));  // Wd
+    int *hist = (int *)(qc + Wd);                                 // Dp + 1
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int SBW = BS >> 3;
+    const int SBW = BS >> 3, NWW = SBW >> 5;  // counters / bitmap words per warp
     const int b_lo = blockIdx.x * BPC, b_hi = min(NB, b_lo + BPC);
     unsigned char *wc = cnt8 + warp * SBW;
+    uint32_t *wbm = bm + warp * NWW;
     const uint32_t sm_cnt = (uint32_t)__cvta_generic_to_shared(cnt8);
     const uint32_t sm_dummy = sm_cnt + (uint32_t)BS;
     // lpre (exclusive prefix of act_len over m) and the cached entries
@@ -539,7 +546,8 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
             S.next = 0;
         }
     }
-    for (int i = tid; i < SBW * WARPS / 16; i += THREADS) ((uint4 *)cnt8)[i] = make_uint4(0, 0, 0, 0);
+    // counters, the dummy counter (padding lanes add 0 to it) and the bitmaps
+    for (int i = tid; i < (BS + 16 + BS / 8) / 16; i += THREADS) ((uint4 *)cnt8)[i] = make_uint4(0, 0, 0, 0);
     if (HAM && hbuf) {
         const float *qrow = qrot + q * pitch;
         for (int d0 = warp * 32; d0 < Wd * 64; d0 += THREADS) {  // bit (i mod 64) of word i/64 = [q'_i > 0] (Z10)
@@ -551,19 +559,13 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
     }
     __syncthreads();
     const int Etot = S.lpre[M];
-    const bool cached = Etot <= CS_CAP;
     const uint32_t *actq = act + q * (int64_t)M * KK;
+    const bool cached = Etot <= CS_CAP && (int64_t)M * KK <= (int64_t)CW_EMASK + 1;
     if (cached)
-        for (int t = tid; t < Etot; t += THREADS) {
-            const int m = m_of_entry(S.lpre, M, t);
-            const uint32_t v = __ldg(actq + (int64_t)m * KK + (t - S.lpre[m]));
-            const uint32_t f = (v >> 16) == 2u ? WFLAG : 0u;
-            S.erow[t] = (uint32_t)(m * KK + (int)(v & 0xffffu)) | f;
-            S.emw[t] = (uint32_t)m | f;
-        }
+        for (int t = tid; t < Etot; t += THREADS) S.erow[t] = cw_entry(actq, S.lpre, M, KK, t);
     __syncthreads();
     const int nchunk = SBW / 512;  // 16-byte lane chunks of the warp's counters (SBW <= 4096: <= 8)
-    const uint32_t tau4 = (uint32_t)tau * 0x01010101u;
+    const uint32_t taum1 = (uint32_t)tau - 1u;
     int32_t *outp = pool + q * CAPQ;
     const int ntask = (b_hi - b_lo) * 8;
     for (;;) {
@@ -582,22 +584,12 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
                 uint32_t wf = 0;
                 int len = 0, g = 0;
                 if (e < Etot) {
-                    uint32_t erw, mw;
-                    if (cached) {
-                        erw = S.erow[e];
-                        mw = S.emw[e];
-                    } else {
-                        const int m = m_of_entry(S.lpre, M, e);
-                        const uint32_t v = __ldg(actq + (int64_t)m * KK + (e - S.lpre[m]));
-                        const uint32_t f = (v >> 16) == 2u ? WFLAG : 0u;
-                        erw = (uint32_t)(m * KK + (int)(v & 0xffffu)) | f;
-                        mw = (uint32_t)m | f;
-                    }
-                    const int32_t *o = off2w + (int64_t)(erw & ~WFLAG) * (NBW + 1) + sb;
+                    const uint32_t er = cached ? S.erow[e] : cw_entry(actq, S.lpre, M, KK, e);
+                    const int32_t *o = off2w + (int64_t)(er & CW_EMASK) * (NBW + 1) + sb;
                     const int s0 = __ldg(o), s1 = __ldg(o + 1);
                     len = s1 - s0;
-                    g = (int)(mw & ~WFLAG) * (int)N + s0;
-                    wf = mw >> 31;
+                    g = (int)((er >> 24) & 127u) * (int)N + s0;
+                    wf = er >> 31;
                 }
                 uint32_t rest = __ballot_sync(0xffffffffu, len > 0);  // slices still to walk
                 // warp-uniform walk state: current slice (start G, length L, flag F), offset p
@@ -611,14 +603,14 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
                     F = __shfl_sync(0xffffffffu, wf, j);
                 }
                 while (L > 0) {
-                    uint32_t xa[CW_U], xf[CW_U];
+                    uint32_t xa[CW_U], xi[CW_U];
 #pragma unroll
                     for (int u = 0; u < CW_U; u++) {
                         const bool ok = p + lane < L;
                         // unconditional load (past the slice end: its first id) so that no
                         // branch joins on the result and all CW_U loads are in flight
                         xa[u] = (uint32_t)__ldg(ids + (uint32_t)(G + (ok ? p + lane : 0)));
-                        xf[u] = ok ? F : 2u;  // 2: not a position
+                        xi[u] = ok ? 1u + F : 0u;  // increment: the weight (Alg. 1 l.10-12); 0 = not a position
                         p += 32;
                         if (p >= L) {  // next slice (uniform)
                             p = 0;
@@ -634,57 +626,54 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
                     }
 #pragma unroll
                     for (int u = 0; u < CW_U; u++) {
-                        const uint32_t a = xf[u] == 2u ? sm_dummy : sm_cnt + (xa[u] - lbase);
-                        sts_u8(a, lds_u8(a) + 1u + xf[u]);
+                        const uint32_t a = xi[u] ? sm_cnt + (xa[u] - lbase) : sm_dummy;
+                        const uint32_t v = lds_u8(a);
+                        sts_u8(a, v + xi[u]);
+                        if (taum1 - v < xi[u]) {  // v < tau <= v + inc: x enters C
+                            const uint32_t off = xa[u] - (uint32_t)sbase;
+                            atomicOr(wbm + (off >> 5), 1u << (off & 31));
+                        }
                         __syncwarp();
                     }
                 }
             }
         }
-        // a4: C = {x : V[x] >= tau} (Alg. 1 l.18) in ascending id; re-zero.
-        // Lane chunk i of the warp covers counters [i*512 + lane*16, +16).
-        uint32_t mk[8];
-        uint32_t s16[4] = {0, 0, 0, 0};  // per-chunk counts, 16-bit fields: chunks (0,1) (2,3) (4,5) (6,7)
+        // a4: read C in ascending id from the bitmap (lane l: words [l*wpl, (l+1)*wpl)),
+        // re-zero bitmap and counters.
+        if (traceV) {
+            for (int i = 0; i < nchunk; i++) {
+                const int64_t x0 = (int64_t)sbase + i * 512 + lane * 16;
+                const unsigned char *vb = wc + i * 512 + lane * 16;
+                for (int j = 0; j < 16; j++)
+                    if (x0 + j < N) traceV[q * N + x0 + j] = vb[j];
+            }
+        }
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            mk[i] = 0;
-            if (i < nchunk) {
-                uint4 *pv = (uint4 *)(wc + i * 512 + lane * 16);
-                const uint4 v = *pv;
-                if (traceV) {
-                    const int64_t x0 = (int64_t)sbase + i * 512 + lane * 16;
-                    const unsigned char *vb = (const unsigned char *)&v;
-                    for (int j = 0; j < 16; j++)
-                        if (x0 + j < N) traceV[q * N + x0 + j] = vb[j];
+        for (int i = 0; i < 8; i++)
+            if (i < nchunk) *(uint4 *)(wc + i * 512 + lane * 16) = make_uint4(0, 0, 0, 0);
+        const int wpl = NWW >= 32 ? NWW >> 5 : 1;  // 1, 2 or 4 (NWW in [16, 128])
+        uint32_t bw[4] = {0, 0, 0, 0};
+        if (lane * wpl < NWW) {
+            uint32_t *pw = wbm + lane * wpl;
+            if (wpl == 4) {
+                const uint4 v = *(const uint4 *)pw;
+                bw[0] = v.x, bw[1] = v.y, bw[2] = v.z, bw[3] = v.w;
+                *(uint4 *)pw = make_uint4(0, 0, 0, 0);
+            } else {
+                for (int j = 0; j < wpl; j++) {
+                    bw[j] = pw[j];
+                    pw[j] = 0;
                 }
-                const uint32_t m16 = bytes_ge<SWAR>(v.x, tau4) | (bytes_ge<SWAR>(v.y, tau4) << 4) |
-                                     (bytes_ge<SWAR>(v.z, tau4) << 8) | (bytes_ge<SWAR>(v.w, tau4) << 12);
-                mk[i] = m16;
-                s16[i >> 1] |= (uint32_t)__popc(m16) << ((i & 1) * 16);
-                *pv = make_uint4(0, 0, 0, 0);
             }
         }
-        uint32_t inc16[4];
+        const int c = __popc(bw[0]) + __popc(bw[1]) + __popc(bw[2]) + __popc(bw[3]);
+        int inc = c;
 #pragma unroll
-        for (int h = 0; h < 4; h++) {
-            uint32_t v = s16[h];
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, v, off);
-                if (lane >= off) v += t;
-            }
-            inc16[h] = v;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int tt = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += tt;
         }
-        int ctot[8];
-#pragma unroll
-        for (int h = 0; h < 4; h++) {
-            const uint32_t t = __shfl_sync(0xffffffffu, inc16[h], 31);
-            ctot[2 * h] = (int)(t & 0xffffu);
-            ctot[2 * h + 1] = (int)(t >> 16);
-        }
-        int n = 0;
-#pragma unroll
-        for (int i = 0; i < 8; i++) n += ctot[i];
+        const int n = __shfl_sync(0xffffffffu, inc, 31);
         int base = 0;
         if (lane == 0) {
             base = atomicAdd(cursor + q, n);
@@ -693,26 +682,18 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
             if ((int64_t)base + n > CAPQ) atomicMax(need, base + n);
         }
         base = __shfl_sync(0xffffffffu, base, 0);
-        int run = base;
-        const bool fits = (int64_t)base + n <= CAPQ;  // else only the positions below CAPQ are written
+        int o = base + inc - c;
+        const int g0 = sbase + lane * wpl * 32;
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            uint32_t word = mk[i];
-            const uint32_t inc = (inc16[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
-            const int o = run + (int)inc - __popc(word);
-            const int g0 = sbase + i * 512 + lane * 16;
-            if (fits) {
-                int32_t *dst = outp + o;
-                while (word) {
-                    *dst++ = g0 + __ffs(word) - 1;
-                    word &= word - 1;
-                }
-            } else {
-                for (int oo = o; word; oo++, word &= word - 1)
-                    if (oo < CAPQ) outp[oo] = g0 + __ffs(word) - 1;
+        for (int j = 0; j < 4; j++) {
+            uint32_t word = bw[j];
+            while (word) {
+                if (o < CAPQ) outp[o] = g0 + j * 32 + __ffs(word) - 1;
+                o++;
+                word &= word - 1;
             }
-            run += ctot[i];
         }
+        __syncwarp();
         if (HAM && hbuf && n > 0) {
             // a4, phi=1: h(x) = popcount(b(q') xor b(x)) (Alg. 1 l.19) of this segment's
             // candidates.  4 lanes per candidate, each lane 16-byte loads of its words
@@ -2242,11 +2223,8 @@ static void set_attrs() {
     if (done) return;
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -2371,7 +2349,7 @@ struct Work {
         probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + (probe_cb ? ((2 * K * ix->dh * 4 + 15) & ~15) : 0) +
                      WARPS * (((4 * K * 8) + 3 * K + 2 * ix->dh * 4 + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
-        countw_smem = BS + 16 + (int)((sizeof(CountWSmem) + 15) & ~(size_t)15);
+        countw_smem = (int)countw_fixed_smem(BS);
         countw_ham_smem = ix->Wp * 8 + (Dp + 1) * 4;
         rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NS + 1) * 4;
         ham_smem = ix->Wp * 8 + (Dp + 1) * 4 + (2 * NS + 1) * 4;
@@ -2432,16 +2410,13 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
         else {
             uint16_t *hb = (w.mode == 1 && w.ham_fused) ? w.hbuf : nullptr;  // phi=1: Hamming fused into the count
             const int smem = w.countw_smem + (hb ? w.countw_ham_smem : 0);
-#define CRISP_COUNT_WARP(SW, HM)                                                                               \
-    k_count_warp<SW, HM><<<g, THREADS, smem, s>>>(w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, \
+#define CRISP_COUNT_WARP(HM)                                                                               \
+    k_count_warp<HM><<<g, THREADS, smem, s>>>(w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, \
                                                   w.BPC, NB, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase, w.ncand,      \
                                                   w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp, hb,      \
                                                   w.ghist, w.qperm)
-            const bool sw = 2 * M < 128;
-            if (sw && hb) CRISP_COUNT_WARP(true, true);
-            else if (sw) CRISP_COUNT_WARP(true, false);
-            else if (hb) CRISP_COUNT_WARP(false, true);
-            else CRISP_COUNT_WARP(false, false);
+            if (hb) CRISP_COUNT_WARP(true);
+            else CRISP_COUNT_WARP(false);
 #undef CRISP_COUNT_WARP
         }
         CRISP_LAUNCH();
