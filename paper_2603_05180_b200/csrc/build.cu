@@ -139,14 +139,65 @@ struct StoreCov {
 // Rotation Y = fl32(X . R), the same sequential fp64 order per
 // output as k_gemm_seq (k ascending from +0; padded k contribute fma(0, 0, s) =
 // s exactly), with a larger register tile: 128x64 outputs per CTA, 8x4 per
-// thread, k-tiles of 32 staged as doubles in shared memory (A via float4).
+// thread, k-tiles of 32 staged as doubles in shared memory, double-buffered:
+// the global loads of tile t+1 are in registers while tile t is multiplied.
 // ---------------------------------------------------------------------------
 constexpr int RT_BM = 128, RT_BN = 64, RT_BK = 32;
-__global__ void __launch_bounds__(256) k_rotate_f64(int64_t Mr, int Dp, const float *__restrict__ X, int64_t ldx,
-                                                     const float *__restrict__ R, float *__restrict__ Y, int64_t ldy) {
+constexpr int RT_AV = RT_BM * (RT_BK / 4) / 256;  // float4s of A per thread per tile (4)
+constexpr int RT_BV = RT_BK * RT_BN / 256;        // floats of B per thread per tile (8)
+struct RotTile {
+    float4 a[RT_AV];
+    float b[RT_BV];
+};
+__device__ __forceinline__ void rot_load(RotTile &t, int64_t Mr, int Dp, const float *__restrict__ X, int64_t ldx,
+                                         const float *__restrict__ R, int64_t m0, int n0, int k0, bool vecA, int tid) {
+#pragma unroll
+    for (int u = 0; u < RT_AV; u++) {
+        const int e = tid + u * 256;
+        const int r = e >> 3, kq = (e & 7) * 4;
+        const int64_t m = m0 + r;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m < Mr) {
+            const float *src = X + m * ldx + k0 + kq;
+            if (vecA && k0 + kq + 3 < Dp) v = __ldg((const float4 *)src);
+            else {
+                v.x = k0 + kq < Dp ? src[0] : 0.f;
+                v.y = k0 + kq + 1 < Dp ? src[1] : 0.f;
+                v.z = k0 + kq + 2 < Dp ? src[2] : 0.f;
+                v.w = k0 + kq + 3 < Dp ? src[3] : 0.f;
+            }
+        }
+        t.a[u] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < RT_BV; u++) {
+        const int e = tid + u * 256;
+        const int kk = e >> 6, nn = e & 63;
+        const int k = k0 + kk, n = n0 + nn;
+        t.b[u] = (k < Dp && n < Dp) ? __ldg(R + (int64_t)k * Dp + n) : 0.f;
+    }
+}
+__device__ __forceinline__ void rot_store(const RotTile &t, double *As, double *Bs, int tid) {
+#pragma unroll
+    for (int u = 0; u < RT_AV; u++) {
+        const int e = tid + u * 256;
+        const int r = e >> 3, kq = (e & 7) * 4;
+        As[(kq + 0) * RT_BM + r] = (double)t.a[u].x;
+        As[(kq + 1) * RT_BM + r] = (double)t.a[u].y;
+        As[(kq + 2) * RT_BM + r] = (double)t.a[u].z;
+        As[(kq + 3) * RT_BM + r] = (double)t.a[u].w;
+    }
+#pragma unroll
+    for (int u = 0; u < RT_BV; u++) {
+        const int e = tid + u * 256;
+        Bs[(e >> 6) * RT_BN + (e & 63)] = (double)t.b[u];
+    }
+}
+__global__ void __launch_bounds__(256, 2) k_rotate_f64(int64_t Mr, int Dp, const float *__restrict__ X, int64_t ldx,
+                                                        const float *__restrict__ R, float *__restrict__ Y,
+                                                        int64_t ldy) {
     extern __shared__ __align__(16) double rsm[];
-    double *As = rsm;                  // [RT_BK][RT_BM]
-    double *Bs = rsm + RT_BK * RT_BM;  // [RT_BK][RT_BN]
+    constexpr int TS = RT_BK * RT_BM + RT_BK * RT_BN;  // doubles per stage
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int64_t m0 = (int64_t)blockIdx.y * RT_BM;
     const int n0 = blockIdx.x * RT_BN;
@@ -156,34 +207,15 @@ __global__ void __launch_bounds__(256) k_rotate_f64(int64_t Mr, int Dp, const fl
 #pragma unroll
         for (int j = 0; j < 4; j++) acc[i][j] = 0.0;
     const bool vecA = (ldx & 3) == 0;
+    RotTile t;
+    rot_load(t, Mr, Dp, X, ldx, R, m0, n0, 0, vecA, tid);
+    rot_store(t, rsm, rsm + RT_BK * RT_BM, tid);
+    __syncthreads();
+    int stage = 0;
     for (int k0 = 0; k0 < Dp; k0 += RT_BK) {
-        // A: 128 rows x 32 k, one float4 of 4 consecutive k per (row, quad)
-        for (int e = tid; e < RT_BM * (RT_BK / 4); e += 256) {
-            const int r = e >> 3, kq = (e & 7) * 4;
-            const int64_t m = m0 + r;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (m < Mr) {
-                const float *src = X + m * ldx + k0 + kq;
-                if (vecA && k0 + kq + 3 < Dp) v = *(const float4 *)src;
-                else {
-                    v.x = k0 + kq < Dp ? src[0] : 0.f;
-                    v.y = k0 + kq + 1 < Dp ? src[1] : 0.f;
-                    v.z = k0 + kq + 2 < Dp ? src[2] : 0.f;
-                    v.w = k0 + kq + 3 < Dp ? src[3] : 0.f;
-                }
-            }
-            As[(kq + 0) * RT_BM + r] = (double)v.x;
-            As[(kq + 1) * RT_BM + r] = (double)v.y;
-            As[(kq + 2) * RT_BM + r] = (double)v.z;
-            As[(kq + 3) * RT_BM + r] = (double)v.w;
-        }
-        // B: 32 k x 64 n
-        for (int e = tid; e < RT_BK * RT_BN; e += 256) {
-            const int kk = e >> 6, nn = e & 63;
-            const int k = k0 + kk, n = n0 + nn;
-            Bs[kk * RT_BN + nn] = (k < Dp && n < Dp) ? (double)R[(int64_t)k * Dp + n] : 0.0;
-        }
-        __syncthreads();
+        const bool more = k0 + RT_BK < Dp;
+        if (more) rot_load(t, Mr, Dp, X, ldx, R, m0, n0, k0 + RT_BK, vecA, tid);
+        const double *As = rsm + stage * TS, *Bs = As + RT_BK * RT_BM;
 #pragma unroll 4
         for (int kk = 0; kk < RT_BK; kk++) {
             double a[8], b[4];
@@ -196,7 +228,12 @@ __global__ void __launch_bounds__(256) k_rotate_f64(int64_t Mr, int Dp, const fl
 #pragma unroll
                 for (int j = 0; j < 4; j++) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
         }
+        if (more) {
+            double *An = rsm + (stage ^ 1) * TS;
+            rot_store(t, An, An + RT_BK * RT_BM, tid);  // the other stage: last read before the previous barrier
+        }
         __syncthreads();
+        stage ^= 1;
     }
 #pragma unroll
     for (int i = 0; i < 8; i++)
@@ -212,7 +249,7 @@ void rotate_rows_f64(const float *X, int64_t rows, int32_t Dp, int64_t ldx, cons
                      cudaStream_t s) {
     if (rows <= 0) return;
     static bool attr = false;
-    const int smem = (RT_BK * RT_BM + RT_BK * RT_BN) * 8;
+    const int smem = 2 * (RT_BK * RT_BM + RT_BK * RT_BN) * 8;
     if (!attr) {
         CRISP_CUDA(cudaFuncSetAttribute(k_rotate_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;

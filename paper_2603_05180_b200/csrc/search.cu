@@ -499,7 +499,7 @@ __device__ __forceinline__ uint32_t cw_entry(const uint32_t *__restrict__ actq, 
     return (uint32_t)(m * KK + (int)(v & 0xffffu)) | ((uint32_t)m << 24) | ((v >> 16) == 2u ? WFLAG : 0u);
 }
 
-template <bool HAM>
+template <bool HAM, bool ATOM>
 __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint32_t *__restrict__ act,
                                                            const int32_t *__restrict__ act_len, int M, int KK,
                                                            const int32_t *__restrict__ off2w, int NBW,
@@ -624,16 +624,29 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
                             }
                         }
                     }
+                    if (ATOM) {
+                        // one shared atomic per position on the counter's 32-bit word (bytes
+                        // never carry: V <= 2M <= 254); no ordering between batches needed
 #pragma unroll
-                    for (int u = 0; u < CW_U; u++) {
-                        const uint32_t a = xi[u] ? sm_cnt + (xa[u] - lbase) : sm_dummy;
-                        const uint32_t v = lds_u8(a);
-                        sts_u8(a, v + xi[u]);
-                        if (taum1 - v < xi[u]) {  // v < tau <= v + inc: x enters C
-                            const uint32_t off = xa[u] - (uint32_t)sbase;
-                            atomicOr(wbm + (off >> 5), 1u << (off & 31));
+                        for (int u = 0; u < CW_U; u++)
+                            if (xi[u]) {
+                                const uint32_t off = xa[u] - (uint32_t)sbase, sh = (off & 3) * 8;
+                                const uint32_t v =
+                                    (atomicAdd((uint32_t *)(wc + (off & ~3u)), xi[u] << sh) >> sh) & 0xffu;
+                                if (taum1 - v < xi[u]) atomicOr(wbm + (off >> 5), 1u << (off & 31));
+                            }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < CW_U; u++) {
+                            const uint32_t a = xi[u] ? sm_cnt + (xa[u] - lbase) : sm_dummy;
+                            const uint32_t v = lds_u8(a);
+                            sts_u8(a, v + xi[u]);
+                            if (taum1 - v < xi[u]) {  // v < tau <= v + inc: x enters C
+                                const uint32_t off = xa[u] - (uint32_t)sbase;
+                                atomicOr(wbm + (off >> 5), 1u << (off & 31));
+                            }
+                            __syncwarp();
                         }
-                        __syncwarp();
                     }
                 }
             }
@@ -1960,7 +1973,8 @@ __device__ __forceinline__ void write_topk(int64_t q, int k, int cnt_top, const 
     }
 }
 
-// warp per query; dynamic smem WARPS x k (d, id)
+// warp per query; dynamic smem WARPS x k (d, id) + WARPS x 32 PSCAN_G staged (d, id)
+constexpr int PSCAN_G = 8;
 __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int32_t *__restrict__ totals,
                                                             const int32_t *__restrict__ pool, int64_t PS,
                                                             int64_t gid_base, const double *__restrict__ dbuf, int j0r,
@@ -1986,13 +2000,34 @@ __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int
     const int32_t *ord = pool + q * PS + j0;
     const double *dq = dbuf + q * (int64_t)dstride;
     ad.q = qrot + q * (int64_t)ad.pitch;
+    // PSCAN_G groups of 32 entries staged per warp with all loads in flight, then
+    // replayed group by group from shared memory
+    double *sd = (double *)((int64_t *)((double *)sm + WARPS * k) + WARPS * k) + warp * (32 * PSCAN_G);
+    int64_t *si = (int64_t *)((double *)sm + WARPS * k) + WARPS * k + WARPS * (32 * PSCAN_G) + warp * (32 * PSCAN_G);
     int64_t stop = -1;
-    for (int g0 = 0; g0 < n && stop < 0; g0 += 32) {
-        const int gn = min(32, n - g0);
-        const double myd = lane < gn ? dq[g0 + lane] : INFINITY;
-        const int64_t myi = lane < gn ? gid_base + ord[g0 + lane] : 0x7fffffffffffffffLL;
-        const int s = patience_group(myd, myi, gn, Td, Ti, cnt_top, pat, k, P, lane, &ad);
-        if (s >= 0) stop = (int64_t)j0 + g0 + s + 1;
+    for (int c0 = 0; c0 < n && stop < 0; c0 += 32 * PSCAN_G) {
+        double vd[PSCAN_G];
+        int32_t vi[PSCAN_G];
+#pragma unroll
+        for (int u = 0; u < PSCAN_G; u++) {
+            const int j = c0 + u * 32 + lane;
+            vd[u] = j < n ? dq[j] : INFINITY;
+            vi[u] = j < n ? ord[j] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < PSCAN_G; u++) {
+            sd[u * 32 + lane] = vd[u];
+            si[u * 32 + lane] = gid_base + vi[u];
+        }
+        __syncwarp();
+        for (int g0 = c0; g0 < min(n, c0 + 32 * PSCAN_G) && stop < 0; g0 += 32) {
+            const int gn = min(32, n - g0);
+            const double myd = lane < gn ? sd[g0 - c0 + lane] : INFINITY;
+            const int64_t myi = lane < gn ? si[g0 - c0 + lane] : 0x7fffffffffffffffLL;
+            const int s = patience_group(myd, myi, gn, Td, Ti, cnt_top, pat, k, P, lane, &ad);
+            if (s >= 0) stop = (int64_t)j0 + g0 + s + 1;
+        }
+        __syncwarp();
     }
     const bool fin = stop >= 0 || j0 + n >= total;
     for (int i = lane; i < cnt_top; i += 32) {
@@ -2223,14 +2258,17 @@ static void set_attrs() {
     if (done) return;
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -2249,7 +2287,7 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
-    int S, HS, S0, R0, BPC, count_kernel, NS, ham_fused, rows4, ad, F, vra_smem;
+    int S, HS, S0, R0, BPC, count_kernel, count_atom, NS, ham_fused, rows4, ad, F, vra_smem;
     // end of the speculative rounds (positions the Hamming order must cover)
     int rounds_end() const { return R0 == 0 ? 0 : F + (R0 - 1) * S0; }
     DevBuf buf;
@@ -2296,6 +2334,7 @@ struct Work {
         // (warp-owned sub-blocks, for slices of >= 8 ids per sub-block); env overrides
         count_kernel = env_int("CRISP_COUNT_KERNEL", ix->slice_hint >= 8.0 ? 1 : 0);
         NS = count_kernel == 0 ? NB : ix->NBW;  // candidate segments per query (id blocks or sub-blocks)
+        count_atom = env_int("CRISP_COUNT_ATOM", 0);  // k_count_warp: shared atomics (else byte load/store pairs; faster)
         ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
         // row kernels: four rows per warp step for rows up to 4 KB (measured: faster at D=960, slower at 4096)
         rows4 = env_int("CRISP_ROWS4", pitch <= 1024 ? 1 : 0);
@@ -2356,7 +2395,7 @@ struct Work {
         hsort_smem = (Dp + 1 + 2 * NS + 1) * 4;
         hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
         vr_smem = pitch * 8;
-        scan_smem = WARPS * k * 16;
+        scan_smem = WARPS * k * 16 + WARPS * 32 * PSCAN_G * 16;
         pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + (Dp / 4 + 1) * 8 + (Dp + 1 + 2 * NS + 1) * 4;
         set_attrs();
         CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
@@ -2410,13 +2449,15 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s)
         else {
             uint16_t *hb = (w.mode == 1 && w.ham_fused) ? w.hbuf : nullptr;  // phi=1: Hamming fused into the count
             const int smem = w.countw_smem + (hb ? w.countw_ham_smem : 0);
-#define CRISP_COUNT_WARP(HM)                                                                               \
-    k_count_warp<HM><<<g, THREADS, smem, s>>>(w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, \
+#define CRISP_COUNT_WARP(HM, AT)                                                                               \
+    k_count_warp<HM, AT><<<g, THREADS, smem, s>>>(w.act, w.act_len, M, KK, ix->off2w, ix->NBW, ix->ids, ix->N, ix->BS, \
                                                   w.BPC, NB, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase, w.ncand,      \
                                                   w.need, w.traceV, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp, hb,      \
                                                   w.ghist, w.qperm)
-            if (hb) CRISP_COUNT_WARP(true);
-            else CRISP_COUNT_WARP(false);
+            if (hb && w.count_atom) CRISP_COUNT_WARP(true, true);
+            else if (hb) CRISP_COUNT_WARP(true, false);
+            else if (w.count_atom) CRISP_COUNT_WARP(false, true);
+            else CRISP_COUNT_WARP(false, false);
 #undef CRISP_COUNT_WARP
         }
         CRISP_LAUNCH();

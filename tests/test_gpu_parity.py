@@ -96,12 +96,14 @@ def compare_trace(t, ot, mode, N):
         assert np.array_equal(t["n_verified"], ot["n_verified"]), "a5 patience stop"
 
 
-# collision-count variants: CTA-flattened, warp-owned (+ standalone dense
-# Hamming at phi=1), warp-owned with the Hamming popcounts fused; the row
+# collision-count variants: CTA-flattened, warp-owned with byte load/store
+# pairs (+ standalone dense Hamming at phi=1), warp-owned with shared atomics
+# and the Hamming popcounts fused; the row
 # kernels run two-row steps in the first and one CTA per query in the last
 COUNT_VARIANTS = {"select": {"CRISP_COUNT_KERNEL": "0", "CRISP_ROWS4": "0"},
                   "warp": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "0"},
-                  "warp_fused": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "1", "CRISP_RERANK_SPLITS": "1"}}
+                  "warp_fused": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "1", "CRISP_RERANK_SPLITS": "1",
+                                 "CRISP_COUNT_ATOM": "1"}}
 
 
 @pytest.mark.parametrize("variant", list(COUNT_VARIANTS))
