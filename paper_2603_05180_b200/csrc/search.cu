@@ -32,7 +32,8 @@ constexpr int THREADS = WARPS * 32;
 constexpr int CS_CAP = 1024;          // slice-table entries per round (count kernel)
 constexpr int CS_U = 16;              // ids staged per thread per round
 constexpr int CS_TCAP = THREADS * CS_U;  // positions per round
-constexpr int PATIENCE_CH = 64;       // rows verified per patience chunk
+constexpr int PATIENCE_CH = 128;      // min rows verified per patience chunk (k_patience_tail)
+constexpr int TAIL_CAP = 1024;        // max rows per chunk of k_patience_tail
 
 __device__ __forceinline__ bool less_di(double a, int64_t ia, double b, int64_t ib) {
     return a < b || (a == b && ia < ib);
@@ -1716,22 +1717,37 @@ struct PatState {
     int32_t *pat;     // Qc, consecutive non-improving verifications
     int32_t *done;    // Qc
     int64_t *nver;    // Qc, rows verified when done
+    int32_t *pos;     // Qc, next position of the query's order to verify
+    int32_t *nlen;    // Qc, rows of its next round (certainly needed: P - pat, clamped)
 };
+
+// rows [j0, j0 + n) of query q in a verification round: the round's fixed span
+// (j0r >= 0) or the query's own (j0r < 0: st.pos, st.nlen), inside its order
+// and below the positions k_hsort ordered (send)
+__device__ __forceinline__ int round_span(const PatState &st, int64_t q, int j0r, int len, int total, int send,
+                                          int &j0) {
+    if (j0r < 0) {
+        j0 = st.pos[q];
+        len = st.nlen[q];
+    } else
+        j0 = j0r;
+    return max(0, min(min(len, total - j0), send - j0));
+}
 
 template <bool ROWS4>
 __global__ void __launch_bounds__(THREADS, 5) k_verify_rows(const float *__restrict__ qrot, int pitch,
                                                           const float *__restrict__ X, const int32_t *__restrict__ pool,
                                                           int64_t PS, const int32_t *__restrict__ totals,
-                                                          const int32_t *__restrict__ done, int j0r, int len,
+                                                          PatState st, int j0r, int len, int send,
                                                           int dstride, double *__restrict__ dbuf,
                                                           const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
-    if (done[q]) return;
+    if (st.done[q]) return;
     const int total = totals[q];
-    const int j0 = j0r;
-    const int n = min(len, total - j0);
+    int j0;
+    const int n = round_span(st, q, j0r, len, total, send, j0);
     if (n <= 0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     load_qd(qd, qrot + q * pitch, pitch);
@@ -1898,7 +1914,8 @@ __global__ void __launch_bounds__(THREADS) k_verify_rows_ad(const float *__restr
                                                              const float *__restrict__ X,
                                                              const int32_t *__restrict__ pool, int64_t PS,
                                                              const int32_t *__restrict__ totals, PatState st, int k,
-                                                             int j0r, int len, int dstride, double *__restrict__ dbuf,
+                                                             int j0r, int len, int send, int dstride,
+                                                             double *__restrict__ dbuf,
                                                              const int32_t *__restrict__ qperm, double eps0,
                                                              int stride) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -1907,8 +1924,8 @@ __global__ void __launch_bounds__(THREADS) k_verify_rows_ad(const float *__restr
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;
     if (st.done[q]) return;
     const int total = totals[q];
-    const int j0 = j0r;
-    const int n = min(len, total - j0);
+    int j0;
+    const int n = round_span(st, q, j0r, len, total, send, j0);
     if (n <= 0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool prune = st.cnt[q] >= k;
@@ -1978,7 +1995,8 @@ constexpr int PSCAN_G = 8;
 __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int32_t *__restrict__ totals,
                                                             const int32_t *__restrict__ pool, int64_t PS,
                                                             int64_t gid_base, const double *__restrict__ dbuf, int j0r,
-                                                            int len, int dstride, int k, int P, PatState st,
+                                                            int len, int send, int nl_min, int nl_max, int dstride,
+                                                            int k, int P, PatState st,
                                                             double *__restrict__ out_d64, float *__restrict__ out_d,
                                                             int64_t *__restrict__ out_i, AdCtx ad,
                                                             const float *__restrict__ qrot) {
@@ -1995,8 +2013,8 @@ __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int
     }
     __syncwarp();
     const int total = totals[q];
-    const int j0 = j0r;
-    const int n = max(0, min(len, total - j0));
+    int j0;
+    const int n = round_span(st, q, j0r, len, total, send, j0);
     const int32_t *ord = pool + q * PS + j0;
     const double *dq = dbuf + q * (int64_t)dstride;
     ad.q = qrot + q * (int64_t)ad.pitch;
@@ -2040,17 +2058,25 @@ __global__ void __launch_bounds__(THREADS) k_patience_scan(int64_t Qc, const int
         if (fin) {
             st.done[q] = 1;
             st.nver[q] = stop >= 0 ? stop : total;
+        } else {
+            // still running: at least P - pat more rows are verified (no improvement
+            // can stop it earlier), the span of its next round
+            st.pos[q] = j0 + n;
+            st.nlen[q] = P > 0 ? min(nl_max, max(nl_min, P - pat)) : nl_max;
         }
     }
     if (fin) write_topk(q, k, cnt_top, Td, Ti, out_d64, out_d, out_i, lane, 32);
 }
 
 // CTA per query still running after the speculative rounds: chunked
-// sequential verification from position `from`.
-__global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restrict__ qrot, int pitch,
+// verification from position `from` (all warps compute the chunk's rows, warp
+// 0 replays them in order).  k_hsort ordered the positions below sorted_end;
+// a query that reaches sorted_end first completes its order.
+__global__ void __launch_bounds__(THREADS, 4) k_patience_tail(const float *__restrict__ qrot, int pitch,
                                                             const float *__restrict__ X, int64_t gid_base,
                                                             int32_t *__restrict__ order, int64_t PS,
-                                                            const int32_t *__restrict__ totals, int from, int k, int P,
+                                                            const int32_t *__restrict__ totals,
+                                                            int sorted_end, int rows4, int k, int P,
                                                             PatState st, double *__restrict__ out_d64,
                                                             float *__restrict__ out_d, int64_t *__restrict__ out_i,
                                                             int Dp, const int32_t *__restrict__ ghist,
@@ -2063,24 +2089,17 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
     const int64_t q = qperm ? qperm[blockIdx.x] : blockIdx.x;  // locality order (query_order)
     if (st.done[q]) return;
     double *qd = (double *)sm;                       // pitch
-    double *chd = qd + pitch;                        // PATIENCE_CH
-    int64_t *chi = (int64_t *)(chd + PATIENCE_CH);   // PATIENCE_CH
-    double *Td = (double *)(chi + PATIENCE_CH);      // k
+    double *chd = qd + pitch;                        // TAIL_CAP
+    int64_t *chi = (int64_t *)(chd + TAIL_CAP);      // TAIL_CAP
+    double *Td = (double *)(chi + TAIL_CAP);         // k
     int64_t *Ti = (int64_t *)(Td + k);               // k
     double *thr = (double *)(Ti + k);                // Dp / 4 + 1 (ADSampling thresholds of a chunk)
     int *hstart = (int *)(thr + Dp / 4 + 1);         // Dp + 1
     int *spre = hstart + Dp + 1;                     // NS + 1
     int *scbs = spre + NS + 1;                       // NS
-    __shared__ int s_stop, s_cnt;
+    __shared__ int s_stop, s_cnt, s_pat;
     __shared__ int64_t s_nver;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // k_hsort ordered only the positions the rounds read: complete the order
-    if (warp == 0) {
-        warp_segments(ncand, cbase, q, NS, spre, scbs);
-        hsort_warp(ghist + q * (int64_t)(Dp + 1), Dp, pool + q * PS, hbuf + q * PS, spre, scbs, order + q * PS,
-                   hstart, 0x7fffffff);
-    }
-    __syncthreads();
     load_qd(qd, qrot + q * pitch, pitch);
     int cnt_top = st.cnt[q], pat = st.pat[q];
     for (int i = tid; i < cnt_top; i += THREADS) {
@@ -2090,6 +2109,7 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
     if (tid == 0) {
         s_stop = 0;
         s_cnt = cnt_top;
+        s_pat = pat;
     }
     __syncthreads();
     const int total = totals[q];
@@ -2097,8 +2117,20 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
     const int nvec = pitch / 4;
     int64_t nver = total;
     ad.q = qrot + q * (int64_t)pitch;
-    for (int pos = from; pos < total; pos += PATIENCE_CH) {
-        const int n = min(PATIENCE_CH, total - pos);
+    bool sorted = false;
+    // chunk: the rows certainly verified next (P - pat: no improvement can stop the
+    // query earlier), at least PATIENCE_CH; ADSampling chunks of PATIENCE_CH
+    for (int pos = st.pos[q], n = 0; pos < total; pos += n) {
+        n = min(total - pos, ad.on || P == 0 ? PATIENCE_CH : max(PATIENCE_CH, min(TAIL_CAP, P - s_pat)));
+        if (!sorted && pos + n > sorted_end) {  // k_hsort ordered only [0, sorted_end): complete the order
+            if (warp == 0) {
+                warp_segments(ncand, cbase, q, NS, spre, scbs);
+                hsort_warp(ghist + q * (int64_t)(Dp + 1), Dp, pool + q * PS, hbuf + q * PS, spre, scbs,
+                           order + q * PS, hstart, 0x7fffffff);
+            }
+            __syncthreads();
+            sorted = true;
+        }
         if (ad.on) {
             // ADSampling: rows of the chunk with the certified early stop under the
             // r_k at the chunk's start (see ad_row), then the in-order scan
@@ -2113,6 +2145,30 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
                 if (lane == 0) {
                     chd[i] = d0;
                     chi[i] = gid_base + l0;
+                }
+            }
+        } else if (rows4) {
+            // four consecutive rows per warp step
+            for (int i = warp * 4; i < n; i += WARPS * 4) {
+                if (i + 3 < n) {
+                    const int l0 = ord[pos + i], l1 = ord[pos + i + 1], l2 = ord[pos + i + 2], l3 = ord[pos + i + 3];
+                    double d4[4];
+                    row_dist4(X + (int64_t)l0 * pitch, X + (int64_t)l1 * pitch, X + (int64_t)l2 * pitch,
+                              X + (int64_t)l3 * pitch, qd, nvec, lane, d4);
+                    if (lane < 4) {
+                        const int li = lane == 0 ? l0 : lane == 1 ? l1 : lane == 2 ? l2 : l3;
+                        chd[i + lane] = d4[lane];
+                        chi[i + lane] = gid_base + li;
+                    }
+                } else {
+                    for (int ii = i; ii < n; ii++) {
+                        const int l0 = ord[pos + ii];
+                        const double d0 = row_dist1(X + (int64_t)l0 * pitch, qd, nvec, lane);
+                        if (lane == 0) {
+                            chd[ii] = d0;
+                            chi[ii] = gid_base + l0;
+                        }
+                    }
                 }
             }
         } else
@@ -2148,6 +2204,7 @@ __global__ void __launch_bounds__(THREADS) k_patience_tail(const float *__restri
             }
             if (lane == 0) {
                 s_cnt = cnt_top;
+                s_pat = pat;
                 if (stop >= 0) {
                     s_stop = 1;
                     s_nver = stop;
@@ -2252,6 +2309,10 @@ static int env_int(const char *name, int dflt) {
     const char *v = getenv(name);
     return v ? atoi(v) : dflt;
 }
+static double env_double(const char *name, double dflt) {
+    const char *v = getenv(name);
+    return v ? atof(v) : dflt;
+}
 
 static void set_attrs() {
     static bool done = false;
@@ -2287,9 +2348,15 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
-    int S, HS, S0, R0, BPC, count_kernel, count_atom, NS, ham_fused, rows4, ad, F, vra_smem;
+    int S, S1, HS, S0, R0, BPC, count_kernel, count_atom, NS, ham_fused, rows4, ad, F, DS, round_rows, nl_min, Pq,
+        vra_smem;
     // end of the speculative rounds (positions the Hamming order must cover)
-    int rounds_end() const { return R0 == 0 ? 0 : F + (R0 - 1) * S0; }
+    // positions k_hsort orders (the rounds stop there; k_patience_tail completes the
+    // order of a query that goes further): ADSampling's fixed rounds + 1024, exact:
+    // F + 2 max(P, 512) + 1024 (measured: nver <= 3.7 P at cfg2, k = 10)
+    int order_end() const {
+        return ad ? (R0 == 0 ? 0 : F + (R0 - 1) * S0) + 1024 : F + 2 * std::max(Pq, 512) + 1024;
+    }
     DevBuf buf;
     float *qpad = nullptr, *qrot = nullptr;
     uint32_t *act = nullptr;
@@ -2309,10 +2376,25 @@ struct Work {
     bool full_order = false;  // trace: order every candidate (not only what the rounds read)
     int probe_gs, probe_cb, probe_qpw, probe_smem, count_smem, countw_smem, countw_ham_smem, rx_smem, ham_smem, hsort_smem, hsort_cta_smem, vr_smem, scan_smem, pat_smem;
 
+    // round 0 of exact verification: f P rows rounded up to 64 (every query
+    // verifies at least min(P, |C|) rows; measured nver / P: ~1.7 at cfg2, k = 10,
+    // ~1.2 at cfg4, k = 100)
+    static int64_t patience_rows(const crisp_index *ix, int k) {
+        return ix->patience_factor > 0 ? (int64_t)ix->patience_factor * k : 0;
+    }
+    static int first_round(const crisp_index *ix, int k) {
+        const int64_t P = patience_rows(ix, k);
+        const double f = env_double("CRISP_PATIENCE_FIRST_F", 1.0);
+        const int64_t r = P > 0 ? std::min<int64_t>(1 << 16, std::max<int64_t>(128, ((int64_t)(f * P) + 63) / 64 * 64))
+                                : 1024;
+        return std::max(32, env_int("CRISP_PATIENCE_FIRST", (int)r));
+    }
     static int64_t per_query_bytes(const crisp_index *ix, int k, int mode, int64_t CAPQ, bool traceV) {
         const int KK = ix->K * ix->K;
         const int S = std::max(1, env_int("CRISP_RERANK_SPLITS", 4));
-        const int S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));
+        // >= the dbuf row stride DS of Work()
+        const int S0 = std::max({first_round(ix, k), std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024)),
+                                 (int)std::min<int64_t>(1 << 16, std::max<int64_t>(patience_rows(ix, k), 1024))});
         int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 4 + (int64_t)ix->M * 12 + CAPQ * 4 +
                        (int64_t)ix->NBW * 8 + 64;
         if (mode == 0) perq += (int64_t)S * k * 16;
@@ -2327,8 +2409,15 @@ struct Work {
         const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, BS = ix->BS, pitch = ix->pitch, Dp = ix->Dp;
         S = std::max(1, env_int("CRISP_RERANK_SPLITS", 4));       // CTAs per query in the row kernels
         HS = std::max(1, env_int("CRISP_HAMMING_SPLITS", 2));     // CTAs per query in k_hamming(_dense)
-        S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // speculative rows per round
-        R0 = std::max(0, env_int("CRISP_PATIENCE_ROUNDS", 2));  // speculative rounds (then the sequential tail)
+        ad = (mode == 1 && ix->ad_on) ? 1 : 0;
+        // speculative rounds (then k_patience_tail): round 0 = F rows, then S0 rows per
+        // round for the queries still running (exact: F about 1.75 P, short rounds after;
+        // ADSampling: an exact round 0 establishes r_k, later rounds prune under it)
+        Pq = (int)std::min<int64_t>(1 << 24, patience_rows(ix, k));
+        S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // ADSampling: rows per round >= 1
+        R0 = std::max(0, std::min(16, env_int("CRISP_PATIENCE_ROUNDS", ad ? 2 : 4)));
+        S1 = std::max(1, env_int("CRISP_ROUND_SPLITS", 2));       // CTAs per query, exact rounds >= 1
+        nl_min = std::max(32, env_int("CRISP_ROUND_MIN", 128));  // min span of an exact round >= 1
         BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 16)));  // id blocks per count CTA
         // 0: k_count_select (CTA-flattened slices, for many small cells), 1: k_count_warp
         // (warp-owned sub-blocks, for slices of >= 8 ids per sub-block); env overrides
@@ -2338,10 +2427,9 @@ struct Work {
         ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
         // row kernels: four rows per warp step for rows up to 4 KB (measured: faster at D=960, slower at 4096)
         rows4 = env_int("CRISP_ROWS4", pitch <= 1024 ? 1 : 0);
-        // ADSampling (Optimized Mode): a short first round establishes r_k, later
-        // rounds prune under it
-        ad = (mode == 1 && ix->ad_on) ? 1 : 0;
-        F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : S0;
+        F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : first_round(ix, k);
+        DS = std::max({F, S0, std::min(std::max(Pq, nl_min), 1 << 16)});  // dbuf row stride (max span of a round)
+        round_rows = std::max(1, env_int("CRISP_ROUND_ROWS", 128));  // min rows per CTA in round 0
         vra_smem = pitch * 8 + (Dp / 4 + 1) * 8;
         qpad = buf.alloc<float>((size_t)Qc * pitch);
         qrot = ix->rotated ? buf.alloc<float>((size_t)Qc * pitch) : qpad;
@@ -2371,12 +2459,14 @@ struct Work {
             hbuf = buf.alloc<uint16_t>((size_t)Qc * CAPQ);
             ghist = buf.alloc<int32_t>((size_t)Qc * (Dp + 1));
             totals = buf.alloc<int32_t>((size_t)Qc);
-            dbuf = buf.alloc<double>((size_t)Qc * S0);
+            dbuf = buf.alloc<double>((size_t)Qc * DS);
             pst.Td = buf.alloc<double>((size_t)Qc * k);
             pst.Ti = buf.alloc<int64_t>((size_t)Qc * k);
-            pst.cnt = buf.alloc<int32_t>((size_t)Qc * 3);
+            pst.cnt = buf.alloc<int32_t>((size_t)Qc * 5);
             pst.pat = pst.cnt + Qc;
             pst.done = pst.pat + Qc;
+            pst.pos = pst.done + Qc;
+            pst.nlen = pst.pos + Qc;
             pst.nver = buf.alloc<int64_t>((size_t)Qc);
             nver = pst.nver;
         }
@@ -2396,7 +2486,7 @@ struct Work {
         hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
         vr_smem = pitch * 8;
         scan_smem = WARPS * k * 16 + WARPS * 32 * PSCAN_G * 16;
-        pat_smem = pitch * 8 + PATIENCE_CH * 16 + k * 16 + (Dp / 4 + 1) * 8 + (Dp + 1 + 2 * NS + 1) * 4;
+        pat_smem = pitch * 8 + TAIL_CAP * 16 + k * 16 + (Dp / 4 + 1) * 8 + (Dp + 1 + 2 * NS + 1) * 4;
         set_attrs();
         CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
                         pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
@@ -2509,7 +2599,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         return;
     }
     const int P = ix->patience_factor > 0 ? ix->patience_factor * k : 0;
-    CRISP_CUDA(cudaMemsetAsync(w.pst.cnt, 0, (size_t)w.Qc * 3 * 4, s));
+    CRISP_CUDA(cudaMemsetAsync(w.pst.cnt, 0, (size_t)w.Qc * 5 * 4, s));
     {
         // h of the queries whose candidate set the fallback replaced (k_hamming),
         // then of all others over their dense pool positions (k_hamming_dense),
@@ -2534,39 +2624,45 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         if (w.hsort_cta_smem <= 200 * 1024)
             k_hsort_cta<<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
                 w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals,
-                w.full_order ? 0x7fffffff : w.rounds_end());
+                w.full_order ? 0x7fffffff : w.order_end());
         else
             k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ,
-                                                           w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.rounds_end());
+                                                           w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.order_end());
         CRISP_LAUNCH();
         g_launches++;
     }
     StageScope st(s, 4);
-    // speculative rounds: round 0 = positions [0, F), round r >= 1 = [F + (r-1) S0, F + r S0)
+    // verification rounds.  Round 0: positions [0, F) of every query.  Exact
+    // verification, rounds >= 1: each running query its own span [pos, pos + nlen)
+    // (the rows it certainly verifies next, set by the scan).  ADSampling: fixed
+    // spans [F + (r-1) S0, F + r S0), pruned under the r_k of the round's start.
     AdCtx ad{w.ad, ix->ad_eps0, ix->ad_stride, Dp, ix->X, pitch, ix->gid_base, nullptr};
+    const int send = w.full_order ? 0x7fffffff : w.order_end();
     for (int r = 0; r < w.R0; r++) {
-        const int j0 = r == 0 ? 0 : w.F + (r - 1) * w.S0, len = r == 0 ? w.F : w.S0;
-        dim3 g(w.S, (unsigned)qn);
+        const bool own = r > 0 && !w.ad;
+        const int j0 = own ? -1 : (r == 0 ? 0 : w.F + (r - 1) * w.S0), len = r == 0 ? w.F : w.S0;
+        // CTAs per query: at most S, at least round_rows rows each (the query staging is per CTA)
+        dim3 g(own ? w.S1 : std::max(1, std::min(w.S, len / w.round_rows)), (unsigned)qn);
         if (w.ad && r > 0)  // round 0 starts with an empty top-k: nothing to prune
             k_verify_rows_ad<<<g, THREADS, w.vra_smem, s>>>(w.qrot, pitch, Dp, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst,
-                                                            k, j0, len, w.S0, w.dbuf, w.qperm, ix->ad_eps0,
+                                                            k, j0, len, send, w.DS, w.dbuf, w.qperm, ix->ad_eps0,
                                                             ix->ad_stride);
         else if (w.rows4)
-            k_verify_rows<true><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst.done,
-                                                              j0, len, w.S0, w.dbuf, w.qperm);
+            k_verify_rows<true><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst,
+                                                              j0, len, send, w.DS, w.dbuf, w.qperm);
         else
             k_verify_rows<false><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals,
-                                                               w.pst.done, j0, len, w.S0, w.dbuf, w.qperm);
+                                                               w.pst, j0, len, send, w.DS, w.dbuf, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
         k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.cbuf, w.CAPQ, ix->gid_base,
-                                                                      w.dbuf, j0, len, w.S0, k, P, w.pst, od64, od, oi,
-                                                                      ad, w.qrot);
+                                                                      w.dbuf, j0, len, send, w.nl_min, w.DS, w.DS, k,
+                                                                      P, w.pst, od64, od, oi, ad, w.qrot);
         CRISP_LAUNCH();
         g_launches++;
     }
     k_patience_tail<<<(unsigned)qn, THREADS, w.pat_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.cbuf, w.CAPQ,
-                                                              w.totals, w.rounds_end(), k, P, w.pst, od64, od, oi, Dp,
+                                                              w.totals, send, w.rows4, k, P, w.pst, od64, od, oi, Dp,
                                                               w.ghist, w.pool, w.hbuf, w.ncand, w.cbase, NB, w.qperm,
                                                               ad);
     CRISP_LAUNCH();
