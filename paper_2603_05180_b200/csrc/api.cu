@@ -376,17 +376,16 @@ static crisp_status search_impl(const crisp_index *ix, const float *queries, int
             sg.v.push_back(p);
             return p;
         };
-        const float *qd = queries;
-        if (!is_device_ptr(queries)) {
-            float *t = (float *)stage((size_t)Q * ix->D * 4);
-            CRISP_CUDA(cudaMemcpyAsync(t, queries, (size_t)Q * ix->D * 4, cudaMemcpyHostToDevice, st));
-            qd = t;
+        const float *qd = queries, *qh = nullptr;
+        if (!is_device_ptr(queries)) {  // staged: the search copies it in parts, overlapped with a0
+            qd = (const float *)stage((size_t)Q * ix->D * 4);
+            qh = queries;
         }
         bool ids_dev = is_device_ptr(out_ids), d_dev = out_d ? is_device_ptr(out_d) : true;
         int64_t *oi = ids_dev ? out_ids : (int64_t *)stage((size_t)Q * k * 8);
         float *od = (out_d && !d_dev) ? (float *)stage((size_t)Q * k * 4) : out_d;
         SearchOut so{oi, od, out_d64};
-        search(ix, qd, Q, k, (int)mode, so, st, tr);
+        search(ix, qd, Q, k, (int)mode, so, st, tr, qh);
         if (!ids_dev) CRISP_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)Q * k * 8, cudaMemcpyDeviceToHost, st));
         if (out_d && !d_dev) CRISP_CUDA(cudaMemcpyAsync(out_d, od, (size_t)Q * k * 4, cudaMemcpyDeviceToHost, st));
         CRISP_CUDA(cudaStreamSynchronize(st));

@@ -109,8 +109,10 @@ struct SearchOut {
     double *d64;       // Q x k fp64 (device) or null
 };
 struct TraceDev;  // device-side trace buffers (search.cu)
+// queries_host: when not null, queries_dev is an uninitialised device staging
+// buffer that the search fills from it (H2D overlapped with the query transform)
 void search(const crisp_index *ix, const float *queries_dev, int64_t Q, int32_t k, int mode, SearchOut out,
-            cudaStream_t s, const crisp_trace_t *host_trace);
+            cudaStream_t s, const crisp_trace_t *host_trace, const float *queries_host = nullptr);
 void merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32_t k, double *out_d64, float *out_d,
                 int64_t *out_ids, cudaStream_t s);
 crisp_session *session_begin(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode,

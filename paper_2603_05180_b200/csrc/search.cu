@@ -2495,17 +2495,44 @@ struct Work {
 };
 
 // a0, a1+a2, a3+a4 (count/select) for queries [0, qn) of the chunk
-static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s) {
+static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s, const float *hq = nullptr) {
     const crisp_index *ix = w.ix;
     const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, pitch = ix->pitch;
     {
         StageScope st(s, 0);
-        k_prep_queries<<<nblk(qn * pitch, 256), 256, 0, s>>>(queries, qn, ix->D, pitch, w.qpad);
-        CRISP_LAUNCH();
-        g_launches++;
-        if (ix->rotated) {
-            rotate_rows_f64(w.qpad, qn, ix->Dp, pitch, ix->R, w.qrot, pitch, s);
+        // a0 in parts; with host queries (hq: the source of the device staging
+        // `queries`) part p's H2D copy runs on a side stream while part p-1 is
+        // padded and rotated
+        const int P = (hq && qn >= 2048) ? 4 : 1;
+        cudaStream_t cs = nullptr;
+        cudaEvent_t ev[5] = {};
+        if (hq) {
+            CRISP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            for (auto &e : ev) CRISP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CRISP_CUDA(cudaEventRecord(ev[4], s));  // the staging buffer is allocated on s
+            CRISP_CUDA(cudaStreamWaitEvent(cs, ev[4], 0));
+            for (int p = 0; p < P; p++) {
+                const int64_t r0 = qn * p / P, r1 = qn * (p + 1) / P;
+                CRISP_CUDA(cudaMemcpyAsync((void *)(queries + r0 * ix->D), hq + r0 * ix->D,
+                                           (size_t)(r1 - r0) * ix->D * 4, cudaMemcpyHostToDevice, cs));
+                CRISP_CUDA(cudaEventRecord(ev[p], cs));
+            }
+        }
+        for (int p = 0; p < P; p++) {
+            const int64_t r0 = qn * p / P, r1 = qn * (p + 1) / P;
+            if (hq) CRISP_CUDA(cudaStreamWaitEvent(s, ev[p], 0));
+            k_prep_queries<<<nblk((r1 - r0) * pitch, 256), 256, 0, s>>>(queries + r0 * ix->D, r1 - r0, ix->D, pitch,
+                                                                        w.qpad + r0 * pitch);
+            CRISP_LAUNCH();
             g_launches++;
+            if (ix->rotated) {
+                rotate_rows_f64(w.qpad + r0 * pitch, r1 - r0, ix->Dp, pitch, ix->R, w.qrot + r0 * pitch, pitch, s);
+                g_launches++;
+            }
+        }
+        if (hq) {
+            for (auto &e : ev) CRISP_CUDA(cudaEventDestroy(e));
+            CRISP_CUDA(cudaStreamDestroy(cs));
         }
     }
     {
@@ -2765,7 +2792,7 @@ static int64_t grow_capacity(const crisp_index *ix, int64_t cap, int64_t need) {
 // One attempt over all queries with candidate capacity CAPQ per query; returns
 // false (and the capacity needed) if some query's candidate set overflowed.
 static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
-                        cudaStream_t s, const crisp_trace_t *tr, int64_t CAPQ, int64_t *need_out) {
+                        cudaStream_t s, const crisp_trace_t *tr, int64_t CAPQ, int64_t *need_out, const float *hq) {
     const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : (16LL << 30);
     const int64_t perq = Work::per_query_bytes(ix, k, mode, CAPQ, tr && tr->V);
     int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
@@ -2774,7 +2801,7 @@ static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, 
     w.full_order = tr != nullptr;
     for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
         const int64_t qn = std::min(Qc, Q - q0);
-        run_front(w, queries + q0 * ix->D, qn, s);
+        run_front(w, queries + q0 * ix->D, qn, s, hq ? hq + q0 * ix->D : nullptr);
         run_fallback_local(w, qn, s);
         const int32_t need = read_need(w, s);  // exactness guard
         if (need > CAPQ) {
@@ -2791,13 +2818,13 @@ static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, 
 }
 
 void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
-            cudaStream_t s, const crisp_trace_t *tr) {
+            cudaStream_t s, const crisp_trace_t *tr, const float *queries_host) {
     // candidate capacity per query: optimistic, grown (and the batch redone)
     // if any query's |C_q| exceeds it, so results never depend on it
     int64_t cap = initial_capacity(ix, tr != nullptr);
     for (;;) {
         int64_t need = 0;
-        if (search_pass(ix, queries, Q, k, mode, out, s, tr, cap, &need)) return;
+        if (search_pass(ix, queries, Q, k, mode, out, s, tr, cap, &need, queries_host)) return;
         cap = grow_capacity(ix, cap, need);
     }
 }

@@ -278,21 +278,45 @@ def test_gpu_rotation_properties(crisp):
     assert auto.info()["rotated"] == (ox["cev"] > 0.85) == 1
 
 
-@pytest.mark.parametrize("batch,rounds", [(64, 1), (64, 0), (128, 3)])
-def test_patience_rounds_and_tail(crisp, monkeypatch, batch, rounds):
-    """Optimized mode through every verification path: speculative rounds of
-    `batch` rows, then the sequential tail kernel; results and the patience stop
-    index must equal the oracle's sequential rule."""
-    monkeypatch.setenv("CRISP_PATIENCE_BATCH", str(batch))
+@pytest.mark.parametrize("first,rounds,rmin", [(64, 1, 128), (64, 0, 128), (128, 3, 32), (256, 16, 64)])
+def test_patience_rounds_and_tail(crisp, monkeypatch, first, rounds, rmin):
+    """Optimized mode through every verification path: round 0 of `first` rows,
+    `rounds` - 1 rounds of per-query spans (>= rmin rows), then the tail kernel;
+    results and the patience stop index must equal the oracle's sequential rule
+    (P:L458).  The untraced search (Hamming order cut at the rounds' reach, the
+    tail completing it for queries that go further) gives the same answer."""
+    monkeypatch.setenv("CRISP_PATIENCE_FIRST", str(first))
     monkeypatch.setenv("CRISP_PATIENCE_ROUNDS", str(rounds))
+    monkeypatch.setenv("CRISP_ROUND_MIN", str(rmin))
     X, Qv, ox = make_case(cfg=1, N=12000, D=128, Q=24, M=4, K=9, seed=7)
     ix = build_gpu(crisp, X, ox, block_ids=4096)
-    for pf, B in ((1, 900), (3, 2500), (0, 700)):
+    for pf, B in ((1, 900), (3, 2500), (0, 700), (60, 3000)):
         ix.set_search_params(budget=B, tau=1, patience_factor=pf)
         ids, d, t = ix.trace(Qv, 5, 1)
         r_ids, r_d, ot = oracle.search(ox, Qv, 5, 1, B, 1, patience_factor=pf, trace=True)
         compare_trace(t, ot, 1, X.shape[0])
-        assert_topk_parity(ids, d, r_ids, r_d, f"patience batch={batch} rounds={rounds} pf={pf}")
+        assert_topk_parity(ids, d, r_ids, r_d, f"patience first={first} rounds={rounds} pf={pf}")
+        ids2, d2 = ix.search(Qv, 5, 1)
+        assert np.array_equal(ids2, ids) and np.array_equal(d2, d), f"untraced pf={pf}"
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_host_buffers_match_device(crisp, mode):
+    """crisp_search with host buffers (the H2D copy overlapped with the query
+    transform in 4 parts) returns what the device-pointer call returns."""
+    import torch
+
+    X, _, ox = make_case(cfg=1, N=20000, Q=10, seed=3)
+    Qv = synth.Workload(1).queries(3000).numpy()
+    ix = build_gpu(crisp, X, ox)
+    ix.set_search_params(budget=oracle.budget_ids(0.01, 20000), tau=3, patience_factor=40)
+    h_ids, h_d = ix.search(Qv, 10, mode)
+    Qd = torch.from_numpy(Qv).cuda()
+    ids = torch.empty((3000, 10), dtype=torch.int64, device="cuda")
+    dd = torch.empty((3000, 10), dtype=torch.float32, device="cuda")
+    ix.search_async(Qd, 10, mode, ids, dd, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_ids, ids.cpu().numpy()) and np.array_equal(h_d, dd.cpu().numpy())
 
 
 @pytest.mark.parametrize("mode", [0, 1])
