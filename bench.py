@@ -333,8 +333,8 @@ def run_crisp(args):
         kernels = {}
         if st["verify"] > 0:
             vb = cnt["verified"] * row_bytes / K  # 4D per verified row (SURVEY 8(d) B_rerank)
-            kernels["verify"] = {"kernel": ["k_rerank_exact", "k_verify_rows+k_patience_scan",
-                                            "k_verify_rows_ad+k_patience_scan"][mode],
+            kernels["verify"] = {"kernel": ["k_rerank_exact", "k_verify_rows+k_patience_scan+k_patience_tail",
+                                            "k_verify_rows(_ad)+k_patience_scan+k_patience_tail"][mode],
                                  "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
                                  "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
         if st["count_select"] > 0:
