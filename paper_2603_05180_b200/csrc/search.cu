@@ -1376,7 +1376,7 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
 // bases come from a cursor starting at 0), so a CTA takes a contiguous range
 // of positions: 4 lanes per candidate with 16-byte code loads, h written at
 // the position, a CTA histogram flushed to the query's histogram.
-__global__ void __launch_bounds__(THREADS) k_hamming_dense(const float *__restrict__ qrot, int pitch, int Dp,
+__global__ void __launch_bounds__(THREADS, 4) k_hamming_dense(const float *__restrict__ qrot, int pitch, int Dp,
                                                             const uint64_t *__restrict__ codes, int Wd,
                                                             const int32_t *__restrict__ pool, int64_t CAPQ,
                                                             const int32_t *__restrict__ cursor,
@@ -1402,6 +1402,13 @@ __global__ void __launch_bounds__(THREADS) k_hamming_dense(const float *__restri
     const int lo = blockIdx.x * per, hi = min(total, lo + per);
     const int32_t *poolq = pool + q * CAPQ;
     const int g4 = lane >> 2, gl = lane & 3, nt = Wd >> 3;
+    // the ids of the next pass are loaded before this pass's code rows
+    int idn[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const int v = lo + warp * 32 + r * 8 + g4;
+        idn[r] = v < hi ? __ldg(poolq + v) : 0;
+    }
     for (int v0 = lo + warp * 32; v0 < hi; v0 += WARPS * 32) {
         int id[4];
         bool okv[4];
@@ -1409,7 +1416,9 @@ __global__ void __launch_bounds__(THREADS) k_hamming_dense(const float *__restri
         for (int r = 0; r < 4; r++) {
             const int v = v0 + r * 8 + g4;
             okv[r] = v < hi;
-            id[r] = okv[r] ? __ldg(poolq + v) : 0;
+            id[r] = idn[r];
+            const int vn = v + WARPS * 32;
+            idn[r] = vn < hi ? __ldg(poolq + vn) : 0;
         }
         int hr[4] = {0, 0, 0, 0};
 #pragma unroll 2
