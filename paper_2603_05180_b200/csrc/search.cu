@@ -698,13 +698,27 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
         base = __shfl_sync(0xffffffffu, base, 0);
         int o = base + inc - c;
         const int g0 = sbase + lane * wpl * 32;
+        if ((int64_t)base + n <= CAPQ) {
+            // the segment fits (the usual case): two 64-bit words per lane, no bound check
+            int32_t *dst = outp + o;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            uint32_t word = bw[j];
-            while (word) {
-                if (o < CAPQ) outp[o] = g0 + j * 32 + __ffs(word) - 1;
-                o++;
-                word &= word - 1;
+            for (int j = 0; j < 2; j++) {
+                uint64_t word = (uint64_t)bw[2 * j] | ((uint64_t)bw[2 * j + 1] << 32);
+                const int gj = g0 + j * 64 - 1;
+                while (word) {
+                    *dst++ = gj + __ffsll((long long)word);
+                    word &= word - 1;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                uint32_t word = bw[j];
+                while (word) {
+                    if (o < CAPQ) outp[o] = g0 + j * 32 + __ffs(word) - 1;
+                    o++;
+                    word &= word - 1;
+                }
             }
         }
         __syncwarp();
