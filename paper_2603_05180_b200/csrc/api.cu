@@ -72,6 +72,10 @@ static void free_index(crisp_index *ix) {
     cudaSetDevice(ix->device);
     cudaFree(ix->X);
     cudaFree(ix->R);
+    cudaFree(ix->Rsl);
+    cudaFree(ix->Rexp);
+    cudaFree(ix->Rn2);
+    cudaFree(ix->Rt);
     cudaFree(ix->cb);
     cudaFree(ix->cells);
     cudaFree(ix->ids);

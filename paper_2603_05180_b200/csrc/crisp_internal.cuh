@@ -64,6 +64,10 @@ struct crisp_index {
     double cev = 0.0;
     float *X = nullptr;        // N x pitch, stored (rotated) vectors, zero padded
     float *R = nullptr;        // Dp x Dp row-major (rotated only)
+    int8_t *Rsl = nullptr;     // Dp x 7 Dpk: int8 slices of R's columns, descending (rotate_imma.cu)
+    int32_t *Rexp = nullptr;   // Dp: column scale exponents of the slices
+    double *Rn2 = nullptr;     // Dp: column 2-norms (x 1.01)
+    float *Rt = nullptr;       // Dp x Dp: R transposed (the certified rotation's exact recompute)
     float *cb = nullptr;       // M x 2 x K x dh
     int32_t *cells = nullptr;  // M x N
     int32_t *ids = nullptr;    // M x N CSR ids
@@ -99,6 +103,11 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
 void finish_csr(crisp_index *ix, cudaStream_t s);
 
 // fp64 sequential-order GEMM: Y(rows x Dp, pitch ldy) = fl32(X(rows x Dp, pitch ldx) . R(Dp x Dp))
+// a0 on the int8 tensor cores, certified (rotate_imma.cu)
+void prepare_rotation_slices(crisp_index *ix, cudaStream_t s);
+bool rotate_imma_enabled();
+void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64_t ldx, float *Y, int64_t ldy,
+                      cudaStream_t s, unsigned long long *nfall);
 void rotate_rows_f64(const float *X, int64_t rows, int32_t Dp, int64_t ldx, const float *R, float *Y, int64_t ldy,
                      cudaStream_t s);
 

@@ -2549,8 +2549,14 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
             CRISP_LAUNCH();
             g_launches++;
             if (ix->rotated) {
-                rotate_rows_f64(w.qpad + r0 * pitch, r1 - r0, ix->Dp, pitch, ix->R, w.qrot + r0 * pitch, pitch, s);
-                g_launches++;
+                if (rotate_imma_enabled()) {  // int8 tensor cores, certified (rotate_imma.cu)
+                    if (!ix->Rsl) prepare_rotation_slices(const_cast<crisp_index *>(ix), s);
+                    rotate_rows_imma(ix, w.qpad + r0 * pitch, r1 - r0, pitch, w.qrot + r0 * pitch, pitch, s, nullptr);
+                    g_launches += 3;  // slices, certify, recompute (+ 7 cuBLASLt GEMMs)
+                } else {
+                    rotate_rows_f64(w.qpad + r0 * pitch, r1 - r0, ix->Dp, pitch, ix->R, w.qrot + r0 * pitch, pitch, s);
+                    g_launches++;
+                }
             }
         }
         if (hq) {
