@@ -278,6 +278,39 @@ def test_gpu_rotation_properties(crisp):
     assert auto.info()["rotated"] == (ox["cev"] > 0.85) == 1
 
 
+def test_certified_rotation_adversarial(crisp):
+    """a0 on the int8 tensor cores with the certified rounding (rotate_imma.cu):
+    q' must equal the oracle's sequential fp64 chain bit for bit on rows chosen
+    to stress the certificate: zeros, a single non-zero, 60 orders of magnitude
+    inside one row, subnormal inputs, power-of-two scalings, alternating signs,
+    exact cancellations, and a D that is not a multiple of 16 (padding)."""
+    rng = np.random.default_rng(11)
+    D, M = 203, 4
+    Dp = oracle.padded_dim(D, M)
+    X = rng.standard_normal((2500, D)).astype(np.float32)
+    R, _ = oracle.rotation(Dp, 9)
+    ix = crisp.Index.build(X, M, R=R, codebooks=oracle.train_codebooks(oracle.rotate_rows(
+        np.pad(X, ((0, 0), (0, Dp - D))), R), M, 6, 2, 2500, 3), K=6, seed=3)
+    rows = []
+    rows.append(np.zeros(D))
+    e = np.zeros(D); e[17] = 3.0; rows.append(e)
+    rows.append(np.where(np.arange(D) % 2 == 0, 1e15, 1e-15) * rng.standard_normal(D))
+    rows.append(np.full(D, 1e-40))                       # subnormal fp32 inputs
+    rows.append(rng.standard_normal(D) * 1e-38)
+    rows.append(np.where(np.arange(D) % 2 == 0, 1.0, -1.0))
+    c = rng.standard_normal(D); c[1::2] = -c[0::2][: D // 2]; rows.append(c)
+    for k in range(-20, 21, 4):
+        rows.append(rng.standard_normal(D) * 2.0 ** k)
+    rows.append(np.abs(rng.standard_normal(D)) * 100 + 1000)  # large common mean (Gist-like)
+    Q = np.vstack(rows + [rng.standard_normal(D) * rng.uniform(0.1, 10) for _ in range(300)]).astype(np.float32)
+    ix.set_search_params(budget=200, tau=1, patience_factor=5)
+    _, _, t = ix.trace(Q, 3, 1)
+    ref = oracle.rotate_rows(np.pad(Q, ((0, 0), (0, Dp - D))), R)
+    got = t["qrot"][:, :Dp]
+    bad = np.nonzero(~np.all(got.view(np.uint32) == ref.view(np.uint32), axis=1))[0]
+    assert bad.size == 0, f"rows {bad[:10]} differ"
+
+
 @pytest.mark.parametrize("first,rounds,rmin", [(64, 1, 128), (64, 0, 128), (128, 3, 32), (256, 16, 64)])
 def test_patience_rounds_and_tail(crisp, monkeypatch, first, rounds, rmin):
     """Optimized mode through every verification path: round 0 of `first` rows,
