@@ -64,7 +64,10 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int32_t *gs = (int32_t *)sm;
     float *cbs = (float *)(sm + (smem_gsize ? ((KK * 4 + 15) & ~15) : 0));  // this subspace's 2 x K x dh (smem_cb)
-    unsigned char *wbase = (unsigned char *)cbs + (smem_cb ? ((2 * K * dh * 4 + 15) & ~15) : 0);
+    // staged codebook rows at an odd stride: the lanes of a warp (one centroid each)
+    // read distinct banks in dist64
+    const int cst = smem_cb ? (dh | 1) : dh;
+    unsigned char *wbase = (unsigned char *)cbs + (smem_cb ? ((2 * K * cst * 4 + 15) & ~15) : 0);
     const int per_warp = ((4 * K * 8) + 3 * K + 2 * dh * 4 + 15) & ~15;
     double *tmp = (double *)(wbase + warp * per_warp);  // 2K
     double *a = tmp + 2 * K, *b = a + K;
@@ -75,7 +78,7 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     if (smem_gsize)
         for (int i = threadIdx.x; i < KK; i += THREADS) gs[i] = gsm[i];
     if (smem_cb)
-        for (int i = threadIdx.x; i < 2 * K * dh; i += THREADS) cbs[i] = cbm[i];
+        for (int i = threadIdx.x; i < 2 * K * dh; i += THREADS) cbs[(i / dh) * cst + i % dh] = cbm[i];
     __syncthreads();
     if (smem_gsize) gsm = gs;
     if (smem_cb) cbm = cbs;
@@ -88,8 +91,8 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     __syncwarp();
     // half distances (Alg. 1 l.4): dist64, exactly the oracle's order
     for (int side = 0; side < 2; side++) {
-        const float *C = cbm + (int64_t)side * K * dh;
-        for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64(qs + side * dh, C + (int64_t)c * dh, dh);
+        const float *C = cbm + (int64_t)side * K * cst;
+        for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64(qs + side * dh, C + (int64_t)c * cst, dh);
     }
     __syncwarp();
     // sort each half by (delta, c) via ranks
@@ -2496,9 +2499,9 @@ struct Work {
         if (want_traceV) traceV = buf.alloc<uint8_t>((size_t)Qc * ix->N);
         if (want_d64tmp) d64tmp = buf.alloc<double>((size_t)Qc * k);
         probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
-        probe_cb = (2 * K * ix->dh * 4 <= 96 * 1024) ? 1 : 0;
+        probe_cb = (2 * K * (ix->dh | 1) * 4 <= 96 * 1024) ? 1 : 0;  // rows padded to an odd stride
         probe_qpw = std::max(1, env_int("CRISP_PROBE_QPW", 4));  // queries per warp in k_probe
-        probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + (probe_cb ? ((2 * K * ix->dh * 4 + 15) & ~15) : 0) +
+        probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + (probe_cb ? ((2 * K * (ix->dh | 1) * 4 + 15) & ~15) : 0) +
                      WARPS * (((4 * K * 8) + 3 * K + 2 * ix->dh * 4 + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
         countw_smem = (int)countw_fixed_smem(BS);
