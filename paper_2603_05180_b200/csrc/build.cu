@@ -457,33 +457,69 @@ __global__ void k_kpp_d2(const float *S, int64_t n, int Dp, int dh, int K, int n
     double d = dist64(S + p * Dp + (int64_t)h * dh, C + ((int64_t)h * K + c) * dh, dh);
     if (c == 0 || d < D2[e]) D2[e] = d;
 }
-__global__ void k_kpp_pick(const float *S, int64_t n, int Dp, int dh, int K, int nh, uint64_t seed, int c,
-                           const double *D2, float *C) {
-    int h = blockIdx.x * blockDim.x + threadIdx.x;
-    if (h >= nh) return;
+// k-means++ pick: the sequential fp64 sums of the oracle (total,
+// then the running sum up to the first position above u * total), one CTA per
+// half-subspace: the CTA stages D2 through shared memory in chunks, one thread
+// keeps the sums in the oracle's order (the loads are no longer on its chain)
+constexpr int KPP_CH = 2048;  // doubles per staged chunk
+__global__ void __launch_bounds__(256) k_kpp_pick(const float *S, int64_t n, int Dp, int dh, int K, int nh,
+                                                  uint64_t seed, int c, const double *D2, float *C) {
+    __shared__ double buf[2][KPP_CH];
+    __shared__ int64_t s_pick;
+    __shared__ int s_stop;
+    const int h = blockIdx.x;
     const double *d = D2 + (int64_t)h * n;
-    double tot = 0.0;
-    for (int64_t p = 0; p < n; p++) tot = __dadd_rn(tot, d[p]);
-    double uc = uniform(seed, STREAM_KM_INIT, (uint64_t)c, (uint32_t)h);
-    int64_t pick;
-    if (tot > 0.0) {
-        double target = uc * tot, cum = 0.0;
-        pick = -1;
-        int64_t lastpos = 0;
-        for (int64_t p = 0; p < n; p++) {
-            if (d[p] > 0.0) lastpos = p;
-            cum = __dadd_rn(cum, d[p]);
-            if (cum > target) {
-                pick = p;
-                break;
+    const int tid = threadIdx.x;
+    // pass 1: total; pass 2: the running sum against the target
+    double tot = 0.0, target = 0.0, cum = 0.0;
+    int64_t lastpos = 0, pick = -1;
+    const double uc = uniform(seed, STREAM_KM_INIT, (uint64_t)c, (uint32_t)h);
+    for (int pass = 0; pass < 2; pass++) {
+        if (pass == 1) {
+            if (tid == 0) s_stop = !(tot > 0.0);
+            __syncthreads();
+            if (s_stop) break;
+            target = uc * tot;
+        }
+        int b = 0;
+        for (int64_t p0 = 0; p0 < n; p0 += KPP_CH, b ^= 1) {
+            // the other threads load chunk i+1 while thread 0 sums chunk i (one barrier
+            // per chunk: chunk i+2 reuses chunk i's buffer only after thread 0 passed it)
+            const int cn = (int)(n - p0 < KPP_CH ? n - p0 : KPP_CH);
+            for (int i = tid; i < cn; i += blockDim.x) buf[b][i] = d[p0 + i];
+            __syncthreads();
+            if (pass == 1 && s_stop) break;
+            if (tid == 0) {
+                const double *x = buf[b];
+                if (pass == 0) {
+                    for (int i = 0; i < cn; i++) tot = __dadd_rn(tot, x[i]);
+                } else if (pick < 0) {
+                    for (int i = 0; i < cn; i++) {
+                        if (x[i] > 0.0) lastpos = p0 + i;
+                        cum = __dadd_rn(cum, x[i]);
+                        if (cum > target) {
+                            pick = p0 + i;
+                            break;
+                        }
+                    }
+                    s_stop = pick >= 0;
+                }
             }
         }
-        if (pick < 0) pick = lastpos;
-    } else {
-        pick = (int64_t)(uc * (double)n);
-        if (pick >= n) pick = n - 1;
+        __syncthreads();
     }
-    for (int t = 0; t < dh; t++) C[((int64_t)h * K + c) * dh + t] = S[pick * Dp + (int64_t)h * dh + t];
+    if (tid == 0) {
+        if (tot > 0.0) {
+            if (pick < 0) pick = lastpos;
+        } else {
+            pick = (int64_t)(uc * (double)n);
+            if (pick >= n) pick = n - 1;
+        }
+        s_pick = pick;
+    }
+    __syncthreads();
+    const int64_t pk = s_pick;
+    for (int t = tid; t < dh; t += blockDim.x) C[((int64_t)h * K + c) * dh + t] = S[pk * Dp + (int64_t)h * dh + t];
 }
 __device__ __forceinline__ int argmin_centroid(const float *x, const float *C, int K, int dh, double *dmin) {
     int best = 0;
@@ -598,7 +634,7 @@ static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, u
     k_kpp_d2<<<nblk(n * nh, 256), 256, 0, s>>>(S, n, Dp, dh, K, nh, C, 0, D2);
     CRISP_LAUNCH();
     for (int c = 1; c < K; c++) {
-        k_kpp_pick<<<nblk(nh, 32), 32, 0, s>>>(S, n, Dp, dh, K, nh, seed, c, D2, C);
+        k_kpp_pick<<<nh, 256, 0, s>>>(S, n, Dp, dh, K, nh, seed, c, D2, C);
         CRISP_LAUNCH();
         k_kpp_d2<<<nblk(n * nh, 256), 256, 0, s>>>(S, n, Dp, dh, K, nh, C, c, D2);
         CRISP_LAUNCH();
