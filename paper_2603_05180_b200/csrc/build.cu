@@ -521,27 +521,78 @@ __global__ void __launch_bounds__(256) k_kpp_pick(const float *S, int64_t n, int
     const int64_t pk = s_pick;
     for (int t = tid; t < dh; t += blockDim.x) C[((int64_t)h * K + c) * dh + t] = S[pk * Dp + (int64_t)h * dh + t];
 }
-__device__ __forceinline__ int argmin_centroid(const float *x, const float *C, int K, int dh, double *dmin) {
+// argmin over the K centroids of one half-subspace h for 128 points per CTA
+// (Alg. "assign" S:L220): the centroids staged as doubles and the
+// points' h-th half staged transposed (Xs[d][pt], pitch 129: conflict-free), so
+// a thread reads its point and every lane the same centroid (broadcast).  Two
+// centroids per pass share the point's conversion; each distance is dist64's
+// sequential chain and ties keep the first centroid.
+constexpr int AS_T = 128;
+__global__ void __launch_bounds__(AS_T) k_argmin_staged(const float *__restrict__ P, int64_t n, int64_t ldp, int dh,
+                                                        int K, const float *__restrict__ C,
+                                                        const int *__restrict__ done, int32_t *__restrict__ a,
+                                                        double *__restrict__ dmin) {
+    extern __shared__ __align__(16) double ssm[];
+    const int h = blockIdx.y;
+    if (done && done[h]) return;
+    double *Cs = ssm;                    // K x dh
+    float *Xs = (float *)(Cs + K * dh);  // dh x (AS_T + 1)
+    const int tid = threadIdx.x;
+    const int64_t p0 = (int64_t)blockIdx.x * AS_T;
+    const float *Ch = C + (int64_t)h * K * dh;
+    for (int i = tid; i < K * dh; i += AS_T) Cs[i] = (double)Ch[i];
+    const int np = (int)(n - p0 < AS_T ? n - p0 : AS_T);
+    for (int i = tid; i < np * dh; i += AS_T) {
+        const int pt = i / dh, d = i - pt * dh;
+        Xs[d * (AS_T + 1) + pt] = P[(p0 + pt) * ldp + (int64_t)h * dh + d];
+    }
+    __syncthreads();
+    if (tid >= np) return;
+    double bd = 0.0;
     int best = 0;
-    double bd = dist64(x, C, dh);
-    for (int c = 1; c < K; c++) {
-        double d = dist64(x, C + (int64_t)c * dh, dh);
-        if (d < bd) {
-            bd = d;
+    for (int c = 0; c < K; c += 2) {
+        const double *c0 = Cs + c * dh, *c1 = c0 + dh;
+        const bool two = c + 1 < K;
+        double s0 = 0.0, s1 = 0.0;
+        for (int d = 0; d < dh; d++) {
+            const double xd = (double)Xs[d * (AS_T + 1) + tid];
+            const double t0 = __dsub_rn(xd, c0[d]);
+            s0 = __fma_rn(t0, t0, s0);
+            if (two) {
+                const double t1 = __dsub_rn(xd, c1[d]);
+                s1 = __fma_rn(t1, t1, s1);
+            }
+        }
+        if (c == 0 || s0 < bd) {
+            bd = s0;
             best = c;
         }
+        if (two && s1 < bd) {
+            bd = s1;
+            best = c + 1;
+        }
     }
-    if (dmin) *dmin = bd;
-    return best;
+    a[(int64_t)h * n + p0 + tid] = best;
+    if (dmin) dmin[(int64_t)h * n + p0 + tid] = bd;
 }
-__global__ void k_km_assign(const float *S, int64_t n, int Dp, int dh, int K, int nh, const float *C,
-                            const int *done, int32_t *a, double *dmin) {
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= n * nh) return;
-    int h = (int)(e / n);
-    if (done[h]) return;
-    int64_t p = e % n;
-    a[e] = argmin_centroid(S + p * Dp + (int64_t)h * dh, C + (int64_t)h * K * dh, K, dh, &dmin[e]);
+__global__ void k_cells_from_halves(const int32_t *__restrict__ ah, int64_t N, int M, int K, int32_t *__restrict__ cells) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // e = m*N + p
+    if (e >= N * M) return;
+    const int64_t m = e / N, p = e - m * N;
+    cells[e] = ah[(2 * m) * N + p] * K + ah[(2 * m + 1) * N + p];
+}
+static int argmin_smem(int K, int dh) { return K * dh * 8 + dh * (AS_T + 1) * 4; }
+static void argmin_staged(const float *P, int64_t n, int64_t ldp, int dh, int K, int nh, const float *C,
+                          const int *done, int32_t *a, double *dmin, cudaStream_t s) {
+    const int sm = argmin_smem(K, dh);
+    static int attr = 0;
+    if (sm > attr) {
+        CRISP_CUDA(cudaFuncSetAttribute(k_argmin_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        attr = sm;
+    }
+    dim3 g((unsigned)((n + AS_T - 1) / AS_T), (unsigned)nh);
+    k_argmin_staged<<<g, AS_T, sm, s>>>(P, n, ldp, dh, K, C, done, a, dmin);
+    CRISP_LAUNCH();
 }
 __global__ void k_km_compare(int64_t n, int nh, const int32_t *a, const int32_t *aold, const int *done, int *diff) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -646,8 +697,7 @@ static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, u
     unsigned char *taken = sc.alloc<unsigned char>((size_t)n * nh);
     CRISP_CUDA(cudaMemsetAsync(done, 0, nh * 4, s));
     for (int it = 0; it < iters; it++) {
-        k_km_assign<<<nblk(n * nh, 128), 128, 0, s>>>(S, n, Dp, dh, K, nh, C, done, a, dmin);
-        CRISP_LAUNCH();
+        argmin_staged(S, n, Dp, dh, K, nh, C, done, a, dmin, s);
         CRISP_CUDA(cudaMemsetAsync(diff, 0, nh * 4, s));
         if (it > 0) {
             k_km_compare<<<nblk(n * nh, 256), 256, 0, s>>>(n, nh, a, aold, done, diff);
@@ -668,17 +718,6 @@ static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, u
 // ---------------------------------------------------------------------------
 // cell assignment, CSR, codes
 // ---------------------------------------------------------------------------
-__global__ void k_assign(const float *X, int64_t N, int64_t pitch, int M, int K, int dh, const float *cb,
-                         int32_t *cells) {
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // e = m*N + p
-    if (e >= N * M) return;
-    int m = (int)(e / N);
-    int64_t p = e % N;
-    const float *x = X + p * pitch + (int64_t)m * 2 * dh;
-    int i = argmin_centroid(x, cb + (int64_t)(m * 2 + 0) * K * dh, K, dh, nullptr);
-    int j = argmin_centroid(x + dh, cb + (int64_t)(m * 2 + 1) * K * dh, K, dh, nullptr);
-    cells[e] = i * K + j;
-}
 __global__ void k_iota(int32_t *v, int64_t n) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = (int32_t)i;
@@ -816,7 +855,14 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
     } else {
         train_codebooks(ix, kmeans_sample, kmeans_iters, seed, s);
     }
-    k_assign<<<nblk(N * ix->M, 128), 128, 0, s>>>(ix->X, N, ix->pitch, ix->M, ix->K, ix->dh, ix->cb, ix->cells);
+    {
+        int32_t *ah = nullptr;  // per half-subspace argmin, then cells = i K + j
+        CRISP_CUDA(cudaMallocAsync(&ah, (size_t)N * 2 * ix->M * 4, s));
+        argmin_staged(ix->X, N, ix->pitch, ix->dh, ix->K, 2 * ix->M, ix->cb, nullptr, ah, nullptr, s);
+        k_cells_from_halves<<<nblk(N * ix->M, 256), 256, 0, s>>>(ah, N, ix->M, ix->K, ix->cells);
+        CRISP_LAUNCH();
+        CRISP_CUDA(cudaFreeAsync(ah, s));
+    }
     CRISP_LAUNCH();
     finish_csr(ix, s);
     k_codes<<<nblk(N * (int64_t)ix->Wp * 64, 256), 256, 0, s>>>(ix->X, N, ix->pitch, ix->Dp, ix->Wp,
