@@ -276,7 +276,7 @@ const Plan &plan_for(int Dp, int Dpk, int64_t rows) {
 int rotation_slices_k(int Dp) { return (Dp + 15) / 16 * 16; }
 
 void prepare_rotation_slices(crisp_index *ix, cudaStream_t s) {
-    if (!ix->rotated || ix->Rsl) return;
+    if (!ix->R || ix->Rsl) return;
     const int Dp = ix->Dp, Dpk = rotation_slices_k(Dp);
     int8_t *tmp = nullptr;
     CRISP_CUDA(cudaMalloc(&ix->Rsl, (size_t)Dp * SL * Dpk));
