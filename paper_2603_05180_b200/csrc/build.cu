@@ -498,14 +498,27 @@ __global__ void __launch_bounds__(256) k_kpp_pick(const float *S, int64_t n, int
             if (tid == 0) {
                 const double *x = buf[b];
                 if (pass == 0) {
-                    for (int i = 0; i < cn; i++) tot = __dadd_rn(tot, x[i]);
+                    int i = 0;
+                    for (; i + 8 <= cn; i += 8) {  // eight loads ahead of the adds
+                        double v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; u++) v[u] = x[i + u];
+#pragma unroll
+                        for (int u = 0; u < 8; u++) tot = __dadd_rn(tot, v[u]);
+                    }
+                    for (; i < cn; i++) tot = __dadd_rn(tot, x[i]);
                 } else if (pick < 0) {
-                    for (int i = 0; i < cn; i++) {
-                        if (x[i] > 0.0) lastpos = p0 + i;
-                        cum = __dadd_rn(cum, x[i]);
-                        if (cum > target) {
-                            pick = p0 + i;
-                            break;
+                    for (int i0 = 0; i0 < cn && pick < 0; i0 += 8) {
+                        double v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; u++) v[u] = i0 + u < cn ? x[i0 + u] : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 8; u++) {
+                            if (i0 + u < cn && pick < 0) {
+                                if (v[u] > 0.0) lastpos = p0 + i0 + u;
+                                cum = __dadd_rn(cum, v[u]);
+                                if (cum > target) pick = p0 + i0 + u;
+                            }
                         }
                     }
                     s_stop = pick >= 0;
@@ -613,22 +626,48 @@ __global__ void k_km_converge(int nh, int it, const int *diff, int *done, int *a
     active[h] = !done[h];
 }
 // thread per (h, c, t): mean over members in ascending point order
-__global__ void k_km_update(const float *S, int64_t n, int Dp, int dh, int K, int nh, const int32_t *a,
-                            const int *active, float *C, int64_t *cnt) {
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= (int64_t)nh * K * dh) return;
-    int t = (int)(e % dh);
-    int c = (int)((e / dh) % K);
-    int h = (int)(e / ((int64_t)dh * K));
-    if (!active[h]) return;
-    const int32_t *ah = a + (int64_t)h * n;
-    double sum = 0.0;
-    int64_t k = 0;
-    for (int64_t p = 0; p < n; p++) {
-        if (ah[p] != c) continue;
-        k++;
-        sum = __dadd_rn(sum, (double)S[p * Dp + (int64_t)h * dh + t]);
+// k-means update: the members of each (h, c) listed in ascending point
+// order (a stable radix sort of (h K + a, p)): a thread per (h, c, t) sums only
+// its members in ascending p (the oracle's order)
+__global__ void k_km_keys(int64_t n, int nh, int K, const int32_t *a, int32_t *key, int32_t *val) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * nh) return;
+    const int h = (int)(e / n);
+    key[e] = h * K + a[e];
+    val[e] = (int32_t)(e - (int64_t)h * n);
+}
+__global__ void k_km_bins(const int32_t *skey, int64_t tot, int nb, int64_t *off) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;  // lower bound of bin b, b <= nb
+    if (b > nb) return;
+    int64_t lo = 0, hi = tot;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (skey[mid] < b) lo = mid + 1;
+        else hi = mid;
     }
+    off[b] = lo;
+}
+__global__ void k_km_update_sorted(const float *S, int Dp, int dh, int K, int nh, const int32_t *pts,
+                                   const int64_t *off, const int *active, float *C, int64_t *cnt) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)nh * K * dh) return;
+    const int t = (int)(e % dh);
+    const int c = (int)((e / dh) % K);
+    const int h = (int)(e / ((int64_t)dh * K));
+    if (!active[h]) return;
+    const int64_t j0 = off[(int64_t)h * K + c], j1 = off[(int64_t)h * K + c + 1];
+    const float *col = S + (int64_t)h * dh + t;
+    double sum = 0.0;
+    int64_t j = j0;
+    for (; j + 8 <= j1; j += 8) {  // eight loads ahead of their adds
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = col[(int64_t)pts[j + u] * Dp];
+#pragma unroll
+        for (int u = 0; u < 8; u++) sum = __dadd_rn(sum, (double)v[u]);
+    }
+    for (; j < j1; j++) sum = __dadd_rn(sum, (double)col[(int64_t)pts[j] * Dp]);
+    const int64_t k = j1 - j0;
     if (k > 0) C[((int64_t)h * K + c) * dh + t] = (float)(sum / (double)k);
     if (t == 0) cnt[(int64_t)h * K + c] = k;
 }
@@ -702,6 +741,16 @@ static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, u
     int64_t *cnt = sc.alloc<int64_t>((size_t)nh * K);
     unsigned char *taken = sc.alloc<unsigned char>((size_t)n * nh);
     CRISP_CUDA(cudaMemsetAsync(done, 0, nh * 4, s));
+    // member lists for the update: keys h K + a, values p, stably sorted
+    const int64_t tot = n * nh;
+    int32_t *key = sc.alloc<int32_t>(tot), *val = sc.alloc<int32_t>(tot), *skey = sc.alloc<int32_t>(tot),
+            *sval = sc.alloc<int32_t>(tot);
+    int64_t *boff = sc.alloc<int64_t>((size_t)nh * K + 1);
+    int kbits = 1;
+    while ((1LL << kbits) < (long long)nh * K) kbits++;
+    size_t stb = 0;
+    CRISP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, stb, key, skey, val, sval, (int)tot, 0, kbits, s));
+    void *stmp = sc.get(stb);
     for (int it = 0; it < iters; it++) {
         argmin_staged(S, n, Dp, dh, K, nh, C, done, a, dmin, s);
         CRISP_CUDA(cudaMemsetAsync(diff, 0, nh * 4, s));
@@ -711,7 +760,13 @@ static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, u
         }
         k_km_converge<<<nblk(nh, 64), 64, 0, s>>>(nh, it, diff, done, active);
         CRISP_LAUNCH();
-        k_km_update<<<nblk((int64_t)nh * K * dh, 128), 128, 0, s>>>(S, n, Dp, dh, K, nh, a, active, C, cnt);
+        k_km_keys<<<nblk(tot, 256), 256, 0, s>>>(n, nh, K, a, key, val);
+        CRISP_LAUNCH();
+        CRISP_CUDA(cub::DeviceRadixSort::SortPairs(stmp, stb, key, skey, val, sval, (int)tot, 0, kbits, s));
+        k_km_bins<<<nblk((int64_t)nh * K + 1, 256), 256, 0, s>>>(skey, tot, nh * K, boff);
+        CRISP_LAUNCH();
+        k_km_update_sorted<<<nblk((int64_t)nh * K * dh, 128), 128, 0, s>>>(S, Dp, dh, K, nh, sval, boff, active, C,
+                                                                            cnt);
         CRISP_LAUNCH();
         k_km_reseed<<<nblk(nh, 32), 32, 0, s>>>(S, n, Dp, dh, K, nh, active, cnt, dmin, taken, C);
         CRISP_LAUNCH();
