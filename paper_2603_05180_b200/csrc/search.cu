@@ -2374,14 +2374,14 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
-    int S, S1, HS, S0, R0, BPC, count_kernel, count_atom, NS, ham_fused, rows4, ad, F, DS, round_rows, nl_min, Pq,
+    int S, S1, HS, S0, R0, BPC, count_kernel, count_atom, NS, ham_fused, rows4, ad, adsp, F, DS, round_rows, nl_min, Pq,
         vra_smem;
     // end of the speculative rounds (positions the Hamming order must cover)
     // positions k_hsort orders (the rounds stop there; k_patience_tail completes the
     // order of a query that goes further): ADSampling's fixed rounds + 1024, exact:
     // F + 2 max(P, 512) + 1024 (measured: nver <= 3.7 P at cfg2, k = 10)
     int order_end() const {
-        return ad ? (R0 == 0 ? 0 : F + (R0 - 1) * S0) + 1024 : F + 2 * std::max(Pq, 512) + 1024;
+        return ad && !adsp ? (R0 == 0 ? 0 : F + (R0 - 1) * S0) + 1024 : F + 2 * std::max(Pq, 512) + 1024;
     }
     DevBuf buf;
     float *qpad = nullptr, *qrot = nullptr;
@@ -2441,7 +2441,9 @@ struct Work {
         // ADSampling: an exact round 0 establishes r_k, later rounds prune under it)
         Pq = (int)std::min<int64_t>(1 << 24, patience_rows(ix, k));
         S0 = std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024));  // ADSampling: rows per round >= 1
-        R0 = std::max(0, std::min(16, env_int("CRISP_PATIENCE_ROUNDS", ad ? 2 : 4)));
+        // ADSampling on the exact schedule's per-query spans (else fixed S0-row rounds)
+        adsp = ad ? env_int("CRISP_AD_SPANS", 1) : 0;
+        R0 = std::max(0, std::min(16, env_int("CRISP_PATIENCE_ROUNDS", ad && !adsp ? 2 : 4)));
         S1 = std::max(1, env_int("CRISP_ROUND_SPLITS", 2));       // CTAs per query, exact rounds >= 1
         nl_min = std::max(32, env_int("CRISP_ROUND_MIN", 128));  // min span of an exact round >= 1
         BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 16)));  // id blocks per count CTA
@@ -2453,7 +2455,7 @@ struct Work {
         ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
         // row kernels: four rows per warp step for rows up to 4 KB (measured: faster at D=960, slower at 4096)
         rows4 = env_int("CRISP_ROWS4", pitch <= 1024 ? 1 : 0);
-        F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : first_round(ix, k);
+        F = ad && !adsp ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : first_round(ix, k);
         DS = std::max({F, S0, std::min(std::max(Pq, nl_min), 1 << 16)});  // dbuf row stride (max span of a round)
         round_rows = std::max(1, env_int("CRISP_ROUND_ROWS", 128));  // min rows per CTA in round 0
         vra_smem = pitch * 8 + (Dp / 4 + 1) * 8;
@@ -2698,7 +2700,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     AdCtx ad{w.ad, ix->ad_eps0, ix->ad_stride, Dp, ix->X, pitch, ix->gid_base, nullptr};
     const int send = w.full_order ? 0x7fffffff : w.order_end();
     for (int r = 0; r < w.R0; r++) {
-        const bool own = r > 0 && !w.ad;
+        const bool own = r > 0 && (!w.ad || w.adsp);
         const int j0 = own ? -1 : (r == 0 ? 0 : w.F + (r - 1) * w.S0), len = r == 0 ? w.F : w.S0;
         // CTAs per query: at most S, at least round_rows rows each (the query staging is per CTA)
         dim3 g(own ? w.S1 : std::max(1, std::min(w.S, len / w.round_rows)), (unsigned)qn);
