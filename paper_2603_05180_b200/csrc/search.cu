@@ -53,7 +53,7 @@ __global__ void k_prep_queries(const float *__restrict__ q, int64_t Qc, int D, i
 // ---------------------------------------------------------------------------
 // a1 + a2: one warp per (query, subspace)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qrot, int pitch, int64_t Qc,
+__global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qrot, int pitch, int64_t q0, int64_t Qc,
                                                     const float *__restrict__ cb, int M, int K, int dh,
                                                     const int32_t *__restrict__ gsize, int smem_gsize, int64_t budget,
                                                     int wk, uint32_t *__restrict__ act, int32_t *__restrict__ act_len,
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     if (smem_cb) cbm = cbs;
     // each warp takes qpw queries in turn (the codebooks and sizes staged once per CTA)
     for (int qi = 0; qi < qpw; qi++) {
-    const int64_t q = ((int64_t)blockIdx.x * WARPS + warp) * qpw + qi;
+    const int64_t q = q0 + ((int64_t)blockIdx.x * WARPS + warp) * qpw + qi;  // queries [q0, Qc)
     if (q >= Qc) return;
     const float *qm = qrot + q * pitch + (int64_t)m * 2 * dh;
     for (int i = lane; i < 2 * dh; i += 32) qs[i] = qm[i];
@@ -2526,19 +2526,27 @@ struct Work {
 static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s, const float *hq = nullptr) {
     const crisp_index *ix = w.ix;
     const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, pitch = ix->pitch;
+    // a0 (and a1+a2) in parts; with host queries (hq: the source of the device
+    // staging `queries`) part p's H2D copy runs on a side stream while part p-1 is
+    // padded, rotated and probed
+    const int P = (hq && qn >= 2048) ? std::max(1, std::min(16, env_int("CRISP_H2D_PARTS", 2))) : 1;
+    auto probe = [&](int64_t r0, int64_t r1) {
+        dim3 g(nblk(r1 - r0, WARPS * w.probe_qpw), M);
+        k_probe<<<g, THREADS, w.probe_smem, s>>>(w.qrot, pitch, r0, r1, ix->cb, M, K, ix->dh, ix->gsize, w.probe_gs,
+                                                 ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr,
+                                                 w.probe_qpw, w.probe_cb);
+        CRISP_LAUNCH();
+        g_launches++;
+    };
     {
         StageScope st(s, 0);
-        // a0 in parts; with host queries (hq: the source of the device staging
-        // `queries`) part p's H2D copy runs on a side stream while part p-1 is
-        // padded and rotated
-        const int P = (hq && qn >= 2048) ? 4 : 1;
         cudaStream_t cs = nullptr;
-        cudaEvent_t ev[5] = {};
+        cudaEvent_t ev[17] = {};
         if (hq) {
             CRISP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
             for (auto &e : ev) CRISP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            CRISP_CUDA(cudaEventRecord(ev[4], s));  // the staging buffer is allocated on s
-            CRISP_CUDA(cudaStreamWaitEvent(cs, ev[4], 0));
+            CRISP_CUDA(cudaEventRecord(ev[16], s));  // the staging buffer is allocated on s
+            CRISP_CUDA(cudaStreamWaitEvent(cs, ev[16], 0));
             for (int p = 0; p < P; p++) {
                 const int64_t r0 = qn * p / P, r1 = qn * (p + 1) / P;
                 CRISP_CUDA(cudaMemcpyAsync((void *)(queries + r0 * ix->D), hq + r0 * ix->D,
@@ -2563,6 +2571,7 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
                     g_launches++;
                 }
             }
+            if (P > 1) probe(r0, r1);
         }
         if (hq) {
             for (auto &e : ev) CRISP_CUDA(cudaEventDestroy(e));
@@ -2571,12 +2580,7 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
     }
     {
         StageScope st(s, 1);
-        dim3 g(nblk(qn, WARPS * w.probe_qpw), M);
-        k_probe<<<g, THREADS, w.probe_smem, s>>>(w.qrot, pitch, qn, ix->cb, M, K, ix->dh, ix->gsize, w.probe_gs,
-                                                 ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr,
-                                                 w.probe_qpw, w.probe_cb);
-        CRISP_LAUNCH();
-        g_launches++;
+        if (P == 1) probe(0, qn);
         if (w.qperm) {
             k_query_key<<<nblk(qn, 256), 256, 0, s>>>(w.act, M, KK, qn, w.qkey, w.qiota);
             CRISP_LAUNCH();

@@ -336,7 +336,8 @@ def test_patience_rounds_and_tail(crisp, monkeypatch, first, rounds, rmin):
 @pytest.mark.parametrize("mode", [0, 1])
 def test_host_buffers_match_device(crisp, mode):
     """crisp_search with host buffers (the H2D copy overlapped with the query
-    transform in 4 parts) returns what the device-pointer call returns."""
+    transform and the probe, in parts) returns what the device-pointer call
+    returns."""
     import torch
 
     X, _, ox = make_case(cfg=1, N=20000, Q=10, seed=3)

@@ -41,14 +41,17 @@ for _ in range(10):
     ix.search_async(Qd, k, 1, ids, dd, s)
 torch.cuda.synchronize()
 t_dev = (time.perf_counter() - t0) / 10
-for _ in range(3):
-    crisp._check(crisp.lib().crisp_search(ix._h, crisp._ptr(qn), Q, k, 1, crisp._ptr(ih), crisp._ptr(dh)))
-ts = []
-for _ in range(10):
-    t0 = time.perf_counter()
-    crisp._check(crisp.lib().crisp_search(ix._h, crisp._ptr(qn), Q, k, 1, crisp._ptr(ih), crisp._ptr(dh)))
-    ts.append(time.perf_counter() - t0)
-t2 = time.perf_counter()
+parts_ms = {}
+for parts in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["4"]):
+    os.environ["CRISP_H2D_PARTS"] = parts
+    for _ in range(3):
+        crisp._check(crisp.lib().crisp_search(ix._h, crisp._ptr(qn), Q, k, 1, crisp._ptr(ih), crisp._ptr(dh)))
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        crisp._check(crisp.lib().crisp_search(ix._h, crisp._ptr(qn), Q, k, 1, crisp._ptr(ih), crisp._ptr(dh)))
+        ts.append(time.perf_counter() - t0)
+    parts_ms[parts] = round(float(np.median(ts)) * 1e3, 3)
 torch.cuda.synchronize()
 hd = torch.empty((Q, D), dtype=torch.float32, device="cuda")
 t0 = time.perf_counter()
@@ -56,5 +59,5 @@ for _ in range(10):
     hd.copy_(qh, non_blocking=True)
 torch.cuda.synchronize()
 t_h2d = (time.perf_counter() - t0) / 10
-print({"device_ms": t_dev * 1e3, "host_ms_each": [round(x * 1e3, 3) for x in ts], "h2d_ms": t_h2d * 1e3,
+print({"device_ms": t_dev * 1e3, "host_ms_median_by_parts": parts_ms, "h2d_ms": t_h2d * 1e3,
        "same": bool(np.array_equal(ih, ids.cpu().numpy()))})
