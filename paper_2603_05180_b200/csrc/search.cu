@@ -29,8 +29,8 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 
 constexpr int WARPS = 8;
 constexpr int THREADS = WARPS * 32;
-constexpr int CS_CAP = 1024;          // slice-table entries per round (count kernel)
-constexpr int CS_U = 16;              // ids staged per thread per round
+constexpr int CS_CAP = 512;           // slice-table entries per round (count kernel)
+constexpr int CS_U = 8;               // ids staged per thread per round
 constexpr int CS_TCAP = THREADS * CS_U;  // positions per round
 constexpr int PATIENCE_CH = 128;      // min rows verified per patience chunk (k_patience_tail)
 constexpr int TAIL_CAP = 1024;        // max rows per chunk of k_patience_tail
@@ -385,7 +385,7 @@ __device__ __forceinline__ void prefetch_first(const CountSmem &S, int Etot, con
 // a3 + a4 for BPC blocks of one query; candidates go to the query's pool
 // region at a per-block base taken from an atomic cursor (blocks keep their
 // ascending-id order inside; consumers enumerate blocks in ascending order).
-__global__ void __launch_bounds__(THREADS) k_count_select(const uint32_t *__restrict__ act,
+__global__ void __launch_bounds__(THREADS, 4) k_count_select(const uint32_t *__restrict__ act,
                                                            const int32_t *__restrict__ act_len, int M, int KK,
                                                            const int32_t *__restrict__ off2, int NB,
                                                            const int32_t *__restrict__ ids, int64_t N, int BS, int BPC,
