@@ -540,6 +540,113 @@ __global__ void __launch_bounds__(256) k_kpp_pick(const float *S, int64_t n, int
     const int64_t pk = s_pick;
     for (int t = tid; t < dh; t += blockDim.x) C[((int64_t)h * K + c) * dh + t] = S[pk * Dp + (int64_t)h * dh + t];
 }
+// k-means++ pick, certified parallel form.  All D2 >= 0, so any summation
+// order of a prefix is within gamma = (n + 64) u of the exact prefix E(p); the
+// oracle's sequential running sums cum(p) and total are too.  A thread sums
+// its contiguous segment, a block scan gives the segment offsets, and from the
+// parallel prefixes Ep and the certified interval [T_lo, T_hi] of the oracle's
+// target u_c * total, the first p with certainly cum(p) > target is the pick
+// when no earlier p possibly exceeds it; when nothing can exceed it the pick is
+// the last positive position.  Any other case (a prefix within ~2e-11 of the
+// target) takes the oracle's sequential rule in thread 0.
+constexpr int KPP_T = 1024;
+__global__ void __launch_bounds__(KPP_T) k_kpp_pick_par(const float *S, int64_t n, int Dp, int dh, int K,
+                                                         uint64_t seed, int c, const double *D2, float *C) {
+    __shared__ double wsum[KPP_T / 32];
+    __shared__ int64_t s_first_sure, s_first_maybe, s_last;
+    __shared__ int64_t s_pick;
+    const int h = blockIdx.x;
+    const double *d = D2 + (int64_t)h * n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t per = (n + KPP_T - 1) / KPP_T, lo = min(n, tid * per), hi = min(n, lo + per);
+    double seg = 0.0;
+    int64_t lastpos = -1;
+    for (int64_t p = lo; p < hi; p++) {
+        const double v = d[p];
+        seg += v;
+        if (v > 0.0) lastpos = p;
+    }
+    // exclusive block scan of the segment sums (warp scan + warp totals)
+    double inc = seg;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    if (tid == 0) {
+        s_first_sure = INT64_MAX;
+        s_first_maybe = INT64_MAX;
+        s_last = -1;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double w = wsum[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= off) w += t;
+        }
+        wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const double total = wsum[KPP_T / 32 - 1];
+    double run = (warp ? wsum[warp - 1] : 0.0) + inc - seg;  // exclusive prefix of this segment
+    atomicMax((unsigned long long *)&s_last, (unsigned long long)(lastpos + 1));  // +1: -1 -> 0
+    const double uc = uniform(seed, STREAM_KM_INIT, (uint64_t)c, (uint32_t)h);
+    const double g = ((double)n + 64.0) * 0x1p-53 * 1.01;  // any-order prefix vs exact
+    const double g2 = 2.0 * g + 0x1p-50;                    // cum (or target) vs the parallel prefix (+ roundings)
+    const double t_lo = uc * total * (1.0 - g2), t_hi = uc * total * (1.0 + g2);
+    for (int64_t p = lo; p < hi; p++) {
+        run += d[p];
+        if (run * (1.0 - g2) > t_hi) {
+            atomicMin((unsigned long long *)&s_first_sure, (unsigned long long)p);
+            break;
+        }
+        if (run * (1.0 + g2) > t_lo) atomicMin((unsigned long long *)&s_first_maybe, (unsigned long long)p);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int64_t last = s_last - 1;
+        int64_t pick = -1;
+        bool sure = false;
+        if (!(total > 0.0)) {  // all D2 == 0 (exactly: non-negative terms)
+            pick = (int64_t)(uc * (double)n);
+            if (pick >= n) pick = n - 1;
+            sure = true;
+        } else if (s_first_sure != INT64_MAX) {
+            // no earlier position may exceed the target
+            if (s_first_maybe == INT64_MAX || s_first_maybe >= s_first_sure) {
+                pick = s_first_sure;
+                sure = true;
+            }
+        } else if (s_first_maybe == INT64_MAX) {
+            pick = last;  // no position can exceed the target
+            sure = true;
+        }
+        if (!sure) {  // the oracle's sequential rule
+            double tot = 0.0;
+            for (int64_t p = 0; p < n; p++) tot = __dadd_rn(tot, d[p]);
+            const double target = uc * tot;
+            double cum = 0.0;
+            int64_t lp = 0;
+            pick = -1;
+            for (int64_t p = 0; p < n; p++) {
+                if (d[p] > 0.0) lp = p;
+                cum = __dadd_rn(cum, d[p]);
+                if (cum > target) {
+                    pick = p;
+                    break;
+                }
+            }
+            if (pick < 0) pick = lp;
+        }
+        s_pick = pick;
+    }
+    __syncthreads();
+    const int64_t pk = s_pick;
+    for (int t = tid; t < dh; t += KPP_T) C[((int64_t)h * K + c) * dh + t] = S[pk * Dp + (int64_t)h * dh + t];
+}
 // argmin over the K centroids of one half-subspace h for 128 points per CTA
 // (Alg. "assign" S:L220): the centroids staged as doubles and the
 // points' h-th half staged transposed (Xs[d][pt], pitch 129: conflict-free), so
@@ -730,7 +837,8 @@ static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, u
     k_kpp_d2<<<nblk(n * nh, 256), 256, 0, s>>>(S, n, Dp, dh, K, nh, C, 0, D2);
     CRISP_LAUNCH();
     for (int c = 1; c < K; c++) {
-        k_kpp_pick<<<nh, 256, 0, s>>>(S, n, Dp, dh, K, nh, seed, c, D2, C);
+        if (getenv("CRISP_KPP_SEQ")) k_kpp_pick<<<nh, 256, 0, s>>>(S, n, Dp, dh, K, nh, seed, c, D2, C);
+        else k_kpp_pick_par<<<nh, KPP_T, 0, s>>>(S, n, Dp, dh, K, seed, c, D2, C);
         CRISP_LAUNCH();
         k_kpp_d2<<<nblk(n * nh, 256), 256, 0, s>>>(S, n, Dp, dh, K, nh, C, c, D2);
         CRISP_LAUNCH();

@@ -262,6 +262,21 @@ def test_gpu_build_matches_oracle_build(crisp):
     compare_index(ix, ox)
 
 
+def test_kmeanspp_parallel_pick_matches_sequential(crisp, monkeypatch):
+    """The certified parallel k-means++ pick (k_kpp_pick_par) against the
+    oracle-order sequential kernel (CRISP_KPP_SEQ=1): the GPU's own builds must
+    give bit-identical codebooks, cells and CSR on a 60k-point sample."""
+    w = synth.Workload(2, D=128)
+    X = w.base(60000).numpy()
+    a = crisp.Index.build(X, 4, K=50, rotation=0, kmeans_iters=4, seed=5)
+    ea = a.export()
+    monkeypatch.setenv("CRISP_KPP_SEQ", "1")
+    b = crisp.Index.build(X, 4, K=50, rotation=0, kmeans_iters=4, seed=5)
+    eb = b.export()
+    for name in ("codebooks", "cells", "offsets", "ids"):
+        assert np.array_equal(ea[name], eb[name]), name
+
+
 def test_gpu_rotation_properties(crisp):
     """Rotation forced on: R orthogonal (fp32 storage, 1e-5), close to the
     oracle's R (same Philox G; QR by cuSOLVER vs Householder), and the CEV gate
