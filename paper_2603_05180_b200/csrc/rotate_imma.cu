@@ -40,7 +40,7 @@ constexpr int LV = 9;  // levels 2..LV (slice pairs s + t <= LV)
 
 std::mutex g_mu;
 cublasLtHandle_t g_lt = nullptr;
-void *g_ws = nullptr;
+std::map<int, void *> g_ws;  // cuBLASLt workspace per device
 constexpr size_t WS_BYTES = 32u << 20;
 
 #define CRISP_LT(call)                                                                  \
@@ -122,17 +122,17 @@ __global__ void k_slice_cols(const float *__restrict__ R, int Dp, int Dpk, int8_
     }
 }
 
-__global__ void k_certify(const int32_t *__restrict__ C, int64_t rows, int Dp, const int32_t *__restrict__ qe,
+__global__ void k_certify(const int32_t *__restrict__ C, int64_t rows, int Dp, int Dpk, const int32_t *__restrict__ qe,
                           const double *__restrict__ qn2, const int32_t *__restrict__ re,
                           const double *__restrict__ rn2, float *__restrict__ Y, int64_t ldy,
                           unsigned long long *__restrict__ nfall, int64_t *__restrict__ flist) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t m = blockIdx.y;
     if (n >= Dp || m >= rows) return;
-    const int64_t plane = rows * (int64_t)Dp;
+    const int64_t plane = rows * (int64_t)Dpk;
     int32_t c[LV - 1];
 #pragma unroll
-    for (int l = 2; l <= LV; l++) c[l - 2] = C[(int64_t)(l - 2) * plane + m * Dp + n];
+    for (int l = 2; l <= LV; l++) c[l - 2] = C[(int64_t)(l - 2) * plane + m * Dpk + n];
     double acc = 0.0, mag = 0.0;
 #pragma unroll
     for (int l = LV; l >= 2; l--) {  // ascending magnitude; 2^-7l exact
@@ -229,11 +229,11 @@ struct Plan {
 };
 std::map<std::tuple<int, int, int64_t>, Plan> g_plans;  // (Dp, Dpk, rows)
 
-void ensure_lt() {
-    if (!g_lt) {
-        CRISP_LT(cublasLtCreate(&g_lt));
-        CRISP_CUDA(cudaMalloc(&g_ws, WS_BYTES));
-    }
+void *ensure_lt(int device) {
+    if (!g_lt) CRISP_LT(cublasLtCreate(&g_lt));
+    void *&ws = g_ws[device];
+    if (!ws) CRISP_CUDA(cudaMalloc(&ws, WS_BYTES));
+    return ws;
 }
 
 const Plan &plan_for(int Dp, int Dpk, int64_t rows) {
@@ -245,16 +245,16 @@ const Plan &plan_for(int Dp, int Dpk, int64_t rows) {
     const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
     CRISP_LT(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta)));
     CRISP_LT(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb)));
-    // column-major: D (Dp x rows) = A^T (Dp x K') B (K' x rows); A = R slices (row n
+    // column-major: D (Dpk x rows) = A^T (Dpk x K') B (K' x rows); A = R slices (row n
     // of Rsl, ld SL Dpk), B = query slices (row m of Qcat, ld SL Dpk)
-    CRISP_LT(cublasLtMatrixLayoutCreate(&p.lc, CUDA_R_32I, Dp, rows, Dp));
+    CRISP_LT(cublasLtMatrixLayoutCreate(&p.lc, CUDA_R_32I, Dpk, rows, Dpk));  // outputs padded to Dpk (aligned)
     cublasLtMatmulPreference_t pref;
     CRISP_LT(cublasLtMatmulPreferenceCreate(&pref));
     size_t wsb = WS_BYTES;
     CRISP_LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb)));
     for (int l = 2; l <= LV; l++) {
         const uint64_t K = (uint64_t)(l - 1) * Dpk;
-        CRISP_LT(cublasLtMatrixLayoutCreate(&p.la[l], CUDA_R_8I, K, Dp, (int64_t)SL * Dpk));
+        CRISP_LT(cublasLtMatrixLayoutCreate(&p.la[l], CUDA_R_8I, K, Dpk, (int64_t)SL * Dpk));
         CRISP_LT(cublasLtMatrixLayoutCreate(&p.lb[l], CUDA_R_8I, K, rows, (int64_t)SL * Dpk));
         cublasLtMatmulHeuristicResult_t res;
         int nres = 0;
@@ -279,11 +279,12 @@ void prepare_rotation_slices(crisp_index *ix, cudaStream_t s) {
     if (!ix->R || ix->Rsl) return;
     const int Dp = ix->Dp, Dpk = rotation_slices_k(Dp);
     int8_t *tmp = nullptr;
-    CRISP_CUDA(cudaMalloc(&ix->Rsl, (size_t)Dp * SL * Dpk));
+    CRISP_CUDA(cudaMalloc(&ix->Rsl, (size_t)Dpk * SL * Dpk));  // rows n >= Dp stay zero
+    CRISP_CUDA(cudaMemsetAsync(ix->Rsl, 0, (size_t)Dpk * SL * Dpk, s));
     CRISP_CUDA(cudaMalloc(&ix->Rexp, (size_t)Dp * 4));
     CRISP_CUDA(cudaMalloc(&ix->Rn2, (size_t)Dp * 8));
     CRISP_CUDA(cudaMalloc(&ix->Rt, (size_t)Dp * Dp * 4));
-    ix->hbm_bytes += (int64_t)Dp * (SL * Dpk + 12) + (int64_t)Dp * Dp * 4;
+    ix->hbm_bytes += (int64_t)Dpk * SL * Dpk + (int64_t)Dp * 12 + (int64_t)Dp * Dp * 4;
     k_transpose<<<dim3((Dp + 31) / 32, (Dp + 31) / 32), dim3(32, 8), 0, s>>>(ix->R, Dp, ix->Rt);
     CRISP_LAUNCH();
     CRISP_CUDA(cudaMallocAsync(&tmp, (size_t)Dp * SL * Dpk, s));
@@ -303,11 +304,11 @@ void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64
     if (rows <= 0) return;
     const int Dp = ix->Dp, Dpk = rotation_slices_k(Dp);
     std::lock_guard<std::mutex> lk(g_mu);
-    ensure_lt();
+    void *ws = ensure_lt(ix->device);
     const Plan &p = plan_for(Dp, Dpk, rows);
     // scratch: Qcat (rows x SL Dpk int8) | C (LV-1 levels x rows x Dp int32) | qn2 | qe
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    const size_t qbytes = up((size_t)rows * SL * Dpk), cbytes = up((size_t)(LV - 1) * rows * Dp * 4);
+    const size_t qbytes = up((size_t)rows * SL * Dpk), cbytes = up((size_t)(LV - 1) * rows * Dpk * 4);
     char *buf = nullptr;
     CRISP_CUDA(cudaMallocAsync(&buf, qbytes + cbytes + up((size_t)rows * 8) + up((size_t)rows * 4), s));
     int8_t *Qcat = (int8_t *)buf;
@@ -319,9 +320,9 @@ void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64
     const int32_t alpha = 1, beta = 0;
     for (int l = 2; l <= LV; l++) {
         const int8_t *A = ix->Rsl + (size_t)(LV - l) * Dpk;  // [b_{l-1} .. b_1]
-        int32_t *Cl = C + (size_t)(l - 2) * rows * Dp;
+        int32_t *Cl = C + (size_t)(l - 2) * rows * Dpk;
         CRISP_LT(cublasLtMatmul(g_lt, p.op, &alpha, A, p.la[l], Qcat, p.lb[l], &beta, Cl, p.lc, Cl, p.lc, &p.algo[l],
-                                g_ws, WS_BYTES, s));
+                                ws, WS_BYTES, s));
     }
     // uncertified outputs: counter + list (at most rows x Dp entries)
     unsigned long long *cnt = nullptr;
@@ -331,7 +332,7 @@ void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64
     flist = (int64_t *)(cnt + 1);
     CRISP_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
     dim3 g((Dp + 127) / 128, (unsigned)rows);
-    k_certify<<<g, 128, 0, s>>>(C, rows, Dp, qe, qn2, ix->Rexp, ix->Rn2, Y, ldy, cnt, flist);
+    k_certify<<<g, 128, 0, s>>>(C, rows, Dp, Dpk, qe, qn2, ix->Rexp, ix->Rn2, Y, ldy, cnt, flist);
     CRISP_LAUNCH();
     k_recompute<<<148 * 8, 128, 0, s>>>(cnt, flist, Dp, X, ldx, ix->Rt, Y, ldy);
     CRISP_LAUNCH();

@@ -293,15 +293,16 @@ def test_gpu_rotation_properties(crisp):
     assert auto.info()["rotated"] == (ox["cev"] > 0.85) == 1
 
 
-def test_certified_rotation_adversarial(crisp):
+@pytest.mark.parametrize("D,M", [(203, 4), (100, 3)])
+def test_certified_rotation_adversarial(crisp, D, M):
     """a0 on the int8 tensor cores with the certified rounding (rotate_imma.cu):
     q' must equal the oracle's sequential fp64 chain bit for bit on rows chosen
     to stress the certificate: zeros, a single non-zero, 60 orders of magnitude
     inside one row, subnormal inputs, power-of-two scalings, alternating signs,
-    exact cancellations, and a D that is not a multiple of 16 (padding)."""
+    exact cancellations, and padded dimensions (D' = 208, and D' = 102 whose
+    digit planes pad to 112)."""
     rng = np.random.default_rng(11)
-    D, M = 203, 4
-    Dp = oracle.padded_dim(D, M)
+    Dp = oracle.padded_dim(D, M)  # 208 (a multiple of 16) and 102 (the int8 planes pad to 112)
     X = rng.standard_normal((2500, D)).astype(np.float32)
     R, _ = oracle.rotation(Dp, 9)
     ix = crisp.Index.build(X, M, R=R, codebooks=oracle.train_codebooks(oracle.rotate_rows(
