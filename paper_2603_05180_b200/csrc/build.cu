@@ -424,18 +424,13 @@ static void make_rotation(int D, uint64_t seed, float *R, cudaStream_t s) {
 // In-place X' = X R over row chunks with one scratch tile.
 static void rotate_in_place(crisp_index *ix, cudaStream_t s) {
     const int64_t rowbytes = (int64_t)ix->pitch * 4;
-    const bool imma = rotate_imma_enabled();  // int8 tensor cores, certified (rotate_imma.cu)
     int64_t rc = std::max<int64_t>(64, std::min<int64_t>(ix->N, (512LL << 20) / rowbytes));
-    if (imma) {
-        rc = std::min<int64_t>(rc, 32768);  // the certify grid and the level scratch per tile
-        prepare_rotation_slices(ix, s);
-    }
+    rc = std::min<int64_t>(rc, 32768);  // the certify grid and the level scratch per tile (rotate_imma.cu)
     Scratch sc;
     float *tile = sc.alloc<float>((size_t)rc * ix->pitch);
     for (int64_t r0 = 0; r0 < ix->N; r0 += rc) {
         int64_t rows = std::min(rc, ix->N - r0);
-        if (imma) rotate_rows_imma(ix, ix->X + r0 * ix->pitch, rows, ix->pitch, tile, ix->pitch, s, nullptr);
-        else rotate_rows_f64(ix->X + r0 * ix->pitch, rows, ix->Dp, ix->pitch, ix->R, tile, ix->pitch, s);
+        rotate_rows(ix, ix->X + r0 * ix->pitch, rows, ix->pitch, tile, ix->pitch, s);
         CRISP_CUDA(cudaMemcpy2DAsync(ix->X + r0 * ix->pitch, rowbytes, tile, rowbytes, (size_t)ix->Dp * 4, rows,
                                      cudaMemcpyDeviceToDevice, s));
     }

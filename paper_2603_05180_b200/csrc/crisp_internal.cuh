@@ -108,6 +108,7 @@ void prepare_rotation_slices(crisp_index *ix, cudaStream_t s);
 bool rotate_imma_enabled();
 void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64_t ldx, float *Y, int64_t ldy,
                       cudaStream_t s, unsigned long long *nfall);
+void rotate_rows(crisp_index *ix, const float *X, int64_t rows, int64_t ldx, float *Y, int64_t ldy, cudaStream_t s);
 void rotate_rows_f64(const float *X, int64_t rows, int32_t Dp, int64_t ldx, const float *R, float *Y, int64_t ldy,
                      cudaStream_t s);
 

@@ -349,4 +349,28 @@ void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64
     CRISP_CUDA(cudaFreeAsync(buf, s));
 }
 
+// a0 for rows of X: the certified int8 path when enabled and available for
+// this D' (cuBLASLt has an int8 kernel for the shapes), else the fp64 FMA
+// kernel; both give the oracle's fl32 of the sequential chain
+void rotate_rows(crisp_index *ix, const float *X, int64_t rows, int64_t ldx, float *Y, int64_t ldy, cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<int, bool> unavailable;  // D' values cuBLASLt rejected
+    bool imma = rotate_imma_enabled();
+    if (imma) {
+        std::lock_guard<std::mutex> lk(mu);
+        imma = !unavailable.count(ix->Dp);
+    }
+    if (imma) {
+        try {
+            prepare_rotation_slices(ix, s);
+            rotate_rows_imma(ix, X, rows, ldx, Y, ldy, s, nullptr);
+            return;
+        } catch (Err &) {
+            std::lock_guard<std::mutex> lk(mu);
+            unavailable[ix->Dp] = true;
+        }
+    }
+    rotate_rows_f64(X, rows, ix->Dp, ldx, ix->R, Y, ldy, s);
+}
+
 }  // namespace crisp

@@ -2561,15 +2561,10 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
                                                                         w.qpad + r0 * pitch);
             CRISP_LAUNCH();
             g_launches++;
-            if (ix->rotated) {
-                if (rotate_imma_enabled()) {  // int8 tensor cores, certified (rotate_imma.cu)
-                    if (!ix->Rsl) prepare_rotation_slices(const_cast<crisp_index *>(ix), s);
-                    rotate_rows_imma(ix, w.qpad + r0 * pitch, r1 - r0, pitch, w.qrot + r0 * pitch, pitch, s, nullptr);
-                    g_launches += 3;  // slices, certify, recompute (+ 7 cuBLASLt GEMMs)
-                } else {
-                    rotate_rows_f64(w.qpad + r0 * pitch, r1 - r0, ix->Dp, pitch, ix->R, w.qrot + r0 * pitch, pitch, s);
-                    g_launches++;
-                }
+            if (ix->rotated) {  // int8 tensor cores, certified, else fp64 FMA (rotate_imma.cu)
+                rotate_rows(const_cast<crisp_index *>(ix), w.qpad + r0 * pitch, r1 - r0, pitch, w.qrot + r0 * pitch,
+                            pitch, s);
+                g_launches += 3;  // slices, certify, recompute (+ 8 cuBLASLt GEMMs), or the FMA kernel
             }
             if (P > 1) probe(r0, r1);
         }
