@@ -410,6 +410,40 @@ def run_crisp(args):
         e2e = {"value": Q * K / dt, "unit": "queries/s", "h2d_bytes_per_step": Q * D * 4,
                "d2h_bytes_per_step": Q * k * 12, "recall@10": recall_at(ih, gt, 10), "api": "crisp_search (host buffers)"}
 
+    if world > 1:
+        # e2e at N GPUs: every rank copies the step's queries from pinned host memory,
+        # runs the sharded search (collectives included) and rank 0 reads the merged
+        # ids back; wall clock between barriers, max over ranks
+        mp = op["modes"][head]
+        index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
+        index.set_adsampling(head == 2)
+        qh = torch.empty((Q, D), dtype=torch.float32).pin_memory()
+        qh.copy_(Qd.cpu())
+        qe = torch.empty_like(Qd)
+        ih = torch.empty((Q, k), dtype=torch.int64).pin_memory()
+
+        def e2e_step():
+            qe.copy_(qh, non_blocking=True)
+            oi, _ = cdist.search_step_exact(engine, qe, k, phi(head), stream)
+            if rank == 0:
+                ih.copy_(oi, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(2):
+            e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            e2e_step()
+        dist.barrier()
+        tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                          device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        e2e = {"value": Q * K / dt, "unit": "queries/s", "h2d_bytes_per_step": world * Q * D * 4,
+               "d2h_bytes_per_step": Q * k * 8, "recall@10": recall_at(ih.numpy(), gt, 10) if rank == 0 else None,
+               "api": "dist.search_step_exact (host queries on every rank, merged ids to rank 0's host)"}
+
     # cpu baseline (rank 0, N=1 only): the oracle as it stands on the host cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -33,7 +33,8 @@ def test_bench_two_ranks_match_one():
     assert two.returncode == 0, two.stderr[-2000:]
     a, b = _line(one.stdout), _line(two.stdout)
     assert a["n_gpus"] == 1 and b["n_gpus"] == 2
-    for key in ("metric", "value", "unit", "ms_per_step", "higher_is_better", "scaling", "roofline", "clocks"):
+    for key in ("metric", "value", "unit", "ms_per_step", "higher_is_better", "scaling", "roofline", "clocks", "e2e"):
         assert key in b
+    assert b["e2e"]["value"] > 0 and b["e2e"]["h2d_bytes_per_step"] > 0  # end to end at N = 2 too
     # phi=0 with the exact global fallback: identical to the single index
     assert b["per_mode"]["guaranteed"]["recall"] == a["per_mode"]["guaranteed"]["recall"]
