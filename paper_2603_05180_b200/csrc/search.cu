@@ -1761,7 +1761,7 @@ __device__ __forceinline__ int round_span(const PatState &st, int64_t q, int j0r
 }
 
 template <bool ROWS4>
-__global__ void __launch_bounds__(THREADS, 5) k_verify_rows(const float *__restrict__ qrot, int pitch,
+__global__ void __launch_bounds__(THREADS, ROWS4 ? 6 : 5) k_verify_rows(const float *__restrict__ qrot, int pitch,
                                                           const float *__restrict__ X, const int32_t *__restrict__ pool,
                                                           int64_t PS, const int32_t *__restrict__ totals,
                                                           PatState st, int j0r, int len, int send,
