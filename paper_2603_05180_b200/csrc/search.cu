@@ -1156,7 +1156,7 @@ __device__ __forceinline__ void block_prefix(const int32_t *__restrict__ ncand, 
 }
 
 template <bool ROWS4>
-__global__ void __launch_bounds__(THREADS, ROWS4 ? 5 : 4) k_rerank_exact(const float *__restrict__ qrot, int pitch,
+__global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restrict__ qrot, int pitch,
                                                            const float *__restrict__ X, int64_t gid_base,
                                                            const int32_t *__restrict__ pool, int64_t CAPQ,
                                                            const int32_t *__restrict__ cbase,
