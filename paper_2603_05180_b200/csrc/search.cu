@@ -53,6 +53,17 @@ __global__ void k_prep_queries(const float *__restrict__ q, int64_t Qc, int D, i
 // ---------------------------------------------------------------------------
 // a1 + a2: one warp per (query, subspace)
 // ---------------------------------------------------------------------------
+// dist64 (sequential fma over the dims, S:App. A.1) of a query half held as
+// doubles and a centroid: ((double)q_i - (double)c_i)^2 accumulated in order
+__device__ __forceinline__ double dist64_qd(const double *__restrict__ q, const float *__restrict__ c, int n) {
+    double s = 0.0;
+    for (int i = 0; i < n; i++) {
+        const double d = __dsub_rn(q[i], (double)c[i]);
+        s = __fma_rn(d, d, s);
+    }
+    return s;
+}
+
 __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qrot, int pitch, int64_t q0, int64_t Qc,
                                                     const float *__restrict__ cb, int M, int K, int dh,
                                                     const int32_t *__restrict__ gsize, int smem_gsize, int64_t budget,
@@ -68,10 +79,10 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     // read distinct banks in dist64
     const int cst = smem_cb ? (dh | 1) : dh;
     unsigned char *wbase = (unsigned char *)cbs + (smem_cb ? ((2 * K * cst * 4 + 15) & ~15) : 0);
-    const int per_warp = ((4 * K * 8) + 3 * K + 2 * dh * 4 + 15) & ~15;
+    const int per_warp = ((4 * K + 2 * dh) * 8 + 3 * K + 15) & ~15;
     double *tmp = (double *)(wbase + warp * per_warp);  // 2K
     double *a = tmp + 2 * K, *b = a + K;
-    float *qs = (float *)(b + K);                       // 2 dh: this query's two halves
+    double *qs = b + K;                                 // 2 dh: this query's two halves, as doubles
     unsigned char *pa = (unsigned char *)(qs + 2 * dh), *pb = pa + K, *col = pb + K;
     const int32_t *gsm = gsize + (int64_t)m * KK;
     const float *cbm = cb + (int64_t)m * 2 * K * dh;
@@ -87,12 +98,18 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     const int64_t q = q0 + ((int64_t)blockIdx.x * WARPS + warp) * qpw + qi;  // queries [q0, Qc)
     if (q >= Qc) return;
     const float *qm = qrot + q * pitch + (int64_t)m * 2 * dh;
-    for (int i = lane; i < 2 * dh; i += 32) qs[i] = qm[i];
+    for (int i = lane; i < 2 * dh; i += 32) qs[i] = (double)qm[i];
     __syncwarp();
-    // half distances (Alg. 1 l.4): dist64, exactly the oracle's order
+    // half distances (Alg. 1 l.4): dist64, exactly the oracle's order (the query
+    // converted once; with staged codebooks the compiler sees shared loads)
     for (int side = 0; side < 2; side++) {
-        const float *C = cbm + (int64_t)side * K * cst;
-        for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64(qs + side * dh, C + (int64_t)c * cst, dh);
+        if (smem_cb) {
+            const float *C = cbs + side * K * cst;
+            for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64_qd(qs + side * dh, C + c * cst, dh);
+        } else {
+            const float *C = cbm + (int64_t)side * K * cst;
+            for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64_qd(qs + side * dh, C + (int64_t)c * cst, dh);
+        }
     }
     __syncwarp();
     // sort each half by (delta, c) via ranks
@@ -2504,7 +2521,7 @@ struct Work {
         probe_cb = (2 * K * (ix->dh | 1) * 4 <= 96 * 1024) ? 1 : 0;  // rows padded to an odd stride
         probe_qpw = std::max(1, env_int("CRISP_PROBE_QPW", 4));  // queries per warp in k_probe
         probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + (probe_cb ? ((2 * K * (ix->dh | 1) * 4 + 15) & ~15) : 0) +
-                     WARPS * (((4 * K * 8) + 3 * K + 2 * ix->dh * 4 + 15) & ~15);
+                     WARPS * ((((4 * K + 2 * ix->dh) * 8) + 3 * K + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
         countw_smem = (int)countw_fixed_smem(BS);
         countw_ham_smem = ix->Wp * 8 + (Dp + 1) * 4;
