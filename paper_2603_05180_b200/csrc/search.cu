@@ -264,7 +264,7 @@ __device__ void count_one_block(CountSmem &S, unsigned char *cnt8, int BS, int64
                                 const uint32_t *__restrict__ act, int M, int KK, const int32_t *__restrict__ off2,
                                 int NB, const int32_t *__restrict__ ids, int64_t N, int (&s0r)[CS_EPT],
                                 int (&s1r)[CS_EPT], int tau, uint32_t *cross) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x;
     const bool cached = Etot <= CS_CAP;
     const uint32_t bbase = (uint32_t)b * (uint32_t)BS;
     for (int e0 = 0; e0 < Etot; e0 += CS_CAP) {
