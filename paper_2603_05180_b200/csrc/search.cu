@@ -1598,6 +1598,7 @@ __device__ void warp_segments(const int32_t *__restrict__ ncand, const int32_t *
 // counts its qualifying elements per bin, the per-(warp, bin) offsets follow
 // from the bin starts (stable: earlier warps first), and each warp scatters
 // its range in order.  smem: start (Dp+1), segments (2NS+1), counts WARPS x (Dp+1).
+template <bool LIST>
 __global__ void __launch_bounds__(THREADS) k_hsort_cta(const int32_t *__restrict__ ncand,
                                                         const int32_t *__restrict__ cbase, int NS, int Dp,
                                                         const int32_t *__restrict__ ghist,
@@ -1658,23 +1659,47 @@ __global__ void __launch_bounds__(THREADS) k_hsort_cta(const int32_t *__restrict
         bl0 = a;
     }
     constexpr int U = 8;
-    // phase A: per-bin counts of this warp's qualifying elements
+    // phase A: per-bin counts of this warp's qualifying elements; their pool
+    // positions are also listed in order in the unused tail of the query's order
+    // row ([total, CS), capw per warp), so phase B visits only them
+    int32_t *out = order + q * CS;
+    // listing pays when the qualifying elements are a small part of the list
+    // (the host picks LIST when the positions the verification reads are few)
+    constexpr bool listing = LIST;
+    const int64_t capw64 = listing ? (CS - total) / WARPS : 0;
+    const int capw = capw64 < (1 << 30) ? (int)capw64 : (1 << 30);
+    int32_t *scr = out + total + (int64_t)warp * capw;
+    __shared__ int s_over;
+    if (tid == 0) s_over = 0;
+    int nq = 0;
     int bl = bl0;
     for (int v00 = lo; v00 < hi; v00 += 32 * U) {
-        int hh[U];
+        int hh[U], pp[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int v = v00 + u * 32 + lane;
             hh[u] = 0x7fffffff;
+            pp[u] = 0;
             if (v < hi) {
                 while (pre[bl + 1] <= v) bl++;
-                hh[u] = hq[cbs[bl] + (v - pre[bl])];
+                pp[u] = cbs[bl] + (v - pre[bl]);
+                hh[u] = hq[pp[u]];
             }
         }
 #pragma unroll
-        for (int u = 0; u < U; u++)
-            if (hh[u] <= cut) atomicAdd(&mycnt[hh[u]], 1);
+        for (int u = 0; u < U; u++) {
+            const bool qual = hh[u] <= cut;
+            if (qual) atomicAdd(&mycnt[hh[u]], 1);
+            const unsigned qm = __ballot_sync(0xffffffffu, qual);
+            if (listing) {
+                const int r = nq + __popc(qm & ((1u << lane) - 1));
+                if (qual && r < capw) scr[r] = pp[u];
+                nq += __popc(qm);
+            }
+        }
     }
+    __syncthreads();  // s_over initialised
+    if (lane == 0 && (!listing || nq > capw)) s_over = 1;
     __syncthreads();
     // per-(warp, bin) output offsets: bin start + the bin's elements of earlier warps
     for (int h = tid; h <= cut; h += THREADS) {
@@ -1686,8 +1711,35 @@ __global__ void __launch_bounds__(THREADS) k_hsort_cta(const int32_t *__restrict
         }
     }
     __syncthreads();
+    if (!s_over) {
+        // phase B over the listed qualifying elements only, in order
+        for (int i0 = 0; i0 < nq; i0 += 32) {
+            const int i = i0 + lane;
+            const bool qual = i < nq;
+            const int pos = qual ? scr[i] : 0;
+            const int h = qual ? (int)hq[pos] : 0x7fffffff;
+            const int id = qual ? cq[pos] : 0;
+            const unsigned qm = __ballot_sync(0xffffffffu, qual);
+            int rank = 0, cnt = 0, leader = 32;
+            if (qual) {
+                const unsigned peers = __match_any_sync(qm, h);
+                leader = __ffs(peers) - 1;
+                rank = __popc(peers & ((1u << lane) - 1));
+                cnt = __popc(peers);
+            }
+            int base = 0;
+            if (qual && lane == leader) {
+                base = mycnt[h];
+                mycnt[h] = base + cnt;
+            }
+            base = __shfl_sync(0xffffffffu, base, qual ? leader : lane);
+            if (qual) out[base + rank] = id;
+            __syncwarp();
+        }
+        if (tid == 0) total_out[q] = total;
+        return;
+    }
     // phase B: stable scatter of this warp's range
-    int32_t *out = order + q * CS;
     bl = bl0;
     for (int v00 = lo; v00 < hi; v00 += 32 * U) {
         int hh[U], ll[U];
@@ -2375,7 +2427,8 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -2699,9 +2752,17 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         // (h, id) order into cbuf
         StageScope st(s, 7);
         if (w.hsort_cta_smem <= 200 * 1024)
-            k_hsort_cta<<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
-                w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals,
-                w.full_order ? 0x7fffffff : w.order_end());
+        {
+            // LIST: phase B visits only the listed qualifying elements (when the
+            // sorted prefix is short: k = 10 configurations)
+            const int lim = w.full_order ? 0x7fffffff : w.order_end();
+            if (lim <= 4096)
+                k_hsort_cta<true><<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
+                    w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals, lim);
+            else
+                k_hsort_cta<false><<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
+                    w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals, lim);
+        }
         else
             k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ,
                                                            w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.order_end());
