@@ -2514,7 +2514,7 @@ struct Work {
         // ADSampling on the exact schedule's per-query spans (else fixed S0-row rounds)
         adsp = ad ? env_int("CRISP_AD_SPANS", 1) : 0;
         R0 = std::max(0, std::min(16, env_int("CRISP_PATIENCE_ROUNDS", ad && !adsp ? 2 : 3)));
-        S1 = std::max(1, env_int("CRISP_ROUND_SPLITS", 2));       // CTAs per query, exact rounds >= 1
+        S1 = std::max(1, env_int("CRISP_ROUND_SPLITS", 3));       // CTAs per query, exact rounds >= 1
         nl_min = std::max(32, env_int("CRISP_ROUND_MIN", 64));  // min span of an exact round >= 1
         BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 16)));  // id blocks per count CTA
         // 0: k_count_select (CTA-flattened slices, for many small cells), 1: k_count_warp
