@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_count_select(const uint32_t *__r
 // bitmap in ascending id (its own candidate segment, base from an atomic
 // cursor) and re-zeroes counters and bitmap; the counters are not scanned.
 // ---------------------------------------------------------------------------
-constexpr int CW_U = 8;  // 32-position batches with loads in flight per warp (k_count_warp)
+constexpr int CW_U = 4;  // 32-position batches with loads in flight per warp (k_count_warp)
 constexpr uint32_t CW_EMASK = 0xffffffu;  // cached entry: (m*KK + cell) | m << 24 | WFLAG
 struct CountWSmem {
     uint32_t erow[CS_CAP];
