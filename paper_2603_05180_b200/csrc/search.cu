@@ -2599,7 +2599,7 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
     // a0 (and a1+a2) in parts; with host queries (hq: the source of the device
     // staging `queries`) part p's H2D copy runs on a side stream while part p-1 is
     // padded, rotated and probed
-    const int P = (hq && qn >= 2048) ? std::max(1, std::min(16, env_int("CRISP_H2D_PARTS", 2))) : 1;
+    const int P = (hq && qn >= 2048) ? std::max(1, std::min(16, env_int("CRISP_H2D_PARTS", 3))) : 1;
     auto probe = [&](int64_t r0, int64_t r1) {
         dim3 g(nblk(r1 - r0, WARPS * w.probe_qpw), M);
         k_probe<<<g, THREADS, w.probe_smem, s>>>(w.qrot, pitch, r0, r1, ix->cb, M, K, ix->dh, ix->gsize, w.probe_gs,
