@@ -4,12 +4,14 @@
 
 A step = one crisp_search_async over the whole query batch (all hot-path
 stages a0..a5, plus the a6 all-gather/merge when G > 1), inputs resident in
-HBM.  Workload at N=1: BASELINE configs[1] (N=1M, D=960, Q=10k, k=10,
-synthetic Gist-like data) at the operating point (M, beta,
-alpha, mode) of configs/operating_points.json, which a sweep (--sweep)
-selected as the fastest with recall@10 >= 0.9 against exact ground truth.
+HBM.  Workload at N=1: BASELINE configs[3] (cfg4: N=2M, D=3072, Q=10k,
+k=100, synthetic Simplewiki-OpenAI-like text embeddings), the
+config the metric's "(1/2/4/8 B200)" names and the largest that fits one GPU,
+at the operating point (M, beta, alpha, mode) of configs/operating_points.json,
+which a sweep (--sweep) selected as the fastest with recall@10 >= 0.9 (of the
+top 10 of the k=100 returned) against exact ground truth.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--cfg 2]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--cfg 4]
 """
 from __future__ import annotations
 
@@ -68,7 +70,12 @@ class Clocks:
 
     def _read(self):
         for line in self.p.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, t0, t1):
+        """Restrict the summary to samples that arrived inside [t0, t1] (host
+        clock around the synchronized, timed region)."""
+        self.win = (t0, t1)
 
     def __exit__(self, *a):
         if self.p:
@@ -81,7 +88,10 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        win = getattr(self, "win", None)
+        for ts, ln in self.lines:
+            if win is not None and not (win[0] <= ts <= win[1] + 0.25):
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -95,7 +105,10 @@ class Clocks:
                     reasons.add(n)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if win is not None:
+            out["window_s"] = round(win[1] - win[0], 3)
+        return out
 
 
 def hbm_peak():
@@ -158,26 +171,71 @@ def recall_at(ids, gt, k=10):
 
 
 # --------------------------------------------------------------------------- oracle (reference arm / cpu_baseline)
-def oracle_qps(X_host, Q_host, op, k, budget_seconds=15.0, max_queries=None):
-    """The CPU oracle as it stands, on all host cores, on a bounded sample."""
+def cpu_info():
+    """lscpu model / sockets / threads of the host the oracle runs on."""
+    kv = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=20).stdout
+        for ln in out.splitlines():
+            if ":" in ln:
+                a, b = ln.split(":", 1)
+                kv[a.strip()] = b.strip()
+    except Exception:
+        pass
+
+    def num(key):
+        try:
+            return int(kv[key])
+        except Exception:
+            return None
+
+    return {"model": kv.get("Model name"), "sockets": num("Socket(s)"), "cores_per_socket": num("Core(s) per socket"),
+            "threads_per_core": num("Thread(s) per core"), "cpus": num("CPU(s)") or os.cpu_count()}
+
+
+def oracle_index_of(index):
+    """The oracle's index dict holding the arrays the GPU index exports (X', R,
+    codebooks, cell assignment, CSR, codes): the same index the GPU searches.
+    The oracle's own build cannot run at cfg4/cfg5 within minutes (X' = X R
+    over 2M x 3072^2 is ~38 TFLOP of sequential fp64 chains), and the build is
+    not part of the timed step; only the oracle's search is timed."""
+    e = index.export()
+    i = index.info()
+    return dict(N=i["N"], D=i["D"], Dp=i["padded_D"], M=i["M"], K=i["K"], dh=i["dh"], X=e["X"], R=e["R"],
+                rotated=bool(i["rotated"]), cev=i["cev"], cb=e["codebooks"], cells=e["cells"], off=e["offsets"],
+                ids=e["ids"], codes=e["codes"], gsize=e["cell_sizes"], gid_base=i["gid_base"], N_budget=i["N_global"])
+
+
+def time_oracle(ox, Qh, k, mode, B, tau, budget_seconds=12.0, single_seconds=4.0, patience_factor=40):
+    """The oracle's search (as it stands) on the host: all cores (OpenMP over
+    queries) on a bounded sample sized to ~budget_seconds, then one thread on
+    up to 100 queries (~single_seconds).  Returns a cpu_baseline dict."""
     import oracle
 
-    M, beta, alpha, mode = op["M"], op["beta"], op["alpha"], op["mode"]
     cores = os.cpu_count() or 1
-    t0 = time.time()
-    ox = oracle.build(X_host, M, K=50, kmeans_iters=20, kmeans_sample=100000, seed=op.get("seed", 1))
-    t_build = time.time() - t0
-    B, tau = oracle.budget_ids(beta, X_host.shape[0]), oracle.tau_int(alpha, M)
-    nq = min(64, Q_host.shape[0])
-    t0 = time.time()
-    oracle.search(ox, Q_host[:nq], k, phi(mode), B, tau, nthreads=cores, adsampling=mode == 2)
-    per_q = (time.time() - t0) / nq
-    n = int(min(max_queries or Q_host.shape[0], max(nq, budget_seconds / max(per_q, 1e-6))))
-    return ox, (B, tau), dict(per_q=per_q, n=n, cores=cores, build_s=t_build)
+    Q = Qh.shape[0]
+    kw = dict(patience_factor=patience_factor, adsampling=mode == 2)
+    nq = min(32, Q)
+    t0 = time.perf_counter()
+    oracle.search(ox, Qh[:nq], k, phi(mode), B, tau, nthreads=cores, **kw)
+    per_q = (time.perf_counter() - t0) / nq
+    n = int(min(Q, max(nq, budget_seconds / max(per_q, 1e-7))))
+    t0 = time.perf_counter()
+    oracle.search(ox, Qh[:n], k, phi(mode), B, tau, nthreads=cores, **kw)
+    dt = time.perf_counter() - t0
+    per_q1 = dt / n * cores  # single-thread estimate for sizing only
+    n1 = int(min(100, Q, max(4, single_seconds / max(per_q1, 1e-7))))
+    t0 = time.perf_counter()
+    oracle.search(ox, Qh[:n1], k, phi(mode), B, tau, nthreads=1, **kw)
+    dt1 = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "single_thread": {"value": n1 / dt1, "unit": "queries/s", "queries": n1},
+            "host": cpu_info(), "queries": n, "seconds": dt}
 
 
 def run_reference(args):
-    """--impl reference: the oracle, timed as it stands on the box's host cores."""
+    """--impl reference: the oracle's search, timed as it stands on the box's
+    host cores, on the GPU arm's config (its index: oracle_index_of)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -185,45 +243,68 @@ def run_reference(args):
 
     cfg = args.cfg
     c = synth.CONFIGS[cfg]
-    N, Q, k = args.N or c["N"], args.Q or c["Q"], c["k"]
+    N, Q, k, D = args.N or c["N"], args.Q or c["Q"], c["k"], c["D"]
     op = load_op(cfg, args.mode)
-    # default: Optimized Mode with exact verification (the paper's default arm, Z12;
-    # the headline mode of the GPU arm at cfg2), else the config's last mode
+    # Optimized Mode with exact verification (the GPU arm's headline mode), else
+    # the config's last mode
     mode0 = (1 if 1 in op["modes"] else sorted(op["modes"])[-1]) if args.mode is None else args.mode
-    op.update(op["modes"][mode0], mode=mode0)
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    w = synth.Workload(cfg, device=dev)
-    X = w.base(N)
-    Qd = w.queries(Q)
-    gt = ground_truth(X, Qd, k) if dev == "cuda" else None
-    Xh, Qh = X.cpu().numpy(), Qd.cpu().numpy()
-    del X
-    ox, (B, tau), cal = oracle_qps(Xh, Qh, op, k)
-    per_step = max(1, min(Q, int(cal["n"] * 1.0 / max(1, args.steps + args.warmup) * 3)))
-    cores = cal["cores"]
+    mp = op["modes"][mode0]
+    cores = os.cpu_count() or 1
+    if torch.cuda.is_available():
+        import __graft_entry__ as ge
+
+        ge.build()
+        import paper_2603_05180_b200 as crisp
+
+        w = synth.Workload(cfg, device="cuda")
+        X = w.base(N)
+        Qd = w.queries(Q)
+        gt = ground_truth(X, Qd, k)
+        ix = crisp.Index.build(X, op["M"], K=50, seed=op.get("seed", 1))
+        del X
+        torch.cuda.empty_cache()
+        ox = oracle_index_of(ix)
+        ix.free()
+        src = "the index the GPU arm searches (crisp_build, exported; build not timed)"
+    else:  # CPU-only host (tests): the oracle builds its own index
+        w = synth.Workload(cfg)
+        X = w.base(N)
+        Qd = w.queries(Q)
+        gt = None
+        ox = oracle.build(X.numpy(), op["M"], K=50, kmeans_iters=20, kmeans_sample=100000, seed=op.get("seed", 1))
+        src = "built by the oracle (not timed)"
+    Qh = Qd.cpu().numpy()
+    B, tau = oracle.budget_ids(mp["beta"], N), oracle.tau_int(mp["alpha"], op["M"])
+    kw = dict(patience_factor=mp.get("patience_factor", 40), adsampling=mode0 == 2)
+    # per step: a bounded sample sized so the whole run takes ~args.cpu_seconds
+    nq = min(32, Q)
+    t0 = time.perf_counter()
+    oracle.search(ox, Qh[:nq], k, phi(mode0), B, tau, nthreads=cores, **kw)
+    per_q = (time.perf_counter() - t0) / nq
+    per_step = max(1, min(Q, int(args.cpu_seconds / max(per_q, 1e-7) / max(1, args.steps + args.warmup))))
     for s in range(args.warmup):
-        oracle.search(ox, Qh[:per_step], k, phi(op["mode"]), B, tau, nthreads=cores, adsampling=op["mode"] == 2)
+        oracle.search(ox, Qh[:per_step], k, phi(mode0), B, tau, nthreads=cores, **kw)
     t0 = time.perf_counter()
     res = []
     for s in range(args.steps):
         lo = (s * per_step) % max(1, Q - per_step + 1)
-        ids, _, _ = oracle.search(ox, Qh[lo:lo + per_step], k, phi(op["mode"]), B, tau, nthreads=cores,
-                                  adsampling=op["mode"] == 2)
+        ids, _, _ = oracle.search(ox, Qh[lo:lo + per_step], k, phi(mode0), B, tau, nthreads=cores, **kw)
         res.append((lo, ids))
     dt = time.perf_counter() - t0
     qps = per_step * args.steps / dt
     rec = None
     if gt is not None:
         rec = float(np.mean([recall_at(ids, gt[lo:lo + per_step], 10) for lo, ids in res]))
-    sample = f"{per_step} queries per step x {args.steps} steps of {c['name']} (oracle index built on all N={N})"
+    sample = (f"{per_step} queries per step x {args.steps} steps of {c['name']} (N={N}); oracle index = {src}")
     line = {
         "impl": "reference", "metric": "QPS at recall@10>=0.9", "value": qps, "unit": "queries/s", "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": c["name"], "N": N, "D": c["D"], "Q": Q, "k": k, "M": op["M"], "beta": op["beta"],
-                   "alpha": op["alpha"], "mode": MODE_NAMES[op["mode"]]},
+        "config": {"workload": c["name"], "N": N, "D": D, "Q": Q, "k": k, "M": op["M"], "beta": mp["beta"],
+                   "alpha": mp["alpha"], "mode": MODE_NAMES[mode0]},
         "recall@10": rec,
-        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "host": cpu_info()},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -302,24 +383,30 @@ def run_crisp(args):
             oi, _ = cdist.search_step_exact(engine, Qd, k, phi(mode), stream)
             return oi
 
-        for _ in range(args.warmup):
-            out = step()
-        torch.cuda.synchronize()
-        crisp.stage_times(reset=True)
-        crisp.search_counters(reset=True)
-        crisp.set_stage_timing(True)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # the clock sampler starts before the warm-up (nvidia-smi needs ~0.5 s to
+        # report) and its summary keeps only the samples of the timed region
         with Clocks(local) as clk:
+            for _ in range(args.warmup):
+                out = step()
+            torch.cuda.synchronize()
+            crisp.stage_times(reset=True)
+            crisp.search_counters(reset=True)
+            crisp.set_stage_timing(True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
+            t_h0 = time.time()
             e0.record()
             for _ in range(K):
                 out = step()
             e1.record()
             torch.cuda.synchronize()
+            t_h1 = time.time()
             if world > 1:
                 dist.barrier()
+            clk.mark(t_h0, t_h1)
+            time.sleep(0.3)  # let the sample of the region's last 200 ms arrive
         ms = e0.elapsed_time(e1)
         st = crisp.stage_times(reset=True)
         cnt = crisp.search_counters(reset=True)
@@ -444,21 +531,22 @@ def run_crisp(args):
                "d2h_bytes_per_step": Q * k * 8, "recall@10": recall_at(ih.numpy(), gt, 10) if rank == 0 else None,
                "api": "dist.search_step_exact (host queries on every rank, merged ids to rank 0's host)"}
 
-    # cpu baseline (rank 0, N=1 only): the oracle as it stands on the host cores
+    # cpu baseline (rank 0, N=1 only): the oracle's search as it stands on the
+    # host cores, on the index the GPU searched (oracle_index_of)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
 
-        opx = dict(op, mode=head, **op["modes"][head])
-        Xh, Qh = X.cpu().numpy(), Qd.cpu().numpy()
-        ox, (B, tau), cal = oracle_qps(Xh, Qh, opx, k, budget_seconds=args.cpu_seconds)
-        n = cal["n"]
-        t0 = time.perf_counter()
-        oracle.search(ox, Qh[:n], k, phi(head), B, tau, nthreads=cal["cores"], adsampling=head == 2)
-        dt = time.perf_counter() - t0
-        cpu = {"value": n / dt, "unit": "queries/s", "cores": cal["cores"], "kind": "oracle",
-               "sample": f"first {n} of the {Q} queries ({MODE_NAMES[head]} mode), oracle index "
-                         f"built on all N={N} (build {cal['build_s']:.0f}s, not timed)"}
+        mp = op["modes"][head]
+        del X
+        torch.cuda.empty_cache()
+        ox = oracle_index_of(index)
+        B, tau = oracle.budget_ids(mp["beta"], N), oracle.tau_int(mp["alpha"], M)
+        cpu = time_oracle(ox, Qd.cpu().numpy(), k, head, B, tau, budget_seconds=args.cpu_seconds,
+                          patience_factor=mp.get("patience_factor", 40))
+        cpu["sample"] = (f"first {cpu['queries']} of the {Q} queries ({MODE_NAMES[head]} mode, all {cpu['cores']} "
+                         f"host threads); single thread on the first {cpu['single_thread']['queries']}; oracle "
+                         f"index = the GPU index's exported arrays (X', R, codebooks, CSR, codes)")
         del ox
 
     if rank == 0:
@@ -553,7 +641,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="crisp", choices=["crisp", "reference"])
-    ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--cfg", type=int, default=4)
     ap.add_argument("--mode", type=int, default=None)
     ap.add_argument("--N", type=int, default=None)
     ap.add_argument("--Q", type=int, default=None)

@@ -67,7 +67,7 @@ typedef struct {
     double min_collision_ratio;/* alpha: tau = ceil(alpha*M) (range 0.1-0.6 P:L525) */
     int32_t tau;               /* if > 0 overrides alpha: integer collision threshold */
     int32_t patience_factor;   /* P = patience_factor * k (default 40); 0 = disabled */
-    int64_t workspace_bytes;   /* per-search scratch cap (query chunking); 0 = default 4 GiB */
+    int64_t workspace_bytes;   /* per-search scratch cap (query chunking); 0 = default: half the free device memory, in [4, 64] GiB */
 } crisp_params;
 
 typedef struct {
@@ -150,9 +150,13 @@ crisp_status crisp_local_cell_sizes(const crisp_index *idx, int64_t *sizes);
  * walk of a2 then activates exactly the cells a single global index would. */
 crisp_status crisp_set_global_cell_sizes(crisp_index *idx, const int64_t *sizes);
 
-/* Set search knobs.  beta/alpha are used only when budget/tau <= 0.  B =
- * ceil(beta*N_global), tau = max(1, ceil(alpha*M)) with a 1e-9 relative snap to
- * the nearest integer (decimal inputs such as 0.035*20000 give 700). */
+/* Set search knobs.  beta/alpha are used only when budget/tau <= 0:
+ * B = max(1, ceil(beta*N_global)) ("retrieve beta of the dataset per
+ * subspace"; Z1/Z3) and tau = max(1, ceil(alpha*M)) (Thm 1's
+ * threshold alpha*M; R1), both computed exactly as crisp_exact_ceil does.  A
+ * budget given as beta follows N_global when crisp_set_global_cell_sizes
+ * changes it; an integer budget is kept as given.  EINVAL: beta or alpha
+ * outside (0, 1] when used, patience_factor < 0. */
 crisp_status crisp_set_search_params(crisp_index *idx, double beta, int64_t budget, double alpha, int32_t tau,
                                      int32_t patience_factor);
 
@@ -236,6 +240,14 @@ crisp_status crisp_stage_times(double *ms, int32_t n, int32_t reset);
  * launched by searches/merges on the calling thread (counted always).  Up to n
  * entries are written; reset != 0 clears them. */
 crisp_status crisp_search_counters(int64_t *out, int32_t n, int32_t reset);
+
+/* ceil(ratio * n) with ratio read as the decimal it was written as: the
+ * shortest decimal string that rounds to `ratio` (what printf("%.17g")-free
+ * languages print, e.g. 0.035), multiplied exactly in 128-bit integers
+ * (floating ceil(0.035*20000) = 701, exact 700; ceil(0.07*100)
+ * = 8, exact 7).  Returns 0 for ratio <= 0, a non-finite ratio or n <= 0.
+ * Host-only; no device needed. */
+int64_t crisp_exact_ceil(double ratio, int64_t n);
 
 void crisp_free(crisp_index *idx);
 const char *crisp_last_error(void);

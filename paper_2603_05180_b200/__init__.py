@@ -64,7 +64,7 @@ ABI_SYMBOLS = (
     "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
     "crisp_set_stage_timing", "crisp_stage_times", "crisp_search_counters", "crisp_free", "crisp_last_error", "crisp_version",
     "crisp_shard_search_begin", "crisp_shard_search_hist", "crisp_shard_search_finish", "crisp_shard_search_free",
-    "crisp_set_adsampling",
+    "crisp_set_adsampling", "crisp_exact_ceil",
 )
 
 _lib = None
@@ -106,6 +106,8 @@ def lib():
         L.crisp_free.restype = None
         L.crisp_last_error.restype = C.c_char_p
         L.crisp_version.restype = C.c_char_p
+        L.crisp_exact_ceil.argtypes = [f64, i64]
+        L.crisp_exact_ceil.restype = i64
         _lib = L
     return _lib
 
@@ -124,15 +126,40 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def _host(a, dtype):
+_TORCH_DT = {np.float32: "float32", np.int64: "int64", np.float64: "float64", np.int32: "int32"}
+
+
+def _host(a, dtype, ndim=2):  # ndim None: any rank
+    """numpy: a C-contiguous copy/view of the given dtype.  torch: the tensor
+    itself after checking that the library can read it as packed row-major
+    `dtype` (the C ABI takes raw pointers, so a wrong dtype, a strided view or
+    a wrong rank would be misread)."""
     if hasattr(a, "data_ptr"):
+        want = _TORCH_DT[dtype]
+        if str(a.dtype) != "torch." + want:
+            raise CrispError(f"tensor dtype {a.dtype}, expected torch.{want}")
+        if not a.is_contiguous():
+            raise CrispError("tensor must be contiguous (row-major)")
+        if ndim is not None and a.dim() != ndim:
+            raise CrispError(f"tensor must have {ndim} dimensions, got {a.dim()}")
         return a
     return np.ascontiguousarray(a, dtype=dtype)
 
 
 def exact_ceil(ratio, n: int) -> int:
-    """ceil(ratio*n) with ratio read as the decimal it was written as (O1)."""
-    return int(math.ceil(Fraction(str(ratio)) * n))
+    """crisp_exact_ceil: ceil(ratio*n) with ratio read as the shortest decimal
+    that rounds to it (the library's rule for B and tau)."""
+    return int(lib().crisp_exact_ceil(float(ratio), int(n)))
+
+
+def _dev(t, dtype, shape=None, what="tensor"):
+    """A device tensor handed to a *_async call: CUDA, dtype, contiguous, shape."""
+    if not hasattr(t, "data_ptr") or not t.is_cuda:
+        raise CrispError(f"{what} must be a CUDA tensor")
+    _host(t, dtype, None if shape is None else len(shape))
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise CrispError(f"{what} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return t
 
 
 def default_params(**kw) -> Params:
@@ -171,11 +198,11 @@ class Index:
         out = C.c_void_p()
         if gid_base is not None:
             Rh = _host(R, np.float32) if R is not None else None
-            cbh = _host(codebooks, np.float32)
+            cbh = _host(codebooks, np.float32, None)
             _check(lib().crisp_build_shard(_ptr(x), N, gid_base, D, C.byref(p), _ptr(Rh), _ptr(cbh), C.byref(out)))
         elif R is not None or codebooks is not None:
             Rh = _host(R, np.float32) if R is not None else None
-            cbh = _host(codebooks, np.float32)
+            cbh = _host(codebooks, np.float32, None)
             _check(lib().crisp_build_with(_ptr(x), N, D, C.byref(p), _ptr(Rh), _ptr(cbh), C.byref(out)))
         else:
             _check(lib().crisp_build(_ptr(x), N, D, C.byref(p), C.byref(out)))
@@ -199,12 +226,12 @@ class Index:
         return {n: getattr(i, n) for n, _ in Info._fields_}
 
     def set_search_params(self, beta=None, budget=None, alpha=None, tau=None, patience_factor=40):
-        """B = ceil(beta*N_global) and tau = ceil(alpha*M) are computed exactly
-        here (decimal semantics) and passed as integers."""
-        info = self.info()
-        B = budget if budget else max(1, exact_ceil(beta if beta is not None else 0.01, info["N_global"]))
-        T = tau if tau else max(1, exact_ceil(alpha if alpha is not None else 0.3, info["M"]))
-        _check(lib().crisp_set_search_params(self._h, 0.0, int(B), 0.0, int(T), int(patience_factor)))
+        """crisp_set_search_params: the library derives B = ceil(beta*N_global)
+        and tau = ceil(alpha*M) from the ratios (decimal semantics, SURVEY 8(c)
+        O1) unless the integers are given."""
+        _check(lib().crisp_set_search_params(self._h, float(beta if beta is not None else 0.01), int(budget or 0),
+                                             float(alpha if alpha is not None else 0.3), int(tau or 0),
+                                             int(patience_factor)))
 
     def set_adsampling(self, enable: bool = True, eps0: float = 2.1, stride: int = 32):
         """crisp_set_adsampling: Optimized Mode verification by ADSampling (Eq. 2)."""
@@ -238,10 +265,19 @@ class Index:
 
     def search_async(self, q_dev, k: int, mode: int, ids_dev, d_dev, stream_ptr: int = 0):
         """crisp_search_async on device tensors; stream_ptr = torch stream.cuda_stream."""
+        Q = int(q_dev.shape[0])
+        _dev(q_dev, np.float32, None, "queries")
+        _dev(ids_dev, np.int64, (Q, k), "ids")
+        if d_dev is not None:
+            _dev(d_dev, np.float32, (Q, k), "distances")
         _check(lib().crisp_search_async(self._h, _ptr(q_dev), int(q_dev.shape[0]), k, mode, _ptr(ids_dev),
                                         _ptr(d_dev), C.c_void_p(stream_ptr)))
 
     def search_shard_async(self, q_dev, k: int, mode: int, ids_dev, d64_dev, stream_ptr: int = 0):
+        Q = int(q_dev.shape[0])
+        _dev(q_dev, np.float32, None, "queries")
+        _dev(ids_dev, np.int64, (Q, k), "ids")
+        _dev(d64_dev, np.float64, (Q, k), "distances")
         _check(lib().crisp_search_shard_async(self._h, _ptr(q_dev), int(q_dev.shape[0]), k, mode, _ptr(ids_dev),
                                               _ptr(d64_dev), C.c_void_p(stream_ptr)))
 

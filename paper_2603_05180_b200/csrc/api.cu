@@ -23,26 +23,55 @@ bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-// ceil(ratio * n) with a 1e-9 relative snap to the nearest integer, so that
-// decimal inputs give the decimal answer (0.035 * 20000 -> 700).
-int64_t snap_ceil(double ratio, int64_t n) {
-    long double x = (long double)ratio * (long double)n;
-    long double r = nearbyintl(x);
-    long double tol = 1e-9L * std::max<long double>(1.0L, fabsl(x));
-    if (fabsl(x - r) <= tol) return (int64_t)r;
-    return (int64_t)ceill(x);
+// ceil(ratio * n) with ratio read as the decimal it was written as (SURVEY
+// 8(c) O1: B = ceil(beta N), tau = ceil(alpha M) "computed exactly: parse beta and
+// alpha as decimal rationals").  The decimal is the shortest one that rounds to
+// the given double (the repr a user types and a language prints: 0.035, not
+// 0.035000000000000003), found by trying 1..17 significant digits; then
+// ceil(mant * 10^e10 * n) in 128-bit integers.  0.035 * 20000 -> 700 and
+// 0.07 * 100 -> 7, where the binary product rounds to 701 and 8.
+int64_t decimal_ceil(double ratio, int64_t n) {
+    if (!(ratio > 0.0) || !std::isfinite(ratio) || n <= 0) return 0;
+    char buf[64];
+    int prec = 1;
+    for (; prec <= 17; prec++) {
+        snprintf(buf, sizeof buf, "%.*e", prec - 1, ratio);
+        if (strtod(buf, nullptr) == ratio) break;
+    }
+    // buf = d.ddd...e[+-]XX : mantissa digits and the decimal exponent
+    __int128 mant = 0;
+    int ndig = 0, e10 = 0;
+    const char *c = buf;
+    for (; *c && *c != 'e'; c++)
+        if (*c >= '0' && *c <= '9') {
+            mant = mant * 10 + (*c - '0');
+            ndig++;
+        }
+    if (*c == 'e') e10 = atoi(c + 1);
+    int scale = e10 - (ndig - 1);  // ratio = mant * 10^scale
+    __int128 num = mant * (__int128)n;
+    if (scale >= 0) {
+        for (int i = 0; i < scale; i++) num *= 10;
+        return (int64_t)num;
+    }
+    __int128 den = 1;
+    for (int i = 0; i < -scale; i++) den *= 10;
+    return (int64_t)((num + den - 1) / den);
 }
 
 static void apply_knobs(crisp_index *ix, double beta, int64_t budget, double alpha, int32_t tau, int32_t pf) {
-    if (budget > 0) ix->budget = budget;
-    else {
+    if (budget > 0) {
+        ix->budget = budget;
+        ix->beta = 0.0;
+    } else {
         CRISP_CHECK(beta > 0.0 && beta <= 1.0, "budget_ratio must be in (0, 1]");
-        ix->budget = std::max<int64_t>(1, snap_ceil(beta, ix->N_global));
+        ix->beta = beta;  // re-derived when the global cell sizes (N_global) change
+        ix->budget = std::max<int64_t>(1, decimal_ceil(beta, ix->N_global));
     }
     if (tau > 0) ix->tau = tau;
     else {
         CRISP_CHECK(alpha > 0.0 && alpha <= 1.0, "min_collision_ratio must be in (0, 1]");
-        ix->tau = (int32_t)std::max<int64_t>(1, snap_ceil(alpha, ix->M));
+        ix->tau = (int32_t)std::max<int64_t>(1, decimal_ceil(alpha, ix->M));
     }
     CRISP_CHECK(pf >= 0, "patience_factor must be >= 0");
     ix->patience_factor = pf;
@@ -199,7 +228,9 @@ using namespace crisp;
 extern "C" {
 
 const char *crisp_last_error(void) { return g_err.c_str(); }
-const char *crisp_version(void) { return "crisp-b200 0.1 (sm_100a)"; }
+const char *crisp_version(void) { return "crisp-b200 0.2 (sm_100a)"; }
+
+int64_t crisp_exact_ceil(double ratio, int64_t n) { return decimal_ceil(ratio, n); }
 
 crisp_status crisp_default_params(crisp_params *p) {
     if (!p) {
@@ -279,6 +310,9 @@ crisp_status crisp_set_global_cell_sizes(crisp_index *ix, const int64_t *sizes) 
         CRISP_CUDA(cudaMemcpy(ix->gsize, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
         ix->N_global = n0;
         ix->slice_hint = slice_hint_of(h.data(), ix->M, KK, n0, ix->SBW);
+        cell_size_maxima(ix, h.data());
+        // a budget given as a ratio follows N_global (B = ceil(beta N_global), O1)
+        if (ix->beta > 0.0) ix->budget = std::max<int64_t>(1, decimal_ceil(ix->beta, ix->N_global));
         return CRISP_OK;
     } catch (Err &e) {
         return e.st;
@@ -362,6 +396,11 @@ static crisp_status search_impl(const crisp_index *ix, const float *queries, int
             search(ix, queries, Q, k, (int)mode, so, s, tr);
             return CRISP_OK;
         }
+        // synchronous call: device arguments may still be written by work the
+        // caller queued on any stream (the search runs on its own non-blocking
+        // stream), so order it after all of it, as crisp_build does
+        if (is_device_ptr(queries) || is_device_ptr(out_ids) || (out_d && is_device_ptr(out_d)))
+            CRISP_CUDA(cudaDeviceSynchronize());
         // host buffers: stream-ordered device staging (H2D in, D2H out)
         cudaStream_t st;
         CRISP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));

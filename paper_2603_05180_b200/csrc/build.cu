@@ -959,8 +959,20 @@ void finish_csr(crisp_index *ix, cudaStream_t s) {
         CRISP_CUDA(cudaMemcpyAsync(h.data(), ix->gsize, h.size() * 4, cudaMemcpyDeviceToHost, s));
         CRISP_CUDA(cudaStreamSynchronize(s));
         ix->slice_hint = slice_hint_of(h.data(), M, KK, ix->N_global, ix->SBW);
+        cell_size_maxima(ix, h.data());
     }
     CRISP_CUDA(cudaStreamSynchronize(s));
+}
+
+void cell_size_maxima(crisp_index *ix, const int32_t *sizes) {
+    const int64_t KK = (int64_t)ix->K * ix->K;
+    int64_t tot = 0;
+    for (int m = 0; m < ix->M; m++) {
+        int32_t mx = 0;
+        for (int64_t c = 0; c < KK; c++) mx = std::max(mx, sizes[m * KK + c]);
+        tot += mx;
+    }
+    ix->maxcell_sum = tot;
 }
 
 double slice_hint_of(const int32_t *sizes, int M, int64_t KK, int64_t N_global, int SBW) {

@@ -79,6 +79,8 @@ struct crisp_index {
     int32_t SBW = 0, NBW = 0;  // warp sub-block: ids per sub-block (BS/8), number of sub-blocks (8*NB)
     double slice_hint = 0.0;   // expected ids of a query's activated slice per warp sub-block (count kernel choice)
     int64_t budget = 0;
+    double beta = 0.0;         // the ratio the budget came from (0: given as an integer)
+    int64_t maxcell_sum = 0;   // sum over subspaces of the largest (global) cell size: bounds R_qm - B
     int32_t tau = 1, patience_factor = 40;
     int32_t ad_on = 0, ad_stride = 32;  // Optimized Mode ADSampling (crisp_set_adsampling)
     double ad_eps0 = 2.1;
@@ -95,7 +97,9 @@ double slice_hint_of(const int32_t *sizes_host, int M, int64_t KK, int64_t N_glo
 // helpers implemented in api.cu
 void *dmalloc(size_t bytes, crisp_index *ix);
 bool is_device_ptr(const void *p);
-int64_t snap_ceil(double ratio, int64_t n);
+int64_t decimal_ceil(double ratio, int64_t n);
+// per-subspace largest cell size (global sizes, host M x K^2) -> ix->maxcell (exact candidate bound)
+void cell_size_maxima(crisp_index *ix, const int32_t *sizes_host);
 
 // build steps (build.cu)
 void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, const float *cb_inj, int64_t kmeans_sample,

@@ -798,6 +798,240 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
 }
 
 // ---------------------------------------------------------------------------
+// a3 + a4, fragment-flattened counting (the small-cell regime: many activated
+// cells per query, each contributing a short run of ids to every id block).
+// A CTA owns one query and one id block of BF = F*BS ids, whose V counters
+// (bytes, packed four to a 32-bit word) and candidate bitmap live in shared
+// memory.  For a chunk of the query's activated cells it stages each cell's
+// fragment inside the block -- [off2[c][F b], off2[c][F b + F]) of the
+// subspace's CSR ids, which holds exactly the cell's ids in the
+// block -- drops the empty ones and takes an exclusive prefix of their chunk
+// counts, so that the chunk's ids form one flat range of 32-id chunks (a
+// chunk = up to 32 consecutive ids of one fragment, one per lane: its load is
+// coalesced).  Warps take tasks of CF_TF consecutive fragments from a shared
+// counter; a chunk's fragment is found by one ballot over the task's
+// fragments held in the lanes, and each lane adds the weight w (Alg. 1
+// l.10-12) of its id with one shared atomic on the counter's word.  The same id can recur only
+// across subspaces (CSR partition property), and shared atomics order
+// those, so no barrier separates subspaces.  V only grows, by 1 or 2, so x
+// enters C = {x : V[x] >= tau} (Alg. 1 l.18) exactly at the increment that
+// lifts its count from below tau to tau or more; that increment sets x's bit
+// in the candidate bitmap, which the CTA finally writes out in ascending id.
+// ---------------------------------------------------------------------------
+constexpr int CF_WARPS = 16;
+constexpr int CF_THREADS = CF_WARPS * 32;
+constexpr int CF_CAP = 2048;  // fragments staged per chunk
+constexpr int CF_EPT = CF_CAP / CF_THREADS;
+constexpr int CF_U = 4;       // 32-position batches with loads in flight per warp
+constexpr int CF_TF = 8;      // fragments per task (<= 32)
+
+struct CountFSmem {
+    int4 tab[CF_CAP + 40];  // staged non-empty fragments: (chunk prefix, ids[] index | WFLAG, length, -); padded
+    int32_t lpre[MAX_M + 2];
+    int32_t wtot[CF_WARPS];
+    long long wtot64[CF_WARPS];
+    int next, total, base;
+};
+__host__ __device__ constexpr size_t countf_smem(int BF) {  // counters, bitmap, CountFSmem
+    return (size_t)BF + (size_t)BF / 8 + ((sizeof(CountFSmem) + 15) & ~(size_t)15);
+}
+
+__global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__restrict__ act,
+                                                               const int32_t *__restrict__ act_len, int M, int KK,
+                                                               const int32_t *__restrict__ off2, int NB, int F,
+                                                               const int32_t *__restrict__ ids, int64_t N, int BS,
+                                                               int NS, int tau, int32_t *__restrict__ pool,
+                                                               int64_t CAPQ, int32_t *__restrict__ cursor,
+                                                               int32_t *__restrict__ cbase,
+                                                               int32_t *__restrict__ ncand, int32_t *__restrict__ need,
+                                                               uint8_t *__restrict__ traceV,
+                                                               const int32_t *__restrict__ qperm) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int BF = BS * F;
+    uint32_t *cw = (uint32_t *)smraw;              // BF byte counters, 4 per word
+    uint32_t *bm = (uint32_t *)(smraw + BF);       // BF-bit candidate bitmap
+    CountFSmem &S = *(CountFSmem *)(smraw + BF + BF / 8);
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
+    const int sb = blockIdx.x;                                 // id block [sb*BF, (sb+1)*BF)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t bbase = (uint32_t)sb * (uint32_t)BF;
+    const int c0 = sb * F, c1 = min(NB, c0 + F);  // off2 columns bounding the block
+    if (warp == 0) {
+        int acc = 0;
+        for (int m0 = 0; m0 < M; m0 += 32) {
+            const int m = m0 + lane;
+            int v = m < M ? __ldg(act_len + q * M + m) : 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += t;
+            }
+            if (m < M) S.lpre[m + 1] = acc + v;
+            acc += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (lane == 0) S.lpre[0] = 0;
+    }
+    for (int i = tid; i < (BF + BF / 8) / 16; i += CF_THREADS) ((uint4 *)smraw)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int Etot = S.lpre[M];
+    const uint32_t *actq = act + q * (int64_t)M * KK;
+    const uint32_t taum1 = (uint32_t)tau - 1u;
+    for (int e0 = 0; e0 < Etot; e0 += CF_CAP) {
+        const int ne = min(CF_CAP, Etot - e0);
+        // stage this chunk's fragments: warp w takes entries [w*32*CF_EPT, (w+1)*32*CF_EPT) of the
+        // chunk, lane l the entries w*32*CF_EPT + 32u + l; the loads of a thread's entries are
+        // issued together (entry -> act word -> off2 pair), then a warp scan of the packed
+        // (length, non-empty) values, one barrier for the warp totals, the scatter of the
+        // non-empty fragments (their order in the table is immaterial: the counts commute)
+        const int W0 = warp * 32 * CF_EPT;
+        const uint32_t *aadr[CF_EPT];
+        int mrow[CF_EPT];
+#pragma unroll
+        for (int u = 0; u < CF_EPT; u++) {
+            const int t = W0 + 32 * u + lane;
+            const int e = e0 + min(t, ne - 1);
+            const int m = m_of_entry(S.lpre, M, e);
+            mrow[u] = m;
+            aadr[u] = actq + (int64_t)m * KK + (e - S.lpre[m]);
+        }
+        uint32_t av[CF_EPT];
+#pragma unroll
+        for (int u = 0; u < CF_EPT; u++) av[u] = (W0 + 32 * u + lane < ne) ? __ldg(aadr[u]) : 0u;
+        int s0[CF_EPT], s1[CF_EPT];
+#pragma unroll
+        for (int u = 0; u < CF_EPT; u++) {
+            const int32_t *o = off2 + ((int64_t)mrow[u] * KK + (int)(av[u] & 0xffffu)) * (NB + 1);
+            const bool ok = W0 + 32 * u + lane < ne;
+            s0[u] = ok ? __ldg(o + c0) : 0;
+            s1[u] = ok ? __ldg(o + c1) : 0;
+        }
+        long long v[CF_EPT], ex[CF_EPT], carry = 0;
+#pragma unroll
+        for (int u = 0; u < CF_EPT; u++) {
+            const int len = s1[u] - s0[u];
+            // (32-id chunks, non-empty) packed for one scan
+            v[u] = len > 0 ? (((long long)((len + 31) >> 5) << 16) | 1) : 0;
+            long long x = v[u];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, x, off);
+                if (lane >= off) x += y;
+            }
+            ex[u] = carry + x - v[u];
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) S.wtot64[warp] = carry;
+        if (tid == 0) S.next = 0;
+        __syncthreads();
+        long long wpre = 0, tot = 0;
+        for (int w2 = 0; w2 < CF_WARPS; w2++) {
+            const long long t = S.wtot64[w2];
+            wpre += w2 < warp ? t : 0;
+            tot += t;
+        }
+        const int NC = (int)(tot >> 16), nnz = (int)(tot & 0xffff);  // chunks, non-empty fragments
+#pragma unroll
+        for (int u = 0; u < CF_EPT; u++)
+            if (v[u]) {
+                const long long xx = wpre + ex[u];
+                S.tab[(int)(xx & 0xffff)] =
+                    make_int4((int)(xx >> 16),
+                              (int)((uint32_t)(mrow[u] * (int)N + s0[u]) | ((av[u] >> 16) == 2u ? WFLAG : 0u)),
+                              s1[u] - s0[u], 0);
+            }
+        if (tid < 40) S.tab[nnz + tid] = make_int4(tid == 0 ? NC : 0x7fffffff, 0, 0, 0);
+        __syncthreads();
+        // Tasks of CF_TF consecutive fragments (their chunks [tab[f0].x, tab[f0+CF_TF].x)).  A
+        // chunk is up to 32 consecutive ids of one fragment, one per lane; its fragment is
+        // found with one ballot over the task's fragments held in lanes 0..CF_TF-1 (chunk
+        // prefixes strictly increase: no empty fragments).
+        for (;;) {
+            int task = 0;
+            if (lane == 0) task = atomicAdd(&S.next, 1);
+            task = __shfl_sync(0xffffffffu, task, 0);
+            const int f0 = task * CF_TF;
+            if (f0 >= nnz) break;
+            const int4 te = lane < CF_TF ? S.tab[f0 + lane] : make_int4(0x7fffffff, 0, 0, 0);
+            const int C0 = __shfl_sync(0xffffffffu, te.x, 0);
+            const int C1 = S.tab[min(f0 + CF_TF, nnz)].x;  // tab[nnz].x = NC
+            for (int c0 = C0; c0 < C1; c0 += CF_U) {
+                uint32_t addr[CF_U], inc[CF_U];
+#pragma unroll
+                for (int u = 0; u < CF_U; u++) {
+                    const int c = c0 + u;
+                    const int j = max(0, __popc(__ballot_sync(0xffffffffu, te.x <= c)) - 1);
+                    const int cx = __shfl_sync(0xffffffffu, te.x, j);
+                    const int gj = __shfl_sync(0xffffffffu, te.y, j);
+                    const int lj = __shfl_sync(0xffffffffu, te.z, j);
+                    const int o = ((c - cx) << 5) + lane;
+                    const bool ok = c < C1 && o < lj;
+                    addr[u] = ((uint32_t)gj & ~WFLAG) + (ok ? (uint32_t)o : 0u);
+                    inc[u] = ok ? 1u + ((uint32_t)gj >> 31) : 0u;
+                }
+                uint32_t x[CF_U];
+#pragma unroll
+                for (int u = 0; u < CF_U; u++) x[u] = (uint32_t)__ldg(ids + addr[u]);
+#pragma unroll
+                for (int u = 0; u < CF_U; u++)
+                    if (inc[u]) {
+                        const uint32_t off = x[u] - bbase, sh = (off & 3u) * 8u;
+                        const uint32_t ov = (atomicAdd(cw + (off >> 2), inc[u] << sh) >> sh) & 0xffu;
+                        if (taum1 - ov < inc[u]) atomicOr(bm + (off >> 5), 1u << (off & 31));  // ov < tau <= ov+inc
+                    }
+            }
+        }
+        __syncthreads();  // the chunk's table is re-staged next
+    }
+    // a4: C in ascending id from the bitmap; each warp compacts a contiguous word range
+    const int nwords = BF / 32, wpw = nwords / CF_WARPS;
+    {
+        int c = 0;
+        for (int i = lane; i < wpw; i += 32) c += __popc(bm[warp * wpw + i]);
+#pragma unroll
+        for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+        if (lane == 0) S.wtot[warp] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int n = 0;
+        for (int w2 = 0; w2 < CF_WARPS; w2++) n += S.wtot[w2];
+        const int base = atomicAdd(cursor + q, n);
+        S.base = base;
+        cbase[q * NS + sb] = base;
+        ncand[q * NS + sb] = n;
+        if ((int64_t)base + n > CAPQ) atomicMax(need, base + n);
+    }
+    __syncthreads();
+    int running = S.base;
+    for (int w2 = 0; w2 < warp; w2++) running += S.wtot[w2];
+    int32_t *outp = pool + q * CAPQ;
+    for (int i0 = 0; i0 < wpw; i0 += 32) {
+        const int i = i0 + lane;
+        uint32_t word = i < wpw ? bm[warp * wpw + i] : 0u;
+        const int c = __popc(word);
+        int inc = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += t;
+        }
+        int o = running + inc - c;
+        const int g0 = (int)bbase + (warp * wpw + i) * 32;
+        while (word) {
+            if (o < CAPQ) outp[o] = g0 + __ffs(word) - 1;
+            o++;
+            word &= word - 1;
+        }
+        running += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (traceV) {
+        const unsigned char *c8 = (const unsigned char *)cw;
+        for (int j = tid; j < BF; j += CF_THREADS)
+            if ((int64_t)bbase + j < N) traceV[q * N + (int64_t)bbase + j] = c8[j];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // a4 fallback (Z8): |C| < k -> the first min(k,|T|) touched ids by
 // (V desc, id asc), restated in ascending id.  Rare; one CTA per query,
 // counting every block twice (histogram of V, then selection).  For a sharded
@@ -2414,6 +2648,7 @@ static void set_attrs() {
     if (done) return;
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_frag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -2444,7 +2679,7 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
-    int S, S1, HS, S0, R0, BPC, count_kernel, count_atom, NS, ham_fused, rows4, ad, adsp, F, DS, round_rows, nl_min, Pq,
+    int S, S1, HS, S0, R0, BPC, count_kernel, count_atom, NS, CF, ham_fused, rows4, ad, adsp, F, DS, round_rows, nl_min, Pq,
         vra_smem;
     // end of the speculative rounds (positions the Hamming order must cover)
     // positions k_hsort orders (the rounds stop there; k_patience_tail completes the
@@ -2519,8 +2754,14 @@ struct Work {
         BPC = std::max(1, std::min(NB, env_int("CRISP_COUNT_BPC", 16)));  // id blocks per count CTA
         // 0: k_count_select (CTA-flattened slices, for many small cells), 1: k_count_warp
         // (warp-owned sub-blocks, for slices of >= 8 ids per sub-block); env overrides
-        count_kernel = env_int("CRISP_COUNT_KERNEL", ix->slice_hint >= 8.0 ? 1 : 0);
-        NS = count_kernel == 0 ? NB : ix->NBW;  // candidate segments per query (id blocks or sub-blocks)
+        // 0: k_count_select (CTA-flattened slices, subspace by subspace; kept for comparison),
+        // 1: k_count_warp (warp-owned sub-blocks, for slices of >= 8 ids per sub-block),
+        // 2: k_count_frag (fragment-flattened, shared atomics; the small-cell regime)
+        count_kernel = env_int("CRISP_COUNT_KERNEL", ix->slice_hint >= 8.0 ? 1 : 2);
+        CF = std::max(1, std::min(std::min(NB, 4), env_int("CRISP_COUNT_F", 2)));  // k_count_frag: BS ids x CF per CTA
+        while (CF > 1 && countf_smem(BS * CF) > 200 * 1024) CF--;
+        // candidate segments per query (id blocks, warp sub-blocks, or frag blocks)
+        NS = count_kernel == 0 ? NB : count_kernel == 1 ? ix->NBW : (NB + CF - 1) / CF;
         count_atom = env_int("CRISP_COUNT_ATOM", 0);  // k_count_warp: shared atomics (else byte load/store pairs; faster)
         ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
         // row kernels: four rows per warp step for rows up to 4 KB (measured: faster at D=960, slower at 4096)
@@ -2662,7 +2903,11 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
         CRISP_CUDA(cudaMemsetAsync(w.cursor, 0, (size_t)(w.Qc + 1) * 4, s));
         if (w.mode == 1) CRISP_CUDA(cudaMemsetAsync(w.ghist, 0, (size_t)qn * (ix->Dp + 1) * 4, s));
         dim3 g(nblk(NB, w.BPC), (unsigned)qn);
-        if (w.count_kernel == 0)
+        if (w.count_kernel == 2)
+            k_count_frag<<<dim3((unsigned)w.NS, (unsigned)qn), CF_THREADS, countf_smem(ix->BS * w.CF), s>>>(
+                w.act, w.act_len, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
+                w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm);
+        else if (w.count_kernel == 0)
             k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N,
                                                             ix->BS, w.BPC, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase,
                                                             w.ncand, w.need, w.traceV, w.qperm);
@@ -2890,21 +3135,43 @@ static void trace_rest(Work &w, int64_t q0, int64_t qn, const crisp_trace_t *tr,
     }
 }
 
-static int64_t initial_capacity(const crisp_index *ix, bool trace) {
-    const int64_t NBS = (int64_t)ix->NB * ix->BS;
-    if (trace) return NBS;
-    return std::min<int64_t>(NBS, std::max<int64_t>(4096, env_int("CRISP_CAND_CAP", 1 << 17)));
+// default per-search scratch cap: half of the device memory free at the call,
+// at least 4 GiB and at most 64 GiB (a 10k-query cfg4 batch needs ~17 GB and
+// must not be split into a full and a nearly empty chunk)
+static int64_t default_workspace() {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return 16LL << 30;
+    }
+    return std::max<int64_t>(4LL << 30, std::min<int64_t>(64LL << 30, (int64_t)(fr / 2)));
 }
 
-static int64_t grow_capacity(const crisp_index *ix, int64_t cap, int64_t need) {
-    return std::min<int64_t>((int64_t)ix->NB * ix->BS, std::max<int64_t>(cap * 2, need + need / 4));
+// Candidate capacity per query: an exact upper bound of |C_q| known before the
+// search, so that crisp_search_async never reads anything back (no host sync).
+// Every x in C has V[x] >= tau (Alg. 1 l.18), and sum_x V[x] = sum over the
+// activated cells of w * |cell| <= wmax * sum_m R_qm with w <= 2 at phi=1 and
+// w = 1 at phi=0 (Alg. 1 l.10-12); the budget walk stops at the first cell that
+// brings R_qm to >= B (Z3), so R_qm <= B - 1 + max_c |cell_{m,c}|.  The fallback
+// (|C| < k) writes at most k.  Trace calls keep room for every id.
+static int64_t candidate_capacity(const crisp_index *ix, int mode, int k, bool trace) {
+    const int64_t all = (int64_t)ix->NB * ix->BS;
+    if (trace) return all;
+    const int64_t wmax = mode == 1 ? 2 : 1;
+    const int64_t R = (int64_t)ix->M * std::max<int64_t>(0, ix->budget - 1) + ix->maxcell_sum;
+    int64_t b = wmax * R / std::max(1, ix->tau);
+    b = std::min<int64_t>(b, ix->N);
+    b = std::max<int64_t>(b, std::min<int64_t>(k, ix->N));
+    if (const char *v = getenv("CRISP_CAND_CAP")) b = std::max<int64_t>(b, atoll(v));  // test hook (only grows)
+    return std::max<int64_t>(16, std::min(b, all));
 }
 
-// One attempt over all queries with candidate capacity CAPQ per query; returns
-// false (and the capacity needed) if some query's candidate set overflowed.
-static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
-                        cudaStream_t s, const crisp_trace_t *tr, int64_t CAPQ, int64_t *need_out, const float *hq) {
-    const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : (16LL << 30);
+// The whole batch, in query chunks that fit the workspace, with candidate
+// capacity CAPQ per query (candidate_capacity: never exceeded).  Only the trace
+// path reads back (its outputs); otherwise everything is stream-ordered on s.
+static void search_pass(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
+                        cudaStream_t s, const crisp_trace_t *tr, int64_t CAPQ, const float *hq) {
+    const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : default_workspace();
     const int64_t perq = Work::per_query_bytes(ix, k, mode, CAPQ, tr && tr->V);
     int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
     Qc = std::min<int64_t>(Qc, 65535);
@@ -2914,30 +3181,20 @@ static bool search_pass(const crisp_index *ix, const float *queries, int64_t Q, 
         const int64_t qn = std::min(Qc, Q - q0);
         run_front(w, queries + q0 * ix->D, qn, s, hq ? hq + q0 * ix->D : nullptr);
         run_fallback_local(w, qn, s);
-        const int32_t need = read_need(w, s);  // exactness guard
-        if (need > CAPQ) {
-            *need_out = need;
-            return false;
+        if (tr) {
+            CRISP_CHECK(read_need(w, s) <= CAPQ, "internal: candidate capacity exceeded");
+            trace_candidates(w, q0, qn, tr, s);
         }
-        if (tr) trace_candidates(w, q0, qn, tr, s);
         run_verify(w, qn, out.ids + q0 * k, out.d32 ? out.d32 + q0 * k : nullptr, out.d64 ? out.d64 + q0 * k : nullptr,
                    s);
         run_stats(w, qn, s);
         if (tr) trace_rest(w, q0, qn, tr, s);
     }
-    return true;
 }
 
 void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
             cudaStream_t s, const crisp_trace_t *tr, const float *queries_host) {
-    // candidate capacity per query: optimistic, grown (and the batch redone)
-    // if any query's |C_q| exceeds it, so results never depend on it
-    int64_t cap = initial_capacity(ix, tr != nullptr);
-    for (;;) {
-        int64_t need = 0;
-        if (search_pass(ix, queries, Q, k, mode, out, s, tr, cap, &need, queries_host)) return;
-        cap = grow_capacity(ix, cap, need);
-    }
+    search_pass(ix, queries, Q, k, mode, out, s, tr, candidate_capacity(ix, mode, k, tr != nullptr), queries_host);
 }
 
 // ---------------------------------------------------------------------------
@@ -2957,24 +3214,21 @@ namespace crisp {
 
 crisp_session *session_begin(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode,
                              int32_t *local_counts, cudaStream_t s) {
-    int64_t cap = initial_capacity(ix, false);
-    for (;;) {
-        Work *w = new Work(ix, k, mode, std::max<int64_t>(Q, 1), cap, false, false, s);
-        try {
-            run_front(*w, queries, Q, s);
-            const int32_t need = read_need(*w, s);
-            if (need <= cap) {
-                k_local_counts<<<nblk(Q, 256), 256, 0, s>>>(w->ncand, w->NS, Q, local_counts);
-                CRISP_LAUNCH();
-                g_launches++;
-                return new crisp_session{ix, w, Q, k, mode};
-            }
-            delete w;
-            cap = grow_capacity(ix, cap, need);
-        } catch (...) {
-            delete w;
-            throw;
-        }
+    CRISP_CHECK(Q <= 65535, "a shard session takes at most 65535 queries (split the batch)");
+    const int64_t cap = candidate_capacity(ix, mode, k, false);
+    const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : default_workspace();
+    CRISP_CHECK(Work::per_query_bytes(ix, k, mode, cap, false) * Q <= ws,
+                "shard session scratch exceeds the workspace (split the batch)");
+    Work *w = new Work(ix, k, mode, std::max<int64_t>(Q, 1), cap, false, false, s);
+    try {
+        run_front(*w, queries, Q, s);
+        k_local_counts<<<nblk(Q, 256), 256, 0, s>>>(w->ncand, w->NS, Q, local_counts);
+        CRISP_LAUNCH();
+        g_launches++;
+        return new crisp_session{ix, w, Q, k, mode};
+    } catch (...) {
+        delete w;
+        throw;
     }
 }
 

@@ -44,11 +44,24 @@ def test_default_params_no_gpu():
     assert (p.M, p.K, round(p.tau_cev, 6), p.kmeans_iters, p.patience_factor) == (8, 50, 0.85, 20, 40)
 
 
-def test_exact_parameters_binding():
+def test_exact_parameters_c_abi():
+    """B and tau are derived inside the C library (crisp_exact_ceil, the rule
+    crisp_set_search_params applies), and agree with the oracle's decimal rule
+    (O1) on the cases binary floating point gets wrong and over a grid."""
+    ge.build()
+    import oracle
     import paper_2603_05180_b200 as crisp
 
-    assert crisp.exact_ceil(0.035, 20000) == 700
-    assert crisp.exact_ceil(0.07, 100) == 7
+    assert crisp.lib().crisp_exact_ceil(0.035, 20000) == 700
+    assert crisp.lib().crisp_exact_ceil(0.07, 100) == 7
+    assert crisp.lib().crisp_exact_ceil(0.0, 10) == 0
+    for a100 in range(1, 101):
+        alpha = a100 / 100
+        for M in range(1, 128):
+            assert crisp.exact_ceil(alpha, M) == oracle.tau_int(alpha, M), (alpha, M)
+    for beta in (0.001, 0.002, 0.005, 0.01, 0.02, 0.035, 0.04, 0.06, 0.1, 0.2, 0.4, 1.0, 1e-7, 0.123456789):
+        for N in (1, 7, 20000, 1_000_000, 2_000_000, 1_281_167, 2 ** 31 - 1):
+            assert crisp.exact_ceil(beta, N) == oracle.budget_ids(beta, N), (beta, N)
 
 
 def test_sm100a_cubin_present():

@@ -103,7 +103,11 @@ def compare_trace(t, ot, mode, N):
 COUNT_VARIANTS = {"select": {"CRISP_COUNT_KERNEL": "0", "CRISP_ROWS4": "0"},
                   "warp": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "0"},
                   "warp_fused": {"CRISP_COUNT_KERNEL": "1", "CRISP_HAMMING_FUSED": "1", "CRISP_RERANK_SPLITS": "1",
-                                 "CRISP_COUNT_ATOM": "1"}}
+                                 "CRISP_COUNT_ATOM": "1"},
+                 # fragment-flattened count (the small-cell default) with 1, 2 and 4 id blocks per CTA
+                 "frag": {"CRISP_COUNT_KERNEL": "2"},
+                 "frag_f1": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "1"},
+                 "frag_f4": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "4"}}
 
 
 @pytest.mark.parametrize("variant", list(COUNT_VARIANTS))
@@ -167,10 +171,12 @@ def test_full_blocks_ragged_tail(crisp, monkeypatch, mode, variant):
     assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
 
 
+@pytest.mark.parametrize("kernel", ["1", "2"])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_many_subspaces_wide_counters(crisp, mode):
+def test_many_subspaces_wide_counters(crisp, monkeypatch, mode, kernel):
     """M=64 (scores up to 2M=128 do not fit the 7-bit SWAR compare: the
     __vcmpgeu4 path of the threshold scan), stage by stage."""
+    monkeypatch.setenv("CRISP_COUNT_KERNEL", kernel)
     X, Qv, ox = make_case(cfg=1, N=9001, D=256, Q=16, M=64, K=6, seed=7)
     ix = build_gpu(crisp, X, ox, block_ids=4096)
     B, tau, k = 1500, 30, 10
@@ -181,6 +187,27 @@ def test_many_subspaces_wide_counters(crisp, mode):
     if mode == 1:
         assert int(ot["V"].max()) >= 64, "scores above 63 exercise the wide compare"
     assert_topk_parity(ids, d, r_ids, r_d, "M=64")
+
+
+@pytest.mark.parametrize("F", ["1", "2"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_count_frag_chunked_entries(crisp, monkeypatch, mode, F):
+    """k_count_frag with more activated cells than one staging chunk holds
+    (M=32 subspaces x 256 cells, budget = N: 8192 activated cells per query, 4
+    chunks), weights 2 on the first k ranks, a 3-block ragged id range."""
+    monkeypatch.setenv("CRISP_COUNT_KERNEL", "2")
+    monkeypatch.setenv("CRISP_COUNT_F", F)
+    X, Qv, ox = make_case(cfg=1, N=9001, D=128, Q=6, M=32, K=16, seed=11, kmeans_iters=4)
+    ix = build_gpu(crisp, X, ox, block_ids=4096)
+    assert ix.info()["n_blocks"] == 3
+    N = X.shape[0]
+    for B, tau, k in ((N, 40, 10), (2500, 5, 10)):
+        ix.set_search_params(budget=B, tau=tau, patience_factor=2)
+        ids, d, t = ix.trace(Qv, k, mode)
+        r_ids, r_d, ot = oracle.search(ox, Qv, k, mode, B, tau, patience_factor=2, trace=True)
+        compare_trace(t, ot, mode, N)
+        assert_topk_parity(ids, d, r_ids, r_d, f"frag chunks B={B}")
+    assert int(t["act_len"].sum(axis=1).max()) == 32 * 256 or B != N
 
 
 @pytest.mark.parametrize("mode", [0, 1])
@@ -370,18 +397,18 @@ def test_host_buffers_match_device(crisp, mode):
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-def test_candidate_capacity_regrow(crisp, monkeypatch, mode):
-    """|C_q| larger than the optimistic per-query candidate capacity: the batch
-    is redone with a larger capacity, results unchanged (exactness guard)."""
-    monkeypatch.setenv("CRISP_CAND_CAP", "4096")
+def test_candidate_capacity_bound(crisp, monkeypatch, mode):
+    """|C_q| close to N (budget 9000 of 14000 ids, tau = 1): the per-query
+    candidate capacity is the exact upper bound derived from B, tau and the
+    largest cells (no read-back, no regrow), and the results are exact."""
     monkeypatch.setenv("CRISP_COUNT_BPC", "2")
     X, Qv, ox = make_case(cfg=1, N=14000, D=64, Q=20, M=4, K=6, seed=11)
     ix = build_gpu(crisp, X, ox, block_ids=4096)
     ix.set_search_params(budget=9000, tau=1, patience_factor=0)
     ids, d = ix.search(Qv, 10, mode)
     r_ids, r_d, ot = oracle.search(ox, Qv, 10, mode, 9000, 1, patience_factor=0, trace=True)
-    assert ot["cand_n"].max() > 4096
-    assert_topk_parity(ids, d, r_ids, r_d, "capacity regrow")
+    assert ot["cand_n"].max() > 8000
+    assert_topk_parity(ids, d, r_ids, r_d, "capacity bound")
 
 
 @pytest.mark.parametrize("tau", [2, 5])
@@ -436,6 +463,71 @@ def test_shard_emulation_exact_fallback(crisp, tau):
         assert ot["fallback"].sum() >= 2
     assert np.array_equal(oi.cpu().numpy(), ids1)
     assert np.array_equal(od.cpu().numpy(), d1)
+    # ... and equal the oracle's single-index search (the comparator is the oracle)
+    r_ids, r_d, _ = oracle.search(ox, Qv, k, 0, B, tau)
+    assert np.array_equal(oi.cpu().numpy(), r_ids)
+    assert np.array_equal(od64.cpu().numpy(), r_d) or np.allclose(od64.cpu().numpy(), r_d, rtol=1e-12, atol=0)
+
+
+def test_merge_topk_matches_oracle(crisp):
+    """a6 (crisp_merge_topk) against oracle.merge_topk on lists with heavy exact
+    distance ties (values from a small integer set, so (d, gid) decides),
+    padded rows (-1, +inf) and shards holding fewer than k results."""
+    import torch
+
+    r = np.random.default_rng(3)
+    for G, Q, k in ((2, 50, 10), (3, 40, 7), (8, 16, 100), (1, 5, 1)):
+        d = np.sort(r.integers(0, 6, (G, Q, k)).astype(np.float64), axis=2)
+        gids = np.empty((G, Q, k), np.int64)
+        for g in range(G):
+            for q in range(Q):
+                gids[g, q] = np.sort(r.choice(np.arange(g * 1000, (g + 1) * 1000), k, replace=False))
+        # each list ascending by (d, gid); pad the tail of some lists
+        o = np.lexsort((gids, d), axis=2)
+        d, gids = np.take_along_axis(d, o, 2), np.take_along_axis(gids, o, 2)
+        pad = r.integers(0, k + 1, (G, Q))
+        for g in range(G):
+            for q in range(Q):
+                d[g, q, pad[g, q]:] = np.inf
+                gids[g, q, pad[g, q]:] = -1
+        ref_d, ref_i = oracle.merge_topk(d, gids)
+        dd, di = torch.from_numpy(d).cuda(), torch.from_numpy(gids).cuda()
+        od64 = torch.empty((Q, k), dtype=torch.float64, device="cuda")
+        od = torch.empty((Q, k), dtype=torch.float32, device="cuda")
+        oi = torch.empty((Q, k), dtype=torch.int64, device="cuda")
+        crisp.merge_topk(dd, di, od64, od, oi)
+        torch.cuda.synchronize()
+        assert np.array_equal(oi.cpu().numpy(), ref_i), (G, Q, k)
+        assert np.array_equal(od64.cpu().numpy(), ref_d), (G, Q, k)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_exact_ties_integer_data_duplicate_rows_and_centroids(crisp, mode):
+    """Integer-valued data (exact distances: ties are real, not near-ties) with
+    duplicated rows, and codebooks with duplicated centroids: the assignment
+    (lowest c wins), the half sorts (delta, c), the cell order (cost, i, j), the
+    Hamming order (h, id) and the top-k (d, id) all hit exact ties on both
+    sides (App. A.2; Fig. 3; MNIST-like integer data)."""
+    r = np.random.default_rng(17)
+    N, D, M, K = 6000, 32, 4, 10
+    X = r.integers(0, 4, (N, D)).astype(np.float32)
+    X[3000:3600] = X[:600]  # duplicate rows
+    Qv = r.integers(0, 4, (30, D)).astype(np.float32)
+    Qv[:5] = X[[7, 3007, 100, 200, 2999]]  # self queries, some duplicated in X
+    cb = oracle.train_codebooks(X, M, K, 5, N, 3)
+    cb[:, :, 1] = cb[:, :, 0]  # duplicate centroids (half-sort and assignment ties)
+    cb[:, :, 5] = np.round(cb[:, :, 5])
+    ox = oracle.build(X, M, K=K, rotation_mode=0, codebooks=cb)
+    ix = crisp.Index.build(X, M, codebooks=cb, K=K)
+    compare_index(ix, ox)
+    assert not np.any(ox["cells"] // K == 1) and not np.any(ox["cells"] % K == 1), "a duplicate never wins (lowest c)"
+    for B, tau, k, P in ((300, 2, 10, 2), (1500, 1, 25, 1), (N, 4, 5, 3)):
+        ix.set_search_params(budget=B, tau=tau, patience_factor=P)
+        ids, d, t = ix.trace(Qv, k, mode)
+        r_ids, r_d, ot = oracle.search(ox, Qv, k, mode, B, tau, patience_factor=P, trace=True)
+        compare_trace(t, ot, mode, N)
+        assert np.array_equal(ids, r_ids), f"(d, id) ties B={B}"
+        assert np.array_equal(d, r_d.astype(np.float32)), "integer distances are exact"
 
 
 def test_build_waits_for_pending_device_writes(crisp):

@@ -580,3 +580,81 @@ def test_adsampling_search_exact_distances_and_recall():
             assert x >= 0 and d_a[q, i] == oracle.dist64(t["qrot"][q], ix["X"][x])
         hits += len(set(ids_a[q].tolist()) & set(ids_e[q].tolist()))
     assert hits / ids_e.size >= 0.9
+
+
+# --------------------------------------------------------------------------
+# Exact patience stop (O15 step 4; Z11) and ADSampling prune-as-miss
+# (Eq. 2 with P:L458), on integer-valued data so every squared distance is an
+# exact integer (no rounding on either side: the Python sums below are exact).
+# --------------------------------------------------------------------------
+def _int_index(N=2500, D=32, M=4, K=6, seed=21, lo=-6, hi=7, rot=0):
+    r = rng(seed)
+    X = r.integers(lo, hi, (N, D)).astype(np.float32)
+    X[N // 2: N // 2 + 40] = X[:40]  # duplicate rows: exact distance ties, broken by id
+    Qv = r.integers(lo, hi, (12, D)).astype(np.float32)
+    ix = oracle.build(X, M, K=K, rotation_mode=rot, kmeans_iters=6, seed=seed)
+    return ix, X, Qv
+
+
+def _exact_d2(q, x):
+    return int(np.sum((q.astype(np.int64) - x.astype(np.int64)) ** 2))
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_patience_stop_is_exact(P):
+    """The stop index n_verified is pinned exactly: the verification at
+    position nv - P*k - 1 (0-based) improved the top-k (the counter was reset
+    there), the P*k after it did not, and no run of P*k consecutive
+    non-improvements ends earlier; an oracle stopping one verification late or
+    early fails one of the three."""
+    ix, X, Qv = _int_index()
+    k = 4
+    ids, d, t = oracle.search(ix, Qv, k=k, mode=1, budget=300, tau=1, patience_factor=P, trace=True)
+    Pk = P * k
+    stopped = 0
+    for q in range(Qv.shape[0]):
+        n, nv = int(t["cand_n"][q]), int(t["n_verified"][q])
+        order = t["order"][q, :n]
+        dd = [(_exact_d2(Qv[q], X[x]), int(x)) for x in order]
+        # improvement flags by definition: |H| < k or (d, id) < max(H) (Z11)
+        imp = []
+        for i in range(n):
+            prev = sorted(dd[:i])[:k]
+            imp.append(len(prev) < k or dd[i] < prev[-1])
+        assert [x for _, x in sorted(dd[:nv])[:k]] == ids[q, :min(k, nv)].tolist()
+        if nv < n:
+            stopped += 1
+            assert imp[nv - Pk - 1], "the counter was reset P*k verifications before the stop"
+            assert not any(imp[nv - Pk:nv]), "the last P*k verifications changed nothing"
+        run = 0
+        for i in range(nv - Pk if nv < n else n - 1):  # (a run may end exactly at the last candidate)
+            run = 0 if imp[i] else run + 1
+            assert run < Pk, "an earlier run of P*k non-improvements would have stopped"
+    assert stopped >= 3
+
+
+def test_adsampling_prune_counts_as_non_improvement():
+    """A constructed case where only prunes can end the search: the query's k
+    near neighbours come first in Hamming order (all coordinates positive, like
+    the query), then only far points (all negative: every one is pruned at
+    the first checkpoint t = 32 by Eq. 2).  Since a prune is a non-improving
+    verification (P:L458), the search stops after exactly k + P*k candidates;
+    an oracle whose prunes did not advance the counter would verify all."""
+    r = rng(5)
+    D, k, P = 64, 5, 2
+    q = np.full((1, D), 3.0, np.float32)
+    near = (3.0 + r.integers(-1, 2, (k, D))).astype(np.float32)
+    far = (-6.0 - r.integers(0, 3, (300, D))).astype(np.float32)
+    X = np.vstack([far[:150], near, far[150:]])
+    ix = oracle.build(X, 2, K=2, rotation_mode=0, kmeans_iters=3, seed=1)
+    N = X.shape[0]
+    kw = dict(k=k, mode=1, budget=N, tau=1, patience_factor=P, trace=True)
+    ids, d, t = oracle.search(ix, q, adsampling=True, **kw)
+    assert int(t["cand_n"][0]) == N
+    assert sorted(t["order"][0, :k].tolist()) == list(range(150, 150 + k)), "near points first in Hamming order"
+    assert int(t["n_verified"][0]) == k + P * k
+    assert sorted(ids[0].tolist()) == list(range(150, 150 + k))
+    # every far point is pruned at t = 32 (its partial sum alone exceeds Eq. 2's bound)
+    rk2 = max(_exact_d2(q[0], X[i]) for i in range(150, 150 + k))
+    thr = oracle.adsampling_threshold(float(rk2), 32, D, 2.1)
+    assert all(_exact_d2(q[0, :32], X[i, :32]) > thr for i in list(range(150)) + list(range(155, N)))

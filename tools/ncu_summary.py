@@ -17,7 +17,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__pcsamp_warps_issue_stalled_mio_throttle", "smsp__pcsamp_sample_count"]
 
 
-SEARCH = ("k_prep_queries", "k_gemm_seq", "k_slice_rows", "k_certify", "k_recompute", "gemm_s8", "k_probe", "k_query_key", "k_count_warp", "k_count_select", "k_fallback",
+SEARCH = ("k_prep_queries", "k_gemm_seq", "k_slice_rows", "k_certify", "k_recompute", "gemm_s8", "k_probe", "k_query_key", "k_count_warp", "k_count_select", "k_count_frag", "k_fallback",
           "k_rerank_exact",
           "k_merge_lists", "k_rerank_patience", "k_stats", "k_hamming", "k_hsort", "k_verify", "k_patience")
 
