@@ -111,6 +111,16 @@ class Clocks:
         return out
 
 
+def l2_peak():
+    """In-repo L2 -> SM read bandwidth (tools/measure_peaks.py), if measured."""
+    f = os.path.join(ROOT, "profiles", "r02_peaks.json")
+    try:
+        with open(f) as fh:
+            return float(json.load(fh)["l2_read_gbs_48MiB"]), "measured in-repo (profiles/r02_peaks.json)"
+    except Exception:
+        return None
+
+
 def hbm_peak():
     try:
         with open(PEAKS) as f:
@@ -460,8 +470,20 @@ def run_crisp(args):
         roof = None
         if dom:
             a = kernels[dom]["achieved_gbs"]
+            sec = kernels[dom]["ms_per_step"] * 1e-3
             roof = {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak, "traffic": traffic,
-                    "kernel": kernels[dom]["kernel"], "peak_source": peak_src}
+                    "kernel": kernels[dom]["kernel"], "peak_source": peak_src,
+                    "per": "step (the stage's launches summed: bytes and CUDA-event time per step)"}
+            if traffic:
+                # the DRAM side of the same stage: measured bytes (ncu) over the live time
+                roof["dram_gbs"] = traffic / sec / 1e9
+                roof["dram_frac"] = roof["dram_gbs"] / peak
+            l2 = l2_peak()
+            if l2:
+                # the algorithmic stream is served from L2 and DRAM: its ceiling is the L2 read rate
+                roof["l2_peak"] = l2[0]
+                roof["l2_frac"] = a / l2[0]
+                roof["l2_peak_source"] = l2[1]
         results[mode] = dict(qps=Q * K / (ms / 1e3), ms=ms / K, recall=rec, beta=mp["beta"], alpha=mp["alpha"],
                              budget_ids=info["budget"], tau=info["tau"], roofline=roof, kernels=kernels,
                              stage_ms_per_step={k_: v / K for k_, v in st.items()},

@@ -156,7 +156,7 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
         ix->X = dalloc<float>(ix, (size_t)N * ix->pitch);
         ix->cb = dalloc<float>(ix, (size_t)ix->M * 2 * ix->K * ix->dh);
         ix->cells = dalloc<int32_t>(ix, (size_t)ix->M * N);
-        ix->ids = dalloc<int32_t>(ix, (size_t)ix->M * N);
+        ix->ids = dalloc<int32_t>(ix, (size_t)ix->M * N + 4);  // +4: k_count_frag's 16-byte loads of the last quad
         ix->off2 = dalloc<int32_t>(ix, (size_t)ix->M * KK * (ix->NB + 1));
         ix->off2w = dalloc<int32_t>(ix, (size_t)ix->M * KK * (ix->NBW + 1));
         ix->gsize = dalloc<int32_t>(ix, (size_t)ix->M * KK);

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "crisp_internal.cuh"
@@ -822,22 +823,53 @@ constexpr int CF_WARPS = 16;
 constexpr int CF_THREADS = CF_WARPS * 32;
 constexpr int CF_CAP = 2048;  // fragments staged per chunk
 constexpr int CF_EPT = CF_CAP / CF_THREADS;
-constexpr int CF_U = 4;       // 32-position batches with loads in flight per warp
-constexpr int CF_TF = 8;      // fragments per task (<= 32)
+constexpr int CF_TF = 8;      // fragments per task (a power of two <= 32)
 
 struct CountFSmem {
-    int4 tab[CF_CAP + 40];  // staged non-empty fragments: (chunk prefix, ids[] index | WFLAG, length, -); padded
-    int32_t lpre[MAX_M + 2];
-    int32_t wtot[CF_WARPS];
+    int4 tab[CF_CAP + 40];  // staged non-empty fragments (quad prefix, first quad, first position | WFLAG, end); padded
     long long wtot64[CF_WARPS];
-    int next, total, base;
+    int32_t wtot[CF_WARPS];
+    int next, base;
 };
-__host__ __device__ constexpr size_t countf_smem(int BF) {  // counters, bitmap, CountFSmem
-    return (size_t)BF + (size_t)BF / 8 + ((sizeof(CountFSmem) + 15) & ~(size_t)15);
+// counters (BF bytes), candidate bitmap (BF bits), 32 dummy words (the atomics of
+// lanes without an id), CountFSmem
+__host__ __device__ constexpr size_t countf_smem(int BF) {
+    return (size_t)BF + (size_t)BF / 8 + 128 + ((sizeof(CountFSmem) + 15) & ~(size_t)15);
 }
 
-__global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__restrict__ act,
-                                                               const int32_t *__restrict__ act_len, int M, int KK,
+__device__ __forceinline__ uint32_t atom_add_sh(uint32_t a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_or_sh(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// The activated cells of each query as one compact row of entries
+// (m*KK + cell) | WFLAG (weight 2), in activation order, and their number:
+// the count kernel's staging then reads a contiguous row.  One warp per query.
+__global__ void k_act_rows(const uint32_t *__restrict__ act, const int32_t *__restrict__ act_len, int M, int KK,
+                           int64_t Qc, uint32_t *__restrict__ erow, int32_t *__restrict__ etot) {
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (q >= Qc) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t *aq = act + q * (int64_t)M * KK;
+    uint32_t *eq = erow + q * (int64_t)M * KK;
+    int base = 0;
+    for (int m = 0; m < M; m++) {
+        const int L = __ldg(act_len + q * M + m);
+        for (int r = lane; r < L; r += 32) {
+            const uint32_t v = __ldg(aq + (int64_t)m * KK + r);
+            eq[base + r] = (uint32_t)(m * KK + (int)(v & 0xffffu)) | ((v >> 16) == 2u ? WFLAG : 0u);
+        }
+        base += L;
+    }
+    if (lane == 0) etot[q] = base;
+}
+
+__global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__restrict__ erow,
+                                                               const int32_t *__restrict__ etot, int M, int KK,
                                                                const int32_t *__restrict__ off2, int NB, int F,
                                                                const int32_t *__restrict__ ids, int64_t N, int BS,
                                                                int NS, int tau, int32_t *__restrict__ pool,
@@ -850,67 +882,51 @@ __global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__
     const int BF = BS * F;
     uint32_t *cw = (uint32_t *)smraw;              // BF byte counters, 4 per word
     uint32_t *bm = (uint32_t *)(smraw + BF);       // BF-bit candidate bitmap
-    CountFSmem &S = *(CountFSmem *)(smraw + BF + BF / 8);
+    CountFSmem &S = *(CountFSmem *)(smraw + BF + BF / 8 + 128);
+    const uint32_t sm_cw = (uint32_t)__cvta_generic_to_shared(cw);
+    const uint32_t sm_bm = sm_cw + (uint32_t)BF;
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;  // locality order (query_order)
     const int sb = blockIdx.x;                                 // id block [sb*BF, (sb+1)*BF)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sm_dummy = sm_bm + (uint32_t)(BF / 8) + 4u * (uint32_t)lane;  // this lane's dummy word
     const uint32_t bbase = (uint32_t)sb * (uint32_t)BF;
     const int c0 = sb * F, c1 = min(NB, c0 + F);  // off2 columns bounding the block
-    if (warp == 0) {
-        int acc = 0;
-        for (int m0 = 0; m0 < M; m0 += 32) {
-            const int m = m0 + lane;
-            int v = m < M ? __ldg(act_len + q * M + m) : 0;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, v, off);
-                if (lane >= off) v += t;
-            }
-            if (m < M) S.lpre[m + 1] = acc + v;
-            acc += __shfl_sync(0xffffffffu, v, 31);
-        }
-        if (lane == 0) S.lpre[0] = 0;
-    }
-    for (int i = tid; i < (BF + BF / 8) / 16; i += CF_THREADS) ((uint4 *)smraw)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    const int Etot = S.lpre[M];
-    const uint32_t *actq = act + q * (int64_t)M * KK;
+    for (int i = tid; i < (BF + BF / 8 + 128) / 16; i += CF_THREADS) ((uint4 *)smraw)[i] = make_uint4(0, 0, 0, 0);
+    const int Etot = __ldg(etot + q);
+    const uint32_t *eq = erow + q * (int64_t)M * KK;
     const uint32_t taum1 = (uint32_t)tau - 1u;
+    __syncthreads();
     for (int e0 = 0; e0 < Etot; e0 += CF_CAP) {
         const int ne = min(CF_CAP, Etot - e0);
         // stage this chunk's fragments: warp w takes entries [w*32*CF_EPT, (w+1)*32*CF_EPT) of the
-        // chunk, lane l the entries w*32*CF_EPT + 32u + l; the loads of a thread's entries are
-        // issued together (entry -> act word -> off2 pair), then a warp scan of the packed
-        // (length, non-empty) values, one barrier for the warp totals, the scatter of the
-        // non-empty fragments (their order in the table is immaterial: the counts commute)
+        // chunk, lane l the entries w*32*CF_EPT + 32u + l (coalesced entry loads, then the
+        // off2 pairs, all in flight together), a warp scan of the packed (chunks,
+        // non-empty) values, one barrier for the warp totals, the scatter of the non-empty
+        // fragments (their order in the table is immaterial: the counts commute)
         const int W0 = warp * 32 * CF_EPT;
-        const uint32_t *aadr[CF_EPT];
-        int mrow[CF_EPT];
+        uint32_t er[CF_EPT];
 #pragma unroll
         for (int u = 0; u < CF_EPT; u++) {
             const int t = W0 + 32 * u + lane;
-            const int e = e0 + min(t, ne - 1);
-            const int m = m_of_entry(S.lpre, M, e);
-            mrow[u] = m;
-            aadr[u] = actq + (int64_t)m * KK + (e - S.lpre[m]);
+            er[u] = t < ne ? __ldg(eq + e0 + t) : 0xffffffffu;
         }
-        uint32_t av[CF_EPT];
-#pragma unroll
-        for (int u = 0; u < CF_EPT; u++) av[u] = (W0 + 32 * u + lane < ne) ? __ldg(aadr[u]) : 0u;
         int s0[CF_EPT], s1[CF_EPT];
 #pragma unroll
         for (int u = 0; u < CF_EPT; u++) {
-            const int32_t *o = off2 + ((int64_t)mrow[u] * KK + (int)(av[u] & 0xffffu)) * (NB + 1);
-            const bool ok = W0 + 32 * u + lane < ne;
+            const bool ok = er[u] != 0xffffffffu;
+            const int32_t *o = off2 + (int64_t)(ok ? (er[u] & ~WFLAG) : 0u) * (NB + 1);
             s0[u] = ok ? __ldg(o + c0) : 0;
             s1[u] = ok ? __ldg(o + c1) : 0;
         }
         long long v[CF_EPT], ex[CF_EPT], carry = 0;
+        int g0[CF_EPT];  // absolute ids[] position of the fragment's first id
 #pragma unroll
         for (int u = 0; u < CF_EPT; u++) {
             const int len = s1[u] - s0[u];
-            // (32-id chunks, non-empty) packed for one scan
-            v[u] = len > 0 ? (((long long)((len + 31) >> 5) << 16) | 1) : 0;
+            g0[u] = (int)((er[u] & ~WFLAG) / (uint32_t)KK) * (int)N + s0[u];
+            // the fragment's 16-byte quads of ids[] (aligned to absolute position 4j)
+            const int nq = ((g0[u] + len + 3) >> 2) - (g0[u] >> 2);
+            v[u] = len > 0 ? (((long long)nq << 16) | 1) : 0;
             long long x = v[u];
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
@@ -929,22 +945,23 @@ __global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__
             wpre += w2 < warp ? t : 0;
             tot += t;
         }
-        const int NC = (int)(tot >> 16), nnz = (int)(tot & 0xffff);  // chunks, non-empty fragments
+        const int NC = (int)(tot >> 16), nnz = (int)(tot & 0xffff);  // quads, non-empty fragments
 #pragma unroll
         for (int u = 0; u < CF_EPT; u++)
             if (v[u]) {
                 const long long xx = wpre + ex[u];
-                S.tab[(int)(xx & 0xffff)] =
-                    make_int4((int)(xx >> 16),
-                              (int)((uint32_t)(mrow[u] * (int)N + s0[u]) | ((av[u] >> 16) == 2u ? WFLAG : 0u)),
-                              s1[u] - s0[u], 0);
+                // (quad prefix, first quad, first position | weight flag, end position)
+                S.tab[(int)(xx & 0xffff)] = make_int4((int)(xx >> 16), g0[u] >> 2, (int)((uint32_t)g0[u] | (er[u] & WFLAG)),
+                                                      g0[u] + s1[u] - s0[u]);
             }
         if (tid < 40) S.tab[nnz + tid] = make_int4(tid == 0 ? NC : 0x7fffffff, 0, 0, 0);
         __syncthreads();
-        // Tasks of CF_TF consecutive fragments (their chunks [tab[f0].x, tab[f0+CF_TF].x)).  A
-        // chunk is up to 32 consecutive ids of one fragment, one per lane; its fragment is
-        // found with one ballot over the task's fragments held in lanes 0..CF_TF-1 (chunk
-        // prefixes strictly increase: no empty fragments).
+        // Tasks of CF_TF consecutive fragments, i.e. their quads [tab[f0].x, tab[f0+CF_TF].x).  A
+        // lane takes one quad per step (a 16-byte load of 4 consecutive ids[] words of one
+        // fragment, edge words masked) and finds its fragment with a 3-step shuffle search over
+        // the task's fragments held in lanes 0..CF_TF-1 (quad prefixes strictly increase: no
+        // empty fragments).  Loads are software-pipelined (the next step's quad is in flight
+        // while this step's atomics run); a lane without an id adds 0 to its own dummy word.
         for (;;) {
             int task = 0;
             if (lane == 0) task = atomicAdd(&S.next, 1);
@@ -952,32 +969,54 @@ __global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__
             const int f0 = task * CF_TF;
             if (f0 >= nnz) break;
             const int4 te = lane < CF_TF ? S.tab[f0 + lane] : make_int4(0x7fffffff, 0, 0, 0);
-            const int C0 = __shfl_sync(0xffffffffu, te.x, 0);
-            const int C1 = S.tab[min(f0 + CF_TF, nnz)].x;  // tab[nnz].x = NC
-            for (int c0 = C0; c0 < C1; c0 += CF_U) {
-                uint32_t addr[CF_U], inc[CF_U];
+            const int P0 = __shfl_sync(0xffffffffu, te.x, 0);
+            const int P1 = S.tab[min(f0 + CF_TF, nnz)].x;  // tab[nnz].x = NC
+            uint4 qn;
+            int gn0 = 0, gn1 = 0, qpn = 0;
+            uint32_t wn = 0;
+            auto issue = [&](int pp) {
+                const int p = pp + lane;
+                int j = 0;
 #pragma unroll
-                for (int u = 0; u < CF_U; u++) {
-                    const int c = c0 + u;
-                    const int j = max(0, __popc(__ballot_sync(0xffffffffu, te.x <= c)) - 1);
-                    const int cx = __shfl_sync(0xffffffffu, te.x, j);
-                    const int gj = __shfl_sync(0xffffffffu, te.y, j);
-                    const int lj = __shfl_sync(0xffffffffu, te.z, j);
-                    const int o = ((c - cx) << 5) + lane;
-                    const bool ok = c < C1 && o < lj;
-                    addr[u] = ((uint32_t)gj & ~WFLAG) + (ok ? (uint32_t)o : 0u);
-                    inc[u] = ok ? 1u + ((uint32_t)gj >> 31) : 0u;
+                for (int st = CF_TF / 2; st; st >>= 1) {
+                    const int xv = __shfl_sync(0xffffffffu, te.x, j + st);
+                    if (xv <= p) j += st;
                 }
-                uint32_t x[CF_U];
+                const int qx = __shfl_sync(0xffffffffu, te.x, j);
+                const int qs = __shfl_sync(0xffffffffu, te.y, j);
+                const int gw = __shfl_sync(0xffffffffu, te.z, j);
+                const int ge = __shfl_sync(0xffffffffu, te.w, j);
+                const bool ok = p < P1;
+                qpn = ok ? qs + (p - qx) : 0;
+                gn0 = ok ? (int)((uint32_t)gw & ~WFLAG) : 1;
+                gn1 = ok ? ge : 0;
+                wn = 1u + ((uint32_t)gw >> 31);
+                qn = __ldg((const uint4 *)ids + qpn);
+            };
+            issue(P0);
+            for (int pp = P0; pp < P1; pp += 32) {
+                const uint4 qv = qn;
+                const int q0 = qpn * 4, lo = gn0, hi = gn1;
+                const uint32_t w = wn;
+                if (pp + 32 < P1) issue(pp + 32);
+                const uint32_t xs[4] = {qv.x, qv.y, qv.z, qv.w};
+                uint32_t ov[4], sh[4], inc[4];
 #pragma unroll
-                for (int u = 0; u < CF_U; u++) x[u] = (uint32_t)__ldg(ids + addr[u]);
+                for (int e = 0; e < 4; e++) {
+                    const bool ok = q0 + e >= lo && q0 + e < hi;
+                    inc[e] = ok ? w : 0u;
+                    const uint32_t off = xs[e] - bbase;
+                    sh[e] = (off & 3u) * 8u;
+                    ov[e] = atom_add_sh(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << sh[e]);
+                }
 #pragma unroll
-                for (int u = 0; u < CF_U; u++)
-                    if (inc[u]) {
-                        const uint32_t off = x[u] - bbase, sh = (off & 3u) * 8u;
-                        const uint32_t ov = (atomicAdd(cw + (off >> 2), inc[u] << sh) >> sh) & 0xffu;
-                        if (taum1 - ov < inc[u]) atomicOr(bm + (off >> 5), 1u << (off & 31));  // ov < tau <= ov+inc
+                for (int e = 0; e < 4; e++) {
+                    const uint32_t o8 = (ov[e] >> sh[e]) & 0xffu;
+                    if (taum1 - o8 < inc[e]) {  // o8 < tau <= o8 + inc: x enters C
+                        const uint32_t off = xs[e] - bbase;
+                        red_or_sh(sm_bm + ((off >> 5) << 2), 1u << (off & 31));
                     }
+                }
             }
         }
         __syncthreads();  // the chunk's table is re-staged next
@@ -2643,9 +2682,14 @@ static double env_double(const char *name, double dflt) {
     return v ? atof(v) : dflt;
 }
 
+// kernel attributes are per device: set them once for each device a search runs on
 static void set_attrs() {
-    static bool done = false;
-    if (done) return;
+    static std::mutex mu;
+    static std::vector<int> done_dev;
+    int dev = 0;
+    CRISP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done_dev.begin(), done_dev.end(), dev) != done_dev.end()) return;
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_frag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -2669,7 +2713,7 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows_ad, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    done = true;
+    done_dev.push_back(dev);
 }
 
 // ---------------------------------------------------------------------------
@@ -2690,8 +2734,8 @@ struct Work {
     }
     DevBuf buf;
     float *qpad = nullptr, *qrot = nullptr;
-    uint32_t *act = nullptr;
-    int32_t *act_len = nullptr;
+    uint32_t *act = nullptr, *erow = nullptr;  // erow: compact activated-cell rows (k_count_frag)
+    int32_t *act_len = nullptr, *etot = nullptr;
     int64_t *retr = nullptr;
     int32_t *pool = nullptr, *ncand = nullptr, *cbase = nullptr, *cursor = nullptr, *need = nullptr, *fb = nullptr;
     double *part_d = nullptr, *dbuf = nullptr, *d64tmp = nullptr;
@@ -2726,7 +2770,7 @@ struct Work {
         // >= the dbuf row stride DS of Work()
         const int S0 = std::max({first_round(ix, k), std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024)),
                                  (int)std::min<int64_t>(1 << 16, std::max<int64_t>(patience_rows(ix, k), 1024))});
-        int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 4 + (int64_t)ix->M * 12 + CAPQ * 4 +
+        int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 8 + (int64_t)ix->M * 12 + CAPQ * 4 + 4 +
                        (int64_t)ix->NBW * 8 + 64;
         if (mode == 0) perq += (int64_t)S * k * 16;
         else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
@@ -2766,7 +2810,19 @@ struct Work {
         ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
         // row kernels: four rows per warp step for rows up to 4 KB (measured: faster at D=960, slower at 4096)
         rows4 = env_int("CRISP_ROWS4", pitch <= 1024 ? 1 : 0);
-        F = ad && !adsp ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : first_round(ix, k);
+        // round 0: exact verification of every query's first F rows.  ADSampling on
+        // the spans: only 2k rows (rounded to 64), enough to give most queries an r_k,
+        // so that the rows after them are verified under Eq. 2 and pruned early
+        // (P:L240-244); exact: F ~ P (first_round)
+        // (measured: on these workloads a 2k-row round 0 is slower -- cfg4 verify 81.7 ms against
+        // 80.1 exact, cfg2 5.33 ms against 3.25 -- the text-like distances are concentrated
+        // (ratio to r_k ~1.3 < Eq. 2's margin), so few rows prune; default: F ~ P as exact)
+        if (ad && adsp)
+            F = env_int("CRISP_AD_FIRST", 0) > 0
+                    ? std::max(64, (std::max(32, env_int("CRISP_AD_FIRST", 0)) + 63) / 64 * 64)
+                    : first_round(ix, k);
+        else
+            F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : first_round(ix, k);
         DS = std::max({F, S0, std::min(std::max(Pq, nl_min), 1 << 16)});  // dbuf row stride (max span of a round)
         round_rows = std::max(1, env_int("CRISP_ROUND_ROWS", 128));  // min rows per CTA in round 0
         vra_smem = pitch * 8 + (Dp / 4 + 1) * 8;
@@ -2775,6 +2831,10 @@ struct Work {
         act = buf.alloc<uint32_t>((size_t)Qc * M * KK);
         act_len = buf.alloc<int32_t>((size_t)Qc * M);
         retr = buf.alloc<int64_t>((size_t)Qc * M);
+        if (count_kernel == 2) {
+            erow = buf.alloc<uint32_t>((size_t)Qc * M * KK);
+            etot = buf.alloc<int32_t>((size_t)Qc);
+        }
         pool = buf.alloc<int32_t>((size_t)Qc * CAPQ);
         ncand = buf.alloc<int32_t>((size_t)Qc * NS);
         cbase = buf.alloc<int32_t>((size_t)Qc * NS);
@@ -2904,9 +2964,14 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
         if (w.mode == 1) CRISP_CUDA(cudaMemsetAsync(w.ghist, 0, (size_t)qn * (ix->Dp + 1) * 4, s));
         dim3 g(nblk(NB, w.BPC), (unsigned)qn);
         if (w.count_kernel == 2)
+        {
+            k_act_rows<<<nblk(qn, 8), 256, 0, s>>>(w.act, w.act_len, M, KK, qn, w.erow, w.etot);
+            CRISP_LAUNCH();
+            g_launches++;
             k_count_frag<<<dim3((unsigned)w.NS, (unsigned)qn), CF_THREADS, countf_smem(ix->BS * w.CF), s>>>(
-                w.act, w.act_len, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
+                w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
                 w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm);
+        }
         else if (w.count_kernel == 0)
             k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N,
                                                             ix->BS, w.BPC, ix->tau, w.pool, w.CAPQ, w.cursor, w.cbase,

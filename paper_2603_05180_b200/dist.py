@@ -4,8 +4,10 @@ Collective call sites:
   N1/N2  broadcast of R and the codebooks from rank 0 (shared by every shard)
   N3     all-reduce (sum) of the local cell sizes -> global sizes, so every
          shard's budget walk activates exactly the cells a single index would
-  N7     all-gather of the per-shard top-k (dist64, gid), then the a6 merge
-         kernel (crisp_merge_topk) by (d, gid)
+  N5     all-reduce (sum) of the local |C_q| (exact global fallback)
+  N6     all-gather of the V histograms (used by underflowing queries only)
+  N7     one all-gather of the per-shard top-k (dist64, gid) packed together,
+         then the a6 merge kernel (crisp_merge_topk) by (d, gid)
 
 The orchestration is written against a small engine interface so the same
 code runs with the CUDA engine (NCCL over NVLink) and, in the CPU tests, with
@@ -121,15 +123,23 @@ def global_cell_sizes(engine):
     return t
 
 
+def gather_topk(ids, d64):
+    """N7 as ONE all-gather: the per-shard (dist64, gid) lists packed as a
+    (2, Q, k) int64 tensor (the fp64 distances travel as their bit patterns,
+    unchanged), unpacked into (G, Q, k) fp64 and int64 for the a6 merge."""
+    world = dist.get_world_size()
+    packed = torch.stack((d64.view(torch.int64), ids))
+    out = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(out, packed)
+    allp = torch.stack(out)
+    return allp[:, 0].contiguous().view(torch.float64), allp[:, 1].contiguous()
+
+
 def search_step(engine, q_dev, k, mode, stream=0):
     """One sharded search of the batch: local a0..a5, then N7 + a6."""
     ids, d64 = engine.search_shard(q_dev, k, mode, stream)
-    world = dist.get_world_size()
-    gd = [torch.empty_like(d64) for _ in range(world)]
-    gi = [torch.empty_like(ids) for _ in range(world)]
-    dist.all_gather(gd, d64)
-    dist.all_gather(gi, ids)
-    return engine.merge(torch.stack(gd), torch.stack(gi), stream)
+    gd, gi = gather_topk(ids, d64)
+    return engine.merge(gd, gi, stream)
 
 
 def search_step_exact(engine, q_dev, k, mode, stream=0):
@@ -144,11 +154,8 @@ def search_step_exact(engine, q_dev, k, mode, stream=0):
     all_h = [torch.empty_like(hist) for _ in range(world)]
     dist.all_gather(all_h, hist)
     ids, d64 = engine.finish(counts, torch.stack(all_h), world, rank, stream)
-    gd = [torch.empty_like(d64) for _ in range(world)]
-    gi = [torch.empty_like(ids) for _ in range(world)]
-    dist.all_gather(gd, d64)
-    dist.all_gather(gi, ids)
-    return engine.merge(torch.stack(gd), torch.stack(gi), stream)
+    gd, gi = gather_topk(ids, d64)
+    return engine.merge(gd, gi, stream)
 
 
 def _coll_device():

@@ -320,14 +320,19 @@ def test_gpu_rotation_properties(crisp):
     assert auto.info()["rotated"] == (ox["cev"] > 0.85) == 1
 
 
+@pytest.mark.parametrize("gemm", ["tcgen05", "cublaslt"])
 @pytest.mark.parametrize("D,M", [(203, 4), (100, 3)])
-def test_certified_rotation_adversarial(crisp, D, M):
+def test_certified_rotation_adversarial(crisp, monkeypatch, D, M, gemm):
     """a0 on the int8 tensor cores with the certified rounding (rotate_imma.cu):
     q' must equal the oracle's sequential fp64 chain bit for bit on rows chosen
     to stress the certificate: zeros, a single non-zero, 60 orders of magnitude
     inside one row, subnormal inputs, power-of-two scalings, alternating signs,
-    exact cancellations, and padded dimensions (D' = 208, and D' = 102 whose
-    digit planes pad to 112)."""
+    exact cancellations, and padded dimensions (D' = 208 and D' = 102, whose
+    digit planes pad to 256 and 128: 2 and 1 k-blocks, 4 and 2 column tiles,
+    ragged 128-row tiles).  Both level-GEMM engines: the hand-written tcgen05
+    kernel with the fused certificate (default) and cuBLASLt + k_certify."""
+    if gemm == "cublaslt":
+        monkeypatch.setenv("CRISP_ROTATE_GEMM", "cublaslt")
     rng = np.random.default_rng(11)
     Dp = oracle.padded_dim(D, M)  # 208 (a multiple of 16) and 102 (the int8 planes pad to 112)
     X = rng.standard_normal((2500, D)).astype(np.float32)
