@@ -432,7 +432,10 @@ def run_crisp(args):
         kernels = {}
         if st["verify"] > 0:
             vb = cnt["verified"] * row_bytes / K  # 4D per verified row (SURVEY 8(d) B_rerank)
-            kernels["verify"] = {"kernel": ["k_rerank_exact", "k_verify_rows+k_patience_scan+k_patience_tail",
+            # phi=0: the grouped re-rank is opt-in (CRISP_RERANK_GROUP=1; search.cu Work)
+            grp = os.environ.get("CRISP_RERANK_GROUP", "0") != "0"
+            kernels["verify"] = {"kernel": ["k_rerank_group" if grp else "k_rerank_exact",
+                                            "k_verify_rows+k_patience_scan+k_patience_tail",
                                             "k_verify_rows(_ad)+k_patience_scan+k_patience_tail"][mode],
                                  "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
                                  "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
@@ -440,9 +443,10 @@ def run_crisp(args):
             # a3 streams 4 B per id (SURVEY 8(d) B_count); at phi=1 the same kernel
             # (k_count_warp) also gathers 8*ceil(D'/64) B of code per candidate (B_ham)
             cb_ = cnt["ids_streamed"] * 4 / K
-            warp_kernel = os.environ.get("CRISP_COUNT_KERNEL", "1" if info["slice_hint"] >= 8.0 else "0") != "0"
+            ck = os.environ.get("CRISP_COUNT_KERNEL", "1" if info["slice_hint"] >= 8.0 else "2")
+            warp_kernel = ck == "1"
             fused = warp_kernel and os.environ.get("CRISP_HAMMING_FUSED", "0") != "0"
-            name = "k_count_warp" if warp_kernel else "k_count_select"
+            name = {"0": "k_count_select", "1": "k_count_warp", "2": "k_act_rows+k_count_frag"}[ck]
             if phi(mode) == 1 and fused:
                 cb_ += cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K
                 name = "k_count_warp (collision count + fused Hamming)"
@@ -450,7 +454,7 @@ def run_crisp(args):
                                 "achieved_gbs": cb_ / (st["count_select"] / K * 1e-3) / 1e9}
             if phi(mode) == 1 and not fused and st.get("hamming", 0) > 0:
                 hb = cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K  # SURVEY 8(d) B_ham
-                kernels["hamming"] = {"kernel": "k_hamming_dense" if warp_kernel else "k_hamming",
+                kernels["hamming"] = {"kernel": "k_hamming+k_hamming_dense",
                                       "bytes_per_step": hb, "ms_per_step": st["hamming"] / K,
                                       "achieved_gbs": hb / (st["hamming"] / K * 1e-3) / 1e9}
         for kk in kernels.values():

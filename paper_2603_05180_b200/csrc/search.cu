@@ -802,22 +802,24 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
 // a3 + a4, fragment-flattened counting (the small-cell regime: many activated
 // cells per query, each contributing a short run of ids to every id block).
 // A CTA owns one query and one id block of BF = F*BS ids, whose V counters
-// (bytes, packed four to a 32-bit word) and candidate bitmap live in shared
-// memory.  For a chunk of the query's activated cells it stages each cell's
-// fragment inside the block -- [off2[c][F b], off2[c][F b + F]) of the
+// (bytes, packed four to a 32-bit word) live in shared memory.  For a chunk of
+// the query's activated cells (k_act_rows lists them per query) it stages each
+// cell's fragment inside the block -- [off2[c][F b], off2[c][F b + F]) of the
 // subspace's CSR ids, which holds exactly the cell's ids in the
-// block -- drops the empty ones and takes an exclusive prefix of their chunk
-// counts, so that the chunk's ids form one flat range of 32-id chunks (a
-// chunk = up to 32 consecutive ids of one fragment, one per lane: its load is
-// coalesced).  Warps take tasks of CF_TF consecutive fragments from a shared
-// counter; a chunk's fragment is found by one ballot over the task's
-// fragments held in the lanes, and each lane adds the weight w (Alg. 1
-// l.10-12) of its id with one shared atomic on the counter's word.  The same id can recur only
-// across subspaces (CSR partition property), and shared atomics order
+// block -- drops the empty ones and takes an exclusive prefix of their counts
+// of 16-byte quads of ids[] (aligned to absolute positions 4j).  Warps take
+// tasks of CF_TF consecutive fragments from a shared counter; a lane takes one
+// quad per step (one 16-byte load), finds its fragment with a 3-step shuffle
+// search over the task's fragments held in the lanes, masks the edge words
+// outside the fragment, and adds the weight w (Alg. 1 l.10-12) of each of its
+// ids with a shared atomic on the counter's word.  The same id can recur only
+// across subspaces (CSR partition property) and the atomics order
 // those, so no barrier separates subspaces.  V only grows, by 1 or 2, so x
 // enters C = {x : V[x] >= tau} (Alg. 1 l.18) exactly at the increment that
 // lifts its count from below tau to tau or more; that increment sets x's bit
 // in the candidate bitmap, which the CTA finally writes out in ascending id.
+// (Measured alternative: fire-and-forget reductions plus a SWAR scan of the
+// counters at the end -- cfg4 count 26.1 ms against 23.4 ms.)
 // ---------------------------------------------------------------------------
 constexpr int CF_WARPS = 16;
 constexpr int CF_THREADS = CF_WARPS * 32;
@@ -841,6 +843,9 @@ __device__ __forceinline__ uint32_t atom_add_sh(uint32_t a, uint32_t v) {
     uint32_t old;
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
     return old;
+}
+__device__ __forceinline__ void red_add_sh(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void red_or_sh(uint32_t a, uint32_t v) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -1021,7 +1026,7 @@ __global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__
         }
         __syncthreads();  // the chunk's table is re-staged next
     }
-    // a4: C in ascending id from the bitmap; each warp compacts a contiguous word range
+    // a4: C in ascending id from the crossing bitmap; each warp compacts a contiguous word range
     const int nwords = BF / 32, wpw = nwords / CF_WARPS;
     {
         int c = 0;
@@ -1554,6 +1559,190 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
             od[rank] = d;
             oi[rank] = id;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a5, Guaranteed Mode, grouped (the dense-candidate regime: |C_q| a large share
+// of N, e.g. cfg3/cfg5).  A CTA owns a group of GR consecutive queries of the
+// locality order (R8) and a range of RW ids.  It marks each query's candidates
+// of the range in a byte mask per id (bit g = query g of the group), lists the
+// ids any of them holds, and reads every such row ONCE: a warp loads the row
+// (float4, lane l takes float4s l, l+32, ...) and accumulates the distance of
+// every member query at the same time, in the same order as k_rerank_exact (the
+// lane's partial sum in ascending float4 order, then the butterfly), so the
+// distances are identical to the ungrouped kernel's.  Per (warp, query) top-k
+// lists, merged per query into the partial list of (query, range); k_merge_lists
+// merges the ranges.  A row shared by the group's queries is read once instead
+// of once per query.
+// ---------------------------------------------------------------------------
+constexpr int RG_MAX = 8;  // queries per group (mask bits)
+
+template <int GR>
+__global__ void __launch_bounds__(THREADS) k_rerank_group(const float *__restrict__ qrot, int pitch,
+                                                           const float *__restrict__ X, int64_t gid_base, int64_t N,
+                                                           const int32_t *__restrict__ pool, int64_t CAPQ,
+                                                           const int32_t *__restrict__ cbase,
+                                                           const int32_t *__restrict__ ncand, int NS, int segw,
+                                                           const int32_t *__restrict__ fb, int RW, int k,
+                                                           int64_t Qc, double *__restrict__ part_d,
+                                                           int64_t *__restrict__ part_i,
+                                                           const int32_t *__restrict__ qperm) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int nvec = pitch / 4;
+    double *qd = (double *)sm;                               // GR x pitch (component-major per query)
+    double *Ld = qd + (size_t)GR * pitch;                    // WARPS x GR x k
+    int64_t *Li = (int64_t *)(Ld + WARPS * GR * k);          // WARPS x GR x k
+    uint32_t *mask = (uint32_t *)(Li + WARPS * GR * k);     // RW bytes (4 ids per word)
+    uint16_t *list = (uint16_t *)((unsigned char *)mask + RW);  // RW
+    __shared__ int wcnt[WARPS][RG_MAX];
+    __shared__ int s_n, s_base[WARPS + 1];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t lo = (int64_t)blockIdx.x * RW;
+    const int64_t hi = min(N, lo + RW);
+    const int seg = (int)(lo / segw);
+    int64_t qs[GR];
+    int ng = 0;
+#pragma unroll
+    for (int g = 0; g < GR; g++) {
+        const int64_t qi = (int64_t)blockIdx.y * GR + g;
+        qs[g] = qi < Qc ? (qperm ? qperm[qi] : qi) : -1;
+        ng += qi < Qc;
+    }
+#pragma unroll
+    for (int g = 0; g < GR; g++)
+        if (qs[g] >= 0) load_qd(qd + (size_t)g * pitch, qrot + qs[g] * pitch, pitch);
+    for (int i = tid; i < RW / 4; i += THREADS) mask[i] = 0u;
+    __syncthreads();
+    // each query's candidates in [lo, hi): its segment of this range (ascending ids), or the
+    // fallback's single segment (segment 0, ascending ids over all of [0, N))
+#pragma unroll
+    for (int g = 0; g < GR; g++) {
+        if (qs[g] < 0) continue;
+        const int64_t q = qs[g];
+        const int sgi = fb[q] ? 0 : seg;
+        const int n = ncand[q * NS + sgi];
+        const int32_t *c = pool + q * CAPQ + cbase[q * NS + sgi];
+        // [a, b): the segment's ids in [lo, hi) (binary searches; ids ascending)
+        int a = 0, b = n;
+        {
+            int l2 = 0, h2 = n;
+            while (l2 < h2) {
+                const int md = (l2 + h2) >> 1;
+                if (c[md] < lo) l2 = md + 1;
+                else h2 = md;
+            }
+            a = l2;
+            h2 = n;
+            while (l2 < h2) {
+                const int md = (l2 + h2) >> 1;
+                if (c[md] < hi) l2 = md + 1;
+                else h2 = md;
+            }
+            b = l2;
+        }
+        for (int i = a + tid; i < b; i += THREADS) {
+            const int x = (int)(c[i] - lo);
+            atomicOr(mask + (x >> 2), 1u << (8 * (x & 3) + g));
+        }
+    }
+    __syncthreads();
+    // list the ids with a non-empty mask, ascending (per-warp contiguous ranges)
+    {
+        const unsigned char *m8 = (const unsigned char *)mask;
+        const int per = RW / WARPS;
+        int cnt = 0;
+        for (int i = lane; i < per; i += 32) cnt += m8[warp * per + i] != 0;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+        if (lane == 0) s_base[warp + 1] = cnt;
+        __syncthreads();
+        if (tid == 0) {
+            s_base[0] = 0;
+            for (int w2 = 0; w2 < WARPS; w2++) s_base[w2 + 1] += s_base[w2];
+            s_n = s_base[WARPS];
+        }
+        __syncthreads();
+        int o = s_base[warp];
+        for (int i0 = 0; i0 < per; i0 += 32) {
+            const int i = i0 + lane;
+            const bool f = i < per && m8[warp * per + i] != 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (f) list[o + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)(warp * per + i);
+            o += __popc(bal);
+        }
+    }
+    for (int i = tid; i < WARPS * RG_MAX; i += THREADS) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const int nl = s_n;
+    const unsigned char *m8 = (const unsigned char *)mask;
+    // rows: warp w takes list entries w, w + WARPS, ...
+    int cnt[GR];
+#pragma unroll
+    for (int g = 0; g < GR; g++) cnt[g] = 0;
+    for (int e = warp; e < nl; e += WARPS) {
+        const int x = list[e];
+        const uint32_t mm = m8[x];
+        const float4 *xr = (const float4 *)(X + (lo + x) * (int64_t)pitch);
+        double acc[GR];
+#pragma unroll
+        for (int g = 0; g < GR; g++) acc[g] = 0.0;
+#pragma unroll 2
+        for (int v = lane; v < nvec; v += 32) {
+            const float4 u = __ldg(xr + v);
+#pragma unroll
+            for (int g = 0; g < GR; g++)
+                if ((mm >> g) & 1u) acc4(acc[g], u, q4_at(qd + (size_t)g * pitch, v, nvec));
+        }
+        const int64_t gid = gid_base + lo + x;
+#pragma unroll
+        for (int g = 0; g < GR; g++) {
+            if (!((mm >> g) & 1u)) continue;
+            const double d = warp_sum(acc[g]);
+            double *myd = Ld + ((size_t)warp * GR + g) * k;
+            int64_t *myi = Li + ((size_t)warp * GR + g) * k;
+            if (cnt[g] < k || less_di(d, gid, myd[k - 1], myi[k - 1])) warp_insert(myd, myi, cnt[g], k, d, gid, lane);
+        }
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int g = 0; g < GR; g++) wcnt[warp][g] = cnt[g];
+    __syncthreads();
+    // per query: merge the WARPS lists by rank into the partial list of (query, range)
+    const int NR = gridDim.x;
+    for (int g = 0; g < ng; g++) {
+        const int64_t q = qs[g];
+        double *od = part_d + ((int64_t)q * NR + blockIdx.x) * k;
+        int64_t *oi = part_i + ((int64_t)q * NR + blockIdx.x) * k;
+        for (int r = tid; r < k; r += THREADS) {
+            od[r] = INFINITY;
+            oi[r] = -1;
+        }
+        __syncthreads();
+        for (int e2 = tid; e2 < WARPS * k; e2 += THREADS) {
+            const int w = e2 / k, i = e2 % k;
+            if (i >= wcnt[w][g]) continue;
+            const double d = Ld[((size_t)w * GR + g) * k + i];
+            const int64_t id = Li[((size_t)w * GR + g) * k + i];
+            int rank = i;
+            for (int w2 = 0; w2 < WARPS; w2++) {
+                if (w2 == w) continue;
+                int l2 = 0, h2 = wcnt[w2][g];
+                const double *L2d = Ld + ((size_t)w2 * GR + g) * k;
+                const int64_t *L2i = Li + ((size_t)w2 * GR + g) * k;
+                while (l2 < h2) {
+                    const int md = (l2 + h2) >> 1;
+                    if (less_di(L2d[md], L2i[md], d, id)) l2 = md + 1;
+                    else h2 = md;
+                }
+                rank += l2;
+            }
+            if (rank < k) {
+                od[rank] = d;
+                oi[rank] = id;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -2701,6 +2890,9 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -2723,6 +2915,7 @@ struct Work {
     const crisp_index *ix;
     int k, mode;
     int64_t Qc, CAPQ;
+    int rgroup = 0, segw = 0, RW = 0, NR = 0, GR = 0, rg_smem = 0;  // grouped phi=0 re-rank
     int S, S1, HS, S0, R0, BPC, count_kernel, count_atom, NS, CF, ham_fused, rows4, ad, adsp, F, DS, round_rows, nl_min, Pq,
         vra_smem;
     // end of the speculative rounds (positions the Hamming order must cover)
@@ -2772,7 +2965,7 @@ struct Work {
                                  (int)std::min<int64_t>(1 << 16, std::max<int64_t>(patience_rows(ix, k), 1024))});
         int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 8 + (int64_t)ix->M * 12 + CAPQ * 4 + 4 +
                        (int64_t)ix->NBW * 8 + 64;
-        if (mode == 0) perq += (int64_t)S * k * 16;
+        if (mode == 0) perq += (int64_t)std::max<int64_t>(S, (ix->N + 4095) / 4096) * k * 16;
         else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
         if (traceV) perq += ix->N;
         return perq;
@@ -2851,8 +3044,23 @@ struct Work {
             qsort_tmp = buf.alloc<unsigned char>(qsort_bytes);
         }
         if (mode == 0) {
-            part_d = buf.alloc<double>((size_t)Qc * S * k);
-            part_i = buf.alloc<int64_t>((size_t)Qc * S * k);
+            // grouped re-rank (k_rerank_group) for dense candidate sets: the expected share of
+            // N a query keeps is about M B / (tau N) (each candidate needs tau of the M
+            // activated slices of ~B ids); CRISP_RERANK_GROUP=0/1 forces it
+            const double dens = (double)ix->M * (double)ix->budget / ((double)std::max(1, ix->tau) * (double)ix->N_global);
+            // measured: slower than k_rerank_exact on cfg3/cfg5 (5.37 s / 13.3 s against 1.45 s / 2.71 s per
+            // 10k queries: one 8-warp CTA per SM with one row per warp step cannot keep enough loads
+            // in flight), so it is opt-in (CRISP_RERANK_GROUP=1); `dens` is kept for that switch
+            rgroup = env_int("CRISP_RERANK_GROUP", 0) != 0 && dens > 0.0 ? 1 : 0;
+            segw = count_kernel == 2 ? BS * CF : count_kernel == 1 ? ix->SBW : BS;
+            RW = std::min(16384, segw);
+            NR = (int)((ix->N + RW - 1) / RW);
+            GR = pitch <= 1024 ? 8 : pitch <= 2048 ? 4 : 2;
+            rg_smem = GR * pitch * 8 + WARPS * GR * k * 16 + 3 * RW;
+            if (rg_smem > 220 * 1024) rgroup = 0;
+            const int L = rgroup ? NR : S;
+            part_d = buf.alloc<double>((size_t)Qc * L * k);
+            part_i = buf.alloc<int64_t>((size_t)Qc * L * k);
         } else {
             cbuf = buf.alloc<int32_t>((size_t)Qc * CAPQ);
             hbuf = buf.alloc<uint16_t>((size_t)Qc * CAPQ);
@@ -3017,6 +3225,26 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     const crisp_index *ix = w.ix;
     const int NB = w.NS, pitch = ix->pitch, Dp = ix->Dp, k = w.k;  // NB: candidate segments
     if (!od64) od64 = w.d64tmp;
+    if (w.mode == 0 && w.rgroup) {
+        {
+            StageScope st(s, 4);
+            dim3 g((unsigned)w.NR, nblk(qn, w.GR));
+#define CRISP_RG(GRV)                                                                                                   k_rerank_group<GRV><<<g, THREADS, w.rg_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, ix->N, w.pool, w.CAPQ,                                                       w.cbase, w.ncand, NB, w.segw, w.fb, w.RW, k, qn, w.part_d,                                                         w.part_i, w.qperm)
+            if (w.GR == 8) CRISP_RG(8);
+            else if (w.GR == 4) CRISP_RG(4);
+            else CRISP_RG(2);
+#undef CRISP_RG
+            CRISP_LAUNCH();
+            g_launches++;
+        }
+        {
+            StageScope st(s, 5);
+            k_merge_lists<<<(unsigned)qn, THREADS, 0, s>>>(w.part_d, w.part_i, w.NR, qn, k, 0, od64, od, oi);
+            CRISP_LAUNCH();
+            g_launches++;
+        }
+        return;
+    }
     if (w.mode == 0) {
         {
             StageScope st(s, 4);

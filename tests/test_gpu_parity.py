@@ -107,7 +107,10 @@ COUNT_VARIANTS = {"select": {"CRISP_COUNT_KERNEL": "0", "CRISP_ROWS4": "0"},
                  # fragment-flattened count (the small-cell default) with 1, 2 and 4 id blocks per CTA
                  "frag": {"CRISP_COUNT_KERNEL": "2"},
                  "frag_f1": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "1"},
-                 "frag_f4": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "4"}}
+                 "frag_f4": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "4"},
+                 # the grouped Guaranteed-Mode re-rank (k_rerank_group) after either count kernel
+                 "frag_group": {"CRISP_COUNT_KERNEL": "2", "CRISP_RERANK_GROUP": "1"},
+                 "warp_group": {"CRISP_COUNT_KERNEL": "1", "CRISP_RERANK_GROUP": "1"}}
 
 
 @pytest.mark.parametrize("variant", list(COUNT_VARIANTS))
@@ -210,9 +213,13 @@ def test_count_frag_chunked_entries(crisp, monkeypatch, mode, F):
     assert int(t["act_len"].sum(axis=1).max()) == 32 * 256 or B != N
 
 
+@pytest.mark.parametrize("group", ["0", "1"])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_fallback_and_small_k(crisp, mode):
-    """tau above every reachable score -> the underflow fallback."""
+def test_fallback_and_small_k(crisp, monkeypatch, mode, group):
+    """tau above every reachable score -> the underflow fallback (P:L449);
+    Guaranteed Mode through both re-rank kernels (the fallback's candidates sit
+    in one segment spanning every id range of the grouped kernel)."""
+    monkeypatch.setenv("CRISP_RERANK_GROUP", group)
     X, Qv, ox = make_case(cfg=3, N=9000, D=64, Q=30, M=4, K=12, seed=5)
     ix = build_gpu(crisp, X, ox, block_ids=4096)
     for k, tau in ((5, 9), (1, 4), (64, 3)):
