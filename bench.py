@@ -364,10 +364,10 @@ def run_crisp(args):
         engine = None
     else:
         engine = cdist.CudaEngine(crisp, dev)
-        R, cb = engine.build_global(X, M, **bparams) if rank == 0 else (None, None)
-        R, cb = cdist.share_model(R, cb, Qd)
         lo, hi = cdist.shard_range(N, rank, world)
         Xs = w.rows(lo, hi - lo)
+        # N1/N2: the model from the gathered CEV / k-means sample rows (no full index on rank 0)
+        R, cb = cdist.model_from_shards(engine, Xs, lo, N, M, seed=bparams["seed"], K=bparams["K"])
         engine.build_shard(Xs, lo, M, R, cb, **bparams)
         del Xs
         cdist.global_cell_sizes(engine)

@@ -237,9 +237,35 @@ crisp_status crisp_stage_times(double *ms, int32_t n, int32_t reset);
  * (current device), for algorithmic-byte accounting: out[0] ids streamed by
  * the collision count (a3), out[1] sum of |C_q| (a4), out[2] rows verified
  * (a5), out[3] queries that took the fallback, out[4] kernels of this library
- * launched by searches/merges on the calling thread (counted always).  Up to n
- * entries are written; reset != 0 clears them. */
+ * launched by searches/merges on the calling thread (counted always), out[5]
+ * exact half distances (dist64) the a1 probe computed, out[6] (query,
+ * subspace) walks whose tensor-core screen did not cover the ranks the walk
+ * reached and were redone on exact half sorts.  Up to n entries are written;
+ * reset != 0 clears them. */
 crisp_status crisp_search_counters(int64_t *out, int32_t n, int32_t reset);
+
+/* Distributed model build (SURVEY 8(e) N1/N2 without a full index on one rank).
+ * The build's randomness is counter-based (Philox keyed by seed, streams per
+ * use; DESIGN R3), so the CEV sample and the k-means sample of a dataset of
+ * N_global rows are fixed sets of global row ids:
+ *   crisp_cev_sample_size(N) = ceil(min(0.1 N, 1e5)) (all rows if N <= 10; P:L264,
+ *     S:L117), the CEV sample's size;
+ *   crisp_sample_rows(N, n, seed, stream, rows_out): the n sampled row ids in
+ *     ascending order (the n rows of smallest (Philox key, id)); stream 1 = CEV
+ *     sample, stream 3 = k-means sample (n = min(N, kmeans_sample));
+ *     rows_out host or device, n int32.
+ * Each rank contributes its rows of both samples; with the rows gathered in
+ * ascending global id, crisp_build_model returns exactly the rotation (Dp x Dp
+ * fp32 into R_out, written only if *rotated_out = 1), the codebooks (M x 2 x K
+ * x dh into codebooks_out) and the CEV that crisp_build over all N_global rows
+ * would use (spectral check P:L262-271, rotation P:L225, k-means S:L221).
+ * cev_rows: n_cev x D fp32 (n_cev = crisp_cev_sample_size(N_global)); km_rows:
+ * n_km x D fp32.  Buffers host or device; the caller owns all of them. */
+int64_t crisp_cev_sample_size(int64_t N);
+crisp_status crisp_sample_rows(int64_t N, int64_t n, uint64_t seed, uint32_t stream, int32_t *rows_out);
+crisp_status crisp_build_model(const float *cev_rows, int64_t n_cev, const float *km_rows, int64_t n_km, int32_t D,
+                               const crisp_params *p, float *R_out, float *codebooks_out, int32_t *rotated_out,
+                               double *cev_out);
 
 /* ceil(ratio * n) with ratio read as the decimal it was written as: the
  * shortest decimal string that rounds to `ratio` (what printf("%.17g")-free

@@ -64,7 +64,7 @@ ABI_SYMBOLS = (
     "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
     "crisp_set_stage_timing", "crisp_stage_times", "crisp_search_counters", "crisp_free", "crisp_last_error", "crisp_version",
     "crisp_shard_search_begin", "crisp_shard_search_hist", "crisp_shard_search_finish", "crisp_shard_search_free",
-    "crisp_set_adsampling", "crisp_exact_ceil",
+    "crisp_set_adsampling", "crisp_exact_ceil", "crisp_cev_sample_size", "crisp_sample_rows", "crisp_build_model",
 )
 
 _lib = None
@@ -108,6 +108,10 @@ def lib():
         L.crisp_version.restype = C.c_char_p
         L.crisp_exact_ceil.argtypes = [f64, i64]
         L.crisp_exact_ceil.restype = i64
+        L.crisp_cev_sample_size.argtypes = [i64]
+        L.crisp_cev_sample_size.restype = i64
+        L.crisp_sample_rows.argtypes = [i64, i64, C.c_uint64, C.c_uint32, vp]
+        L.crisp_build_model.argtypes = [vp, i64, vp, i64, i32, vp, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -150,6 +154,39 @@ def exact_ceil(ratio, n: int) -> int:
     """crisp_exact_ceil: ceil(ratio*n) with ratio read as the shortest decimal
     that rounds to it (the library's rule for B and tau)."""
     return int(lib().crisp_exact_ceil(float(ratio), int(n)))
+
+
+STREAM_CEV_SAMPLE, STREAM_KM_SAMPLE = 1, 3  # the build's Philox streams (DESIGN R3)
+
+
+def sample_rows(N: int, n: int, seed: int, stream: int) -> np.ndarray:
+    """crisp_sample_rows: the n sampled global row ids (ascending) of a dataset of N rows."""
+    out = np.zeros(max(n, 1), np.int32)
+    _check(lib().crisp_sample_rows(int(N), int(n), int(seed), int(stream), _ptr(out)))
+    return out[:n]
+
+
+def model_samples(N: int, seed: int, kmeans_sample: int = 100000):
+    """(CEV sample row ids, k-means sample row ids) of a dataset of N rows."""
+    n_cev = int(lib().crisp_cev_sample_size(int(N)))
+    n_km = min(int(N), max(1, int(kmeans_sample)))
+    return sample_rows(N, n_cev, seed, STREAM_CEV_SAMPLE), sample_rows(N, n_km, seed, STREAM_KM_SAMPLE)
+
+
+def build_model(cev_rows, km_rows, M: int, **params):
+    """crisp_build_model: (R or None, codebooks, cev) from the gathered sample rows."""
+    p = default_params(M=M, **params)
+    cr = _host(cev_rows, np.float32)
+    kr = _host(km_rows, np.float32)
+    D = int(kr.shape[1])
+    Dp = ((D + 2 * M - 1) // (2 * M)) * (2 * M)
+    R = np.zeros((Dp, Dp), np.float32)
+    cb = np.zeros((M, 2, p.K, Dp // (2 * M)), np.float32)
+    rot = C.c_int32(0)
+    cev = C.c_double(0.0)
+    _check(lib().crisp_build_model(_ptr(cr), int(cr.shape[0]), _ptr(kr), int(kr.shape[0]), D, C.byref(p), _ptr(R),
+                                   _ptr(cb), C.byref(rot), C.byref(cev)))
+    return (R if rot.value else None), cb, cev.value
 
 
 def _dev(t, dtype, shape=None, what="tensor"):
@@ -355,7 +392,7 @@ def stage_times(reset: bool = True) -> dict:
 
 def search_counters(reset: bool = True) -> dict:
     """Work counters of the searches run with stage timing on (crisp_search_counters)."""
-    a = np.zeros(5, np.int64)
-    _check(lib().crisp_search_counters(_ptr(a), 5, 1 if reset else 0))
+    a = np.zeros(7, np.int64)
+    _check(lib().crisp_search_counters(_ptr(a), 7, 1 if reset else 0))
     return dict(ids_streamed=int(a[0]), candidates=int(a[1]), verified=int(a[2]), fallback=int(a[3]),
-                launches=int(a[4]))
+                launches=int(a[4]), probe_exact_half_distances=int(a[5]), probe_screen_redone=int(a[6]))

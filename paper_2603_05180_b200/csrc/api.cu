@@ -106,6 +106,8 @@ static void free_index(crisp_index *ix) {
     cudaFree(ix->Rn2);
     cudaFree(ix->Rt);
     cudaFree(ix->cb);
+    cudaFree(ix->cbp);
+    cudaFree(ix->cn2);
     cudaFree(ix->cells);
     cudaFree(ix->ids);
     cudaFree(ix->off2);
@@ -262,6 +264,78 @@ crisp_status crisp_build(const float *data, int64_t N, int32_t D, const crisp_pa
 crisp_status crisp_build_with(const float *data, int64_t N, int32_t D, const crisp_params *p, const float *R,
                               const float *codebooks, crisp_index **out) {
     return build_common(data, N, 0, D, p, R, codebooks, true, out);
+}
+
+int64_t crisp_cev_sample_size(int64_t N) { return N < 0 ? 0 : cev_sample_size(N); }
+
+crisp_status crisp_sample_rows(int64_t N, int64_t n, uint64_t seed, uint32_t stream, int32_t *rows_out) {
+    try {
+        CRISP_CHECK(rows_out != nullptr, "rows_out is NULL");
+        CRISP_CHECK(N >= 1 && n >= 0 && n <= N && N < (1LL << 31), "need 0 <= n <= N < 2^31");
+        if (n == 0) return CRISP_OK;
+        int dev = 0;
+        CRISP_CUDA(cudaGetDevice(&dev));
+        const bool on_dev = is_device_ptr(rows_out);
+        int32_t *d = rows_out;
+        if (!on_dev) CRISP_CUDA(cudaMalloc(&d, (size_t)n * 4));
+        struct F {
+            int32_t *p;
+            bool own;
+            ~F() {
+                if (own) cudaFree(p);
+            }
+        } f{d, !on_dev};
+        sample_row_ids(N, n, seed, stream, d, 0);
+        CRISP_CUDA(cudaDeviceSynchronize());
+        if (!on_dev) CRISP_CUDA(cudaMemcpy(rows_out, d, (size_t)n * 4, cudaMemcpyDeviceToHost));
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_build_model(const float *cev_rows, int64_t n_cev, const float *km_rows, int64_t n_km, int32_t D,
+                               const crisp_params *p, float *R_out, float *codebooks_out, int32_t *rotated_out,
+                               double *cev_out) {
+    crisp_index *ix = nullptr;
+    try {
+        CRISP_CHECK(p && km_rows && codebooks_out && rotated_out, "NULL argument");
+        CRISP_CHECK(n_km >= 1 && n_cev >= 0 && D >= 1, "bad sizes");
+        CRISP_CHECK(n_cev < 2 || cev_rows != nullptr, "cev_rows is NULL");
+        ix = new_index(n_km, D, p);
+        CRISP_CUDA(cudaDeviceSynchronize());
+        TmpFree tf;
+        double cev = 0.0;
+        cudaStream_t s;
+        CRISP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct SG {
+            cudaStream_t s;
+            ~SG() { cudaStreamDestroy(s); }
+        } sg{s};
+        if (n_cev >= 2) {
+            const float *cd = to_device(cev_rows, (size_t)n_cev * D, tf.v);
+            cev = cev_of_sample(cd, n_cev, D, s);
+        }
+        const float *kd = to_device(km_rows, (size_t)n_km * D, tf.v);
+        // an index over the k-means sample: the same rotation (seed) and k-means (every row of
+        // the sample, ascending global id) as a build over the whole dataset
+        build_index(ix, kd, nullptr, nullptr, n_km, p->kmeans_iters > 0 ? p->kmeans_iters : 20, p->rotation,
+                    p->tau_cev, p->seed, s, &cev);
+        *rotated_out = ix->rotated;
+        if (cev_out) *cev_out = cev;
+        if (ix->rotated && R_out)
+            CRISP_CUDA(cudaMemcpy(R_out, ix->R, (size_t)ix->Dp * ix->Dp * 4, cudaMemcpyDefault));
+        CRISP_CUDA(cudaMemcpy(codebooks_out, ix->cb, (size_t)ix->M * 2 * ix->K * ix->dh * 4, cudaMemcpyDefault));
+        free_index(ix);
+        return CRISP_OK;
+    } catch (Err &e) {
+        free_index(ix);
+        return e.st;
+    } catch (std::exception &e) {
+        set_error(e.what());
+        free_index(ix);
+        return CRISP_ECUDA;
+    }
 }
 
 crisp_status crisp_build_shard(const float *shard, int64_t N_local, int64_t gid_base, int32_t D, const crisp_params *p,

@@ -308,21 +308,43 @@ __global__ void k_colmean(const float *S, int64_t n, int D, double *mu) {
     mu[i] = s / (double)n;
 }
 
-static double compute_cev(const float *X, int64_t N, int64_t ld, int D, uint64_t seed, cudaStream_t s) {
-    int64_t n = (N <= 10) ? N : std::min<int64_t>((N + 9) / 10, 100000);
-    if (n < 2) return 0.0;
-    Scratch sc;
-    int32_t *rows = sc.alloc<int32_t>(n);
+// CEV sample size (Z16): ceil(min(0.1 N, 1e5)), all rows if N <= 10
+int64_t cev_sample_size(int64_t N) { return (N <= 10) ? N : std::min<int64_t>((N + 9) / 10, 100000); }
+
+// rows of the sample of size n (ascending index): all rows when n == N
+static void sample_or_all(int64_t N, int64_t n, uint64_t seed, uint32_t stream, int32_t *rows, cudaStream_t s) {
     if (n == N) {
         std::vector<int32_t> h(n);
         for (int64_t i = 0; i < n; i++) h[i] = (int32_t)i;
         CRISP_CUDA(cudaMemcpy(rows, h.data(), n * 4, cudaMemcpyHostToDevice));
     } else {
-        sample_rows(N, n, seed, STREAM_CEV_SAMPLE, rows, s);
+        sample_rows(N, n, seed, stream, rows, s);
     }
+}
+
+void sample_row_ids(int64_t N, int64_t n, uint64_t seed, uint32_t stream, int32_t *rows_dev, cudaStream_t s) {
+    sample_or_all(N, n, seed, stream, rows_dev, s);
+}
+
+static double cev_of_rows(const float *S, int64_t n, int D, cudaStream_t s);
+
+static double compute_cev(const float *X, int64_t N, int64_t ld, int D, uint64_t seed, cudaStream_t s) {
+    const int64_t n = cev_sample_size(N);
+    if (n < 2) return 0.0;
+    Scratch sc;
+    int32_t *rows = sc.alloc<int32_t>(n);
+    sample_or_all(N, n, seed, STREAM_CEV_SAMPLE, rows, s);
     float *S = sc.alloc<float>((size_t)n * D);
     k_gather_rows<<<nblk(n * D, 256), 256, 0, s>>>(X, ld, rows, n, D, S);
     CRISP_LAUNCH();
+    return cev_of_rows(S, n, D, s);
+}
+
+// CEV of the sample rows S (n x D, packed, ascending global index): covariance with
+// divisor n-1 in the sequential fp64 order, eigenvalues, top floor(0.2 D) share
+static double cev_of_rows(const float *S, int64_t n, int D, cudaStream_t s) {
+    if (n < 2) return 0.0;
+    Scratch sc;
     double *mu = sc.alloc<double>(D);
     k_colmean<<<nblk(D, 128), 128, 0, s>>>(S, n, D, mu);
     CRISP_LAUNCH();
@@ -810,13 +832,7 @@ static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, u
     int64_t n = std::min<int64_t>(N, std::max<int64_t>(1, kmeans_sample));
     Scratch sc;
     int32_t *rows = sc.alloc<int32_t>(n);
-    if (n == N) {
-        std::vector<int32_t> h(n);
-        for (int64_t i = 0; i < n; i++) h[i] = (int32_t)i;
-        CRISP_CUDA(cudaMemcpy(rows, h.data(), n * 4, cudaMemcpyHostToDevice));
-    } else {
-        sample_rows(N, n, seed, STREAM_KM_SAMPLE, rows, s);
-    }
+    sample_or_all(N, n, seed, STREAM_KM_SAMPLE, rows, s);
     float *S = sc.alloc<float>((size_t)n * Dp);
     // gather with pitch Dp (the padded dims of X are zero)
     {
@@ -993,7 +1009,7 @@ __global__ void k_check_finite(const float *X, int64_t N, int64_t pitch, int D, 
 // ---------------------------------------------------------------------------
 void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, const float *cb_inj,
                  int64_t kmeans_sample, int32_t kmeans_iters, int32_t rotation_mode, float tau_cev, uint64_t seed,
-                 cudaStream_t s) {
+                 cudaStream_t s, const double *cev_given) {
     const int64_t N = ix->N;
     // X <- data, zero padded to pitch
     CRISP_CUDA(cudaMemsetAsync(ix->X, 0, (size_t)N * ix->pitch * 4, s));
@@ -1010,8 +1026,9 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
         CRISP_CUDA(cudaStreamSynchronize(s));
         CRISP_CHECK(hb == 0, "data contains non-finite values");
     }
-    // spectral check on the original D columns
-    ix->cev = compute_cev(ix->X, N, ix->pitch, ix->D, seed, s);
+    // spectral check on the original D columns; a model build over a
+    // gathered sample (build_model) supplies the global sample's CEV instead
+    ix->cev = cev_given ? *cev_given : compute_cev(ix->X, N, ix->pitch, ix->D, seed, s);
     bool rotate;
     if (R_inj) rotate = true;
     else if (cb_inj) rotate = false;  // injected build without R: no rotation
@@ -1047,4 +1064,8 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
     CRISP_CUDA(cudaStreamSynchronize(s));
 }
 
+}  // namespace crisp
+
+namespace crisp {
+double cev_of_sample(const float *S_dev, int64_t n, int D, cudaStream_t s) { return cev_of_rows(S_dev, n, D, s); }
 }  // namespace crisp

@@ -69,6 +69,8 @@ struct crisp_index {
     double *Rn2 = nullptr;     // Dp: column 2-norms (x 1.01)
     float *Rt = nullptr;       // Dp x Dp: R transposed (the certified rotation's exact recompute)
     float *cb = nullptr;       // M x 2 x K x dh
+    float *cbp = nullptr;      // 2M x 64 x DHP: codebooks padded for the a1 screen (probe_tc.cu)
+    double *cn2 = nullptr;     // 2M x K: centroid squared norms (fp64) for the screen
     int32_t *cells = nullptr;  // M x N
     int32_t *ids = nullptr;    // M x N CSR ids
     int32_t *off2 = nullptr;   // M x K^2 x (NB+1): start of ids >= b*BS inside cell c
@@ -103,7 +105,11 @@ void cell_size_maxima(crisp_index *ix, const int32_t *sizes_host);
 
 // build steps (build.cu)
 void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, const float *cb_inj, int64_t kmeans_sample,
-                 int32_t kmeans_iters, int32_t rotation_mode, float tau_cev, uint64_t seed, cudaStream_t s);
+                 int32_t kmeans_iters, int32_t rotation_mode, float tau_cev, uint64_t seed, cudaStream_t s,
+                 const double *cev_given = nullptr);
+int64_t cev_sample_size(int64_t N);
+void sample_row_ids(int64_t N, int64_t n, uint64_t seed, uint32_t stream, int32_t *rows_dev, cudaStream_t s);
+double cev_of_sample(const float *S_dev, int64_t n, int D, cudaStream_t s);
 void finish_csr(crisp_index *ix, cudaStream_t s);
 
 // fp64 sequential-order GEMM: Y(rows x Dp, pitch ldy) = fl32(X(rows x Dp, pitch ldx) . R(Dp x Dp))
@@ -115,6 +121,18 @@ void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64
 void rotate_rows(crisp_index *ix, const float *X, int64_t rows, int64_t ldx, float *Y, int64_t ldy, cudaStream_t s);
 void rotate_rows_f64(const float *X, int64_t rows, int32_t Dp, int64_t ldx, const float *R, float *Y, int64_t ldy,
                      cudaStream_t s);
+
+// a1 screen on the tensor cores (probe_tc.cu): per (query, half-subspace) the
+// threshold t (the RQ-th smallest certified upper bound of dist64) and the mask
+// of the centroids whose certified lower bound is <= t
+struct ScreenOut {
+    float t;
+    int32_t pad;
+    unsigned long long mask;
+};
+bool screen_supported(const crisp_index *ix);
+void screen_halves(crisp_index *ix, const float *qrot, int64_t q0, int64_t q1, ScreenOut *scr, int RQ,
+                   cudaStream_t s);
 
 // search (search.cu)
 struct SearchOut {

@@ -35,6 +35,7 @@
 #include <tuple>
 
 #include "crisp_internal.cuh"
+#include "tc_util.cuh"
 
 namespace crisp {
 
@@ -191,66 +192,17 @@ constexpr int NA = 4;                                          // A ring: digit-
 constexpr int SMEM_TILES = 2 * SL * B_TILE + NA * A_TILE;      // B double-buffered (2 x 56 KB) + A ring (64 KB)
 constexpr int THREADS_TC = 128;                                // warp 0: TMA, warp 1: MMA issue; all 4: epilogue
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-// wait until the phase of the given parity has completed (a fresh barrier counts its
-// "previous" phase, parity 1, as complete: producers start waiting on parity 1)
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    const uint32_t a = smem_u32(bar);
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(a), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t *bar) {  // converged warp; one elected lane commits
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
-        : "memory");
-}
-// K-major operand, 128-byte swizzle: 8-row atoms of 1024 bytes (SBO), version 1 (sm_100)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3fff);        // start address
-    d |= (uint64_t)1 << 16;                          // leading byte offset (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset: next 8-row group
-    d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
-    return d;
-}
+using tcu::mbar_expect_tx;
+using tcu::mbar_init;
+using tcu::mbar_wait;
+using tcu::mma_commit;
+using tcu::smem_u32;
+using tcu::sw128_desc;
+using tcu::tma_load_2d;
 // instruction descriptor: s8 x s8 -> s32, K-major A and B, M = 128, N = 64
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-
-// issued by one elected lane of a converged warp (the elect sits inside the asm, so the
-// compiler does not wrap every MMA in its own election loop)
+constexpr uint32_t IDESC = tcu::idesc(2u, 1u, BM, BN);
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
-        : "memory");
+    tcu::mma<0>(d_tmem, a, b, IDESC, accumulate);
 }
 
 // Pipeline: per k-block the seven R planes b_1..b_7 go to one of two B buffers and
@@ -264,7 +216,8 @@ __global__ void __launch_bounds__(THREADS_TC, 1)
              const double *__restrict__ rn2, float *__restrict__ Y, int64_t ldy, unsigned long long *__restrict__ nfall,
              int64_t *__restrict__ flist) {
     extern __shared__ __align__(1024) unsigned char smraw[];
-    unsigned char *base = (unsigned char *)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+    // 1024-byte aligned (the 128-byte swizzle atoms), keeping the shared-memory provenance
+    unsigned char *base = smraw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smraw) & 1023u)) & 1023u);
     unsigned char *Bs = base;                          // 2 x SL tiles of B_TILE
     unsigned char *As = base + 2 * SL * B_TILE;        // NA tiles of A_TILE
     __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[NA], emptyA[NA], done;

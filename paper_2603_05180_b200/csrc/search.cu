@@ -69,7 +69,9 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
                                                     const float *__restrict__ cb, int M, int K, int dh,
                                                     const int32_t *__restrict__ gsize, int smem_gsize, int64_t budget,
                                                     int wk, uint32_t *__restrict__ act, int32_t *__restrict__ act_len,
-                                                    int64_t *__restrict__ retrieved, int qpw, int smem_cb) {
+                                                    int64_t *__restrict__ retrieved, int qpw, int smem_cb,
+                                                    const ScreenOut *__restrict__ scr,
+                                                    unsigned long long *__restrict__ probe_stats) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int KK = K * K;
     const int m = blockIdx.y;
@@ -94,86 +96,150 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     __syncthreads();
     if (smem_gsize) gsm = gs;
     if (smem_cb) cbm = cbs;
-    // each warp takes qpw queries in turn (the codebooks and sizes staged once per CTA)
-    for (int qi = 0; qi < qpw; qi++) {
-    const int64_t q = q0 + ((int64_t)blockIdx.x * WARPS + warp) * qpw + qi;  // queries [q0, Qc)
-    if (q >= Qc) return;
-    const float *qm = qrot + q * pitch + (int64_t)m * 2 * dh;
-    for (int i = lane; i < 2 * dh; i += 32) qs[i] = (double)qm[i];
-    __syncwarp();
-    // half distances (Alg. 1 l.4): dist64, exactly the oracle's order (the query
-    // converted once; with staged codebooks the compiler sees shared loads)
-    for (int side = 0; side < 2; side++) {
-        if (smem_cb) {
-            const float *C = cbs + side * K * cst;
-            for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64_qd(qs + side * dh, C + c * cst, dh);
-        } else {
-            const float *C = cbm + (int64_t)side * K * cst;
-            for (int c = lane; c < K; c += 32) tmp[side * K + c] = dist64_qd(qs + side * dh, C + (int64_t)c * cst, dh);
-        }
-    }
-    __syncwarp();
-    // sort each half by (delta, c) via ranks
-    for (int side = 0; side < 2; side++) {
-        const double *t = tmp + side * K;
-        double *dst = side ? b : a;
-        unsigned char *pdst = side ? pb : pa;
-        for (int c = lane; c < K; c += 32) {
-            double v = t[c];
-            int r = 0;
-            for (int c2 = 0; c2 < K; c2++) {
-                double u = t[c2];
-                r += (u < v) || (u == v && c2 < c);
+    // dist64 of this query's half `side` to centroid c (exactly the oracle's order)
+    auto half_dist = [&](int side, int c) -> double {
+        return smem_cb ? dist64_qd(qs + side * dh, cbs + (side * K + c) * cst, dh)
+                       : dist64_qd(qs + side * dh, cbm + (int64_t)(side * K + c) * cst, dh);
+    };
+    // every centroid exact, each half sorted by (delta, c) via ranks
+    auto full_halves = [&]() {
+        for (int side = 0; side < 2; side++)
+            for (int c = lane; c < K; c += 32) tmp[side * K + c] = half_dist(side, c);
+        __syncwarp();
+        for (int side = 0; side < 2; side++) {
+            const double *t = tmp + side * K;
+            double *dst = side ? b : a;
+            unsigned char *pdst = side ? pb : pa;
+            for (int c = lane; c < K; c += 32) {
+                double v = t[c];
+                int r = 0;
+                for (int c2 = 0; c2 < K; c2++) {
+                    double u = t[c2];
+                    r += (u < v) || (u == v && c2 < c);
+                }
+                dst[r] = v;
+                pdst[r] = (unsigned char)c;
             }
-            dst[r] = v;
-            pdst[r] = (unsigned char)c;
         }
-    }
-    for (int i = lane; i < K; i += 32) col[i] = 0;
-    __syncwarp();
-    // Multi-Sequence as a staircase argmin over (a_i + b_col[i], i)
-    uint32_t *out = act + (q * M + m) * (int64_t)KK;
-    int rank = 0;
-    int64_t ret = 0;
-    while (ret < budget && rank < KK) {
-        double bc = INFINITY;
-        int bi = 0x7fffffff;
-        for (int i = lane; i < K; i += 32) {
-            int ci = col[i];
-            if (ci < K && (i == 0 || col[i - 1] > ci)) {
-                double cost = __dadd_rn(a[i], b[ci]);
-                if (cost < bc) {  // rows visited in ascending i: first wins ties
-                    bc = cost;
-                    bi = i;
+        __syncwarp();
+    };
+    // each query: the (q, m) activated list, or false if the walk needs a rank at or past
+    // the certified prefixes (ra, rb) of the half sorts (then the caller redoes it exactly)
+    auto walk = [&](int64_t q, int ra, int rb) -> bool {
+        for (int i = lane; i < K; i += 32) col[i] = 0;
+        __syncwarp();
+        // Multi-Sequence as a staircase argmin over (a_i + b_col[i], i)
+        uint32_t *out = act + (q * M + m) * (int64_t)KK;
+        int rank = 0;
+        int64_t ret = 0;
+        while (ret < budget && rank < KK) {
+            double bc = INFINITY;
+            int bi = 0x7fffffff;
+            bool past = false;
+            for (int i = lane; i < K; i += 32) {
+                int ci = col[i];
+                if (ci < K && (i == 0 || col[i - 1] > ci)) {
+                    if (i >= ra || ci >= rb) {
+                        past = true;
+                        continue;
+                    }
+                    double cost = __dadd_rn(a[i], b[ci]);
+                    if (cost < bc) {  // rows visited in ascending i: first wins ties
+                        bc = cost;
+                        bi = i;
+                    }
                 }
             }
-        }
+            if (__any_sync(0xffffffffu, past)) return false;
 #pragma unroll
-        for (int off = 16; off; off >>= 1) {
-            double oc = __shfl_xor_sync(0xffffffffu, bc, off);
-            int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-            if (oc < bc || (oc == bc && oi < bi)) {
-                bc = oc;
-                bi = oi;
+            for (int off = 16; off; off >>= 1) {
+                double oc = __shfl_xor_sync(0xffffffffu, bc, off);
+                int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (oc < bc || (oc == bc && oi < bi)) {
+                    bc = oc;
+                    bi = oi;
+                }
             }
+            const int j = col[bi];
+            const int cell = pa[bi] * K + pb[j];
+            rank++;
+            const int w = (wk > 0 && rank <= wk) ? 2 : 1;  // Alg. 1 l.10-12
+            __syncwarp();
+            if (lane == 0) {
+                out[rank - 1] = (uint32_t)cell | ((uint32_t)w << 16);
+                col[bi] = (unsigned char)(j + 1);
+            }
+            ret += gsm[cell];
+            __syncwarp();
         }
-        const int j = col[bi];
-        const int cell = pa[bi] * K + pb[j];
-        rank++;
-        const int w = (wk > 0 && rank <= wk) ? 2 : 1;  // Alg. 1 l.10-12
-        __syncwarp();
         if (lane == 0) {
-            out[rank - 1] = (uint32_t)cell | ((uint32_t)w << 16);
-            col[bi] = (unsigned char)(j + 1);
+            act_len[q * M + m] = rank;
+            retrieved[q * M + m] = ret;
         }
-        ret += gsm[cell];
         __syncwarp();
+        return true;
+    };
+    unsigned long long n_exact = 0, n_redo = 0;
+    // each warp takes qpw queries in turn (the codebooks and sizes staged once per CTA)
+    for (int qi = 0; qi < qpw; qi++) {
+        const int64_t q = q0 + ((int64_t)blockIdx.x * WARPS + warp) * qpw + qi;  // queries [q0, Qc)
+        if (q >= Qc) break;
+        const float *qm = qrot + q * pitch + (int64_t)m * 2 * dh;
+        for (int i = lane; i < 2 * dh; i += 32) qs[i] = (double)qm[i];
+        __syncwarp();
+        if (scr) {
+            // a1 screened (probe_tc.cu): per half, t = the RQ-th smallest certified upper bound
+            // and the mask of the centroids whose lower bound is <= t -- the only ones that can
+            // be among the RQ smallest dist64 values; dist64 runs for them alone, and those with
+            // dist64 <= t are, in (delta, c) order, exactly the first r of the full sort (every
+            // other centroid has dist64 > t)
+            int rr[2];
+            for (int side = 0; side < 2; side++) {
+                const ScreenOut so = scr[(q - q0) * 2 * M + 2 * m + side];
+                const unsigned long long mk = so.mask;
+                const double t = (double)so.t;
+                const int S = __popcll(mk);
+                // the members, listed in ascending c (col[] is scratch until the walk)
+                for (int c = lane; c < K; c += 32)
+                    if ((mk >> c) & 1ull) col[__popcll(mk & ((1ull << c) - 1ull))] = (unsigned char)c;
+                __syncwarp();
+                double *tt = tmp + side * K;
+                for (int i = lane; i < S; i += 32) tt[i] = half_dist(side, col[i]);
+                __syncwarp();
+                double *dst = side ? b : a;
+                unsigned char *pdst = side ? pb : pa;
+                int nval = 0;
+                for (int i = lane; i < S; i += 32) {
+                    const double v = tt[i];
+                    const int c = col[i];
+                    int r = 0;
+                    for (int i2 = 0; i2 < S; i2++) {  // members in ascending c: ties by c = by i2
+                        const double u = tt[i2];
+                        r += (u < v) || (u == v && i2 < i);
+                    }
+                    dst[r] = v;
+                    pdst[r] = (unsigned char)c;
+                    nval += v <= t;
+                }
+                n_exact += (lane == 0) ? S : 0;
+                __syncwarp();
+                for (int off = 16; off; off >>= 1) nval += __shfl_xor_sync(0xffffffffu, nval, off);
+                rr[side] = nval;
+                __syncwarp();
+            }
+            if (walk(q, rr[0], rr[1])) continue;
+            n_redo++;
+        }
+        full_halves();
+        if (scr) n_exact += (lane == 0) ? 2 * K : 0;
+        walk(q, K, K);
     }
-    if (lane == 0) {
-        act_len[q * M + m] = rank;
-        retrieved[q * M + m] = ret;
-    }
-    __syncwarp();
+    if (probe_stats) {
+        for (int off = 16; off; off >>= 1) n_exact += __shfl_xor_sync(0xffffffffu, n_exact, off);
+        if (lane == 0) {
+            atomicAdd(probe_stats, n_exact);
+            atomicAdd(probe_stats + 1, n_redo);
+        }
     }
 }
 
@@ -2790,6 +2856,12 @@ __global__ void __launch_bounds__(THREADS, 4) k_patience_tail(const float *__res
 // cells), [1] sum |C_q|, [2] rows verified, [3] fallback queries
 // ---------------------------------------------------------------------------
 __device__ unsigned long long d_stats[4];
+__device__ unsigned long long d_probe_stats[2];  // a1: exact half distances computed, screened walks redone exactly
+static unsigned long long *d_probe_stats_ptr() {
+    void *p = nullptr;
+    cudaGetSymbolAddress(&p, d_probe_stats);
+    return (unsigned long long *)p;
+}
 
 __global__ void k_stats(const uint32_t *__restrict__ act, const int32_t *__restrict__ act_len, int M, int KK,
                         const int32_t *__restrict__ off2, int NB, const int32_t *__restrict__ ncand, int NS,
@@ -2916,6 +2988,8 @@ struct Work {
     int k, mode;
     int64_t Qc, CAPQ;
     int rgroup = 0, segw = 0, RW = 0, NR = 0, GR = 0, rg_smem = 0;  // grouped phi=0 re-rank
+    ScreenOut *scr = nullptr;  // a1 screen (Qc x 2M), if the screen runs
+    int probe_r = 24;
     int S, S1, HS, S0, R0, BPC, count_kernel, count_atom, NS, CF, ham_fused, rows4, ad, adsp, F, DS, round_rows, nl_min, Pq,
         vra_smem;
     // end of the speculative rounds (positions the Hamming order must cover)
@@ -2964,6 +3038,7 @@ struct Work {
         const int S0 = std::max({first_round(ix, k), std::max(64, env_int("CRISP_PATIENCE_BATCH", 1024)),
                                  (int)std::min<int64_t>(1 << 16, std::max<int64_t>(patience_rows(ix, k), 1024))});
         int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 8 + (int64_t)ix->M * 12 + CAPQ * 4 + 4 +
+                       (int64_t)ix->M * 2 * 16 +
                        (int64_t)ix->NBW * 8 + 64;
         if (mode == 0) perq += (int64_t)std::max<int64_t>(S, (ix->N + 4095) / 4096) * k * 16;
         else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
@@ -3082,6 +3157,11 @@ struct Work {
         probe_gs = (KK * 4 <= 48 * 1024) ? 1 : 0;
         probe_cb = (2 * K * (ix->dh | 1) * 4 <= 96 * 1024) ? 1 : 0;  // rows padded to an odd stride
         probe_qpw = std::max(1, env_int("CRISP_PROBE_QPW", 4));  // queries per warp in k_probe
+        // a1 screen on the tensor cores (CRISP_PROBE_SCREEN=0 disables); dist64 for the
+        // centroids that can reach the probe_r smallest of each half
+        probe_r = std::max(1, env_int("CRISP_PROBE_R", 24));
+        if (env_int("CRISP_PROBE_SCREEN", 1) && screen_supported(ix))
+            scr = buf.alloc<ScreenOut>((size_t)Qc * 2 * M);
         probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + (probe_cb ? ((2 * K * (ix->dh | 1) * 4 + 15) & ~15) : 0) +
                      WARPS * ((((4 * K + 2 * ix->dh) * 8) + 3 * K + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
@@ -3111,9 +3191,14 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
     const int P = (hq && qn >= 2048) ? std::max(1, std::min(16, env_int("CRISP_H2D_PARTS", 3))) : 1;
     auto probe = [&](int64_t r0, int64_t r1) {
         dim3 g(nblk(r1 - r0, WARPS * w.probe_qpw), M);
+        if (w.scr) {  // a1's contraction on the tensor cores: certified screen intervals (probe_tc.cu)
+            screen_halves(const_cast<crisp_index *>(ix), w.qrot, r0, r1, w.scr, w.probe_r, s);
+            g_launches++;
+        }
         k_probe<<<g, THREADS, w.probe_smem, s>>>(w.qrot, pitch, r0, r1, ix->cb, M, K, ix->dh, ix->gsize, w.probe_gs,
                                                  ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr,
-                                                 w.probe_qpw, w.probe_cb);
+                                                 w.probe_qpw, w.probe_cb, w.scr,
+                                                 g_timing ? d_probe_stats_ptr() : nullptr);
         CRISP_LAUNCH();
         g_launches++;
     };
@@ -3576,16 +3661,20 @@ extern "C" crisp_status crisp_set_stage_timing(int32_t on) {
 }
 
 extern "C" crisp_status crisp_search_counters(int64_t *out, int32_t n, int32_t reset) {
-    unsigned long long h[4];
-    if (cudaMemcpyFromSymbol(h, crisp::d_stats, sizeof(h)) != cudaSuccess) {
+    unsigned long long h[4], hp[2];
+    if (cudaMemcpyFromSymbol(h, crisp::d_stats, sizeof(h)) != cudaSuccess ||
+        cudaMemcpyFromSymbol(hp, crisp::d_probe_stats, sizeof(hp)) != cudaSuccess) {
         crisp::set_error("cudaMemcpyFromSymbol failed");
         return CRISP_ECUDA;
     }
     for (int i = 0; i < 4 && i < n; i++) out[i] = (int64_t)h[i];
     if (n > 4) out[4] = crisp::g_launches;
+    if (n > 5) out[5] = (int64_t)hp[0];
+    if (n > 6) out[6] = (int64_t)hp[1];
     if (reset) {
         unsigned long long z[4] = {0, 0, 0, 0};
         cudaMemcpyToSymbol(crisp::d_stats, z, sizeof(z));
+        cudaMemcpyToSymbol(crisp::d_probe_stats, z, 2 * sizeof(unsigned long long));
         crisp::g_launches = 0;
     }
     return CRISP_OK;

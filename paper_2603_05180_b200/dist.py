@@ -1,6 +1,9 @@
 """Point-sharded multi-GPU search: one process per GPU.
 
 Collective call sites:
+  N0     all-gathers of each rank's rows of the CEV and k-means samples (fixed
+         global ids of the counter-based sampler) to rank 0, which builds the
+         model (crisp_build_model: the R and codebooks of a build over all rows)
   N1/N2  broadcast of R and the codebooks from rank 0 (shared by every shard)
   N3     all-reduce (sum) of the local cell sizes -> global sizes, so every
          shard's budget walk activates exactly the cells a single index would
@@ -28,14 +31,14 @@ class CudaEngine:
         self.device = device
         self.index = None
 
-    def build_global(self, X, M, **params):
-        """Full build on this rank (rank 0): the shared (R or None, codebooks)
-        come from the global CEV sample and the global k-means sample."""
-        ix = self.crisp.Index.build(X, M, **params)
-        e = ix.export()
-        ix.free()
-        R = torch.from_numpy(e["R"]) if e["R"] is not None else None
-        return R, torch.from_numpy(e["codebooks"])
+    def build_model(self, cev_rows, km_rows, M, **params):
+        """crisp_build_model on this rank (rank 0) from the gathered sample rows."""
+        R, cb, _ = self.crisp.build_model(cev_rows, km_rows, M, **params)
+        return (torch.from_numpy(R) if R is not None else None), torch.from_numpy(cb)
+
+    def sample_ids(self, N_global, seed, kmeans_sample=100000):
+        cev_ids, km_ids = self.crisp.model_samples(N_global, seed, kmeans_sample)
+        return torch.from_numpy(cev_ids.astype(np.int64)), torch.from_numpy(km_ids.astype(np.int64))
 
     def build_shard(self, X_shard, gid_base, M, R, codebooks, **params):
         R = R.cpu().numpy() if R is not None else None
@@ -111,6 +114,47 @@ def share_model(R, codebooks, like, src=0):
         Rt = R.to(like.device) if R is not None else torch.empty((Dp, Dp), dtype=torch.float32, device=like.device)
         dist.broadcast(Rt, src)
     return Rt, cb
+
+
+def gather_sample_rows(X_local, lo, ids, dst=0):
+    """Rows `ids` (ascending global ids) of the point-sharded dataset, gathered on
+    rank dst in ascending global id: each rank contributes its rows in [lo,
+    lo + len(X_local)) (a padded all-gather; shards are contiguous id ranges in
+    rank order, so concatenating by rank keeps the order).  Returns the (n, D)
+    tensor on rank dst, None elsewhere."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    dev = _coll_device()
+    ids = torch.as_tensor(ids, dtype=torch.int64)
+    hi = lo + X_local.shape[0]
+    mine = ids[(ids >= lo) & (ids < hi)] - lo
+    rows = X_local[mine.to(X_local.device)].to(dev).contiguous()
+    cnt = torch.tensor([rows.shape[0]], dtype=torch.int64, device=dev)
+    cnts = [torch.empty_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt)
+    mx = int(max(int(c.item()) for c in cnts))
+    D = X_local.shape[1]
+    pad = torch.zeros((mx, D), dtype=rows.dtype, device=dev)
+    pad[: rows.shape[0]] = rows
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad)
+    if rank != dst:
+        return None
+    return torch.cat([o[: int(c.item())] for o, c in zip(outs, cnts)])
+
+
+def model_from_shards(engine, X_local, lo, N_global, M, seed, kmeans_sample=100000, **params):
+    """N1/N2 without a full index on one rank: every rank contributes its rows of
+    the CEV and k-means samples (fixed global row ids, counter-based sampling),
+    rank 0 builds the model (R, codebooks) from them (crisp_build_model), and the
+    model is broadcast (share_model).  Identical to a single build over all rows."""
+    cev_ids, km_ids = engine.sample_ids(N_global, seed, kmeans_sample)
+    cev_rows = gather_sample_rows(X_local, lo, cev_ids)
+    km_rows = gather_sample_rows(X_local, lo, km_ids)
+    R = cb = None
+    if dist.get_rank() == 0:
+        R, cb = engine.build_model(cev_rows.cpu().numpy(), km_rows.cpu().numpy(), M, seed=seed,
+                                   kmeans_sample=kmeans_sample, **params)
+    return share_model(R, cb, torch.empty(0, device=_coll_device()))
 
 
 def global_cell_sizes(engine):

@@ -178,3 +178,39 @@ def test_sharded_orchestration_matches_single_index():
     assert ok.sum() >= 10
     assert np.array_equal(res["ids"][ok], ids[ok])
     assert np.allclose(res["d"][ok], d[ok].astype(np.float32))
+
+
+def _gather_worker(rank, world, port, N, D, ids, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_05180_b200 import dist as cdist
+
+    X = torch.arange(N * D, dtype=torch.float32).reshape(N, D)
+    lo, hi = cdist.shard_range(N, rank, world)
+    got = cdist.gather_sample_rows(X[lo:hi], lo, torch.from_numpy(ids))
+    if rank == 0:
+        torch.save(got, out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_sample_rows(world):
+    """The model build's sample rows (fixed global ids from the counter-based
+    sampler, here the oracle's) gathered from point shards arrive on rank 0 in
+    ascending global id, equal to the rows of the whole dataset."""
+    import oracle
+
+    N, D = 1003, 5
+    ids = oracle.sample_rows(N, 101, 7, 1)
+    assert np.all(np.diff(ids) > 0)
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "g.pt")
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        mp.spawn(_gather_worker, args=(world, port, N, D, ids, out), nprocs=world, join=True)
+        got = torch.load(out)
+    X = np.arange(N * D, dtype=np.float32).reshape(N, D)
+    assert np.array_equal(got.numpy(), X[ids])

@@ -625,3 +625,56 @@ def test_adsampling_rejects_bad_stride(crisp):
         ix.set_adsampling(True, 2.1, 24)
     with pytest.raises(crisp.CrispError):
         ix.set_adsampling(True, -1.0, 32)
+
+
+@pytest.mark.parametrize("rotation", [1, -1])
+def test_model_from_gathered_samples_equals_full_build(crisp, rotation):
+    """crisp_build_model on the gathered CEV and k-means sample rows (the
+    multi-GPU model build) gives exactly the rotation, the
+    codebooks and the CEV of crisp_build over all rows; the library's sampled
+    row ids equal the oracle's (both implement the counter-based sampler)."""
+    w = synth.Workload(2, D=96)
+    X = w.base(30000).numpy()
+    params = dict(K=8, kmeans_iters=4, kmeans_sample=5000, seed=11, rotation=rotation)
+    full = crisp.Index.build(X, 4, **params)
+    e, info = full.export(), full.info()
+    cev_ids, km_ids = crisp.model_samples(30000, 11, 5000)
+    assert np.array_equal(cev_ids, oracle.sample_rows(30000, oracle.cev_sample_size(30000), 11, 1))
+    assert np.array_equal(km_ids, oracle.sample_rows(30000, 5000, 11, 3))
+    R, cb, cev = crisp.build_model(X[cev_ids], X[km_ids], 4, **params)
+    assert cev == info["cev"]
+    assert (R is not None) == bool(info["rotated"])
+    if R is not None:
+        assert np.array_equal(R, e["R"])
+    assert np.array_equal(cb, e["codebooks"])
+    full.free()
+
+
+@pytest.mark.parametrize("screen,R", [("1", "1"), ("1", "3"), ("1", "24"), ("0", "24")])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_probe_screen_on_tensor_cores(crisp, monkeypatch, mode, screen, R):
+    """a1 with the tensor-core screen (probe_tc.cu): the activated cells, their
+    pop order and weights stay bit-exact whatever prefix length R the screen
+    certifies (R = 1 and 3 force most walks past the certified prefix and
+    through the exact redo), and equal the unscreened probe's."""
+    import torch
+
+    monkeypatch.setenv("CRISP_PROBE_SCREEN", screen)
+    monkeypatch.setenv("CRISP_PROBE_R", R)
+    X, Qv, ox = make_case(cfg=1, N=20000, D=256, Q=64, M=8, K=50, seed=0)
+    ix = build_gpu(crisp, X, ox)
+    B, tau, k = 300, 3, 10
+    ix.set_search_params(budget=B, tau=tau, patience_factor=40)
+    crisp.set_stage_timing(True)
+    crisp.search_counters(reset=True)
+    ids, d, t = ix.trace(Qv, k, mode)
+    cnt = crisp.search_counters(reset=True)
+    crisp.set_stage_timing(False)
+    torch.cuda.synchronize()
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, mode, B, tau, patience_factor=40, trace=True)
+    compare_trace(t, ot, mode, X.shape[0])
+    assert_topk_parity(ids, d, r_ids, r_d, f"screen={screen} R={R}")
+    if screen == "1" and R == "1":
+        assert cnt["probe_screen_redone"] > 0, "R = 1 must send walks through the exact redo"
+    if screen == "1" and R == "24":
+        assert cnt["probe_exact_half_distances"] < 64 * 8 * 2 * 50, "the screen must save exact half distances"

@@ -15,6 +15,8 @@ q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
 out["nvidia_smi_after"] = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader"], capture_output=True,
                                          text=True).stdout.strip()
 name = sys.argv[1] if len(sys.argv) > 1 else "r02_peaks"
-with open(os.path.join(ROOT, "profiles", name + ".json"), "w") as f:
+for d in ("profiles", "gpurun_out"):
+    os.makedirs(os.path.join(ROOT, d), exist_ok=True)
+with open(os.path.join(ROOT, "gpurun_out", name + ".json"), "w") as f:
     json.dump(out, f, indent=1)
 print(json.dumps(out))
