@@ -634,10 +634,12 @@ def run_sweep(args):
         t0 = time.time()
         ix = crisp.Index.build(X, M, K=50, seed=c["seed"])
         log(f"built M={M} in {time.time() - t0:.1f}s rotated={ix.info()['rotated']} cev={ix.info()['cev']:.3f}")
+        pfs = [int(x) for x in args.sweep_patience.split(",")]
         for mode in modes:
+          for pf in (pfs if mode != 0 else [40]):
             for beta in betas:
                 for alpha in alphas:
-                    ix.set_search_params(beta=beta, alpha=alpha, patience_factor=40)
+                    ix.set_search_params(beta=beta, alpha=alpha, patience_factor=pf)
                     ix.set_adsampling(mode == 2)
                     ix.search_async(Qd, k, phi(mode), ids, dd, stream)
                     torch.cuda.synchronize()
@@ -647,8 +649,8 @@ def run_sweep(args):
                     e1.record()
                     torch.cuda.synchronize()
                     ms = e0.elapsed_time(e1)
-                    r = dict(cfg=cfg, M=M, mode=mode, beta=beta, alpha=alpha, recall=recall_at(ids, gt, 10),
-                             qps=Q / ms * 1e3, ms=ms)
+                    r = dict(cfg=cfg, M=M, mode=mode, beta=beta, alpha=alpha, patience_factor=pf,
+                             recall=recall_at(ids, gt, 10), qps=Q / ms * 1e3, ms=ms)
                     rows.append(r)
                     print(json.dumps(r), flush=True)
         ix.free()
@@ -678,6 +680,7 @@ def main():
     ap.add_argument("--sweep-beta", default="0.005,0.01,0.02,0.04")
     ap.add_argument("--sweep-alpha", default="0.1,0.2,0.3,0.4")
     ap.add_argument("--sweep-modes", default="0,1")
+    ap.add_argument("--sweep-patience", default="40", help="patience factors for phi=1 (P = factor * k; P:L713-718)")
     args = ap.parse_args()
     if args.warmup < 3 and not args.sweep:
         log("warning: fewer than 3 warm-up steps")

@@ -68,6 +68,9 @@ typedef struct {
     int32_t tau;               /* if > 0 overrides alpha: integer collision threshold */
     int32_t patience_factor;   /* P = patience_factor * k (default 40); 0 = disabled */
     int64_t workspace_bytes;   /* per-search scratch cap (query chunking); 0 = default: half the free device memory, in [4, 64] GiB */
+    int32_t rotation_block;    /* 0: global rotation when it applies; b > 0: block-wise variance
+                                  redistribution (DESIGN R16): rotate only the dimensions of the b
+                                  subspaces of largest sample variance, R = I elsewhere */
 } crisp_params;
 
 typedef struct {
@@ -89,6 +92,7 @@ typedef struct {
     int64_t logical_bytes; /* 4ND + 4MN + 8M(K^2+1) + codebooks + 8*ceil(D/64)*N + 4D^2 if rotated */
     double slice_hint;  /* expected ids per activated slice and 4096-id warp sub-block: >= 8 selects the
                            warp-owned collision-count kernel, else the CTA-flattened one (env CRISP_COUNT_KERNEL) */
+    int32_t rotation_block; /* subspaces of a block-wise rotation (0: global or none) */
 } crisp_index_info_t;
 
 /* Host buffers filled by crisp_export (any may be NULL to skip). */

@@ -185,6 +185,46 @@ def cev(X, seed: int) -> float:
     return cev_from_eigs(w)
 
 
+def dim_variances(X, seed: int):
+    """Per-dimension variances of the CEV sample (the diagonal of its covariance,
+    divisor n-1), fp64; zeros if the sample has fewer than 2 rows."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    N, D = X.shape
+    n = cev_sample_size(N)
+    if n < 2:
+        return np.zeros(D)
+    rows = np.arange(N, dtype=np.int64) if n == N else sample_rows(N, n, seed, 1)
+    return np.diag(covariance(X, rows)).copy()
+
+
+def rotation_block(var, M: int, Dp: int, b: int):
+    """Block-wise variance redistribution (reading R16): the b subspaces
+    of largest variance energy E_m = sum of the per-dimension variances of
+    their 2 d_h dimensions (summed in ascending dimension, fp64; ties to the
+    smaller m), returned as their dimensions in ascending order."""
+    v = np.zeros(Dp)
+    v[: len(var)] = var
+    w = Dp // M
+    E = []
+    for m in range(M):
+        e = 0.0
+        for i in range(m * w, (m + 1) * w):
+            e += v[i]
+        E.append(e)
+    top = sorted(range(M), key=lambda m: (-E[m], m))[:b]
+    return np.concatenate([np.arange(m * w, (m + 1) * w) for m in sorted(top)])
+
+
+def blockwise_rotation(X, M: int, Dp: int, b: int, seed: int):
+    """R = I except on the block's dimensions, where it is Q of QR of a d_sub x
+    d_sub Gaussian (the rotation of P:L225 restricted to the block)."""
+    blk = rotation_block(dim_variances(X, seed), M, Dp, b)
+    Rs, _ = rotation(len(blk), seed)
+    R = np.eye(Dp, dtype=np.float32)
+    R[np.ix_(blk, blk)] = Rs
+    return R, blk
+
+
 def qr(G):
     A = np.array(G, dtype=np.float64, order="C", copy=True)
     D = A.shape[0]
@@ -338,7 +378,8 @@ def max_threads() -> int:
 # Composition: build (P:L249-256 phases 1-2) and search (Alg. 1)
 # --------------------------------------------------------------------------
 def build(X, M: int, K: int = 50, tau_cev: float = 0.85, rotation_mode: int = -1, kmeans_iters: int = 20,
-          kmeans_sample: int = 100000, seed: int = 0, R=None, codebooks=None, gid_base: int = 0):
+          kmeans_sample: int = 100000, seed: int = 0, R=None, codebooks=None, gid_base: int = 0,
+          rotation_block: int = 0):
     """Index build: spectral check + adaptive rotation, codebooks,
     cell assignment, CSR, binary codes.
 
@@ -356,7 +397,9 @@ def build(X, M: int, K: int = 50, tau_cev: float = 0.85, rotation_mode: int = -1
     else:
         rotated = (cev_v > tau_cev) if rotation_mode < 0 else bool(rotation_mode)  # strict ">" (Z15)
         if rotated:
-            R, _ = rotation(Dp, seed)
+            # rotation_block = b > 0: block-wise variance redistribution over the b subspaces of
+            # largest variance energy (reading R16); else the global rotation
+            R = blockwise_rotation(X, M, Dp, rotation_block, seed)[0] if rotation_block > 0 else rotation(Dp, seed)[0]
     if rotated:
         Xp = rotate_rows(Xp, R)
     if codebooks is None:

@@ -34,7 +34,7 @@ class Params(C.Structure):
         ("M", C.c_int32), ("K", C.c_int32), ("tau_cev", C.c_float), ("rotation", C.c_int32),
         ("kmeans_iters", C.c_int32), ("kmeans_sample", C.c_int64), ("seed", C.c_uint64), ("device", C.c_int32),
         ("budget_ratio", C.c_double), ("budget", C.c_int64), ("min_collision_ratio", C.c_double), ("tau", C.c_int32),
-        ("patience_factor", C.c_int32), ("workspace_bytes", C.c_int64),
+        ("patience_factor", C.c_int32), ("workspace_bytes", C.c_int64), ("rotation_block", C.c_int32),
     ]
 
 
@@ -44,7 +44,7 @@ class Info(C.Structure):
         ("padded_D", C.c_int32), ("pitch", C.c_int32), ("M", C.c_int32), ("K", C.c_int32), ("dh", C.c_int32),
         ("rotated", C.c_int32), ("cev", C.c_double), ("budget", C.c_int64), ("tau", C.c_int32),
         ("patience_factor", C.c_int32), ("block_ids", C.c_int32), ("n_blocks", C.c_int32), ("hbm_bytes", C.c_int64),
-        ("logical_bytes", C.c_int64), ("slice_hint", C.c_double),
+        ("logical_bytes", C.c_int64), ("slice_hint", C.c_double), ("rotation_block", C.c_int32),
     ]
 
 

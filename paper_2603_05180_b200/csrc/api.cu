@@ -148,6 +148,8 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
     ix->pitch = ((ix->Dp + 3) / 4) * 4;
     ix->W = (ix->Dp + 63) / 64;
     ix->Wp = (ix->W + 7) / 8 * 8;
+    CRISP_CHECK(p->rotation_block >= 0 && p->rotation_block <= p->M, "rotation_block must be in [0, M]");
+    ix->rot_block = p->rotation_block;
     ix->BS = block_ids_for(N);
     ix->NB = (int32_t)((N + ix->BS - 1) / ix->BS);
     ix->SBW = ix->BS / 8;
@@ -312,15 +314,17 @@ crisp_status crisp_build_model(const float *cev_rows, int64_t n_cev, const float
             cudaStream_t s;
             ~SG() { cudaStreamDestroy(s); }
         } sg{s};
+        std::vector<double> var(D, 0.0);
         if (n_cev >= 2) {
             const float *cd = to_device(cev_rows, (size_t)n_cev * D, tf.v);
-            cev = cev_of_sample(cd, n_cev, D, s);
+            cev = cev_of_sample(cd, n_cev, D, s, &var);
         }
         const float *kd = to_device(km_rows, (size_t)n_km * D, tf.v);
-        // an index over the k-means sample: the same rotation (seed) and k-means (every row of
-        // the sample, ascending global id) as a build over the whole dataset
+        // an index over the k-means sample: the same rotation (seed; a block rotation from the
+        // CEV sample's variances) and k-means (every row of the sample, ascending global id) as
+        // a build over the whole dataset
         build_index(ix, kd, nullptr, nullptr, n_km, p->kmeans_iters > 0 ? p->kmeans_iters : 20, p->rotation,
-                    p->tau_cev, p->seed, s, &cev);
+                    p->tau_cev, p->seed, s, &cev, &var);
         *rotated_out = ix->rotated;
         if (cev_out) *cev_out = cev;
         if (ix->rotated && R_out)
@@ -444,6 +448,7 @@ crisp_status crisp_index_info(const crisp_index *ix, crisp_index_info_t *o) {
     o->block_ids = ix->BS;
     o->n_blocks = ix->NB;
     o->hbm_bytes = ix->hbm_bytes;
+    o->rotation_block = ix->rotated ? ix->rot_block : 0;
     const int64_t KK = (int64_t)ix->K * ix->K;
     o->logical_bytes = 4 * ix->N * ix->Dp + 4 * (int64_t)ix->M * ix->N + 8 * (int64_t)ix->M * (KK + 1) +
                        4 * (int64_t)ix->M * 2 * ix->K * ix->dh + 8 * (int64_t)ix->W * ix->N +

@@ -326,10 +326,14 @@ void sample_row_ids(int64_t N, int64_t n, uint64_t seed, uint32_t stream, int32_
     sample_or_all(N, n, seed, stream, rows_dev, s);
 }
 
-static double cev_of_rows(const float *S, int64_t n, int D, cudaStream_t s);
+static double cev_of_rows(const float *S, int64_t n, int D, cudaStream_t s, std::vector<double> *var = nullptr);
 
-static double compute_cev(const float *X, int64_t N, int64_t ld, int D, uint64_t seed, cudaStream_t s) {
+// the CEV of the dataset's sample; var (optional) receives the sample's per-dimension
+// variances (the covariance diagonal), zeros if the sample has fewer than 2 rows
+static double compute_cev(const float *X, int64_t N, int64_t ld, int D, uint64_t seed, cudaStream_t s,
+                          std::vector<double> *var = nullptr) {
     const int64_t n = cev_sample_size(N);
+    if (var) var->assign(D, 0.0);
     if (n < 2) return 0.0;
     Scratch sc;
     int32_t *rows = sc.alloc<int32_t>(n);
@@ -337,12 +341,13 @@ static double compute_cev(const float *X, int64_t N, int64_t ld, int D, uint64_t
     float *S = sc.alloc<float>((size_t)n * D);
     k_gather_rows<<<nblk(n * D, 256), 256, 0, s>>>(X, ld, rows, n, D, S);
     CRISP_LAUNCH();
-    return cev_of_rows(S, n, D, s);
+    return cev_of_rows(S, n, D, s, var);
 }
 
 // CEV of the sample rows S (n x D, packed, ascending global index): covariance with
 // divisor n-1 in the sequential fp64 order, eigenvalues, top floor(0.2 D) share
-static double cev_of_rows(const float *S, int64_t n, int D, cudaStream_t s) {
+static double cev_of_rows(const float *S, int64_t n, int D, cudaStream_t s, std::vector<double> *var) {
+    if (var) var->assign(D, 0.0);
     if (n < 2) return 0.0;
     Scratch sc;
     double *mu = sc.alloc<double>(D);
@@ -353,6 +358,10 @@ static double cev_of_rows(const float *S, int64_t n, int D, cudaStream_t s) {
     k_gemm_seq<<<grid, 256, 0, s>>>((int64_t)D, D, (int)n, LoadCentT{S, mu, D}, LoadCent{S, mu, D},
                                     StoreCov{Cm, D, 0.0, (double)(n - 1)});
     CRISP_LAUNCH();
+    if (var) {  // the per-dimension variances (block-wise rotation, R16), before the solver overwrites Cm
+        CRISP_CUDA(cudaMemcpy2DAsync(var->data(), 8, Cm, (size_t)(D + 1) * 8, 8, D, cudaMemcpyDeviceToHost, s));
+        CRISP_CUDA(cudaStreamSynchronize(s));
+    }
     // eigenvalues only (symmetric; layout irrelevant)
     cusolverDnHandle_t h;
     CRISP_SOLVER(cusolverDnCreate(&h));
@@ -1007,9 +1016,43 @@ __global__ void k_check_finite(const float *X, int64_t N, int64_t pitch, int D, 
 }
 
 // ---------------------------------------------------------------------------
+// Block-wise variance redistribution (reading R16): R = I except on the dimensions
+// of the rot_block subspaces of largest variance energy E_m (the sum of their 2 d_h
+// per-dimension sample variances, ascending dimension, fp64; ties to the smaller m), where
+// it is the rotation of P:L225 of that size (Q of QR of a Philox Gaussian, seed)
+static void make_block_rotation(crisp_index *ix, const std::vector<double> &var, uint64_t seed, cudaStream_t s) {
+    const int Dp = ix->Dp, M = ix->M, w = Dp / M, b = std::min(ix->rot_block, M);
+    std::vector<double> E(M, 0.0);
+    for (int m = 0; m < M; m++) {
+        double e = 0.0;
+        for (int i = m * w; i < (m + 1) * w; i++) e += i < (int)var.size() ? var[i] : 0.0;
+        E[m] = e;
+    }
+    std::vector<int> order(M);
+    for (int m = 0; m < M; m++) order[m] = m;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return E[x] > E[y]; });
+    std::vector<int> top(order.begin(), order.begin() + b);
+    std::sort(top.begin(), top.end());
+    std::vector<int> blk;
+    for (int m : top)
+        for (int i = m * w; i < (m + 1) * w; i++) blk.push_back(i);
+    const int ds = (int)blk.size();
+    Scratch sc;
+    float *Rs = sc.alloc<float>((size_t)ds * ds);
+    make_rotation(ds, seed, Rs, s);
+    std::vector<float> hs((size_t)ds * ds), hR((size_t)Dp * Dp, 0.0f);
+    CRISP_CUDA(cudaMemcpyAsync(hs.data(), Rs, hs.size() * 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < Dp; i++) hR[(size_t)i * Dp + i] = 1.0f;
+    for (int i = 0; i < ds; i++)
+        for (int j = 0; j < ds; j++) hR[(size_t)blk[i] * Dp + blk[j]] = hs[(size_t)i * ds + j];
+    CRISP_CUDA(cudaMemcpyAsync(ix->R, hR.data(), hR.size() * 4, cudaMemcpyHostToDevice, s));
+    CRISP_CUDA(cudaStreamSynchronize(s));
+}
+
 void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, const float *cb_inj,
                  int64_t kmeans_sample, int32_t kmeans_iters, int32_t rotation_mode, float tau_cev, uint64_t seed,
-                 cudaStream_t s, const double *cev_given) {
+                 cudaStream_t s, const double *cev_given, const std::vector<double> *var_given) {
     const int64_t N = ix->N;
     // X <- data, zero padded to pitch
     CRISP_CUDA(cudaMemsetAsync(ix->X, 0, (size_t)N * ix->pitch * 4, s));
@@ -1028,7 +1071,13 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
     }
     // spectral check on the original D columns; a model build over a
     // gathered sample (build_model) supplies the global sample's CEV instead
-    ix->cev = cev_given ? *cev_given : compute_cev(ix->X, N, ix->pitch, ix->D, seed, s);
+    std::vector<double> var;
+    if (cev_given) {
+        ix->cev = *cev_given;
+        if (var_given) var = *var_given;
+    } else {
+        ix->cev = compute_cev(ix->X, N, ix->pitch, ix->D, seed, s, &var);
+    }
     bool rotate;
     if (R_inj) rotate = true;
     else if (cb_inj) rotate = false;  // injected build without R: no rotation
@@ -1038,6 +1087,8 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
         ix->hbm_bytes += (int64_t)ix->Dp * ix->Dp * 4;
         if (R_inj)
             CRISP_CUDA(cudaMemcpyAsync(ix->R, R_inj, (size_t)ix->Dp * ix->Dp * 4, cudaMemcpyDefault, s));
+        else if (ix->rot_block > 0)
+            make_block_rotation(ix, var, seed, s);
         else
             make_rotation(ix->Dp, seed, ix->R, s);
         rotate_in_place(ix, s);
@@ -1067,5 +1118,7 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
 }  // namespace crisp
 
 namespace crisp {
-double cev_of_sample(const float *S_dev, int64_t n, int D, cudaStream_t s) { return cev_of_rows(S_dev, n, D, s); }
+double cev_of_sample(const float *S_dev, int64_t n, int D, cudaStream_t s, std::vector<double> *var) {
+    return cev_of_rows(S_dev, n, D, s, var);
+}
 }  // namespace crisp

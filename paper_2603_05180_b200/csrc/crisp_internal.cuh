@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/crisp.h"
 
@@ -60,7 +61,8 @@ struct crisp_index {
     int64_t N = 0, N_global = 0, gid_base = 0;
     int32_t D = 0, Dp = 0, pitch = 0, M = 0, K = 0, dh = 0, W = 0;
     int32_t Wp = 0;            // code row stride in words: W rounded up to 8 (64-B rows, 16-B loads)
-    int32_t rotated = 0;
+    int32_t rotated = 0;       // 1: global rotation; 2: block-wise (R16)
+    int32_t rot_block = 0;     // block-wise rotation over this many subspaces (0: global)
     double cev = 0.0;
     float *X = nullptr;        // N x pitch, stored (rotated) vectors, zero padded
     float *R = nullptr;        // Dp x Dp row-major (rotated only)
@@ -106,10 +108,10 @@ void cell_size_maxima(crisp_index *ix, const int32_t *sizes_host);
 // build steps (build.cu)
 void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, const float *cb_inj, int64_t kmeans_sample,
                  int32_t kmeans_iters, int32_t rotation_mode, float tau_cev, uint64_t seed, cudaStream_t s,
-                 const double *cev_given = nullptr);
+                 const double *cev_given = nullptr, const std::vector<double> *var_given = nullptr);
 int64_t cev_sample_size(int64_t N);
 void sample_row_ids(int64_t N, int64_t n, uint64_t seed, uint32_t stream, int32_t *rows_dev, cudaStream_t s);
-double cev_of_sample(const float *S_dev, int64_t n, int D, cudaStream_t s);
+double cev_of_sample(const float *S_dev, int64_t n, int D, cudaStream_t s, std::vector<double> *var = nullptr);
 void finish_csr(crisp_index *ix, cudaStream_t s);
 
 // fp64 sequential-order GEMM: Y(rows x Dp, pitch ldy) = fl32(X(rows x Dp, pitch ldx) . R(Dp x Dp))

@@ -887,16 +887,14 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
 // (Measured alternative: fire-and-forget reductions plus a SWAR scan of the
 // counters at the end -- cfg4 count 26.1 ms against 23.4 ms.)
 // ---------------------------------------------------------------------------
-constexpr int CF_WARPS = 16;
-constexpr int CF_THREADS = CF_WARPS * 32;
 constexpr int CF_CAP = 2048;  // fragments staged per chunk
-constexpr int CF_EPT = CF_CAP / CF_THREADS;
 constexpr int CF_TF = 8;      // fragments per task (a power of two <= 32)
+constexpr int CF_MAXW = 32;   // warps per CTA: 16 (two CTAs per SM, F <= 2) or 32 (one CTA per SM, F = 4)
 
 struct CountFSmem {
     int4 tab[CF_CAP + 40];  // staged non-empty fragments (quad prefix, first quad, first position | WFLAG, end); padded
-    long long wtot64[CF_WARPS];
-    int32_t wtot[CF_WARPS];
+    long long wtot64[CF_MAXW];
+    int32_t wtot[CF_MAXW];
     int next, base;
 };
 // counters (BF bytes), candidate bitmap (BF bits), 32 dummy words (the atomics of
@@ -939,7 +937,8 @@ __global__ void k_act_rows(const uint32_t *__restrict__ act, const int32_t *__re
     if (lane == 0) etot[q] = base;
 }
 
-__global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__restrict__ erow,
+template <int CF_WARPS>
+__global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(const uint32_t *__restrict__ erow,
                                                                const int32_t *__restrict__ etot, int M, int KK,
                                                                const int32_t *__restrict__ off2, int NB, int F,
                                                                const int32_t *__restrict__ ids, int64_t N, int BS,
@@ -949,6 +948,8 @@ __global__ void __launch_bounds__(CF_THREADS, 2) k_count_frag(const uint32_t *__
                                                                int32_t *__restrict__ ncand, int32_t *__restrict__ need,
                                                                uint8_t *__restrict__ traceV,
                                                                const int32_t *__restrict__ qperm) {
+    constexpr int CF_THREADS = CF_WARPS * 32;
+    constexpr int CF_EPT = CF_CAP / CF_THREADS;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int BF = BS * F;
     uint32_t *cw = (uint32_t *)smraw;              // BF byte counters, 4 per word
@@ -2953,7 +2954,8 @@ static void set_attrs() {
     if (std::find(done_dev.begin(), done_dev.end(), dev) != done_dev.end()) return;
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_count_frag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -3261,9 +3263,15 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
             k_act_rows<<<nblk(qn, 8), 256, 0, s>>>(w.act, w.act_len, M, KK, qn, w.erow, w.etot);
             CRISP_LAUNCH();
             g_launches++;
-            k_count_frag<<<dim3((unsigned)w.NS, (unsigned)qn), CF_THREADS, countf_smem(ix->BS * w.CF), s>>>(
-                w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
-                w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm);
+            // 64K ids per CTA: 16 warps, two CTAs per SM; 128K ids: 32 warps, one CTA per SM
+            if (w.CF * ix->BS > 65536)
+                k_count_frag<32><<<dim3((unsigned)w.NS, (unsigned)qn), 1024, countf_smem(ix->BS * w.CF), s>>>(
+                    w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
+                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm);
+            else
+                k_count_frag<16><<<dim3((unsigned)w.NS, (unsigned)qn), 512, countf_smem(ix->BS * w.CF), s>>>(
+                    w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
+                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm);
         }
         else if (w.count_kernel == 0)
             k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N,

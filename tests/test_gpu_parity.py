@@ -678,3 +678,40 @@ def test_probe_screen_on_tensor_cores(crisp, monkeypatch, mode, screen, R):
         assert cnt["probe_screen_redone"] > 0, "R = 1 must send walks through the exact redo"
     if screen == "1" and R == "24":
         assert cnt["probe_exact_half_distances"] < 64 * 8 * 2 * 50, "the screen must save exact half distances"
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_blockwise_rotation_f4(crisp, mode):
+    """f4, block-wise variance redistribution (DESIGN R16): the GPU build
+    picks the oracle's block (the b subspaces of largest sample variance; the
+    covariance diagonal is computed in the same sequential fp64 order), its R is
+    the identity outside the block exactly and matches the oracle's rotation on
+    it (cuSOLVER vs LAPACK QR: 1e-5); with the oracle's R injected, X', cells,
+    CSR, codes and the search are bit-exact, and the rows outside the block keep
+    their input values."""
+    r = np.random.default_rng(12)
+    M, D, N = 8, 64, 12000
+    scale = np.ones(D)
+    scale[16:24] = 12.0
+    scale[48:56] = 5.0
+    X = (r.standard_normal((N, D)) * scale).astype(np.float32)
+    Qv = (r.standard_normal((40, D)) * scale).astype(np.float32)
+    ox = oracle.build(X, M, K=10, rotation_mode=1, kmeans_iters=4, seed=5, rotation_block=2)
+    gix = crisp.Index.build(X, M, K=10, rotation=1, kmeans_iters=4, seed=5, rotation_block=2)
+    assert gix.info()["rotation_block"] == 2
+    Rg = gix.export()["R"]
+    blk = oracle.rotation_block(oracle.dim_variances(X, 5), M, D, 2)
+    assert blk.tolist() == list(range(16, 24)) + list(range(48, 56))
+    out = np.setdiff1d(np.arange(D), blk)
+    assert np.array_equal(Rg[out], np.eye(D, dtype=np.float32)[out])
+    assert np.array_equal(Rg[:, out], np.eye(D, dtype=np.float32)[:, out])
+    assert np.abs(Rg - ox["R"]).max() < 1e-5
+    gix.free()
+    ix = crisp.Index.build(X, M, R=ox["R"], codebooks=ox["cb"], K=10, seed=5)
+    compare_index(ix, ox)
+    assert np.array_equal(ix.export()["X"][:, out], X[:, out])
+    ix.set_search_params(budget=600, tau=2, patience_factor=3)
+    ids, d, t = ix.trace(Qv, 10, mode)
+    r_ids, r_d, ot = oracle.search(ox, Qv, 10, mode, 600, 2, patience_factor=3, trace=True)
+    compare_trace(t, ot, mode, N)
+    assert_topk_parity(ids, d, r_ids, r_d, "block-wise rotation")

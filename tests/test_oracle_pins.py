@@ -658,3 +658,46 @@ def test_adsampling_prune_counts_as_non_improvement():
     rk2 = max(_exact_d2(q[0], X[i]) for i in range(150, 150 + k))
     thr = oracle.adsampling_threshold(float(rk2), 32, D, 2.1)
     assert all(_exact_d2(q[0, :32], X[i, :32]) > thr for i in list(range(150)) + list(range(155, N)))
+
+
+# --------------------------------------------------------------------------
+# f4: block-wise variance redistribution (DESIGN reading R16)
+# --------------------------------------------------------------------------
+def test_blockwise_rotation_selects_the_energetic_subspaces():
+    """A dataset whose subspace 2 carries 100x the variance of the others (and
+    subspace 5 10x): the block of b = 1 is subspace 2's dimensions, of b = 2
+    subspaces 2 and 5, in ascending order; equal energies go to the smaller m."""
+    r = rng(7)
+    M, D = 8, 64
+    scale = np.ones(D)
+    scale[16:24] = 10.0   # subspace 2 (8 dims each)
+    scale[40:48] = np.sqrt(10.0)  # subspace 5
+    X = (r.standard_normal((20000, D)) * scale).astype(np.float32)
+    var = oracle.dim_variances(X, 3)  # the 2000-row CEV sample
+    assert np.allclose(var, scale ** 2, rtol=0.2)
+    assert oracle.rotation_block(var, M, D, 1).tolist() == list(range(16, 24))
+    assert oracle.rotation_block(var, M, D, 2).tolist() == list(range(16, 24)) + list(range(40, 48))
+    assert oracle.rotation_block(np.ones(D), M, D, 2).tolist() == list(range(0, 16))
+
+
+def test_blockwise_rotation_is_identity_outside_and_orthogonal_inside():
+    """R is the identity outside the block (exactly), orthogonal on it; X' keeps
+    every dimension outside the block bit for bit and the block's norm per row
+    (isometry), and the block is really mixed."""
+    r = rng(8)
+    M, D = 8, 64
+    scale = np.ones(D)
+    scale[24:32] = 20.0
+    X = (r.standard_normal((3000, D)) * scale).astype(np.float32)
+    R, blk = oracle.blockwise_rotation(X, M, D, 2, 5)
+    out = np.setdiff1d(np.arange(D), blk)
+    assert np.array_equal(R[np.ix_(out, np.arange(D))], np.eye(D, dtype=np.float32)[out])
+    assert np.array_equal(R[np.ix_(np.arange(D), out)], np.eye(D, dtype=np.float32)[:, out])
+    Rb = R[np.ix_(blk, blk)].astype(np.float64)
+    assert np.abs(Rb @ Rb.T - np.eye(len(blk))).max() < 1e-5
+    assert np.abs(Rb - np.eye(len(blk))).max() > 0.1
+    ox = oracle.build(X, M, K=6, rotation_mode=1, kmeans_iters=2, seed=5, rotation_block=2)
+    assert np.array_equal(ox["R"], R)
+    assert np.array_equal(ox["X"][:, out], X[:, out])
+    nb = np.linalg.norm(X[:, blk].astype(np.float64), axis=1)
+    assert np.allclose(np.linalg.norm(ox["X"][:, blk].astype(np.float64), axis=1), nb, rtol=1e-5)
