@@ -896,6 +896,7 @@ struct CountFSmem {
     long long wtot64[CF_MAXW];
     int32_t wtot[CF_MAXW];
     int next, base;
+    uint64_t qc[64];  // b(q'), phi=1 fused Hamming (D' <= 4096)
 };
 // counters (BF bytes), candidate bitmap (BF bits), 32 dummy words (the atomics of
 // lanes without an id), CountFSmem
@@ -947,7 +948,11 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                                                                int32_t *__restrict__ cbase,
                                                                int32_t *__restrict__ ncand, int32_t *__restrict__ need,
                                                                uint8_t *__restrict__ traceV,
-                                                               const int32_t *__restrict__ qperm) {
+                                                               const int32_t *__restrict__ qperm,
+                                                               const float *__restrict__ qrot, int pitch, int Dp,
+                                                               const uint64_t *__restrict__ codes, int Wd,
+                                                               uint16_t *__restrict__ hbuf,
+                                                               int32_t *__restrict__ ghist) {
     constexpr int CF_THREADS = CF_WARPS * 32;
     constexpr int CF_EPT = CF_CAP / CF_THREADS;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -966,6 +971,14 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
     for (int i = tid; i < (BF + BF / 8 + 128) / 16; i += CF_THREADS) ((uint4 *)smraw)[i] = make_uint4(0, 0, 0, 0);
     const int Etot = __ldg(etot + q);
     const uint32_t *eq = erow + q * (int64_t)M * KK;
+    if (hbuf && warp == 0) {
+        const float *qrow = qrot + q * pitch;
+        for (int d0 = 0; d0 < Wd * 64; d0 += 32) {  // bit (i mod 64) of word i/64 = [q'_i > 0] (Z10)
+            const int d = d0 + lane;
+            const unsigned bits = __ballot_sync(0xffffffffu, d < Dp && qrow[d] > 0.0f);
+            if (lane == 0) ((uint32_t *)S.qc)[d0 >> 5] = bits;
+        }
+    }
     const uint32_t taum1 = (uint32_t)tau - 1u;
     __syncthreads();
     for (int e0 = 0; e0 < Etot; e0 += CF_CAP) {
@@ -1139,6 +1152,54 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
         const unsigned char *c8 = (const unsigned char *)cw;
         for (int j = tid; j < BF; j += CF_THREADS)
             if ((int64_t)bbase + j < N) traceV[q * N + (int64_t)bbase + j] = c8[j];
+    }
+    if (hbuf) {
+        // a4, phi=1, fused: h(x) = popcount(b(q') xor b(x)) (Alg. 1 l.19) of this
+        // block's candidates, right after they are listed (the count is issue-bound, so these
+        // code-row streams overlap it).  4 lanes per candidate, 16-byte loads of its code row;
+        // h at the candidate's pool position, the query's histogram of h by reductions.
+        __syncthreads();  // the candidate ids in the pool, b(q') in shared memory
+        int n = 0;
+        for (int w2 = 0; w2 < CF_WARPS; w2++) n += S.wtot[w2];
+        const int base = S.base;
+        const int g4 = lane >> 2, gl = lane & 3, nt = Wd >> 3;
+        int32_t *gh = ghist + q * (int64_t)(Dp + 1);
+        for (int v0 = warp * 32; v0 < n; v0 += CF_WARPS * 32) {
+            int pos[4], id[4];
+            bool okv[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const int vi = v0 + r * 8 + g4;
+                pos[r] = base + vi;
+                okv[r] = vi < n && pos[r] < CAPQ;
+                id[r] = okv[r] ? outp[pos[r]] : (int)bbase;
+            }
+            int hr[4] = {0, 0, 0, 0};
+#pragma unroll 2
+            for (int t = 0; t < nt; t++) {
+                const int wd = 2 * gl + 8 * t;
+                const uint64_t q0w = S.qc[wd], q1w = S.qc[wd + 1];
+                ulonglong2 cwd[4];
+#pragma unroll
+                for (int r = 0; r < 4; r++) cwd[r] = __ldg((const ulonglong2 *)(codes + (int64_t)id[r] * Wd + wd));
+#pragma unroll
+                for (int r = 0; r < 4; r++) hr[r] += __popcll(q0w ^ cwd[r].x) + __popcll(q1w ^ cwd[r].y);
+            }
+            uint32_t p01 = (uint32_t)hr[0] | ((uint32_t)hr[1] << 16), p23 = (uint32_t)hr[2] | ((uint32_t)hr[3] << 16);
+            p01 += __shfl_xor_sync(0xffffffffu, p01, 1);
+            p23 += __shfl_xor_sync(0xffffffffu, p23, 1);
+            p01 += __shfl_xor_sync(0xffffffffu, p01, 2);
+            p23 += __shfl_xor_sync(0xffffffffu, p23, 2);
+            if (gl == 0) {
+                const int hh[4] = {(int)(p01 & 0xffffu), (int)(p01 >> 16), (int)(p23 & 0xffffu), (int)(p23 >> 16)};
+#pragma unroll
+                for (int r = 0; r < 4; r++)
+                    if (okv[r]) {
+                        hbuf[q * CAPQ + pos[r]] = (uint16_t)hh[r];
+                        atomicAdd(&gh[hh[r]], 1);
+                    }
+            }
+        }
     }
 }
 
@@ -3077,7 +3138,12 @@ struct Work {
         // candidate segments per query (id blocks, warp sub-blocks, or frag blocks)
         NS = count_kernel == 0 ? NB : count_kernel == 1 ? ix->NBW : (NB + CF - 1) / CF;
         count_atom = env_int("CRISP_COUNT_ATOM", 0);  // k_count_warp: shared atomics (else byte load/store pairs; faster)
-        ham_fused = env_int("CRISP_HAMMING_FUSED", 0);  // phi=1: popcounts inside k_count_warp (else k_hamming_dense)
+        // phi=1: popcounts inside the count kernel (CRISP_HAMMING_FUSED=1), else k_hamming_dense.
+        // Measured at cfg4: fused into k_count_frag 65.4 ms against 21.7 + 16.2 ms separate (each
+        // CTA's code-row stream runs after its counting, with only two CTAs per SM); into
+        // k_count_warp at cfg2 6.1 against 3.6 + 2.0 ms (r01): off by default
+        ham_fused = env_int("CRISP_HAMMING_FUSED", 0);
+        if (count_kernel == 2 && ix->Wp > 64) ham_fused = 0;  // b(q') is staged in 64 words
         // row kernels: four rows per warp step for rows up to 4 KB (measured: faster at D=960, slower at 4096)
         rows4 = env_int("CRISP_ROWS4", pitch <= 1024 ? 1 : 0);
         // round 0: exact verification of every query's first F rows.  ADSampling on
@@ -3264,14 +3330,17 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
             CRISP_LAUNCH();
             g_launches++;
             // 64K ids per CTA: 16 warps, two CTAs per SM; 128K ids: 32 warps, one CTA per SM
+            uint16_t *hb = (w.mode == 1 && w.ham_fused) ? w.hbuf : nullptr;  // phi=1: Hamming fused into the count
             if (w.CF * ix->BS > 65536)
                 k_count_frag<32><<<dim3((unsigned)w.NS, (unsigned)qn), 1024, countf_smem(ix->BS * w.CF), s>>>(
                     w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
-                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm);
+                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp,
+                    hb, w.ghist);
             else
                 k_count_frag<16><<<dim3((unsigned)w.NS, (unsigned)qn), 512, countf_smem(ix->BS * w.CF), s>>>(
                     w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
-                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm);
+                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp,
+                    hb, w.ghist);
         }
         else if (w.count_kernel == 0)
             k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N,
@@ -3371,7 +3440,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
                                                  NB, w.hbuf, w.ghist, w.fb, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
-        if (!(w.count_kernel == 1 && w.ham_fused)) {
+        if (!((w.count_kernel == 1 || w.count_kernel == 2) && w.ham_fused)) {
             dim3 g2(w.HS, (unsigned)qn);
             k_hamming_dense<<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
                                                                    w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb, w.qperm);

@@ -108,6 +108,7 @@ COUNT_VARIANTS = {"select": {"CRISP_COUNT_KERNEL": "0", "CRISP_ROWS4": "0"},
                  "frag": {"CRISP_COUNT_KERNEL": "2"},
                  "frag_f1": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "1"},
                  "frag_f4": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "4"},
+                 "frag_fused": {"CRISP_COUNT_KERNEL": "2", "CRISP_HAMMING_FUSED": "1"},
                  # the grouped Guaranteed-Mode re-rank (k_rerank_group) after either count kernel
                  "frag_group": {"CRISP_COUNT_KERNEL": "2", "CRISP_RERANK_GROUP": "1"},
                  "warp_group": {"CRISP_COUNT_KERNEL": "1", "CRISP_RERANK_GROUP": "1"}}
@@ -715,3 +716,34 @@ def test_blockwise_rotation_f4(crisp, mode):
     r_ids, r_d, ot = oracle.search(ox, Qv, 10, mode, 600, 2, patience_factor=3, trace=True)
     compare_trace(t, ot, mode, N)
     assert_topk_parity(ids, d, r_ids, r_d, "block-wise rotation")
+
+
+def test_search_async_returns_before_the_kernels_finish(crisp):
+    """crisp_search_async is stream-ordered: it enqueues the whole search and
+    returns (no read-back inside: the candidate capacity is an exact bound known
+    in advance).  Evidence without a tracer: with the stream held busy by a
+    kernel queued first, the call returns while that kernel still runs, and the
+    results are then complete and exact."""
+    import time
+
+    import torch
+
+    X, Qv, ox = make_case(cfg=1, N=20000, D=256, Q=200, M=8, K=50, seed=0)
+    ix = build_gpu(crisp, X, ox)
+    ix.set_search_params(budget=300, tau=3, patience_factor=40)
+    ref_ids, ref_d = ix.search(Qv, 10, 1)
+    q = torch.from_numpy(Qv).cuda()
+    ids = torch.empty((200, 10), dtype=torch.int64, device="cuda")
+    dd = torch.empty((200, 10), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(2e9))  # ~1 s of GPU time queued ahead of the search
+        t0 = time.perf_counter()
+        ix.search_async(q, 10, 1, ids, dd, stream.cuda_stream)
+        t_call = time.perf_counter() - t0
+        busy = not stream.query()
+    torch.cuda.synchronize()
+    assert busy, "the stream finished before the call returned"
+    assert t_call < 0.3, f"crisp_search_async blocked for {t_call:.3f} s"
+    assert np.array_equal(ids.cpu().numpy(), ref_ids) and np.array_equal(dd.cpu().numpy(), ref_d)
