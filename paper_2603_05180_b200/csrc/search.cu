@@ -2000,7 +2000,8 @@ __global__ void __launch_bounds__(THREADS) k_hamming(const float *__restrict__ q
 // bases come from a cursor starting at 0), so a CTA takes a contiguous range
 // of positions: 4 lanes per candidate with 16-byte code loads, h written at
 // the position, a CTA histogram flushed to the query's histogram.
-__global__ void __launch_bounds__(THREADS, 4) k_hamming_dense(const float *__restrict__ qrot, int pitch, int Dp,
+template <int HT>
+__global__ void __launch_bounds__(THREADS, HT > 2 ? 2 : 4) k_hamming_dense(const float *__restrict__ qrot, int pitch, int Dp,
                                                             const uint64_t *__restrict__ codes, int Wd,
                                                             const int32_t *__restrict__ pool, int64_t CAPQ,
                                                             const int32_t *__restrict__ cursor,
@@ -2045,15 +2046,23 @@ __global__ void __launch_bounds__(THREADS, 4) k_hamming_dense(const float *__res
             idn[r] = vn < hi ? __ldg(poolq + vn) : 0;
         }
         int hr[4] = {0, 0, 0, 0};
-#pragma unroll 2
-        for (int t = 0; t < nt; t++) {
-            const int wd = 2 * gl + 8 * t;
-            const uint64_t q0 = qc[wd], q1 = qc[wd + 1];
-            ulonglong2 cw[4];
+        // HT 16-byte chunks of each of the 4 rows issued together before their popcounts
+        // (DRAM-bound at cfg4: the loads in flight set the rate)
+        for (int t0 = 0; t0 < nt; t0 += HT) {
+            ulonglong2 cw[HT][4];
 #pragma unroll
-            for (int r = 0; r < 4; r++) cw[r] = __ldg((const ulonglong2 *)(codes + (int64_t)id[r] * Wd + wd));
+            for (int tt = 0; tt < HT; tt++)
 #pragma unroll
-            for (int r = 0; r < 4; r++) hr[r] += __popcll(q0 ^ cw[r].x) + __popcll(q1 ^ cw[r].y);
+                for (int r = 0; r < 4; r++)
+                    cw[tt][r] = t0 + tt < nt ? __ldg((const ulonglong2 *)(codes + (int64_t)id[r] * Wd + 2 * gl + 8 * (t0 + tt)))
+                                             : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+            for (int tt = 0; tt < HT; tt++) {
+                const int wd = 2 * gl + 8 * min(t0 + tt, nt - 1);
+                const uint64_t q0 = t0 + tt < nt ? qc[wd] : 0ull, q1 = t0 + tt < nt ? qc[wd + 1] : 0ull;
+#pragma unroll
+                for (int r = 0; r < 4; r++) hr[r] += __popcll(q0 ^ cw[tt][r].x) + __popcll(q1 ^ cw[tt][r].y);
+            }
         }
         uint32_t p01 = (uint32_t)hr[0] | ((uint32_t)hr[1] << 16), p23 = (uint32_t)hr[2] | ((uint32_t)hr[3] << 16);
         p01 += __shfl_xor_sync(0xffffffffu, p01, 1);
@@ -3031,7 +3040,8 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -3442,8 +3452,16 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         g_launches++;
         if (!((w.count_kernel == 1 || w.count_kernel == 2) && w.ham_fused)) {
             dim3 g2(w.HS, (unsigned)qn);
-            k_hamming_dense<<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
-                                                                   w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb, w.qperm);
+            // 16-byte chunks of each code row issued together per lane (CRISP_HAMMING_HT: 2, or 4 with
+            // 2 CTAs per SM; measured at cfg4: 12.4 ms with 2 (8 loads in flight), 14.7 with 4, 14.0 before)
+            if (env_int("CRISP_HAMMING_HT", 2) >= 4)
+                k_hamming_dense<4><<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
+                                                                          w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb,
+                                                                          w.qperm);
+            else
+                k_hamming_dense<2><<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
+                                                                          w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb,
+                                                                          w.qperm);
             CRISP_LAUNCH();
             g_launches++;
         }
@@ -3624,10 +3642,56 @@ static int64_t candidate_capacity(const crisp_index *ix, int mode, int k, bool t
 // The whole batch, in query chunks that fit the workspace, with candidate
 // capacity CAPQ per query (candidate_capacity: never exceeded).  Only the trace
 // path reads back (its outputs); otherwise everything is stream-ordered on s.
+// CRISP_PIPE = p >= 2: the batch in p query chunks on two side streams, so that one
+// chunk's front (a0-a4: the issue-bound collision count) runs while the previous
+// chunk's verification streams HBM.  Stream-ordered: forked from and joined into s.
+static void search_pipelined(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode,
+                             SearchOut out, cudaStream_t s, int64_t CAPQ, int parts) {
+    const int64_t Qc = (Q + parts - 1) / parts;
+    cudaStream_t ss[2];
+    cudaEvent_t fork, done[2];
+    for (int i = 0; i < 2; i++) {
+        CRISP_CUDA(cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking));
+        CRISP_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    CRISP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    {
+        Work w0(ix, k, mode, Qc, CAPQ, false, out.d64 == nullptr, s), w1(ix, k, mode, Qc, CAPQ, false, out.d64 == nullptr, s);
+        Work *ws[2] = {&w0, &w1};
+        CRISP_CUDA(cudaEventRecord(fork, s));  // the Work buffers were allocated on s
+        for (int i = 0; i < 2; i++) CRISP_CUDA(cudaStreamWaitEvent(ss[i], fork, 0));
+        int c = 0;
+        for (int64_t q0 = 0; q0 < Q; q0 += Qc, c++) {
+            const int64_t qn = std::min(Qc, Q - q0);
+            Work &w = *ws[c & 1];
+            cudaStream_t st = ss[c & 1];
+            run_front(w, queries + q0 * ix->D, qn, st, nullptr);
+            run_fallback_local(w, qn, st);
+            run_verify(w, qn, out.ids + q0 * k, out.d32 ? out.d32 + q0 * k : nullptr,
+                       out.d64 ? out.d64 + q0 * k : nullptr, st);
+            run_stats(w, qn, st);
+        }
+        for (int i = 0; i < 2; i++) {
+            CRISP_CUDA(cudaEventRecord(done[i], ss[i]));
+            CRISP_CUDA(cudaStreamWaitEvent(s, done[i], 0));  // joined before the buffers are freed on s
+        }
+    }
+    for (int i = 0; i < 2; i++) {
+        cudaEventDestroy(done[i]);
+        cudaStreamDestroy(ss[i]);
+    }
+    cudaEventDestroy(fork);
+}
+
 static void search_pass(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode, SearchOut out,
                         cudaStream_t s, const crisp_trace_t *tr, int64_t CAPQ, const float *hq) {
     const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : default_workspace();
     const int64_t perq = Work::per_query_bytes(ix, k, mode, CAPQ, tr && tr->V);
+    const int parts = std::max(1, std::min(16, env_int("CRISP_PIPE", 1)));
+    if (parts >= 2 && !tr && !hq && Q >= 2048 && perq * 2 * ((Q + parts - 1) / parts) <= ws) {
+        search_pipelined(ix, queries, Q, k, mode, out, s, CAPQ, parts);
+        return;
+    }
     int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, ws / perq));
     Qc = std::min<int64_t>(Qc, 65535);
     Work w(ix, k, mode, Qc, CAPQ, tr && tr->V, out.d64 == nullptr, s);

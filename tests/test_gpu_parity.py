@@ -747,3 +747,29 @@ def test_search_async_returns_before_the_kernels_finish(crisp):
     assert busy, "the stream finished before the call returned"
     assert t_call < 0.3, f"crisp_search_async blocked for {t_call:.3f} s"
     assert np.array_equal(ids.cpu().numpy(), ref_ids) and np.array_equal(dd.cpu().numpy(), ref_d)
+
+
+@pytest.mark.parametrize("parts", ["2", "3"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_pipelined_chunks_equal_one_pass(crisp, monkeypatch, mode, parts):
+    """CRISP_PIPE: the batch in query chunks on two side streams (one chunk's
+    count overlapping the previous chunk's verification) gives the one-pass
+    results exactly, and the oracle's on a sample."""
+    import torch
+
+    X, Qv, ox = make_case(cfg=1, N=20000, D=256, Q=4100, M=8, K=50, seed=0)
+    ix = build_gpu(crisp, X, ox)
+    ix.set_search_params(budget=300, tau=3, patience_factor=40)
+    q = torch.from_numpy(Qv).cuda()
+    outs = []
+    for p in ("1", parts):
+        monkeypatch.setenv("CRISP_PIPE", p)
+        ids = torch.empty((4100, 10), dtype=torch.int64, device="cuda")
+        dd = torch.empty((4100, 10), dtype=torch.float32, device="cuda")
+        ix.search_async(q, 10, mode, ids, dd, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        outs.append((ids.cpu().numpy(), dd.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    sample = np.arange(0, 4100, 41)
+    r_ids, r_d, _ = oracle.search(ox, Qv[sample], 10, mode, 300, 3, patience_factor=40)
+    assert_topk_parity(outs[1][0][sample], outs[1][1][sample], r_ids, r_d, f"pipe={parts}")
