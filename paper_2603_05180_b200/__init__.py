@@ -19,7 +19,7 @@ from fractions import Fraction
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcrisp.so")
+LIB_PATH = os.environ.get("CRISP_LIB") or os.path.join(_HERE, "libcrisp.so")  # CRISP_LIB: an A/B build variant
 
 GUARANTEED, OPTIMIZED = 0, 1
 STAGES = ("transform", "probe", "count_select", "fallback", "verify", "merge", "hamming", "hsort")

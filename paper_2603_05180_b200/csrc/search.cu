@@ -24,6 +24,9 @@
 
 #include "crisp_internal.cuh"
 
+#ifndef CRISP_CF_CAP
+#define CRISP_CF_CAP 1024  // measured: 1024 (two entries per thread) beats 2048 at cfg4 (22.9 vs 24.6 ms) and cfg3
+#endif
 namespace crisp {
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -887,7 +890,7 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
 // (Measured alternative: fire-and-forget reductions plus a SWAR scan of the
 // counters at the end -- cfg4 count 26.1 ms against 23.4 ms.)
 // ---------------------------------------------------------------------------
-constexpr int CF_CAP = 2048;  // fragments staged per chunk
+constexpr int CF_CAP = CRISP_CF_CAP;  // fragments staged per chunk
 constexpr int CF_TF = 8;      // fragments per task (a power of two <= 32)
 constexpr int CF_MAXW = 32;   // warps per CTA: 16 (two CTAs per SM, F <= 2) or 32 (one CTA per SM, F = 4)
 
@@ -3237,9 +3240,17 @@ struct Work {
         probe_qpw = std::max(1, env_int("CRISP_PROBE_QPW", 4));  // queries per warp in k_probe
         // a1 screen on the tensor cores (CRISP_PROBE_SCREEN=0 disables); dist64 for the
         // centroids that can reach the probe_r smallest of each half
-        probe_r = std::max(1, env_int("CRISP_PROBE_R", 24));
-        if (env_int("CRISP_PROBE_SCREEN", 1) && screen_supported(ix))
-            scr = buf.alloc<ScreenOut>((size_t)Qc * 2 * M);
+        // The walk pops about L = B K^2 / N cells per subspace (cells of average size); a
+        // staircase of L cells reaches ranks ~sqrt(2L) in each half.  The screen certifies a
+        // prefix of about probe_r ranks; when that is most of K it saves nothing (and a short
+        // prefix would send walks through the exact redo), so the probe then runs unscreened.
+        {
+            const double L = (double)ix->budget * (double)KK / (double)std::max<int64_t>(1, ix->N_global);
+            const int r_auto = std::max(24, (int)std::ceil(2.0 * std::sqrt(2.0 * L)) + 4);
+            probe_r = std::max(1, env_int("CRISP_PROBE_R", r_auto));
+            const int want = env_int("CRISP_PROBE_SCREEN", probe_r < (4 * K) / 5 ? 1 : 0);
+            if (want && screen_supported(ix)) scr = buf.alloc<ScreenOut>((size_t)Qc * 2 * M);
+        }
         probe_smem = (probe_gs ? ((KK * 4 + 15) & ~15) : 0) + (probe_cb ? ((2 * K * (ix->dh | 1) * 4 + 15) & ~15) : 0) +
                      WARPS * ((((4 * K + 2 * ix->dh) * 8) + 3 * K + 15) & ~15);
         count_smem = BS + BS / 8 + (int)sizeof(CountSmem);
