@@ -434,11 +434,23 @@ def run_crisp(args):
             vb = cnt["verified"] * row_bytes / K  # 4D per verified row (SURVEY 8(d) B_rerank)
             # phi=0: the grouped re-rank is opt-in (CRISP_RERANK_GROUP=1; search.cu Work)
             grp = os.environ.get("CRISP_RERANK_GROUP", "0") != "0"
-            kernels["verify"] = {"kernel": ["k_rerank_group" if grp else "k_rerank_exact",
-                                            "k_verify_rows+k_patience_scan+k_patience_tail",
-                                            "k_verify_rows(_ad)+k_patience_scan+k_patience_tail"][mode],
-                                 "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
-                                 "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9}
+            vname = ["k_rerank_group" if grp else "k_rerank_exact", "k_verify_rows+k_patience_scan+k_patience_tail",
+                     "k_verify_rows(_ad)+k_patience_scan+k_patience_tail"][mode]
+            model = "4 pitch B per verified row (SURVEY 8(d) B_rerank)"
+            if cnt.get("filter_rows", 0) > 0:
+                # verification filter (DESIGN R17): 2 hpitch B per row bounded through the fp16
+                # copy, 4 pitch B per row read exactly (round 0, rows the bound keeps, the tail)
+                hrow = 2 * ((info["pitch"] + 7) // 8 * 8)
+                fr, fe = cnt["filter_rows"], cnt["filter_exact"]
+                if mode == 0:
+                    vb = (cnt["candidates"] * (hrow + 16) + fe * row_bytes) / K
+                    vname = "k_lb_bounds+k_lb_threshold+k_rerank_exact"
+                else:
+                    vb = ((max(0, cnt["verified"] - fr) + fe) * row_bytes + fr * hrow) / K
+                    vname = "k_verify_rows+k_verify_rows_lb+k_patience_scan+k_patience_tail"
+                model = "2 hpitch B per row bounded through the fp16 copy + 4 pitch B per row read exactly (R17)"
+            kernels["verify"] = {"kernel": vname, "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
+                                 "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9, "bytes_model": model}
         if st["count_select"] > 0:
             # a3 streams 4 B per id (SURVEY 8(d) B_count); at phi=1 the same kernel
             # (k_count_warp) also gathers 8*ceil(D'/64) B of code per candidate (B_ham)
@@ -478,6 +490,8 @@ def run_crisp(args):
             roof = {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak, "traffic": traffic,
                     "kernel": kernels[dom]["kernel"], "peak_source": peak_src,
                     "per": "step (the stage's launches summed: bytes and CUDA-event time per step)"}
+            if kernels[dom].get("bytes_model"):
+                roof["bytes_model"] = kernels[dom]["bytes_model"]
             if traffic:
                 # the DRAM side of the same stage: measured bytes (ncu) over the live time
                 roof["dram_gbs"] = traffic / sec / 1e9

@@ -175,6 +175,21 @@ crisp_status crisp_set_search_params(crisp_index *idx, double beta, int64_t budg
  * must be >= 0.  Applies to searches with mode CRISP_OPTIMIZED only. */
 crisp_status crisp_set_adsampling(crisp_index *idx, int32_t enable, double eps0, int32_t stride);
 
+/* Verification filter (a5 of both modes; DESIGN R17).  The exact re-rank
+ * (Alg. 1 l.22-27) only needs the exact distance of a candidate
+ * that can enter the current top-k.  With the filter on, the index keeps a
+ * 2-byte copy fp16(s x) of every stored row (s a power of two) and the
+ * residual norm of each row, rounded up; a search first bounds
+ * ||q' - x|| from below through that copy (triangle inequality, certified
+ * rounding) and reads the fp32 row only when the bound does not exceed the
+ * current k-th best distance.  A candidate skipped this way is one the exact
+ * rule would verify without improving the top-k, so ids, distances, patience
+ * stops and counters of the results are unchanged.  enable = 1 builds the copy
+ * (N x padded_D x 2 bytes of HBM) if absent; enable = 0 frees it.  Indexes are
+ * built with the filter on unless the environment sets CRISP_VERIFY_FILTER=0.
+ * Blocks until searches in flight on the index's device have finished. */
+crisp_status crisp_set_verify_filter(crisp_index *idx, int32_t enable);
+
 crisp_status crisp_index_info(const crisp_index *idx, crisp_index_info_t *out);
 
 /* Batched search, Alg. 1: a0 query transform, a1 half distances,
@@ -244,7 +259,10 @@ crisp_status crisp_stage_times(double *ms, int32_t n, int32_t reset);
  * launched by searches/merges on the calling thread (counted always), out[5]
  * exact half distances (dist64) the a1 probe computed, out[6] (query,
  * subspace) walks whose tensor-core screen did not cover the ranks the walk
- * reached and were redone on exact half sorts.  Up to n entries are written;
+ * reached and were redone on exact half sorts, out[7] candidate rows whose
+ * distance bound the verification filter computed (crisp_set_verify_filter),
+ * out[8] of those, rows whose fp32 row was read for the exact distance because
+ * the bound could not exclude them.  Up to n entries are written;
  * reset != 0 clears them. */
 crisp_status crisp_search_counters(int64_t *out, int32_t n, int32_t reset);
 

@@ -64,7 +64,7 @@ ABI_SYMBOLS = (
     "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
     "crisp_set_stage_timing", "crisp_stage_times", "crisp_search_counters", "crisp_free", "crisp_last_error", "crisp_version",
     "crisp_shard_search_begin", "crisp_shard_search_hist", "crisp_shard_search_finish", "crisp_shard_search_free",
-    "crisp_set_adsampling", "crisp_exact_ceil", "crisp_cev_sample_size", "crisp_sample_rows", "crisp_build_model",
+    "crisp_set_adsampling", "crisp_set_verify_filter", "crisp_exact_ceil", "crisp_cev_sample_size", "crisp_sample_rows", "crisp_build_model",
 )
 
 _lib = None
@@ -85,6 +85,7 @@ def lib():
         L.crisp_build_shard.argtypes = [vp, i64, i64, i32, P(Params), vp, vp, P(vp)]
         L.crisp_local_cell_sizes.argtypes = [vp, vp]
         L.crisp_set_adsampling.argtypes = [vp, i32, f64, i32]
+        L.crisp_set_verify_filter.argtypes = [vp, i32]
         L.crisp_set_global_cell_sizes.argtypes = [vp, vp]
         L.crisp_set_search_params.argtypes = [vp, f64, i64, f64, i32, i32]
         L.crisp_index_info.argtypes = [vp, P(Info)]
@@ -274,6 +275,11 @@ class Index:
         """crisp_set_adsampling: Optimized Mode verification by ADSampling (Eq. 2)."""
         _check(lib().crisp_set_adsampling(self._h, 1 if enable else 0, float(eps0), int(stride)))
 
+    def set_verify_filter(self, enable: bool = True):
+        """crisp_set_verify_filter: the certified fp16 distance bound in front of the
+        exact re-rank (results unchanged; DESIGN R17)."""
+        _check(lib().crisp_set_verify_filter(self._h, 1 if enable else 0))
+
     def local_cell_sizes(self) -> np.ndarray:
         i = self.info()
         out = np.zeros((i["M"], i["K"] * i["K"]), np.int64)
@@ -392,7 +398,8 @@ def stage_times(reset: bool = True) -> dict:
 
 def search_counters(reset: bool = True) -> dict:
     """Work counters of the searches run with stage timing on (crisp_search_counters)."""
-    a = np.zeros(7, np.int64)
-    _check(lib().crisp_search_counters(_ptr(a), 7, 1 if reset else 0))
+    a = np.zeros(9, np.int64)
+    _check(lib().crisp_search_counters(_ptr(a), 9, 1 if reset else 0))
     return dict(ids_streamed=int(a[0]), candidates=int(a[1]), verified=int(a[2]), fallback=int(a[3]),
-                launches=int(a[4]), probe_exact_half_distances=int(a[5]), probe_screen_redone=int(a[6]))
+                launches=int(a[4]), probe_exact_half_distances=int(a[5]), probe_screen_redone=int(a[6]),
+                filter_rows=int(a[7]), filter_exact=int(a[8]))

@@ -114,6 +114,8 @@ static void free_index(crisp_index *ix) {
     cudaFree(ix->off2w);
     cudaFree(ix->gsize);
     cudaFree(ix->codes);
+    cudaFree(ix->Xh);
+    cudaFree(ix->xerr);
     delete ix;
 }
 
@@ -155,6 +157,10 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
     ix->SBW = ix->BS / 8;
     ix->NBW = ix->NB * 8;
     ix->workspace_bytes = p->workspace_bytes;
+    {
+        const char *e = getenv("CRISP_VERIFY_FILTER");  // build-time default of crisp_set_verify_filter
+        ix->vfilter = (e && *e) ? (atoi(e) != 0) : 1;
+    }
     try {
         const int64_t KK = (int64_t)ix->K * ix->K;
         ix->X = dalloc<float>(ix, (size_t)N * ix->pitch);
@@ -408,6 +414,36 @@ crisp_status crisp_set_adsampling(crisp_index *ix, int32_t enable, double eps0, 
             ix->ad_eps0 = eps0;
             ix->ad_stride = stride;
         }
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_set_verify_filter(crisp_index *ix, int32_t enable) {
+    try {
+        CRISP_CHECK(ix != nullptr, "index is NULL");
+        CRISP_CUDA(cudaSetDevice(ix->device));
+        CRISP_CUDA(cudaDeviceSynchronize());  // searches in flight may read the copy
+        if (enable && !ix->Xh) {
+            cudaStream_t s;
+            CRISP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            try {
+                crisp::build_verify_filter(ix, s);
+                CRISP_CUDA(cudaStreamSynchronize(s));
+            } catch (...) {
+                cudaStreamDestroy(s);
+                throw;
+            }
+            cudaStreamDestroy(s);
+        } else if (!enable && ix->Xh) {
+            cudaFree(ix->Xh);
+            cudaFree(ix->xerr);
+            ix->Xh = nullptr;
+            ix->xerr = nullptr;
+            ix->hbm_bytes -= ix->N * (int64_t)ix->hpitch * 2 + ix->N * 4;
+        }
+        ix->vfilter = enable ? 1 : 0;
         return CRISP_OK;
     } catch (Err &e) {
         return e.st;

@@ -8,6 +8,7 @@
 // summation order; they feed a threshold decision (CEV > 0.85) and R, which
 // parity tests inject (crisp_build_with) or check by property.
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -1112,7 +1113,73 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
     k_codes<<<nblk(N * (int64_t)ix->Wp * 64, 256), 256, 0, s>>>(ix->X, N, ix->pitch, ix->Dp, ix->Wp,
                                                                   (uint32_t *)ix->codes);
     CRISP_LAUNCH();
+    if (ix->vfilter) build_verify_filter(ix, s);
     CRISP_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
+// Verification filter (DESIGN R17).  x~ = fp16(s x) with s = 2^e chosen so that
+// max |s x| <= 2^15 (no fp16 overflow; s x is exact in fp32), and per row the
+// residual norm rho = ||s x - x~|| (every difference exact in fp64, the sum in
+// fp64, rounded up with a 1e-9 relative margin).  By the triangle inequality
+// ||s q - s x|| >= ||s q - x~|| - rho, so the search can certify that a row
+// does not enter the top-k from its 2-byte copy (search.cu, k_verify_rows_lb).
+// ---------------------------------------------------------------------------
+__global__ void k_absmax(const float *X, int64_t n, unsigned *out) {
+    unsigned m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, __float_as_uint(fabsf(X[i])));  // non-negative floats order as their bits
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void k_half_copy(const float *__restrict__ X, int64_t N, int pitch, int hpitch, float scale,
+                            __half *__restrict__ Xh, float *__restrict__ xerr) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= N) return;
+    const float *x = X + row * pitch;
+    __half *h = Xh + row * hpitch;
+    double e = 0.0;
+    for (int i = lane; i < hpitch; i += 32) {
+        const float xs = (i < pitch ? x[i] : 0.0f) * scale;  // exact: scale = 2^e and |xs| < 2^15
+        const __half hv = __float2half_rn(xs);
+        h[i] = hv;
+        const double r = (double)xs - (double)__half2float(hv);  // exact in fp64
+        e = fma(r, r, e);
+    }
+    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    // the fp64 sum of D non-negative terms is within D 2^-53 relative of the exact sum
+    if (lane == 0) xerr[row] = __double2float_ru(sqrt(e) * (1.0 + 1e-9));
+}
+
+void build_verify_filter(crisp_index *ix, cudaStream_t s) {
+    const int64_t N = ix->N, n = N * (int64_t)ix->pitch;
+    ix->hpitch = (ix->pitch + 7) / 8 * 8;
+    if (!ix->Xh) {
+        CRISP_CUDA(cudaMalloc(&ix->Xh, (size_t)N * ix->hpitch * 2 + 16));
+        CRISP_CUDA(cudaMalloc(&ix->xerr, (size_t)N * 4 + 16));
+        ix->hbm_bytes += N * (int64_t)ix->hpitch * 2 + N * 4;
+    }
+    Scratch sc;
+    unsigned *mx = sc.alloc<unsigned>(1);
+    CRISP_CUDA(cudaMemsetAsync(mx, 0, 4, s));
+    k_absmax<<<1184, 256, 0, s>>>(ix->X, n, mx);
+    CRISP_LAUNCH();
+    unsigned hm = 0;
+    CRISP_CUDA(cudaMemcpyAsync(&hm, mx, 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaStreamSynchronize(s));
+    float amax;
+    memcpy(&amax, &hm, 4);
+    int e = 0;
+    if (amax > 0.0f) {
+        std::frexp(amax, &e);          // amax < 2^e
+        e = std::max(-100, std::min(100, 15 - e));  // |s x| < 2^15
+    }
+    ix->xh_scale = std::ldexp(1.0f, e);
+    k_half_copy<<<nblk(N, 8), 256, 0, s>>>(ix->X, N, ix->pitch, ix->hpitch, ix->xh_scale, (__half *)ix->Xh,
+                                           ix->xerr);
+    CRISP_LAUNCH();
 }
 
 }  // namespace crisp

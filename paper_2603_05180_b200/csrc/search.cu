@@ -14,6 +14,7 @@
 //                      with patience P = factor*k
 //   a6  k_merge_lists  cross-shard merge (multi-GPU)
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1556,6 +1557,102 @@ __device__ __forceinline__ void load_qd(double *qd, const float *qrow, int pitch
 }
 
 // ---------------------------------------------------------------------------
+// Verification filter (DESIGN R17; crisp_set_verify_filter).  The index keeps
+// x~ = fp16(s x) (s = 2^e) and rho = ||s x - x~|| rounded up.  For a query q'
+// (s q' exact in fp32, checked when it is staged) the warp forms
+// S = fl32(sum_i (s q'_i - x~_i)^2) (lane partials of 8 ceil(nv8/32) terms, then
+// a 5-level butterfly: every term carries at most m = 8 ceil(nv8/32) + 7
+// roundings of 2^-24, the subtraction and the square included), so
+// A_lo = S (1 - (m+1) 2^-24) - tiny <= ||s q' - x~||^2 <= S (1 + (m+2) 2^-24) + tiny
+// = A_hi (tiny covers subnormal rounding).  With the triangle inequality
+//   s ||q' - x|| >= sqrt(A_lo) - rho   and   s ||q' - x|| <= sqrt(A_hi) + rho,
+// and 1e-12 relative slack on each fp64 operation, lb <= s sqrt(d) <= ub for the
+// exact d of the row.  A row whose lb exceeds s sqrt(d_k) (1 + 1e-9), d_k the
+// k-th best distance a top-k already holds, has d > d_k (1 + 2e-9): its
+// exact verification would be a miss, so its fp32 row is not read.
+// ---------------------------------------------------------------------------
+struct FiltArgs {
+    const uint4 *Xh;     // N x nv8 uint4 (8 fp16 each); null: filter off
+    const float *xerr;   // N: rho, rounded up
+    int nv8;             // uint4 per fp16 row (hpitch / 8)
+    float scale;         // s
+    double lo_f, hi_f;   // 1 - (m+1) 2^-24, 1 + (m+2) 2^-24
+    double tiny;         // absolute slack for subnormal rounding
+};
+
+// q' scaled by s, staged as two float4 planes (qh4[v] = s q'[8v..8v+3],
+// qh4[nv8 + v] = s q'[8v+4..8v+7]) so that a warp's reads are contiguous;
+// returns (CTA-uniform) whether every s q'_i is exact (else the filter is off
+// for this query)
+__device__ __forceinline__ bool load_qh(float *qh, const float *qrow, int pitch, int nv8, float scale) {
+    int bad = 0;
+    for (int i = threadIdx.x; i < nv8 * 8; i += blockDim.x) {
+        const float v = i < pitch ? qrow[i] : 0.0f, sv = v * scale;
+        if ((double)sv != (double)v * (double)scale) bad = 1;
+        const int v8 = i >> 3, c = i & 7;
+        qh[((c >> 2) * nv8 + v8) * 4 + (c & 3)] = sv;
+    }
+    return __syncthreads_or(bad) == 0;
+}
+
+__device__ __forceinline__ float h8_acc(const uint4 u, const float4 qa, const float4 qb, float acc) {
+    const float2 f0 = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
+    const float2 f1 = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
+    const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&u.z));
+    const float2 f3 = __half22float2(*reinterpret_cast<const __half2 *>(&u.w));
+    float t;
+    t = __fsub_rn(qa.x, f0.x); acc = __fmaf_rn(t, t, acc);
+    t = __fsub_rn(qa.y, f0.y); acc = __fmaf_rn(t, t, acc);
+    t = __fsub_rn(qa.z, f1.x); acc = __fmaf_rn(t, t, acc);
+    t = __fsub_rn(qa.w, f1.y); acc = __fmaf_rn(t, t, acc);
+    t = __fsub_rn(qb.x, f2.x); acc = __fmaf_rn(t, t, acc);
+    t = __fsub_rn(qb.y, f2.y); acc = __fmaf_rn(t, t, acc);
+    t = __fsub_rn(qb.z, f3.x); acc = __fmaf_rn(t, t, acc);
+    t = __fsub_rn(qb.w, f3.y); acc = __fmaf_rn(t, t, acc);
+    return acc;
+}
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
+// S of R rows at once (lanes take uint4 v = lane, lane + 32, ...; the query
+// plane reads are shared by the R rows); every lane returns the sums
+template <int R>
+__device__ __forceinline__ void rows_h(const uint4 *const (&r)[R], const float4 *__restrict__ qh4, int nv8, int lane,
+                                       float (&o)[R]) {
+    float a[R];
+#pragma unroll
+    for (int u = 0; u < R; u++) a[u] = 0.0f;
+#pragma unroll 2
+    for (int v = lane; v < nv8; v += 32) {
+        uint4 x[R];
+#pragma unroll
+        for (int u = 0; u < R; u++) x[u] = __ldg(r[u] + v);
+        const float4 qa = qh4[v], qb = qh4[nv8 + v];
+#pragma unroll
+        for (int u = 0; u < R; u++) a[u] = h8_acc(x[u], qa, qb, a[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < R; u++) o[u] = warp_sum_f(a[u]);
+}
+
+// certified bounds of s sqrt(d) from S and rho (see above)
+__device__ __forceinline__ double filt_lb(const FiltArgs &f, float S, float rho) {
+    if (!isfinite(S)) return 0.0;
+    const double alo = (double)S * f.lo_f - f.tiny;
+    if (!(alo > 0.0)) return 0.0;
+    return sqrt(alo) * (1.0 - 1e-12) - (double)rho * (1.0 + 1e-12);
+}
+__device__ __forceinline__ double filt_ub(const FiltArgs &f, float S, float rho) {
+    const double ahi = (double)S * f.hi_f + f.tiny;
+    if (!(ahi < INFINITY)) return INFINITY;
+    return sqrt(ahi) * (1.0 + 1e-12) + (double)rho * (1.0 + 1e-12);
+}
+
+// ---------------------------------------------------------------------------
 // a5, Guaranteed Mode: exact L2 of every candidate, per-warp top-k, CTA merge.
 // grid (S, Qc); candidates of query q are split over S*WARPS warps.
 // ---------------------------------------------------------------------------
@@ -1581,14 +1678,16 @@ __device__ __forceinline__ void block_prefix(const int32_t *__restrict__ ncand, 
     }
 }
 
-template <bool ROWS4>
+template <bool ROWS4, bool FILT>
 __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restrict__ qrot, int pitch,
                                                            const float *__restrict__ X, int64_t gid_base,
                                                            const int32_t *__restrict__ pool, int64_t CAPQ,
                                                            const int32_t *__restrict__ cbase,
                                                            const int32_t *__restrict__ ncand, int NB, int k,
                                                            double *__restrict__ part_d, int64_t *__restrict__ part_i,
-                                                           const int32_t *__restrict__ qperm) {
+                                                           const int32_t *__restrict__ qperm,
+                                                           const float2 *__restrict__ lbb, const float *__restrict__ Tq,
+                                                           unsigned long long *__restrict__ fstats) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;
     double *Ld = qd + pitch;                         // WARPS x k
@@ -1627,7 +1726,59 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
             }
         }
     };
-    for (int v = gw; v < total; v += 4 * W) {
+    if (FILT) {
+        // R17: only the candidates whose lower bound does not exceed T (the k-th
+        // smallest upper bound of the query, k_lb_threshold) can be in the top-k;
+        // a warp takes 32 consecutive positions, reads their bounds, and computes
+        // the exact distances of the passing ones four at a time
+        const double Tm = (double)Tq[q] * (1.0 + 1e-9);
+        const float2 *lbq = lbb + q * CAPQ;
+        int bl = 0;  // this lane's segment pointer (its positions only increase)
+        unsigned nb = 0, ne = 0;
+        for (int base = gw * 32; base < total; base += W * 32) {
+            const int v = base + lane;
+            int lid = -1;
+            if (v < total) {
+                while (pre[bl + 1] <= v) bl++;
+                const int p = cbs[bl] + (v - pre[bl]);
+                if (!((double)lbq[p].x > Tm)) lid = poolq[p];
+            }
+            unsigned m = __ballot_sync(0xffffffffu, lid >= 0);
+            nb += min(32, total - base);
+            ne += __popc(m);
+            while (m) {
+                int ls[4], nl = 0;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    ls[u] = -1;
+                    if (m) {
+                        ls[u] = __shfl_sync(0xffffffffu, lid, __ffs(m) - 1);
+                        m &= m - 1;
+                        nl++;
+                    }
+                }
+                if (nl == 4) {
+                    double d4[4];
+                    row_dist4(X + (int64_t)ls[0] * pitch, X + (int64_t)ls[1] * pitch, X + (int64_t)ls[2] * pitch,
+                              X + (int64_t)ls[3] * pitch, qd, nvec, lane, d4);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) offer(d4[u], gid_base + ls[u]);
+                } else {
+                    if (nl >= 2) {
+                        double d0, d1;
+                        row_dist2(X + (int64_t)ls[0] * pitch, X + (int64_t)ls[1] * pitch, qd, nvec, lane, d0, d1);
+                        offer(d0, gid_base + ls[0]);
+                        offer(d1, gid_base + ls[1]);
+                    } else {
+                        offer(row_dist1(X + (int64_t)ls[0] * pitch, qd, nvec, lane), gid_base + ls[0]);
+                    }
+                    if (nl == 3) offer(row_dist1(X + (int64_t)ls[2] * pitch, qd, nvec, lane), gid_base + ls[2]);
+                }
+            }
+        }
+        if (fstats && lane == 0 && nb) atomicAdd(fstats + 1, (unsigned long long)ne);
+    }
+    for (int v = FILT ? total : gw; v < total; v += 4 * W) {
         if (ROWS4 && v + 3 * W < total) {
             int b1 = bcur;
             const int l0 = lid_at(v, bcur), l1 = lid_at(v + W, b1), l2 = lid_at(v + 2 * W, b1),
@@ -1691,6 +1842,144 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
             oi[rank] = id;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// a5, Guaranteed Mode with the verification filter (R17), passes 1 and 2:
+// k_lb_bounds streams the fp16 copies of the query's candidates and writes
+// (lb, ub) per pool slot (lb rounded down, ub rounded up); k_lb_threshold
+// selects T >= the k-th smallest ub (two 11/12-bit histogram passes over the
+// bits of the non-negative floats; T is the upper edge of the bin that holds
+// it).  k rows then have s sqrt(d) <= T, so a row with lb > T (1 + 1e-9) is
+// outside the top-k, and k_rerank_exact<., true> reads only the others.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(THREADS, 3) k_lb_bounds(const float *__restrict__ qrot, int pitch, FiltArgs fa,
+                                                        const int32_t *__restrict__ pool, int64_t CAPQ,
+                                                        const int32_t *__restrict__ cbase,
+                                                        const int32_t *__restrict__ ncand, int NB,
+                                                        float2 *__restrict__ lbb, const int32_t *__restrict__ qperm,
+                                                        unsigned long long *__restrict__ fstats) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    float *qh = (float *)sm;                   // 8 nv8
+    int *pre = (int *)(qh + 8 * fa.nv8);       // NB + 1
+    int *cbs = pre + NB + 1;                   // NB
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    block_prefix(ncand, cbase, q, NB, pre, cbs);
+    const bool exact_q = load_qh(qh, qrot + q * pitch, pitch, fa.nv8, fa.scale);  // syncs the CTA
+    const int total = pre[NB];
+    const int W = gridDim.x * WARPS;
+    const int gw = blockIdx.x * WARPS + warp;
+    const int32_t *poolq = pool + q * CAPQ;
+    float2 *lbq = lbb + q * CAPQ;
+    const float4 *qh4 = (const float4 *)qh;
+    int bcur = 0;
+    auto slot_at = [&](int vv, int &bc) -> int {
+        while (pre[bc + 1] <= vv) bc++;
+        return cbs[bc] + (vv - pre[bc]);
+    };
+    if (!exact_q) {  // s q' not exact: no bound for this query (every row exact)
+        for (int v = blockIdx.x * THREADS + threadIdx.x; v < total; v += gridDim.x * THREADS) {
+            int b = 0;
+            lbq[slot_at(v, b)] = make_float2(0.0f, INFINITY);
+        }
+        return;
+    }
+    for (int v = gw; v < total; v += 4 * W) {
+        int slot[4], rows[4];
+        int b1 = bcur;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int vv = v + u * W;
+            slot[u] = vv < total ? (u == 0 ? slot_at(vv, bcur) : slot_at(vv, b1)) : -1;
+            rows[u] = slot[u] >= 0 ? poolq[slot[u]] : -1;
+        }
+        const uint4 *r4[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) r4[u] = fa.Xh + (int64_t)(rows[u] >= 0 ? rows[u] : rows[0]) * fa.nv8;
+        float S[4];
+        rows_h<4>(r4, qh4, fa.nv8, lane, S);
+        int sl = -1, rl = 0;
+        float Sl = 0.0f;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (lane == u) {
+                sl = slot[u];
+                rl = rows[u];
+                Sl = S[u];
+            }
+        if (sl >= 0) {
+            const float rho = __ldg(fa.xerr + rl);
+            const double lb = filt_lb(fa, Sl, rho), ub = filt_ub(fa, Sl, rho);
+            lbq[sl] = make_float2(__double2float_rd(fmax(lb, 0.0)), __double2float_ru(ub));
+        }
+    }
+    if (fstats && threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(fstats, (unsigned long long)total);
+}
+
+__global__ void __launch_bounds__(THREADS) k_lb_threshold(const int32_t *__restrict__ cbase,
+                                                          const int32_t *__restrict__ ncand, int NB, int64_t CAPQ,
+                                                          const float2 *__restrict__ lbb, int k,
+                                                          float *__restrict__ Tq) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    int *pre = (int *)sm;            // NB + 1
+    int *cbs = pre + NB + 1;         // NB
+    __shared__ unsigned hist[4096];
+    __shared__ unsigned s_bin, s_rank;
+    const int64_t q = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    block_prefix(ncand, cbase, q, NB, pre, cbs);
+    __syncthreads();
+    const int total = pre[NB];
+    if (total <= k) {
+        if (tid == 0) Tq[q] = INFINITY;
+        return;
+    }
+    const float2 *lbq = lbb + q * CAPQ;
+    unsigned prefix = 0, rank = (unsigned)(k - 1);  // 0-based rank of the k-th smallest
+    // pass 0: bits 30..20 (2048 bins); pass 1: bits 19..8 (4096 bins) inside the bin of pass 0
+    for (int pass = 0; pass < 2; pass++) {
+        const int shift = pass == 0 ? 20 : 8, nbins = pass == 0 ? 2048 : 4096;
+        for (int i = tid; i < nbins; i += THREADS) hist[i] = 0;
+        __syncthreads();
+        int b = 0;
+        for (int v = tid; v < total; v += THREADS) {
+            while (pre[b + 1] <= v) b++;
+            const unsigned u = __float_as_uint(lbq[cbs[b] + (v - pre[b])].y);
+            if (pass == 0 || (u >> 20) == prefix) atomicAdd(&hist[(u >> shift) & (nbins - 1)], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            // lane-contiguous bins, lane sums, warp scan, then the bin that holds rank
+            const int per = nbins / 32;
+            unsigned ls = 0;
+            for (int i = 0; i < per; i++) ls += hist[lane * per + i];
+            unsigned inc = ls;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            const unsigned exc = inc - ls;
+            if (rank >= exc && rank < inc) {
+                unsigned c = exc;
+                for (int i = 0; i < per; i++) {
+                    const unsigned h = hist[lane * per + i];
+                    if (rank < c + h) {
+                        s_bin = lane * per + i;
+                        s_rank = rank - c;
+                        break;
+                    }
+                    c += h;
+                }
+            }
+        }
+        __syncthreads();
+        if (pass == 0) prefix = s_bin;
+        else prefix = (prefix << 12) | s_bin;
+        rank = s_rank;
+        __syncthreads();
+    }
+    if (tid == 0) Tq[q] = __uint_as_float((prefix << 8) | 0xffu);  // upper edge of the bin (>= the k-th ub)
 }
 
 // ---------------------------------------------------------------------------
@@ -2485,6 +2774,101 @@ __global__ void __launch_bounds__(THREADS, ROWS4 ? 6 : 5) k_verify_rows(const fl
     }
 }
 
+// A verification round >= 1 with the filter (R17): every row of the span is
+// first bounded through its fp16 copy against the query's k-th best distance
+// at the start of the round (the k-th best only shrinks, so a miss certified
+// against it is a miss at the row's own turn); only rows the bound cannot
+// exclude are read in fp32 for their exact distance.  Excluded rows get +inf
+// in dbuf, which the in-order replay (k_patience_scan) counts as a miss,
+// exactly as their exact distance would be.
+__global__ void __launch_bounds__(THREADS, 3) k_verify_rows_lb(const float *__restrict__ qrot, int pitch,
+                                                             const float *__restrict__ X, FiltArgs fa,
+                                                             const int32_t *__restrict__ pool, int64_t PS,
+                                                             const int32_t *__restrict__ totals, PatState st, int k,
+                                                             int j0r, int len, int send, int dstride,
+                                                             double *__restrict__ dbuf,
+                                                             const int32_t *__restrict__ qperm,
+                                                             unsigned long long *__restrict__ fstats) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    double *qd = (double *)sm;                   // pitch
+    float *qh = (float *)(qd + pitch);           // 8 nv8
+    const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;
+    if (st.done[q]) return;
+    const int total = totals[q];
+    int j0;
+    const int n = round_span(st, q, j0r, len, total, send, j0);
+    if (n <= 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    load_qd(qd, qrot + q * pitch, pitch);
+    const bool exact_q = load_qh(qh, qrot + q * pitch, pitch, fa.nv8, fa.scale);  // syncs the CTA
+    // threshold s sqrt(d_k) (1 + 1e-9); none while the top-k is not full
+    const double thr = (exact_q && st.cnt[q] >= k) ? (double)fa.scale * sqrt(st.Td[q * k + k - 1]) * (1.0 + 1e-9)
+                                                   : -1.0;
+    const int nvec = pitch / 4;
+    const int W = gridDim.x * WARPS;
+    const int32_t *ord = pool + q * PS + j0;
+    double *dq = dbuf + q * (int64_t)dstride;
+    const float4 *qh4 = (const float4 *)qh;
+    unsigned nb = 0, ne = 0;
+    for (int j = blockIdx.x * WARPS + warp; j < n; j += 4 * W) {
+        int rows[4], jj[4], nr = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            jj[u] = j + u * W;
+            rows[u] = jj[u] < n ? ord[jj[u]] : -1;
+            nr += rows[u] >= 0;
+        }
+        unsigned need = 0;  // rows whose exact distance is needed
+        if (thr < 0.0) {
+            need = (1u << nr) - 1u;
+        } else {
+            const uint4 *r4[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) r4[u] = fa.Xh + (int64_t)(rows[u] >= 0 ? rows[u] : rows[0]) * fa.nv8;
+            float S[4];
+            rows_h<4>(r4, qh4, fa.nv8, lane, S);
+            nb += nr;
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (rows[u] >= 0) {
+                    if (filt_lb(fa, S[u], __ldg(fa.xerr + rows[u])) > thr) {
+                        if (lane == 0) dq[jj[u]] = INFINITY;
+                    } else {
+                        need |= 1u << u;
+                    }
+                }
+        }
+        // exact distances of the needed rows, two at a time (need is warp-uniform;
+        // static indices keep rows[] and jj[] in registers)
+        int pr = -1, pj = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if ((need >> u) & 1u) {
+                if (pr < 0) {
+                    pr = rows[u];
+                    pj = jj[u];
+                } else {
+                    double d0, d1;
+                    row_dist2(X + (int64_t)pr * pitch, X + (int64_t)rows[u] * pitch, qd, nvec, lane, d0, d1);
+                    if (lane == 0) {
+                        dq[pj] = d0;
+                        dq[jj[u]] = d1;
+                    }
+                    pr = -1;
+                }
+            }
+        if (pr >= 0) {
+            const double d0 = row_dist1(X + (int64_t)pr * pitch, qd, nvec, lane);
+            if (lane == 0) dq[pj] = d0;
+        }
+        ne += __popc(need);
+    }
+    if (fstats && lane == 0 && (nb | ne)) {
+        atomicAdd(fstats, (unsigned long long)nb);
+        atomicAdd(fstats + 1, (unsigned long long)(thr < 0.0 ? 0 : ne));
+    }
+}
+
 // ADSampling context of Optimized Mode verification (Eq. 2; crisp_set_adsampling)
 struct AdCtx {
     int on;
@@ -2930,6 +3314,12 @@ __global__ void __launch_bounds__(THREADS, 4) k_patience_tail(const float *__res
 // cells), [1] sum |C_q|, [2] rows verified, [3] fallback queries
 // ---------------------------------------------------------------------------
 __device__ unsigned long long d_stats[4];
+__device__ unsigned long long d_filter_stats[2];  // R17: rows bounded through the fp16 copy, of those read exactly
+static unsigned long long *d_filter_stats_ptr() {
+    void *p = nullptr;
+    cudaGetSymbolAddress(&p, d_filter_stats);
+    return (unsigned long long *)p;
+}
 __device__ unsigned long long d_probe_stats[2];  // a1: exact half distances computed, screened walks redone exactly
 static unsigned long long *d_probe_stats_ptr() {
     void *p = nullptr;
@@ -3036,11 +3426,15 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_lb_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_lb_threshold, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows_lb, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -3068,12 +3462,18 @@ struct Work {
     int probe_r = 24;
     int S, S1, HS, S0, R0, BPC, count_kernel, count_atom, NS, CF, ham_fused, rows4, ad, adsp, F, DS, round_rows, nl_min, Pq,
         vra_smem;
+    // verification filter (R17): phi=1 rounds >= 1 (lbf) / phi=0 two-pass re-rank (lb0)
+    FiltArgs fa{};
+    int lbf = 0, lb0 = 0, nl_max = 0, vrl_smem = 0, lbb_smem = 0, lbt_smem = 0;
+    float2 *lbb = nullptr;
+    float *Tq = nullptr;
     // end of the speculative rounds (positions the Hamming order must cover)
     // positions k_hsort orders (the rounds stop there; k_patience_tail completes the
     // order of a query that goes further): ADSampling's fixed rounds + 1024, exact:
     // F + 2 max(P, 512) + 1024 (measured: nver <= 3.7 P at cfg2, k = 10)
     int order_end() const {
-        return ad && !adsp ? (R0 == 0 ? 0 : F + (R0 - 1) * S0) + 1024 : F + 2 * std::max(Pq, 512) + 1024;
+        return ad && !adsp ? (R0 == 0 ? 0 : F + (R0 - 1) * S0) + 1024
+                           : std::max(F, first_round(ix, k)) + 2 * std::max(Pq, 512) + 1024;
     }
     DevBuf buf;
     float *qpad = nullptr, *qrot = nullptr;
@@ -3116,7 +3516,7 @@ struct Work {
         int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 8 + (int64_t)ix->M * 12 + CAPQ * 4 + 4 +
                        (int64_t)ix->M * 2 * 16 +
                        (int64_t)ix->NBW * 8 + 64;
-        if (mode == 0) perq += (int64_t)std::max<int64_t>(S, (ix->N + 4095) / 4096) * k * 16;
+        if (mode == 0) perq += (int64_t)std::max<int64_t>(S, (ix->N + 4095) / 4096) * k * 16 + (ix->Xh ? CAPQ * 8 + 4 : 0);
         else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
         if (traceV) perq += ix->N;
         return perq;
@@ -3172,7 +3572,26 @@ struct Work {
                     : first_round(ix, k);
         else
             F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : first_round(ix, k);
+        // verification filter: a short exact round 0 (the top-k forms), then rounds whose
+        // rows are bounded through the fp16 copy against the k-th best at the round's start;
+        // spans of at most nl_max rows refresh that threshold as the top-k improves
+        lbf = (mode == 1 && !ad && ix->Xh && ix->vfilter && env_int("CRISP_FILTER_ROUNDS", 1)) ? 1 : 0;
+        if (lbf) {
+            F = std::max(64, (std::max(k, env_int("CRISP_LB_FIRST", 512)) + 63) / 64 * 64);
+            R0 = std::max(1, std::min(16, env_int("CRISP_LB_ROUNDS", 6)));
+        }
         DS = std::max({F, S0, std::min(std::max(Pq, nl_min), 1 << 16)});  // dbuf row stride (max span of a round)
+        nl_max = lbf ? std::max(nl_min, std::min(DS, env_int("CRISP_LB_SPAN", 2048))) : DS;
+        if (ix->Xh) {
+            const int nv8 = ix->hpitch / 8, m = 8 * ((nv8 + 31) / 32) + 7;
+            fa.Xh = (const uint4 *)ix->Xh;
+            fa.xerr = ix->xerr;
+            fa.nv8 = nv8;
+            fa.scale = ix->xh_scale;
+            fa.lo_f = 1.0 - (m + 1) * std::ldexp(1.0, -24);
+            fa.hi_f = 1.0 + (m + 2) * std::ldexp(1.0, -24);
+            fa.tiny = (nv8 + 1) * std::ldexp(1.0, -140);
+        }
         round_rows = std::max(1, env_int("CRISP_ROUND_ROWS", 128));  // min rows per CTA in round 0
         vra_smem = pitch * 8 + (Dp / 4 + 1) * 8;
         qpad = buf.alloc<float>((size_t)Qc * pitch);
@@ -3217,6 +3636,11 @@ struct Work {
             const int L = rgroup ? NR : S;
             part_d = buf.alloc<double>((size_t)Qc * L * k);
             part_i = buf.alloc<int64_t>((size_t)Qc * L * k);
+            lb0 = (!rgroup && ix->Xh && ix->vfilter && env_int("CRISP_FILTER_RERANK", 1)) ? 1 : 0;
+            if (lb0) {
+                lbb = buf.alloc<float2>((size_t)Qc * CAPQ);
+                Tq = buf.alloc<float>((size_t)Qc);
+            }
         } else {
             cbuf = buf.alloc<int32_t>((size_t)Qc * CAPQ);
             hbuf = buf.alloc<uint16_t>((size_t)Qc * CAPQ);
@@ -3261,9 +3685,14 @@ struct Work {
         hsort_smem = (Dp + 1 + 2 * NS + 1) * 4;
         hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
         vr_smem = pitch * 8;
+        vrl_smem = pitch * 8 + (ix->hpitch > 0 ? ix->hpitch : 8) * 4;
+        lbb_smem = (ix->hpitch > 0 ? ix->hpitch : 8) * 4 + (2 * NS + 1) * 4;
+        lbt_smem = (2 * NS + 1) * 4;
         scan_smem = WARPS * k * 16 + WARPS * 32 * PSCAN_G * 16;
         pat_smem = pitch * 8 + TAIL_CAP * 16 + k * 16 + (Dp / 4 + 1) * 8 + (Dp + 1 + 2 * NS + 1) * 4;
         set_attrs();
+        if (lbf && vrl_smem > 220 * 1024) lbf = 0;
+        if (lb0 && (lbb_smem > 200 * 1024 || lbt_smem > 140 * 1024)) lb0 = 0;
         CRISP_CHECK(probe_smem <= 200 * 1024 && count_smem <= 200 * 1024 && rx_smem <= 220 * 1024 &&
                         pat_smem <= 220 * 1024 && ham_smem <= 200 * 1024 && scan_smem <= 220 * 1024,
                     "shared-memory footprint too large for this (D, K, k)");
@@ -3432,12 +3861,26 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         {
             StageScope st(s, 4);
             dim3 g(w.S, (unsigned)qn);
-            if (w.rows4)
-                k_rerank_exact<true><<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ,
-                                                                   w.cbase, w.ncand, NB, k, w.part_d, w.part_i, w.qperm);
+            unsigned long long *fst = g_timing ? d_filter_stats_ptr() : nullptr;
+            if (w.lb0) {
+                k_lb_bounds<<<g, THREADS, w.lbb_smem, s>>>(w.qrot, pitch, w.fa, w.pool, w.CAPQ, w.cbase, w.ncand, NB,
+                                                           w.lbb, w.qperm, fst);
+                CRISP_LAUNCH();
+                k_lb_threshold<<<(unsigned)qn, THREADS, w.lbt_smem, s>>>(w.cbase, w.ncand, NB, w.CAPQ, w.lbb, k, w.Tq);
+                CRISP_LAUNCH();
+                k_rerank_exact<false, true><<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool,
+                                                                          w.CAPQ, w.cbase, w.ncand, NB, k, w.part_d,
+                                                                          w.part_i, w.qperm, w.lbb, w.Tq, fst);
+                g_launches += 2;
+            } else if (w.rows4)
+                k_rerank_exact<true, false><<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool,
+                                                                          w.CAPQ, w.cbase, w.ncand, NB, k, w.part_d,
+                                                                          w.part_i, w.qperm, nullptr, nullptr, nullptr);
             else
-                k_rerank_exact<false><<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool, w.CAPQ,
-                                                                    w.cbase, w.ncand, NB, k, w.part_d, w.part_i, w.qperm);
+                k_rerank_exact<false, false><<<g, THREADS, w.rx_smem, s>>>(w.qrot, pitch, ix->X, ix->gid_base, w.pool,
+                                                                           w.CAPQ, w.cbase, w.ncand, NB, k, w.part_d,
+                                                                           w.part_i, w.qperm, nullptr, nullptr,
+                                                                           nullptr);
             CRISP_LAUNCH();
             g_launches++;
         }
@@ -3510,7 +3953,11 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         const int j0 = own ? -1 : (r == 0 ? 0 : w.F + (r - 1) * w.S0), len = r == 0 ? w.F : w.S0;
         // CTAs per query: at most S, at least round_rows rows each (the query staging is per CTA)
         dim3 g(own ? w.S1 : std::max(1, std::min(w.S, len / w.round_rows)), (unsigned)qn);
-        if (w.ad && r > 0)  // round 0 starts with an empty top-k: nothing to prune
+        if (w.lbf && r > 0)
+            k_verify_rows_lb<<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
+                                                            w.pst, k, j0, len, send, w.DS, w.dbuf, w.qperm,
+                                                            g_timing ? d_filter_stats_ptr() : nullptr);
+        else if (w.ad && r > 0)  // round 0 starts with an empty top-k: nothing to prune
             k_verify_rows_ad<<<g, THREADS, w.vra_smem, s>>>(w.qrot, pitch, Dp, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst,
                                                             k, j0, len, send, w.DS, w.dbuf, w.qperm, ix->ad_eps0,
                                                             ix->ad_stride);
@@ -3523,7 +3970,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         CRISP_LAUNCH();
         g_launches++;
         k_patience_scan<<<nblk(qn, WARPS), THREADS, w.scan_smem, s>>>(qn, w.totals, w.cbuf, w.CAPQ, ix->gid_base,
-                                                                      w.dbuf, j0, len, send, w.nl_min, w.DS, w.DS, k,
+                                                                      w.dbuf, j0, len, send, w.nl_min, w.nl_max, w.DS, k,
                                                                       P, w.pst, od64, od, oi, ad, w.qrot);
         CRISP_LAUNCH();
         g_launches++;
@@ -3813,9 +4260,10 @@ extern "C" crisp_status crisp_set_stage_timing(int32_t on) {
 }
 
 extern "C" crisp_status crisp_search_counters(int64_t *out, int32_t n, int32_t reset) {
-    unsigned long long h[4], hp[2];
+    unsigned long long h[4], hp[2], hf[2];
     if (cudaMemcpyFromSymbol(h, crisp::d_stats, sizeof(h)) != cudaSuccess ||
-        cudaMemcpyFromSymbol(hp, crisp::d_probe_stats, sizeof(hp)) != cudaSuccess) {
+        cudaMemcpyFromSymbol(hp, crisp::d_probe_stats, sizeof(hp)) != cudaSuccess ||
+        cudaMemcpyFromSymbol(hf, crisp::d_filter_stats, sizeof(hf)) != cudaSuccess) {
         crisp::set_error("cudaMemcpyFromSymbol failed");
         return CRISP_ECUDA;
     }
@@ -3823,10 +4271,13 @@ extern "C" crisp_status crisp_search_counters(int64_t *out, int32_t n, int32_t r
     if (n > 4) out[4] = crisp::g_launches;
     if (n > 5) out[5] = (int64_t)hp[0];
     if (n > 6) out[6] = (int64_t)hp[1];
+    if (n > 7) out[7] = (int64_t)hf[0];
+    if (n > 8) out[8] = (int64_t)hf[1];
     if (reset) {
         unsigned long long z[4] = {0, 0, 0, 0};
         cudaMemcpyToSymbol(crisp::d_stats, z, sizeof(z));
         cudaMemcpyToSymbol(crisp::d_probe_stats, z, 2 * sizeof(unsigned long long));
+        cudaMemcpyToSymbol(crisp::d_filter_stats, z, 2 * sizeof(unsigned long long));
         crisp::g_launches = 0;
     }
     return CRISP_OK;
