@@ -438,9 +438,9 @@ def run_crisp(args):
                      "k_verify_rows(_ad)+k_patience_scan+k_patience_tail"][mode]
             model = "4 pitch B per verified row (SURVEY 8(d) B_rerank)"
             if cnt.get("filter_rows", 0) > 0:
-                # verification filter (DESIGN R17): 2 hpitch B per row bounded through the fp16
-                # copy, 4 pitch B per row read exactly (round 0, rows the bound keeps, the tail)
-                hrow = 2 * ((info["pitch"] + 7) // 8 * 8)
+                # verification filter (DESIGN R17): c8pitch + 16 B per row bounded through the
+                # int8 copy, 4 pitch B per row read exactly (round 0, rows the bound keeps, the tail)
+                hrow = (info["pitch"] + 15) // 16 * 16 + 16
                 fr, fe = cnt["filter_rows"], cnt["filter_exact"]
                 if mode == 0:
                     vb = (cnt["candidates"] * (hrow + 16) + fe * row_bytes) / K
@@ -448,7 +448,7 @@ def run_crisp(args):
                 else:
                     vb = ((max(0, cnt["verified"] - fr) + fe) * row_bytes + fr * hrow) / K
                     vname = "k_verify_rows+k_verify_rows_lb+k_patience_scan+k_patience_tail"
-                model = "2 hpitch B per row bounded through the fp16 copy + 4 pitch B per row read exactly (R17)"
+                model = "c8pitch + 16 B per row bounded through the int8 copy + 4 pitch B per row read exactly (R17)"
             kernels["verify"] = {"kernel": vname, "bytes_per_step": vb, "ms_per_step": st["verify"] / K,
                                  "achieved_gbs": vb / (st["verify"] / K * 1e-3) / 1e9, "bytes_model": model}
         if st["count_select"] > 0:

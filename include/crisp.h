@@ -177,17 +177,19 @@ crisp_status crisp_set_adsampling(crisp_index *idx, int32_t enable, double eps0,
 
 /* Verification filter (a5 of both modes; DESIGN R17).  The exact re-rank
  * (Alg. 1 l.22-27) only needs the exact distance of a candidate
- * that can enter the current top-k.  With the filter on, the index keeps a
- * 2-byte copy fp16(s x) of every stored row (s a power of two) and the
- * residual norm of each row, rounded up; a search first bounds
- * ||q' - x|| from below through that copy (triangle inequality, certified
- * rounding) and reads the fp32 row only when the bound does not exceed the
- * current k-th best distance.  A candidate skipped this way is one the exact
- * rule would verify without improving the top-k, so ids, distances, patience
- * stops and counters of the results are unchanged.  enable = 1 builds the copy
- * (N x padded_D x 2 bytes of HBM) if absent; enable = 0 frees it.  Indexes are
- * built with the filter on unless the environment sets CRISP_VERIFY_FILTER=0.
- * Blocks until searches in flight on the index's device have finished. */
+ * that can enter the current top-k.  With the filter on, the index keeps every
+ * stored row centred on the column means and quantised per row to int8
+ * (x - mu ~ 2^e c), with c.c, e and a rounded-up residual norm per row; a
+ * search first bounds ||q' - x|| from below through that copy (exact integer
+ * dot products with two int8 digit planes of q' - mu, Cauchy-Schwarz and the
+ * triangle inequality, certified fp64 rounding) and reads the fp32 row only
+ * when the bound does not exceed the current k-th best distance.  A candidate
+ * skipped this way is one the exact rule would verify without improving the
+ * top-k, so ids, distances and patience stops are unchanged.  enable = 1
+ * builds the copy (N x padded_D bytes + 16 B per row of HBM) if absent;
+ * enable = 0 frees it.  Indexes are built with the filter on unless the
+ * environment sets CRISP_VERIFY_FILTER=0.  Blocks until searches in flight on
+ * the index's device have finished. */
 crisp_status crisp_set_verify_filter(crisp_index *idx, int32_t enable);
 
 crisp_status crisp_index_info(const crisp_index *idx, crisp_index_info_t *out);

@@ -276,7 +276,7 @@ class Index:
         _check(lib().crisp_set_adsampling(self._h, 1 if enable else 0, float(eps0), int(stride)))
 
     def set_verify_filter(self, enable: bool = True):
-        """crisp_set_verify_filter: the certified fp16 distance bound in front of the
+        """crisp_set_verify_filter: the certified int8 distance bound in front of the
         exact re-rank (results unchanged; DESIGN R17)."""
         _check(lib().crisp_set_verify_filter(self._h, 1 if enable else 0))
 

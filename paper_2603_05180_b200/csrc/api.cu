@@ -114,8 +114,9 @@ static void free_index(crisp_index *ix) {
     cudaFree(ix->off2w);
     cudaFree(ix->gsize);
     cudaFree(ix->codes);
-    cudaFree(ix->Xh);
-    cudaFree(ix->xerr);
+    cudaFree(ix->C8);
+    cudaFree(ix->c8meta);
+    cudaFree(ix->mu);
     delete ix;
 }
 
@@ -425,7 +426,7 @@ crisp_status crisp_set_verify_filter(crisp_index *ix, int32_t enable) {
         CRISP_CHECK(ix != nullptr, "index is NULL");
         CRISP_CUDA(cudaSetDevice(ix->device));
         CRISP_CUDA(cudaDeviceSynchronize());  // searches in flight may read the copy
-        if (enable && !ix->Xh) {
+        if (enable && !ix->C8) {
             cudaStream_t s;
             CRISP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
             try {
@@ -436,12 +437,14 @@ crisp_status crisp_set_verify_filter(crisp_index *ix, int32_t enable) {
                 throw;
             }
             cudaStreamDestroy(s);
-        } else if (!enable && ix->Xh) {
-            cudaFree(ix->Xh);
-            cudaFree(ix->xerr);
-            ix->Xh = nullptr;
-            ix->xerr = nullptr;
-            ix->hbm_bytes -= ix->N * (int64_t)ix->hpitch * 2 + ix->N * 4;
+        } else if (!enable && ix->C8) {
+            cudaFree(ix->C8);
+            cudaFree(ix->c8meta);
+            cudaFree(ix->mu);
+            ix->C8 = nullptr;
+            ix->c8meta = nullptr;
+            ix->mu = nullptr;
+            ix->hbm_bytes -= ix->N * (int64_t)ix->c8pitch + ix->N * 16 + (int64_t)ix->pitch * 4;
         }
         ix->vfilter = enable ? 1 : 0;
         return CRISP_OK;

@@ -8,7 +8,6 @@
 // summation order; they feed a threshold decision (CEV > 0.85) and R, which
 // parity tests inject (crisp_build_with) or check by property.
 #include <cub/cub.cuh>
-#include <cuda_fp16.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -1118,68 +1117,101 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
 }
 
 // ---------------------------------------------------------------------------
-// Verification filter (DESIGN R17).  x~ = fp16(s x) with s = 2^e chosen so that
-// max |s x| <= 2^15 (no fp16 overflow; s x is exact in fp32), and per row the
-// residual norm rho = ||s x - x~|| (every difference exact in fp64, the sum in
-// fp64, rounded up with a 1e-9 relative margin).  By the triangle inequality
-// ||s q - s x|| >= ||s q - x~|| - rho, so the search can certify that a row
-// does not enter the top-k from its 2-byte copy (search.cu, k_verify_rows_lb).
+// Verification filter (DESIGN R17).  mu = column means (fp64 sums in a fixed
+// order, rounded to fp32); per row, y = x - mu (fp64, exact up to 2^-53
+// relative), e with max |y_i| < 2^(e+7), c_i = clamp(rint(y_i 2^-e), +-127),
+// the integer c.c, and rho = ||y - 2^e c|| (fp64 sum, rounded up with a 1e-9
+// relative and a 1e-15 ||y|| absolute margin).  The search bounds
+// ||q' - x|| from these (search.cu, filt_bounds) and reads the fp32 row only
+// when the bound cannot exclude it.
 // ---------------------------------------------------------------------------
-__global__ void k_absmax(const float *X, int64_t n, unsigned *out) {
-    unsigned m = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        m = max(m, __float_as_uint(fabsf(X[i])));  // non-negative floats order as their bits
-    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+constexpr int MU_CHUNKS = 512;
+__global__ void k_mu_partial(const float *__restrict__ X, int64_t N, int pitch, double *__restrict__ part) {
+    // block (32 columns x 8 row lanes), chunk blockIdx.y of the rows
+    const int col = blockIdx.x * 32 + (threadIdx.x & 31), rl = threadIdx.x >> 5;
+    const int64_t r0 = N * blockIdx.y / MU_CHUNKS, r1 = N * (blockIdx.y + 1) / MU_CHUNKS;
+    __shared__ double sh[8][32];
+    double a = 0.0;
+    if (col < pitch)
+        for (int64_t r = r0 + rl; r < r1; r += 8) a += (double)X[r * pitch + col];
+    sh[rl][threadIdx.x & 31] = a;
+    __syncthreads();
+    if (rl == 0 && col < pitch) {
+        double t = 0.0;
+        for (int i = 0; i < 8; i++) t += sh[i][threadIdx.x & 31];
+        part[(int64_t)blockIdx.y * pitch + col] = t;
+    }
+}
+__global__ void k_mu_final(const double *__restrict__ part, int pitch, int64_t N, float *__restrict__ mu) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= pitch) return;
+    double t = 0.0;
+    for (int c = 0; c < MU_CHUNKS; c++) t += part[(int64_t)c * pitch + col];
+    mu[col] = (float)(t / (double)N);
 }
 
-__global__ void k_half_copy(const float *__restrict__ X, int64_t N, int pitch, int hpitch, float scale,
-                            __half *__restrict__ Xh, float *__restrict__ xerr) {
+__global__ void k_int8_copy(const float *__restrict__ X, int64_t N, int pitch, int c8pitch,
+                            const float *__restrict__ mu, int8_t *__restrict__ C8, int4 *__restrict__ meta) {
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= N) return;
     const float *x = X + row * pitch;
-    __half *h = Xh + row * hpitch;
-    double e = 0.0;
-    for (int i = lane; i < hpitch; i += 32) {
-        const float xs = (i < pitch ? x[i] : 0.0f) * scale;  // exact: scale = 2^e and |xs| < 2^15
-        const __half hv = __float2half_rn(xs);
-        h[i] = hv;
-        const double r = (double)xs - (double)__half2float(hv);  // exact in fp64
-        e = fma(r, r, e);
+    double m = 0.0, n2 = 0.0;
+    for (int i = lane; i < pitch; i += 32) {
+        const double y = (double)x[i] - (double)mu[i];
+        m = fmax(m, fabs(y));
+        n2 = fma(y, y, n2);
     }
-    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-    // the fp64 sum of D non-negative terms is within D 2^-53 relative of the exact sum
-    if (lane == 0) xerr[row] = __double2float_ru(sqrt(e) * (1.0 + 1e-9));
+    for (int o = 16; o; o >>= 1) {
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    }
+    int e = 0;
+    if (m > 0.0) {
+        frexp(m, &e);  // m < 2^e
+        e -= 7;        // |y_i 2^-e| < 128
+    }
+    const double up = ldexp(1.0, -e), dn = ldexp(1.0, e);
+    int8_t *c = C8 + row * c8pitch;
+    double r2 = 0.0;
+    int cc = 0;
+    for (int i = lane; i < c8pitch; i += 32) {
+        const double y = i < pitch ? (double)x[i] - (double)mu[i] : 0.0;
+        const double v = fmin(127.0, fmax(-127.0, rint(y * up)));
+        c[i] = (int8_t)v;
+        cc += (int)v * (int)v;
+        const double r = y - v * dn;
+        r2 = fma(r, r, r2);
+    }
+    for (int o = 16; o; o >>= 1) {
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        cc += __shfl_xor_sync(0xffffffffu, cc, o);
+    }
+    if (lane == 0) {
+        const float rho = __double2float_ru(sqrt(r2) * (1.0 + 1e-9) + 1e-15 * sqrt(n2));
+        meta[row] = make_int4(cc, e, __float_as_int(rho), 0);
+    }
 }
 
 void build_verify_filter(crisp_index *ix, cudaStream_t s) {
-    const int64_t N = ix->N, n = N * (int64_t)ix->pitch;
-    ix->hpitch = (ix->pitch + 7) / 8 * 8;
-    if (!ix->Xh) {
-        CRISP_CUDA(cudaMalloc(&ix->Xh, (size_t)N * ix->hpitch * 2 + 16));
-        CRISP_CUDA(cudaMalloc(&ix->xerr, (size_t)N * 4 + 16));
-        ix->hbm_bytes += N * (int64_t)ix->hpitch * 2 + N * 4;
+    const int64_t N = ix->N;
+    const int pitch = ix->pitch;
+    ix->c8pitch = (pitch + 15) / 16 * 16;
+    if (!ix->C8) {
+        CRISP_CUDA(cudaMalloc(&ix->C8, (size_t)N * ix->c8pitch + 64));
+        CRISP_CUDA(cudaMalloc(&ix->c8meta, (size_t)N * 16 + 16));
+        CRISP_CUDA(cudaMalloc(&ix->mu, (size_t)pitch * 4 + 16));
+        ix->hbm_bytes += N * (int64_t)ix->c8pitch + N * 16 + (int64_t)pitch * 4;
     }
     Scratch sc;
-    unsigned *mx = sc.alloc<unsigned>(1);
-    CRISP_CUDA(cudaMemsetAsync(mx, 0, 4, s));
-    k_absmax<<<1184, 256, 0, s>>>(ix->X, n, mx);
+    double *part = sc.alloc<double>((size_t)MU_CHUNKS * pitch);
+    k_mu_partial<<<dim3(nblk(pitch, 32), MU_CHUNKS), 256, 0, s>>>(ix->X, N, pitch, part);
     CRISP_LAUNCH();
-    unsigned hm = 0;
-    CRISP_CUDA(cudaMemcpyAsync(&hm, mx, 4, cudaMemcpyDeviceToHost, s));
-    CRISP_CUDA(cudaStreamSynchronize(s));
-    float amax;
-    memcpy(&amax, &hm, 4);
-    int e = 0;
-    if (amax > 0.0f) {
-        std::frexp(amax, &e);          // amax < 2^e
-        e = std::max(-100, std::min(100, 15 - e));  // |s x| < 2^15
-    }
-    ix->xh_scale = std::ldexp(1.0f, e);
-    k_half_copy<<<nblk(N, 8), 256, 0, s>>>(ix->X, N, ix->pitch, ix->hpitch, ix->xh_scale, (__half *)ix->Xh,
-                                           ix->xerr);
+    k_mu_final<<<nblk(pitch, 128), 128, 0, s>>>(part, pitch, N, ix->mu);
     CRISP_LAUNCH();
+    k_int8_copy<<<nblk(N, 8), 256, 0, s>>>(ix->X, N, pitch, ix->c8pitch, ix->mu, ix->C8, (int4 *)ix->c8meta);
+    CRISP_LAUNCH();
+    CRISP_CUDA(cudaStreamSynchronize(s));  // the scratch is freed on return
 }
 
 }  // namespace crisp

@@ -79,12 +79,13 @@ struct crisp_index {
     int32_t *off2w = nullptr;  // M x K^2 x (NBW+1): the same at warp sub-block granularity SBW = BS/8
     int32_t *gsize = nullptr;  // M x K^2 sizes for the budget walk (local or global)
     uint64_t *codes = nullptr; // N x W
-    // verification filter (DESIGN R17): fp16 copy of s X (s = xh_scale, a power of two) and the
-    // residual norms ||s x - fp16(s x)||, rounded up; certified lower bounds of the exact distances
-    uint16_t *Xh = nullptr;    // N x pitch fp16 bit patterns (null: filter off)
-    float *xerr = nullptr;     // N
-    float xh_scale = 1.0f;
-    int32_t hpitch = 0;        // fp16 row stride (pitch rounded up to 8)
+    // verification filter (DESIGN R17): rows centred on the column means and quantised per
+    // row to int8 (x - mu ~ 2^e c), with c.c, e and rho >= ||(x - mu) - 2^e c|| per row;
+    // certified bounds of the exact distances from a D-byte read
+    int8_t *C8 = nullptr;      // N x c8pitch codes (null: filter off)
+    int32_t *c8meta = nullptr; // N x 4: {c.c, e, rho (float bits), 0}
+    float *mu = nullptr;       // pitch: column means (fp32)
+    int32_t c8pitch = 0;       // code row stride (pitch rounded up to 16)
     int32_t vfilter = 1;       // build (and use) the filter
     int32_t BS = 0, NB = 0;    // on-chip counter block: ids per block, number of blocks
     int32_t SBW = 0, NBW = 0;  // warp sub-block: ids per sub-block (BS/8), number of sub-blocks (8*NB)
@@ -120,7 +121,7 @@ int64_t cev_sample_size(int64_t N);
 void sample_row_ids(int64_t N, int64_t n, uint64_t seed, uint32_t stream, int32_t *rows_dev, cudaStream_t s);
 double cev_of_sample(const float *S_dev, int64_t n, int D, cudaStream_t s, std::vector<double> *var = nullptr);
 void finish_csr(crisp_index *ix, cudaStream_t s);
-// the verification filter's fp16 copy of X and residual norms (build.cu; R17)
+// the verification filter's int8 copy of the centred rows (build.cu; R17)
 void build_verify_filter(crisp_index *ix, cudaStream_t s);
 
 // fp64 sequential-order GEMM: Y(rows x Dp, pitch ldy) = fl32(X(rows x Dp, pitch ldx) . R(Dp x Dp))

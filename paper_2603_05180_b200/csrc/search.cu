@@ -14,7 +14,6 @@
 //                      with patience P = factor*k
 //   a6  k_merge_lists  cross-shard merge (multi-GPU)
 #include <cub/cub.cuh>
-#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1558,98 +1557,153 @@ __device__ __forceinline__ void load_qd(double *qd, const float *qrow, int pitch
 
 // ---------------------------------------------------------------------------
 // Verification filter (DESIGN R17; crisp_set_verify_filter).  The index keeps
-// x~ = fp16(s x) (s = 2^e) and rho = ||s x - x~|| rounded up.  For a query q'
-// (s q' exact in fp32, checked when it is staged) the warp forms
-// S = fl32(sum_i (s q'_i - x~_i)^2) (lane partials of 8 ceil(nv8/32) terms, then
-// a 5-level butterfly: every term carries at most m = 8 ceil(nv8/32) + 7
-// roundings of 2^-24, the subtraction and the square included), so
-// A_lo = S (1 - (m+1) 2^-24) - tiny <= ||s q' - x~||^2 <= S (1 + (m+2) 2^-24) + tiny
-// = A_hi (tiny covers subnormal rounding).  With the triangle inequality
-//   s ||q' - x|| >= sqrt(A_lo) - rho   and   s ||q' - x|| <= sqrt(A_hi) + rho,
-// and 1e-12 relative slack on each fp64 operation, lb <= s sqrt(d) <= ub for the
-// exact d of the row.  A row whose lb exceeds s sqrt(d_k) (1 + 1e-9), d_k the
-// k-th best distance a top-k already holds, has d > d_k (1 + 2e-9): its
-// exact verification would be a miss, so its fp32 row is not read.
+// every row centred on the column means mu (fp32) and quantised per row:
+// x~ = 2^e c with c in [-127, 127]^D (int8), the integer sum c.c, and
+// rho >= ||(x - mu) - x~|| (fp64, rounded up).  Per query, y = q' - mu (fp64)
+// is written as y_fx = 2^(E-6) (d1 + 2^-7 d2) with int8 digits d1, d2 in
+// [-64, 64] (k_q8_prep) and R >= ||y - y_fx||.  A warp then forms the integer
+// dot products S1 = d1.c, S2 = d2.c exactly (dp4a, int32), so that
+//   P = <y_fx, x~> = 2^(E-6+e) (S1 + S2/128)       (exact in fp64)
+//   ||y - x~||^2 = ||y||^2 - 2 P + ||x~||^2 - 2 <y - y_fx, x~>,
+//   |<y - y_fx, x~>| <= R ||x~||                   (Cauchy-Schwarz),
+// and, with the triangle inequality ||q' - x|| = ||y - (x - mu)||,
+//   sqrt(A_lo) - rho <= ||q' - x|| <= sqrt(A_hi) + rho
+// where A_lo/A_hi carry the Cauchy-Schwarz term and 1e-11 relative slack for
+// the fp64 evaluation (every other factor 1e-12).  A row whose lower bound
+// exceeds sqrt(d_k) (1 + 1e-9), d_k the k-th best distance a top-k already
+// holds, has d > d_k (1 + 2e-9): its exact verification would be a miss, so
+// its fp32 row is not read.  Bytes per bounded row: D (codes) + 16 (meta).
 // ---------------------------------------------------------------------------
 struct FiltArgs {
-    const uint4 *Xh;     // N x nv8 uint4 (8 fp16 each); null: filter off
-    const float *xerr;   // N: rho, rounded up
-    int nv8;             // uint4 per fp16 row (hpitch / 8)
-    float scale;         // s
-    double lo_f, hi_f;   // 1 - (m+1) 2^-24, 1 + (m+2) 2^-24
-    double tiny;         // absolute slack for subnormal rounding
+    const uint4 *C8;     // N x nv16 (16 int8 codes each); null: filter off
+    const int4 *meta;    // N: {c.c, e, rho (float bits), 0}
+    int nv16;            // uint4 per code row (c8pitch / 16)
+    const uint4 *qd;     // Qc x 2 nv16: digit planes d1 | d2 of each query (k_q8_prep)
+    const double *qi;    // Qc x 4: {2^(E-6), ||y||^2, R, ok}
 };
 
-// q' scaled by s, staged as two float4 planes (qh4[v] = s q'[8v..8v+3],
-// qh4[nv8 + v] = s q'[8v+4..8v+7]) so that a warp's reads are contiguous;
-// returns (CTA-uniform) whether every s q'_i is exact (else the filter is off
-// for this query)
-__device__ __forceinline__ bool load_qh(float *qh, const float *qrow, int pitch, int nv8, float scale) {
+// per query: y = q' - mu, its two digit planes and the bound terms
+__global__ void __launch_bounds__(256) k_q8_prep(const float *__restrict__ qrot, int pitch,
+                                                 const float *__restrict__ mu, int c8pitch, uint4 *__restrict__ qd,
+                                                 double *__restrict__ qi) {
+    const int64_t q = blockIdx.x;
+    const float *qr = qrot + q * pitch;
+    __shared__ double red[3][8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double m = 0.0, n2 = 0.0;
     int bad = 0;
-    for (int i = threadIdx.x; i < nv8 * 8; i += blockDim.x) {
-        const float v = i < pitch ? qrow[i] : 0.0f, sv = v * scale;
-        if ((double)sv != (double)v * (double)scale) bad = 1;
-        const int v8 = i >> 3, c = i & 7;
-        qh[((c >> 2) * nv8 + v8) * 4 + (c & 3)] = sv;
+    for (int i = tid; i < pitch; i += 256) {
+        const double y = (double)qr[i] - (double)mu[i];
+        if (!isfinite(y)) bad = 1;
+        m = fmax(m, fabs(y));
+        n2 = fma(y, y, n2);
     }
-    return __syncthreads_or(bad) == 0;
+    for (int o = 16; o; o >>= 1) {
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    }
+    if (lane == 0) {
+        red[0][warp] = m;
+        red[1][warp] = n2;
+    }
+    bad = __syncthreads_or(bad);
+    m = 0.0;
+    n2 = 0.0;
+    for (int w = 0; w < 8; w++) {
+        m = fmax(m, red[0][w]);
+        n2 += red[1][w];
+    }
+    int E = 0;
+    if (m > 0.0) frexp(m, &E);  // m < 2^E
+    const double up = ldexp(1.0, 6 - E), dn = ldexp(1.0, E - 6);
+    int8_t *d1 = (int8_t *)(qd + q * 2 * (c8pitch / 16)), *d2 = d1 + c8pitch;
+    double r2 = 0.0;
+    for (int i = tid; i < c8pitch; i += 256) {
+        const double y = i < pitch ? (double)qr[i] - (double)mu[i] : 0.0;
+        const double v = y * up;                      // |v| < 64
+        const double a = rint(v), b = rint((v - a) * 128.0);  // both in [-64, 64]
+        d1[i] = bad ? 0 : (int8_t)a;
+        d2[i] = bad ? 0 : (int8_t)b;
+        const double r = y - dn * (a + b * 0.0078125);  // |r| <= 2^(E-14)
+        r2 = fma(r, r, r2);
+    }
+    for (int o = 16; o; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    __syncthreads();
+    if (lane == 0) red[2][warp] = r2;
+    __syncthreads();
+    if (tid == 0) {
+        r2 = 0.0;
+        for (int w = 0; w < 8; w++) r2 += red[2][w];
+        // y itself is exact up to 2^-53 relative (fp32 - fp32 in fp64): 1e-15 ||y|| covers it
+        qi[q * 4 + 0] = dn;
+        qi[q * 4 + 1] = n2;
+        qi[q * 4 + 2] = sqrt(r2) * (1.0 + 1e-9) + 1e-15 * sqrt(n2);
+        qi[q * 4 + 3] = (bad || !isfinite(n2)) ? 0.0 : 1.0;
+    }
 }
 
-__device__ __forceinline__ float h8_acc(const uint4 u, const float4 qa, const float4 qb, float acc) {
-    const float2 f0 = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
-    const float2 f1 = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
-    const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&u.z));
-    const float2 f3 = __half22float2(*reinterpret_cast<const __half2 *>(&u.w));
-    float t;
-    t = __fsub_rn(qa.x, f0.x); acc = __fmaf_rn(t, t, acc);
-    t = __fsub_rn(qa.y, f0.y); acc = __fmaf_rn(t, t, acc);
-    t = __fsub_rn(qa.z, f1.x); acc = __fmaf_rn(t, t, acc);
-    t = __fsub_rn(qa.w, f1.y); acc = __fmaf_rn(t, t, acc);
-    t = __fsub_rn(qb.x, f2.x); acc = __fmaf_rn(t, t, acc);
-    t = __fsub_rn(qb.y, f2.y); acc = __fmaf_rn(t, t, acc);
-    t = __fsub_rn(qb.z, f3.x); acc = __fmaf_rn(t, t, acc);
-    t = __fsub_rn(qb.w, f3.y); acc = __fmaf_rn(t, t, acc);
-    return acc;
-}
-
-__device__ __forceinline__ float warp_sum_f(float v) {
-#pragma unroll
-    for (int off = 16; off; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-    return v;
-}
-
-// S of R rows at once (lanes take uint4 v = lane, lane + 32, ...; the query
-// plane reads are shared by the R rows); every lane returns the sums
+// S1 = d1.c and S2 = d2.c of R rows at once (lanes take uint4 v = lane, lane +
+// 32, ...; the digit reads are shared by the R rows); every lane returns them
 template <int R>
-__device__ __forceinline__ void rows_h(const uint4 *const (&r)[R], const float4 *__restrict__ qh4, int nv8, int lane,
-                                       float (&o)[R]) {
-    float a[R];
+__device__ __forceinline__ void rows_q8(const uint4 *const (&r)[R], const uint4 *__restrict__ sq, int nv16, int lane,
+                                        int (&S1)[R], int (&S2)[R]) {
+    int a[R], b[R];
 #pragma unroll
-    for (int u = 0; u < R; u++) a[u] = 0.0f;
+    for (int u = 0; u < R; u++) a[u] = b[u] = 0;
 #pragma unroll 2
-    for (int v = lane; v < nv8; v += 32) {
+    for (int v = lane; v < nv16; v += 32) {
         uint4 x[R];
 #pragma unroll
         for (int u = 0; u < R; u++) x[u] = __ldg(r[u] + v);
-        const float4 qa = qh4[v], qb = qh4[nv8 + v];
+        const uint4 p = sq[v], t = sq[nv16 + v];
 #pragma unroll
-        for (int u = 0; u < R; u++) a[u] = h8_acc(x[u], qa, qb, a[u]);
+        for (int u = 0; u < R; u++) {
+            a[u] = __dp4a((int)x[u].x, (int)p.x, a[u]);
+            a[u] = __dp4a((int)x[u].y, (int)p.y, a[u]);
+            a[u] = __dp4a((int)x[u].z, (int)p.z, a[u]);
+            a[u] = __dp4a((int)x[u].w, (int)p.w, a[u]);
+            b[u] = __dp4a((int)x[u].x, (int)t.x, b[u]);
+            b[u] = __dp4a((int)x[u].y, (int)t.y, b[u]);
+            b[u] = __dp4a((int)x[u].z, (int)t.z, b[u]);
+            b[u] = __dp4a((int)x[u].w, (int)t.w, b[u]);
+        }
     }
 #pragma unroll
-    for (int u = 0; u < R; u++) o[u] = warp_sum_f(a[u]);
+    for (int u = 0; u < R; u++) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            a[u] += __shfl_xor_sync(0xffffffffu, a[u], off);
+            b[u] += __shfl_xor_sync(0xffffffffu, b[u], off);
+        }
+        S1[u] = a[u];
+        S2[u] = b[u];
+    }
 }
 
-// certified bounds of s sqrt(d) from S and rho (see above)
-__device__ __forceinline__ double filt_lb(const FiltArgs &f, float S, float rho) {
-    if (!isfinite(S)) return 0.0;
-    const double alo = (double)S * f.lo_f - f.tiny;
-    if (!(alo > 0.0)) return 0.0;
-    return sqrt(alo) * (1.0 - 1e-12) - (double)rho * (1.0 + 1e-12);
+// per-query terms of the bound, staged once per CTA
+struct QTerms {
+    double dn, n2, R;
+    bool ok;
+};
+__device__ __forceinline__ QTerms load_q8(uint4 *sq, const FiltArgs &fa, int64_t q) {
+    const uint4 *g = fa.qd + q * 2 * fa.nv16;
+    for (int i = threadIdx.x; i < 2 * fa.nv16; i += blockDim.x) sq[i] = g[i];
+    const double *t = fa.qi + q * 4;
+    return QTerms{t[0], t[1], t[2], t[3] != 0.0};
 }
-__device__ __forceinline__ double filt_ub(const FiltArgs &f, float S, float rho) {
-    const double ahi = (double)S * f.hi_f + f.tiny;
-    if (!(ahi < INFINITY)) return INFINITY;
-    return sqrt(ahi) * (1.0 + 1e-12) + (double)rho * (1.0 + 1e-12);
+
+// certified lower / upper bounds of ||q' - x|| (see above)
+__device__ __forceinline__ void filt_bounds(const QTerms &qt, int S1, int S2, int4 meta, double &lb, double &ub) {
+    const double sc = ldexp(qt.dn, meta.y);
+    const double P = sc * ((double)S1 + (double)S2 * 0.0078125);
+    const double X2 = ldexp((double)meta.x, 2 * meta.y);
+    const double xn = sqrt(X2) * (1.0 + 1e-12);
+    const double A = qt.n2 - 2.0 * P + X2;
+    const double slack = 2.0 * qt.R * xn * (1.0 + 1e-12) + 1e-11 * (qt.n2 + X2 + 2.0 * fabs(P));
+    const double rho = (double)__int_as_float(meta.z) * (1.0 + 1e-12);
+    const double alo = A - slack, ahi = A + slack;
+    lb = (qt.ok && alo > 0.0) ? sqrt(alo) * (1.0 - 1e-12) - rho : 0.0;
+    ub = qt.ok ? sqrt(fmax(ahi, 0.0)) * (1.0 + 1e-12) + rho : INFINITY;
 }
 
 // ---------------------------------------------------------------------------
@@ -1846,11 +1900,11 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
 
 // ---------------------------------------------------------------------------
 // a5, Guaranteed Mode with the verification filter (R17), passes 1 and 2:
-// k_lb_bounds streams the fp16 copies of the query's candidates and writes
-// (lb, ub) per pool slot (lb rounded down, ub rounded up); k_lb_threshold
-// selects T >= the k-th smallest ub (two 11/12-bit histogram passes over the
-// bits of the non-negative floats; T is the upper edge of the bin that holds
-// it).  k rows then have s sqrt(d) <= T, so a row with lb > T (1 + 1e-9) is
+// k_lb_bounds streams the int8 copies of the query's candidates and writes
+// (lb, ub) of ||q' - x|| per pool slot (lb rounded down, ub rounded up);
+// k_lb_threshold selects T >= the k-th smallest ub (two 11/12-bit histogram
+// passes over the bits of the non-negative floats; T is the upper edge of the
+// bin that holds it).  k rows then have sqrt(d) <= T, so a row with lb > T (1 + 1e-9) is
 // outside the top-k, and k_rerank_exact<., true> reads only the others.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(THREADS, 3) k_lb_bounds(const float *__restrict__ qrot, int pitch, FiltArgs fa,
@@ -1860,25 +1914,25 @@ __global__ void __launch_bounds__(THREADS, 3) k_lb_bounds(const float *__restric
                                                         float2 *__restrict__ lbb, const int32_t *__restrict__ qperm,
                                                         unsigned long long *__restrict__ fstats) {
     extern __shared__ __align__(16) unsigned char sm[];
-    float *qh = (float *)sm;                   // 8 nv8
-    int *pre = (int *)(qh + 8 * fa.nv8);       // NB + 1
+    uint4 *sq = (uint4 *)sm;                   // 2 nv16 (the query's digit planes)
+    int *pre = (int *)(sq + 2 * fa.nv16);      // NB + 1
     int *cbs = pre + NB + 1;                   // NB
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     block_prefix(ncand, cbase, q, NB, pre, cbs);
-    const bool exact_q = load_qh(qh, qrot + q * pitch, pitch, fa.nv8, fa.scale);  // syncs the CTA
+    const QTerms qt = load_q8(sq, fa, q);
+    __syncthreads();
     const int total = pre[NB];
     const int W = gridDim.x * WARPS;
     const int gw = blockIdx.x * WARPS + warp;
     const int32_t *poolq = pool + q * CAPQ;
     float2 *lbq = lbb + q * CAPQ;
-    const float4 *qh4 = (const float4 *)qh;
     int bcur = 0;
     auto slot_at = [&](int vv, int &bc) -> int {
         while (pre[bc + 1] <= vv) bc++;
         return cbs[bc] + (vv - pre[bc]);
     };
-    if (!exact_q) {  // s q' not exact: no bound for this query (every row exact)
+    if (!qt.ok) {  // non-finite q': no bound for this query (every row exact)
         for (int v = blockIdx.x * THREADS + threadIdx.x; v < total; v += gridDim.x * THREADS) {
             int b = 0;
             lbq[slot_at(v, b)] = make_float2(0.0f, INFINITY);
@@ -1896,21 +1950,21 @@ __global__ void __launch_bounds__(THREADS, 3) k_lb_bounds(const float *__restric
         }
         const uint4 *r4[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) r4[u] = fa.Xh + (int64_t)(rows[u] >= 0 ? rows[u] : rows[0]) * fa.nv8;
-        float S[4];
-        rows_h<4>(r4, qh4, fa.nv8, lane, S);
-        int sl = -1, rl = 0;
-        float Sl = 0.0f;
+        for (int u = 0; u < 4; u++) r4[u] = fa.C8 + (int64_t)(rows[u] >= 0 ? rows[u] : rows[0]) * fa.nv16;
+        int S1[4], S2[4];
+        rows_q8<4>(r4, sq, fa.nv16, lane, S1, S2);
+        int sl = -1, rl = 0, s1 = 0, s2 = 0;
 #pragma unroll
         for (int u = 0; u < 4; u++)
             if (lane == u) {
                 sl = slot[u];
                 rl = rows[u];
-                Sl = S[u];
+                s1 = S1[u];
+                s2 = S2[u];
             }
         if (sl >= 0) {
-            const float rho = __ldg(fa.xerr + rl);
-            const double lb = filt_lb(fa, Sl, rho), ub = filt_ub(fa, Sl, rho);
+            double lb, ub;
+            filt_bounds(qt, s1, s2, __ldg(fa.meta + rl), lb, ub);
             lbq[sl] = make_float2(__double2float_rd(fmax(lb, 0.0)), __double2float_ru(ub));
         }
     }
@@ -2775,7 +2829,7 @@ __global__ void __launch_bounds__(THREADS, ROWS4 ? 6 : 5) k_verify_rows(const fl
 }
 
 // A verification round >= 1 with the filter (R17): every row of the span is
-// first bounded through its fp16 copy against the query's k-th best distance
+// first bounded through its int8 copy against the query's k-th best distance
 // at the start of the round (the k-th best only shrinks, so a miss certified
 // against it is a miss at the row's own turn); only rows the bound cannot
 // exclude are read in fp32 for their exact distance.  Excluded rows get +inf
@@ -2791,7 +2845,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_verify_rows_lb(const float *__re
                                                              unsigned long long *__restrict__ fstats) {
     extern __shared__ __align__(16) unsigned char sm[];
     double *qd = (double *)sm;                   // pitch
-    float *qh = (float *)(qd + pitch);           // 8 nv8
+    uint4 *sq = (uint4 *)(qd + pitch);           // 2 nv16 (the query's digit planes)
     const int64_t q = qperm ? qperm[blockIdx.y] : blockIdx.y;
     if (st.done[q]) return;
     const int total = totals[q];
@@ -2800,15 +2854,14 @@ __global__ void __launch_bounds__(THREADS, 3) k_verify_rows_lb(const float *__re
     if (n <= 0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     load_qd(qd, qrot + q * pitch, pitch);
-    const bool exact_q = load_qh(qh, qrot + q * pitch, pitch, fa.nv8, fa.scale);  // syncs the CTA
-    // threshold s sqrt(d_k) (1 + 1e-9); none while the top-k is not full
-    const double thr = (exact_q && st.cnt[q] >= k) ? (double)fa.scale * sqrt(st.Td[q * k + k - 1]) * (1.0 + 1e-9)
-                                                   : -1.0;
+    const QTerms qt = load_q8(sq, fa, q);
+    __syncthreads();
+    // threshold sqrt(d_k) (1 + 1e-9); none while the top-k is not full
+    const double thr = (qt.ok && st.cnt[q] >= k) ? sqrt(st.Td[q * k + k - 1]) * (1.0 + 1e-9) : -1.0;
     const int nvec = pitch / 4;
     const int W = gridDim.x * WARPS;
     const int32_t *ord = pool + q * PS + j0;
     double *dq = dbuf + q * (int64_t)dstride;
-    const float4 *qh4 = (const float4 *)qh;
     unsigned nb = 0, ne = 0;
     for (int j = blockIdx.x * WARPS + warp; j < n; j += 4 * W) {
         int rows[4], jj[4], nr = 0;
@@ -2824,14 +2877,16 @@ __global__ void __launch_bounds__(THREADS, 3) k_verify_rows_lb(const float *__re
         } else {
             const uint4 *r4[4];
 #pragma unroll
-            for (int u = 0; u < 4; u++) r4[u] = fa.Xh + (int64_t)(rows[u] >= 0 ? rows[u] : rows[0]) * fa.nv8;
-            float S[4];
-            rows_h<4>(r4, qh4, fa.nv8, lane, S);
+            for (int u = 0; u < 4; u++) r4[u] = fa.C8 + (int64_t)(rows[u] >= 0 ? rows[u] : rows[0]) * fa.nv16;
+            int S1[4], S2[4];
+            rows_q8<4>(r4, sq, fa.nv16, lane, S1, S2);
             nb += nr;
 #pragma unroll
             for (int u = 0; u < 4; u++)
                 if (rows[u] >= 0) {
-                    if (filt_lb(fa, S[u], __ldg(fa.xerr + rows[u])) > thr) {
+                    double lb, ub;
+                    filt_bounds(qt, S1[u], S2[u], __ldg(fa.meta + rows[u]), lb, ub);
+                    if (lb > thr) {
                         if (lane == 0) dq[jj[u]] = INFINITY;
                     } else {
                         need |= 1u << u;
@@ -3314,7 +3369,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_patience_tail(const float *__res
 // cells), [1] sum |C_q|, [2] rows verified, [3] fallback queries
 // ---------------------------------------------------------------------------
 __device__ unsigned long long d_stats[4];
-__device__ unsigned long long d_filter_stats[2];  // R17: rows bounded through the fp16 copy, of those read exactly
+__device__ unsigned long long d_filter_stats[2];  // R17: rows bounded through the int8 copy, of those read exactly
 static unsigned long long *d_filter_stats_ptr() {
     void *p = nullptr;
     cudaGetSymbolAddress(&p, d_filter_stats);
@@ -3467,6 +3522,13 @@ struct Work {
     int lbf = 0, lb0 = 0, nl_max = 0, vrl_smem = 0, lbb_smem = 0, lbt_smem = 0;
     float2 *lbb = nullptr;
     float *Tq = nullptr;
+    // the query's digit planes and bound terms (k_q8_prep), before the filtered kernels
+    void q8_prep(int64_t qn, cudaStream_t s) const {
+        k_q8_prep<<<(unsigned)qn, 256, 0, s>>>(qrot, ix->pitch, ix->mu, ix->c8pitch, const_cast<uint4 *>(fa.qd),
+                                               const_cast<double *>(fa.qi));
+        CRISP_LAUNCH();
+        g_launches++;
+    }
     // end of the speculative rounds (positions the Hamming order must cover)
     // positions k_hsort orders (the rounds stop there; k_patience_tail completes the
     // order of a query that goes further): ADSampling's fixed rounds + 1024, exact:
@@ -3516,7 +3578,8 @@ struct Work {
         int64_t perq = (int64_t)ix->pitch * 8 + (int64_t)ix->M * KK * 8 + (int64_t)ix->M * 12 + CAPQ * 4 + 4 +
                        (int64_t)ix->M * 2 * 16 +
                        (int64_t)ix->NBW * 8 + 64;
-        if (mode == 0) perq += (int64_t)std::max<int64_t>(S, (ix->N + 4095) / 4096) * k * 16 + (ix->Xh ? CAPQ * 8 + 4 : 0);
+        if (mode == 0) perq += (int64_t)std::max<int64_t>(S, (ix->N + 4095) / 4096) * k * 16 + (ix->C8 ? CAPQ * 8 + 4 : 0);
+        if (ix->C8) perq += 2 * (int64_t)ix->c8pitch + 32;  // query digit planes + bound terms
         else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
         if (traceV) perq += ix->N;
         return perq;
@@ -3573,24 +3636,26 @@ struct Work {
         else
             F = ad ? std::min(S0, std::max(32, env_int("CRISP_AD_FIRST", S0))) : first_round(ix, k);
         // verification filter: a short exact round 0 (the top-k forms), then rounds whose
-        // rows are bounded through the fp16 copy against the k-th best at the round's start;
+        // rows are bounded through the int8 copy against the k-th best at the round's start;
         // spans of at most nl_max rows refresh that threshold as the top-k improves
-        lbf = (mode == 1 && !ad && ix->Xh && ix->vfilter && env_int("CRISP_FILTER_ROUNDS", 1)) ? 1 : 0;
-        if (lbf) {
-            F = std::max(64, (std::max(k, env_int("CRISP_LB_FIRST", 512)) + 63) / 64 * 64);
-            R0 = std::max(1, std::min(16, env_int("CRISP_LB_ROUNDS", 6)));
+        // (on when the patience P is long against that round: measured at cfg2, k = 10, P = 400,
+        // the extra rounds cost more than the bytes they save, 3.47 against 3.25 ms; at cfg4,
+        // k = 100, P = 4000, verification 79.4 -> 34.3 ms.  CRISP_FILTER_ROUNDS=2 forces it)
+        {
+            const int fr = env_int("CRISP_FILTER_ROUNDS", 1);
+            const int F0 = std::max(64, (std::max(k, env_int("CRISP_LB_FIRST", 256)) + 63) / 64 * 64);
+            lbf = (mode == 1 && !ad && ix->C8 && ix->vfilter && fr && (fr == 2 || Pq >= 4 * F0)) ? 1 : 0;
+            if (lbf) {
+                F = F0;
+                R0 = std::max(1, std::min(16, env_int("CRISP_LB_ROUNDS", 6)));
+            }
         }
         DS = std::max({F, S0, std::min(std::max(Pq, nl_min), 1 << 16)});  // dbuf row stride (max span of a round)
         nl_max = lbf ? std::max(nl_min, std::min(DS, env_int("CRISP_LB_SPAN", 2048))) : DS;
-        if (ix->Xh) {
-            const int nv8 = ix->hpitch / 8, m = 8 * ((nv8 + 31) / 32) + 7;
-            fa.Xh = (const uint4 *)ix->Xh;
-            fa.xerr = ix->xerr;
-            fa.nv8 = nv8;
-            fa.scale = ix->xh_scale;
-            fa.lo_f = 1.0 - (m + 1) * std::ldexp(1.0, -24);
-            fa.hi_f = 1.0 + (m + 2) * std::ldexp(1.0, -24);
-            fa.tiny = (nv8 + 1) * std::ldexp(1.0, -140);
+        if (ix->C8) {
+            fa.C8 = (const uint4 *)ix->C8;
+            fa.meta = (const int4 *)ix->c8meta;
+            fa.nv16 = ix->c8pitch / 16;
         }
         round_rows = std::max(1, env_int("CRISP_ROUND_ROWS", 128));  // min rows per CTA in round 0
         vra_smem = pitch * 8 + (Dp / 4 + 1) * 8;
@@ -3636,7 +3701,7 @@ struct Work {
             const int L = rgroup ? NR : S;
             part_d = buf.alloc<double>((size_t)Qc * L * k);
             part_i = buf.alloc<int64_t>((size_t)Qc * L * k);
-            lb0 = (!rgroup && ix->Xh && ix->vfilter && env_int("CRISP_FILTER_RERANK", 1)) ? 1 : 0;
+            lb0 = (!rgroup && ix->C8 && ix->vfilter && env_int("CRISP_FILTER_RERANK", 1)) ? 1 : 0;
             if (lb0) {
                 lbb = buf.alloc<float2>((size_t)Qc * CAPQ);
                 Tq = buf.alloc<float>((size_t)Qc);
@@ -3656,6 +3721,10 @@ struct Work {
             pst.nlen = pst.pos + Qc;
             pst.nver = buf.alloc<int64_t>((size_t)Qc);
             nver = pst.nver;
+        }
+        if (lbf || lb0) {
+            fa.qd = buf.alloc<uint4>((size_t)Qc * 2 * fa.nv16);
+            fa.qi = buf.alloc<double>((size_t)Qc * 4);
         }
         if (want_traceV) traceV = buf.alloc<uint8_t>((size_t)Qc * ix->N);
         if (want_d64tmp) d64tmp = buf.alloc<double>((size_t)Qc * k);
@@ -3685,8 +3754,8 @@ struct Work {
         hsort_smem = (Dp + 1 + 2 * NS + 1) * 4;
         hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
         vr_smem = pitch * 8;
-        vrl_smem = pitch * 8 + (ix->hpitch > 0 ? ix->hpitch : 8) * 4;
-        lbb_smem = (ix->hpitch > 0 ? ix->hpitch : 8) * 4 + (2 * NS + 1) * 4;
+        vrl_smem = pitch * 8 + 2 * std::max(16, ix->c8pitch);
+        lbb_smem = 2 * std::max(16, ix->c8pitch) + (2 * NS + 1) * 4;
         lbt_smem = (2 * NS + 1) * 4;
         scan_smem = WARPS * k * 16 + WARPS * 32 * PSCAN_G * 16;
         pat_smem = pitch * 8 + TAIL_CAP * 16 + k * 16 + (Dp / 4 + 1) * 8 + (Dp + 1 + 2 * NS + 1) * 4;
@@ -3863,6 +3932,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
             dim3 g(w.S, (unsigned)qn);
             unsigned long long *fst = g_timing ? d_filter_stats_ptr() : nullptr;
             if (w.lb0) {
+                w.q8_prep(qn, s);
                 k_lb_bounds<<<g, THREADS, w.lbb_smem, s>>>(w.qrot, pitch, w.fa, w.pool, w.CAPQ, w.cbase, w.ncand, NB,
                                                            w.lbb, w.qperm, fst);
                 CRISP_LAUNCH();
@@ -3948,6 +4018,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
     // spans [F + (r-1) S0, F + r S0), pruned under the r_k of the round's start.
     AdCtx ad{w.ad, ix->ad_eps0, ix->ad_stride, Dp, ix->X, pitch, ix->gid_base, nullptr};
     const int send = w.full_order ? 0x7fffffff : w.order_end();
+    if (w.lbf) w.q8_prep(qn, s);
     for (int r = 0; r < w.R0; r++) {
         const bool own = r > 0 && (!w.ad || w.adsp);
         const int j0 = own ? -1 : (r == 0 ? 0 : w.F + (r - 1) * w.S0), len = r == 0 ? w.F : w.S0;

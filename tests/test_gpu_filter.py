@@ -1,11 +1,12 @@
 """The verification filter (DESIGN R17, crisp_set_verify_filter): a certified
-lower bound of ||q' - x|| from the index's fp16 copy decides that a candidate
-cannot enter the current top-k, so its fp32 row is not read.  The outputs
+lower bound of ||q' - x|| from the index's int8 copy (rows centred on the
+column means, quantised per row) decides that a candidate cannot enter the
+current top-k, so its fp32 row is not read.  The outputs
 must not change: ids, distances and the patience stop with the filter on equal
 those with it off and the oracle's (exact re-rank; patience,
-P:L458), on inputs built to stress the bound (values at 2^-40 and 2^40,
-queries whose scaled copy is not exact, near-duplicate rows closer than the
-fp16 resolution, exact integer ties)."""
+P:L458), on inputs built to stress the bound (values at 2^-40 and 2^40 with
+query components 2^-105 below them, a large common mean, near-duplicate rows
+closer than the int8 resolution, exact integer ties)."""
 import numpy as np
 import pytest
 
@@ -61,6 +62,7 @@ def test_filter_equals_exact(crisp, monkeypatch, mode, first, span):
     """Text-like data (the cfg4 stand-in at D = 256), k = 10 and 40: rounds of
     the filtered verification after a short exact round 0 (phi = 1), the
     two-pass re-rank (phi = 0); both against the oracle, trace included."""
+    monkeypatch.setenv("CRISP_FILTER_ROUNDS", "2")  # also where P < 4 F (off by default there)
     monkeypatch.setenv("CRISP_LB_FIRST", str(first))
     monkeypatch.setenv("CRISP_LB_SPAN", str(span))
     monkeypatch.setenv("CRISP_ROUND_MIN", "32")
@@ -77,12 +79,13 @@ def test_filter_equals_exact(crisp, monkeypatch, mode, first, span):
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("scale_exp", [-40, 40])
+@pytest.mark.parametrize("scale_exp", [-40, 0, 40])
 def test_filter_extreme_scales(crisp, monkeypatch, mode, scale_exp):
-    """Data and queries scaled by 2^-40 / 2^40 (the index's power-of-two scale
-    maps them into fp16 range exactly); at 2^40 two queries carry components far
-    below the data's scale (s q' is subnormal, not exact in fp32, so the filter
-    is off for them) and must still match."""
+    """Data and queries scaled by 2^-40 / 2^40 (per-row power-of-two scales of
+    the codes, fp64 digits of the query); at 2^40 two queries carry components
+    far below the data's scale; a third variant adds a large common mean (the
+    centring on the column means keeps the bound useful)."""
+    monkeypatch.setenv("CRISP_FILTER_ROUNDS", "2")
     monkeypatch.setenv("CRISP_LB_FIRST", "64")
     monkeypatch.setenv("CRISP_LB_SPAN", "256")
     X, Qv, _ = make_case(cfg=1, N=12000, D=64, Q=32, M=4, K=12, seed=5)
@@ -90,7 +93,10 @@ def test_filter_extreme_scales(crisp, monkeypatch, mode, scale_exp):
     X = X * f
     Qv = Qv * f
     if scale_exp > 0:
-        Qv[:2, ::3] = np.float32(1.2345 * 2.0 ** (scale_exp - 145))  # s ~ 2^(12 - scale_exp): s q' subnormal
+        Qv[:2, ::3] = np.float32(1.2345 * 2.0 ** (scale_exp - 145))
+    if scale_exp == 0:
+        X = X + np.float32(1000.0)
+        Qv = Qv + np.float32(1000.0)
     ox = oracle.build(X, 4, K=12, rotation_mode=0, kmeans_iters=10, kmeans_sample=12000, seed=5)
     ix = build_gpu(crisp, X, ox, block_ids=4096)
     B, tau, k, P = 2500, 1, 10, 30
@@ -105,15 +111,16 @@ def test_filter_extreme_scales(crisp, monkeypatch, mode, scale_exp):
 @pytest.mark.parametrize("mode", [0, 1])
 def test_filter_near_duplicates_and_ties(crisp, monkeypatch, mode):
     """Rows that differ from the query, and from one another, by less than the
-    fp16 resolution (the bound cannot separate them: the exact rows decide),
+    int8 resolution (the bound cannot separate them: the exact rows decide),
     plus exact integer ties broken by id (d, id)."""
+    monkeypatch.setenv("CRISP_FILTER_ROUNDS", "2")
     monkeypatch.setenv("CRISP_LB_FIRST", "64")
     monkeypatch.setenv("CRISP_LB_SPAN", "128")
     r = np.random.default_rng(11)
     N, D, M, K = 8000, 48, 4, 8
     X = r.integers(0, 3, (N, D)).astype(np.float32)
     base = r.standard_normal(D).astype(np.float32)
-    X[:400] = base + (r.standard_normal((400, D)) * 1e-5).astype(np.float32)  # within fp16 resolution
+    X[:400] = base + (r.standard_normal((400, D)) * 1e-5).astype(np.float32)  # within int8 resolution
     X[400:800] = X[:400]  # exact duplicates: ties broken by id
     Qv = np.vstack([base[None, :] + (r.standard_normal((6, D)) * 1e-6).astype(np.float32),
                     r.integers(0, 3, (14, D)).astype(np.float32)]).astype(np.float32)
@@ -128,8 +135,9 @@ def test_filter_near_duplicates_and_ties(crisp, monkeypatch, mode):
 
 
 def test_filter_toggle_and_memory(crisp):
-    """crisp_set_verify_filter frees and rebuilds the fp16 copy (hbm_bytes
-    follows), and an index built with CRISP_VERIFY_FILTER=0 has none."""
+    """crisp_set_verify_filter frees and rebuilds the int8 copy (hbm_bytes
+    follows: codes, 16 B of row terms, the column means), and an index built
+    with CRISP_VERIFY_FILTER=0 has none."""
     import os
 
     X, Qv, ox = make_case(cfg=1, N=5000, D=64, Q=8, M=4, K=8, seed=1)
@@ -137,7 +145,7 @@ def test_filter_toggle_and_memory(crisp):
     h_on = ix.info()["hbm_bytes"]
     ix.set_verify_filter(False)
     h_off = ix.info()["hbm_bytes"]
-    assert h_on - h_off == 5000 * 64 * 2 + 5000 * 4
+    assert h_on - h_off == 5000 * 64 + 5000 * 16 + 64 * 4
     ix.set_verify_filter(True)
     assert ix.info()["hbm_bytes"] == h_on
     os.environ["CRISP_VERIFY_FILTER"] = "0"
