@@ -1907,7 +1907,8 @@ __global__ void __launch_bounds__(THREADS) k_rerank_exact(const float *__restric
 // bin that holds it).  k rows then have sqrt(d) <= T, so a row with lb > T (1 + 1e-9) is
 // outside the top-k, and k_rerank_exact<., true> reads only the others.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(THREADS, 3) k_lb_bounds(const float *__restrict__ qrot, int pitch, FiltArgs fa,
+template <int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_lb_bounds(const float *__restrict__ qrot, int pitch, FiltArgs fa,
                                                         const int32_t *__restrict__ pool, int64_t CAPQ,
                                                         const int32_t *__restrict__ cbase,
                                                         const int32_t *__restrict__ ncand, int NB,
@@ -2835,7 +2836,8 @@ __global__ void __launch_bounds__(THREADS, ROWS4 ? 6 : 5) k_verify_rows(const fl
 // exclude are read in fp32 for their exact distance.  Excluded rows get +inf
 // in dbuf, which the in-order replay (k_patience_scan) counts as a miss,
 // exactly as their exact distance would be.
-__global__ void __launch_bounds__(THREADS, 3) k_verify_rows_lb(const float *__restrict__ qrot, int pitch,
+template <int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_verify_rows_lb(const float *__restrict__ qrot, int pitch,
                                                              const float *__restrict__ X, FiltArgs fa,
                                                              const int32_t *__restrict__ pool, int64_t PS,
                                                              const int32_t *__restrict__ totals, PatState st, int k,
@@ -2863,15 +2865,61 @@ __global__ void __launch_bounds__(THREADS, 3) k_verify_rows_lb(const float *__re
     const int32_t *ord = pool + q * PS + j0;
     double *dq = dbuf + q * (int64_t)dstride;
     unsigned nb = 0, ne = 0;
-    for (int j = blockIdx.x * WARPS + warp; j < n; j += 4 * W) {
-        int rows[4], jj[4], nr = 0;
+    // rows the bound keeps wait in a per-warp queue and are read four at a time
+    int *eq_j = (int *)(sq + 2 * fa.nv16) + warp * 64, *eq_r = eq_j + 32;
+    int eqn = 0;  // warp-uniform
+    auto exact_flush = [&](int min_rows) {
+        while (eqn >= min_rows && eqn > 0) {
+            __syncwarp();
+            const int m = min(eqn, 4);
+            int jr[4], rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                jr[u] = eq_j[max(0, eqn - 1 - u)];
+                rr[u] = eq_r[max(0, eqn - 1 - u)];
+            }
+            if (m == 4) {
+                double d4[4];
+                row_dist4(X + (int64_t)rr[0] * pitch, X + (int64_t)rr[1] * pitch, X + (int64_t)rr[2] * pitch,
+                          X + (int64_t)rr[3] * pitch, qd, nvec, lane, d4);
+                if (lane == 0) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) dq[jr[u]] = d4[u];
+                }
+            } else if (m >= 2) {
+                double d0, d1;
+                row_dist2(X + (int64_t)rr[0] * pitch, X + (int64_t)rr[1] * pitch, qd, nvec, lane, d0, d1);
+                if (lane == 0) {
+                    dq[jr[0]] = d0;
+                    dq[jr[1]] = d1;
+                }
+                if (m == 3) {
+                    const double d2 = row_dist1(X + (int64_t)rr[2] * pitch, qd, nvec, lane);
+                    if (lane == 0) dq[jr[2]] = d2;
+                }
+            } else {
+                const double d0 = row_dist1(X + (int64_t)rr[0] * pitch, qd, nvec, lane);
+                if (lane == 0) dq[jr[0]] = d0;
+            }
+            eqn -= m;
+            ne += m;
+            __syncwarp();
+        }
+    };
+    int j = blockIdx.x * WARPS + warp;
+    int nxt[4];  // the next group's row ids, loaded one group ahead
+#pragma unroll
+    for (int u = 0; u < 4; u++) nxt[u] = j + u * W < n ? ord[j + u * W] : -1;
+    for (; j < n; j += 4 * W) {
+        int rows[4], nr = 0;
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-            jj[u] = j + u * W;
-            rows[u] = jj[u] < n ? ord[jj[u]] : -1;
+            rows[u] = nxt[u];
             nr += rows[u] >= 0;
+            const int jn = j + (4 + u) * W;
+            nxt[u] = jn < n ? ord[jn] : -1;
         }
-        unsigned need = 0;  // rows whose exact distance is needed
+        unsigned need;  // rows whose exact distance is needed (bit u: row u)
         if (thr < 0.0) {
             need = (1u << nr) - 1u;
         } else {
@@ -2881,43 +2929,40 @@ __global__ void __launch_bounds__(THREADS, 3) k_verify_rows_lb(const float *__re
             int S1[4], S2[4];
             rows_q8<4>(r4, sq, fa.nv16, lane, S1, S2);
             nb += nr;
+            // lane u bounds row u
+            int s1 = 0, s2 = 0, rr = -1;
 #pragma unroll
             for (int u = 0; u < 4; u++)
-                if (rows[u] >= 0) {
-                    double lb, ub;
-                    filt_bounds(qt, S1[u], S2[u], __ldg(fa.meta + rows[u]), lb, ub);
-                    if (lb > thr) {
-                        if (lane == 0) dq[jj[u]] = INFINITY;
-                    } else {
-                        need |= 1u << u;
-                    }
+                if (lane == u) {
+                    s1 = S1[u];
+                    s2 = S2[u];
+                    rr = rows[u];
                 }
-        }
-        // exact distances of the needed rows, two at a time (need is warp-uniform;
-        // static indices keep rows[] and jj[] in registers)
-        int pr = -1, pj = 0;
-#pragma unroll
-        for (int u = 0; u < 4; u++)
-            if ((need >> u) & 1u) {
-                if (pr < 0) {
-                    pr = rows[u];
-                    pj = jj[u];
-                } else {
-                    double d0, d1;
-                    row_dist2(X + (int64_t)pr * pitch, X + (int64_t)rows[u] * pitch, qd, nvec, lane, d0, d1);
-                    if (lane == 0) {
-                        dq[pj] = d0;
-                        dq[jj[u]] = d1;
-                    }
-                    pr = -1;
-                }
+            bool keep = false;
+            if (rr >= 0) {
+                double lb, ub;
+                filt_bounds(qt, s1, s2, __ldg(fa.meta + rr), lb, ub);
+                keep = !(lb > thr);
+                if (!keep) dq[j + lane * W] = INFINITY;
             }
-        if (pr >= 0) {
-            const double d0 = row_dist1(X + (int64_t)pr * pitch, qd, nvec, lane);
-            if (lane == 0) dq[pj] = d0;
+            need = __ballot_sync(0xffffffffu, keep);
         }
-        ne += __popc(need);
+        // queue the kept rows (warp-uniform bookkeeping; lane 0 writes)
+        if (need) {
+            if (lane == 0) {
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if ((need >> u) & 1u) {
+                        eq_j[eqn] = j + u * W;
+                        eq_r[eqn] = rows[u];
+                        eqn++;
+                    }
+            }
+            eqn = __shfl_sync(0xffffffffu, eqn, 0);
+            if (eqn >= 28) exact_flush(4);
+        }
     }
+    exact_flush(1);
     if (fstats && lane == 0 && (nb | ne)) {
         atomicAdd(fstats, (unsigned long long)nb);
         atomicAdd(fstats + 1, (unsigned long long)(thr < 0.0 ? 0 : ne));
@@ -3483,9 +3528,11 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_fb_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_exact<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_lb_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_lb_bounds<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_lb_bounds<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_lb_threshold, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows_lb, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows_lb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows_lb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -3648,6 +3695,7 @@ struct Work {
             if (lbf) {
                 F = F0;
                 R0 = std::max(1, std::min(16, env_int("CRISP_LB_ROUNDS", 6)));
+                S1 = std::max(1, env_int("CRISP_ROUND_SPLITS", 2));  // measured at cfg4: 29.1 (2) / 29.8 (3) / 31.6 ms (6)
             }
         }
         DS = std::max({F, S0, std::min(std::max(Pq, nl_min), 1 << 16)});  // dbuf row stride (max span of a round)
@@ -3754,7 +3802,7 @@ struct Work {
         hsort_smem = (Dp + 1 + 2 * NS + 1) * 4;
         hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
         vr_smem = pitch * 8;
-        vrl_smem = pitch * 8 + 2 * std::max(16, ix->c8pitch);
+        vrl_smem = pitch * 8 + 2 * std::max(16, ix->c8pitch) + WARPS * 64 * 4;
         lbb_smem = 2 * std::max(16, ix->c8pitch) + (2 * NS + 1) * 4;
         lbt_smem = (2 * NS + 1) * 4;
         scan_smem = WARPS * k * 16 + WARPS * 32 * PSCAN_G * 16;
@@ -3933,8 +3981,13 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
             unsigned long long *fst = g_timing ? d_filter_stats_ptr() : nullptr;
             if (w.lb0) {
                 w.q8_prep(qn, s);
-                k_lb_bounds<<<g, THREADS, w.lbb_smem, s>>>(w.qrot, pitch, w.fa, w.pool, w.CAPQ, w.cbase, w.ncand, NB,
-                                                           w.lbb, w.qperm, fst);
+                // 4 CTAs/SM (64 registers): 186.7 against 198.2 ms with 3 at cfg4
+                if (env_int("CRISP_LBB_CTAS", 4) == 4)
+                    k_lb_bounds<4><<<g, THREADS, w.lbb_smem, s>>>(w.qrot, pitch, w.fa, w.pool, w.CAPQ, w.cbase, w.ncand,
+                                                                  NB, w.lbb, w.qperm, fst);
+                else
+                    k_lb_bounds<3><<<g, THREADS, w.lbb_smem, s>>>(w.qrot, pitch, w.fa, w.pool, w.CAPQ, w.cbase, w.ncand,
+                                                                  NB, w.lbb, w.qperm, fst);
                 CRISP_LAUNCH();
                 k_lb_threshold<<<(unsigned)qn, THREADS, w.lbt_smem, s>>>(w.cbase, w.ncand, NB, w.CAPQ, w.lbb, k, w.Tq);
                 CRISP_LAUNCH();
@@ -4024,10 +4077,14 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         const int j0 = own ? -1 : (r == 0 ? 0 : w.F + (r - 1) * w.S0), len = r == 0 ? w.F : w.S0;
         // CTAs per query: at most S, at least round_rows rows each (the query staging is per CTA)
         dim3 g(own ? w.S1 : std::max(1, std::min(w.S, len / w.round_rows)), (unsigned)qn);
-        if (w.lbf && r > 0)
-            k_verify_rows_lb<<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
-                                                            w.pst, k, j0, len, send, w.DS, w.dbuf, w.qperm,
-                                                            g_timing ? d_filter_stats_ptr() : nullptr);
+        if (w.lbf && r > 0 && env_int("CRISP_LB_CTAS", 3) == 4)
+            k_verify_rows_lb<4><<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
+                                                               w.pst, k, j0, len, send, w.DS, w.dbuf, w.qperm,
+                                                               g_timing ? d_filter_stats_ptr() : nullptr);
+        else if (w.lbf && r > 0)
+            k_verify_rows_lb<3><<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
+                                                               w.pst, k, j0, len, send, w.DS, w.dbuf, w.qperm,
+                                                               g_timing ? d_filter_stats_ptr() : nullptr);
         else if (w.ad && r > 0)  // round 0 starts with an empty top-k: nothing to prune
             k_verify_rows_ad<<<g, THREADS, w.vra_smem, s>>>(w.qrot, pitch, Dp, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst,
                                                             k, j0, len, send, w.DS, w.dbuf, w.qperm, ix->ad_eps0,
