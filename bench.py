@@ -374,6 +374,16 @@ def run_crisp(args):
         index = engine.index
     torch.cuda.synchronize()
     build_s = time.time() - t0
+    if world > 1:
+        # Optimized Mode: the patience rule over the global (h, gid) order (exact for every G,
+        # dist.search_step_global); CRISP_SHARD_PATIENCE=local keeps per-shard patience (Z23)
+        gid_bases = [cdist.shard_range(N, r, world)[0] for r in range(world)]
+        local_pat = os.environ.get("CRISP_SHARD_PATIENCE", "global") == "local"
+
+        def shard_step(eng, q, k_, m_, st_):
+            if m_ == 1 and not local_pat:
+                return cdist.search_step_global(eng, q, k_, m_, gid_bases, st_)
+            return cdist.search_step_exact(eng, q, k_, m_, st_)
     gt = ground_truth(X, Qd, k) if rank == 0 else None
     stream = torch.cuda.current_stream().cuda_stream
     ids = torch.empty((Q, k), dtype=torch.int64, device=dev)
@@ -390,7 +400,7 @@ def run_crisp(args):
             if world == 1:
                 index.search_async(Qd, k, phi(mode), ids, dd, stream)
                 return ids
-            oi, _ = cdist.search_step_exact(engine, Qd, k, phi(mode), stream)
+            oi, _ = shard_step(engine, Qd, k, phi(mode), stream)
             return oi
 
         # the clock sampler starts before the warm-up (nvidia-smi needs ~0.5 s to
@@ -551,7 +561,7 @@ def run_crisp(args):
 
         def e2e_step():
             qe.copy_(qh, non_blocking=True)
-            oi, _ = cdist.search_step_exact(engine, qe, k, phi(head), stream)
+            oi, _ = shard_step(engine, qe, k, phi(head), stream)
             if rank == 0:
                 ih.copy_(oi, non_blocking=True)
             torch.cuda.current_stream().synchronize()
@@ -569,7 +579,7 @@ def run_crisp(args):
         dt = float(tt.item())
         e2e = {"value": Q * K / dt, "unit": "queries/s", "h2d_bytes_per_step": world * Q * D * 4,
                "d2h_bytes_per_step": Q * k * 8, "recall@10": recall_at(ih.numpy(), gt, 10) if rank == 0 else None,
-               "api": "dist.search_step_exact (host queries on every rank, merged ids to rank 0's host)"}
+               "api": "dist.search_step_global (host queries on every rank, merged ids to rank 0's host)"}
 
     # cpu baseline (rank 0, N=1 only): the oracle's search as it stands on the
     # host cores, on the index the GPU searched (oracle_index_of)

@@ -239,6 +239,45 @@ crisp_status crisp_shard_search_finish(crisp_session *s, const int32_t *global_c
                                        int32_t G, int32_t rank, int64_t *out_ids, double *out_dist64, void *stream);
 void crisp_shard_search_free(crisp_session *s);
 
+/* Exact global patience for Optimized Mode over G point shards (Alg. 1
+ * l.22-27 with the patience rule of P:L458 applied to the union of the shards'
+ * candidates, in the global (h, gid) order).  Instead
+ * of crisp_shard_search_finish, an Optimized-Mode session continues with:
+ *   1. gp_order: the fallback selection (as finish), then the Hamming
+ *      distances and the full local (h, gid) order; local_hhist[q][h] = number
+ *      of this shard's candidates of query q at Hamming distance h
+ *      (Q x (padded_D + 1) int32, device).
+ *   2. caller: all-gather local_hhist -> all_hhist (G x Q x (padded_D + 1)).
+ *   3. gp_prepare: position tables (the global position of every local
+ *      candidate follows from all_hhist), round 0's window; gid_bases (host,
+ *      G int64) are the shards' first global ids.
+ *   4. rounds, until *running == 0:
+ *      gp_round: verifies this shard's candidates in every running query's
+ *        global window and keeps the ones that may improve the query's top-k
+ *        (all others are certain misses) as 16-byte records
+ *        {int32 global position, int32 local id, double exact distance},
+ *        packed by query in ascending query and position; *n_entries (host)
+ *        = how many;
+ *      gp_fetch: copies them to entries (>= n_entries x 16 B, device) and
+ *        their number per query to counts (Q int32, device);
+ *      caller: all-gather counts -> all_counts (G x Q) and entries, each
+ *        rank's padded to `stride` records -> all_entries (G x stride);
+ *      gp_replay: every rank replays the windows in global order with the
+ *        sequential rule (identical state on every rank); *running (host) =
+ *        queries still running.
+ *   5. gp_result: out_ids / out_dist64 (Q x k, device) = the global top-k by
+ *      (d, gid), identical on every rank and to a single index over all rows.
+ * G <= 32.  Host-synchronising (the sizes of the all-gathers). */
+crisp_status crisp_shard_gp_order(crisp_session *s, const int32_t *global_counts, const int32_t *all_hist, int32_t G,
+                                  int32_t rank, int32_t *local_hhist, void *stream);
+crisp_status crisp_shard_gp_prepare(crisp_session *s, const int32_t *all_hhist, int32_t G, int32_t rank,
+                                    const int64_t *gid_bases, void *stream);
+crisp_status crisp_shard_gp_round(crisp_session *s, int64_t *n_entries, void *stream);
+crisp_status crisp_shard_gp_fetch(crisp_session *s, void *entries, int32_t *counts, void *stream);
+crisp_status crisp_shard_gp_replay(crisp_session *s, const int32_t *all_counts, const void *all_entries, int64_t stride,
+                                   int32_t G, int32_t *running, void *stream);
+crisp_status crisp_shard_gp_result(crisp_session *s, int64_t *out_ids, double *out_dist64, void *stream);
+
 /* Search with stage outputs copied to host buffers (parity / tracing). */
 crisp_status crisp_search_trace(const crisp_index *idx, const float *queries, int64_t Q, int32_t k, crisp_mode mode,
                                 int64_t *out_ids, float *out_dist2, crisp_trace_t *trace);

@@ -64,6 +64,8 @@ ABI_SYMBOLS = (
     "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
     "crisp_set_stage_timing", "crisp_stage_times", "crisp_search_counters", "crisp_free", "crisp_last_error", "crisp_version",
     "crisp_shard_search_begin", "crisp_shard_search_hist", "crisp_shard_search_finish", "crisp_shard_search_free",
+    "crisp_shard_gp_order", "crisp_shard_gp_prepare", "crisp_shard_gp_round", "crisp_shard_gp_fetch",
+    "crisp_shard_gp_replay", "crisp_shard_gp_result",
     "crisp_set_adsampling", "crisp_set_verify_filter", "crisp_exact_ceil", "crisp_cev_sample_size", "crisp_sample_rows", "crisp_build_model",
 )
 
@@ -101,6 +103,12 @@ def lib():
         L.crisp_shard_search_begin.argtypes = [vp, vp, i64, i32, i32, vp, P(vp), vp]
         L.crisp_shard_search_hist.argtypes = [vp, vp, vp, vp]
         L.crisp_shard_search_finish.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp]
+        L.crisp_shard_gp_order.argtypes = [vp, vp, vp, i32, i32, vp, vp]
+        L.crisp_shard_gp_prepare.argtypes = [vp, vp, i32, i32, vp, vp]
+        L.crisp_shard_gp_round.argtypes = [vp, P(i64), vp]
+        L.crisp_shard_gp_fetch.argtypes = [vp, vp, vp, vp]
+        L.crisp_shard_gp_replay.argtypes = [vp, vp, vp, i64, i32, P(i32), vp]
+        L.crisp_shard_gp_result.argtypes = [vp, vp, vp, vp]
         L.crisp_shard_search_free.argtypes = [vp]
         L.crisp_shard_search_free.restype = None
         L.crisp_free.argtypes = [vp]
@@ -345,6 +353,38 @@ class Index:
     @staticmethod
     def shard_free(ss):
         lib().crisp_shard_search_free(ss)
+
+    # exact global patience (Optimized Mode over G shards; include/crisp.h)
+    @staticmethod
+    def gp_order(ss, global_counts_dev, all_hist_dev, G: int, rank: int, local_hh_dev, stream_ptr: int = 0):
+        _check(lib().crisp_shard_gp_order(ss, _ptr(global_counts_dev), _ptr(all_hist_dev), G, rank,
+                                          _ptr(local_hh_dev), C.c_void_p(stream_ptr)))
+
+    @staticmethod
+    def gp_prepare(ss, all_hh_dev, G: int, rank: int, gid_bases, stream_ptr: int = 0):
+        gb = np.ascontiguousarray(gid_bases, dtype=np.int64)
+        _check(lib().crisp_shard_gp_prepare(ss, _ptr(all_hh_dev), G, rank, _ptr(gb), C.c_void_p(stream_ptr)))
+
+    @staticmethod
+    def gp_round(ss, stream_ptr: int = 0) -> int:
+        n = C.c_int64(0)
+        _check(lib().crisp_shard_gp_round(ss, C.byref(n), C.c_void_p(stream_ptr)))
+        return int(n.value)
+
+    @staticmethod
+    def gp_fetch(ss, entries_dev, counts_dev, stream_ptr: int = 0):
+        _check(lib().crisp_shard_gp_fetch(ss, _ptr(entries_dev), _ptr(counts_dev), C.c_void_p(stream_ptr)))
+
+    @staticmethod
+    def gp_replay(ss, all_counts_dev, all_entries_dev, stride: int, G: int, stream_ptr: int = 0) -> int:
+        r = C.c_int32(0)
+        _check(lib().crisp_shard_gp_replay(ss, _ptr(all_counts_dev), _ptr(all_entries_dev), int(stride), G,
+                                           C.byref(r), C.c_void_p(stream_ptr)))
+        return int(r.value)
+
+    @staticmethod
+    def gp_result(ss, ids_dev, d64_dev, stream_ptr: int = 0):
+        _check(lib().crisp_shard_gp_result(ss, _ptr(ids_dev), _ptr(d64_dev), C.c_void_p(stream_ptr)))
 
     def trace(self, queries, k: int, mode: int = GUARANTEED):
         """crisp_search_trace: stage outputs as numpy arrays."""

@@ -631,6 +631,75 @@ crisp_status crisp_shard_search_finish(crisp_session *s, const int32_t *global_c
     }
 }
 
+crisp_status crisp_shard_gp_order(crisp_session *s, const int32_t *global_counts, const int32_t *all_hist, int32_t G,
+                                  int32_t rank, int32_t *local_hhist, void *stream) {
+    try {
+        CRISP_CHECK(s && global_counts && all_hist && local_hhist, "NULL argument");
+        CRISP_CHECK(G >= 1 && G <= 32 && rank >= 0 && rank < G, "bad G / rank (G <= 32)");
+        CRISP_CHECK(is_device_ptr(local_hhist), "device pointers required");
+        session_gp_order(s, global_counts, all_hist, G, rank, local_hhist, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_shard_gp_prepare(crisp_session *s, const int32_t *all_hhist, int32_t G, int32_t rank,
+                                    const int64_t *gid_bases, void *stream) {
+    try {
+        CRISP_CHECK(s && all_hhist && gid_bases, "NULL argument");
+        CRISP_CHECK(G >= 1 && G <= 32 && rank >= 0 && rank < G, "bad G / rank (G <= 32)");
+        CRISP_CHECK(is_device_ptr(all_hhist), "device pointers required");
+        session_gp_prepare(s, all_hhist, G, rank, gid_bases, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_shard_gp_round(crisp_session *s, int64_t *n_entries, void *stream) {
+    try {
+        CRISP_CHECK(s && n_entries, "NULL argument");
+        session_gp_round(s, n_entries, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_shard_gp_fetch(crisp_session *s, void *entries, int32_t *counts, void *stream) {
+    try {
+        CRISP_CHECK(s && entries && counts, "NULL argument");
+        CRISP_CHECK(is_device_ptr(entries) && is_device_ptr(counts), "device pointers required");
+        session_gp_fetch(s, entries, counts, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_shard_gp_replay(crisp_session *s, const int32_t *all_counts, const void *all_entries, int64_t stride,
+                                   int32_t G, int32_t *running, void *stream) {
+    try {
+        CRISP_CHECK(s && all_counts && all_entries && running, "NULL argument");
+        CRISP_CHECK(stride >= 0, "bad stride");
+        session_gp_replay(s, all_counts, all_entries, stride, G, running, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_shard_gp_result(crisp_session *s, int64_t *out_ids, double *out_dist64, void *stream) {
+    try {
+        CRISP_CHECK(s && out_ids && out_dist64, "NULL argument");
+        session_gp_result(s, out_ids, out_dist64, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
 void crisp_shard_search_free(crisp_session *s) { session_free(s); }
 
 crisp_status crisp_export(const crisp_index *ix, crisp_export_t *o) {

@@ -165,6 +165,16 @@ void session_hist(crisp_session *ss, const int32_t *gcount, int32_t *lhist, cuda
 void session_finish(crisp_session *ss, const int32_t *gcount, const int32_t *allhist, int32_t G, int32_t rank,
                     int64_t *out_ids, double *out_d64, cudaStream_t s);
 void session_free(crisp_session *ss);
+// exact global patience over G shards (phi=1; search.cu)
+void session_gp_order(crisp_session *ss, const int32_t *gcount, const int32_t *allhist, int32_t G, int32_t rank,
+                      int32_t *local_hh, cudaStream_t s);
+void session_gp_prepare(crisp_session *ss, const int32_t *all_hh, int32_t G, int32_t rank, const int64_t *gid_bases,
+                        cudaStream_t s);
+void session_gp_round(crisp_session *ss, int64_t *n_entries, cudaStream_t s);
+void session_gp_fetch(crisp_session *ss, void *entries, int32_t *counts, cudaStream_t s);
+void session_gp_replay(crisp_session *ss, const int32_t *all_cnt, const void *all_ent, int64_t stride, int32_t G,
+                       int32_t *running, cudaStream_t s);
+void session_gp_result(crisp_session *ss, int64_t *out_ids, double *out_d64, cudaStream_t s);
 
 // stage timing
 bool stage_timing_on();

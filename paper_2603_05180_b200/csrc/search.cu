@@ -876,10 +876,10 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
 // cell's fragment inside the block -- [off2[c][F b], off2[c][F b + F]) of the
 // subspace's CSR ids, which holds exactly the cell's ids in the
 // block -- drops the empty ones and takes an exclusive prefix of their counts
-// of 16-byte quads of ids[] (aligned to absolute positions 4j).  Warps take
-// tasks of CF_TF consecutive fragments from a shared counter; a lane takes one
-// quad per step (one 16-byte load), finds its fragment with a 3-step shuffle
-// search over the task's fragments held in the lanes, masks the edge words
+// of 16-byte quads of ids[] (aligned to absolute positions 4j).  Each warp
+// takes an equal share of the chunk's quads; a lane takes one quad per step
+// (one 16-byte load), finds its fragment with a 5-step shuffle search over a
+// sliding window of 32 fragments held in the lanes, masks the edge words
 // outside the fragment, and adds the weight w (Alg. 1 l.10-12) of each of its
 // ids with a shared atomic on the counter's word.  The same id can recur only
 // across subspaces (CSR partition property) and the atomics order
@@ -891,7 +891,6 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
 // counters at the end -- cfg4 count 26.1 ms against 23.4 ms.)
 // ---------------------------------------------------------------------------
 constexpr int CF_CAP = CRISP_CF_CAP;  // fragments staged per chunk
-constexpr int CF_TF = 8;      // fragments per task (a power of two <= 32)
 constexpr int CF_MAXW = 32;   // warps per CTA: 16 (two CTAs per SM, F <= 2) or 32 (one CTA per SM, F = 4)
 
 struct CountFSmem {
@@ -1025,7 +1024,6 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
         if (lane == 0) S.wtot64[warp] = carry;
-        if (tid == 0) S.next = 0;
         __syncthreads();
         long long wpre = 0, tot = 0;
         for (int w2 = 0; w2 < CF_WARPS; w2++) {
@@ -1044,21 +1042,28 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
             }
         if (tid < 40) S.tab[nnz + tid] = make_int4(tid == 0 ? NC : 0x7fffffff, 0, 0, 0);
         __syncthreads();
-        // Tasks of CF_TF consecutive fragments, i.e. their quads [tab[f0].x, tab[f0+CF_TF].x).  A
-        // lane takes one quad per step (a 16-byte load of 4 consecutive ids[] words of one
-        // fragment, edge words masked) and finds its fragment with a 3-step shuffle search over
-        // the task's fragments held in lanes 0..CF_TF-1 (quad prefixes strictly increase: no
-        // empty fragments).  Loads are software-pipelined (the next step's quad is in flight
+        // Warp w takes the chunk's quads [w NC / W, (w+1) NC / W) (static, equal shares).  A lane
+        // takes one quad per step (a 16-byte load of 4 consecutive ids[] words of one fragment,
+        // edge words masked) and finds its fragment with a 5-step shuffle search over a window of
+        // 32 consecutive fragments held in the lanes (quad prefixes strictly increase: no empty
+        // fragments), which slides to the fragment of the step's last quad (32 quads span at
+        // most 32 fragments).  Loads are software-pipelined (the next step's quad is in flight
         // while this step's atomics run); a lane without an id adds 0 to its own dummy word.
-        for (;;) {
-            int task = 0;
-            if (lane == 0) task = atomicAdd(&S.next, 1);
-            task = __shfl_sync(0xffffffffu, task, 0);
-            const int f0 = task * CF_TF;
-            if (f0 >= nnz) break;
-            const int4 te = lane < CF_TF ? S.tab[f0 + lane] : make_int4(0x7fffffff, 0, 0, 0);
-            const int P0 = __shfl_sync(0xffffffffu, te.x, 0);
-            const int P1 = S.tab[min(f0 + CF_TF, nnz)].x;  // tab[nnz].x = NC
+        // (Measured: the earlier dynamic tasks of 8 fragments cost about as many instructions per
+        // task as the ~1.1 steps of quads a task holds.)
+        const int Q0 = (int)((long long)NC * warp / CF_WARPS), Q1 = (int)((long long)NC * (warp + 1) / CF_WARPS);
+        if (Q0 < Q1) {
+            // the fragment holding quad Q0: the last f with tab[f].x <= Q0 (nnz <= CF_CAP = 32 x 32)
+            int fb;
+            {
+                const int ci = lane * 32;
+                const unsigned m1 = __ballot_sync(0xffffffffu, ci < nnz && S.tab[ci].x <= Q0);
+                const int c = 31 - __clz(m1);  // bit 0 is set: tab[0].x = 0
+                const int fi = c * 32 + lane;
+                const unsigned m2 = __ballot_sync(0xffffffffu, fi < nnz && S.tab[fi].x <= Q0);
+                fb = c * 32 + (31 - __clz(m2));
+            }
+            int4 te = S.tab[fb + lane];  // the table is padded past nnz (tab[nnz].x = NC, then +inf)
             uint4 qn;
             int gn0 = 0, gn1 = 0, qpn = 0;
             uint32_t wn = 0;
@@ -1066,7 +1071,7 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                 const int p = pp + lane;
                 int j = 0;
 #pragma unroll
-                for (int st = CF_TF / 2; st; st >>= 1) {
+                for (int st = 16; st; st >>= 1) {
                     const int xv = __shfl_sync(0xffffffffu, te.x, j + st);
                     if (xv <= p) j += st;
                 }
@@ -1074,19 +1079,25 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                 const int qs = __shfl_sync(0xffffffffu, te.y, j);
                 const int gw = __shfl_sync(0xffffffffu, te.z, j);
                 const int ge = __shfl_sync(0xffffffffu, te.w, j);
-                const bool ok = p < P1;
+                const bool ok = p < Q1;
                 qpn = ok ? qs + (p - qx) : 0;
                 gn0 = ok ? (int)((uint32_t)gw & ~WFLAG) : 1;
                 gn1 = ok ? ge : 0;
                 wn = 1u + ((uint32_t)gw >> 31);
                 qn = __ldg((const uint4 *)ids + qpn);
+                // slide the window to the fragment of this step's last quad
+                const int jl = __shfl_sync(0xffffffffu, j, 31);
+                if (jl > 0) {
+                    fb += jl;
+                    te = S.tab[fb + lane];
+                }
             };
-            issue(P0);
-            for (int pp = P0; pp < P1; pp += 32) {
+            issue(Q0);
+            for (int pp = Q0; pp < Q1; pp += 32) {
                 const uint4 qv = qn;
                 const int q0 = qpn * 4, lo = gn0, hi = gn1;
                 const uint32_t w = wn;
-                if (pp + 32 < P1) issue(pp + 32);
+                if (pp + 32 < Q1) issue(pp + 32);
                 const uint32_t xs[4] = {qv.x, qv.y, qv.z, qv.w};
                 uint32_t ov[4], sh[4], inc[4];
 #pragma unroll
@@ -3949,6 +3960,61 @@ static void run_fallback_local(Work &w, int64_t qn, cudaStream_t s) {
     g_launches++;
 }
 
+// a4 at phi=1: the Hamming distances of every candidate and the (h, id) order
+// (cbuf, up to order_end, or all of it with full_order); resets the patience state
+static void run_order(Work &w, int64_t qn, cudaStream_t s) {
+    const crisp_index *ix = w.ix;
+    const int NB = w.NS, pitch = ix->pitch, Dp = ix->Dp;
+    CRISP_CUDA(cudaMemsetAsync(w.pst.cnt, 0, (size_t)w.Qc * 5 * 4, s));
+    {
+        // h of the queries whose candidate set the fallback replaced (k_hamming),
+        // then of all others over their dense pool positions (k_hamming_dense),
+        // unless k_count_warp computed it with the count
+        StageScope st(s, 6);
+        dim3 g(w.HS, (unsigned)qn);
+        k_hamming<<<g, THREADS, w.ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool, w.CAPQ, w.cbase, w.ncand,
+                                                 NB, w.hbuf, w.ghist, w.fb, w.qperm);
+        CRISP_LAUNCH();
+        g_launches++;
+        if (!((w.count_kernel == 1 || w.count_kernel == 2) && w.ham_fused)) {
+            dim3 g2(w.HS, (unsigned)qn);
+            // 16-byte chunks of each code row issued together per lane (CRISP_HAMMING_HT: 2, or 4 with
+            // 2 CTAs per SM; measured at cfg4: 12.4 ms with 2 (8 loads in flight), 14.7 with 4, 14.0 before)
+            if (env_int("CRISP_HAMMING_HT", 2) >= 4)
+                k_hamming_dense<4><<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
+                                                                          w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb,
+                                                                          w.qperm);
+            else
+                k_hamming_dense<2><<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
+                                                                          w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb,
+                                                                          w.qperm);
+            CRISP_LAUNCH();
+            g_launches++;
+        }
+    }
+    {
+        // (h, id) order into cbuf
+        StageScope st(s, 7);
+        if (w.hsort_cta_smem <= 200 * 1024)
+        {
+            // LIST: phase B visits only the listed qualifying elements (when the
+            // sorted prefix is short: k = 10 configurations)
+            const int lim = w.full_order ? 0x7fffffff : w.order_end();
+            if (lim <= 4096)
+                k_hsort_cta<true><<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
+                    w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals, lim);
+            else
+                k_hsort_cta<false><<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
+                    w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals, lim);
+        }
+        else
+            k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ,
+                                                           w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.order_end());
+        CRISP_LAUNCH();
+        g_launches++;
+    }
+}
+
 // a4 (phi=1 Hamming order) + a5 for queries [0, qn) of the chunk -> outputs
 static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64, cudaStream_t s) {
     const crisp_index *ix = w.ix;
@@ -4016,54 +4082,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         return;
     }
     const int P = ix->patience_factor > 0 ? ix->patience_factor * k : 0;
-    CRISP_CUDA(cudaMemsetAsync(w.pst.cnt, 0, (size_t)w.Qc * 5 * 4, s));
-    {
-        // h of the queries whose candidate set the fallback replaced (k_hamming),
-        // then of all others over their dense pool positions (k_hamming_dense),
-        // unless k_count_warp computed it with the count
-        StageScope st(s, 6);
-        dim3 g(w.HS, (unsigned)qn);
-        k_hamming<<<g, THREADS, w.ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool, w.CAPQ, w.cbase, w.ncand,
-                                                 NB, w.hbuf, w.ghist, w.fb, w.qperm);
-        CRISP_LAUNCH();
-        g_launches++;
-        if (!((w.count_kernel == 1 || w.count_kernel == 2) && w.ham_fused)) {
-            dim3 g2(w.HS, (unsigned)qn);
-            // 16-byte chunks of each code row issued together per lane (CRISP_HAMMING_HT: 2, or 4 with
-            // 2 CTAs per SM; measured at cfg4: 12.4 ms with 2 (8 loads in flight), 14.7 with 4, 14.0 before)
-            if (env_int("CRISP_HAMMING_HT", 2) >= 4)
-                k_hamming_dense<4><<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
-                                                                          w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb,
-                                                                          w.qperm);
-            else
-                k_hamming_dense<2><<<g2, THREADS, w.countw_ham_smem, s>>>(w.qrot, pitch, Dp, ix->codes, ix->Wp, w.pool,
-                                                                          w.CAPQ, w.cursor, w.hbuf, w.ghist, w.fb,
-                                                                          w.qperm);
-            CRISP_LAUNCH();
-            g_launches++;
-        }
-    }
-    {
-        // (h, id) order into cbuf
-        StageScope st(s, 7);
-        if (w.hsort_cta_smem <= 200 * 1024)
-        {
-            // LIST: phase B visits only the listed qualifying elements (when the
-            // sorted prefix is short: k = 10 configurations)
-            const int lim = w.full_order ? 0x7fffffff : w.order_end();
-            if (lim <= 4096)
-                k_hsort_cta<true><<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
-                    w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals, lim);
-            else
-                k_hsort_cta<false><<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
-                    w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals, lim);
-        }
-        else
-            k_hsort<<<(unsigned)qn, 32, w.hsort_smem, s>>>(w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ,
-                                                           w.cbuf, w.totals, w.full_order ? 0x7fffffff : w.order_end());
-        CRISP_LAUNCH();
-        g_launches++;
-    }
+    run_order(w, qn, s);
     StageScope st(s, 4);
     // verification rounds.  Round 0: positions [0, F) of every query.  Exact
     // verification, rounds >= 1: each running query its own span [pos, pos + nlen)
@@ -4308,11 +4327,15 @@ void search(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, i
 // ---------------------------------------------------------------------------
 }  // namespace crisp
 
+namespace crisp {
+struct GPBuf;
+}
 struct crisp_session {
     const crisp_index *ix;
     crisp::Work *w;
     int64_t Q;
     int k, mode;
+    crisp::GPBuf *gp = nullptr;  // exact global patience (phi=1 over G shards)
 };
 
 namespace crisp {
@@ -4363,8 +4386,420 @@ void session_finish(crisp_session *ss, const int32_t *gcount, const int32_t *all
     run_stats(w, ss->Q, s);
 }
 
+// ---------------------------------------------------------------------------
+// Exact global patience over G point shards (phi=1).  The global
+// verification order is (h, gid) over the union of the shards' candidate sets
+// (P:L455-458 applied to the whole dataset).  Every rank keeps the same global
+// state per query (top-k, patience counter, position, window length); a round
+// takes the global window [pos, pos + len), each rank verifies its own rows in
+// it (their local positions follow from the all-gathered Hamming histograms),
+// emits the rows that may improve the top-k as it stood at the round's start
+// (the k-th best only shrinks, so every other row is a certain miss), and after
+// an all-gather every rank replays the window in global order with the
+// sequential rule.  The result and the stop index equal those of a single
+// index over all rows, for every G.
+// ---------------------------------------------------------------------------
+struct GEnt {
+    int32_t gpos;  // position in the global (h, gid) order
+    int32_t lid;   // local id on the emitting shard
+    double d;      // exact distance
+};
+static_assert(sizeof(GEnt) == 16, "GEnt is the 16-byte record of include/crisp.h");
+
+struct GPBuf {
+    int G = 1, rank = 0, H = 0;
+    int32_t *base = nullptr, *lcum = nullptr;  // Q x (H + 1)
+    int32_t *gtot = nullptr, *gpos = nullptr, *glen = nullptr;
+    int32_t *cnt = nullptr, *offs = nullptr;  // Q + 1
+    GEnt *stage = nullptr, *packed = nullptr;  // Q x DS
+    int32_t *running = nullptr;
+    int32_t *all_off = nullptr;  // G x (Q + 1)
+    int64_t *gbase = nullptr;    // G
+    void *scan_tmp = nullptr;
+    size_t scan_bytes = 0;
+    int nl_min = 512, nl_max = 4096;
+    int64_t n_packed = 0;
+    std::vector<void *> ptrs;
+    template <class T>
+    T *alloc(size_t n, cudaStream_t s) {
+        void *p = nullptr;
+        CRISP_CUDA(cudaMallocAsync(&p, std::max<size_t>(n * sizeof(T), 16), s));
+        ptrs.push_back(p);
+        return (T *)p;
+    }
+    ~GPBuf() {
+        for (void *p : ptrs) cudaFree(p);
+    }
+};
+
+__global__ void __launch_bounds__(256) k_gp_tables(const int32_t *__restrict__ allh, int G, int rank, int64_t Q, int H,
+                                                   int32_t *__restrict__ base, int32_t *__restrict__ lcum,
+                                                   int32_t *__restrict__ gtot) {
+    // base[h] = global position of this rank's first candidate with Hamming distance h
+    //         = (all candidates with h' < h) + (candidates of ranks < rank with h);
+    // lcum[h] = local position of that candidate; [H] are the totals
+    typedef cub::BlockScan<int, 256> BScan;
+    __shared__ typename BScan::TempStorage ts;
+    __shared__ int carry_all, carry_me;
+    const int64_t q = blockIdx.x;
+    if (threadIdx.x == 0) carry_all = carry_me = 0;
+    __syncthreads();
+    for (int h0 = 0; h0 < H; h0 += 256) {
+        const int h = h0 + threadIdx.x;
+        int tot = 0, pre = 0, mine = 0;
+        if (h < H)
+            for (int g = 0; g < G; g++) {
+                const int v = allh[((int64_t)g * Q + q) * H + h];
+                tot += v;
+                pre += g < rank ? v : 0;
+                mine += g == rank ? v : 0;
+            }
+        int ea, em, sa, sme;
+        BScan(ts).ExclusiveSum(tot, ea, sa);
+        __syncthreads();
+        BScan(ts).ExclusiveSum(mine, em, sme);
+        if (h < H) {
+            base[q * (H + 1) + h] = carry_all + ea + pre;
+            lcum[q * (H + 1) + h] = carry_me + em;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            carry_all += sa;
+            carry_me += sme;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        base[q * (H + 1) + H] = carry_all;
+        lcum[q * (H + 1) + H] = carry_me;
+        gtot[q] = carry_all;
+    }
+}
+
+// number of this rank's candidates whose global position is < P
+__device__ __forceinline__ int gp_loc(const int32_t *__restrict__ base, const int32_t *__restrict__ lcum, int H, int P) {
+    if (base[0] > P) return 0;
+    int lo = 0, hi = H;  // the last h with base[h] <= P (base is non-decreasing)
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (base[mid] <= P) lo = mid;
+        else hi = mid - 1;
+    }
+    const int mine = lo < H ? lcum[lo + 1] - lcum[lo] : 0;
+    return lcum[lo] + min(max(P - base[lo], 0), mine);
+}
+
+// global position of this rank's candidate at local position i
+__device__ __forceinline__ int gp_gpos(const int32_t *__restrict__ base, const int32_t *__restrict__ lcum, int H, int i) {
+    int lo = 0, hi = H;  // the last h with lcum[h] <= i: the (non-empty) bin holding i
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (lcum[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return base[lo] + (i - lcum[lo]);
+}
+
+// this round's local span of every running query: st.pos / st.nlen (the own-span
+// convention of the verification kernels)
+__global__ void k_gp_span(int64_t Q, int H, const int32_t *__restrict__ base, const int32_t *__restrict__ lcum,
+                          const int32_t *__restrict__ gtot, const int32_t *__restrict__ gpos,
+                          const int32_t *__restrict__ glen, PatState st) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Q) return;
+    if (st.done[q]) {
+        st.nlen[q] = 0;
+        return;
+    }
+    const int P0 = gpos[q], P1 = min(P0 + glen[q], gtot[q]);
+    const int32_t *b = base + q * (H + 1), *l = lcum + q * (H + 1);
+    const int a = gp_loc(b, l, H, P0), e = gp_loc(b, l, H, P1);
+    st.pos[q] = a;
+    st.nlen[q] = e - a;
+}
+
+// the window's rows that may improve the top-k as it stood at the round's start,
+// in ascending position (warp per query)
+__global__ void __launch_bounds__(THREADS) k_gp_emit(int64_t Q, int k, PatState st, const double *__restrict__ dbuf,
+                                                      int DS, const int32_t *__restrict__ order, int64_t CAPQ,
+                                                      int64_t gid_base, int H,
+                                                      const int32_t *__restrict__ base,
+                                                      const int32_t *__restrict__ lcum, GEnt *__restrict__ stage,
+                                                      int32_t *__restrict__ cnt) {
+    const int64_t q = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= Q) return;
+    if (st.done[q]) {
+        if (lane == 0) cnt[q] = 0;
+        return;
+    }
+    const int a = st.pos[q], n = st.nlen[q];
+    const bool full = st.cnt[q] >= k;
+    const double dk = full ? st.Td[q * k + k - 1] : 0.0;
+    const int64_t ik = full ? st.Ti[q * k + k - 1] : 0;
+    const int32_t *b = base + q * (H + 1), *l = lcum + q * (H + 1);
+    GEnt *out = stage + q * (int64_t)DS;
+    int c = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        bool em = false;
+        int lid = 0;
+        double d = 0.0;
+        if (j < n) {
+            d = dbuf[q * (int64_t)DS + j];
+            lid = order[q * CAPQ + a + j];
+            em = !full || less_di(d, gid_base + lid, dk, ik);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, em);
+        if (em) out[c + __popc(m & ((1u << lane) - 1u))] = GEnt{gp_gpos(b, l, H, a + j), lid, d};
+        c += __popc(m);
+    }
+    if (lane == 0) cnt[q] = c;
+}
+
+__global__ void k_gp_pack(int64_t Q, int DS, const GEnt *__restrict__ stage, const int32_t *__restrict__ cnt,
+                          const int32_t *__restrict__ offs, GEnt *__restrict__ packed) {
+    const int64_t q = blockIdx.x;
+    const int n = cnt[q], o = offs[q];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) packed[o + i] = stage[q * (int64_t)DS + i];
+}
+
+// every rank replays the window in global order (warp per query; lane g < G
+// holds the head of rank g's list, a warp arg-min picks the next entry)
+__global__ void __launch_bounds__(THREADS) k_gp_replay(int64_t Q, int G, int k, int P, const int32_t *__restrict__ all_cnt,
+                                                        const int32_t *__restrict__ all_off,
+                                                        const GEnt *__restrict__ all_ent, int64_t stride,
+                                                        const int64_t *__restrict__ gbase, PatState st,
+                                                        int32_t *__restrict__ gpos, int32_t *__restrict__ glen,
+                                                        const int32_t *__restrict__ gtot, int nl_min, int nl_max,
+                                                        int32_t *__restrict__ running) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * WARPS + warp;
+    if (q >= Q || st.done[q]) return;
+    double *Td = (double *)sm + warp * k;
+    int64_t *Ti = (int64_t *)((double *)sm + WARPS * k) + warp * k;
+    int cnt_top = st.cnt[q], pat = st.pat[q];
+    for (int i = lane; i < cnt_top; i += 32) {
+        Td[i] = st.Td[q * k + i];
+        Ti[i] = st.Ti[q * k + i];
+    }
+    __syncwarp();
+    const int P0 = gpos[q], P1 = min(P0 + glen[q], gtot[q]);
+    // lane g: rank g's list of this query
+    const int nmine = lane < G ? all_cnt[(int64_t)lane * Q + q] : 0;
+    const GEnt *mine = lane < G ? all_ent + (int64_t)lane * stride + all_off[(int64_t)lane * (Q + 1) + q] : nullptr;
+    int head = 0;
+    int last = P0 - 1, stop = -1;
+    for (;;) {
+        const int hp = head < nmine ? mine[head].gpos : 0x7fffffff;
+        // arg-min over the lanes (positions are distinct across ranks)
+        int mp = hp, ml = lane;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const int op = __shfl_xor_sync(0xffffffffu, mp, o), ol = __shfl_xor_sync(0xffffffffu, ml, o);
+            if (op < mp || (op == mp && ol < ml)) {
+                mp = op;
+                ml = ol;
+            }
+        }
+        if (mp == 0x7fffffff) break;
+        int lid = 0;
+        double d = 0.0;
+        if (lane == ml) {
+            lid = mine[head].lid;
+            d = mine[head].d;
+            head++;
+        }
+        lid = __shfl_sync(0xffffffffu, lid, ml);
+        d = __shfl_sync(0xffffffffu, d, ml);
+        const int gap = mp - last - 1;  // certain misses before this entry
+        if (P > 0 && pat + gap >= P) {
+            stop = last + (P - pat);
+            break;
+        }
+        pat += gap;
+        const int64_t gid = gbase[ml] + lid;
+        if (cnt_top < k || less_di(d, gid, Td[k - 1], Ti[k - 1])) {
+            warp_insert(Td, Ti, cnt_top, k, d, gid, lane);
+            pat = 0;
+        } else {
+            pat++;
+            if (P > 0 && pat >= P) {
+                stop = mp;
+                break;
+            }
+        }
+        last = mp;
+    }
+    if (stop < 0) {
+        const int gap = P1 - 1 - last;
+        if (P > 0 && pat + gap >= P) stop = last + (P - pat);
+        else pat += gap;
+    }
+    for (int i = lane; i < cnt_top; i += 32) {
+        st.Td[q * k + i] = Td[i];
+        st.Ti[q * k + i] = Ti[i];
+    }
+    if (lane == 0) {
+        st.cnt[q] = cnt_top;
+        st.pat[q] = pat;
+        if (stop >= 0 || P1 >= gtot[q]) {
+            st.done[q] = 1;
+            st.nver[q] = stop >= 0 ? stop + 1 : gtot[q];
+        } else {
+            gpos[q] = P1;
+            glen[q] = P > 0 ? min(nl_max, max(nl_min, P - pat)) : nl_max;
+            atomicAdd(running, 1);
+        }
+    }
+}
+
+__global__ void k_gp_result(int64_t Q, int k, PatState st, double *__restrict__ out_d64, int64_t *__restrict__ out_i) {
+    const int64_t q = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= Q) return;
+    write_topk(q, k, st.cnt[q], st.Td + q * k, st.Ti + q * k, out_d64, nullptr, out_i, lane, 32);
+}
+
+void session_gp_order(crisp_session *ss, const int32_t *gcount, const int32_t *allhist, int32_t G, int32_t rank,
+                      int32_t *local_hh, cudaStream_t s) {
+    Work &w = *ss->w;
+    const crisp_index *ix = ss->ix;
+    CRISP_CHECK(ss->mode == 1, "global patience is for Optimized Mode sessions");
+    {
+        StageScope st(s, 3);
+        k_fb_select<<<(unsigned)ss->Q, THREADS, w.count_smem, s>>>(
+            w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB, ix->ids, ix->N, ix->BS, ss->k, gcount, allhist,
+            G, rank, ss->Q, w.pool, w.CAPQ, w.cbase, w.ncand, w.NS, w.fb, w.ghist, ix->Dp + 1);
+        CRISP_LAUNCH();
+        g_launches++;
+    }
+    w.full_order = true;  // the global window may reach any local position
+    run_order(w, ss->Q, s);
+    CRISP_CUDA(cudaMemcpyAsync(local_hh, w.ghist, (size_t)ss->Q * (ix->Dp + 1) * 4, cudaMemcpyDeviceToDevice, s));
+}
+
+void session_gp_prepare(crisp_session *ss, const int32_t *all_hh, int32_t G, int32_t rank, const int64_t *gid_bases,
+                        cudaStream_t s) {
+    Work &w = *ss->w;
+    const crisp_index *ix = ss->ix;
+    const int64_t Q = ss->Q;
+    delete ss->gp;
+    GPBuf *gp = ss->gp = new GPBuf();
+    gp->G = G;
+    gp->rank = rank;
+    gp->H = ix->Dp + 1;
+    gp->nl_min = std::max(32, env_int("CRISP_GP_MIN", 512));
+    gp->nl_max = std::max(gp->nl_min, std::min(w.DS, env_int("CRISP_GP_MAX", 4096)));
+    gp->base = gp->alloc<int32_t>((size_t)Q * (gp->H + 1), s);
+    gp->lcum = gp->alloc<int32_t>((size_t)Q * (gp->H + 1), s);
+    gp->gtot = gp->alloc<int32_t>((size_t)Q, s);
+    gp->gpos = gp->alloc<int32_t>((size_t)Q, s);
+    gp->glen = gp->alloc<int32_t>((size_t)Q, s);
+    gp->cnt = gp->alloc<int32_t>((size_t)Q + 1, s);
+    gp->offs = gp->alloc<int32_t>((size_t)Q + 1, s);
+    gp->stage = gp->alloc<GEnt>((size_t)Q * w.DS, s);
+    gp->packed = gp->alloc<GEnt>((size_t)Q * w.DS, s);
+    gp->running = gp->alloc<int32_t>(1, s);
+    gp->all_off = gp->alloc<int32_t>((size_t)G * (Q + 1), s);
+    gp->gbase = gp->alloc<int64_t>((size_t)G, s);
+    CRISP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, gp->scan_bytes, gp->cnt, gp->offs, (int)Q + 1, s));
+    gp->scan_tmp = gp->alloc<unsigned char>(gp->scan_bytes, s);
+    CRISP_CUDA(cudaMemcpyAsync(gp->gbase, gid_bases, (size_t)G * 8, cudaMemcpyHostToDevice, s));
+    k_gp_tables<<<(unsigned)Q, 256, 0, s>>>(all_hh, G, rank, Q, gp->H, gp->base, gp->lcum, gp->gtot);
+    CRISP_LAUNCH();
+    g_launches++;
+    // round 0: the first F positions (exact, or F ~ P without the filter)
+    CRISP_CUDA(cudaMemsetAsync(gp->gpos, 0, (size_t)Q * 4, s));
+    std::vector<int32_t> h0((size_t)Q, std::min(w.F, w.DS));
+    CRISP_CUDA(cudaMemcpyAsync(gp->glen, h0.data(), (size_t)Q * 4, cudaMemcpyHostToDevice, s));
+    CRISP_CUDA(cudaStreamSynchronize(s));  // h0 is a host temporary
+    if (w.lbf) w.q8_prep(Q, s);
+}
+
+void session_gp_round(crisp_session *ss, int64_t *n_entries, cudaStream_t s) {
+    Work &w = *ss->w;
+    const crisp_index *ix = ss->ix;
+    GPBuf *gp = ss->gp;
+    CRISP_CHECK(gp != nullptr, "crisp_shard_gp_prepare first");
+    const int64_t Q = ss->Q;
+    const int k = ss->k, pitch = ix->pitch;
+    StageScope st(s, 4);
+    k_gp_span<<<nblk(Q, 256), 256, 0, s>>>(Q, gp->H, gp->base, gp->lcum, gp->gtot, gp->gpos, gp->glen, w.pst);
+    CRISP_LAUNCH();
+    dim3 g(w.S1, (unsigned)Q);
+    if (w.lbf)
+        k_verify_rows_lb<3><<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
+                                                           w.pst, k, -1, 0, 0x7fffffff, w.DS, w.dbuf, w.qperm,
+                                                           g_timing ? d_filter_stats_ptr() : nullptr);
+    else if (w.rows4)
+        k_verify_rows<true><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst, -1,
+                                                          0, 0x7fffffff, w.DS, w.dbuf, w.qperm);
+    else
+        k_verify_rows<false><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst, -1,
+                                                           0, 0x7fffffff, w.DS, w.dbuf, w.qperm);
+    CRISP_LAUNCH();
+    k_gp_emit<<<nblk(Q, WARPS), THREADS, 0, s>>>(Q, k, w.pst, w.dbuf, w.DS, w.cbuf, w.CAPQ, ix->gid_base, gp->H,
+                                                  gp->base, gp->lcum, gp->stage, gp->cnt);
+    CRISP_LAUNCH();
+    CRISP_CUDA(cudaMemsetAsync(gp->cnt + Q, 0, 4, s));
+    CRISP_CUDA(cub::DeviceScan::ExclusiveSum(gp->scan_tmp, gp->scan_bytes, gp->cnt, gp->offs, (int)Q + 1, s));
+    k_gp_pack<<<(unsigned)Q, 128, 0, s>>>(Q, w.DS, gp->stage, gp->cnt, gp->offs, gp->packed);
+    CRISP_LAUNCH();
+    g_launches += 5;
+    int32_t tot = 0;
+    CRISP_CUDA(cudaMemcpyAsync(&tot, gp->offs + Q, 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaStreamSynchronize(s));
+    gp->n_packed = tot;
+    *n_entries = tot;
+}
+
+void session_gp_fetch(crisp_session *ss, void *entries, int32_t *counts, cudaStream_t s) {
+    GPBuf *gp = ss->gp;
+    CRISP_CHECK(gp != nullptr, "crisp_shard_gp_round first");
+    CRISP_CUDA(cudaMemcpyAsync(entries, gp->packed, (size_t)gp->n_packed * sizeof(GEnt), cudaMemcpyDeviceToDevice, s));
+    CRISP_CUDA(cudaMemcpyAsync(counts, gp->cnt, (size_t)ss->Q * 4, cudaMemcpyDeviceToDevice, s));
+}
+
+void session_gp_replay(crisp_session *ss, const int32_t *all_cnt, const void *all_ent, int64_t stride, int32_t G,
+                       int32_t *running, cudaStream_t s) {
+    Work &w = *ss->w;
+    const crisp_index *ix = ss->ix;
+    GPBuf *gp = ss->gp;
+    CRISP_CHECK(gp != nullptr && G == gp->G, "crisp_shard_gp_prepare first (same G)");
+    const int64_t Q = ss->Q;
+    const int k = ss->k;
+    const int P = ix->patience_factor > 0 ? ix->patience_factor * k : 0;
+    StageScope st(s, 4);
+    for (int g = 0; g < G; g++) {
+        // rank g's counts, then a 0 for the exclusive scan's total
+        CRISP_CUDA(cudaMemcpyAsync(gp->cnt, all_cnt + (int64_t)g * Q, (size_t)Q * 4, cudaMemcpyDeviceToDevice, s));
+        CRISP_CUDA(cudaMemsetAsync(gp->cnt + Q, 0, 4, s));
+        CRISP_CUDA(cub::DeviceScan::ExclusiveSum(gp->scan_tmp, gp->scan_bytes, gp->cnt, gp->all_off + (int64_t)g * (Q + 1),
+                                                 (int)Q + 1, s));
+    }
+    CRISP_CUDA(cudaMemsetAsync(gp->running, 0, 4, s));
+    k_gp_replay<<<nblk(Q, WARPS), THREADS, WARPS * k * 16, s>>>(Q, G, k, P, all_cnt, gp->all_off, (const GEnt *)all_ent,
+                                                                 stride, gp->gbase, w.pst, gp->gpos, gp->glen, gp->gtot,
+                                                                 gp->nl_min, gp->nl_max, gp->running);
+    CRISP_LAUNCH();
+    g_launches++;
+    CRISP_CUDA(cudaMemcpyAsync(running, gp->running, 4, cudaMemcpyDeviceToHost, s));
+    CRISP_CUDA(cudaStreamSynchronize(s));
+}
+
+void session_gp_result(crisp_session *ss, int64_t *out_ids, double *out_d64, cudaStream_t s) {
+    Work &w = *ss->w;
+    k_gp_result<<<nblk(ss->Q, WARPS), THREADS, 0, s>>>(ss->Q, ss->k, w.pst, out_d64, out_ids);
+    CRISP_LAUNCH();
+    g_launches++;
+    run_stats(w, ss->Q, s);
+}
+
 void session_free(crisp_session *ss) {
     if (!ss) return;
+    delete ss->gp;
     delete ss->w;
     delete ss;
 }

@@ -11,6 +11,10 @@ Collective call sites:
   N6     all-gather of the V histograms (used by underflowing queries only)
   N7     one all-gather of the per-shard top-k (dist64, gid) packed together,
          then the a6 merge kernel (crisp_merge_topk) by (d, gid)
+  N8     (Optimized Mode, search_step_global) all-gather of the per-shard Hamming
+         histograms, then per verification round all-gathers of the entries that
+         may improve a top-k: the patience rule runs over the GLOBAL (h, gid)
+         order, so the result equals a single index for every G
 
 The orchestration is written against a small engine interface so the same
 code runs with the CUDA engine (NCCL over NVLink) and, in the CPU tests, with
@@ -78,6 +82,38 @@ class CudaEngine:
         ids = torch.empty((self._Q, self._k), dtype=torch.int64, device=global_counts.device)
         d64 = torch.empty((self._Q, self._k), dtype=torch.float64, device=global_counts.device)
         self.index.shard_finish(self._ss, global_counts, all_hist, G, rank, ids, d64, stream)
+        self.index.shard_free(self._ss)
+        self._ss = None
+        return ids, d64
+
+    # exact global patience (phi=1), see include/crisp.h crisp_shard_gp_*
+    def gp_order(self, global_counts, all_hist, G, rank, stream=0):
+        H = self.index.info()["padded_D"] + 1
+        hh = torch.zeros((self._Q, H), dtype=torch.int32, device=global_counts.device)
+        self.index.gp_order(self._ss, global_counts, all_hist, G, rank, hh, stream)
+        return hh
+
+    def gp_prepare(self, all_hh, G, rank, gid_bases, stream=0):
+        self.index.gp_prepare(self._ss, all_hh, G, rank, gid_bases, stream)
+
+    def gp_round(self, stream=0):
+        return self.index.gp_round(self._ss, stream)
+
+    def gp_fetch(self, n_pad, stream=0):
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ent = torch.zeros((max(1, n_pad), 16), dtype=torch.uint8, device=dev)
+        cnt = torch.empty(self._Q, dtype=torch.int32, device=dev)
+        self.index.gp_fetch(self._ss, ent, cnt, stream)
+        return ent, cnt
+
+    def gp_replay(self, all_counts, all_entries, stride, G, stream=0):
+        return self.index.gp_replay(self._ss, all_counts, all_entries, stride, G, stream)
+
+    def gp_result(self, stream=0):
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ids = torch.empty((self._Q, self._k), dtype=torch.int64, device=dev)
+        d64 = torch.empty((self._Q, self._k), dtype=torch.float64, device=dev)
+        self.index.gp_result(self._ss, ids, d64, stream)
         self.index.shard_free(self._ss)
         self._ss = None
         return ids, d64
@@ -200,6 +236,75 @@ def search_step_exact(engine, q_dev, k, mode, stream=0):
     ids, d64 = engine.finish(counts, torch.stack(all_h), world, rank, stream)
     gd, gi = gather_topk(ids, d64)
     return engine.merge(gd, gi, stream)
+
+
+def _all_gather_stack(t):
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return torch.stack(out)
+
+
+def search_step_global(engine, q_dev, k, mode, gid_bases, stream=0):
+    """One sharded search whose Optimized-Mode verification follows the
+    patience rule over the GLOBAL (h, gid) order (exact for every G: the result
+    equals a single index over all rows).  Collectives per step: N5 all-reduce
+    of |C_q|, N6 all-gather of the V histograms (exact fallback), N8 all-gather
+    of the Hamming histograms, then per verification round one all-gather of
+    the entry counts and one of the entries that may improve a top-k (their
+    number first, for the padded size).  Guaranteed Mode is search_step_exact."""
+    if mode != 1:
+        return search_step_exact(engine, q_dev, k, mode, stream)
+    world, rank = dist.get_world_size(), dist.get_rank()
+    counts = engine.begin(q_dev, k, mode, stream)
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    hist = engine.hist(counts, stream)
+    hh = engine.gp_order(counts, _all_gather_stack(hist), world, rank, stream)
+    engine.gp_prepare(_all_gather_stack(hh), world, rank, gid_bases, stream)
+    dev = counts.device
+    while True:
+        n = engine.gp_round(stream)
+        ns = _all_gather_stack(torch.tensor([n], dtype=torch.int64, device=dev))
+        stride = max(1, int(ns.max().item()))
+        ent, cnt = engine.gp_fetch(stride, stream)
+        running = engine.gp_replay(_all_gather_stack(cnt), _all_gather_stack(ent), stride, world, stream)
+        if running == 0:
+            break
+    ids, d64 = engine.gp_result(stream)
+    return ids, d64.to(torch.float32)
+
+
+def emulate_global_search(engines, gid_bases, q_dev, k, mode, stream=0, stats=None):
+    """The search_step_global protocol for G shard engines in ONE process (the
+    collectives done by concatenation): a single-GPU emulation for the tests."""
+    G = len(engines)
+    counts = [e.begin(q_dev, k, mode, stream) for e in engines]
+    gc = torch.stack(counts).sum(0).to(torch.int32)
+    hists = torch.stack([e.hist(gc, stream) for e in engines])
+    if mode != 1:
+        outs = [e.finish(gc, hists, G, r, stream) for r, e in enumerate(engines)]
+        ids, d64 = torch.stack([o[0] for o in outs]), torch.stack([o[1] for o in outs])
+        return engines[0].merge(d64, ids, stream)
+    hh = torch.stack([e.gp_order(gc, hists, G, r, stream) for r, e in enumerate(engines)])
+    for r, e in enumerate(engines):
+        e.gp_prepare(hh, G, r, gid_bases, stream)
+    rounds = 0
+    while True:
+        ns = [e.gp_round(stream) for e in engines]
+        stride = max(1, max(ns))
+        got = [e.gp_fetch(stride, stream) for e in engines]
+        all_ent = torch.stack([g_[0] for g_ in got])
+        all_cnt = torch.stack([g_[1] for g_ in got])
+        running = [e.gp_replay(all_cnt, all_ent, stride, G, stream) for e in engines]
+        assert len(set(running)) == 1, "replicated replay diverged"
+        rounds += 1
+        if running[0] == 0:
+            break
+    if stats is not None:
+        stats["rounds"] = rounds
+    res = [e.gp_result(stream) for e in engines]
+    for r in range(1, G):
+        assert torch.equal(res[r][0], res[0][0]) and torch.equal(res[r][1], res[0][1]), "ranks disagree"
+    return res[0][0], res[0][1].to(torch.float32)
 
 
 def _coll_device():

@@ -1,7 +1,8 @@
 """bench.py's N > 1 path (points sharded over ranks) end to end
 on one GPU: two torchrun ranks pinned to cuda:0 with the gloo backend
 (CRISP_BENCH_DEVICE; no GPU kernel waits on another rank).  Guaranteed Mode
-with the exact global fallback must give the single-index recall for every G;
+with the exact global fallback and Optimized Mode with global patience must
+give the single-index recall for every G;
 the JSON line must follow the driver contract."""
 import json
 import os
@@ -36,5 +37,7 @@ def test_bench_two_ranks_match_one():
     for key in ("metric", "value", "unit", "ms_per_step", "higher_is_better", "scaling", "roofline", "clocks", "e2e"):
         assert key in b
     assert b["e2e"]["value"] > 0 and b["e2e"]["h2d_bytes_per_step"] > 0  # end to end at N = 2 too
-    # phi=0 with the exact global fallback: identical to the single index
+    # phi=0 with the exact global fallback, phi=1 with the patience rule over the global
+    # (h, gid) order: both identical to the single index
     assert b["per_mode"]["guaranteed"]["recall"] == a["per_mode"]["guaranteed"]["recall"]
+    assert b["per_mode"]["optimized"]["recall"] == a["per_mode"]["optimized"]["recall"]
