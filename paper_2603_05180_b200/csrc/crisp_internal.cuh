@@ -178,7 +178,6 @@ void session_gp_result(crisp_session *ss, int64_t *out_ids, double *out_d64, cud
 
 // stage timing
 bool stage_timing_on();
-void stage_record(int stage, cudaEvent_t a, cudaEvent_t b);
 
 }  // namespace crisp
 

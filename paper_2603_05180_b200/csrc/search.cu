@@ -16,6 +16,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -3471,7 +3472,7 @@ struct StageEv {
 };
 static thread_local std::vector<StageEv> g_events;
 static thread_local double g_stage_ms[8];  // 0 transform 1 probe 2 count 3 fallback 4 verify 5 merge 6 hamming
-static bool g_timing = false;
+static std::atomic<bool> g_timing{false};  // process-wide switch (crisp_set_stage_timing); tables are per thread
 static thread_local int64_t g_launches = 0;  // kernels of this library launched by searches on this thread
 
 bool stage_timing_on() { return g_timing; }
@@ -4812,7 +4813,6 @@ void merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32
     g_launches++;
 }
 
-void stage_record(int, cudaEvent_t, cudaEvent_t) {}
 
 }  // namespace crisp
 
