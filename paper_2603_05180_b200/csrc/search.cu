@@ -3711,7 +3711,10 @@ struct Work {
             }
         }
         DS = std::max({F, S0, std::min(std::max(Pq, nl_min), 1 << 16)});  // dbuf row stride (max span of a round)
-        nl_max = lbf ? std::max(nl_min, std::min(DS, env_int("CRISP_LB_SPAN", 2048))) : DS;
+        // filtered spans: 2048 rows (cfg4, P = 4000: 29.1 ms; 1024 / 4096: 37.4 / 35.0 ms before the
+        // exact-row queue), or P/2 for long patience (cfg3 P = 100k, cfg5 P = 20k: six rounds of 2048 rows
+        // left most rows to the unfiltered tail)
+        nl_max = lbf ? std::max(nl_min, std::min(DS, env_int("CRISP_LB_SPAN", std::max(2048, Pq / 2)))) : DS;
         if (ix->C8) {
             fa.C8 = (const uint4 *)ix->C8;
             fa.meta = (const int4 *)ix->c8meta;
