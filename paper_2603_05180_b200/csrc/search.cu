@@ -892,6 +892,10 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
 // counters at the end -- cfg4 count 26.1 ms against 23.4 ms.)
 // ---------------------------------------------------------------------------
 constexpr int CF_CAP = CRISP_CF_CAP;  // fragments staged per chunk
+#ifndef CRISP_COUNT_LAG
+#define CRISP_COUNT_LAG 0
+#endif
+constexpr bool CF_LAG = CRISP_COUNT_LAG != 0;
 constexpr int CF_MAXW = 32;   // warps per CTA: 16 (two CTAs per SM, F <= 2) or 32 (one CTA per SM, F = 4)
 
 struct CountFSmem {
@@ -910,6 +914,13 @@ __host__ __device__ constexpr size_t countf_smem(int BF) {
 __device__ __forceinline__ uint32_t atom_add_sh(uint32_t a, uint32_t v) {
     uint32_t old;
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    return old;
+}
+// the same without a compiler memory barrier (the count loop's other shared accesses are
+// reads of the staged table, which no atomic touches)
+__device__ __forceinline__ uint32_t atom_add_sh_nc(uint32_t a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v));
     return old;
 }
 __device__ __forceinline__ void red_add_sh(uint32_t a, uint32_t v) {
@@ -1094,30 +1105,46 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                 }
             };
             issue(Q0);
+            // CRISP_COUNT_LAG=1 (compile time) runs a step's crossing checks one step late, so that
+            // its atomics' returns arrive while the next step's atomics issue: measured slower at
+            // cfg4 (17.6 against 16.9 ms; 64 registers leave no room for the extra live values)
+            uint32_t pov[4] = {0u, 0u, 0u, 0u}, pxs[4] = {0u, 0u, 0u, 0u}, pinc[4] = {0u, 0u, 0u, 0u};
+            auto cross = [&](const uint32_t (&ov)[4], const uint32_t (&xs)[4], const uint32_t (&inc)[4]) {
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const uint32_t off = xs[e] - bbase;
+                    const uint32_t o8 = (ov[e] >> ((off & 3u) * 8u)) & 0xffu;
+                    if (taum1 - o8 < inc[e])  // o8 < tau <= o8 + inc: x enters C
+                        red_or_sh(sm_bm + ((off >> 5) << 2), 1u << (off & 31));
+                }
+            };
             for (int pp = Q0; pp < Q1; pp += 32) {
                 const uint4 qv = qn;
                 const int q0 = qpn * 4, lo = gn0, hi = gn1;
                 const uint32_t w = wn;
                 if (pp + 32 < Q1) issue(pp + 32);
                 const uint32_t xs[4] = {qv.x, qv.y, qv.z, qv.w};
-                uint32_t ov[4], sh[4], inc[4];
+                uint32_t ov[4], inc[4];
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
                     const bool ok = q0 + e >= lo && q0 + e < hi;
                     inc[e] = ok ? w : 0u;
                     const uint32_t off = xs[e] - bbase;
-                    sh[e] = (off & 3u) * 8u;
-                    ov[e] = atom_add_sh(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << sh[e]);
+                    ov[e] = atom_add_sh_nc(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << ((off & 3u) * 8u));
                 }
+                if (CF_LAG) {
+                    cross(pov, pxs, pinc);
 #pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const uint32_t o8 = (ov[e] >> sh[e]) & 0xffu;
-                    if (taum1 - o8 < inc[e]) {  // o8 < tau <= o8 + inc: x enters C
-                        const uint32_t off = xs[e] - bbase;
-                        red_or_sh(sm_bm + ((off >> 5) << 2), 1u << (off & 31));
+                    for (int e = 0; e < 4; e++) {
+                        pov[e] = ov[e];
+                        pxs[e] = xs[e];
+                        pinc[e] = inc[e];
                     }
+                } else {
+                    cross(ov, xs, inc);
                 }
             }
+            if (CF_LAG) cross(pov, pxs, pinc);
         }
         __syncthreads();  // the chunk's table is re-staged next
     }
@@ -3529,6 +3556,7 @@ static void set_attrs() {
     if (std::find(done_dev.begin(), done_dev.end(), dev) != done_dev.end()) return;
     CRISP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -3913,7 +3941,12 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
             g_launches++;
             // 64K ids per CTA: 16 warps, two CTAs per SM; 128K ids: 32 warps, one CTA per SM
             uint16_t *hb = (w.mode == 1 && w.ham_fused) ? w.hbuf : nullptr;  // phi=1: Hamming fused into the count
-            if (w.CF * ix->BS > 65536)
+            if (w.CF * ix->BS <= 32768 && env_int("CRISP_COUNT_W8", 0))
+                k_count_frag<8><<<dim3((unsigned)w.NS, (unsigned)qn), 256, countf_smem(ix->BS * w.CF), s>>>(
+                    w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
+                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp,
+                    hb, w.ghist);
+            else if (w.CF * ix->BS > 65536)
                 k_count_frag<32><<<dim3((unsigned)w.NS, (unsigned)qn), 1024, countf_smem(ix->BS * w.CF), s>>>(
                     w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
                     w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp,
