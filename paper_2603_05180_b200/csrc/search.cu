@@ -2471,6 +2471,120 @@ __global__ void __launch_bounds__(THREADS, HT > 2 ? 2 : 4) k_hamming_dense(const
         if (hist[i]) atomicAdd(&gh[i], hist[i]);
 }
 
+// k_hamming_seg (a4, phi=1): the same h, segment-major.  Grid (query groups,
+// candidate segments) with the segment as the slow index: the CTAs in flight
+// all work inside one id block, whose code rows (BF x 8 Wd bytes, 24 MB at
+// cfg4) stay in L2 while every query's candidates in that block are scored,
+// so each code row comes from DRAM about once per step instead of once per
+// query that holds it.  A warp takes one query of the group (its b(q') in its
+// own shared slice) and that query's candidates of the segment, 4 lanes per
+// candidate; h goes to the candidate's pool position (k_hhist then builds the
+// per-query histograms).
+template <int HT>
+__global__ void __launch_bounds__(THREADS, 4) k_hamming_seg(const uint64_t *__restrict__ qcodes,
+                                                          const uint64_t *__restrict__ codes, int Wd,
+                                                          const int32_t *__restrict__ pool, int64_t CAPQ,
+                                                          const int32_t *__restrict__ cbase,
+                                                          const int32_t *__restrict__ ncand, int NS, int64_t Qn,
+                                                          uint16_t *__restrict__ hbuf, const int32_t *__restrict__ fb,
+                                                          const int32_t *__restrict__ qperm) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint64_t *qc = (uint64_t *)sm + warp * Wd;  // this warp's b(q')
+    const int64_t qi = (int64_t)blockIdx.x * WARPS + warp;
+    if (qi >= Qn) return;
+    const int64_t q = qperm ? qperm[qi] : qi;
+    if (fb[q]) return;  // the fallback replaced C_q: k_hamming handles it
+    const int sb = blockIdx.y;
+    const int n = ncand[q * NS + sb];
+    if (n <= 0) return;
+    for (int i = lane; i < Wd; i += 32) qc[i] = qcodes[q * Wd + i];
+    __syncwarp();
+    const int base = cbase[q * NS + sb];
+    const int32_t *poolq = pool + q * CAPQ + base;
+    uint16_t *hq = hbuf + q * CAPQ + base;
+    const int g4 = lane >> 2, gl = lane & 3, nt = Wd >> 3;
+    int idn[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const int v = r * 8 + g4;
+        idn[r] = v < n ? __ldg(poolq + v) : 0;
+    }
+    for (int v0 = 0; v0 < n; v0 += 32) {
+        int id[4];
+        bool okv[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const int v = v0 + r * 8 + g4;
+            okv[r] = v < n;
+            id[r] = idn[r];
+            const int vn = v + 32;
+            idn[r] = vn < n ? __ldg(poolq + vn) : 0;
+        }
+        int hr[4] = {0, 0, 0, 0};
+        for (int t0 = 0; t0 < nt; t0 += HT) {
+            ulonglong2 cw[HT][4];
+#pragma unroll
+            for (int tt = 0; tt < HT; tt++)
+#pragma unroll
+                for (int r = 0; r < 4; r++)
+                    cw[tt][r] = t0 + tt < nt ? __ldg((const ulonglong2 *)(codes + (int64_t)id[r] * Wd + 2 * gl + 8 * (t0 + tt)))
+                                             : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+            for (int tt = 0; tt < HT; tt++) {
+                const int wd = 2 * gl + 8 * min(t0 + tt, nt - 1);
+                const uint64_t q0 = t0 + tt < nt ? qc[wd] : 0ull, q1 = t0 + tt < nt ? qc[wd + 1] : 0ull;
+#pragma unroll
+                for (int r = 0; r < 4; r++) hr[r] += __popcll(q0 ^ cw[tt][r].x) + __popcll(q1 ^ cw[tt][r].y);
+            }
+        }
+        uint32_t p01 = (uint32_t)hr[0] | ((uint32_t)hr[1] << 16), p23 = (uint32_t)hr[2] | ((uint32_t)hr[3] << 16);
+        p01 += __shfl_xor_sync(0xffffffffu, p01, 1);
+        p23 += __shfl_xor_sync(0xffffffffu, p23, 1);
+        p01 += __shfl_xor_sync(0xffffffffu, p01, 2);
+        p23 += __shfl_xor_sync(0xffffffffu, p23, 2);
+        if (gl == 0) {
+            const int hh[4] = {(int)(p01 & 0xffffu), (int)(p01 >> 16), (int)(p23 & 0xffffu), (int)(p23 >> 16)};
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (okv[r]) hq[v0 + r * 8 + g4] = (uint16_t)hh[r];
+        }
+    }
+}
+
+// b(q') of every query (Wd words; bit (i mod 64) of word i/64 = [q'_i > 0], Z10), warp per query
+__global__ void k_qcodes(const float *__restrict__ qrot, int pitch, int Dp, int Wd, int64_t Qn,
+                         uint64_t *__restrict__ qcodes) {
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= Qn) return;
+    const float *qrow = qrot + q * pitch;
+    for (int d0 = 0; d0 < Wd * 64; d0 += 32) {
+        const int d = d0 + lane;
+        const unsigned bits = __ballot_sync(0xffffffffu, d < Dp && qrow[d] > 0.0f);
+        if (lane == 0) ((uint32_t *)(qcodes + q * Wd))[d0 >> 5] = bits;
+    }
+}
+
+// per-query histogram of h over the dense pool positions (after k_hamming_seg)
+__global__ void __launch_bounds__(THREADS) k_hhist(int Dp, const int32_t *__restrict__ cursor, int64_t CAPQ,
+                                                   const uint16_t *__restrict__ hbuf, int32_t *__restrict__ ghist,
+                                                   const int32_t *__restrict__ fb) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    int *hist = (int *)sm;  // Dp + 1
+    const int64_t q = blockIdx.x;
+    if (fb[q]) return;
+    for (int i = threadIdx.x; i < Dp + 1; i += THREADS) hist[i] = 0;
+    __syncthreads();
+    const int total = (int)min((int64_t)cursor[q], CAPQ);
+    const uint16_t *hq = hbuf + q * CAPQ;
+    for (int v = threadIdx.x; v < total; v += THREADS) atomicAdd(&hist[hq[v]], 1);
+    __syncthreads();
+    int32_t *gh = ghist + q * (int64_t)(Dp + 1);
+    for (int i = threadIdx.x; i < Dp + 1; i += THREADS)
+        if (hist[i]) atomicAdd(&gh[i], hist[i]);
+}
+
 // k_hsort: one warp per query; stable counting sort of the ascending-id list by
 // h -> order (h, id), written over the query's pool region.
 // One warp: bin starts of the per-query histogram (start[], Dp+1) and the
@@ -3580,6 +3694,9 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_patience_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hamming_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hamming_seg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_hhist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hamming_dense<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_hsort_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -3638,6 +3755,7 @@ struct Work {
     void *qsort_tmp = nullptr;
     size_t qsort_bytes = 0;
     uint16_t *hbuf = nullptr;
+    uint64_t *qcodes = nullptr;  // b(q') per query (k_hamming_seg)
     PatState pst{};
     uint8_t *traceV = nullptr;
     bool full_order = false;  // trace: order every candidate (not only what the rounds read)
@@ -3667,7 +3785,7 @@ struct Work {
                        (int64_t)ix->NBW * 8 + 64;
         if (mode == 0) perq += (int64_t)std::max<int64_t>(S, (ix->N + 4095) / 4096) * k * 16 + (ix->C8 ? CAPQ * 8 + 4 : 0);
         if (ix->C8) perq += 2 * (int64_t)ix->c8pitch + 32;  // query digit planes + bound terms
-        else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32;
+        else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32 + (int64_t)ix->Wp * 8;
         if (traceV) perq += ix->N;
         return perq;
     }
@@ -3800,6 +3918,7 @@ struct Work {
         } else {
             cbuf = buf.alloc<int32_t>((size_t)Qc * CAPQ);
             hbuf = buf.alloc<uint16_t>((size_t)Qc * CAPQ);
+            qcodes = buf.alloc<uint64_t>((size_t)Qc * ix->Wp);
             ghist = buf.alloc<int32_t>((size_t)Qc * (Dp + 1));
             totals = buf.alloc<int32_t>((size_t)Qc);
             dbuf = buf.alloc<double>((size_t)Qc * DS);
@@ -4013,7 +4132,29 @@ static void run_order(Work &w, int64_t qn, cudaStream_t s) {
                                                  NB, w.hbuf, w.ghist, w.fb, w.qperm);
         CRISP_LAUNCH();
         g_launches++;
-        if (!((w.count_kernel == 1 || w.count_kernel == 2) && w.ham_fused)) {
+        if (w.count_kernel == 2 && !w.ham_fused && env_int("CRISP_HAMMING_SEG", 1) &&
+            (size_t)WARPS * ix->Wp * 8 <= 48 * 1024) {
+            // segment-major over the 64K-id segments of k_count_frag (the code rows of one id
+            // block stay in L2; measured at cfg4: 8.6 against 11.3 ms), then the histograms.
+            // (The 4096-id segments of k_count_warp, cfg2, hold too few candidates per warp:
+            // 3.6 against 1.9 ms, so that path keeps the per-query kernel.)
+            k_qcodes<<<nblk(qn, 8), 256, 0, s>>>(w.qrot, pitch, Dp, ix->Wp, qn, w.qcodes);
+            CRISP_LAUNCH();
+            dim3 g2(nblk(qn, WARPS), (unsigned)NB);
+            if (env_int("CRISP_HAMMING_SEG_HT", 2) >= 4)
+                k_hamming_seg<4><<<g2, THREADS, WARPS * ix->Wp * 8, s>>>(w.qcodes, ix->codes, ix->Wp, w.pool, w.CAPQ,
+                                                                         w.cbase, w.ncand, NB, qn, w.hbuf, w.fb,
+                                                                         w.qperm);
+            else
+                k_hamming_seg<2><<<g2, THREADS, WARPS * ix->Wp * 8, s>>>(w.qcodes, ix->codes, ix->Wp, w.pool, w.CAPQ,
+                                                                         w.cbase, w.ncand, NB, qn, w.hbuf, w.fb,
+                                                                         w.qperm);
+            CRISP_LAUNCH();
+            g_launches++;
+            k_hhist<<<(unsigned)qn, THREADS, (Dp + 1) * 4, s>>>(Dp, w.cursor, w.CAPQ, w.hbuf, w.ghist, w.fb);
+            CRISP_LAUNCH();
+            g_launches += 2;
+        } else if (!((w.count_kernel == 1 || w.count_kernel == 2) && w.ham_fused)) {
             dim3 g2(w.HS, (unsigned)qn);
             // 16-byte chunks of each code row issued together per lane (CRISP_HAMMING_HT: 2, or 4 with
             // 2 CTAs per SM; measured at cfg4: 12.4 ms with 2 (8 loads in flight), 14.7 with 4, 14.0 before)
