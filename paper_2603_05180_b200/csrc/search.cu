@@ -3122,6 +3122,211 @@ __global__ void __launch_bounds__(THREADS, MINB) k_verify_rows_lb(const float *_
     }
 }
 
+// Block-major filtered round (opt-in CRISP_LB_BLOCKS=1; measured slower): the same bounds as
+// k_verify_rows_lb, but the rows of every running query's span are first
+// bucketed by id block (BSZ ids, k_span_bucket), and k_verify_lb_blk takes
+// (query group, id block) with the block as the slow grid index, so the int8
+// rows of one block (BSZ x c8pitch bytes, ~50 MB) stay in L2 while all the
+// queries' rows in it are bounded: a row is read from DRAM about once per
+// round instead of once per query that verifies it.  Exact distances of the
+// kept rows read q' from global memory (same arithmetic and order as
+// row_dist*: identical values).
+__device__ __forceinline__ Q4 q4_g(const float4 *__restrict__ q4, int v) {
+    const float4 t = __ldg(q4 + v);
+    return {(double)t.x, (double)t.y, (double)t.z, (double)t.w};
+}
+__device__ __forceinline__ void row_dist4_g(const float *__restrict__ r0, const float *__restrict__ r1,
+                                            const float *__restrict__ r2, const float *__restrict__ r3,
+                                            const float *__restrict__ qrow, int nvec, int lane, double (&o)[4]) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const float4 *x0 = (const float4 *)r0, *x1 = (const float4 *)r1, *x2 = (const float4 *)r2,
+                 *x3 = (const float4 *)r3, *q4 = (const float4 *)qrow;
+#pragma unroll 2
+    for (int v = lane; v < nvec; v += 32) {
+        const float4 u0 = __ldg(x0 + v), u1 = __ldg(x1 + v), u2 = __ldg(x2 + v), u3 = __ldg(x3 + v);
+        const Q4 qv = q4_g(q4, v);
+        acc4(a0, u0, qv);
+        acc4(a1, u1, qv);
+        acc4(a2, u2, qv);
+        acc4(a3, u3, qv);
+    }
+    o[0] = warp_sum(a0);
+    o[1] = warp_sum(a1);
+    o[2] = warp_sum(a2);
+    o[3] = warp_sum(a3);
+}
+__device__ __forceinline__ double row_dist1_g(const float *__restrict__ r0, const float *__restrict__ qrow, int nvec,
+                                              int lane) {
+    double a0 = 0.0;
+    const float4 *x0 = (const float4 *)r0, *q4 = (const float4 *)qrow;
+#pragma unroll 4
+    for (int v = lane; v < nvec; v += 32) acc4(a0, __ldg(x0 + v), q4_g(q4, v));
+    return warp_sum(a0);
+}
+
+// per running query (CTA): its span's (id, position) pairs grouped by id block
+__global__ void __launch_bounds__(256) k_span_bucket(const int32_t *__restrict__ pool, int64_t PS,
+                                                     const int32_t *__restrict__ totals, PatState st, int send,
+                                                     int BSH, int NBB, int DS, int2 *__restrict__ spair,
+                                                     int32_t *__restrict__ boff) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    int *cnt = (int *)sm;  // NBB + 1
+    const int64_t q = blockIdx.x;
+    int32_t *bo = boff + q * (int64_t)(NBB + 1);
+    if (st.done[q]) {
+        for (int b = threadIdx.x; b <= NBB; b += blockDim.x) bo[b] = 0;
+        return;
+    }
+    int j0;
+    const int n = round_span(st, q, -1, 0, totals[q], send, j0);
+    const int32_t *ord = pool + q * PS + j0;
+    for (int b = threadIdx.x; b <= NBB; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) atomicAdd(&cnt[ord[j] >> BSH], 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the counts (one warp)
+        int carry = 0;
+        for (int b0 = 0; b0 <= NBB; b0 += 32) {
+            const int b = b0 + threadIdx.x;
+            const int v = b <= NBB ? cnt[b] : 0;
+            int inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if ((int)threadIdx.x >= o) inc += t;
+            }
+            if (b <= NBB) {
+                bo[b] = carry + inc - v;
+                cnt[b] = carry + inc - v;  // running insert position
+            }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    __syncthreads();
+    int2 *sp = spair + q * (int64_t)DS;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const int id = ord[j];
+        sp[atomicAdd(&cnt[id >> BSH], 1)] = make_int2(id, j);
+    }
+}
+
+template <int QPC>
+__global__ void __launch_bounds__(THREADS, 3) k_verify_lb_blk(const float *__restrict__ qrot, int pitch,
+                                                           const float *__restrict__ X, FiltArgs fa, PatState st,
+                                                           int k, int64_t Qn, int NBB, int DS,
+                                                           const int2 *__restrict__ spair,
+                                                           const int32_t *__restrict__ boff,
+                                                           double *__restrict__ dbuf,
+                                                           unsigned long long *__restrict__ fstats) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.y;
+    int *eq_j = (int *)sm + warp * 64, *eq_r = eq_j + 32;
+    unsigned nb = 0, ne = 0;
+    // a CTA takes QPC consecutive queries of block b; warp w takes queries w, w + WARPS, ...
+    for (int64_t q = (int64_t)blockIdx.x * QPC + warp; q < min(Qn, (int64_t)(blockIdx.x + 1) * QPC); q += WARPS) {
+    if (st.done[q]) continue;
+    const int32_t *bo = boff + q * (int64_t)(NBB + 1);
+    const int p0 = bo[b], p1 = bo[b + 1];
+    if (p0 >= p1) continue;
+    const double *qi = fa.qi + q * 4;
+    const QTerms qt{qi[0], qi[1], qi[2], qi[3] != 0.0};
+    const double thr = (qt.ok && st.cnt[q] >= k) ? sqrt(st.Td[q * k + k - 1]) * (1.0 + 1e-9) : -1.0;
+    const uint4 *sq = fa.qd + q * 2 * fa.nv16;  // the digit planes (global; L1 keeps them)
+    const float *qrow = qrot + q * pitch;
+    const int nvec = pitch / 4;
+    const int2 *sp = spair + q * (int64_t)DS;
+    double *dq = dbuf + q * (int64_t)DS;
+    int eqn = 0;
+    auto exact_flush = [&](int min_rows) {
+        while (eqn >= min_rows && eqn > 0) {
+            __syncwarp();
+            const int m = min(eqn, 4);
+            int jr[4], rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                jr[u] = eq_j[max(0, eqn - 1 - u)];
+                rr[u] = eq_r[max(0, eqn - 1 - u)];
+            }
+            if (m == 4) {
+                double d4[4];
+                row_dist4_g(X + (int64_t)rr[0] * pitch, X + (int64_t)rr[1] * pitch, X + (int64_t)rr[2] * pitch,
+                            X + (int64_t)rr[3] * pitch, qrow, nvec, lane, d4);
+                if (lane == 0) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) dq[jr[u]] = d4[u];
+                }
+            } else {
+                for (int u = 0; u < m; u++) {
+                    const double d0 = row_dist1_g(X + (int64_t)rr[u] * pitch, qrow, nvec, lane);
+                    if (lane == 0) dq[jr[u]] = d0;
+                }
+            }
+            eqn -= m;
+            ne += m;
+            __syncwarp();
+        }
+    };
+    for (int p = p0; p < p1; p += 4) {
+        int rows[4], jj[4], nr = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int2 e = p + u < p1 ? sp[p + u] : make_int2(-1, 0);
+            rows[u] = e.x;
+            jj[u] = e.y;
+            nr += e.x >= 0;
+        }
+        unsigned need;
+        if (thr < 0.0) {
+            need = (1u << nr) - 1u;
+        } else {
+            const uint4 *r4[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) r4[u] = fa.C8 + (int64_t)(rows[u] >= 0 ? rows[u] : rows[0]) * fa.nv16;
+            int S1[4], S2[4];
+            rows_q8<4>(r4, sq, fa.nv16, lane, S1, S2);
+            nb += nr;
+            int s1 = 0, s2 = 0, rr = -1, jl = 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (lane == u) {
+                    s1 = S1[u];
+                    s2 = S2[u];
+                    rr = rows[u];
+                    jl = jj[u];
+                }
+            bool keep = false;
+            if (rr >= 0) {
+                double lb, ub;
+                filt_bounds(qt, s1, s2, __ldg(fa.meta + rr), lb, ub);
+                keep = !(lb > thr);
+                if (!keep) dq[jl] = INFINITY;
+            }
+            need = __ballot_sync(0xffffffffu, keep);
+        }
+        if (need) {
+            if (lane == 0) {
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if ((need >> u) & 1u) {
+                        eq_j[eqn] = jj[u];
+                        eq_r[eqn] = rows[u];
+                        eqn++;
+                    }
+            }
+            eqn = __shfl_sync(0xffffffffu, eqn, 0);
+            if (eqn >= 28) exact_flush(4);
+        }
+    }
+    exact_flush(1);
+    if (thr < 0.0) ne = 0;
+    }
+    if (fstats && lane == 0 && (nb | ne)) {
+        atomicAdd(fstats, (unsigned long long)nb);
+        atomicAdd(fstats + 1, (unsigned long long)ne);
+    }
+}
+
 // ADSampling context of Optimized Mode verification (Eq. 2; crisp_set_adsampling)
 struct AdCtx {
     int on;
@@ -3686,6 +3891,7 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_lb_bounds<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_lb_threshold, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows_lb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_span_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_verify_rows_lb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_rerank_group<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -3726,6 +3932,9 @@ struct Work {
     int lbf = 0, lb0 = 0, nl_max = 0, vrl_smem = 0, lbb_smem = 0, lbt_smem = 0;
     float2 *lbb = nullptr;
     float *Tq = nullptr;
+    int lbblk = 0, BSH = 0, NBB = 0, bkt_smem = 0;  // block-major filtered rounds
+    int2 *spair = nullptr;
+    int32_t *boff = nullptr;
     // the query's digit planes and bound terms (k_q8_prep), before the filtered kernels
     void q8_prep(int64_t qn, cudaStream_t s) const {
         k_q8_prep<<<(unsigned)qn, 256, 0, s>>>(qrot, ix->pitch, ix->mu, ix->c8pitch, const_cast<uint4 *>(fa.qd),
@@ -3785,7 +3994,8 @@ struct Work {
                        (int64_t)ix->NBW * 8 + 64;
         if (mode == 0) perq += (int64_t)std::max<int64_t>(S, (ix->N + 4095) / 4096) * k * 16 + (ix->C8 ? CAPQ * 8 + 4 : 0);
         if (ix->C8) perq += 2 * (int64_t)ix->c8pitch + 32;  // query digit planes + bound terms
-        else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 8 + (int64_t)k * 16 + 32 + (int64_t)ix->Wp * 8;
+        else perq += CAPQ * 6 + (int64_t)(ix->Dp + 1) * 4 + (int64_t)S0 * 16 + (int64_t)k * 16 + 32 + (int64_t)ix->Wp * 8 +
+                     (ix->N >> 10) * 4 + 8;  // + the span buckets of the block-major filtered rounds
         if (traceV) perq += ix->N;
         return perq;
     }
@@ -3935,6 +4145,24 @@ struct Work {
         if (lbf || lb0) {
             fa.qd = buf.alloc<uint4>((size_t)Qc * 2 * fa.nv16);
             fa.qi = buf.alloc<double>((size_t)Qc * 4);
+        }
+        // block-major filtered rounds (opt-in CRISP_LB_BLOCKS=1).  Measured at cfg4: slower
+        // (verify 34.6-35.1 against 29.1 ms): the round-1 DRAM bytes drop only from ~64 to 52 GB
+        // (L2 hit rate 44-52%: the CTAs in flight span several id blocks) while the bucketing
+        // and the short per-(query, block) tasks add work
+        if (lbf && env_int("CRISP_LB_BLOCKS", 0)) {
+            // id blocks of 2^BSH ids whose int8 rows take <= ~64 MB (half of L2)
+            const int64_t rowb = ix->c8pitch + 16;
+            BSH = 10;
+            while (BSH < 24 && ((int64_t)1 << (BSH + 1)) * rowb <= (int64_t)64 << 20) BSH++;
+            BSH = env_int("CRISP_LB_BSH", BSH);
+            NBB = (int)((ix->N + ((int64_t)1 << BSH) - 1) >> BSH);
+            bkt_smem = (NBB + 1) * 4;
+            if (NBB <= 65535 && bkt_smem <= 200 * 1024) {
+                lbblk = 1;
+                spair = buf.alloc<int2>((size_t)Qc * DS);
+                boff = buf.alloc<int32_t>((size_t)Qc * (NBB + 1));
+            }
         }
         if (want_traceV) traceV = buf.alloc<uint8_t>((size_t)Qc * ix->N);
         if (want_d64tmp) d64tmp = buf.alloc<double>((size_t)Qc * k);
@@ -4274,7 +4502,20 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         const int j0 = own ? -1 : (r == 0 ? 0 : w.F + (r - 1) * w.S0), len = r == 0 ? w.F : w.S0;
         // CTAs per query: at most S, at least round_rows rows each (the query staging is per CTA)
         dim3 g(own ? w.S1 : std::max(1, std::min(w.S, len / w.round_rows)), (unsigned)qn);
-        if (w.lbf && r > 0 && env_int("CRISP_LB_CTAS", 3) == 4)
+        if (w.lbf && r > 0 && w.lbblk) {
+            k_span_bucket<<<(unsigned)qn, 256, w.bkt_smem, s>>>(w.cbuf, w.CAPQ, w.totals, w.pst, send, w.BSH, w.NBB,
+                                                                  w.DS, w.spair, w.boff);
+            CRISP_LAUNCH();
+            g_launches++;
+            if (env_int("CRISP_LB_QPC", 64) >= 64)
+                k_verify_lb_blk<64><<<dim3(nblk(qn, 64), (unsigned)w.NBB), THREADS, WARPS * 64 * 4, s>>>(
+                    w.qrot, pitch, ix->X, w.fa, w.pst, k, qn, w.NBB, w.DS, w.spair, w.boff, w.dbuf,
+                    g_timing ? d_filter_stats_ptr() : nullptr);
+            else
+                k_verify_lb_blk<WARPS><<<dim3(nblk(qn, WARPS), (unsigned)w.NBB), THREADS, WARPS * 64 * 4, s>>>(
+                    w.qrot, pitch, ix->X, w.fa, w.pst, k, qn, w.NBB, w.DS, w.spair, w.boff, w.dbuf,
+                    g_timing ? d_filter_stats_ptr() : nullptr);
+        } else if (w.lbf && r > 0 && env_int("CRISP_LB_CTAS", 3) == 4)
             k_verify_rows_lb<4><<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
                                                                w.pst, k, j0, len, send, w.DS, w.dbuf, w.qperm,
                                                                g_timing ? d_filter_stats_ptr() : nullptr);
