@@ -77,14 +77,14 @@ def _declare(L):
     L.or_argmin_centroid.argtypes = [vp, vp, i32, i32, vp]
     L.or_argmin_centroid.restype = i32
     L.or_kmeans.argtypes = [vp, i64, i64, i32, i32, i32, u64, u32, vp, vp]
-    L.or_train_codebooks.argtypes = [vp, i64, i64, i32, i32, i32, i32, i64, u64, vp]
-    L.or_assign.argtypes = [vp, i64, i64, i32, i32, i32, vp, vp]
+    L.or_train_codebooks.argtypes = [vp, i64, i64, i32, i32, i32, i32, i64, u64, vp, vp]
+    L.or_assign.argtypes = [vp, i64, i64, i32, i32, i32, vp, vp, vp]
     L.or_csr.argtypes = [vp, i64, i32, i32, vp, vp]
     L.or_codes.argtypes = [vp, i64, i64, i32, vp]
     L.or_half_sorted.argtypes = [vp, vp, i32, i32, vp, vp]
     L.or_multisequence.argtypes = [vp, vp, vp, vp, i32, vp, i64, i32, vp, vp, vp]
     L.or_multisequence.restype = i32
-    L.or_search.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, f64, i32,
+    L.or_search.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, f64, i32,
                             i32, vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.or_adsampling_threshold.argtypes = [f64, i32, i32, f64]
     L.or_adsampling_threshold.restype = f64
@@ -92,7 +92,7 @@ def _declare(L):
     L.or_adsampling_verify.restype = i32
     L.or_max_threads.restype = i32
     L.or_bruteforce_knn.argtypes = [vp, i64, i32, vp, i64, i32, vp, vp]
-    L.or_bruteforce_scores.argtypes = [vp, i64, i32, i32, i32, i32, vp, vp, i64, i64, i32, vp]
+    L.or_bruteforce_scores.argtypes = [vp, i64, i32, i32, i32, i32, vp, vp, vp, i64, i64, i32, vp]
     L.or_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp]
     L.or_hoeffding_bound.argtypes = [i32, f64, f64]
     L.or_hoeffding_bound.restype = f64
@@ -225,6 +225,50 @@ def blockwise_rotation(X, M: int, Dp: int, b: int, seed: int):
     return R, blk
 
 
+def adaptive_widths(var, M: int, Dp: int):
+    """Adaptive subspace decomposition (reading R18): contiguous
+    subspace widths, even and >= 2, cut where the running variance first
+    reaches j/M of the total, so that high-variance regions get fewer
+    dimensions and low-variance regions more.  var: per-dimension variances
+    (zero beyond its length); sums in ascending dimension, fp64.  Cut j is the
+    smallest even e in [c_{j-1} + 2, Dp - 2(M - j)] with S(e) >= T j / M
+    (S(e) = sum of v_i for i < e, T = S(Dp)), else the upper end."""
+    v = np.zeros(Dp)
+    v[: len(var)] = var
+    S = [0.0]
+    for x in v:
+        S.append(S[-1] + float(x))
+    T = S[Dp]
+    cuts = [0]
+    for j in range(1, M):
+        e, hi, target = cuts[-1] + 2, Dp - 2 * (M - j), (T * j) / M
+        while e < hi and S[e] < target:
+            e += 2
+        cuts.append(e)
+    cuts.append(Dp)
+    return [cuts[j + 1] - cuts[j] for j in range(M)]
+
+
+def half_offsets(widths):
+    """2M+1 half offsets from M even subspace widths (equal halves)."""
+    h, o = [], 0
+    for w in widths:
+        assert w >= 2 and w % 2 == 0, "subspace widths must be even and >= 2"
+        h += [o, o + w // 2]
+        o += w
+    return np.array(h + [o], dtype=np.int32)
+
+
+def half_stride(hoff) -> int:
+    """codebook row stride: the largest half width"""
+    hoff = np.asarray(hoff)
+    return int(np.max(hoff[1:] - hoff[:-1]))
+
+
+def _hoff(hoff):
+    return None if hoff is None else np.ascontiguousarray(hoff, dtype=np.int32)
+
+
 def qr(G):
     A = np.array(G, dtype=np.float64, order="C", copy=True)
     D = A.shape[0]
@@ -269,22 +313,23 @@ def kmeans(pts, K: int, iters: int, seed: int, half: int = 0):
     return Cm, obj[:iters]
 
 
-def train_codebooks(X, M: int, K: int, iters: int, sample: int, seed: int):
+def train_codebooks(X, M: int, K: int, iters: int, sample: int, seed: int, hoff=None):
+    """Codebooks of the 2M halves; hoff (2M+1 half offsets, R18) or equal halves."""
     X = np.ascontiguousarray(X, dtype=np.float32)
     N, Dp = X.shape
-    dh = Dp // (2 * M)
+    dh = Dp // (2 * M) if hoff is None else half_stride(hoff)
     cb = np.zeros((M, 2, K, dh), dtype=np.float32)
-    lib().or_train_codebooks(_p(X), N, Dp, M, K, dh, iters, sample, seed, _p(cb))
+    lib().or_train_codebooks(_p(X), N, Dp, M, K, dh, iters, sample, seed, _p(_hoff(hoff)), _p(cb))
     return cb
 
 
-def assign(X, cb):
+def assign(X, cb, hoff=None):
     X = np.ascontiguousarray(X, dtype=np.float32)
     cb = np.ascontiguousarray(cb, dtype=np.float32)
     N, Dp = X.shape
     M, _, K, dh = cb.shape
     cells = np.zeros((M, N), dtype=np.int32)
-    lib().or_assign(_p(X), N, Dp, M, K, dh, _p(cb), _p(cells))
+    lib().or_assign(_p(X), N, Dp, M, K, dh, _p(_hoff(hoff)), _p(cb), _p(cells))
     return cells
 
 
@@ -347,7 +392,7 @@ def bruteforce_knn(X, Qv, k: int):
     return ids, d
 
 
-def bruteforce_scores(cells, cb, qrot, budget: int, wk: int = 0):
+def bruteforce_scores(cells, cb, qrot, budget: int, wk: int = 0, hoff=None):
     cells = np.ascontiguousarray(cells, dtype=np.int32)
     cb = np.ascontiguousarray(cb, dtype=np.float32)
     qrot = np.ascontiguousarray(qrot, dtype=np.float32)
@@ -355,7 +400,7 @@ def bruteforce_scores(cells, cb, qrot, budget: int, wk: int = 0):
     _, _, K, dh = cb.shape
     Q, D = qrot.shape
     S = np.zeros((Q, N), dtype=np.uint16)
-    lib().or_bruteforce_scores(_p(cells), N, D, M, K, dh, _p(cb), _p(qrot), Q, budget, wk, _p(S))
+    lib().or_bruteforce_scores(_p(cells), N, D, M, K, dh, _p(_hoff(hoff)), _p(cb), _p(qrot), Q, budget, wk, _p(S))
     return S
 
 
@@ -379,11 +424,14 @@ def max_threads() -> int:
 # --------------------------------------------------------------------------
 def build(X, M: int, K: int = 50, tau_cev: float = 0.85, rotation_mode: int = -1, kmeans_iters: int = 20,
           kmeans_sample: int = 100000, seed: int = 0, R=None, codebooks=None, gid_base: int = 0,
-          rotation_block: int = 0):
+          rotation_block: int = 0, adaptive_subspaces: bool = False, subspace_widths=None):
     """Index build: spectral check + adaptive rotation, codebooks,
     cell assignment, CSR, binary codes.
 
-    ``R`` / ``codebooks`` inject the rotation / codebooks (as crisp_build_with)."""
+    ``R`` / ``codebooks`` inject the rotation / codebooks (as crisp_build_with).
+    ``subspace_widths`` (M even widths summing to Dp) or ``adaptive_subspaces``
+    (widths from the stored vectors' per-dimension variances, R18) replace the
+    equal split."""
     X = np.ascontiguousarray(X, dtype=np.float32)
     N, D = X.shape
     Dp = padded_dim(D, M)
@@ -402,15 +450,22 @@ def build(X, M: int, K: int = 50, tau_cev: float = 0.85, rotation_mode: int = -1
             R = blockwise_rotation(X, M, Dp, rotation_block, seed)[0] if rotation_block > 0 else rotation(Dp, seed)[0]
     if rotated:
         Xp = rotate_rows(Xp, R)
+    hoff = None
+    if subspace_widths is not None or adaptive_subspaces:
+        widths = list(subspace_widths) if subspace_widths is not None else adaptive_widths(
+            dim_variances(Xp, seed), M, Dp)
+        assert len(widths) == M and sum(widths) == Dp, "M widths summing to the padded dimensionality"
+        hoff = half_offsets(widths)
+        dh = half_stride(hoff)
     if codebooks is None:
-        cb = train_codebooks(Xp, M, K, kmeans_iters, min(N, kmeans_sample), seed)
+        cb = train_codebooks(Xp, M, K, kmeans_iters, min(N, kmeans_sample), seed, hoff)
     else:
         cb = np.ascontiguousarray(codebooks, dtype=np.float32).reshape(M, 2, K, dh)
-    cells = assign(Xp, cb)
+    cells = assign(Xp, cb, hoff)
     off, ids = csr(cells, K)
     cds = codes(Xp)
     gsize = (off[:, 1:] - off[:, :-1]).astype(np.int64)
-    return dict(N=N, D=D, Dp=Dp, M=M, K=K, dh=dh, X=Xp, R=R if rotated else None, rotated=rotated, cev=cev_v,
+    return dict(N=N, D=D, Dp=Dp, M=M, K=K, dh=dh, hoff=hoff, X=Xp, R=R if rotated else None, rotated=rotated, cev=cev_v,
                 cb=cb, cells=cells, off=off, ids=ids, codes=cds, gsize=gsize, gid_base=gid_base, N_budget=N)
 
 
@@ -458,7 +513,7 @@ def search(index, queries, k: int, mode: int, budget: int, tau: int, patience_fa
     gsize = np.ascontiguousarray(ix["gsize"], dtype=np.int64)
     ec = np.ascontiguousarray(ext_cand, dtype=np.int32) if ext_cand is not None else None
     en = np.ascontiguousarray(ext_n, dtype=np.int64) if ext_n is not None else None
-    lib().or_search(N, ix["gid_base"], ix["Dp"], M, K, ix["dh"], _p(ix["X"]),
+    lib().or_search(N, ix["gid_base"], ix["Dp"], M, K, ix["dh"], _p(_hoff(ix.get("hoff"))), _p(ix["X"]),
                     _p(ix["R"]) if ix["R"] is not None else None, _p(ix["cb"]), _p(ix["off"]), _p(ix["ids"]),
                     _p(ix["codes"]), _p(gsize), budget, tau, patience, 1 if adsampling else 0, eps0, ad_stride,
                     0 if fallback else 1, _p(ec), _p(en),

@@ -390,6 +390,26 @@ int32_t or_argmin_centroid(const float *x, const float *C, int32_t K, int32_t dh
     return best;
 }
 
+/* Half-subspace h covers dims [hoff[h], hoff[h+1]) of the stored vectors.
+ * Equal widths: hoff[h] = h*dh (hoff == NULL).  Adaptive subspace
+ * decomposition (reading R18): any even widths w_m = hoff[2m+2] -
+ * hoff[2m] with equal halves; codebook rows keep the stride dh = max half
+ * width, zero beyond the half's own width. */
+static int64_t half_off(const int32_t *hoff, int32_t h, int32_t dh) { return hoff ? hoff[h] : (int64_t)h * dh; }
+static int32_t half_w(const int32_t *hoff, int32_t h, int32_t dh) { return hoff ? hoff[h + 1] - hoff[h] : dh; }
+
+/* nearest of K centroids (rows of `stride` floats, first w used) by (dist64, c) */
+static int32_t argmin_centroid_w(const float *x, const float *C, int32_t K, int32_t w, int32_t stride)
+{
+    int32_t best = 0;
+    double bd = or_dist64(x, C, w);
+    for (int32_t c = 1; c < K; c++) {
+        double d = or_dist64(x, C + (int64_t)c * stride, w);
+        if (d < bd) { bd = d; best = c; }
+    }
+    return best;
+}
+
 void or_kmeans(const float *pts, int64_t n, int64_t ldp, int32_t dh, int32_t K, int32_t iters,
                uint64_t seed, uint32_t half, float *C, double *obj)
 {
@@ -479,20 +499,27 @@ void or_kmeans(const float *pts, int64_t n, int64_t ldp, int32_t dh, int32_t K, 
 /* Codebooks for all 2M halves from the k-means sample (min(N, 1e5)
  * rows, drawn with stream KM_SAMPLE).  Layout cb[((m*2+side)*K + c)*dh + t].
  * Subspace m covers dims [m*2dh, (m+1)*2dh); left = first dh, right = next dh
- * (Z17 for padding). */
+ * (Z17 for padding); with hoff (R18) half h covers [hoff[h], hoff[h+1])
+ * and its centroids fill the first hoff[h+1]-hoff[h] floats of their rows. */
 void or_train_codebooks(const float *X, int64_t N, int64_t ld, int32_t M, int32_t K, int32_t dh,
-                        int32_t iters, int64_t sample, uint64_t seed, float *cb)
+                        int32_t iters, int64_t sample, uint64_t seed, const int32_t *hoff, float *cb)
 {
     int64_t n = sample < N ? sample : N;
     int64_t *rows = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
     or_sample_rows(N, n, seed, OR_STREAM_KM_SAMPLE, rows);
 #pragma omp parallel for schedule(dynamic)
     for (int32_t h = 0; h < 2 * M; h++) {
-        float *pts = (float *)malloc(sizeof(float) * (size_t)n * dh);
+        const int32_t w = half_w(hoff, h, dh);
+        const int64_t o = half_off(hoff, h, dh);
+        float *pts = (float *)malloc(sizeof(float) * (size_t)n * w);
+        float *Cw = (float *)malloc(sizeof(float) * (size_t)K * w);
         for (int64_t r = 0; r < n; r++)
-            memcpy(pts + r * dh, X + rows[r] * ld + (int64_t)h * dh, sizeof(float) * (size_t)dh);
-        or_kmeans(pts, n, dh, dh, K, iters, seed, (uint32_t)h, cb + (int64_t)h * K * dh, NULL);
-        free(pts);
+            memcpy(pts + r * w, X + rows[r] * ld + o, sizeof(float) * (size_t)w);
+        or_kmeans(pts, n, w, w, K, iters, seed, (uint32_t)h, Cw, NULL);
+        float *ch = cb + (int64_t)h * K * dh;
+        for (int32_t c = 0; c < K; c++)
+            for (int32_t t = 0; t < dh; t++) ch[(int64_t)c * dh + t] = t < w ? Cw[(int64_t)c * w + t] : 0.0f;
+        free(pts); free(Cw);
     }
     free(rows);
 }
@@ -502,14 +529,16 @@ void or_train_codebooks(const float *X, int64_t N, int64_t ld, int32_t M, int32_
 /* left/right centroid by (dist64, c).  cells: M x N (row m contiguous).      */
 /* ------------------------------------------------------------------------- */
 void or_assign(const float *X, int64_t N, int64_t ld, int32_t M, int32_t K, int32_t dh,
-               const float *cb, int32_t *cells)
+               const int32_t *hoff, const float *cb, int32_t *cells)
 {
 #pragma omp parallel for schedule(static)
     for (int64_t p = 0; p < N; p++) {
         for (int32_t m = 0; m < M; m++) {
-            const float *x = X + p * ld + (int64_t)m * 2 * dh;
-            int32_t i = or_argmin_centroid(x, cb + ((int64_t)(m * 2 + 0) * K) * dh, K, dh, NULL);
-            int32_t j = or_argmin_centroid(x + dh, cb + ((int64_t)(m * 2 + 1) * K) * dh, K, dh, NULL);
+            const int32_t hl = 2 * m, hr = 2 * m + 1;
+            int32_t i = argmin_centroid_w(X + p * ld + half_off(hoff, hl, dh), cb + ((int64_t)hl * K) * dh, K,
+                                          half_w(hoff, hl, dh), dh);
+            int32_t j = argmin_centroid_w(X + p * ld + half_off(hoff, hr, dh), cb + ((int64_t)hr * K) * dh, K,
+                                          half_w(hoff, hr, dh), dh);
             cells[(int64_t)m * N + p] = i * K + j;
         }
     }
@@ -603,11 +632,20 @@ static heap_ent heap_pop(heap_ent *h, int32_t *n)
     return top;
 }
 
+void or_half_sorted_w(const float *qh, const float *Ch, int32_t K, int32_t w, int32_t stride, double *dist,
+                      int32_t *perm);
 /* Sorted partial distances of one half (Alg. 1 line 4; Z4). */
 void or_half_sorted(const float *qh, const float *Ch, int32_t K, int32_t dh, double *dist, int32_t *perm)
 {
+    or_half_sorted_w(qh, Ch, K, dh, dh, dist, perm);
+}
+
+/* the same over the first w floats of centroid rows of `stride` floats (R18) */
+void or_half_sorted_w(const float *qh, const float *Ch, int32_t K, int32_t w, int32_t stride, double *dist,
+                      int32_t *perm)
+{
     dist_c *t = (dist_c *)malloc(sizeof(dist_c) * (size_t)K);
-    for (int32_t c = 0; c < K; c++) { t[c].d = or_dist64(qh, Ch + (int64_t)c * dh, dh); t[c].c = c; }
+    for (int32_t c = 0; c < K; c++) { t[c].d = or_dist64(qh, Ch + (int64_t)c * stride, w); t[c].c = c; }
     qsort(t, (size_t)K, sizeof(dist_c), cmp_dist_c);
     for (int32_t r = 0; r < K; r++) { dist[r] = t[r].d; perm[r] = t[r].c; }
     free(t);
@@ -658,7 +696,8 @@ typedef struct {
     int64_t N;            /* local points */
     int64_t gid_base;     /* global id of local point 0 (shards) */
     int32_t D;            /* stored (padded) dimensionality Dp, = 2*M*dh */
-    int32_t M, K, dh;
+    int32_t M, K, dh;     /* dh: codebook row stride = the (largest) half width */
+    const int32_t *hoff;  /* 2M+1 half offsets (R18), NULL = equal halves of dh */
     const float *X;       /* N x D stored (rotated if applicable) */
     const float *R;       /* D x D or NULL */
     const float *cb;      /* M x 2 x K x dh */
@@ -748,8 +787,10 @@ static void search_one(const or_index *ix, const float *q_in, int32_t k, int32_t
     int32_t wk = (mode == 1) ? k : 0;
     for (int32_t m = 0; m < M; m++) {
         /* a1: Dist(q_left, C_left), Dist(q_right, C_right), sorted (Alg. 1 l.3-4) */
-        or_half_sorted(q + (int64_t)m * 2 * dh, ix->cb + ((int64_t)(m * 2 + 0) * K) * dh, K, dh, a, pa);
-        or_half_sorted(q + (int64_t)m * 2 * dh + dh, ix->cb + ((int64_t)(m * 2 + 1) * K) * dh, K, dh, b, pb);
+        or_half_sorted_w(q + half_off(ix->hoff, 2 * m, dh), ix->cb + ((int64_t)(m * 2 + 0) * K) * dh, K,
+                         half_w(ix->hoff, 2 * m, dh), dh, a, pa);
+        or_half_sorted_w(q + half_off(ix->hoff, 2 * m + 1, dh), ix->cb + ((int64_t)(m * 2 + 1) * K) * dh, K,
+                         half_w(ix->hoff, 2 * m + 1, dh), dh, b, pb);
         /* a2: Multi-Sequence traversal under the budget (Alg. 1 l.5-17) */
         int64_t ret = 0;
         int32_t L = or_multisequence(a, pa, b, pb, K, ix->gsize + (int64_t)m * KK, ix->budget, wk, cl, wl, &ret);
@@ -872,7 +913,7 @@ static void search_one(const or_index *ix, const float *q_in, int32_t k, int32_t
     free(q); free(V); free(a); free(b); free(pa); free(pb); free(cl); free(wl); free(C); free(best);
 }
 
-void or_search(int64_t N, int64_t gid_base, int32_t D, int32_t M, int32_t K, int32_t dh,
+void or_search(int64_t N, int64_t gid_base, int32_t D, int32_t M, int32_t K, int32_t dh, const int32_t *hoff,
                const float *X, const float *R, const float *cb, const int64_t *off, const int32_t *ids,
                const uint64_t *codes, const int64_t *gsize, int64_t budget, int32_t tau, int32_t patience,
                int32_t ad_on, double ad_eps0, int32_t ad_stride,
@@ -883,7 +924,7 @@ void or_search(int64_t N, int64_t gid_base, int32_t D, int32_t M, int32_t K, int
                uint16_t *t_V, int64_t *t_cand_n, int32_t *t_cand, int32_t *t_order, int64_t *t_nver,
                int32_t *t_fallback, float *t_qrot)
 {
-    or_index ix = {N, gid_base, D, M, K, dh, X, R, cb, off, ids, codes, gsize, budget, tau, patience,
+    or_index ix = {N, gid_base, D, M, K, dh, hoff, X, R, cb, off, ids, codes, gsize, budget, tau, patience,
                    ad_on, ad_eps0, ad_stride, fb_mode, ext_cand, ext_n};
     or_trace tr = {t_act_len, t_act_cell, t_act_w, t_retrieved, t_V, t_cand_n, t_cand, t_order, t_nver,
                    t_fallback, t_qrot};
@@ -940,7 +981,7 @@ static int cmp_cost_ij(const void *a, const void *b)
     return x->j < y->j ? -1 : (x->j > y->j);
 }
 void or_bruteforce_scores(const int32_t *cells, int64_t N, int32_t D, int32_t M, int32_t K, int32_t dh,
-                          const float *cb, const float *qrot, int64_t Q, int64_t budget, int32_t wk,
+                          const int32_t *hoff, const float *cb, const float *qrot, int64_t Q, int64_t budget, int32_t wk,
                           uint16_t *S)
 {
     int64_t KK = (int64_t)K * K;
@@ -953,7 +994,7 @@ void or_bruteforce_scores(const int32_t *cells, int64_t N, int32_t D, int32_t M,
         int32_t *pa = (int32_t *)malloc(sizeof(int32_t) * (size_t)K), *pb = (int32_t *)malloc(sizeof(int32_t) * (size_t)K);
         for (int64_t x = 0; x < N; x++) S[qi * N + x] = 0;
         for (int32_t m = 0; m < M; m++) {
-            const float *q = qrot + qi * D + (int64_t)m * 2 * dh;
+            const float *q = qrot + qi * D;
             for (int64_t c = 0; c < KK; c++) { size[c] = 0; wcell[c] = 0; }
             for (int64_t x = 0; x < N; x++) size[cells[(int64_t)m * N + x]]++;
             /* sorted halves by a plain selection sort on (dist64, c) */
@@ -961,7 +1002,11 @@ void or_bruteforce_scores(const int32_t *cells, int64_t N, int32_t D, int32_t M,
                 double *dd = side ? b : a;
                 int32_t *pp = side ? pb : pa;
                 const float *Ch = cb + ((int64_t)(m * 2 + side) * K) * dh;
-                for (int32_t c = 0; c < K; c++) { dd[c] = or_dist64(q + side * dh, Ch + (int64_t)c * dh, dh); pp[c] = c; }
+                const int32_t h = 2 * m + side;
+                for (int32_t c = 0; c < K; c++) {
+                    dd[c] = or_dist64(q + half_off(hoff, h, dh), Ch + (int64_t)c * dh, half_w(hoff, h, dh));
+                    pp[c] = c;
+                }
                 for (int32_t r = 0; r < K; r++) {
                     int32_t mi = r;
                     for (int32_t s = r + 1; s < K; s++)

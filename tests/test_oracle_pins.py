@@ -701,3 +701,79 @@ def test_blockwise_rotation_is_identity_outside_and_orthogonal_inside():
     assert np.array_equal(ox["X"][:, out], X[:, out])
     nb = np.linalg.norm(X[:, blk].astype(np.float64), axis=1)
     assert np.allclose(np.linalg.norm(ox["X"][:, blk].astype(np.float64), axis=1), nb, rtol=1e-5)
+
+
+# --------------------------------------------------------------------------
+# f4: adaptive subspace decomposition (DESIGN reading R18)
+# --------------------------------------------------------------------------
+def test_adaptive_widths_rule_by_hand_and_limits():
+    """Worked case: v = (8,4,2,1,1,1,1,.5 x5), M = 3, T = 20.5: cut 1 is the
+    first even e with S(e) >= 6.83 (S(2) = 12), cut 2 the first even e >= 4
+    with S(e) >= 13.67 (S(4) = 15): widths (2, 2, 8), the high-variance region
+    in narrow subspaces.  A flat spectrum gives the paper's equal split; a
+    single spike squeezes every cut to the minimum width 2."""
+    v = [8, 4, 2, 1, 1, 1, 1, .5, .5, .5, .5, .5]
+    assert oracle.adaptive_widths(v, 3, 12) == [2, 2, 8]
+    assert oracle.adaptive_widths(np.ones(48), 4, 48) == [12] * 4
+    assert oracle.adaptive_widths(np.ones(40), 4, 48) == [10, 10, 10, 18]  # zero-variance padding
+    assert oracle.adaptive_widths([100.0] + [0.0] * 31, 4, 32) == [2, 2, 2, 26]
+    for seed in range(5):
+        w = oracle.adaptive_widths(rng(seed).exponential(1.0, 60) ** 3, 6, 60)
+        assert sum(w) == 60 and all(x >= 2 and x % 2 == 0 for x in w)
+    h = oracle.half_offsets([2, 2, 8])
+    assert h.tolist() == [0, 1, 2, 3, 4, 8, 12] and oracle.half_stride(h) == 4
+
+
+def _pad_halves(X, hoff, dh):
+    """each half's dims first in a slot of dh, zeros after (the equal-width layout)"""
+    out = np.zeros((X.shape[0], (len(hoff) - 1) * dh), dtype=np.float32)
+    for h in range(len(hoff) - 1):
+        w = hoff[h + 1] - hoff[h]
+        out[:, h * dh: h * dh + w] = X[:, hoff[h]: hoff[h + 1]]
+    return out
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_adaptive_subspaces_equal_zero_padded_equal_split(mode):
+    """An index with widths (2, 2, 8) equals, bit for bit, the equal-split index
+    of the same vectors with each half moved into a dh = 4 slot and zero
+    filled: zero dimensions add exact zeros to every dist64 (k-means++, Lloyd,
+    assignment, half distances, verification keep their real terms in the same
+    order) and a 0 bit to both codes.  A wrong half offset, width or codebook
+    stride breaks the equality."""
+    r = rng(11)
+    N, D, M, K = 3000, 12, 3, 5
+    X = (r.standard_normal((N, D)) * np.array([6, 5, 4, 3, 1, 1, 1, 1, .5, .5, .5, .5])).astype(np.float32)
+    Qv = (r.standard_normal((20, D)) * 2).astype(np.float32)
+    oa = oracle.build(X, M, K=K, rotation_mode=0, kmeans_iters=6, seed=2, subspace_widths=[2, 2, 8])
+    assert oa["hoff"].tolist() == [0, 1, 2, 3, 4, 8, 12] and oa["dh"] == 4
+    Xp = _pad_halves(X, oa["hoff"], 4)
+    ou = oracle.build(Xp, M, K=K, rotation_mode=0, kmeans_iters=6, seed=2)
+    assert ou["dh"] == 4 and ou["hoff"] is None
+    assert np.array_equal(oa["cb"], ou["cb"]) and np.array_equal(oa["cells"], ou["cells"])
+    assert np.array_equal(oa["ids"], ou["ids"])
+    B, tau, k = 600, 2, 10
+    ia, da, ta = oracle.search(oa, Qv, k, mode, B, tau, patience_factor=3, trace=True)
+    iu, du, tu = oracle.search(ou, _pad_halves(Qv, oa["hoff"], 4), k, mode, B, tau, patience_factor=3, trace=True)
+    assert np.array_equal(ia, iu) and np.array_equal(da, du)
+    assert np.array_equal(ta["act_cell"], tu["act_cell"]) and np.array_equal(ta["V"], tu["V"])
+    assert np.array_equal(ta["n_verified"], tu["n_verified"])
+    # the brute-force scores (no CSR, no heap) agree with the search's V
+    S = oracle.bruteforce_scores(oa["cells"], oa["cb"], ta["qrot"], B, k if mode == 1 else 0, oa["hoff"])
+    assert np.array_equal(S, ta["V"])
+
+
+def test_adaptive_rule_in_build_and_equal_widths_are_the_default():
+    """adaptive_subspaces=True takes the widths of the rule on the stored
+    vectors' CEV-sample variances (a decaying spectrum: narrow leading
+    subspaces); explicit equal widths reproduce the default index."""
+    r = rng(12)
+    N, D, M = 4000, 32, 4
+    X = (r.standard_normal((N, D)) * np.exp(-np.arange(D) / 6.0)).astype(np.float32)
+    oa = oracle.build(X, M, K=4, rotation_mode=0, kmeans_iters=3, seed=1, adaptive_subspaces=True)
+    w = oracle.adaptive_widths(oracle.dim_variances(X, 1), M, 32)
+    assert (oa["hoff"][2::2] - oa["hoff"][:-1:2]).tolist() == w
+    assert w[0] < 8 < w[-1]
+    o1 = oracle.build(X, M, K=4, rotation_mode=0, kmeans_iters=3, seed=1)
+    o2 = oracle.build(X, M, K=4, rotation_mode=0, kmeans_iters=3, seed=1, subspace_widths=[8] * 4)
+    assert np.array_equal(o1["cb"], o2["cb"]) and np.array_equal(o1["cells"], o2["cells"])
