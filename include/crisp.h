@@ -71,6 +71,16 @@ typedef struct {
     int32_t rotation_block;    /* 0: global rotation when it applies; b > 0: block-wise variance
                                   redistribution (DESIGN R16): rotate only the dimensions of the b
                                   subspaces of largest sample variance, R = I elsewhere */
+    int32_t adaptive_subspaces; /* 0: M equal subspaces; 1: adaptive subspace decomposition
+                                   (DESIGN R18): contiguous even widths cut where the stored
+                                   vectors' running per-dimension variance (CEV sample) first reaches
+                                   j/M of the total, halves of equal width; ignored if subspace_widths */
+    const int32_t *subspace_widths; /* NULL, or M even widths >= 2 summing to padded_D (host memory,
+                                   read during the build call only): subspace m covers dims
+                                   [sum_{j<m} w_j, sum_{j<=m} w_j), halves of w_m / 2; required with
+                                   injected codebooks of a non-equal split.  Codebook rows keep the
+                                   stride dh = max w_m / 2, zero beyond the half's width.  Not
+                                   supported by crisp_build_model (equal split only). */
 } crisp_params;
 
 typedef struct {
@@ -93,6 +103,7 @@ typedef struct {
     double slice_hint;  /* expected ids per activated slice and 4096-id warp sub-block: >= 8 selects the
                            warp-owned collision-count kernel, else the CTA-flattened one (env CRISP_COUNT_KERNEL) */
     int32_t rotation_block; /* subspaces of a block-wise rotation (0: global or none) */
+    int32_t adaptive;       /* 1 if the subspace widths are not the equal split (R18) */
 } crisp_index_info_t;
 
 /* Host buffers filled by crisp_export (any may be NULL to skip). */
@@ -105,6 +116,7 @@ typedef struct {
     int32_t *ids;      /* M x N CSR ids, local */
     uint64_t *codes;   /* N x ceil(padded_D/64) binary codes */
     int64_t *cell_sizes; /* M x K^2 sizes used for budgets (global after crisp_set_global_cell_sizes) */
+    int32_t *subspace_widths; /* M: the subspace widths in effect (equal: 2 dh each) */
 } crisp_export_t;
 
 /* Host buffers filled by crisp_search_trace (any may be NULL).  Stage outputs of

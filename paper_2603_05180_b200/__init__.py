@@ -35,6 +35,7 @@ class Params(C.Structure):
         ("kmeans_iters", C.c_int32), ("kmeans_sample", C.c_int64), ("seed", C.c_uint64), ("device", C.c_int32),
         ("budget_ratio", C.c_double), ("budget", C.c_int64), ("min_collision_ratio", C.c_double), ("tau", C.c_int32),
         ("patience_factor", C.c_int32), ("workspace_bytes", C.c_int64), ("rotation_block", C.c_int32),
+        ("adaptive_subspaces", C.c_int32), ("subspace_widths", C.c_void_p),
     ]
 
 
@@ -45,11 +46,13 @@ class Info(C.Structure):
         ("rotated", C.c_int32), ("cev", C.c_double), ("budget", C.c_int64), ("tau", C.c_int32),
         ("patience_factor", C.c_int32), ("block_ids", C.c_int32), ("n_blocks", C.c_int32), ("hbm_bytes", C.c_int64),
         ("logical_bytes", C.c_int64), ("slice_hint", C.c_double), ("rotation_block", C.c_int32),
+        ("adaptive", C.c_int32),
     ]
 
 
 class Export(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("R", "X", "codebooks", "cells", "offsets", "ids", "codes", "cell_sizes")]
+    _fields_ = [(n, C.c_void_p) for n in ("R", "X", "codebooks", "cells", "offsets", "ids", "codes", "cell_sizes",
+                                          "subspace_widths")]
 
 
 class Trace(C.Structure):
@@ -237,8 +240,15 @@ class Index:
     @staticmethod
     def build(data, M: int, R=None, codebooks=None, gid_base: int | None = None, **params) -> "Index":
         """crisp_build (or crisp_build_with when R/codebooks are given, or
-        crisp_build_shard when gid_base is given)."""
+        crisp_build_shard when gid_base is given).  subspace_widths: M even
+        widths summing to the padded dimensionality (R18), or None."""
+        widths = params.pop("subspace_widths", None)
         p = default_params(M=M, **params)
+        if widths is not None:
+            wv = np.ascontiguousarray(widths, dtype=np.int32)
+            if wv.shape != (M,):
+                raise CrispError(f"subspace_widths must hold M={M} widths")
+            p.subspace_widths = wv.ctypes.data  # wv stays alive for the call
         x = _host(data, np.float32)
         N, D = int(x.shape[0]), int(x.shape[1])
         out = C.c_void_p()
@@ -409,7 +419,7 @@ class Index:
         e = dict(X=np.zeros((N, Dp), np.float32), codebooks=np.zeros((M, 2, K, dh), np.float32),
                  cells=np.zeros((M, N), np.int32), offsets=np.zeros((M, K * K + 1), np.int64),
                  ids=np.zeros((M, N), np.int32), codes=np.zeros((N, W), np.uint64),
-                 cell_sizes=np.zeros((M, K * K), np.int64))
+                 cell_sizes=np.zeros((M, K * K), np.int64), subspace_widths=np.zeros(M, np.int32))
         if i["rotated"]:
             e["R"] = np.zeros((Dp, Dp), np.float32)
         ex = Export(**{n: e[n].ctypes.data for n in e})

@@ -117,6 +117,7 @@ static void free_index(crisp_index *ix) {
     cudaFree(ix->C8);
     cudaFree(ix->c8meta);
     cudaFree(ix->mu);
+    cudaFree(ix->hoff);
     delete ix;
 }
 
@@ -153,6 +154,10 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
     ix->Wp = (ix->W + 7) / 8 * 8;
     CRISP_CHECK(p->rotation_block >= 0 && p->rotation_block <= p->M, "rotation_block must be in [0, M]");
     ix->rot_block = p->rotation_block;
+    if (p->subspace_widths) set_subspace_widths(ix, p->subspace_widths);
+    else ix->adaptive_req = p->adaptive_subspaces != 0;
+    CRISP_CHECK(!(ix->rot_block > 0 && (ix->adaptive_req || !ix->hoff_h.empty())),
+                "rotation_block with adaptive subspaces is not supported");
     ix->BS = block_ids_for(N);
     ix->NB = (int32_t)((N + ix->BS - 1) / ix->BS);
     ix->SBW = ix->BS / 8;
@@ -165,7 +170,7 @@ static crisp_index *new_index(int64_t N, int32_t D, const crisp_params *p) {
     try {
         const int64_t KK = (int64_t)ix->K * ix->K;
         ix->X = dalloc<float>(ix, (size_t)N * ix->pitch);
-        ix->cb = dalloc<float>(ix, (size_t)ix->M * 2 * ix->K * ix->dh);
+        if (!ix->adaptive_req) ix->cb = dalloc<float>(ix, (size_t)ix->M * 2 * ix->K * ix->dh);  // else: in the build
         ix->cells = dalloc<int32_t>(ix, (size_t)ix->M * N);
         ix->ids = dalloc<int32_t>(ix, (size_t)ix->M * N + 4);  // +4: k_count_frag's 16-byte loads of the last quad
         ix->off2 = dalloc<int32_t>(ix, (size_t)ix->M * KK * (ix->NB + 1));
@@ -202,6 +207,8 @@ static crisp_status build_common(const float *data, int64_t N, int64_t gid_base,
         CRISP_CHECK(out != nullptr, "out is NULL");
         CRISP_CHECK(data != nullptr, "data is NULL");
         if (inject) CRISP_CHECK(cb != nullptr, "codebooks are NULL");
+        CRISP_CHECK(!(inject && p->adaptive_subspaces && !p->subspace_widths),
+                    "injected codebooks of an adaptive split need subspace_widths");
         ix = new_index(N, D, p);
         ix->gid_base = gid_base;
         // device inputs may still be in flight on the caller's streams (the build
@@ -310,6 +317,7 @@ crisp_status crisp_build_model(const float *cev_rows, int64_t n_cev, const float
     try {
         CRISP_CHECK(p && km_rows && codebooks_out && rotated_out, "NULL argument");
         CRISP_CHECK(n_km >= 1 && n_cev >= 0 && D >= 1, "bad sizes");
+        CRISP_CHECK(!p->adaptive_subspaces && !p->subspace_widths, "crisp_build_model takes the equal split only");
         CRISP_CHECK(n_cev < 2 || cev_rows != nullptr, "cev_rows is NULL");
         ix = new_index(n_km, D, p);
         CRISP_CUDA(cudaDeviceSynchronize());
@@ -488,6 +496,7 @@ crisp_status crisp_index_info(const crisp_index *ix, crisp_index_info_t *o) {
     o->n_blocks = ix->NB;
     o->hbm_bytes = ix->hbm_bytes;
     o->rotation_block = ix->rotated ? ix->rot_block : 0;
+    o->adaptive = ix->hoff_h.empty() ? 0 : 1;
     const int64_t KK = (int64_t)ix->K * ix->K;
     o->logical_bytes = 4 * ix->N * ix->Dp + 4 * (int64_t)ix->M * ix->N + 8 * (int64_t)ix->M * (KK + 1) +
                        4 * (int64_t)ix->M * 2 * ix->K * ix->dh + 8 * (int64_t)ix->W * ix->N +
@@ -732,6 +741,9 @@ crisp_status crisp_export(const crisp_index *ix, crisp_export_t *o) {
             CRISP_CUDA(cudaMemcpy(g.data(), ix->gsize, g.size() * 4, cudaMemcpyDeviceToHost));
             for (size_t i = 0; i < g.size(); i++) o->cell_sizes[i] = g[i];
         }
+        if (o->subspace_widths)
+            for (int m = 0; m < ix->M; m++)
+                o->subspace_widths[m] = ix->hoff_h.empty() ? 2 * ix->dh : ix->hoff_h[2 * m + 2] - ix->hoff_h[2 * m];
         return CRISP_OK;
     } catch (Err &e) {
         return e.st;

@@ -683,7 +683,7 @@ constexpr int AS_T = 128;
 __global__ void __launch_bounds__(AS_T) k_argmin_staged(const float *__restrict__ P, int64_t n, int64_t ldp, int dh,
                                                         int K, const float *__restrict__ C,
                                                         const int *__restrict__ done, int32_t *__restrict__ a,
-                                                        double *__restrict__ dmin) {
+                                                        double *__restrict__ dmin, const int32_t *__restrict__ hoff) {
     extern __shared__ __align__(16) double ssm[];
     const int h = blockIdx.y;
     if (done && done[h]) return;
@@ -694,9 +694,13 @@ __global__ void __launch_bounds__(AS_T) k_argmin_staged(const float *__restrict_
     const float *Ch = C + (int64_t)h * K * dh;
     for (int i = tid; i < K * dh; i += AS_T) Cs[i] = (double)Ch[i];
     const int np = (int)(n - p0 < AS_T ? n - p0 : AS_T);
+    // half h's dims (hoff: [hoff[h], hoff[h+1]), R18), zero beyond its width up to dh: the
+    // zero terms of the centroids' padded rows add exact zeros to each dist64 chain
+    const int64_t ho = hoff ? hoff[h] : (int64_t)h * dh;
+    const int hw = hoff ? hoff[h + 1] - hoff[h] : dh;
     for (int i = tid; i < np * dh; i += AS_T) {
         const int pt = i / dh, d = i - pt * dh;
-        Xs[d * (AS_T + 1) + pt] = P[(p0 + pt) * ldp + (int64_t)h * dh + d];
+        Xs[d * (AS_T + 1) + pt] = d < hw ? P[(p0 + pt) * ldp + ho + d] : 0.0f;
     }
     __syncthreads();
     if (tid >= np) return;
@@ -735,7 +739,8 @@ __global__ void k_cells_from_halves(const int32_t *__restrict__ ah, int64_t N, i
 }
 static int argmin_smem(int K, int dh) { return K * dh * 8 + dh * (AS_T + 1) * 4; }
 static void argmin_staged(const float *P, int64_t n, int64_t ldp, int dh, int K, int nh, const float *C,
-                          const int *done, int32_t *a, double *dmin, cudaStream_t s) {
+                          const int *done, int32_t *a, double *dmin, cudaStream_t s,
+                          const int32_t *hoff = nullptr) {
     const int sm = argmin_smem(K, dh);
     static int attr = 0;
     if (sm > attr) {
@@ -743,7 +748,7 @@ static void argmin_staged(const float *P, int64_t n, int64_t ldp, int dh, int K,
         attr = sm;
     }
     dim3 g((unsigned)((n + AS_T - 1) / AS_T), (unsigned)nh);
-    k_argmin_staged<<<g, AS_T, sm, s>>>(P, n, ldp, dh, K, C, done, a, dmin);
+    k_argmin_staged<<<g, AS_T, sm, s>>>(P, n, ldp, dh, K, C, done, a, dmin, hoff);
     CRISP_LAUNCH();
 }
 __global__ void k_km_compare(int64_t n, int nh, const int32_t *a, const int32_t *aold, const int *done, int *diff) {
@@ -835,9 +840,22 @@ __global__ void k_km_copy(int64_t n, int nh, const int *active, const int32_t *a
     if (active[e / n]) aold[e] = a[e];
 }
 
+// the k-means sample of an adaptive split (R18): row r holds half h's dims in [h dh, h dh + w_h),
+// zeros after, so every k-means kernel runs on equal dh-wide halves (zero dims add exact zeros)
+__global__ void k_gather_halves(const float *__restrict__ X, int64_t ld, const int32_t *__restrict__ rows, int64_t n,
+                                const int32_t *__restrict__ hoff, int nh, int dh, float *__restrict__ S) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rw = (int64_t)nh * dh;
+    if (e >= n * rw) return;
+    const int64_t r = e / rw;
+    const int c = (int)(e - r * rw), h = c / dh, t = c - h * dh;
+    S[e] = t < hoff[h + 1] - hoff[h] ? X[(int64_t)rows[r] * ld + hoff[h] + t] : 0.0f;
+}
+
 static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, uint64_t seed, cudaStream_t s) {
     const int64_t N = ix->N;
-    const int Dp = ix->Dp, dh = ix->dh, K = ix->K, nh = 2 * ix->M;
+    const int dh = ix->dh, K = ix->K, nh = 2 * ix->M;
+    const int Dp = ix->hoff ? nh * dh : ix->Dp;  // sample row width
     int64_t n = std::min<int64_t>(N, std::max<int64_t>(1, kmeans_sample));
     Scratch sc;
     int32_t *rows = sc.alloc<int32_t>(n);
@@ -847,7 +865,10 @@ static void train_codebooks(crisp_index *ix, int64_t kmeans_sample, int iters, u
     {
         struct G {
         };
-        k_gather_rows<<<nblk(n * Dp, 256), 256, 0, s>>>(ix->X, ix->pitch, rows, n, Dp, S);
+        if (ix->hoff)
+            k_gather_halves<<<nblk(n * Dp, 256), 256, 0, s>>>(ix->X, ix->pitch, rows, n, ix->hoff, nh, dh, S);
+        else
+            k_gather_rows<<<nblk(n * Dp, 256), 256, 0, s>>>(ix->X, ix->pitch, rows, n, Dp, S);
         CRISP_LAUNCH();
     }
     float *C = ix->cb;
@@ -1050,6 +1071,59 @@ static void make_block_rotation(crisp_index *ix, const std::vector<double> &var,
     CRISP_CUDA(cudaStreamSynchronize(s));
 }
 
+// ---------------------------------------------------------------------------
+// Adaptive subspace decomposition (reading R18).  With S(e) the sum of the
+// per-dimension variances v_i for i < e (ascending, fp64) and T = S(Dp), cut j (1 <= j < M)
+// is the smallest even e in [c_{j-1} + 2, Dp - 2 (M - j)] with S(e) >= T j / M, else the
+// upper end; the widths c_j - c_{j-1} put few dimensions where the variance is high.
+std::vector<int32_t> adaptive_widths(const std::vector<double> &var, int M, int Dp) {
+    std::vector<double> S((size_t)Dp + 1, 0.0);
+    for (int i = 0; i < Dp; i++) S[i + 1] = S[i] + (i < (int)var.size() ? var[i] : 0.0);
+    const double T = S[Dp];
+    std::vector<int32_t> w;
+    int prev = 0;
+    for (int j = 1; j < M; j++) {
+        const int hi = Dp - 2 * (M - j);
+        const double target = (T * j) / M;
+        int e = prev + 2;
+        while (e < hi && S[e] < target) e += 2;
+        w.push_back(e - prev);
+        prev = e;
+    }
+    w.push_back(Dp - prev);
+    return w;
+}
+
+void set_subspace_widths(crisp_index *ix, const int32_t *widths) {
+    const int M = ix->M;
+    int64_t sum = 0;
+    int wmax = 0;
+    bool equal = true;
+    for (int m = 0; m < M; m++) {
+        CRISP_CHECK(widths[m] >= 2 && widths[m] % 2 == 0, "subspace widths must be even and >= 2");
+        sum += widths[m];
+        wmax = std::max(wmax, (int)widths[m]);
+        equal = equal && widths[m] == widths[0];
+    }
+    CRISP_CHECK(sum == ix->Dp, "subspace widths must sum to padded_D");
+    cudaFree(ix->hoff);
+    ix->hoff = nullptr;
+    ix->hoff_h.clear();
+    if (equal) return;  // the equal split: dh = Dp / 2M as set
+    ix->hoff_h.resize((size_t)2 * M + 1);
+    int o = 0;
+    for (int m = 0; m < M; m++) {
+        ix->hoff_h[2 * m] = o;
+        ix->hoff_h[2 * m + 1] = o + widths[m] / 2;
+        o += widths[m];
+    }
+    ix->hoff_h[2 * M] = o;
+    ix->dh = wmax / 2;
+    CRISP_CUDA(cudaMalloc(&ix->hoff, ix->hoff_h.size() * 4));
+    CRISP_CUDA(cudaMemcpy(ix->hoff, ix->hoff_h.data(), ix->hoff_h.size() * 4, cudaMemcpyHostToDevice));
+    ix->hbm_bytes += (int64_t)ix->hoff_h.size() * 4;
+}
+
 void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, const float *cb_inj,
                  int64_t kmeans_sample, int32_t kmeans_iters, int32_t rotation_mode, float tau_cev, uint64_t seed,
                  cudaStream_t s, const double *cev_given, const std::vector<double> *var_given) {
@@ -1094,6 +1168,18 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
         rotate_in_place(ix, s);
         ix->rotated = 1;
     }
+    if (ix->adaptive_req) {
+        // R18: widths from the per-dimension variances of the stored vectors on the CEV sample
+        // (those of X when not rotated, zero on the padding; else recomputed on X')
+        std::vector<double> v2;
+        if (ix->rotated) compute_cev(ix->X, N, ix->pitch, ix->Dp, seed, s, &v2);
+        const std::vector<int32_t> w = adaptive_widths(ix->rotated ? v2 : var, ix->M, ix->Dp);
+        set_subspace_widths(ix, w.data());
+        ix->adaptive_req = 0;
+        ix->cb = (float *)nullptr;
+        CRISP_CUDA(cudaMalloc(&ix->cb, (size_t)ix->M * 2 * ix->K * ix->dh * 4));
+        ix->hbm_bytes += (int64_t)ix->M * 2 * ix->K * ix->dh * 4;
+    }
     if (cb_inj) {
         CRISP_CUDA(cudaMemcpyAsync(ix->cb, cb_inj, (size_t)ix->M * 2 * ix->K * ix->dh * 4, cudaMemcpyDefault, s));
     } else {
@@ -1102,7 +1188,7 @@ void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, con
     {
         int32_t *ah = nullptr;  // per half-subspace argmin, then cells = i K + j
         CRISP_CUDA(cudaMallocAsync(&ah, (size_t)N * 2 * ix->M * 4, s));
-        argmin_staged(ix->X, N, ix->pitch, ix->dh, ix->K, 2 * ix->M, ix->cb, nullptr, ah, nullptr, s);
+        argmin_staged(ix->X, N, ix->pitch, ix->dh, ix->K, 2 * ix->M, ix->cb, nullptr, ah, nullptr, s, ix->hoff);
         k_cells_from_halves<<<nblk(N * ix->M, 256), 256, 0, s>>>(ah, N, ix->M, ix->K, ix->cells);
         CRISP_LAUNCH();
         CRISP_CUDA(cudaFreeAsync(ah, s));

@@ -63,6 +63,12 @@ struct crisp_index {
     int32_t Wp = 0;            // code row stride in words: W rounded up to 8 (64-B rows, 16-B loads)
     int32_t rotated = 0;       // 1: global rotation; 2: block-wise (R16)
     int32_t rot_block = 0;     // block-wise rotation over this many subspaces (0: global)
+    // adaptive subspace decomposition (R18): half h covers dims [hoff_h[h], hoff_h[h+1]);
+    // empty = the equal split (half h at h*dh).  dh is then the largest half width (the codebook
+    // row stride; rows are zero beyond their half's width)
+    std::vector<int32_t> hoff_h;
+    int32_t *hoff = nullptr;   // device copy of hoff_h (nullptr: equal split)
+    int32_t adaptive_req = 0;  // widths from the variance rule, chosen during the build
     double cev = 0.0;
     float *X = nullptr;        // N x pitch, stored (rotated) vectors, zero padded
     float *R = nullptr;        // Dp x Dp row-major (rotated only)
@@ -114,6 +120,11 @@ int64_t decimal_ceil(double ratio, int64_t n);
 void cell_size_maxima(crisp_index *ix, const int32_t *sizes_host);
 
 // build steps (build.cu)
+// adaptive subspace decomposition (R18): validate M even widths summing to Dp and
+// set the half offsets (an equal split leaves the index on the equal-split path)
+void set_subspace_widths(crisp_index *ix, const int32_t *widths);
+// the width rule on per-dimension variances (zero beyond var.size())
+std::vector<int32_t> adaptive_widths(const std::vector<double> &var, int M, int Dp);
 void build_index(crisp_index *ix, const float *data_dev, const float *R_inj, const float *cb_inj, int64_t kmeans_sample,
                  int32_t kmeans_iters, int32_t rotation_mode, float tau_cev, uint64_t seed, cudaStream_t s,
                  const double *cev_given = nullptr, const std::vector<double> *var_given = nullptr);

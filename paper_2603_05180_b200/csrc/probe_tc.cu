@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(SB_THREADS) k_screen_tc(const __grid_constant_
                                                           const float *__restrict__ qrot, int pitch, int64_t q0,
                                                           int64_t Qc, int K, int dh, int nhalf,
                                                           const double *__restrict__ cn2,
-                                                          ScreenOut *__restrict__ scr, int RQ, int dbg) {
+                                                          ScreenOut *__restrict__ scr, int RQ, int dbg,
+                                                          const int32_t *__restrict__ hoff) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     // 1024-byte aligned (the 128-byte swizzle atoms), keeping the shared-memory provenance
     unsigned char *base = smraw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smraw) & 1023u)) & 1023u);
@@ -99,6 +100,9 @@ __global__ void __launch_bounds__(SB_THREADS) k_screen_tc(const __grid_constant_
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int hs = blockIdx.x;                       // half-subspace 2m + h
     const int64_t m0 = q0 + (int64_t)blockIdx.y * SB_M;
+    // the half's dims: [hoff[hs], hoff[hs] + hw) (R18), else [hs dh, (hs + 1) dh); query dims read
+    // past hw meet zero codebook entries (exact zero products)
+    const int ho = hoff ? hoff[hs] : hs * dh, hw = hoff ? hoff[hs + 1] - hoff[hs] : dh;
     if (tid == 0) {
         tcu::mbar_init(&full, 1);
         tcu::mbar_init(&done, 1);
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_screen_tc(const __grid_constant_
     if (tid == 0 && !(dbg & 4)) {
         tcu::mbar_expect_tx(&full, (uint32_t)(NKB * (SB_M + SB_N) * 128));
         for (int kb = 0; kb < NKB; kb++) {
-            tcu::tma_load_2d(As + kb * SB_M * 128, &mapQ, hs * dh + kb * 32, (int)m0, &full);
+            tcu::tma_load_2d(As + kb * SB_M * 128, &mapQ, ho + kb * 32, (int)m0, &full);
             tcu::tma_load_2d(Bs + kb * SB_N * 128, &mapC, kb * 32, hs * SB_N, &full);
         }
     }
@@ -147,8 +151,8 @@ __global__ void __launch_bounds__(SB_THREADS) k_screen_tc(const __grid_constant_
     const bool live = q < Qc;
     double nq = 0.0;
     if (live) {
-        const float *qr = qrot + q * pitch + (int64_t)hs * dh;
-        for (int j = 0; j < dh; j++) {
+        const float *qr = qrot + q * pitch + ho;
+        for (int j = 0; j < hw; j++) {
             const double v = (double)qr[j];
             nq = __fma_rn(v, v, nq);
         }
@@ -233,7 +237,9 @@ bool screen_supported(const crisp_index *ix) {
     // K <= 64 centroids per half (one N = 64 tile), d_h <= 128 (four 32-float k-blocks), a
     // 16-byte row pitch (TMA strides)
     // and 16-byte-aligned half-subspace slices (d_h a multiple of 4: TMA box starts)
-    return ix->K <= SB_N && ix->dh <= 128 && (ix->dh % 4) == 0 && (ix->pitch % 4) == 0;
+    bool ok = ix->K <= SB_N && ix->dh <= 128 && (ix->dh % 4) == 0 && (ix->pitch % 4) == 0;
+    for (int32_t o : ix->hoff_h) ok = ok && (o % 4) == 0;  // adaptive widths (R18): aligned half starts
+    return ok;
 }
 
 // intervals [lo, hi] of dist64(q'_{m,h}, C_{m,h,c}) for queries [q0, q1) of qrot:
@@ -262,7 +268,8 @@ void screen_halves(crisp_index *ix, const float *qrot, int64_t q0, int64_t q1, S
     dim3 g((unsigned)nh, (unsigned)((q1 - q0 + SB_M - 1) / SB_M));
     const int dbg = getenv("CRISP_SCREEN_DEBUG") ? atoi(getenv("CRISP_SCREEN_DEBUG")) : 0;  // bisection knobs
 #define CRISP_SCR(NK)                                                                                              \
-    k_screen_tc<NK><<<g, SB_THREADS, smem, s>>>(mQ, mC, qrot, ix->pitch, q0, q1, ix->K, ix->dh, nh, ix->cn2, scr, RQ, dbg)
+    k_screen_tc<NK><<<g, SB_THREADS, smem, s>>>(mQ, mC, qrot, ix->pitch, q0, q1, ix->K, ix->dh, nh, ix->cn2, scr, RQ, dbg, \
+                                                ix->hoff)
     if (NKB == 1) CRISP_SCR(1);
     else if (NKB == 2) CRISP_SCR(2);
     else if (NKB == 3) CRISP_SCR(3);

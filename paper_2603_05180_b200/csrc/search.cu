@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
                                                     int wk, uint32_t *__restrict__ act, int32_t *__restrict__ act_len,
                                                     int64_t *__restrict__ retrieved, int qpw, int smem_cb,
                                                     const ScreenOut *__restrict__ scr,
-                                                    unsigned long long *__restrict__ probe_stats) {
+                                                    unsigned long long *__restrict__ probe_stats,
+                                                    const int32_t *__restrict__ hoff) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int KK = K * K;
     const int m = blockIdx.y;
@@ -188,8 +189,15 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
     for (int qi = 0; qi < qpw; qi++) {
         const int64_t q = q0 + ((int64_t)blockIdx.x * WARPS + warp) * qpw + qi;  // queries [q0, Qc)
         if (q >= Qc) break;
-        const float *qm = qrot + q * pitch + (int64_t)m * 2 * dh;
-        for (int i = lane; i < 2 * dh; i += 32) qs[i] = (double)qm[i];
+        if (hoff) {  // adaptive widths (R18): each half's dims, zero beyond its width (exact zero terms)
+            for (int i = lane; i < 2 * dh; i += 32) {
+                const int h = 2 * m + (i >= dh), t = i - (i >= dh ? dh : 0);
+                qs[i] = t < hoff[h + 1] - hoff[h] ? (double)qrot[q * pitch + hoff[h] + t] : 0.0;
+            }
+        } else {
+            const float *qm = qrot + q * pitch + (int64_t)m * 2 * dh;
+            for (int i = lane; i < 2 * dh; i += 32) qs[i] = (double)qm[i];
+        }
         __syncwarp();
         if (scr) {
             // a1 screened (probe_tc.cu): per half, t = the RQ-th smallest certified upper bound
@@ -4223,7 +4231,7 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
         k_probe<<<g, THREADS, w.probe_smem, s>>>(w.qrot, pitch, r0, r1, ix->cb, M, K, ix->dh, ix->gsize, w.probe_gs,
                                                  ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr,
                                                  w.probe_qpw, w.probe_cb, w.scr,
-                                                 g_timing ? d_probe_stats_ptr() : nullptr);
+                                                 g_timing ? d_probe_stats_ptr() : nullptr, ix->hoff);
         CRISP_LAUNCH();
         g_launches++;
     };

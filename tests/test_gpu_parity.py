@@ -773,3 +773,85 @@ def test_pipelined_chunks_equal_one_pass(crisp, monkeypatch, mode, parts):
     sample = np.arange(0, 4100, 41)
     r_ids, r_d, _ = oracle.search(ox, Qv[sample], 10, mode, 300, 3, patience_factor=40)
     assert_topk_parity(outs[1][0][sample], outs[1][1][sample], r_ids, r_d, f"pipe={parts}")
+
+
+def _skewed(seed, N, D, Q, decay=10.0):
+    r = np.random.default_rng(seed)
+    scale = np.exp(-np.arange(D) / decay) * 4.0 + 0.05
+    X = (r.standard_normal((N, D)) * scale).astype(np.float32)
+    Qv = (r.standard_normal((Q, D)) * scale).astype(np.float32)
+    return X, Qv
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_adaptive_subspaces_f4(crisp, mode):
+    """f4, adaptive subspace decomposition (DESIGN R18): on a decaying
+    spectrum (unrotated) the GPU build picks the oracle's widths (the rule on
+    the CEV sample's variances, same sequential fp64 order), trains the same
+    codebooks on the zero-padded halves, and assigns, lists and searches
+    exactly as the oracle's variable-width index (a1 on the exact probe: the
+    rule's half starts are not 16-byte aligned)."""
+    X, Qv = _skewed(21, 15000, 96, 48)
+    M = 6
+    ox = oracle.build(X, M, K=12, rotation_mode=0, kmeans_iters=5, seed=4, adaptive_subspaces=True)
+    w = (ox["hoff"][2::2] - ox["hoff"][:-1:2]).tolist()
+    assert w[0] < 16 < w[-1], w
+    ix = crisp.Index.build(X, M, K=12, rotation=0, kmeans_iters=5, seed=4, adaptive_subspaces=1)
+    info, e = ix.info(), ix.export()
+    assert info["adaptive"] == 1 and info["dh"] == ox["dh"]
+    assert e["subspace_widths"].tolist() == w
+    assert np.array_equal(e["codebooks"], ox["cb"]), "k-means codebooks of the variable halves"
+    compare_index(ix, ox)
+    B, tau, k = 900, 2, 10
+    ix.set_search_params(budget=B, tau=tau, patience_factor=4)
+    ids, d, t = ix.trace(Qv, k, mode)
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, mode, B, tau, patience_factor=4, trace=True)
+    compare_trace(t, ot, mode, X.shape[0])
+    assert_topk_parity(ids, d, r_ids, r_d, "adaptive widths")
+    ids2, d2 = ix.search(Qv, k, mode)
+    assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_adaptive_widths_given_screened_and_injected(crisp, mode):
+    """Given widths (8, 8, 16, 32): half starts at multiples of 4, so a1 runs the
+    tensor-core screen with per-half TMA offsets; the GPU's own build and the
+    oracle's codebooks injected (crisp_build_with + subspace_widths) both match
+    the oracle stage by stage."""
+    import torch
+
+    X, Qv = _skewed(22, 12000, 64, 40, decay=14.0)
+    widths = [8, 8, 16, 32]
+    ox = oracle.build(X, 4, K=16, rotation_mode=0, kmeans_iters=4, seed=6, subspace_widths=widths)
+    assert ox["hoff"].tolist() == [0, 4, 8, 12, 16, 24, 32, 48, 64] and ox["dh"] == 16
+    own = crisp.Index.build(X, 4, K=16, rotation=0, kmeans_iters=4, seed=6, subspace_widths=widths)
+    assert np.array_equal(own.export()["codebooks"], ox["cb"])
+    compare_index(own, ox)
+    own.free()
+    ix = crisp.Index.build(X, 4, codebooks=ox["cb"], K=16, subspace_widths=widths)
+    compare_index(ix, ox)
+    B, tau, k = 700, 2, 10
+    ix.set_search_params(budget=B, tau=tau, patience_factor=4)
+    crisp.set_stage_timing(True)
+    crisp.search_counters(reset=True)
+    ids, d, t = ix.trace(Qv, k, mode)
+    cnt = crisp.search_counters(reset=True)
+    crisp.set_stage_timing(False)
+    torch.cuda.synchronize()
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, mode, B, tau, patience_factor=4, trace=True)
+    compare_trace(t, ot, mode, X.shape[0])
+    assert_topk_parity(ids, d, r_ids, r_d, "given widths")
+    assert cnt["probe_exact_half_distances"] < 40 * 4 * 2 * 16, "the screen must run (and save exact distances)"
+
+
+def test_adaptive_subspaces_rotated_rule_on_stored_vectors(crisp):
+    """Rotated + adaptive: the widths come from the variances of the stored
+    X' (here teacher-forced: the oracle rule on the GPU's exported X', the CEV
+    sample's sequential fp64 variances) and the build is self-consistent."""
+    X, _ = _skewed(23, 8000, 64, 1, decay=6.0)
+    ix = crisp.Index.build(X, 4, K=8, rotation=1, kmeans_iters=3, seed=2, adaptive_subspaces=1)
+    e = ix.export()
+    w = oracle.adaptive_widths(oracle.dim_variances(e["X"], 2), 4, 64)
+    assert e["subspace_widths"].tolist() == w
+    ox = oracle.build(e["X"], 4, K=8, rotation_mode=0, codebooks=e["codebooks"], seed=2, subspace_widths=w)
+    assert np.array_equal(e["cells"], ox["cells"]) and np.array_equal(e["ids"], ox["ids"])
