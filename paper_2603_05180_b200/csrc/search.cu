@@ -890,14 +890,18 @@ __global__ void __launch_bounds__(THREADS, HAM ? 4 : 5) k_count_warp(const uint3
 // (one 16-byte load), finds its fragment with a 5-step shuffle search over a
 // sliding window of 32 fragments held in the lanes, masks the edge words
 // outside the fragment, and adds the weight w (Alg. 1 l.10-12) of each of its
-// ids with a shared atomic on the counter's word.  The same id can recur only
-// across subspaces (CSR partition property) and the atomics order
-// those, so no barrier separates subspaces.  V only grows, by 1 or 2, so x
-// enters C = {x : V[x] >= tau} (Alg. 1 l.18) exactly at the increment that
-// lifts its count from below tau to tau or more; that increment sets x's bit
-// in the candidate bitmap, which the CTA finally writes out in ascending id.
-// (Measured alternative: fire-and-forget reductions plus a SWAR scan of the
-// counters at the end -- cfg4 count 26.1 ms against 23.4 ms.)
+// ids with a shared reduction on the counter's word.  The same id can recur only
+// across subspaces (CSR partition property) and the reductions order
+// those, so no barrier separates subspaces.  After the last chunk a SWAR scan
+// of the counters sets the bit of every x with V[x] >= tau (C, Alg. 1 l.18) in
+// the candidate bitmap, which the CTA finally writes out in ascending id.
+// (CRISP_COUNT_SWAR=0: atomics with return; V only grows, by 1 or 2, so x enters
+// C exactly at the increment that lifts its count from below tau to tau or
+// more, and that increment sets x's bit.  Measured in round 2: 17.1 / 86.1 /
+// 32.4 ms at cfg4/3/5 against 16.9 / 81.2 / 29.5 ms with the scan.  A variant
+// that expanded each chunk into a table of one descriptor per quad instead of
+// the shuffle search measured 18.4 ms at cfg4: the expansion's imbalanced
+// per-thread loops cost what the search saved; profiles/r02_ncu_count_cfg4_s3.json.)
 // ---------------------------------------------------------------------------
 constexpr int CF_CAP = CRISP_CF_CAP;  // fragments staged per chunk
 #ifndef CRISP_COUNT_LAG
@@ -931,6 +935,9 @@ __device__ __forceinline__ uint32_t atom_add_sh_nc(uint32_t a, uint32_t v) {
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v));
     return old;
 }
+__device__ __forceinline__ void red_add_sh_nc(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
 __device__ __forceinline__ void red_add_sh(uint32_t a, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -960,7 +967,7 @@ __global__ void k_act_rows(const uint32_t *__restrict__ act, const int32_t *__re
     if (lane == 0) etot[q] = base;
 }
 
-template <int CF_WARPS>
+template <int CF_WARPS, bool SWAR = false>
 __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(const uint32_t *__restrict__ erow,
                                                                const int32_t *__restrict__ etot, int M, int KK,
                                                                const int32_t *__restrict__ off2, int NB, int F,
@@ -1138,9 +1145,11 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                     const bool ok = q0 + e >= lo && q0 + e < hi;
                     inc[e] = ok ? w : 0u;
                     const uint32_t off = xs[e] - bbase;
-                    ov[e] = atom_add_sh_nc(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << ((off & 3u) * 8u));
+                    if (SWAR) red_add_sh_nc(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << ((off & 3u) * 8u));
+                    else ov[e] = atom_add_sh_nc(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << ((off & 3u) * 8u));
                 }
-                if (CF_LAG) {
+                if (SWAR) {
+                } else if (CF_LAG) {
                     cross(pov, pxs, pinc);
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
@@ -1152,9 +1161,29 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                     cross(ov, xs, inc);
                 }
             }
-            if (CF_LAG) cross(pov, pxs, pinc);
+            if (CF_LAG && !SWAR) cross(pov, pxs, pinc);
         }
         __syncthreads();  // the chunk's table is re-staged next
+    }
+    if (SWAR) {
+        // CRISP_COUNT_SWAR=1: the counts above are fire-and-forget reductions; C = {x : V[x] >= tau}
+        // (Alg. 1 l.18) from the final counters, 32 per bitmap word: bit 7 of ((c | 0x80) - tau)
+        // is [c >= tau] for c < 128 (M < 64), else a per-byte compare; one multiply gathers a
+        // word's four flags
+        const uint32_t t4 = (uint32_t)tau * 0x01010101u;
+        for (int wi = tid; wi < BF / 32; wi += CF_THREADS) {
+            const uint4 a = ((const uint4 *)cw)[2 * wi], b = ((const uint4 *)cw)[2 * wi + 1];
+            const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint32_t word = 0u;
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                const uint32_t f = M < 64 ? (((v[t] | 0x80808080u) - t4) >> 7) & 0x01010101u
+                                          : __vcmpgeu4(v[t], t4) & 0x01010101u;
+                word |= ((f * 0x10204080u) >> 28) << (4 * t);
+            }
+            bm[wi] = word;
+        }
+        __syncthreads();
     }
     // a4: C in ascending id from the crossing bitmap; each warp compacts a contiguous word range
     const int nwords = BF / 32, wpw = nwords / CF_WARPS;
@@ -3886,6 +3915,8 @@ static void set_attrs() {
     CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CRISP_CUDA(cudaFuncSetAttribute(k_count_frag<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CRISP_CUDA(cudaFuncSetAttribute(k_count_warp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -4301,16 +4332,22 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
                     w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
                     w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp,
                     hb, w.ghist);
-            else if (w.CF * ix->BS > 65536)
-                k_count_frag<32><<<dim3((unsigned)w.NS, (unsigned)qn), 1024, countf_smem(ix->BS * w.CF), s>>>(
-                    w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
-                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp,
-                    hb, w.ghist);
-            else
-                k_count_frag<16><<<dim3((unsigned)w.NS, (unsigned)qn), 512, countf_smem(ix->BS * w.CF), s>>>(
-                    w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ,
-                    w.cursor, w.cbase, w.ncand, w.need, w.traceV, w.qperm, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp,
-                    hb, w.ghist);
+            else {
+                // reductions without return + a final threshold scan over the counters (measured at
+                // cfg4/3/5 phi=1: count 16.9 / 81.2 / 29.5 ms against 17.1 / 86.1 / 32.4 ms with the
+                // atomics' returns and crossing bits); CRISP_COUNT_SWAR=0 keeps the crossing bits
+                const bool sw = env_int("CRISP_COUNT_SWAR", 1) != 0;
+#define CRISP_CF(WN, SW)                                                                                          \
+    k_count_frag<WN, SW><<<dim3((unsigned)w.NS, (unsigned)qn), WN * 32, countf_smem(ix->BS * w.CF), s>>>(           \
+        w.erow, w.etot, M, KK, ix->off2, NB, w.CF, ix->ids, ix->N, ix->BS, w.NS, ix->tau, w.pool, w.CAPQ, w.cursor, \
+        w.cbase, w.ncand, w.need, w.traceV, w.qperm, w.qrot, pitch, ix->Dp, ix->codes, ix->Wp, hb, w.ghist)
+                if (w.CF * ix->BS > 65536) {
+                    if (sw) CRISP_CF(32, true);
+                    else CRISP_CF(32, false);
+                } else if (sw) CRISP_CF(16, true);
+                else CRISP_CF(16, false);
+#undef CRISP_CF
+            }
         }
         else if (w.count_kernel == 0)
             k_count_select<<<g, THREADS, w.count_smem, s>>>(w.act, w.act_len, M, KK, ix->off2, NB, ix->ids, ix->N,

@@ -108,7 +108,11 @@ COUNT_VARIANTS = {"select": {"CRISP_COUNT_KERNEL": "0", "CRISP_ROWS4": "0"},
                  "frag": {"CRISP_COUNT_KERNEL": "2"},
                  "frag_f1": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "1"},
                  "frag_f4": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_F": "4"},
+                 # crossing bits from the atomics' returns (CRISP_COUNT_SWAR=0) instead of the scan
+                 "frag_cross": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_SWAR": "0"},
                  "frag_fused": {"CRISP_COUNT_KERNEL": "2", "CRISP_HAMMING_FUSED": "1"},
+                 # reductions without return + the final SWAR threshold scan (the default) with 4 blocks
+                 "frag_swar_f4": {"CRISP_COUNT_KERNEL": "2", "CRISP_COUNT_SWAR": "1", "CRISP_COUNT_F": "4"},
                  # the grouped Guaranteed-Mode re-rank (k_rerank_group) after either count kernel
                  "frag_group": {"CRISP_COUNT_KERNEL": "2", "CRISP_RERANK_GROUP": "1"},
                  "warp_group": {"CRISP_COUNT_KERNEL": "1", "CRISP_RERANK_GROUP": "1"}}
@@ -175,12 +179,16 @@ def test_full_blocks_ragged_tail(crisp, monkeypatch, mode, variant):
     assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
 
 
-@pytest.mark.parametrize("kernel", ["1", "2"])
+@pytest.mark.parametrize("kernel", ["1", "2", "frag_cross"])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_many_subspaces_wide_counters(crisp, monkeypatch, mode, kernel):
     """M=64 (scores up to 2M=128 do not fit the 7-bit SWAR compare: the
     __vcmpgeu4 path of the threshold scan), stage by stage."""
-    monkeypatch.setenv("CRISP_COUNT_KERNEL", kernel)
+    if kernel in COUNT_VARIANTS:
+        for k_, v_ in COUNT_VARIANTS[kernel].items():
+            monkeypatch.setenv(k_, v_)
+    else:
+        monkeypatch.setenv("CRISP_COUNT_KERNEL", kernel)
     X, Qv, ox = make_case(cfg=1, N=9001, D=256, Q=16, M=64, K=6, seed=7)
     ix = build_gpu(crisp, X, ox, block_ids=4096)
     B, tau, k = 1500, 30, 10
