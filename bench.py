@@ -60,7 +60,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
                                       stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -479,8 +479,19 @@ def run_crisp(args):
                 kernels["hamming"] = {"kernel": "k_hamming+k_hamming_dense",
                                       "bytes_per_step": hb, "ms_per_step": st["hamming"] / K,
                                       "achieved_gbs": hb / (st["hamming"] / K * 1e-3) / 1e9}
-        for kk in kernels.values():
+        l2 = l2_peak()
+        for name_, kk in kernels.items():
             kk["frac_of_peak"] = kk["achieved_gbs"] / peak
+            kk["bound"] = "hbm"
+            if name_ == "hamming" and l2:
+                # the code rows of one id block stay in L2 while every query's candidates in it are
+                # scored (k_hamming_seg): the ceiling that binds is the L2 read rate
+                kk["bound"], kk["peak"], kk["peak_source"] = "l2", l2[0], l2[1]
+                kk["frac_of_peak"] = kk["achieved_gbs"] / l2[0]
+            elif name_ == "count":
+                # shared-memory reductions at issue rate (ncu: issue ~73% busy, LSU ~66%; DESIGN 7):
+                # the HBM fraction of its id stream is reported, the stream does not bind
+                kk["bound"] = "issue (shared-memory reductions); frac = id stream / HBM"
         dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"]) if kernels else None
         traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic.json")
@@ -506,7 +517,6 @@ def run_crisp(args):
                 # the DRAM side of the same stage: measured bytes (ncu) over the live time
                 roof["dram_gbs"] = traffic / sec / 1e9
                 roof["dram_frac"] = roof["dram_gbs"] / peak
-            l2 = l2_peak()
             if l2:
                 # the algorithmic stream is served from L2 and DRAM: its ceiling is the L2 read rate
                 roof["l2_peak"] = l2[0]
