@@ -908,6 +908,10 @@ constexpr int CF_CAP = CRISP_CF_CAP;  // fragments staged per chunk
 #define CRISP_COUNT_LAG 0
 #endif
 constexpr bool CF_LAG = CRISP_COUNT_LAG != 0;
+#ifndef CRISP_COUNT_REDUX
+#define CRISP_COUNT_REDUX 1  // the fragment search by one warp OR-reduction (0: 5-step shuffle search)
+#endif
+constexpr bool CF_REDUX = CRISP_COUNT_REDUX != 0;
 constexpr int CF_MAXW = 32;   // warps per CTA: 16 (two CTAs per SM, F <= 2) or 32 (one CTA per SM, F = 4)
 
 struct CountFSmem {
@@ -1094,13 +1098,26 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
             uint4 qn;
             int gn0 = 0, gn1 = 0, qpn = 0;
             uint32_t wn = 0;
+            const unsigned lemask = (2u << lane) - 1u;  // lanes <= this lane
             auto issue = [&](int pp) {
                 const int p = pp + lane;
-                int j = 0;
+                int j = 0, jl = 0;
+                if (CF_REDUX) {
+                    // fragment fb holds quad pp; fragments fb+1.. start at distinct quads >= pp:
+                    // OR their start offsets inside the step into one mask; lane l's fragment is
+                    // fb + (number of starts at or before pp + l)
+                    const int off = te.x - pp;
+                    const unsigned starts =
+                        __reduce_or_sync(0xffffffffu, (lane > 0 && off >= 0 && off < 32) ? (1u << off) : 0u);
+                    j = __popc(starts & lemask);
+                    jl = __popc(starts);
+                } else {
 #pragma unroll
-                for (int st = 16; st; st >>= 1) {
-                    const int xv = __shfl_sync(0xffffffffu, te.x, j + st);
-                    if (xv <= p) j += st;
+                    for (int st = 16; st; st >>= 1) {
+                        const int xv = __shfl_sync(0xffffffffu, te.x, j + st);
+                        if (xv <= p) j += st;
+                    }
+                    jl = __shfl_sync(0xffffffffu, j, 31);
                 }
                 const int qx = __shfl_sync(0xffffffffu, te.x, j);
                 const int qs = __shfl_sync(0xffffffffu, te.y, j);
@@ -1113,7 +1130,6 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                 wn = 1u + ((uint32_t)gw >> 31);
                 qn = __ldg((const uint4 *)ids + qpn);
                 // slide the window to the fragment of this step's last quad
-                const int jl = __shfl_sync(0xffffffffu, j, 31);
                 if (jl > 0) {
                     fb += jl;
                     te = S.tab[fb + lane];
