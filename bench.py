@@ -523,7 +523,9 @@ def run_crisp(args):
                 roof["l2_frac"] = a / l2[0]
                 roof["l2_peak_source"] = l2[1]
         results[mode] = dict(qps=Q * K / (ms / 1e3), ms=ms / K, recall=rec, beta=mp["beta"], alpha=mp["alpha"],
-                             budget_ids=info["budget"], tau=info["tau"], roofline=roof, kernels=kernels,
+                             budget_ids=info["budget"], tau=info["tau"],
+                             patience_factor=info["patience_factor"] if phi(mode) == 1 else None,
+                             roofline=roof, kernels=kernels,
                              stage_ms_per_step={k_: v / K for k_, v in st.items()},
                              counters_per_step={k_: v / K for k_, v in cnt.items()}, launches=cnt["launches"],
                              clocks=clk.summary())
@@ -617,6 +619,7 @@ def run_crisp(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": c["name"], "N": N, "D": D, "Q": Q, "k": k, "M": M, "beta": hr["beta"],
                        "alpha": hr["alpha"], "mode": MODE_NAMES[head], "budget_ids": hr["budget_ids"],
+                       "patience_factor": hr.get("patience_factor"),
                        "tau": hr["tau"], "rotated": bool(info["rotated"]), "cev": info["cev"],
                        "l2": "inputs larger than L2 (X = %.2f GB >> 126 MB); no flush" % (N * D * 4 / 1e9),
                        "parallelism": f"points sharded x{world}" if world > 1 else "single GPU"},
