@@ -4080,7 +4080,7 @@ struct Work {
         // 2: k_count_frag (fragment-flattened, shared atomics; the small-cell regime)
         count_kernel = env_int("CRISP_COUNT_KERNEL", ix->slice_hint >= 8.0 ? 1 : 2);
         CF = std::max(1, std::min(std::min(NB, 4), env_int("CRISP_COUNT_F", 2)));  // k_count_frag: BS ids x CF per CTA
-        while (CF > 1 && countf_smem(BS * CF) > 200 * 1024) CF--;
+        while (CF > 1 && countf_smem(BS * CF) > 200 * 1024) CF >>= 1;
         // candidate segments per query (id blocks, warp sub-blocks, or frag blocks)
         NS = count_kernel == 0 ? NB : count_kernel == 1 ? ix->NBW : (NB + CF - 1) / CF;
         count_atom = env_int("CRISP_COUNT_ATOM", 0);  // k_count_warp: shared atomics (else byte load/store pairs; faster)
