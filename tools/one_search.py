@@ -22,7 +22,7 @@ w = synth.Workload(cfg, device=dev)
 X, Qd = w.base(c["N"]), w.queries(Qn or c["Q"])
 index = crisp.Index.build(X, op["M"], K=50, seed=op.get("seed", 1))
 mp = op["modes"][mode]
-index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=40)
+index.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
 index.set_adsampling(mode == 1 and os.environ.get("PROBE_AD", "0") == "1")
 k = c["k"]
 ids = torch.empty((Qd.shape[0], k), dtype=torch.int64, device=dev)

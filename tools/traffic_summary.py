@@ -9,14 +9,15 @@ import json
 import sys
 from collections import OrderedDict
 
-STAGE = {"k_rot_tc": "transform", "k_slice_rows": "transform", "k_recompute": "transform", "k_prep_queries": "transform",
+STAGE = {"k_rot_tc": "transform", "k_slice_rows": "transform", "k_recompute": "transform",
          "k_probe": "probe", "k_query_key": "probe", "k_act_rows": "count_select", "k_count_frag": "count_select",
          "k_count_warp": "count_select", "k_count_select": "count_select", "k_fallback": "fallback",
          "k_hamming_dense": "hamming", "k_hamming": "hamming", "k_hsort_cta": "hsort", "k_hsort": "hsort",
          "k_verify_rows": "verify", "k_verify_rows_ad": "verify", "k_patience_scan": "verify",
          "k_patience_tail": "verify", "k_rerank_exact": "verify", "k_merge_lists": "merge",
          "k_verify_rows_lb": "verify", "k_q8_prep": "verify", "k_lb_bounds": "verify", "k_lb_threshold": "verify",
-         "k_screen_tc": "probe"}
+         "k_screen_tc": "probe", "k_qcodes": "hamming", "k_hamming_seg": "hamming", "k_hhist": "hamming",
+         "k_prep_queries": "transform"}
 
 
 def main():
