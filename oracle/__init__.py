@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import hashlib
 import os
 import subprocess
 from fractions import Fraction
@@ -30,10 +31,16 @@ CFLAGS = ["-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fno-fast-math", "-fo
 
 def compile_oracle(force: bool = False) -> str:
     """Compile liboracle.so in-tree with gcc (the checker, not the product)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    with open(_SRC, "rb") as f:
+        digest = hashlib.sha256(f.read() + " ".join(CFLAGS).encode()).hexdigest()
+    stamp = _LIB + ".sha256"
+    fresh = os.path.exists(_LIB) and os.path.exists(stamp) and open(stamp).read().strip() == digest
+    if force or not fresh:  # content-based: a checkout that changes the source always rebuilds
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
+        with open(stamp, "w") as f:
+            f.write(digest + "\n")
     return _LIB
 
 
