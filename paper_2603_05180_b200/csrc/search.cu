@@ -4114,7 +4114,10 @@ struct Work {
         {
             const int fr = env_int("CRISP_FILTER_ROUNDS", 1);
             const int F0 = std::max(64, (std::max(k, env_int("CRISP_LB_FIRST", 256)) + 63) / 64 * 64);
-            lbf = (mode == 1 && !ad && ix->C8 && ix->vfilter && fr && (fr == 2 || Pq >= 4 * F0)) ? 1 : 0;
+            // ADSampling (f1) keeps it: a row the bound excludes has d > the round's d_k >= the running
+            // r_k, so it is a miss whether Eq. 2 prunes it or not; the replay applies Eq. 2 to every
+            // row that would enter the top-k (patience_group), exactly as the sequential rule
+            lbf = (mode == 1 && (!ad || adsp) && ix->C8 && ix->vfilter && fr && (fr == 2 || Pq >= 4 * F0)) ? 1 : 0;
             if (lbf) {
                 F = F0;
                 R0 = std::max(1, std::min(16, env_int("CRISP_LB_ROUNDS", 6)));

@@ -627,6 +627,27 @@ def test_adsampling_k100(crisp):
     assert_topk_parity(ids, d, r_ids, r_d, "adsampling k=100")
 
 
+@pytest.mark.parametrize("filt", ["0", "2"])
+def test_adsampling_behind_the_verification_filter(crisp, monkeypatch, filt):
+    """f1 with the certified int8 filter (R17) forced on for every round >= 1
+    (CRISP_FILTER_ROUNDS=2): rows the bound excludes are misses under Eq. 2
+    too, and Eq. 2 is still applied in order to every row that would enter the
+    top-k, so the patience stop, ids and distances equal the oracle's
+    ADSampling search (k = 100 and k = 7, short and long patience)."""
+    monkeypatch.setenv("CRISP_FILTER_ROUNDS", filt)
+    X, Qv, ox = make_case(cfg=4, N=30000, D=192, Q=20, M=8, K=24, rotation=1, seed=9)
+    ix = build_gpu(crisp, X, ox, block_ids=8192)
+    for (B, tau, k, pf) in ((1500, 3, 100, 4), (1500, 3, 100, 40), (900, 2, 7, 40)):
+        ix.set_search_params(budget=B, tau=tau, patience_factor=pf)
+        ix.set_adsampling(True)
+        ids, d, t = ix.trace(Qv, k, 1)
+        r_ids, r_d, ot = oracle.search(ox, Qv, k, 1, B, tau, patience_factor=pf, trace=True, adsampling=True)
+        compare_trace(t, ot, 1, X.shape[0])
+        assert_topk_parity(ids, d, r_ids, r_d, f"adsampling + filter k={k} pf={pf}")
+        ids2, d2 = ix.search(Qv, k, 1)
+        assert np.array_equal(ids2, ids) and np.array_equal(d2, d)
+
+
 def test_adsampling_rejects_bad_stride(crisp):
     X, Qv, ox = make_case(cfg=1, N=2000, D=64, Q=4, M=4, K=6)
     ix = build_gpu(crisp, X, ox)
