@@ -78,7 +78,11 @@ def test_fullsize_sampled_queries(setup, mode):
     if str(mode) not in op["modes"]:
         pytest.skip("mode not at this config's operating point")
     mp = op["modes"][str(mode)]
-    ix.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=40)
+    # the operating point's patience factor (cfg2: 20), or 40 where it is far longer (cfg3/cfg5:
+    # the oracle would re-rank nearly all of a 40%-of-N candidate set per query)
+    pf = mp.get("patience_factor", 40)
+    pf = pf if pf <= 40 else 40
+    ix.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=pf)
     k = c["k"]
     ids = torch.empty((c["Q"], k), dtype=torch.int64, device="cuda")
     dd = torch.empty((c["Q"], k), dtype=torch.float32, device="cuda")
@@ -89,7 +93,7 @@ def test_fullsize_sampled_queries(setup, mode):
     n = c["Q"] if cfg_of(c) == 2 else (1000 if mode == 1 else 200)
     sample = np.sort(np.random.default_rng(mode).choice(c["Q"], n, replace=False))
     B, tau = oracle.budget_ids(mp["beta"], c["N"]), oracle.tau_int(mp["alpha"], op["M"])
-    r_ids, r_d, _ = oracle.search(ox, Qh[sample], k, mode, B, tau, patience_factor=40)
+    r_ids, r_d, _ = oracle.search(ox, Qh[sample], k, mode, B, tau, patience_factor=pf)
     g_ids, g_d = ids.cpu().numpy()[sample], dd.cpu().numpy()[sample]
     assert np.array_equal(g_ids, r_ids)
     fin = np.isfinite(r_d)
@@ -155,17 +159,19 @@ def test_fullsize_cfg4_index(cfg4):
         assert np.array_equal(e[name], ref), name
 
 
-@pytest.mark.parametrize("mode", [0, 1])
-def test_fullsize_cfg4_sampled_queries(cfg4, mode):
-    """200 of the 10k queries, k = 100 (P = 40k = 4000: the Hamming order is
-    cut past 4096 positions, k_hsort_cta's two-pass path, and k_patience_tail
-    completes the order of the queries that go further), in the bench's launch
-    configuration (one crisp_search_async over all 10k queries)."""
+@pytest.mark.parametrize("mode,pf", [(0, 40), (1, 40), (1, "op")])
+def test_fullsize_cfg4_sampled_queries(cfg4, mode, pf):
+    """200 of the 10k queries, k = 100, in the bench's launch configuration (one
+    crisp_search_async over all 10k queries): phi=1 at the bench's operating
+    point (patience factor 20) and at the paper's default 40 (P = 4000: the
+    Hamming order is cut past 4096 positions, k_hsort_cta's two-pass path, and
+    k_patience_tail completes the order of the queries that go further)."""
     import torch
 
     crisp, ix, ox, e, Qd, Qh, op, c = cfg4
     mp = op["modes"][str(mode)]
-    ix.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=40)
+    pf = mp.get("patience_factor", 40) if pf == "op" else pf
+    ix.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=pf)
     k = c["k"]
     ids = torch.empty((c["Q"], k), dtype=torch.int64, device="cuda")
     dd = torch.empty((c["Q"], k), dtype=torch.float32, device="cuda")
@@ -173,12 +179,12 @@ def test_fullsize_cfg4_sampled_queries(cfg4, mode):
     torch.cuda.synchronize()
     sample = np.sort(np.random.default_rng(40 + mode).choice(c["Q"], 200, replace=False))
     B, tau = oracle.budget_ids(mp["beta"], c["N"]), oracle.tau_int(mp["alpha"], op["M"])
-    r_ids, r_d, t = oracle.search(ox, Qh[sample], k, mode, B, tau, patience_factor=40, trace=mode == 1)
+    r_ids, r_d, t = oracle.search(ox, Qh[sample], k, mode, B, tau, patience_factor=pf, trace=mode == 1)
     g_ids, g_d = ids.cpu().numpy()[sample], dd.cpu().numpy()[sample]
     assert np.array_equal(g_ids, r_ids)
     fin = np.isfinite(r_d)
     assert np.array_equal(np.isfinite(g_d), fin)
     assert np.all(np.abs(g_d[fin] - r_d[fin]) <= 1e-5 * np.abs(r_d[fin]))
-    if mode == 1:
+    if mode == 1 and pf == 40:
         # the paths named above are exercised: queries verify past the 4096-position cut
         assert int(t["n_verified"].max()) > 4096
