@@ -37,6 +37,7 @@ constexpr int THREADS = WARPS * 32;
 constexpr int CS_CAP = 512;           // slice-table entries per round (count kernel)
 constexpr int CS_U = 8;               // ids staged per thread per round
 constexpr int CS_TCAP = THREADS * CS_U;  // positions per round
+constexpr int HSORT_BW = 1024;       // bins per window of k_hsort_cta's per-warp counters
 constexpr int PATIENCE_CH = 128;      // min rows verified per patience chunk (k_patience_tail)
 constexpr int TAIL_CAP = 1024;        // max rows per chunk of k_patience_tail
 
@@ -2762,7 +2763,7 @@ __global__ void __launch_bounds__(THREADS) k_hsort_cta(const int32_t *__restrict
     int *start = (int *)sm;         // Dp + 1
     int *pre = start + Dp + 1;      // NS + 1
     int *cbs = pre + NS + 1;        // NS
-    int *wcnt = cbs + NS;           // WARPS x (Dp + 1)
+    int *wcnt = cbs + NS;           // WARPS x HSORT_BW (one window of bins)
     __shared__ int s_total, s_cut;
     const int64_t q = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -2793,13 +2794,11 @@ __global__ void __launch_bounds__(THREADS) k_hsort_cta(const int32_t *__restrict
     }
     __syncthreads();
     const int total = s_total, cut = s_cut;
-    for (int i = tid; i < WARPS * (cut + 1); i += THREADS) wcnt[(i / (cut + 1)) * HB + i % (cut + 1)] = 0;
-    __syncthreads();
     const int per = (total + WARPS - 1) / WARPS;
     const int lo = min(total, warp * per), hi = min(total, lo + per);
     const int32_t *cq = pool + q * CS;
     const uint16_t *hq = hbuf + q * CS;
-    int *mycnt = wcnt + warp * HB;
+    int *mycnt = wcnt + warp * HSORT_BW;
     int bl0 = 0;  // segment holding position lo
     {
         int a = 0, b = NS;  // largest a with pre[a] <= lo
@@ -2811,124 +2810,124 @@ __global__ void __launch_bounds__(THREADS) k_hsort_cta(const int32_t *__restrict
         bl0 = a;
     }
     constexpr int U = 8;
-    // phase A: per-bin counts of this warp's qualifying elements; their pool
-    // positions are also listed in order in the unused tail of the query's order
-    // row ([total, CS), capw per warp), so phase B visits only them
+    // the qualifying bins [0, cut] in windows of HSORT_BW bins (the per-warp counters cover
+    // one window: ~45 KB of shared memory instead of 8 (D'+1) ints, so several CTAs fit an
+    // SM; at cfg4 every query's cut lies in the first window).  Per window, phase A counts
+    // this warp's elements per bin; the per-(warp, bin) output offsets follow; phase B
+    // scatters them stably.  LIST: window 0's phase A also lists the pool positions of all
+    // qualifying elements, in order, in the unused tail of the query's order row ([total,
+    // CS), capw per warp), and later work visits only them.
     int32_t *out = order + q * CS;
-    // listing pays when the qualifying elements are a small part of the list
-    // (the host picks LIST when the positions the verification reads are few)
     constexpr bool listing = LIST;
     const int64_t capw64 = listing ? (CS - total) / WARPS : 0;
     const int capw = capw64 < (1 << 30) ? (int)capw64 : (1 << 30);
     int32_t *scr = out + total + (int64_t)warp * capw;
     __shared__ int s_over;
-    if (tid == 0) s_over = 0;
+    if (tid == 0) s_over = listing ? 0 : 1;
     int nq = 0;
-    int bl = bl0;
-    for (int v00 = lo; v00 < hi; v00 += 32 * U) {
-        int hh[U], pp[U];
+    for (int w0 = 0; w0 <= cut; w0 += HSORT_BW) {
+        const int w1 = min(cut, w0 + HSORT_BW - 1);
+        const int nbw = w1 - w0 + 1;
+        for (int i = tid; i < WARPS * HSORT_BW; i += THREADS) wcnt[i] = 0;
+        __syncthreads();  // counters zeroed (and s_over initialised)
+        const bool use_list = listing && w0 > 0 && !s_over;
+        if (use_list) {
+            for (int i0 = 0; i0 < nq; i0 += 32) {
+                const int i = i0 + lane;
+                const int h = i < nq ? (int)hq[scr[i]] : 0x7fffffff;
+                if (h >= w0 && h <= w1) atomicAdd(&mycnt[h - w0], 1);
+            }
+        } else {
+            int bl = bl0;
+            for (int v00 = lo; v00 < hi; v00 += 32 * U) {
+                int hh[U], pp[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int v = v00 + u * 32 + lane;
-            hh[u] = 0x7fffffff;
-            pp[u] = 0;
-            if (v < hi) {
-                while (pre[bl + 1] <= v) bl++;
-                pp[u] = cbs[bl] + (v - pre[bl]);
-                hh[u] = hq[pp[u]];
+                for (int u = 0; u < U; u++) {
+                    const int v = v00 + u * 32 + lane;
+                    hh[u] = 0x7fffffff;
+                    pp[u] = 0;
+                    if (v < hi) {
+                        while (pre[bl + 1] <= v) bl++;
+                        pp[u] = cbs[bl] + (v - pre[bl]);
+                        hh[u] = hq[pp[u]];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if (hh[u] >= w0 && hh[u] <= w1) atomicAdd(&mycnt[hh[u] - w0], 1);
+                    if (listing && w0 == 0) {
+                        const bool qual = hh[u] <= cut;
+                        const unsigned qm = __ballot_sync(0xffffffffu, qual);
+                        const int r = nq + __popc(qm & ((1u << lane) - 1));
+                        if (qual && r < capw) scr[r] = pp[u];
+                        nq += __popc(qm);
+                    }
+                }
+            }
+            if (listing && w0 == 0 && lane == 0 && nq > capw) atomicOr(&s_over, 1);
+        }
+        __syncthreads();
+        // per-(warp, bin) output offsets: bin start + the bin's elements of earlier warps
+        for (int h = tid; h < nbw; h += THREADS) {
+            int run = start[w0 + h];
+            for (int w2 = 0; w2 < WARPS; w2++) {
+                const int c = wcnt[w2 * HSORT_BW + h];
+                wcnt[w2 * HSORT_BW + h] = run;
+                run += c;
             }
         }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const bool qual = hh[u] <= cut;
-            if (qual) atomicAdd(&mycnt[hh[u]], 1);
-            const unsigned qm = __ballot_sync(0xffffffffu, qual);
-            if (listing) {
-                const int r = nq + __popc(qm & ((1u << lane) - 1));
-                if (qual && r < capw) scr[r] = pp[u];
-                nq += __popc(qm);
-            }
-        }
-    }
-    __syncthreads();  // s_over initialised
-    if (lane == 0 && (!listing || nq > capw)) s_over = 1;
-    __syncthreads();
-    // per-(warp, bin) output offsets: bin start + the bin's elements of earlier warps
-    for (int h = tid; h <= cut; h += THREADS) {
-        int run = start[h];
-        for (int w2 = 0; w2 < WARPS; w2++) {
-            const int c = wcnt[w2 * HB + h];
-            wcnt[w2 * HB + h] = run;
-            run += c;
-        }
-    }
-    __syncthreads();
-    if (!s_over) {
-        // phase B over the listed qualifying elements only, in order
-        for (int i0 = 0; i0 < nq; i0 += 32) {
-            const int i = i0 + lane;
-            const bool qual = i < nq;
-            const int pos = qual ? scr[i] : 0;
-            const int h = qual ? (int)hq[pos] : 0x7fffffff;
-            const int id = qual ? cq[pos] : 0;
-            const unsigned qm = __ballot_sync(0xffffffffu, qual);
+        __syncthreads();
+        // one element per lane: stable placement within its bin (peers ranked by lane)
+        auto place = [&](bool inw, int h, int id) {
+            const unsigned qm = __ballot_sync(0xffffffffu, inw);
+            if (!qm) return;
             int rank = 0, cnt = 0, leader = 32;
-            if (qual) {
+            if (inw) {
                 const unsigned peers = __match_any_sync(qm, h);
                 leader = __ffs(peers) - 1;
                 rank = __popc(peers & ((1u << lane) - 1));
                 cnt = __popc(peers);
             }
             int base = 0;
-            if (qual && lane == leader) {
-                base = mycnt[h];
-                mycnt[h] = base + cnt;
+            if (inw && lane == leader) {
+                base = mycnt[h - w0];
+                mycnt[h - w0] = base + cnt;
             }
-            base = __shfl_sync(0xffffffffu, base, qual ? leader : lane);
-            if (qual) out[base + rank] = id;
+            base = __shfl_sync(0xffffffffu, base, inw ? leader : lane);
+            if (inw) out[base + rank] = id;
             __syncwarp();
-        }
-        if (tid == 0) total_out[q] = total;
-        return;
-    }
-    // phase B: stable scatter of this warp's range
-    bl = bl0;
-    for (int v00 = lo; v00 < hi; v00 += 32 * U) {
-        int hh[U], ll[U];
+        };
+        if (listing && !s_over) {
+            // phase B over the listed qualifying elements only, in order
+            for (int i0 = 0; i0 < nq; i0 += 32) {
+                const int i = i0 + lane;
+                const int pos = i < nq ? scr[i] : 0;
+                const int h = i < nq ? (int)hq[pos] : 0x7fffffff;
+                const bool inw = h >= w0 && h <= w1;
+                place(inw, h, inw ? cq[pos] : 0);
+            }
+        } else {
+            // phase B: stable scatter of this warp's range
+            int bl = bl0;
+            for (int v00 = lo; v00 < hi; v00 += 32 * U) {
+                int hh[U], ll[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int v = v00 + u * 32 + lane;
-            hh[u] = 0x7fffffff;
-            ll[u] = 0;
-            if (v < hi) {
-                while (pre[bl + 1] <= v) bl++;
-                const int pos = cbs[bl] + (v - pre[bl]);
-                hh[u] = hq[pos];
-                ll[u] = cq[pos];
-            }
-        }
+                for (int u = 0; u < U; u++) {
+                    const int v = v00 + u * 32 + lane;
+                    hh[u] = 0x7fffffff;
+                    ll[u] = 0;
+                    if (v < hi) {
+                        while (pre[bl + 1] <= v) bl++;
+                        const int pos = cbs[bl] + (v - pre[bl]);
+                        hh[u] = hq[pos];
+                        ll[u] = cq[pos];
+                    }
+                }
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int h = hh[u];
-            const bool qual = h <= cut;
-            const unsigned qm = __ballot_sync(0xffffffffu, qual);
-            if (!qm) continue;
-            int rank = 0, cnt = 0, leader = 32;
-            if (qual) {
-                const unsigned peers = __match_any_sync(qm, h);
-                leader = __ffs(peers) - 1;
-                rank = __popc(peers & ((1u << lane) - 1));
-                cnt = __popc(peers);
+                for (int u = 0; u < U; u++) place(hh[u] >= w0 && hh[u] <= w1, hh[u], ll[u]);
             }
-            int base = 0;
-            if (qual && lane == leader) {
-                base = mycnt[h];
-                mycnt[h] = base + cnt;
-            }
-            base = __shfl_sync(0xffffffffu, base, qual ? leader : lane);
-            if (qual) out[base + rank] = ll[u];
-            __syncwarp();
         }
+        __syncthreads();  // the window's counters are reused next
     }
     if (tid == 0) total_out[q] = total;
 }
@@ -4248,7 +4247,7 @@ struct Work {
         rx_smem = pitch * 8 + WARPS * k * 16 + (2 * NS + 1) * 4;
         ham_smem = ix->Wp * 8 + (Dp + 1) * 4 + (2 * NS + 1) * 4;
         hsort_smem = (Dp + 1 + 2 * NS + 1) * 4;
-        hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * (Dp + 1)) * 4;
+        hsort_cta_smem = (Dp + 1 + 2 * NS + 1 + WARPS * HSORT_BW) * 4;
         vr_smem = pitch * 8;
         vrl_smem = pitch * 8 + 2 * std::max(16, ix->c8pitch) + WARPS * 64 * 4;
         lbb_smem = 2 * std::max(16, ix->c8pitch) + (2 * NS + 1) * 4;

@@ -884,3 +884,34 @@ def test_adaptive_subspaces_rotated_rule_on_stored_vectors(crisp):
     assert e["subspace_widths"].tolist() == w
     ox = oracle.build(e["X"], 4, K=8, rotation_mode=0, codebooks=e["codebooks"], seed=2, subspace_widths=w)
     assert np.array_equal(e["cells"], ox["cells"]) and np.array_equal(e["ids"], ox["ids"])
+
+
+@pytest.mark.parametrize("pf", [3, 40])
+def test_hamming_order_multiwindow_bins(crisp, pf):
+    """k_hsort_cta's per-warp counters cover windows of 1024 Hamming bins: at
+    D' = 2560 the candidates' h spread past bin 1024, so the traced search
+    (the whole order) and the untraced one (the order up to its cut, LIST
+    phase B for k = 10) sort across several windows; order, patience stop,
+    ids and distances equal the oracle's."""
+    r = np.random.default_rng(31)
+    N, D, Q, M = 8000, 2560, 24, 8
+    X = r.standard_normal((N, D)).astype(np.float32)
+    Qv = (X[r.choice(N, Q, replace=False)] + 0.8 * r.standard_normal((Q, D))).astype(np.float32)
+    ox = oracle.build(X, M, K=16, rotation_mode=0, kmeans_iters=3, seed=4)
+    ix = build_gpu(crisp, X, ox)
+    B, tau, k = 3000, 2, 10
+    ix.set_search_params(budget=B, tau=tau, patience_factor=pf)
+    ids, d, t = ix.trace(Qv, k, 1)
+    r_ids, r_d, ot = oracle.search(ox, Qv, k, 1, B, tau, patience_factor=pf, trace=True)
+    compare_trace(t, ot, 1, N)
+    qc = oracle.codes(ot["qrot"])
+    hmax = 0
+    for q in range(Q):
+        n = int(ot["cand_n"][q])
+        if n:
+            x = ox["codes"][ot["order"][q, :n]] ^ qc[q]
+            hmax = max(hmax, int(np.unpackbits(x.view(np.uint8), axis=1).sum(axis=1).max()))
+    assert hmax > 1024, f"candidates' h must reach past the first window ({hmax})"
+    assert_topk_parity(ids, d, r_ids, r_d, f"multi-window hsort pf={pf}")
+    ids2, d2 = ix.search(Qv, k, 1)
+    assert np.array_equal(ids2, r_ids)
