@@ -489,9 +489,9 @@ def run_crisp(args):
                 kk["bound"], kk["peak"], kk["peak_source"] = "l2", l2[0], l2[1]
                 kk["frac_of_peak"] = kk["achieved_gbs"] / l2[0]
             elif name_ == "count":
-                # shared-memory reductions at issue rate (ncu: issue ~73% busy, LSU ~66%; DESIGN 7):
+                # bound by the shared-memory atomic unit (ncu: 3.7 wavefronts per red.shared, DESIGN 7):
                 # the HBM fraction of its id stream is reported, the stream does not bind
-                kk["bound"] = "issue (shared-memory reductions); frac = id stream / HBM"
+                kk["bound"] = "shared-memory reductions (atomic unit); frac = id stream / HBM"
         dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"]) if kernels else None
         traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic.json")
