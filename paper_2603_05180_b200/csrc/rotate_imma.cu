@@ -132,9 +132,17 @@ __global__ void k_slice_cols(const float *__restrict__ R, int Dp, int Dpk, int8_
 // yhat = 2^(e_q + f_n) sum_l 2^-8l C_l and its bound b (see the top); returns
 // fl32(yhat) and, if [yhat - b, yhat + b] is not strictly inside the fp32
 // rounding cell of fl32(yhat), lists the output for k_recompute.
+// uncertified outputs: total count, then per query row (up to RCAP columns per row; a row's
+// list is recomputed by one warp sharing the row in shared memory), the rest in a flat list
+constexpr int RCAP = 32;
+struct FallLists {
+    unsigned long long *nfall;  // [0] all uncertified outputs, [1] those in the flat list
+    int64_t *flist;             // m Dp + n
+    int32_t *rowcnt;            // rows
+    int32_t *rowlist;           // rows x RCAP columns n
+};
 __device__ __forceinline__ float certify_one(const int32_t (&c)[LV - 1], int32_t e_q, double n_q, int32_t e_n,
-                                             double n_n, int Dp, int64_t m, int n, unsigned long long *nfall,
-                                             int64_t *flist) {
+                                             double n_n, int Dp, int64_t m, int n, const FallLists &fl) {
     double acc = 0.0, mag = 0.0;
 #pragma unroll
     for (int l = LV; l >= 2; l--) {  // ascending magnitude; 2^-8l exact
@@ -152,14 +160,18 @@ __device__ __forceinline__ float certify_one(const int32_t (&c)[LV - 1], int32_t
     const float fup = f == 0.f ? 1.4e-45f : __int_as_float(f > 0.f ? fb + 1 : fb - 1);
     const double lo = 0.5 * ((double)f + (double)fdn);
     const double hi = 0.5 * ((double)f + (double)fup);
-    if (!(y - b > lo && y + b < hi)) flist[atomicAdd(nfall, 1ull)] = m * Dp + n;  // k_recompute
+    if (!(y - b > lo && y + b < hi)) {  // k_recompute_rows / k_recompute
+        atomicAdd(fl.nfall, 1ull);
+        const int slot = atomicAdd(fl.rowcnt + m, 1);
+        if (slot < RCAP) fl.rowlist[m * RCAP + slot] = n;
+        else fl.flist[atomicAdd(fl.nfall + 1, 1ull)] = m * Dp + n;
+    }
     return f;
 }
 
 __global__ void k_certify(const int32_t *__restrict__ C, int64_t rows, int Dp, int Dpk, const int32_t *__restrict__ qe,
                           const double *__restrict__ qn2, const int32_t *__restrict__ re,
-                          const double *__restrict__ rn2, float *__restrict__ Y, int64_t ldy,
-                          unsigned long long *__restrict__ nfall, int64_t *__restrict__ flist) {
+                          const double *__restrict__ rn2, float *__restrict__ Y, int64_t ldy, FallLists fl) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t m = blockIdx.y;
     if (n >= Dp || m >= rows) return;
@@ -167,7 +179,7 @@ __global__ void k_certify(const int32_t *__restrict__ C, int64_t rows, int Dp, i
     int32_t c[LV - 1];
 #pragma unroll
     for (int l = 2; l <= LV; l++) c[l - 2] = C[(int64_t)(l - 2) * plane + m * Dpk + n];
-    Y[m * ldy + n] = certify_one(c, qe[m], qn2[m], re[n], rn2[n], Dp, m, n, nfall, flist);
+    Y[m * ldy + n] = certify_one(c, qe[m], qn2[m], re[n], rn2[n], Dp, m, n, fl);
 }
 
 // ---------------------------------------------------------------------------
@@ -213,8 +225,7 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, 
 __global__ void __launch_bounds__(THREADS_TC, 1)
     k_rot_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t rows, int Dp,
              int Dpk, const int32_t *__restrict__ qe, const double *__restrict__ qn2, const int32_t *__restrict__ re,
-             const double *__restrict__ rn2, float *__restrict__ Y, int64_t ldy, unsigned long long *__restrict__ nfall,
-             int64_t *__restrict__ flist) {
+             const double *__restrict__ rn2, float *__restrict__ Y, int64_t ldy, FallLists fl) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     // 1024-byte aligned (the 128-byte swizzle atoms), keeping the shared-memory provenance
     unsigned char *base = smraw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smraw) & 1023u)) & 1023u);
@@ -330,7 +341,7 @@ __global__ void __launch_bounds__(THREADS_TC, 1)
             int32_t c[LV - 1];
 #pragma unroll
             for (int l = 2; l <= LV; l++) c[l - 2] = (int32_t)v[l - 2][j];
-            Y[m * ldy + n] = certify_one(c, e_q, n_q, s_re[c8 + j], s_rn2[c8 + j], Dp, m, n, nfall, flist);
+            Y[m * ldy + n] = certify_one(c, e_q, n_q, s_re[c8 + j], s_rn2[c8 + j], Dp, m, n, fl);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -343,7 +354,72 @@ __global__ void __launch_bounds__(THREADS_TC, 1)
 
 // the uncertified outputs: the sequential chain itself, a thread per output,
 // reading q' s row and R's column n (Rt: R transposed) as float4 streams with
-// 32 terms in flight ahead of their fma's
+// 32 terms in flight ahead of their fma's (per-row lists: k_recompute_rows;
+// the flat overflow list: k_recompute)
+// one output's chain from a query row (global or shared) and R's column n (Rt row n)
+__device__ __forceinline__ double chain_one(const float *__restrict__ xr, const float *__restrict__ rr, int Dp,
+                                            bool vec) {
+    double s = 0.0;
+    int k = 0;
+    if (vec) {
+        const float4 *x4 = (const float4 *)xr, *r4 = (const float4 *)rr;
+        const int nv = Dp / 4;
+        float4 xa[8], ra[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            xa[j] = j < nv ? x4[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+            ra[j] = j < nv ? __ldg(r4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int v0 = 0; v0 < nv; v0 += 8) {
+            float4 xb[8], rb[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int v = v0 + 8 + j;
+                xb[j] = v < nv ? x4[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+                rb[j] = v < nv ? __ldg(r4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (v0 + j < nv) {
+                    s = __fma_rn((double)xa[j].x, (double)ra[j].x, s);
+                    s = __fma_rn((double)xa[j].y, (double)ra[j].y, s);
+                    s = __fma_rn((double)xa[j].z, (double)ra[j].z, s);
+                    s = __fma_rn((double)xa[j].w, (double)ra[j].w, s);
+                }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                xa[j] = xb[j];
+                ra[j] = rb[j];
+            }
+        }
+        k = nv * 4;
+    }
+    for (; k < Dp; k++) s = __fma_rn((double)xr[k], (double)rr[k], s);
+    return s;
+}
+
+// the per-row lists: a warp per query row, the row staged once in shared memory, a lane per
+// listed output (the rows' X reads are no longer repeated per output; R's columns come
+// from L2)
+__global__ void __launch_bounds__(32) k_recompute_rows(const int32_t *__restrict__ rowcnt,
+                                                       const int32_t *__restrict__ rowlist, int64_t rows, int Dp,
+                                                       const float *__restrict__ X, int64_t ldx,
+                                                       const float *__restrict__ Rt, float *__restrict__ Y,
+                                                       int64_t ldy) {
+    extern __shared__ __align__(16) float xs[];  // Dp
+    const int64_t m = blockIdx.x;
+    const int cnt = min(rowcnt[m], RCAP);
+    if (cnt == 0) return;
+    const int lane = threadIdx.x;
+    const float *xr = X + m * ldx;
+    for (int k = lane; k < Dp; k += 32) xs[k] = xr[k];
+    __syncwarp();
+    if (lane < cnt) {
+        const int n = rowlist[m * RCAP + lane];
+        Y[m * ldy + n] = (float)chain_one(xs, Rt + (int64_t)n * Dp, Dp, (Dp & 3) == 0);
+    }
+}
+
 __global__ void __launch_bounds__(128) k_recompute(const unsigned long long *__restrict__ nfall,
                                                    const int64_t *__restrict__ flist, int Dp,
                                                    const float *__restrict__ X, int64_t ldx,
@@ -353,44 +429,7 @@ __global__ void __launch_bounds__(128) k_recompute(const unsigned long long *__r
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t mn = flist[i], m = mn / Dp;
         const int n = (int)(mn - m * Dp);
-        const float *xr = X + m * ldx, *rr = Rt + (int64_t)n * Dp;
-        double s = 0.0;
-        int k = 0;
-        if (((ldx | Dp) & 3) == 0) {
-            const float4 *x4 = (const float4 *)xr, *r4 = (const float4 *)rr;
-            const int nv = Dp / 4;
-            float4 xa[8], ra[8];
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-                xa[j] = j < nv ? __ldg(x4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-                ra[j] = j < nv ? __ldg(r4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            for (int v0 = 0; v0 < nv; v0 += 8) {
-                float4 xb[8], rb[8];
-#pragma unroll
-                for (int j = 0; j < 8; j++) {
-                    const int v = v0 + 8 + j;
-                    xb[j] = v < nv ? __ldg(x4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    rb[j] = v < nv ? __ldg(r4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-#pragma unroll
-                for (int j = 0; j < 8; j++)
-                    if (v0 + j < nv) {
-                        s = __fma_rn((double)xa[j].x, (double)ra[j].x, s);
-                        s = __fma_rn((double)xa[j].y, (double)ra[j].y, s);
-                        s = __fma_rn((double)xa[j].z, (double)ra[j].z, s);
-                        s = __fma_rn((double)xa[j].w, (double)ra[j].w, s);
-                    }
-#pragma unroll
-                for (int j = 0; j < 8; j++) {
-                    xa[j] = xb[j];
-                    ra[j] = rb[j];
-                }
-            }
-            k = nv * 4;
-        }
-        for (; k < Dp; k++) s = __fma_rn((double)xr[k], (double)rr[k], s);
-        Y[m * ldy + n] = (float)s;
+        Y[m * ldy + n] = (float)chain_one(X + m * ldx, Rt + (int64_t)n * Dp, Dp, ((ldx | Dp) & 3) == 0);
     }
 }
 
@@ -537,13 +576,19 @@ void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64
     int32_t *qe = (int32_t *)(buf + qbytes + cbytes + up((size_t)rows * 8));
     k_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(X, rows, Dp, ldx, Dpk, Qcat, qe, qn2);
     CRISP_LAUNCH();
-    // uncertified outputs: counter + list (at most rows x Dp entries)
+    // uncertified outputs: counters, per-row lists (RCAP columns) and the flat overflow list
+    // (at most rows x Dp entries)
     unsigned long long *cnt = nullptr;
-    int64_t *flist = nullptr;
     const size_t fcap = (size_t)rows * Dp;
-    CRISP_CUDA(cudaMallocAsync(&cnt, 8 + fcap * 8, s));
-    flist = (int64_t *)(cnt + 1);
-    CRISP_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
+    const size_t lbytes = up(16) + up(fcap * 8) + up((size_t)rows * 4) + up((size_t)rows * RCAP * 4);
+    CRISP_CUDA(cudaMallocAsync(&cnt, lbytes, s));
+    FallLists fl;
+    fl.nfall = cnt;
+    fl.flist = (int64_t *)((char *)cnt + up(16));
+    fl.rowcnt = (int32_t *)((char *)fl.flist + up(fcap * 8));
+    fl.rowlist = fl.rowcnt + up((size_t)rows * 4) / 4;
+    CRISP_CUDA(cudaMemsetAsync(cnt, 0, 16, s));
+    CRISP_CUDA(cudaMemsetAsync(fl.rowcnt, 0, (size_t)rows * 4, s));
     if (use_lt) {
         std::lock_guard<std::mutex> lk(g_mu);
         ensure_lt();
@@ -559,7 +604,7 @@ void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64
         }
         CRISP_CUDA(cudaFreeAsync(ws, s));
         dim3 g((Dp + 127) / 128, (unsigned)rows);
-        k_certify<<<g, 128, 0, s>>>(C, rows, Dp, Dpk, qe, qn2, ix->Rexp, ix->Rn2, Y, ldy, cnt, flist);
+        k_certify<<<g, 128, 0, s>>>(C, rows, Dp, Dpk, qe, qn2, ix->Rexp, ix->Rn2, Y, ldy, fl);
         CRISP_LAUNCH();
     } else {
         static std::mutex amu;
@@ -575,11 +620,20 @@ void rotate_rows_imma(const crisp_index *ix, const float *X, int64_t rows, int64
         const CUtensorMap mA = make_map_u8(Qcat, (uint64_t)SL * Dpk, (uint64_t)rows, tc::BK, tc::BM);
         const CUtensorMap mB = make_map_u8(ix->Rsl, (uint64_t)SL * Dpk, (uint64_t)Dpk, tc::BK, tc::BN);
         dim3 g((unsigned)(Dpk / tc::BN), (unsigned)((rows + tc::BM - 1) / tc::BM));
-        tc::k_rot_tc<<<g, tc::THREADS_TC, smem, s>>>(mA, mB, rows, Dp, Dpk, qe, qn2, ix->Rexp, ix->Rn2, Y, ldy, cnt,
-                                                     flist);
+        tc::k_rot_tc<<<g, tc::THREADS_TC, smem, s>>>(mA, mB, rows, Dp, Dpk, qe, qn2, ix->Rexp, ix->Rn2, Y, ldy, fl);
         CRISP_LAUNCH();
     }
-    k_recompute<<<148 * 8, 128, 0, s>>>(cnt, flist, Dp, X, ldx, ix->Rt, Y, ldy);
+    {
+        const int xsm = Dp * 4;
+        if (xsm > 48 * 1024) {
+            static std::mutex rmu;
+            std::lock_guard<std::mutex> lk(rmu);
+            CRISP_CUDA(cudaFuncSetAttribute(k_recompute_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, xsm));
+        }
+        k_recompute_rows<<<(unsigned)rows, 32, xsm, s>>>(fl.rowcnt, fl.rowlist, rows, Dp, X, ldx, ix->Rt, Y, ldy);
+        CRISP_LAUNCH();
+    }
+    k_recompute<<<148 * 8, 128, 0, s>>>(cnt + 1, fl.flist, Dp, X, ldx, ix->Rt, Y, ldy);
     CRISP_LAUNCH();
     if (nfall) CRISP_CUDA(cudaMemcpyAsync(nfall, cnt, 8, cudaMemcpyDeviceToDevice, s));
     // CRISP_IMMA_STATS=1: report the uncertified outputs on stderr (diagnostics; syncs)
