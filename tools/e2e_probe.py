@@ -24,7 +24,7 @@ X, Qd = w.base(c["N"]), w.queries(c["Q"])
 Q, D, k = Qd.shape[0], Qd.shape[1], c["k"]
 ix = crisp.Index.build(X, op["M"], K=50, seed=op.get("seed", 1))
 mp = op["modes"][1]
-ix.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=40)
+ix.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
 qh = torch.empty((Q, D), dtype=torch.float32).pin_memory()
 qh.copy_(Qd.cpu())
 qn = qh.numpy()
