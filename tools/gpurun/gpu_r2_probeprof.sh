@@ -1,0 +1,3 @@
+export PROBE_PF=20
+timeout 600 python tools/one_search.py 4 1 1 > gpurun_out/p1p.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_probe -s 0 -c 1 -o gpurun_out/s3_probe_full python tools/one_search.py 4 1 1 > gpurun_out/ncu_probe.log 2>&1; echo ncu_rc=$?
