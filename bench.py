@@ -411,7 +411,9 @@ def run_crisp(args):
             torch.cuda.synchronize()
             crisp.stage_times(reset=True)
             crisp.search_counters(reset=True)
-            crisp.set_stage_timing(True)
+            # the timed steps record the stage events only (no tally kernels in the timed work);
+            # the work counters of one step come from an extra step after the timed region
+            crisp.set_stage_timing(2)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if world > 1:
                 dist.barrier()
@@ -429,7 +431,12 @@ def run_crisp(args):
             time.sleep(0.3)  # let the sample of the region's last 200 ms arrive
         ms = e0.elapsed_time(e1)
         st = crisp.stage_times(reset=True)
-        cnt = crisp.search_counters(reset=True)
+        crisp.set_stage_timing(1)
+        crisp.search_counters(reset=True)
+        step()
+        torch.cuda.synchronize()
+        crisp.stage_times(reset=True)
+        cnt = {kk: v * K for kk, v in crisp.search_counters(reset=True).items()}  # K identical steps
         crisp.set_stage_timing(False)
         if world > 1:
             t = torch.tensor([ms], dtype=torch.float64, device=dev)

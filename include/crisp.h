@@ -301,7 +301,10 @@ crisp_status crisp_export(const crisp_index *idx, crisp_export_t *out);
  * each stage on its stream and accumulates the device time per stage (ms) into
  * a per-thread table; crisp_stage_times synchronises on those events, copies up
  * to n entries (stage order: 0 transform, 1 probe a1+a2, 2 count+select a3+a4,
- * 3 fallback, 4 hamming+verify a4/a5, 5 merge) and, if reset != 0, clears it. */
+ * 3 fallback, 4 hamming+verify a4/a5, 5 merge) and, if reset != 0, clears it.
+ * on = 1 also accumulates the work counters of crisp_search_counters (extra
+ * tally kernels in the searched stream); on = 2 records the stage events only;
+ * 0 turns both off. */
 crisp_status crisp_set_stage_timing(int32_t on);
 crisp_status crisp_stage_times(double *ms, int32_t n, int32_t reset);
 

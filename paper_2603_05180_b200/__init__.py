@@ -436,8 +436,10 @@ def merge_topk(d64_dev, ids_dev, out_d64, out_d, out_ids, stream_ptr: int = 0):
                                   C.c_void_p(stream_ptr)))
 
 
-def set_stage_timing(on: bool):
-    _check(lib().crisp_set_stage_timing(1 if on else 0))
+def set_stage_timing(on):
+    """crisp_set_stage_timing: True / 1 stage events + work counters, 2 stage
+    events only, False / 0 off."""
+    _check(lib().crisp_set_stage_timing(int(on) if not isinstance(on, bool) else (1 if on else 0)))
 
 
 def stage_times(reset: bool = True) -> dict:

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "crisp_internal.cuh"
@@ -528,16 +529,19 @@ static crisp_status search_impl(const crisp_index *ix, const float *queries, int
         // stream), so order it after all of it, as crisp_build does
         if (is_device_ptr(queries) || is_device_ptr(out_ids) || (out_d && is_device_ptr(out_d)))
             CRISP_CUDA(cudaDeviceSynchronize());
-        // host buffers: stream-ordered device staging (H2D in, D2H out)
-        cudaStream_t st;
-        CRISP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        // host buffers: stream-ordered device staging (H2D in, D2H out) on this host thread's
+        // own stream for the device (kept for the thread's lifetime: the pool then reuses the
+        // previous call's scratch on the same stream; measured with a fresh stream per call:
+        // occasional 10-15 ms calls at cfg4)
+        static thread_local std::map<int, cudaStream_t> tl_streams;
+        cudaStream_t &st = tl_streams[ix->device];
+        if (!st) CRISP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         struct SG {
             cudaStream_t s;
             std::vector<void *> v;
             ~SG() {
                 for (void *p : v) cudaFreeAsync(p, s);
                 cudaStreamSynchronize(s);
-                cudaStreamDestroy(s);
             }
         } sg{st, {}};
         auto stage = [&](size_t bytes) {

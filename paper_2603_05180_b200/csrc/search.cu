@@ -3870,7 +3870,8 @@ struct StageEv {
 };
 static thread_local std::vector<StageEv> g_events;
 static thread_local double g_stage_ms[8];  // 0 transform 1 probe 2 count 3 fallback 4 verify 5 merge 6 hamming
-static std::atomic<bool> g_timing{false};  // process-wide switch (crisp_set_stage_timing); tables are per thread
+static std::atomic<bool> g_timing{false};    // process-wide switch (crisp_set_stage_timing); tables are per thread
+static std::atomic<bool> g_counters{false};  // the work counters (k_stats, probe and filter tallies) as well
 static thread_local int64_t g_launches = 0;  // kernels of this library launched by searches on this thread
 
 bool stage_timing_on() { return g_timing; }
@@ -4280,7 +4281,7 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
         k_probe<<<g, THREADS, w.probe_smem, s>>>(w.qrot, pitch, r0, r1, ix->cb, M, K, ix->dh, ix->gsize, w.probe_gs,
                                                  ix->budget, w.mode == 1 ? w.k : 0, w.act, w.act_len, w.retr,
                                                  w.probe_qpw, w.probe_cb, w.scr,
-                                                 g_timing ? d_probe_stats_ptr() : nullptr, ix->hoff);
+                                                 g_counters ? d_probe_stats_ptr() : nullptr, ix->hoff);
         CRISP_LAUNCH();
         g_launches++;
     };
@@ -4513,7 +4514,7 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
         {
             StageScope st(s, 4);
             dim3 g(w.S, (unsigned)qn);
-            unsigned long long *fst = g_timing ? d_filter_stats_ptr() : nullptr;
+            unsigned long long *fst = g_counters ? d_filter_stats_ptr() : nullptr;
             if (w.lb0) {
                 w.q8_prep(qn, s);
                 // 4 CTAs/SM (64 registers): 186.7 against 198.2 ms with 3 at cfg4
@@ -4573,19 +4574,19 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
             if (env_int("CRISP_LB_QPC", 64) >= 64)
                 k_verify_lb_blk<64><<<dim3(nblk(qn, 64), (unsigned)w.NBB), THREADS, WARPS * 64 * 4, s>>>(
                     w.qrot, pitch, ix->X, w.fa, w.pst, k, qn, w.NBB, w.DS, w.spair, w.boff, w.dbuf,
-                    g_timing ? d_filter_stats_ptr() : nullptr);
+                    g_counters ? d_filter_stats_ptr() : nullptr);
             else
                 k_verify_lb_blk<WARPS><<<dim3(nblk(qn, WARPS), (unsigned)w.NBB), THREADS, WARPS * 64 * 4, s>>>(
                     w.qrot, pitch, ix->X, w.fa, w.pst, k, qn, w.NBB, w.DS, w.spair, w.boff, w.dbuf,
-                    g_timing ? d_filter_stats_ptr() : nullptr);
+                    g_counters ? d_filter_stats_ptr() : nullptr);
         } else if (w.lbf && r > 0 && env_int("CRISP_LB_CTAS", 3) == 4)
             k_verify_rows_lb<4><<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
                                                                w.pst, k, j0, len, send, w.DS, w.dbuf, w.qperm,
-                                                               g_timing ? d_filter_stats_ptr() : nullptr);
+                                                               g_counters ? d_filter_stats_ptr() : nullptr);
         else if (w.lbf && r > 0)
             k_verify_rows_lb<3><<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
                                                                w.pst, k, j0, len, send, w.DS, w.dbuf, w.qperm,
-                                                               g_timing ? d_filter_stats_ptr() : nullptr);
+                                                               g_counters ? d_filter_stats_ptr() : nullptr);
         else if (w.ad && r > 0)  // round 0 starts with an empty top-k: nothing to prune
             k_verify_rows_ad<<<g, THREADS, w.vra_smem, s>>>(w.qrot, pitch, Dp, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst,
                                                             k, j0, len, send, w.DS, w.dbuf, w.qperm, ix->ad_eps0,
@@ -4613,12 +4614,12 @@ static void run_verify(Work &w, int64_t qn, int64_t *oi, float *od, double *od64
 }
 
 static void run_stats(Work &w, int64_t qn, cudaStream_t s) {
-    if (!g_timing) return;
+    if (!g_counters) return;
     const crisp_index *ix = w.ix;
     k_stats<<<(unsigned)qn, 128, 0, s>>>(w.act, w.act_len, ix->M, ix->K * ix->K, ix->off2, ix->NB, w.ncand, w.NS,
                                          w.mode == 1 ? w.nver : nullptr, w.fb, qn);
     CRISP_LAUNCH();
-    g_launches++;
+    // a diagnostics kernel (work counters): not counted among the search's launches
 }
 
 static void trace_candidates(Work &w, int64_t q0, int64_t qn, const crisp_trace_t *tr, cudaStream_t s) {
@@ -5214,7 +5215,7 @@ void session_gp_round(crisp_session *ss, int64_t *n_entries, cudaStream_t s) {
     if (w.lbf)
         k_verify_rows_lb<3><<<g, THREADS, w.vrl_smem, s>>>(w.qrot, pitch, ix->X, w.fa, w.cbuf, w.CAPQ, w.totals,
                                                            w.pst, k, -1, 0, 0x7fffffff, w.DS, w.dbuf, w.qperm,
-                                                           g_timing ? d_filter_stats_ptr() : nullptr);
+                                                           g_counters ? d_filter_stats_ptr() : nullptr);
     else if (w.rows4)
         k_verify_rows<true><<<g, THREADS, w.vr_smem, s>>>(w.qrot, pitch, ix->X, w.cbuf, w.CAPQ, w.totals, w.pst, -1,
                                                           0, 0x7fffffff, w.DS, w.dbuf, w.qperm);
@@ -5300,6 +5301,7 @@ void merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32
 // stage timing ABI
 extern "C" crisp_status crisp_set_stage_timing(int32_t on) {
     crisp::g_timing = on != 0;
+    crisp::g_counters = on == 1;  // 2: stage events only (no extra kernels in the timed work)
     return CRISP_OK;
 }
 

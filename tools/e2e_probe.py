@@ -47,11 +47,12 @@ for parts in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["4"]):
     for _ in range(3):
         crisp._check(crisp.lib().crisp_search(ix._h, crisp._ptr(qn), Q, k, 1, crisp._ptr(ih), crisp._ptr(dh)))
     ts = []
-    for _ in range(10):
+    for _ in range(20):
         t0 = time.perf_counter()
         crisp._check(crisp.lib().crisp_search(ix._h, crisp._ptr(qn), Q, k, 1, crisp._ptr(ih), crisp._ptr(dh)))
         ts.append(time.perf_counter() - t0)
     parts_ms[parts] = round(float(np.median(ts)) * 1e3, 3)
+    print("per-call ms", parts, [round(t * 1e3, 2) for t in ts], flush=True)
 torch.cuda.synchronize()
 hd = torch.empty((Q, D), dtype=torch.float32, device="cuda")
 t0 = time.perf_counter()
