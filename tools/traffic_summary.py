@@ -9,7 +9,7 @@ import json
 import sys
 from collections import OrderedDict
 
-STAGE = {"k_rot_tc": "transform", "k_slice_rows": "transform", "k_recompute": "transform",
+STAGE = {"k_rot_tc": "transform", "k_slice_rows": "transform", "k_recompute": "transform", "k_recompute_rows": "transform",
          "k_probe": "probe", "k_query_key": "probe", "k_act_rows": "count_select", "k_count_frag": "count_select",
          "k_count_warp": "count_select", "k_count_select": "count_select", "k_fallback": "fallback",
          "k_hamming_dense": "hamming", "k_hamming": "hamming", "k_hsort_cta": "hsort", "k_hsort": "hsort",
