@@ -555,7 +555,7 @@ def run_crisp(args):
         qn = qh.numpy()
         ih = torch.empty((Q, k), dtype=torch.int64).pin_memory().numpy()
         dh = torch.empty((Q, k), dtype=torch.float32).pin_memory().numpy()
-        for _ in range(2):
+        for _ in range(max(3, args.warmup)):  # the same warm-up as the device-timed steps
             crisp._check(crisp.lib().crisp_search(index._h, crisp._ptr(qn), Q, k, phi(head), crisp._ptr(ih),
                                                   crisp._ptr(dh)))
         t0 = time.perf_counter()
