@@ -70,7 +70,7 @@ modes = [int(m) for m in args.modes.split(",")]
 single = {}
 for mode in modes:  # the single index first (then freed: the G shard sessions need the memory)
     mp = op["modes"][mode]
-    full.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=40)
+    full.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
     ids1 = torch.empty((Q, k), dtype=torch.int64, device=dev)
     dd1 = torch.empty((Q, k), dtype=torch.float32, device=dev)
     full.search_async(Qd, k, mode, ids1, dd1, stream)
@@ -94,7 +94,7 @@ for mode in modes:
         engines = []
         for s in shards:
             s.set_global_cell_sizes(sizes)
-            s.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=40)
+            s.set_search_params(beta=mp["beta"], alpha=mp["alpha"], patience_factor=mp.get("patience_factor", 40))
             e = dist.CudaEngine(crisp, dev)
             e.index = s
             engines.append(e)
