@@ -251,6 +251,21 @@ crisp_status crisp_shard_search_finish(crisp_session *s, const int32_t *global_c
                                        int32_t G, int32_t rank, int64_t *out_ids, double *out_dist64, void *stream);
 void crisp_shard_search_free(crisp_session *s);
 
+/* a0 alone: qrot[q][0..pitch) = fl32(q R) zero-padded (the
+ * queries themselves, padded, when the index is not rotated), pitch = the
+ * stored row pitch of crisp_index_info_t.  queries: Q x D, qrot: Q x pitch
+ * fp32, both device memory; stream-ordered.  With
+ * crisp_shard_search_begin_transformed a sharded search transforms each
+ * rank's slice of the batch once and all-gathers q' instead of
+ * every rank transforming every query; the results are identical. */
+crisp_status crisp_transform_queries_async(const crisp_index *idx, const float *queries, int64_t Q, float *qrot,
+                                           void *stream);
+/* crisp_shard_search_begin with the queries already transformed (qrot: Q x
+ * pitch fp32 device memory as written by crisp_transform_queries_async). */
+crisp_status crisp_shard_search_begin_transformed(const crisp_index *idx, const float *qrot, int64_t Q, int32_t k,
+                                                  crisp_mode mode, int32_t *local_counts, crisp_session **out,
+                                                  void *stream);
+
 /* Exact global patience for Optimized Mode over G point shards (Alg. 1
  * l.22-27 with the patience rule of P:L458 applied to the union of the shards'
  * candidates, in the global (h, gid) order).  Instead

@@ -67,6 +67,7 @@ ABI_SYMBOLS = (
     "crisp_search_async", "crisp_search_shard_async", "crisp_merge_topk", "crisp_search_trace", "crisp_export",
     "crisp_set_stage_timing", "crisp_stage_times", "crisp_search_counters", "crisp_free", "crisp_last_error", "crisp_version",
     "crisp_shard_search_begin", "crisp_shard_search_hist", "crisp_shard_search_finish", "crisp_shard_search_free",
+    "crisp_transform_queries_async", "crisp_shard_search_begin_transformed",
     "crisp_shard_gp_order", "crisp_shard_gp_prepare", "crisp_shard_gp_round", "crisp_shard_gp_fetch",
     "crisp_shard_gp_replay", "crisp_shard_gp_result",
     "crisp_set_adsampling", "crisp_set_verify_filter", "crisp_exact_ceil", "crisp_cev_sample_size", "crisp_sample_rows", "crisp_build_model",
@@ -104,6 +105,8 @@ def lib():
         L.crisp_stage_times.argtypes = [vp, i32, i32]
         L.crisp_search_counters.argtypes = [vp, i32, i32]
         L.crisp_shard_search_begin.argtypes = [vp, vp, i64, i32, i32, vp, P(vp), vp]
+        L.crisp_shard_search_begin_transformed.argtypes = [vp, vp, i64, i32, i32, vp, P(vp), vp]
+        L.crisp_transform_queries_async.argtypes = [vp, vp, i64, vp, vp]
         L.crisp_shard_search_hist.argtypes = [vp, vp, vp, vp]
         L.crisp_shard_search_finish.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp]
         L.crisp_shard_gp_order.argtypes = [vp, vp, vp, i32, i32, vp, vp]
@@ -348,6 +351,20 @@ class Index:
         ss = C.c_void_p()
         _check(lib().crisp_shard_search_begin(self._h, _ptr(q_dev), int(q_dev.shape[0]), k, mode,
                                               _ptr(local_counts_dev), C.byref(ss), C.c_void_p(stream_ptr)))
+        return ss
+
+    def transform_queries(self, q_dev, qrot_dev, stream_ptr: int = 0):
+        """crisp_transform_queries_async: qrot (Q x pitch) = a0 of q (Q x D), device tensors."""
+        q_dev = _host(q_dev, np.float32)
+        _check(lib().crisp_transform_queries_async(self._h, _ptr(q_dev), int(q_dev.shape[0]), _ptr(qrot_dev),
+                                                   C.c_void_p(stream_ptr)))
+
+    def shard_begin_transformed(self, qrot_dev, k: int, mode: int, local_counts_dev, stream_ptr: int = 0):
+        """crisp_shard_search_begin_transformed: crisp_shard_search_begin on q' (Q x pitch)."""
+        ss = C.c_void_p()
+        _check(lib().crisp_shard_search_begin_transformed(self._h, _ptr(qrot_dev), int(qrot_dev.shape[0]), k, mode,
+                                                          _ptr(local_counts_dev), C.byref(ss),
+                                                          C.c_void_p(stream_ptr)))
         return ss
 
     @staticmethod

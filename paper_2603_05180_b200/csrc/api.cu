@@ -621,6 +621,37 @@ crisp_status crisp_shard_search_begin(const crisp_index *ix, const float *querie
     }
 }
 
+crisp_status crisp_transform_queries_async(const crisp_index *ix, const float *queries, int64_t Q, float *qrot,
+                                           void *stream) {
+    try {
+        CRISP_CHECK(ix && queries && qrot, "NULL argument");
+        CRISP_CHECK(Q >= 0, "Q must be >= 0");
+        CRISP_CHECK(is_device_ptr(queries) && is_device_ptr(qrot), "device pointers required");
+        CRISP_CUDA(cudaSetDevice(ix->device));
+        transform_queries(ix, queries, Q, qrot, (cudaStream_t)stream);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
+crisp_status crisp_shard_search_begin_transformed(const crisp_index *ix, const float *qrot, int64_t Q, int32_t k,
+                                                  crisp_mode mode, int32_t *local_counts, crisp_session **out,
+                                                  void *stream) {
+    try {
+        CRISP_CHECK(ix && qrot && local_counts && out, "NULL argument");
+        CRISP_CHECK(Q >= 1, "Q must be >= 1");
+        CRISP_CHECK(k >= 1 && k <= MAX_TOPK && k <= ix->N_global, "bad k");
+        CRISP_CHECK(mode == CRISP_GUARANTEED || mode == CRISP_OPTIMIZED, "bad mode");
+        CRISP_CHECK(is_device_ptr(qrot) && is_device_ptr(local_counts), "device pointers required");
+        CRISP_CUDA(cudaSetDevice(ix->device));
+        *out = session_begin(ix, qrot, Q, k, (int)mode, local_counts, (cudaStream_t)stream, true);
+        return CRISP_OK;
+    } catch (Err &e) {
+        return e.st;
+    }
+}
+
 crisp_status crisp_shard_search_hist(crisp_session *s, const int32_t *global_counts, int32_t *local_hist,
                                      void *stream) {
     try {

@@ -171,7 +171,8 @@ void search(const crisp_index *ix, const float *queries_dev, int64_t Q, int32_t 
 void merge_topk(const double *d, const int64_t *ids, int32_t G, int64_t Q, int32_t k, double *out_d64, float *out_d,
                 int64_t *out_ids, cudaStream_t s);
 crisp_session *session_begin(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode,
-                             int32_t *local_counts, cudaStream_t s);
+                             int32_t *local_counts, cudaStream_t s, bool transformed = false);
+void transform_queries(const crisp_index *ix, const float *queries, int64_t Q, float *qrot, cudaStream_t s);
 void session_hist(crisp_session *ss, const int32_t *gcount, int32_t *lhist, cudaStream_t s);
 void session_finish(crisp_session *ss, const int32_t *gcount, const int32_t *allhist, int32_t G, int32_t rank,
                     int64_t *out_ids, double *out_d64, cudaStream_t s);

@@ -4265,7 +4265,8 @@ struct Work {
 };
 
 // a0, a1+a2, a3+a4 (count/select) for queries [0, qn) of the chunk
-static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s, const float *hq = nullptr) {
+static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s, const float *hq = nullptr,
+                      bool transformed = false) {
     const crisp_index *ix = w.ix;
     const int M = ix->M, K = ix->K, KK = K * K, NB = ix->NB, pitch = ix->pitch;
     // a0 (and a1+a2) in parts; with host queries (hq: the source of the device
@@ -4285,7 +4286,10 @@ static void run_front(Work &w, const float *queries, int64_t qn, cudaStream_t s,
         CRISP_LAUNCH();
         g_launches++;
     };
-    {
+    if (transformed) {  // q' given (crisp_transform_queries_async): rows of pitch floats
+        StageScope st(s, 0);
+        CRISP_CUDA(cudaMemcpyAsync(w.qrot, queries, (size_t)qn * pitch * 4, cudaMemcpyDeviceToDevice, s));
+    } else {
         StageScope st(s, 0);
         cudaStream_t cs = nullptr;
         cudaEvent_t ev[17] = {};
@@ -4823,8 +4827,25 @@ struct crisp_session {
 
 namespace crisp {
 
+// a0 alone for Q queries into qrot (Q x pitch): the zero-padded copy, then the certified
+// int8 tensor-core transform when the index is rotated (as run_front)
+void transform_queries(const crisp_index *ix, const float *queries, int64_t Q, float *qrot, cudaStream_t s) {
+    if (Q <= 0) return;
+    const int pitch = ix->pitch;
+    float *qpad = qrot;
+    if (ix->rotated) CRISP_CUDA(cudaMallocAsync(&qpad, (size_t)Q * pitch * 4, s));
+    k_prep_queries<<<nblk(Q * pitch, 256), 256, 0, s>>>(queries, Q, ix->D, pitch, qpad);
+    CRISP_LAUNCH();
+    g_launches++;
+    if (ix->rotated) {
+        rotate_rows(const_cast<crisp_index *>(ix), qpad, Q, pitch, qrot, pitch, s);
+        g_launches += 3;
+        CRISP_CUDA(cudaFreeAsync(qpad, s));
+    }
+}
+
 crisp_session *session_begin(const crisp_index *ix, const float *queries, int64_t Q, int32_t k, int mode,
-                             int32_t *local_counts, cudaStream_t s) {
+                             int32_t *local_counts, cudaStream_t s, bool transformed) {
     CRISP_CHECK(Q <= 65535, "a shard session takes at most 65535 queries (split the batch)");
     const int64_t cap = candidate_capacity(ix, mode, k, false);
     const int64_t ws = ix->workspace_bytes > 0 ? ix->workspace_bytes : default_workspace();
@@ -4832,7 +4853,7 @@ crisp_session *session_begin(const crisp_index *ix, const float *queries, int64_
                 "shard session scratch exceeds the workspace (split the batch)");
     Work *w = new Work(ix, k, mode, std::max<int64_t>(Q, 1), cap, false, false, s);
     try {
-        run_front(*w, queries, Q, s);
+        run_front(*w, queries, Q, s, nullptr, transformed);
         k_local_counts<<<nblk(Q, 256), 256, 0, s>>>(w->ncand, w->NS, Q, local_counts);
         CRISP_LAUNCH();
         g_launches++;

@@ -15,6 +15,8 @@ Collective call sites:
          histograms, then per verification round all-gathers of the entries that
          may improve a top-k: the patience rule runs over the GLOBAL (h, gid)
          order, so the result equals a single index for every G
+  N9     all-gather of q' (sharded_transform): each rank runs a0 on its slice of
+         the batch only
 
 The orchestration is written against a small engine interface so the same
 code runs with the CUDA engine (NCCL over NVLink) and, in the CPU tests, with
@@ -64,6 +66,20 @@ class CudaEngine:
         d64 = torch.empty((Q, k), dtype=torch.float64, device=q_dev.device)
         self.index.search_shard_async(q_dev, k, mode, ids, d64, stream)
         return ids, d64
+
+    # a0 alone (crisp_transform_queries_async): q' of a slice of the batch, rows of pitch floats
+    def transform(self, q_dev, stream=0):
+        pitch = self.index.info()["pitch"]
+        out = torch.empty((q_dev.shape[0], pitch), dtype=torch.float32, device=q_dev.device)
+        if q_dev.shape[0]:
+            self.index.transform_queries(q_dev.contiguous(), out, stream)
+        return out
+
+    def begin_transformed(self, qrot, k, mode, stream=0):
+        counts = torch.empty(qrot.shape[0], dtype=torch.int32, device=qrot.device)
+        self._ss = self.index.shard_begin_transformed(qrot, k, mode, counts, stream)
+        self._Q, self._k = qrot.shape[0], k
+        return counts
 
     # phased shard search (exact global fallback), see include/crisp.h
     def begin(self, q_dev, k, mode, stream=0):
@@ -222,13 +238,41 @@ def search_step(engine, q_dev, k, mode, stream=0):
     return engine.merge(gd, gi, stream)
 
 
+def sharded_transform(engine, q_dev, stream=0):
+    """a0 sharded by query (N9): rank r transforms rows [r P, (r+1) P) of the batch (P =
+    ceil(Q/G)) and one all-gather assembles q' for every rank, instead of every rank
+    transforming every query; q' is bit-exact either way, so the results are unchanged."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    Q = q_dev.shape[0]
+    per = (Q + world - 1) // world
+    lo, hi = min(Q, rank * per), min(Q, (rank + 1) * per)
+    part = engine.transform(q_dev[lo:hi], stream)
+    pad = torch.zeros((per, part.shape[1]), dtype=part.dtype, device=part.device)
+    pad[: hi - lo] = part
+    out = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(out, pad)
+    return torch.cat(out)[:Q].contiguous()
+
+
+def _begin(engine, q_dev, k, mode, stream=0):
+    """The phased search's first phase: with G > 1 and an engine that supports it, on q'
+    transformed once across the ranks (sharded_transform; CRISP_SHARD_A0=0 keeps every
+    rank transforming the whole batch)."""
+    import os
+
+    if (dist.get_world_size() > 1 and hasattr(engine, "begin_transformed")
+            and os.environ.get("CRISP_SHARD_A0", "1") != "0"):
+        return engine.begin_transformed(sharded_transform(engine, q_dev, stream), k, mode, stream)
+    return engine.begin(q_dev, k, mode, stream)
+
+
 def search_step_exact(engine, q_dev, k, mode, stream=0):
     """One sharded search with the EXACT global underflow fallback: N5
     all-reduce of |C_q|, all-gather of the V histograms of underflowing
     queries, then a5 on each shard and N7 + a6.  For phi=0 the result equals
     the single index for every G."""
     world, rank = dist.get_world_size(), dist.get_rank()
-    counts = engine.begin(q_dev, k, mode, stream)
+    counts = _begin(engine, q_dev, k, mode, stream)
     dist.all_reduce(counts, op=dist.ReduceOp.SUM)
     hist = engine.hist(counts, stream)
     all_h = [torch.empty_like(hist) for _ in range(world)]
@@ -255,7 +299,7 @@ def search_step_global(engine, q_dev, k, mode, gid_bases, stream=0):
     if mode != 1:
         return search_step_exact(engine, q_dev, k, mode, stream)
     world, rank = dist.get_world_size(), dist.get_rank()
-    counts = engine.begin(q_dev, k, mode, stream)
+    counts = _begin(engine, q_dev, k, mode, stream)
     dist.all_reduce(counts, op=dist.ReduceOp.SUM)
     hist = engine.hist(counts, stream)
     hh = engine.gp_order(counts, _all_gather_stack(hist), world, rank, stream)
@@ -273,11 +317,20 @@ def search_step_global(engine, q_dev, k, mode, gid_bases, stream=0):
     return ids, d64.to(torch.float32)
 
 
-def emulate_global_search(engines, gid_bases, q_dev, k, mode, stream=0, stats=None):
+def emulate_global_search(engines, gid_bases, q_dev, k, mode, stream=0, stats=None, sharded_a0=False):
     """The search_step_global protocol for G shard engines in ONE process (the
-    collectives done by concatenation): a single-GPU emulation for the tests."""
+    collectives done by concatenation): a single-GPU emulation for the tests.
+    sharded_a0: each engine transforms its slice of the batch (N9) and every
+    engine begins on the concatenated q'."""
     G = len(engines)
-    counts = [e.begin(q_dev, k, mode, stream) for e in engines]
+    if sharded_a0:
+        Q = q_dev.shape[0]
+        per = (Q + G - 1) // G
+        qrot = torch.cat([e.transform(q_dev[min(Q, r * per):min(Q, (r + 1) * per)], stream)
+                          for r, e in enumerate(engines)]).contiguous()
+        counts = [e.begin_transformed(qrot, k, mode, stream) for e in engines]
+    else:
+        counts = [e.begin(q_dev, k, mode, stream) for e in engines]
     gc = torch.stack(counts).sum(0).to(torch.int32)
     hists = torch.stack([e.hist(gc, stream) for e in engines])
     if mode != 1:

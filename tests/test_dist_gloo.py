@@ -47,6 +47,15 @@ class OracleEngine:
         ids, d, _ = oracle.search(self.ix, q.numpy(), k, mode, self.B, self.tau, patience_factor=0)
         return torch.from_numpy(ids), torch.from_numpy(d)
 
+    # a0 alone: the oracle engine's "q'" is the query itself (its search rotates internally),
+    # so the query-sharded a0 of dist.sharded_transform is exercised for its slicing and the
+    # all-gather that reassembles the batch
+    def transform(self, q, stream=0):
+        return q.clone()
+
+    def begin_transformed(self, qrot, k, mode, stream=0):
+        return self.begin(qrot, k, mode, stream)
+
     # phased protocol (exact global fallback), emulated on the oracle
     def begin(self, q, k, mode, stream=0):
         import oracle

@@ -5,7 +5,8 @@ dataset (shared R and codebooks, summed cell sizes) run the protocol on one GPU
 (dist.emulate_global_search: the collectives done by concatenation); ids and
 distances must equal the single index over all rows and the oracle's search,
 for every G, with and without the verification filter, with the exact global
-fallback and with many short rounds."""
+fallback, with many short rounds, and with a0 sharded by query (each
+shard transforms its slice of the batch, q' concatenated: N9)."""
 import numpy as np
 import pytest
 
@@ -52,7 +53,7 @@ def shard_indexes(crisp, X, ox, G):
 
 
 @pytest.mark.parametrize("G", [2, 3])
-@pytest.mark.parametrize("variant", ["exact", "filter", "short_rounds"])
+@pytest.mark.parametrize("variant", ["exact", "filter", "short_rounds", "sharded_a0"])
 def test_global_patience_equals_single_index(crisp, case, monkeypatch, G, variant):
     import torch
 
@@ -82,7 +83,8 @@ def test_global_patience_equals_single_index(crisp, case, monkeypatch, G, varian
             e.index = s
             engines.append(e)
         st = {}
-        ids_g, d_g = dist.emulate_global_search(engines, bases, q_dev, k, 1, stats=st)
+        ids_g, d_g = dist.emulate_global_search(engines, bases, q_dev, k, 1, stats=st,
+                                                sharded_a0=variant == "sharded_a0")
         if variant == "short_rounds" and k == 10:  # |C_q| ~ 8k, stops up to ~1100: many 64-position windows
             assert st["rounds"] >= 10, st
         torch.cuda.synchronize()
