@@ -95,3 +95,32 @@ def test_global_patience_equals_single_index(crisp, case, monkeypatch, G, varian
     for s in shards:
         s.free()
     single.set_verify_filter(True)
+
+
+@pytest.mark.parametrize("rotation", [0, 1])
+def test_transform_queries_is_the_searchs_a0(crisp, rotation):
+    """crisp_transform_queries_async writes the q' a search computes (the
+    oracle's fl32(q R), zero-padded to the row pitch; the padded queries when
+    the index is not rotated), for a slice too (the sharded a0 of N9), and Q = 0
+    is a no-op."""
+    import torch
+
+    from paper_2603_05180_b200 import dist
+
+    X, Qv, ox = make_case(cfg=2, N=6000, D=90, Q=37, M=4, K=12, rotation=rotation, seed=7)
+    ix = build_gpu(crisp, X, ox)
+    pitch = ix.info()["pitch"]
+    ix.set_search_params(budget=500, tau=2, patience_factor=3)
+    _, _, t = ix.trace(Qv, 5, 1)
+    e = dist.CudaEngine(crisp, torch.device("cuda", 0))
+    e.index = ix
+    q_dev = torch.from_numpy(Qv).cuda()
+    full = e.transform(q_dev)
+    part = e.transform(q_dev[10:29])
+    torch.cuda.synchronize()
+    assert full.shape == (37, pitch) and np.array_equal(full.cpu().numpy()[:, : ox["Dp"]], t["qrot"])
+    assert np.array_equal(full.cpu().numpy()[:, : ox["Dp"]], oracle.search(ox, Qv, 5, 1, 500, 2, trace=True,
+                                                                          patience_factor=3)[2]["qrot"])
+    assert np.array_equal(part.cpu().numpy(), full.cpu().numpy()[10:29])
+    assert e.transform(q_dev[:0]).shape == (0, pitch)
+    ix.free()
