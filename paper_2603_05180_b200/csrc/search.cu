@@ -157,14 +157,18 @@ __global__ void __launch_bounds__(THREADS) k_probe(const float *__restrict__ qro
                 }
             }
             if (__any_sync(0xffffffffu, past)) return false;
-#pragma unroll
-            for (int off = 16; off; off >>= 1) {
-                double oc = __shfl_xor_sync(0xffffffffu, bc, off);
-                int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                if (oc < bc || (oc == bc && oi < bi)) {
-                    bc = oc;
-                    bi = oi;
-                }
+            // warp argmin of (cost, i) by three 32-bit min reductions: the costs are
+            // non-negative doubles (sums of dist64 values, or +inf), whose bit patterns order
+            // as unsigned integers: min of the high words, then of the low words among the
+            // lanes at that high word, then the smallest i among the lanes at that cost
+            {
+                const unsigned long long cb = (unsigned long long)__double_as_longlong(bc);
+                const unsigned hi = (unsigned)(cb >> 32), lo = (unsigned)cb;
+                const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+                const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+                const bool at = hi == mh && lo == ml;
+                bi = (int)__reduce_min_sync(0xffffffffu, at ? (unsigned)bi : 0x7fffffffu);
+                bc = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
             }
             const int j = col[bi];
             const int cell = pa[bi] * K + pb[j];
