@@ -4478,7 +4478,9 @@ static void run_order(Work &w, int64_t qn, cudaStream_t s) {
             // LIST: phase B visits only the listed qualifying elements (when the
             // sorted prefix is short: k = 10 configurations)
             const int lim = w.full_order ? 0x7fffffff : w.order_end();
-            if (lim <= 4096)
+            // (measured at cfg4, k = 100, cut 7072: LIST 1.67 against 1.83 ms; the listing falls
+            // back to the scan by itself when the order row's tail cannot hold the list)
+            if (lim <= env_int("CRISP_HSORT_LIST_MAX", 16384))
                 k_hsort_cta<true><<<(unsigned)qn, THREADS, w.hsort_cta_smem, s>>>(
                     w.ncand, w.cbase, NB, Dp, w.ghist, w.pool, w.hbuf, w.CAPQ, w.cbuf, w.totals, lim);
             else
