@@ -397,12 +397,16 @@ def test_patience_rounds_and_tail(crisp, monkeypatch, first, rounds, rmin):
         assert np.array_equal(ids2, ids) and np.array_equal(d2, d), f"untraced pf={pf}"
 
 
+@pytest.mark.parametrize("parts", ["3", "5", "3eq"])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_host_buffers_match_device(crisp, mode):
+def test_host_buffers_match_device(crisp, monkeypatch, mode, parts):
     """crisp_search with host buffers (the H2D copy overlapped with the query
-    transform and the probe, in parts) returns what the device-pointer call
-    returns."""
+    transform and the probe, in parts of sizes 1 : 2 : ... : P, or equal parts)
+    returns what the device-pointer call returns."""
     import torch
+
+    monkeypatch.setenv("CRISP_H2D_PARTS", parts.rstrip("eq"))
+    monkeypatch.setenv("CRISP_H2D_TRI", "0" if parts.endswith("eq") else "1")
 
     X, _, ox = make_case(cfg=1, N=20000, Q=10, seed=3)
     Qv = synth.Workload(1).queries(3000).numpy()

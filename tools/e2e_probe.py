@@ -43,7 +43,9 @@ torch.cuda.synchronize()
 t_dev = (time.perf_counter() - t0) / 10
 parts_ms = {}
 for parts in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["4"]):
-    os.environ["CRISP_H2D_PARTS"] = parts
+    tri = parts.startswith("t")
+    os.environ["CRISP_H2D_TRI"] = "1" if tri else "0"
+    os.environ["CRISP_H2D_PARTS"] = parts.lstrip("t")
     for _ in range(3):
         crisp._check(crisp.lib().crisp_search(ix._h, crisp._ptr(qn), Q, k, 1, crisp._ptr(ih), crisp._ptr(dh)))
     ts = []
