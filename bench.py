@@ -111,6 +111,17 @@ class Clocks:
         return out
 
 
+def smem_update_peak():
+    """(lane updates/s, source) of random-word red.shared.add measured in-repo
+    (tools/peaks/smem_red_peak.cu -> profiles/r02_smem_peak.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r02_smem_peak.json")
+    try:
+        with open(p) as f:
+            return json.load(f)["red_random"]["lane_updates_per_s"], "measured in-repo (profiles/r02_smem_peak.json)"
+    except Exception:
+        return None
+
+
 def l2_peak():
     """In-repo L2 -> SM read bandwidth (tools/measure_peaks.py), if measured."""
     f = os.path.join(ROOT, "profiles", "r02_peaks.json")
@@ -483,7 +494,7 @@ def run_crisp(args):
                                 "achieved_gbs": cb_ / (st["count_select"] / K * 1e-3) / 1e9}
             if phi(mode) == 1 and not fused and st.get("hamming", 0) > 0:
                 hb = cnt["candidates"] * 8 * ((info["padded_D"] + 63) // 64) / K  # SURVEY 8(d) B_ham
-                kernels["hamming"] = {"kernel": "k_hamming+k_hamming_dense",
+                kernels["hamming"] = {"kernel": "k_qcodes+k_hamming_seg(or k_hamming_dense)+k_hhist",
                                       "bytes_per_step": hb, "ms_per_step": st["hamming"] / K,
                                       "achieved_gbs": hb / (st["hamming"] / K * 1e-3) / 1e9}
         l2 = l2_peak()
@@ -499,6 +510,13 @@ def run_crisp(args):
                 # bound by the shared-memory atomic unit (ncu: 3.7 wavefronts per red.shared, DESIGN 7):
                 # the HBM fraction of its id stream is reported, the stream does not bind
                 kk["bound"] = "shared-memory reductions (atomic unit); frac = id stream / HBM"
+                sp = smem_update_peak()
+                if sp:
+                    # one counter update per streamed id (Alg. 1 l.14-17); the ceiling is the measured
+                    # rate of random-word red.shared.add on this GPU in the count's launch shape
+                    ups = cnt["ids_streamed"] / K / (kk["ms_per_step"] * 1e-3)
+                    kk["updates_per_s"], kk["update_peak_per_s"], kk["update_peak_source"] = ups, sp[0], sp[1]
+                    kk["update_frac"] = ups / sp[0]
         dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"]) if kernels else None
         traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic.json")
