@@ -507,9 +507,9 @@ def run_crisp(args):
                 kk["bound"], kk["peak"], kk["peak_source"] = "l2", l2[0], l2[1]
                 kk["frac_of_peak"] = kk["achieved_gbs"] / l2[0]
             elif name_ == "count":
-                # bound by the shared-memory atomic unit (ncu: 3.7 wavefronts per red.shared, DESIGN 7):
-                # the HBM fraction of its id stream is reported, the stream does not bind
-                kk["bound"] = "shared-memory reductions (atomic unit); frac = id stream / HBM"
+                # issue / LSU-latency bound (DESIGN 7: ncu with source, 0.17 of the measured red.shared
+                # ceiling): the HBM fraction of its id stream is reported, the stream does not bind
+                kk["bound"] = "issue/LSU latency (shared-memory reductions); frac = id stream / HBM, update_frac = updates / measured red.shared ceiling"
                 sp = smem_update_peak()
                 if sp:
                     # one counter update per streamed id (Alg. 1 l.14-17); the ceiling is the measured
