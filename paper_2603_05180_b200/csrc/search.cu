@@ -1186,31 +1186,42 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
         }
         __syncthreads();  // the chunk's table is re-staged next
     }
+    // a4: C in ascending id from the bitmap; warp w owns the contiguous bitmap words [w wpw, (w+1) wpw)
+    const int nwords = BF / 32, wpw = nwords / CF_WARPS;  // wpw <= 128 (BF <= 131072 ids at 32 warps)
+    uint32_t wr[4] = {0u, 0u, 0u, 0u};  // SWAR: this warp's words lane + 32 r, kept in registers
     if (SWAR) {
         // CRISP_COUNT_SWAR=1: the counts above are fire-and-forget reductions; C = {x : V[x] >= tau}
-        // (Alg. 1 l.18) from the final counters, 32 per bitmap word: bit 7 of ((c | 0x80) - tau)
-        // is [c >= tau] for c < 128 (M < 64), else a per-byte compare; one multiply gathers a
-        // word's four flags
+        // (Alg. 1 l.18) from the final counters (the chunk loop ended on a barrier), 32 per bitmap
+        // word: bit 7 of ((c | 0x80) - tau) is [c >= tau] for c < 128 (M < 64), else a per-byte
+        // compare; one multiply gathers a word's four flags.  Each warp scans the counters of its
+        // own bitmap words and keeps them in registers for the listing below (no bitmap round trip
+        // through shared memory, no barrier)
         const uint32_t t4 = (uint32_t)tau * 0x01010101u;
-        for (int wi = tid; wi < BF / 32; wi += CF_THREADS) {
-            const uint4 a = ((const uint4 *)cw)[2 * wi], b = ((const uint4 *)cw)[2 * wi + 1];
-            const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            uint32_t word = 0u;
 #pragma unroll
-            for (int t = 0; t < 8; t++) {
-                const uint32_t f = M < 64 ? (((v[t] | 0x80808080u) - t4) >> 7) & 0x01010101u
-                                          : __vcmpgeu4(v[t], t4) & 0x01010101u;
-                word |= ((f * 0x10204080u) >> 28) << (4 * t);
+        for (int r = 0; r < 4; r++) {
+            const int wi = warp * wpw + lane + 32 * r;
+            if (lane + 32 * r < wpw) {
+                const uint4 a = ((const uint4 *)cw)[2 * wi], b = ((const uint4 *)cw)[2 * wi + 1];
+                const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                uint32_t word = 0u;
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    const uint32_t f = M < 64 ? (((v[t] | 0x80808080u) - t4) >> 7) & 0x01010101u
+                                              : __vcmpgeu4(v[t], t4) & 0x01010101u;
+                    word |= ((f * 0x10204080u) >> 28) << (4 * t);
+                }
+                wr[r] = word;
             }
-            bm[wi] = word;
         }
-        __syncthreads();
     }
-    // a4: C in ascending id from the crossing bitmap; each warp compacts a contiguous word range
-    const int nwords = BF / 32, wpw = nwords / CF_WARPS;
     {
         int c = 0;
-        for (int i = lane; i < wpw; i += 32) c += __popc(bm[warp * wpw + i]);
+        if (SWAR) {
+#pragma unroll
+            for (int r = 0; r < 4; r++) c += __popc(wr[r]);
+        } else {
+            for (int i = lane; i < wpw; i += 32) c += __popc(bm[warp * wpw + i]);
+        }
 #pragma unroll
         for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
         if (lane == 0) S.wtot[warp] = c;
@@ -1229,9 +1240,11 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
     int running = S.base;
     for (int w2 = 0; w2 < warp; w2++) running += S.wtot[w2];
     int32_t *outp = pool + q * CAPQ;
-    for (int i0 = 0; i0 < wpw; i0 += 32) {
-        const int i = i0 + lane;
-        uint32_t word = i < wpw ? bm[warp * wpw + i] : 0u;
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const int i0 = 32 * r, i = i0 + lane;
+        if (i0 >= wpw) break;
+        uint32_t word = SWAR ? wr[r] : (i < wpw ? bm[warp * wpw + i] : 0u);
         const int c = __popc(word);
         int inc = c;
 #pragma unroll
