@@ -1042,6 +1042,7 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
             s1[u] = ok ? __ldg(o + c1) : 0;
         }
         long long v[CF_EPT], ex[CF_EPT], carry = 0;
+        const unsigned lemask_st = (2u << lane) - 1u;  // lanes <= this lane
         int g0[CF_EPT];  // absolute ids[] position of the fragment's first id
 #pragma unroll
         for (int u = 0; u < CF_EPT; u++) {
@@ -1050,14 +1051,18 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
             // the fragment's 16-byte quads of ids[] (aligned to absolute position 4j)
             const int nq = ((g0[u] + len + 3) >> 2) - (g0[u] >> 2);
             v[u] = len > 0 ? (((long long)nq << 16) | 1) : 0;
-            long long x = v[u];
+            // the packed (quads << 16 | non-empty) prefix from a 32-bit scan of the quads and a
+            // ballot of the non-empty fragments (half the shuffles of a 64-bit scan)
+            const int vq = len > 0 ? nq : 0;
+            int x = vq;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
-                const long long y = __shfl_up_sync(0xffffffffu, x, off);
+                const int y = __shfl_up_sync(0xffffffffu, x, off);
                 if (lane >= off) x += y;
             }
-            ex[u] = carry + x - v[u];
-            carry += __shfl_sync(0xffffffffu, x, 31);
+            const unsigned bal = __ballot_sync(0xffffffffu, len > 0);
+            ex[u] = carry + ((long long)(x - vq) << 16) + __popc(bal & (lemask_st >> 1));
+            carry += ((long long)__shfl_sync(0xffffffffu, x, 31) << 16) + __popc(bal);
         }
         if (lane == 0) S.wtot64[warp] = carry;
         __syncthreads();
