@@ -1005,6 +1005,7 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sm_dummy = sm_bm + (uint32_t)(BF / 8) + 4u * (uint32_t)lane;  // this lane's dummy word
     const uint32_t bbase = (uint32_t)sb * (uint32_t)BF;
+    const uint32_t cw_rel = sm_cw - bbase;  // + (x & ~3): the counter word of id x (BF % 4 == 0)
     const int c0 = sb * F, c1 = min(NB, c0 + F);  // off2 columns bounding the block
     for (int i = tid; i < (BF + BF / 8 + 128) / 16; i += CF_THREADS) ((uint4 *)smraw)[i] = make_uint4(0, 0, 0, 0);
     const int Etot = __ldg(etot + q);
@@ -1136,7 +1137,7 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                 const bool ok = p < Q1;
                 qpn = ok ? qs + (p - qx) : 0;
                 gn0 = ok ? (int)((uint32_t)gw & ~WFLAG) : 1;
-                gn1 = ok ? ge : 0;
+                gn1 = ok ? ge : 1;  // an empty range [1, 1) for lanes past Q1
                 wn = 1u + ((uint32_t)gw >> 31);
                 qn = __ldg((const uint4 *)ids + qpn);
                 // slide the window to the fragment of this step's last quad
@@ -1165,17 +1166,26 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                 const uint32_t w = wn;
                 if (pp + 32 < Q1) issue(pp + 32);
                 const uint32_t xs[4] = {qv.x, qv.y, qv.z, qv.w};
+                if constexpr (SWAR) {
+                    // an element outside its fragment (quad edges, lanes past Q1) adds to the lane's
+                    // dummy word (never read); bbase is a multiple of 4, so the counter word of x is
+                    // sm_cw - bbase + (x & ~3) and its byte x & 3: the shift (x << 3) mod 32 by a
+                    // wrapping funnel shift (89 instead of 99 instructions per step)
+                    const int a = lo - q0, b = hi - q0;
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        red_add_sh_nc(e >= a && e < b ? cw_rel + (xs[e] & ~3u) : sm_dummy,
+                                      __funnelshift_l(0u, w, xs[e] << 3));
+                } else {
                 uint32_t ov[4], inc[4];
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
                     const bool ok = q0 + e >= lo && q0 + e < hi;
                     inc[e] = ok ? w : 0u;
                     const uint32_t off = xs[e] - bbase;
-                    if (SWAR) red_add_sh_nc(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << ((off & 3u) * 8u));
-                    else ov[e] = atom_add_sh_nc(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << ((off & 3u) * 8u));
+                    ov[e] = atom_add_sh_nc(ok ? sm_cw + (off & ~3u) : sm_dummy, inc[e] << ((off & 3u) * 8u));
                 }
-                if (SWAR) {
-                } else if (CF_LAG) {
+                if (CF_LAG) {
                     cross(pov, pxs, pinc);
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
@@ -1185,6 +1195,7 @@ __global__ void __launch_bounds__(CF_WARPS * 32, 32 / CF_WARPS) k_count_frag(con
                     }
                 } else {
                     cross(ov, xs, inc);
+                }
                 }
             }
             if (CF_LAG && !SWAR) cross(pov, pxs, pinc);
